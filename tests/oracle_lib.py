@@ -1,0 +1,223 @@
+"""ctypes binding of the CPU oracle (oracle/_build/liborc.so).
+
+TEST INFRASTRUCTURE ONLY: the oracle is the checker for parity tests and the
+CPU baseline; the product (paper_2303_06762_b200) never imports this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE_DIR = os.path.join(ROOT, "oracle")
+LIB_PATH = os.path.join(ORACLE_DIR, "_build", "liborc.so")
+
+# enums shared with oracle/orc_capi.cpp
+BC_NONE, BC_LID_TOP, BC_LID_ALL, BC_INLET, BC_LID_UNIT, BC_CONST, BC_ZERO = range(7)
+LOAD_NONE, LOAD_ARRAY, LOAD_SMOOTH_UZAWA, LOAD_SIN_ADV, LOAD_EQUIV, LOAD_ASSEMBLY = range(6)
+WIND_NONE, WIND_ROT, WIND_CURL = range(3)
+CYCLE_V, CYCLE_W, CYCLE_VARV = range(3)
+SM_MULT, SM_ADD = range(2)
+
+
+class Problem(C.Structure):
+    _fields_ = [
+        ("mesh_kind", C.c_int), ("base_n", C.c_int), ("levels", C.c_int), ("k", C.c_int),
+        ("nu", C.c_double), ("beta", C.c_double), ("mass_coef", C.c_double), ("inv_eps", C.c_double),
+        ("bc_kind", C.c_int), ("load_kind", C.c_int), ("load", C.POINTER(C.c_double)),
+        ("wind_kind", C.c_int), ("cycle", C.c_int), ("smoother", C.c_int), ("smooth_steps", C.c_int),
+        ("jacobi_damping", C.c_double),
+    ]
+
+
+class Stats(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("not_applicable", C.c_int),
+                ("residual", C.c_double)]
+
+
+_lib = None
+
+
+def build():
+    subprocess.run(["make", "-s", "-C", ORACLE_DIR], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            build()
+        L = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        dp = C.POINTER(C.c_double)
+        lp = C.POINTER(C.c_longlong)
+        L.orc_mg_create.restype = P
+        L.orc_mg_create.argtypes = [C.POINTER(Problem)]
+        L.orc_last_error.restype = C.c_char_p
+        for name in ["orc_mg_n", "orc_mg_n_full", "orc_mg_nnz", "orc_mg_rows", "orc_mg_P_nnz", "orc_mg_patches"]:
+            getattr(L, name).restype = C.c_longlong
+        L.orc_mg_setup_seconds.restype = C.c_double
+        L.orc_mg_time_apply.restype = C.c_double
+        L.orc_check_picard_newton.restype = C.c_double
+        L.orc_check_upwind_lifting.restype = C.c_double
+        L.orc_seeded_load.argtypes = [C.c_int, C.c_uint, C.c_double, C.c_double, dp]
+        L.orc_mg_krylov.argtypes = [P, C.c_int, dp, dp, C.c_double, C.c_double, C.c_int, C.POINTER(Stats)]
+        L.orc_mg_uzawa.argtypes = [P, C.c_int, C.c_double, C.c_double, C.c_int, dp, dp,
+                                   C.POINTER(C.c_int), dp, C.POINTER(C.c_int), dp]
+        L.orc_mg_smooth.argtypes = [P, C.c_int, C.c_int, dp, dp, C.c_int, C.c_double]
+        L.orc_check_cr_equivalence.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                               C.c_double, C.c_int, dp]
+        for name in ["orc_mg_destroy", "orc_mg_n", "orc_mg_n_full", "orc_mg_num_levels", "orc_mg_ne",
+                     "orc_mg_setup_seconds"]:
+            getattr(L, name).argtypes = [P]
+        L.orc_mg_time_apply.argtypes = [P, C.c_int]
+        _lib = L
+    return _lib
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _lp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_longlong))
+
+
+def random_vec(n, seed):
+    """std::mt19937 + uniform(-1,1), the reference tests' random_vec."""
+    out = np.empty(int(n))
+    lib().orc_random_vec(C.c_longlong(int(n)), C.c_uint(seed), _dp(out))
+    return out
+
+
+def seeded_load(n, seed, lo=-1.0, hi=1.0):
+    out = np.empty(4 * n * n)
+    lib().orc_seeded_load(n, seed, lo, hi, _dp(out))
+    return out
+
+
+class OracleMG:
+    """Oracle MGPreconditioner + solvers for one problem (reference inc/multigrid.hpp)."""
+
+    def __init__(self, *, mesh_kind=0, base_n=2, levels=2, k=0, nu=1.0, beta=0.0, mass_coef=0.0,
+                 inv_eps=1e6, bc=BC_NONE, load_kind=LOAD_NONE, load=None, wind=WIND_NONE,
+                 cycle=CYCLE_W, smoother=SM_MULT, smooth_steps=1, jacobi_damping=1.0 / 3.0):
+        L = lib()
+        self._load = None if load is None else np.ascontiguousarray(load, dtype=np.float64)
+        p = Problem(mesh_kind, base_n, levels, k, nu, beta, mass_coef, inv_eps, bc, load_kind,
+                    _dp(self._load) if self._load is not None else None, wind, cycle, smoother,
+                    smooth_steps, jacobi_damping)
+        self.h = L.orc_mg_create(C.byref(p))
+        if not self.h:
+            raise RuntimeError(L.orc_last_error().decode())
+        self.n = L.orc_mg_n(self.h)
+        self.n_full = L.orc_mg_n_full(self.h)
+        self.ne = L.orc_mg_ne(self.h)
+        self.k = k
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().orc_mg_destroy(self.h)
+            self.h = None
+
+    @property
+    def setup_seconds(self):
+        return lib().orc_mg_setup_seconds(self.h)
+
+    def csr(self, level=-1):
+        import scipy.sparse as sp
+        L = lib()
+        rows = L.orc_mg_rows(self.h, level)
+        nnz = L.orc_mg_nnz(self.h, level)
+        ptr = np.empty(rows + 1, np.int64)
+        idx = np.empty(nnz, np.int64)
+        val = np.empty(nnz)
+        L.orc_mg_csr(self.h, level, _lp(ptr), _lp(idx), _dp(val))
+        return sp.csr_matrix((val, idx, ptr), shape=(rows, rows))
+
+    def prolongation(self, level):
+        import scipy.sparse as sp
+        L = lib()
+        rows = L.orc_mg_rows(self.h, level)
+        cols = L.orc_mg_rows(self.h, level - 1)
+        nnz = L.orc_mg_P_nnz(self.h, level)
+        ptr = np.empty(rows + 1, np.int64)
+        idx = np.empty(nnz, np.int64)
+        val = np.empty(nnz)
+        L.orc_mg_P_csr(self.h, level, _lp(ptr), _lp(idx), _dp(val))
+        return sp.csr_matrix((val, idx, ptr), shape=(rows, cols))
+
+    def rhs(self):
+        out = np.empty(self.n)
+        lib().orc_mg_rhs(self.h, _dp(out))
+        return out
+
+    def free_to_full(self):
+        out = np.empty(self.n, np.int64)
+        lib().orc_mg_free_to_full(self.h, _lp(out))
+        return out
+
+    def g_full(self):
+        out = np.empty(self.n_full)
+        lib().orc_mg_g_full(self.h, _dp(out))
+        return out
+
+    def apply(self, b):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.empty(self.n)
+        lib().orc_mg_apply(self.h, _dp(b), _dp(x))
+        return x
+
+    def spmv(self, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty(self.n)
+        lib().orc_mg_spmv(self.h, _dp(x), _dp(y))
+        return y
+
+    def smooth(self, level, which, x, b, sweeps=1, damping=1.0 / 3.0):
+        x = np.array(x, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        lib().orc_mg_smooth(self.h, level, which, _dp(x), _dp(b), sweeps, damping)
+        return x
+
+    def patches(self, level=-1):
+        L = lib()
+        n = L.orc_mg_num_patches(self.h, level)
+        tot = L.orc_mg_patches(self.h, level, None, None)
+        offs = np.empty(n + 1, np.int64)
+        dofs = np.empty(tot, np.int64)
+        L.orc_mg_patches(self.h, level, _lp(offs), _lp(dofs))
+        return [dofs[offs[j]:offs[j + 1]] for j in range(n)]
+
+    def krylov(self, b, x0=None, method=0, rel_tol=1e-8, abs_tol=1e-10, max_it=500):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.zeros(self.n) if x0 is None else np.array(x0, dtype=np.float64)
+        st = Stats()
+        lib().orc_mg_krylov(self.h, method, _dp(b), _dp(x), rel_tol, abs_tol, max_it, C.byref(st))
+        return x, dict(iterations=st.iterations, converged=bool(st.converged),
+                       not_applicable=bool(st.not_applicable), residual=st.residual)
+
+    def uzawa(self, outer=2, rel_tol=1e-8, abs_tol=1e-10, max_it=500):
+        vel = np.empty(self.n_full)
+        p = np.empty(self.ne)
+        inner = (C.c_int * outer)()
+        hist = np.zeros(outer)
+        flags = (C.c_int * 2)()
+        secs = np.zeros(1)
+        done = lib().orc_mg_uzawa(self.h, outer, rel_tol, abs_tol, max_it, _dp(vel), _dp(p), inner,
+                                  _dp(hist), flags, _dp(secs))
+        return dict(velocity=vel, pressure=p, inner_iterations=list(inner)[:done],
+                    divergence_history=list(hist[:done]), converged=bool(flags[0]),
+                    not_applicable=bool(flags[1]), seconds=float(secs[0]))
+
+    def time_apply(self, reps):
+        return lib().orc_mg_time_apply(self.h, reps)
+
+
+def check(name, *args, n_out):
+    out = np.zeros(n_out)
+    getattr(lib(), name)(*args, _dp(out))
+    return out
