@@ -1,0 +1,185 @@
+/* hpmg C ABI: B200-native hp-multigrid preconditioned Krylov solve for the
+ * statically condensed H(div)-HDG Stokes/Oseen operator.
+ *
+ * Drop-in boundary for the reference (hdivmg) operator API. Each entry point
+ * names the reference interface it replaces (paths relative to
+ * /root/reference/proj/include/hdivmg):
+ *
+ *   hpmg_create / hpmg_destroy  <- MGPreconditioner::MGPreconditioner(hier, k, bc,
+ *                                  fine_opt, inv_eps, mg)          multigrid.hpp:45-114
+ *   hpmg_apply                  <- MGPreconditioner::apply / as_operator
+ *                                                                  multigrid.hpp:117-131
+ *   hpmg_spmv                   <- the LinearOperator [&B](v){ return B.matrix()*v; }
+ *                                                                  uzawa.hpp:42, krylov.hpp:10
+ *   hpmg_matrix_csr, hpmg_rhs,  <- matrix(), rhs(), constraints(), symmetric(), penalty()
+ *   hpmg_free_to_full, ...                                          multigrid.hpp:133-146
+ *   hpmg_pcg / hpmg_gmres       <- pcg(A, M, b, x, opt) / gmres(...)  krylov.hpp:30-144
+ *   hpmg_uzawa                  <- uzawa_solve(B, opt)             uzawa.hpp:51-91
+ *   hpmg_recover                <- recover_locals(mesh, V, opt, u) assembly.hpp:513-549
+ *   hpmg_smooth                 <- PatchSmoother::forward/backward/jacobi
+ *                                                                  smoother.hpp:53-80
+ *
+ * Conventions (identical to the reference):
+ *  - Vectors crossing the boundary are in the reference FREE order
+ *    (Constraints::free_to_full, fespace.hpp:508-513): all free normal-flux
+ *    coefficients (facet-major, mode-minor) then all free tangential ones.
+ *    Internally the device uses a facet-major block layout; the permutation
+ *    is applied inside the call.
+ *  - Pointers are host memory unless HPMG_DEVICE_PTRS is passed in `flags`,
+ *    in which case they are device pointers (still reference order).
+ *  - Errors: setup errors return a nonzero status and hpmg_last_error()
+ *    describes them (the C++ adapter rethrows them as the reference's
+ *    exception types); solver breakdown / indefiniteness is reported in-band
+ *    (hpmg_solve_stats.not_applicable), never as an error.
+ *  - One context is bound to one CUDA stream and is not thread-safe.
+ *  - No CPU fallback: without a usable CUDA device every call fails with
+ *    HPMG_ERR_CUDA.
+ */
+#ifndef HPMG_CAPI_H
+#define HPMG_CAPI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hpmg_ctx hpmg_ctx;
+
+enum { HPMG_OK = 0, HPMG_ERR_ARG = 1, HPMG_ERR_CUDA = 2, HPMG_ERR_SETUP = 3, HPMG_ERR_LOGIC = 4 };
+enum { HPMG_CYCLE_V = 0, HPMG_CYCLE_W = 1, HPMG_CYCLE_VARIABLE_V = 2 };        /* CycleKind */
+enum { HPMG_SMOOTH_MULTIPLICATIVE = 0, HPMG_SMOOTH_ADDITIVE = 1 };            /* SmootherKind */
+enum { HPMG_TAG_INTERIOR = 0, HPMG_TAG_DIRICHLET = 1, HPMG_TAG_OUTFLOW = 2 };  /* bc:: tags */
+enum { HPMG_DEVICE_PTRS = 1 };
+
+/* Point callback: out[0..1] = field(x, y) (VelocityBC::g, AssemblyOptions::load). */
+typedef void (*hpmg_field_fn)(double x, double y, double* out, void* user);
+
+/* Base mesh of the hierarchy (the reference Mesh before MeshHierarchy::build).
+ * Elements are counter-clockwise vertex triples; facets are discovered from
+ * them exactly as Mesh::finalize does; boundary facets default to Dirichlet
+ * and `tag_overrides` (a, b, tag) triples retag facets (e.g. outflow). */
+typedef struct {
+  int n_vertices;
+  const double* xy;        /* 2 * n_vertices */
+  int n_elements;
+  const int* elements;     /* 3 * n_elements */
+  int n_tag_overrides;
+  const int* tag_overrides; /* 3 * n_tag_overrides */
+  int levels;              /* MeshHierarchy::build(base, levels) */
+} hpmg_mesh_desc;
+
+/* AssemblyOptions + inv_eps + MGOptions (assembly.hpp:69-77, multigrid.hpp:24-34). */
+typedef struct {
+  int k;                   /* order 0..3 */
+  double nu, beta, mass_coef, inv_eps;
+  int cycle, smoother, smooth_steps;
+  double jacobi_damping;
+} hpmg_options;
+
+/* Problem data: boundary values, load and (Oseen) advection state. */
+typedef struct {
+  hpmg_field_fn bc;           /* NULL: homogeneous Dirichlet data */
+  void* bc_user;
+  hpmg_field_fn load;         /* point load, evaluated on the host at the quadrature points */
+  void* load_user;
+  const double* load_per_element; /* alternative: constant force per finest element (2*ne) */
+  const double* wind_compound;    /* advection HDGVelocity on the finest mesh at order k: */
+  const double* wind_interior;    /*   compound (n_full) and interior (ne*k(k+1)); NULL = Stokes */
+  int newton;
+  const double* structured_load;  /* alternative: seeded structured force (hpmg_seeded_load layout) */
+  int structured_n;               /*   on an n x n unit-square grid, mapped onto the finest elements */
+} hpmg_problem;
+
+typedef struct {
+  double rel_tol, abs_tol;    /* KrylovOptions (krylov.hpp:12-16): 1e-8, 1e-10 */
+  int max_iterations;         /* 500 */
+  int restart;                /* GMRes only: 0 = reference semantics (no cap); m = GMRes(m) */
+} hpmg_krylov_opts;
+
+typedef struct {
+  int iterations, converged, not_applicable;
+  double residual;
+} hpmg_solve_stats;
+
+typedef struct {
+  int outer_iterations;       /* UzawaOptions (uzawa.hpp:9-21): 2 */
+  hpmg_krylov_opts krylov;
+} hpmg_uzawa_opts;
+
+typedef struct {
+  int n_outer;
+  int inner_iterations[64];
+  double divergence_history[64];
+  int converged, not_applicable;
+  double final_divergence;
+  double seconds;             /* device time of the whole outer loop */
+} hpmg_uzawa_report;
+
+/* ---- lifecycle ---- */
+int hpmg_create(hpmg_ctx** out, const hpmg_mesh_desc* mesh, const hpmg_options* opt, const hpmg_problem* prob);
+void hpmg_destroy(hpmg_ctx* ctx);
+const char* hpmg_last_error(void);
+const char* hpmg_ctx_error(const hpmg_ctx* ctx);
+
+/* ---- sizes and host mirrors ---- */
+int64_t hpmg_n(const hpmg_ctx* ctx);            /* free DOFs of the finest system */
+int64_t hpmg_n_full(const hpmg_ctx* ctx);       /* compound DOFs */
+int hpmg_ne(const hpmg_ctx* ctx);               /* finest elements */
+int hpmg_num_levels(const hpmg_ctx* ctx);
+int64_t hpmg_level_n(const hpmg_ctx* ctx, int level); /* free DOFs of level l (-1: finest system) */
+int hpmg_symmetric(const hpmg_ctx* ctx);
+double hpmg_penalty(const hpmg_ctx* ctx);
+int hpmg_free_to_full(const hpmg_ctx* ctx, int64_t* out);
+int hpmg_g_full(const hpmg_ctx* ctx, double* out);
+int hpmg_rhs(hpmg_ctx* ctx, double* out, int flags);
+/* CSR of the finest operator (level -1) or of lowest-order level l, reference
+ * order: call with NULL arrays to get nnz through *nnz. */
+int hpmg_matrix_csr(hpmg_ctx* ctx, int level, int64_t* nnz, int64_t* ptr, int64_t* idx, double* val);
+
+/* ---- operators ---- */
+int hpmg_spmv(hpmg_ctx* ctx, const double* x, double* y, int flags);
+int hpmg_apply(hpmg_ctx* ctx, const double* r, double* z, int flags);
+/* which: 0 forward, 1 backward, 2 additive (jacobi) on level l (-1 = order-k head) */
+int hpmg_smooth(hpmg_ctx* ctx, int level, int which, double* x, const double* b, int sweeps, int flags);
+
+/* ---- solvers ---- */
+int hpmg_pcg(hpmg_ctx* ctx, const double* b, double* x, const hpmg_krylov_opts* o, hpmg_solve_stats* st, int flags);
+int hpmg_gmres(hpmg_ctx* ctx, const double* b, double* x, const hpmg_krylov_opts* o, hpmg_solve_stats* st, int flags);
+/* velocity: full compound (n_full), pressure: element means (ne); host pointers */
+int hpmg_uzawa(hpmg_ctx* ctx, const hpmg_uzawa_opts* o, double* velocity, double* pressure, hpmg_uzawa_report* rep);
+/* recover_locals on the finest system: interior (ne*k(k+1)), p_ortho (ne*(ns-1)),
+ * grad (ne*4*ns, element-major); interior coefficients refer to this library's
+ * interior RT basis (same span as the reference's). */
+int hpmg_recover(hpmg_ctx* ctx, const double* velocity_full, double* interior, double* p_ortho, double* grad);
+
+/* ---- measurement hooks (bench.py) ---- */
+void* hpmg_stream(hpmg_ctx* ctx);               /* cudaStream_t the context launches on */
+/* Algorithmic bytes of one apply() / one spmv() in the reference storage
+ * accounting; `parts` (optional, 8 doubles) splits the
+ * V-cycle: head sweeps, head residual, level sweeps, level residuals, transfers, coarse. */
+double hpmg_vcycle_bytes(const hpmg_ctx* ctx, double* parts);
+double hpmg_spmv_bytes(const hpmg_ctx* ctx);
+/* Device-resident timing of `reps` applies (graph-launched) on device buffers
+ * already in the internal layout; returns ms per apply. phase_ms (optional,
+ * 8 doubles) receives per-phase averages from an event-instrumented pass. */
+double hpmg_time_apply(hpmg_ctx* ctx, int reps, double* phase_ms);
+int hpmg_kernel_launches_per_apply(const hpmg_ctx* ctx);
+double hpmg_setup_seconds(const hpmg_ctx* ctx, double* parts);
+
+/* Seeded per-triangle force of the BASELINE configs: std::mt19937(seed) and
+ * uniform_real_distribution(lo, hi) drawn in structured (j, i, lower/upper,
+ * (fx, fy)) order for an n x n unit-square mesh; map_structured_load turns it
+ * into per-element values for the finest mesh of a hierarchy. */
+void hpmg_seeded_load(int n, unsigned seed, double lo, double hi, double* out);
+int hpmg_structured_to_elements(const hpmg_ctx* ctx, int n, const double* structured, double* per_element);
+
+/* Base meshes of the reference (mesh.hpp:220-279): fills a descriptor whose
+ * arrays stay valid until the next call from the same thread. */
+int hpmg_unit_square_mesh(int n, int levels, hpmg_mesh_desc* out);
+int hpmg_step_mesh(int n, int levels, hpmg_mesh_desc* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

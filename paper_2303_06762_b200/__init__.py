@@ -1,0 +1,365 @@
+"""hpmg: B200-native hp-multigrid preconditioned Krylov solver (Python mirror).
+
+Mirrors the reference hdivmg operator interface (proj/include/hdivmg):
+``MGPreconditioner`` (multigrid.hpp:43-146), ``pcg`` / ``gmres`` (krylov.hpp:30-144)
+and ``uzawa_solve`` (uzawa.hpp:51-91), on top of the C ABI in
+include/hpmg/capi.h implemented by the in-tree ``lib/libhpmg.so`` (CUDA,
+sm_100a). There is no CPU fallback: loading fails loudly without the library,
+and every call fails without a CUDA device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libhpmg.so")
+
+CYCLE_V, CYCLE_W, CYCLE_VARIABLE_V = 0, 1, 2
+SMOOTH_MULTIPLICATIVE, SMOOTH_ADDITIVE = 0, 1
+DEVICE_PTRS = 1
+
+FIELD_FN = C.CFUNCTYPE(None, C.c_double, C.c_double, C.POINTER(C.c_double), C.c_void_p)
+
+
+class _Mesh(C.Structure):
+    _fields_ = [("n_vertices", C.c_int), ("xy", C.POINTER(C.c_double)), ("n_elements", C.c_int),
+                ("elements", C.POINTER(C.c_int)), ("n_tag_overrides", C.c_int),
+                ("tag_overrides", C.POINTER(C.c_int)), ("levels", C.c_int)]
+
+
+class _Options(C.Structure):
+    _fields_ = [("k", C.c_int), ("nu", C.c_double), ("beta", C.c_double), ("mass_coef", C.c_double),
+                ("inv_eps", C.c_double), ("cycle", C.c_int), ("smoother", C.c_int), ("smooth_steps", C.c_int),
+                ("jacobi_damping", C.c_double)]
+
+
+class _Problem(C.Structure):
+    _fields_ = [("bc", FIELD_FN), ("bc_user", C.c_void_p), ("load", FIELD_FN), ("load_user", C.c_void_p),
+                ("load_per_element", C.POINTER(C.c_double)), ("wind_compound", C.POINTER(C.c_double)),
+                ("wind_interior", C.POINTER(C.c_double)), ("newton", C.c_int),
+                ("structured_load", C.POINTER(C.c_double)), ("structured_n", C.c_int)]
+
+
+class _KOpts(C.Structure):
+    _fields_ = [("rel_tol", C.c_double), ("abs_tol", C.c_double), ("max_iterations", C.c_int), ("restart", C.c_int)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("not_applicable", C.c_int),
+                ("residual", C.c_double)]
+
+
+class _UOpts(C.Structure):
+    _fields_ = [("outer_iterations", C.c_int), ("krylov", _KOpts)]
+
+
+class _UReport(C.Structure):
+    _fields_ = [("n_outer", C.c_int), ("inner_iterations", C.c_int * 64), ("divergence_history", C.c_double * 64),
+                ("converged", C.c_int), ("not_applicable", C.c_int), ("final_divergence", C.c_double),
+                ("seconds", C.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    """Loads lib/libhpmg.so (builds it with nvcc first if it is missing)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        from . import build as _build
+        _build.build()
+    L = C.CDLL(LIB_PATH)
+    vp, dp, lp = C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)
+    L.hpmg_create.argtypes = [C.POINTER(vp), C.POINTER(_Mesh), C.POINTER(_Options), C.POINTER(_Problem)]
+    L.hpmg_destroy.argtypes = [vp]
+    L.hpmg_last_error.restype = C.c_char_p
+    L.hpmg_ctx_error.restype = C.c_char_p
+    L.hpmg_ctx_error.argtypes = [vp]
+    for name in ("hpmg_n", "hpmg_n_full"):
+        getattr(L, name).restype = C.c_int64
+        getattr(L, name).argtypes = [vp]
+    for name in ("hpmg_ne", "hpmg_num_levels", "hpmg_symmetric", "hpmg_kernel_launches_per_apply"):
+        getattr(L, name).argtypes = [vp]
+    L.hpmg_level_n.restype = C.c_int64
+    L.hpmg_level_n.argtypes = [vp, C.c_int]
+    L.hpmg_penalty.restype = C.c_double
+    L.hpmg_penalty.argtypes = [vp]
+    L.hpmg_free_to_full.argtypes = [vp, lp]
+    L.hpmg_g_full.argtypes = [vp, dp]
+    L.hpmg_rhs.argtypes = [vp, vp, C.c_int]
+    L.hpmg_matrix_csr.argtypes = [vp, C.c_int, lp, lp, lp, dp]
+    L.hpmg_spmv.argtypes = [vp, vp, vp, C.c_int]
+    L.hpmg_apply.argtypes = [vp, vp, vp, C.c_int]
+    L.hpmg_smooth.argtypes = [vp, C.c_int, C.c_int, vp, vp, C.c_int, C.c_int]
+    L.hpmg_pcg.argtypes = [vp, vp, vp, C.POINTER(_KOpts), C.POINTER(_Stats), C.c_int]
+    L.hpmg_gmres.argtypes = [vp, vp, vp, C.POINTER(_KOpts), C.POINTER(_Stats), C.c_int]
+    L.hpmg_uzawa.argtypes = [vp, C.POINTER(_UOpts), dp, dp, C.POINTER(_UReport)]
+    L.hpmg_stream.restype = vp
+    L.hpmg_stream.argtypes = [vp]
+    L.hpmg_vcycle_bytes.restype = C.c_double
+    L.hpmg_vcycle_bytes.argtypes = [vp, dp]
+    L.hpmg_spmv_bytes.restype = C.c_double
+    L.hpmg_spmv_bytes.argtypes = [vp]
+    L.hpmg_time_apply.restype = C.c_double
+    L.hpmg_time_apply.argtypes = [vp, C.c_int, dp]
+    L.hpmg_setup_seconds.restype = C.c_double
+    L.hpmg_setup_seconds.argtypes = [vp, dp]
+    L.hpmg_seeded_load.argtypes = [C.c_int, C.c_uint, C.c_double, C.c_double, dp]
+    L.hpmg_structured_to_elements.argtypes = [vp, C.c_int, dp, dp]
+    L.hpmg_unit_square_mesh.argtypes = [C.c_int, C.c_int, C.POINTER(_Mesh)]
+    L.hpmg_step_mesh.argtypes = [C.c_int, C.c_int, C.POINTER(_Mesh)]
+    _lib = L
+    return L
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _field(fn):
+    """Wraps a python callable (x, y) -> (fx, fy) as a C point callback."""
+    if fn is None:
+        return FIELD_FN()
+
+    def cb(x, y, out, _user):
+        v = fn(x, y)
+        out[0] = float(v[0])
+        out[1] = float(v[1])
+
+    return FIELD_FN(cb)
+
+
+def seeded_load(n, seed, lo=-1.0, hi=1.0):
+    """BASELINE per-triangle force: mt19937(seed), uniform(lo, hi), structured order."""
+    out = np.empty(4 * n * n)
+    lib().hpmg_seeded_load(n, seed, lo, hi, _dp(out))
+    return out
+
+
+@dataclass
+class KrylovOptions:
+    """reference krylov.hpp:12-16"""
+    rel_tol: float = 1e-8
+    abs_tol: float = 1e-10
+    max_iterations: int = 500
+    restart: int = 0
+
+    def c(self):
+        return _KOpts(self.rel_tol, self.abs_tol, self.max_iterations, self.restart)
+
+
+@dataclass
+class SolveStats:
+    """reference krylov.hpp:18-26"""
+    iterations: int = 0
+    converged: bool = False
+    not_applicable: bool = False
+    residual: float = 0.0
+
+
+@dataclass
+class UzawaReport:
+    """reference uzawa.hpp:23-33"""
+    inner_iterations: list = field(default_factory=list)
+    divergence_history: list = field(default_factory=list)
+    converged: bool = False
+    not_applicable: bool = False
+    final_divergence: float = 0.0
+    seconds: float = 0.0
+
+
+@dataclass
+class StokesSolution:
+    velocity: np.ndarray
+    pressure: np.ndarray
+    report: UzawaReport
+
+
+class HpmgError(RuntimeError):
+    pass
+
+
+class MGPreconditioner:
+    """hp-multigrid preconditioner on the device (reference multigrid.hpp:43-146).
+
+    mesh: "unit_square" or "step" with base size ``base_n`` refined to ``levels``
+    mesh levels (MeshHierarchy::build). ``load`` is a point callback, or
+    ``load_per_element`` a per-finest-element constant force, or
+    ``structured_load=(n, array)`` the seeded BASELINE force on an n x n grid.
+    """
+
+    def __init__(self, *, mesh="unit_square", base_n=2, levels=2, k=0, nu=1.0, beta=0.0, mass_coef=0.0,
+                 inv_eps=1e6, cycle=CYCLE_W, smoother=SMOOTH_MULTIPLICATIVE, smooth_steps=1,
+                 jacobi_damping=1.0 / 3.0, bc=None, load=None, load_per_element=None, structured_load=None):
+        L = lib()
+        md = _Mesh()
+        rc = (L.hpmg_unit_square_mesh if mesh == "unit_square" else L.hpmg_step_mesh)(base_n, levels, C.byref(md))
+        if rc:
+            raise HpmgError(L.hpmg_last_error().decode())
+        opt = _Options(k, nu, beta, mass_coef, inv_eps, cycle, smoother, smooth_steps, jacobi_damping)
+        self._bc = _field(bc)
+        self._load = _field(load)
+        self._keep = []
+        prob = _Problem(self._bc, None, self._load, None, None, None, None, 0, None, 0)
+        if load_per_element is not None:
+            a = np.ascontiguousarray(load_per_element, dtype=np.float64)
+            self._keep.append(a)
+            prob.load_per_element = _dp(a)
+        if structured_load is not None:
+            n, arr = structured_load
+            a = np.ascontiguousarray(arr, dtype=np.float64)
+            self._keep.append(a)
+            prob.structured_load = _dp(a)
+            prob.structured_n = int(n)
+        h = C.c_void_p()
+        rc = L.hpmg_create(C.byref(h), C.byref(md), C.byref(opt), C.byref(prob))
+        if rc:
+            raise HpmgError(L.hpmg_last_error().decode())
+        self.h = h
+        self.k = k
+        self.n = L.hpmg_n(h)
+        self.n_full = L.hpmg_n_full(h)
+        self.ne = L.hpmg_ne(h)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().hpmg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc:
+            raise HpmgError(lib().hpmg_ctx_error(self.h).decode())
+
+    # -- reference accessors
+    def symmetric(self):
+        return bool(lib().hpmg_symmetric(self.h))
+
+    def penalty(self):
+        return lib().hpmg_penalty(self.h)
+
+    def num_levels(self):
+        return lib().hpmg_num_levels(self.h)
+
+    def free_to_full(self):
+        out = np.empty(self.n, np.int64)
+        lib().hpmg_free_to_full(self.h, out.ctypes.data_as(C.POINTER(C.c_int64)))
+        return out
+
+    def g_full(self):
+        out = np.empty(self.n_full)
+        lib().hpmg_g_full(self.h, _dp(out))
+        return out
+
+    def rhs(self):
+        out = np.empty(self.n)
+        self._check(lib().hpmg_rhs(self.h, out.ctypes.data, 0))
+        return out
+
+    def level_n(self, level=-1):
+        return int(lib().hpmg_level_n(self.h, level))
+
+    def matrix(self, level=-1):
+        """Host CSR mirror in the reference free order (multigrid.hpp:133)."""
+        import scipy.sparse as sp
+        L = lib()
+        nnz = C.c_int64()
+        self._check(L.hpmg_matrix_csr(self.h, level, C.byref(nnz), None, None, None))
+        rows = self.level_n(level)
+        ptr = np.empty(rows + 1, np.int64)
+        idx = np.empty(nnz.value, np.int64)
+        val = np.empty(nnz.value)
+        self._check(L.hpmg_matrix_csr(self.h, level, C.byref(nnz), ptr.ctypes.data_as(C.POINTER(C.c_int64)),
+                                      idx.ctypes.data_as(C.POINTER(C.c_int64)), _dp(val)))
+        return sp.csr_matrix((val, idx, ptr), shape=(rows, rows))
+
+    # -- operators (host numpy in, host numpy out)
+    def apply(self, b):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        z = np.empty(self.n)
+        self._check(lib().hpmg_apply(self.h, b.ctypes.data, z.ctypes.data, 0))
+        return z
+
+    def spmv(self, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty(self.n)
+        self._check(lib().hpmg_spmv(self.h, x.ctypes.data, y.ctypes.data, 0))
+        return y
+
+    def smooth(self, level, which, x, b, sweeps=1):
+        x = np.array(x, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        self._check(lib().hpmg_smooth(self.h, level, which, x.ctypes.data, b.ctypes.data, sweeps, 0))
+        return x
+
+    def as_operator(self):
+        return self.apply
+
+    # -- measurement hooks
+    def stream(self):
+        return lib().hpmg_stream(self.h)
+
+    def vcycle_bytes(self):
+        parts = np.zeros(8)
+        tot = lib().hpmg_vcycle_bytes(self.h, _dp(parts))
+        return tot, parts
+
+    def spmv_bytes(self):
+        return lib().hpmg_spmv_bytes(self.h)
+
+    def time_apply(self, reps, phases=False):
+        ph = np.zeros(8)
+        ms = lib().hpmg_time_apply(self.h, reps, _dp(ph) if phases else None)
+        return ms, ph
+
+    def launches_per_apply(self):
+        return lib().hpmg_kernel_launches_per_apply(self.h)
+
+    def setup_seconds(self):
+        parts = np.zeros(8)
+        tot = lib().hpmg_setup_seconds(self.h, _dp(parts))
+        return tot, parts
+
+
+def pcg(B: MGPreconditioner, b, x=None, opt: KrylovOptions | None = None):
+    """Device PCG with B.matrix() and B.apply (reference krylov.hpp:30-73)."""
+    opt = opt or KrylovOptions()
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.zeros(B.n) if x is None else np.array(x, dtype=np.float64)
+    st = _Stats()
+    B._check(lib().hpmg_pcg(B.h, b.ctypes.data, x.ctypes.data, C.byref(opt.c()), C.byref(st), 0))
+    return x, SolveStats(st.iterations, bool(st.converged), bool(st.not_applicable), st.residual)
+
+
+def gmres(B: MGPreconditioner, b, x=None, opt: KrylovOptions | None = None):
+    """Device right-preconditioned MGS GMRES (reference krylov.hpp:79-144)."""
+    opt = opt or KrylovOptions()
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.zeros(B.n) if x is None else np.array(x, dtype=np.float64)
+    st = _Stats()
+    B._check(lib().hpmg_gmres(B.h, b.ctypes.data, x.ctypes.data, C.byref(opt.c()), C.byref(st), 0))
+    return x, SolveStats(st.iterations, bool(st.converged), bool(st.not_applicable), st.residual)
+
+
+def uzawa_solve(B: MGPreconditioner, outer_iterations=2, krylov: KrylovOptions | None = None):
+    """Augmented-Lagrangian Uzawa loop on the device (reference uzawa.hpp:51-91)."""
+    krylov = krylov or KrylovOptions()
+    vel = np.empty(B.n_full)
+    p = np.empty(B.ne)
+    rep = _UReport()
+    o = _UOpts(outer_iterations, krylov.c())
+    B._check(lib().hpmg_uzawa(B.h, C.byref(o), _dp(vel), _dp(p), C.byref(rep)))
+    r = UzawaReport(list(rep.inner_iterations[: rep.n_outer]), list(rep.divergence_history[: rep.n_outer]),
+                    bool(rep.converged), bool(rep.not_applicable), rep.final_divergence, rep.seconds)
+    return StokesSolution(vel, p, r)

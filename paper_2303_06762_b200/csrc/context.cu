@@ -1,0 +1,1224 @@
+// hpmg context: owns every device structure of one hp-MG preconditioner and
+// implements the C ABI of include/hpmg/capi.h. Setup builds the mesh
+// hierarchy and bookkeeping on the host, condenses every level on the GPU,
+// inverts the patch blocks on the GPU, builds the CR-GMG transfers on the host
+// and uploads them; apply/spmv/pcg/gmres/uzawa run entirely on the device
+// (host syncs only to read convergence scalars).
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/hpmg/capi.h"
+#include "host/basis.hpp"
+#include "host/plan.hpp"
+#include "host/transfer.hpp"
+#include "kernels/kernels.hpp"
+
+using namespace hpmg;
+
+#define CK(x)                                                                                              \
+  do {                                                                                                     \
+    cudaError_t e__ = (x);                                                                                 \
+    if (e__ != cudaSuccess) throw std::runtime_error(std::string(#x) + ": " + cudaGetErrorString(e__)); \
+  } while (0)
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename T>
+T* dalloc(size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  CK(cudaMalloc(&p, n * sizeof(T)));
+  return static_cast<T*>(p);
+}
+template <typename T>
+T* dupload(const std::vector<T>& v, cudaStream_t s) {
+  T* p = dalloc<T>(v.size());
+  if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  return p;
+}
+
+// device scalar slots
+enum { S_RZ0 = 0, S_RZ1, S_PAP, S_RR, S_BB, S_TMP, S_PS, S_PA, S_PMAX, S_H0 = 16, S_COUNT = 16 + 520 };
+
+struct DevRef {
+  RefT T{};
+  std::vector<void*> owned;
+};
+
+struct Level {
+  host::LevelPlan plan;
+  int k = 0, bs = 2, nb = 0;
+  int64_t n = 0;
+  dev::Bsr A, AT;
+  int* tslot = nullptr;
+  dev::Patches P;
+  int max_nf = 0;
+  std::vector<int> wave_ptr;
+  dev::BlockCsr Pm, PT;  // from level l-1 to l (lowest-order levels l >= 1)
+  double *x = nullptr, *b = nullptr, *r = nullptr, *y = nullptr, *bw = nullptr, *xw = nullptr, *dbuf = nullptr;
+  int steps = 1;
+  ElemGeo* geo = nullptr;
+  int ne = 0;
+  std::vector<double> Ahost;  // BSR values mirror (filled on demand)
+  // finest-system extras
+  int* row_elems = nullptr;
+  int* elem_facets = nullptr;
+  int* facet_block = nullptr;
+  double bytes_sweep = 0, bytes_spmv = 0;
+};
+
+}  // namespace
+
+struct hpmg_ctx {
+  cudaStream_t s = nullptr;
+  std::string err;
+  hpmg_options opt{};
+  bool advected = false;
+  int L = 0;  // finest lowest-order level index
+  std::vector<host::TriMesh> mesh;
+  std::vector<host::Refinement> ref;
+  std::vector<std::unique_ptr<Level>> lv;
+  std::unique_ptr<Level> head;  // order-k system (k >= 1)
+  DevRef ref0, refk;
+  double* coarse_inv = nullptr;
+  double* gemv_work = nullptr;
+  int n0 = 0;
+  dev::Reduce red;
+  double* sc = nullptr;
+  double* sc_host = nullptr;  // pinned mirror
+  double* rhs = nullptr;      // finest rhs, block layout
+  double* g_fac = nullptr;    // finest Dirichlet data per facet (bs each)
+  char* facet_dir = nullptr;
+  std::vector<double> g_full;  // reference compound order
+  std::vector<int64_t> free_to_full;
+  // krylov workspace (block layout, finest system)
+  double *kx = nullptr, *kb = nullptr, *kr = nullptr, *kz = nullptr, *kp = nullptr, *kAp = nullptr, *ktmp = nullptr;
+  double *io_a = nullptr, *io_b = nullptr;  // reference-order staging
+  std::vector<double*> gm_basis;
+  // uzawa
+  double *pres = nullptr, *div = nullptr, *urhs = nullptr;
+  bool enclosed = true;
+  int launches_per_apply = 0;
+  bool counting = false;
+  double setup_parts[8] = {0};
+  // CUDA graph of apply(kr -> kz)
+  cudaGraphExec_t apply_graph = nullptr;
+
+  Level& top() { return opt.k > 0 ? *head : *lv[L]; }
+  int64_t nfree() { return top().n; }
+};
+
+namespace {
+
+void upload_ref(DevRef& D, const host::RefTensors& T, cudaStream_t s) {
+  auto up = [&](const std::vector<double>& v) {
+    double* p = dupload(v, s);
+    D.owned.push_back(p);
+    return p;
+  };
+  D.T.k = T.k;
+  D.T.nfd = T.nfd;
+  D.T.nrt = T.nrt;
+  D.T.no = T.no;
+  D.T.ns = T.ns;
+  D.T.nc = T.nc;
+  D.T.nv = T.nv;
+  D.T.G = up(T.G);
+  D.T.Mm = up(T.Mm);
+  D.T.Dv = up(T.Dv);
+  D.T.Lv = up(T.Lv);
+  D.T.Ev = up(T.Ev);
+  D.T.Tv = up(T.Tv);
+  D.T.vval = up(T.vval);
+  D.T.qw = up(T.qw);
+  D.T.nq = T.nq;
+}
+
+/// Legendre moments of the boundary data on Dirichlet facets, block layout
+/// per facet (reference Constraints::build, inc/fespace.hpp:477-515).
+std::vector<double> dirichlet_data(const host::TriMesh& m, int k, hpmg_field_fn bc, void* user) {
+  const int bs = 2 * (k + 1);
+  std::vector<double> g(size_t(m.nf()) * bs, 0.0);
+  if (!bc) return g;
+  std::vector<double> gx, gw;
+  host::gauss(2 * k + 6, gx, gw);
+  double L[8], out[2];
+  for (int f = 0; f < m.nf(); ++f) {
+    if (m.ftag[f] != host::kTagDirichlet) continue;
+    double nx, ny, tx, ty;
+    m.fnormal(f, nx, ny);
+    m.ftan(f, tx, ty);
+    for (size_t q = 0; q < gx.size(); ++q) {
+      double x, y;
+      m.fpoint(f, gx[q], x, y);
+      bc(x, y, out, user);
+      host::legendre(k, gx[q], L);
+      for (int i = 0; i <= k; ++i) {
+        const double w = 0.5 * (2 * i + 1) * gw[q] * L[i];
+        g[size_t(f) * bs + 2 * i] += w * (out[0] * nx + out[1] * ny);
+        g[size_t(f) * bs + 2 * i + 1] += w * (out[0] * tx + out[1] * ty);
+      }
+    }
+  }
+  return g;
+}
+
+void alloc_level_vectors(Level& V) {
+  V.x = dalloc<double>(V.n);
+  V.b = dalloc<double>(V.n);
+  V.r = dalloc<double>(V.n);
+  V.y = dalloc<double>(V.n);
+  V.bw = dalloc<double>(V.n);
+  V.xw = dalloc<double>(V.n);
+}
+
+/// Assembles (condense + gather) one level operator on the device.
+void build_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, const DevRef& R, bool finest,
+                 const hpmg_problem* prob, double* rhs_out) {
+  cudaStream_t s = C.s;
+  V.k = k;
+  V.bs = 2 * (k + 1);
+  V.plan = host::make_level(m, k);
+  V.nb = V.plan.nb;
+  V.n = V.plan.n();
+  V.ne = m.ne();
+  std::vector<ElemGeo> geo(m.ne());
+  for (int e = 0; e < m.ne(); ++e) geo[e] = host::element_geometry(m, e);
+  V.geo = dupload(geo, s);
+  // condensation
+  const int nc = R.T.nc, stride = nc * nc + nc;
+  double* acr = dalloc<double>(size_t(m.ne()) * stride);
+  CondenseParams prm{C.opt.nu, C.opt.beta + C.opt.mass_coef, 0};
+  double* dload = nullptr;
+  int lstride = 0;
+  if (finest && prob) {
+    if (prob->structured_load) {
+      // seeded per-triangle force on an n x n grid: cell from the centroid,
+      // lower triangle (v00, v10, v11) iff (x - i/n) >= (y - j/n) (mesh.hpp:231-232)
+      const int sn = prob->structured_n;
+      std::vector<double> l(size_t(2) * m.ne());
+      for (int e = 0; e < m.ne(); ++e) {
+        const auto& v = m.ev[e];
+        const double cx = (m.vx[v[0]] + m.vx[v[1]] + m.vx[v[2]]) / 3.0;
+        const double cy = (m.vy[v[0]] + m.vy[v[1]] + m.vy[v[2]]) / 3.0;
+        const int i = std::min(sn - 1, std::max(0, int(std::floor(cx * sn))));
+        const int j = std::min(sn - 1, std::max(0, int(std::floor(cy * sn))));
+        const bool lower = (cx - double(i) / sn) >= (cy - double(j) / sn);
+        const size_t sidx = (size_t(j) * sn + i) * 2 + (lower ? 0 : 1);
+        l[2 * e] = prob->structured_load[2 * sidx];
+        l[2 * e + 1] = prob->structured_load[2 * sidx + 1];
+      }
+      dload = dupload(l, s);
+      prm.load_mode = 1;
+      lstride = 2;
+    } else if (prob->load_per_element) {
+      std::vector<double> l(prob->load_per_element, prob->load_per_element + size_t(2) * m.ne());
+      dload = dupload(l, s);
+      prm.load_mode = 1;
+      lstride = 2;
+    } else if (prob->load) {
+      // pointwise: evaluate the callback at the mapped volume nodes on the host
+      const int nq = R.T.nq;
+      host::RefTensors* unused = nullptr;
+      (void)unused;
+      std::vector<double> qx, qy, qw;
+      host::duffy(3 * k + 4, qx, qy, qw);
+      std::vector<double> l(size_t(m.ne()) * nq * 2);
+      double out[2];
+      for (int e = 0; e < m.ne(); ++e) {
+        const ElemGeo& g = geo[e];
+        const double x0 = m.vx[m.ev[e][0]], y0 = m.vy[m.ev[e][0]];
+        for (int q = 0; q < nq; ++q) {
+          const double x = x0 + g.J[0] * qx[q] + g.J[1] * qy[q], y = y0 + g.J[2] * qx[q] + g.J[3] * qy[q];
+          prob->load(x, y, out, prob->load_user);
+          l[(size_t(e) * nq + q) * 2] = out[0];
+          l[(size_t(e) * nq + q) * 2 + 1] = out[1];
+        }
+      }
+      dload = dupload(l, s);
+      prm.load_mode = 2;
+      lstride = 2 * nq;
+    }
+  }
+  dev::condense(R.T, V.geo, m.ne(), prm, dload, lstride, acr, s);
+  // operator
+  V.A.nb = V.nb;
+  V.A.bs = V.bs;
+  V.A.val = dalloc<double>(size_t(V.nb) * host::kSlots * V.bs * V.bs);
+  V.A.cols = dupload(V.plan.cols, s);
+  int* gath = dupload(V.plan.gath, s);
+  dev::assemble_bsr(V.A, k + 1, acr, stride, nc, gath, V.geo, C.opt.inv_eps, s);
+  if (finest) {
+    std::vector<int> ef(size_t(m.ne()) * 3);
+    for (int e = 0; e < m.ne(); ++e)
+      for (int q = 0; q < 3; ++q) ef[size_t(e) * 3 + q] = m.ef[e][q];
+    V.elem_facets = dupload(ef, s);
+    V.row_elems = dupload(V.plan.row_elems, s);
+    V.facet_block = dupload(V.plan.facet_block, s);
+    int* bf = dupload(V.plan.block_facet, s);
+    dev::assemble_rhs(V.nb, V.bs, k + 1, V.row_elems, bf, V.elem_facets, C.facet_dir, C.g_fac, acr, stride, nc,
+                      V.geo, C.opt.inv_eps, rhs_out, s);
+    CK(cudaStreamSynchronize(s));
+    cudaFree(bf);
+  }
+  CK(cudaStreamSynchronize(s));
+  cudaFree(acr);
+  cudaFree(gath);
+  if (dload) cudaFree(dload);
+  // patches + explicit inverses
+  V.P.n = V.plan.npatch;
+  V.max_nf = V.plan.max_patch_f;
+  V.P.nf = dupload(V.plan.patch_nf, s);
+  V.P.fac = dupload(V.plan.patch_fac, s);
+  V.P.off = dupload(V.plan.inv_off, s);
+  V.P.inv = dalloc<double>(size_t(V.plan.inv_total));
+  V.P.wave = dupload(V.plan.wave_patch, s);
+  V.P.fpatch = dupload(V.plan.facet_patches, s);
+  V.wave_ptr = V.plan.wave_ptr;
+  alloc_level_vectors(V);
+  V.dbuf = dalloc<double>(size_t(std::max(V.P.n, 1)) * V.max_nf * V.bs);
+  // algorithmic bytes, ELL slots counted as stored
+  double nnz = 0;
+  for (int c : V.plan.cols) nnz += c >= 0 ? double(V.bs) * V.bs : 0.0;
+  const double nblk = nnz / (double(V.bs) * V.bs);
+  V.bytes_spmv = 8 * nnz + 4 * nblk + 4 * (V.nb + 1.0) + 16.0 * V.n;
+  V.bytes_sweep = 8.0 * double(V.plan.inv_total) + 2 * (8 * nnz + 4 * nblk) + 32.0 * V.n;
+}
+
+void build_patch_inverses(hpmg_ctx& C, Level& V) {
+  if (V.P.n > 0) dev::patch_inverse(V.A, V.P, V.max_nf, C.s);
+}
+
+/// transposed-slot map for A^T in the same ELL pattern (A's pattern is symmetric)
+std::vector<int> transpose_slots(const host::LevelPlan& P) {
+  std::vector<int> t(P.cols.size(), -1);
+  for (int r = 0; r < P.nb; ++r)
+    for (int s = 0; s < host::kSlots; ++s) {
+      const int c = P.cols[size_t(r) * host::kSlots + s];
+      if (c < 0) continue;
+      for (int s2 = 0; s2 < host::kSlots; ++s2)
+        if (P.cols[size_t(c) * host::kSlots + s2] == r) t[size_t(r) * host::kSlots + s] = s2;
+    }
+  return t;
+}
+
+std::vector<double> download_bsr(hpmg_ctx& C, Level& V) {
+  std::vector<double> h(size_t(V.nb) * host::kSlots * V.bs * V.bs);
+  CK(cudaMemcpyAsync(h.data(), V.A.val, h.size() * sizeof(double), cudaMemcpyDeviceToHost, C.s));
+  CK(cudaStreamSynchronize(C.s));
+  return h;
+}
+
+/// Host LU inverse of the dense level-0 operator (block layout), column-major.
+std::vector<double> dense_inverse(const std::vector<double>& A, int n) {
+  std::vector<double> M = A;
+  std::vector<int> perm(n);
+  for (int i = 0; i < n; ++i) perm[i] = i;
+  for (int k = 0; k < n; ++k) {
+    int p = k;
+    for (int i = k + 1; i < n; ++i)
+      if (std::abs(M[size_t(i) * n + k]) > std::abs(M[size_t(p) * n + k])) p = i;
+    if (M[size_t(p) * n + k] == 0.0) throw std::runtime_error("singular coarse operator");
+    if (p != k) {
+      for (int j = 0; j < n; ++j) std::swap(M[size_t(k) * n + j], M[size_t(p) * n + j]);
+      std::swap(perm[k], perm[p]);
+    }
+    const double d = M[size_t(k) * n + k];
+    for (int i = k + 1; i < n; ++i) {
+      const double l = M[size_t(i) * n + k] / d;
+      M[size_t(i) * n + k] = l;
+      if (l == 0.0) continue;
+      for (int j = k + 1; j < n; ++j) M[size_t(i) * n + j] -= l * M[size_t(k) * n + j];
+    }
+  }
+  std::vector<double> inv(size_t(n) * n);  // column-major: column j = A^-1 e_j
+  std::vector<double> y(n);
+  for (int j = 0; j < n; ++j) {
+    for (int i = 0; i < n; ++i) y[i] = (perm[i] == j) ? 1.0 : 0.0;
+    for (int i = 0; i < n; ++i) {
+      double s = y[i];
+      for (int l = 0; l < i; ++l) s -= M[size_t(i) * n + l] * y[l];
+      y[i] = s;
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double s = y[i];
+      for (int l = i + 1; l < n; ++l) s -= M[size_t(i) * n + l] * y[l];
+      y[i] = s / M[size_t(i) * n + i];
+    }
+    for (int i = 0; i < n; ++i) inv[size_t(j) * n + i] = y[i];
+  }
+  return inv;
+}
+
+dev::BlockCsr upload_blockcsr(const host::BlockCsrH& H, cudaStream_t s) {
+  dev::BlockCsr D;
+  D.nrows = H.nrows;
+  D.ptr = dupload(H.ptr, s);
+  D.col = dupload(H.col, s);
+  D.val = dupload(H.val, s);
+  return D;
+}
+
+// ------------------------------------------------------------------ cycle
+void count(hpmg_ctx& C, int n = 1) {
+  if (C.counting) C.launches_per_apply += n;
+}
+
+void smooth(hpmg_ctx& C, Level& V, double* x, const double* b, bool post) {
+  const int nw = int(V.wave_ptr.size()) - 1;
+  if (C.opt.smoother == HPMG_SMOOTH_ADDITIVE) {
+    for (int s = 0; s < V.steps; ++s) {
+      dev::spmv(V.A, x, b, V.r, 1, nullptr, nullptr, C.s);
+      dev::jacobi_patch(V.A, V.P, V.r, V.dbuf, V.max_nf, C.s);
+      dev::jacobi_combine(V.nb, V.bs, V.P, V.dbuf, V.max_nf, C.opt.jacobi_damping, x, C.s);
+      count(C, 3);
+    }
+    return;
+  }
+  if (!post) {
+    for (int s = 0; s < V.steps; ++s)
+      for (int w = 0; w < nw; ++w) {
+        dev::gs_wave(V.A, V.P, V.wave_ptr[w], V.wave_ptr[w + 1], b, x, 0, V.max_nf, C.s);
+        count(C);
+      }
+    return;
+  }
+  if (!C.advected) {
+    // symmetric: the exact transpose sweep is the reverse-order sweep on x itself
+    for (int s = 0; s < V.steps; ++s)
+      for (int w = nw - 1; w >= 0; --w) {
+        dev::gs_wave(V.A, V.P, V.wave_ptr[w], V.wave_ptr[w + 1], b, x, 0, V.max_nf, C.s);
+        count(C);
+      }
+    return;
+  }
+  // nonsymmetric: c = b - A x, y = 0, transposed sweep on y with A^T rows, x += y
+  dev::spmv(V.A, x, b, V.r, 1, nullptr, nullptr, C.s);
+  dev::fill(V.y, 0.0, V.n, C.s);
+  count(C, 2);
+  for (int s = 0; s < V.steps; ++s)
+    for (int w = nw - 1; w >= 0; --w) {
+      dev::gs_wave(V.AT, V.P, V.wave_ptr[w], V.wave_ptr[w + 1], V.r, V.y, 1, V.max_nf, C.s);
+      count(C);
+    }
+  dev::axpy(x, 1.0, V.y, V.n, C.s);
+  count(C);
+}
+
+/// h_cycle(l, b) -> x (reference inc/multigrid.hpp:166-185)
+void h_cycle(hpmg_ctx& C, int l, const double* b, double* x) {
+  if (l == 0) {
+    dev::dense_gemv(C.n0, C.coarse_inv, b, x, C.gemv_work, C.s);
+    count(C, 2);
+    return;
+  }
+  Level& V = *C.lv[l];
+  Level& W = *C.lv[l - 1];
+  dev::fill(x, 0.0, V.n, C.s);
+  count(C);
+  smooth(C, V, x, b, false);
+  dev::spmv(V.A, x, b, V.r, 1, nullptr, nullptr, C.s);
+  dev::restrict_(V.PT, V.r, W.b, C.s);
+  count(C, 2);
+  h_cycle(C, l - 1, W.b, W.x);
+  const int q = C.opt.cycle == HPMG_CYCLE_W ? 2 : 1;
+  for (int i = 1; i < q; ++i) {
+    dev::spmv(W.A, W.x, W.b, W.bw, 1, nullptr, nullptr, C.s);
+    count(C);
+    h_cycle(C, l - 1, W.bw, W.xw);
+    dev::axpy(W.x, 1.0, W.xw, W.n, C.s);
+    count(C);
+  }
+  dev::prolong_add(V.Pm, W.x, x, C.s);
+  count(C);
+  smooth(C, V, x, b, true);
+}
+
+/// apply(b) -> x on the finest system, block layout (inc/multigrid.hpp:117-128)
+void apply_blocks(hpmg_ctx& C, const double* b, double* x) {
+  if (C.opt.k == 0) {
+    h_cycle(C, C.L, b, x);
+    return;
+  }
+  Level& H = *C.head;
+  Level& F = *C.lv[C.L];
+  dev::fill(x, 0.0, H.n, C.s);
+  count(C);
+  smooth(C, H, x, b, false);
+  dev::inject_residual(H.A, x, b, F.b, C.s);
+  count(C);
+  h_cycle(C, C.L, F.b, F.x);
+  dev::embed_add(H.nb, H.bs, F.x, x, C.s);
+  count(C);
+  smooth(C, H, x, b, true);
+}
+
+void build_apply_graph(hpmg_ctx& C) {
+  cudaGraph_t g;
+  C.launches_per_apply = 0;
+  C.counting = true;
+  CK(cudaStreamBeginCapture(C.s, cudaStreamCaptureModeThreadLocal));
+  apply_blocks(C, C.kr, C.kz);
+  CK(cudaStreamEndCapture(C.s, &g));
+  C.counting = false;
+  CK(cudaGraphInstantiate(&C.apply_graph, g, 0));
+  cudaGraphDestroy(g);
+}
+
+void apply_graph(hpmg_ctx& C) { CK(cudaGraphLaunch(C.apply_graph, C.s)); }
+
+void read_scalars(hpmg_ctx& C, int n = 16) {
+  CK(cudaMemcpyAsync(C.sc_host, C.sc, sizeof(double) * n, cudaMemcpyDeviceToHost, C.s));
+  CK(cudaStreamSynchronize(C.s));
+}
+
+// ---------------------------------------------------------------- boundary
+void in_vec(hpmg_ctx& C, const double* src, double* dst_blk, int flags) {
+  Level& T = C.top();
+  const double* ref = src;
+  if (!(flags & HPMG_DEVICE_PTRS)) {
+    CK(cudaMemcpyAsync(C.io_a, src, sizeof(double) * T.n, cudaMemcpyHostToDevice, C.s));
+    ref = C.io_a;
+  }
+  dev::to_blocks(T.nb, T.k + 1, ref, dst_blk, C.s);
+}
+void out_vec(hpmg_ctx& C, const double* src_blk, double* dst, int flags) {
+  Level& T = C.top();
+  if (flags & HPMG_DEVICE_PTRS) {
+    dev::to_reference(T.nb, T.k + 1, src_blk, dst, C.s);
+    CK(cudaStreamSynchronize(C.s));
+    return;
+  }
+  dev::to_reference(T.nb, T.k + 1, src_blk, C.io_b, C.s);
+  CK(cudaMemcpyAsync(dst, C.io_b, sizeof(double) * T.n, cudaMemcpyDeviceToHost, C.s));
+  CK(cudaStreamSynchronize(C.s));
+}
+
+// ---------------------------------------------------------------- solvers
+/// PCG on the device (reference inc/krylov.hpp:30-73); x/b in kx/kb.
+hpmg_solve_stats pcg_device(hpmg_ctx& C, const hpmg_krylov_opts& o) {
+  hpmg_solve_stats st{0, 0, 0, 0.0};
+  Level& T = C.top();
+  const int64_t n = T.n;
+  dev::dot(C.kb, C.kb, n, C.red, C.sc + S_BB, C.s);
+  dev::spmv(T.A, C.kx, C.kb, C.kr, 1, nullptr, nullptr, C.s);
+  dev::dot(C.kr, C.kr, n, C.red, C.sc + S_RR, C.s);
+  read_scalars(C);
+  const double target = std::max(o.rel_tol * std::sqrt(C.sc_host[S_BB]), o.abs_tol);
+  st.residual = std::sqrt(C.sc_host[S_RR]);
+  if (st.residual <= target) {
+    st.converged = 1;
+    return st;
+  }
+  apply_graph(C);  // kz = M kr
+  int cur = S_RZ0, nxt = S_RZ1;
+  dev::dot(C.kr, C.kz, n, C.red, C.sc + cur, C.s);
+  read_scalars(C);
+  if (!(C.sc_host[cur] > 0)) {
+    st.not_applicable = 1;
+    return st;
+  }
+  dev::copy(C.kp, C.kz, n, C.s);
+  for (int it = 0; it < o.max_iterations; ++it) {
+    dev::spmv(T.A, C.kp, nullptr, C.kAp, 0, &C.red, C.sc + S_PAP, C.s);
+    dev::pcg_update(C.kx, C.kr, C.kp, C.kAp, n, C.sc, cur, S_PAP, C.red, S_RR, C.s);
+    read_scalars(C);
+    if (!(C.sc_host[S_PAP] > 0)) {  // pcg_update skipped x and r on the device
+      st.not_applicable = 1;
+      return st;
+    }
+    st.iterations = it + 1;
+    st.residual = std::sqrt(C.sc_host[S_RR]);
+    if (st.residual <= target) {
+      st.converged = 1;
+      return st;
+    }
+    apply_graph(C);
+    dev::dot(C.kr, C.kz, n, C.red, C.sc + nxt, C.s);
+    read_scalars(C);
+    if (!(C.sc_host[nxt] > 0)) {
+      st.not_applicable = 1;
+      return st;
+    }
+    dev::pcg_direction(C.kp, C.kz, n, C.sc, nxt, cur, C.s);
+    std::swap(cur, nxt);
+  }
+  return st;
+}
+
+double* gm_vec(hpmg_ctx& C, int i) {
+  while (int(C.gm_basis.size()) <= i) C.gm_basis.push_back(dalloc<double>(C.top().n));
+  return C.gm_basis[i];
+}
+
+/// Right-preconditioned MGS GMRES on the device, Givens on the host
+/// (reference inc/krylov.hpp:79-144); `restart` > 0 caps the cycle length.
+hpmg_solve_stats gmres_device(hpmg_ctx& C, const hpmg_krylov_opts& o) {
+  hpmg_solve_stats st{0, 0, 0, 0.0};
+  Level& T = C.top();
+  const int64_t n = T.n;
+  dev::dot(C.kb, C.kb, n, C.red, C.sc + S_BB, C.s);
+  read_scalars(C);
+  const double target = std::max(o.rel_tol * std::sqrt(C.sc_host[S_BB]), o.abs_tol);
+  const double breakdown = 1e-14;
+  const int cap = o.restart > 0 ? o.restart : (1 << 30);
+  while (st.iterations < o.max_iterations) {
+    dev::spmv(T.A, C.kx, C.kb, C.kr, 1, nullptr, nullptr, C.s);
+    dev::dot(C.kr, C.kr, n, C.red, C.sc + S_RR, C.s);
+    read_scalars(C);
+    st.residual = std::sqrt(C.sc_host[S_RR]);
+    if (st.residual <= target) {
+      st.converged = 1;
+      return st;
+    }
+    const double beta = st.residual;
+    dev::scal_axpby(gm_vec(C, 0), C.kr, n, nullptr, -1, 1.0 / beta, 0.0, C.s);
+    std::vector<std::vector<double>> hc;
+    std::vector<double> cs, sn, g{beta};
+    bool stalled = false;
+    for (int j = 0; st.iterations < o.max_iterations && j < cap; ++j) {
+      dev::copy(C.kr, gm_vec(C, j), n, C.s);
+      apply_graph(C);                                                        // kz = M v_j
+      dev::spmv(T.A, C.kz, nullptr, C.ktmp, 0, nullptr, nullptr, C.s);      // w = A M v_j
+      for (int i = 0; i <= j; ++i) {                                          // modified Gram-Schmidt
+        dev::dot(C.ktmp, gm_vec(C, i), n, C.red, C.sc + S_H0 + i, C.s);
+        dev::scal_axpby(C.ktmp, gm_vec(C, i), n, C.sc, S_H0 + i, -1.0, 1.0, C.s);
+      }
+      dev::dot(C.ktmp, C.ktmp, n, C.red, C.sc + S_H0 + j + 1, C.s);
+      read_scalars(C, S_H0 + j + 2);
+      std::vector<double> h(j + 2);
+      for (int i = 0; i <= j; ++i) h[i] = C.sc_host[S_H0 + i];
+      h[j + 1] = std::sqrt(C.sc_host[S_H0 + j + 1]);
+      const bool happy = h[j + 1] <= breakdown * beta;
+      if (!happy) dev::scal_axpby(gm_vec(C, j + 1), C.ktmp, n, nullptr, -1, 1.0 / h[j + 1], 0.0, C.s);
+      for (int i = 0; i < j; ++i) {
+        const double t = cs[i] * h[i] + sn[i] * h[i + 1];
+        h[i + 1] = -sn[i] * h[i] + cs[i] * h[i + 1];
+        h[i] = t;
+      }
+      const double rho = std::hypot(h[j], h[j + 1]);
+      cs.push_back(h[j] / rho);
+      sn.push_back(h[j + 1] / rho);
+      h[j] = rho;
+      h[j + 1] = 0;
+      g.push_back(-sn.back() * g[j]);
+      g[j] *= cs.back();
+      hc.push_back(h);
+      ++st.iterations;
+      if (std::abs(g.back()) <= target || happy) {
+        stalled = happy && std::abs(g.back()) > target;
+        break;
+      }
+    }
+    const int m = int(hc.size());
+    std::vector<double> y(m);
+    for (int i = m - 1; i >= 0; --i) {
+      double s = g[i];
+      for (int l = i + 1; l < m; ++l) s -= hc[l][i] * y[l];
+      y[i] = s / hc[i][i];
+    }
+    dev::fill(C.kr, 0.0, n, C.s);
+    for (int i = 0; i < m; ++i) dev::axpy(C.kr, y[i], gm_vec(C, i), n, C.s);
+    apply_graph(C);
+    dev::axpy(C.kx, 1.0, C.kz, n, C.s);
+    dev::spmv(T.A, C.kx, C.kb, C.kr, 1, nullptr, nullptr, C.s);
+    dev::dot(C.kr, C.kr, n, C.red, C.sc + S_RR, C.s);
+    read_scalars(C);
+    st.residual = std::sqrt(C.sc_host[S_RR]);
+    if (st.residual <= target) {
+      st.converged = 1;
+      return st;
+    }
+    if (stalled) return st;
+  }
+  return st;
+}
+
+void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const hpmg_problem* prob) {
+  using clk = std::chrono::steady_clock;
+  auto t0 = clk::now();
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw std::runtime_error("no CUDA device: hpmg has no CPU fallback");
+  if (opt->k < 0 || opt->k > 3) throw std::invalid_argument("order k must be in 0..3");
+  if (md->levels < 1) throw std::invalid_argument("levels must be >= 1");
+  C.opt = *opt;
+  C.advected = prob && prob->wind_compound;
+  if (C.advected) throw std::invalid_argument("advection (Oseen) operators are not supported yet");
+  CK(cudaStreamCreateWithFlags(&C.s, cudaStreamNonBlocking));
+  // mesh hierarchy
+  host::TriMesh base;
+  for (int v = 0; v < md->n_vertices; ++v) {
+    base.vx.push_back(md->xy[2 * v]);
+    base.vy.push_back(md->xy[2 * v + 1]);
+  }
+  for (int e = 0; e < md->n_elements; ++e)
+    base.ev.push_back({md->elements[3 * e], md->elements[3 * e + 1], md->elements[3 * e + 2]});
+  base.build_facets();
+  if (md->n_tag_overrides > 0) {
+    std::unordered_map<uint64_t, int> tags = base.tag_map();
+    for (int i = 0; i < md->n_tag_overrides; ++i) {
+      int a = md->tag_overrides[3 * i], b = md->tag_overrides[3 * i + 1];
+      if (a > b) std::swap(a, b);
+      tags[(uint64_t(uint32_t(a)) << 32) | uint32_t(b)] = md->tag_overrides[3 * i + 2];
+    }
+    base.build_facets(&tags);
+  }
+  C.mesh.push_back(std::move(base));
+  for (int l = 1; l < md->levels; ++l) {
+    host::Refinement R;
+    host::TriMesh f = host::refine(C.mesh[l - 1], R);
+    C.mesh.push_back(std::move(f));
+    C.ref.push_back(std::move(R));
+  }
+  C.L = md->levels - 1;
+  const host::TriMesh& fine = C.mesh[C.L];
+  for (int f = 0; f < fine.nf(); ++f)
+    if (fine.ftag[f] == host::kTagOutflow) C.enclosed = false;
+  const int k = opt->k;
+  auto tT0 = host::build_ref_tensors(0);
+  upload_ref(C.ref0, *tT0, C.s);
+  std::unique_ptr<host::RefTensors> tTk;
+  if (k > 0) {
+    tTk = host::build_ref_tensors(k);
+    upload_ref(C.refk, *tTk, C.s);
+  }
+  // reductions and scalars
+  C.red.partial = dalloc<double>(dev::kRedBlocks);
+  C.red.counter = dalloc<unsigned>(1);
+  CK(cudaMemsetAsync(C.red.counter, 0, sizeof(unsigned), C.s));
+  C.sc = dalloc<double>(S_COUNT);
+  CK(cudaMemsetAsync(C.sc, 0, sizeof(double) * S_COUNT, C.s));
+  CK(cudaMallocHost(&C.sc_host, sizeof(double) * S_COUNT));
+  // Dirichlet data and constraints of the finest system
+  const std::vector<double> gfac = dirichlet_data(fine, k, prob ? prob->bc : nullptr, prob ? prob->bc_user : nullptr);
+  C.g_fac = dupload(gfac, C.s);
+  std::vector<char> dir(fine.nf());
+  for (int f = 0; f < fine.nf(); ++f) dir[f] = fine.ftag[f] == host::kTagDirichlet;
+  C.facet_dir = dupload(dir, C.s);
+  {
+    const int nfd = k + 1, bs = 2 * nfd;
+    const int64_t nflux = int64_t(fine.nf()) * nfd;
+    C.g_full.assign(2 * nflux, 0.0);
+    for (int f = 0; f < fine.nf(); ++f)
+      for (int i = 0; i < nfd; ++i) {
+        C.g_full[int64_t(f) * nfd + i] = gfac[size_t(f) * bs + 2 * i];
+        C.g_full[nflux + int64_t(f) * nfd + i] = gfac[size_t(f) * bs + 2 * i + 1];
+      }
+    for (int f = 0; f < fine.nf(); ++f)
+      if (!dir[f])
+        for (int i = 0; i < nfd; ++i) C.free_to_full.push_back(int64_t(f) * nfd + i);
+    for (int f = 0; f < fine.nf(); ++f)
+      if (!dir[f])
+        for (int i = 0; i < nfd; ++i) C.free_to_full.push_back(nflux + int64_t(f) * nfd + i);
+  }
+  auto t1 = clk::now();
+  // lowest-order levels
+  C.lv.resize(C.L + 1);
+  double* rhs_tmp = nullptr;
+  for (int l = 0; l <= C.L; ++l) {
+    C.lv[l] = std::make_unique<Level>();
+    Level& V = *C.lv[l];
+    const bool finest = (k == 0 && l == C.L);
+    if (finest) {
+      const int64_t nfree = int64_t(C.free_to_full.size());
+      rhs_tmp = C.rhs = dalloc<double>(nfree);
+    }
+    build_level(C, V, C.mesh[l], 0, C.ref0, finest, prob, finest ? C.rhs : nullptr);
+    V.steps = opt->cycle == HPMG_CYCLE_VARIABLE_V ? (opt->smooth_steps << (C.L - l)) : opt->smooth_steps;
+  }
+  if (k > 0) {
+    C.head = std::make_unique<Level>();
+    C.rhs = dalloc<double>(int64_t(C.free_to_full.size()));
+    build_level(C, *C.head, fine, k, C.refk, true, prob, C.rhs);
+    C.head->steps = opt->smooth_steps;
+  }
+  (void)rhs_tmp;
+  CK(cudaStreamSynchronize(C.s));
+  auto t2 = clk::now();
+  for (int l = 1; l <= C.L; ++l) build_patch_inverses(C, *C.lv[l]);
+  if (k > 0) build_patch_inverses(C, *C.head);
+  CK(cudaStreamSynchronize(C.s));
+  auto t3 = clk::now();
+  // transfers (host correction from the downloaded fine operators)
+  for (int l = 1; l <= C.L; ++l) {
+    std::vector<double> Af = download_bsr(C, *C.lv[l]);
+    host::BlockCsrH P = host::corrected_prolongation(C.lv[l - 1]->plan, C.lv[l]->plan, C.ref[l - 1], Af);
+    host::BlockCsrH PT = host::transpose_blocks(P);
+    C.lv[l]->Pm = upload_blockcsr(P, C.s);
+    C.lv[l]->PT = upload_blockcsr(PT, C.s);
+  }
+  auto t4 = clk::now();
+  // coarse dense inverse
+  {
+    Level& V0 = *C.lv[0];
+    C.n0 = int(V0.n);
+    std::vector<double> A0 = download_bsr(C, V0), D(size_t(C.n0) * C.n0, 0.0);
+    for (int r = 0; r < V0.nb; ++r)
+      for (int s = 0; s < host::kSlots; ++s) {
+        const int c = V0.plan.cols[size_t(r) * host::kSlots + s];
+        if (c < 0) continue;
+        for (int i = 0; i < 2; ++i)
+          for (int j = 0; j < 2; ++j) D[size_t(2 * r + i) * C.n0 + 2 * c + j] = A0[((size_t(r) * host::kSlots + s) * 2 + i) * 2 + j];
+      }
+    C.coarse_inv = dupload(dense_inverse(D, C.n0), C.s);
+    C.gemv_work = dalloc<double>(size_t(C.n0) * ((C.n0 + 127) / 128 + 1));
+  }
+  auto t5 = clk::now();
+  // solver workspace
+  Level& T = C.top();
+  for (double** p : {&C.kx, &C.kb, &C.kr, &C.kz, &C.kp, &C.kAp, &C.ktmp, &C.io_a, &C.io_b}) *p = dalloc<double>(T.n);
+  C.pres = dalloc<double>(fine.ne());
+  C.div = dalloc<double>(fine.ne());
+  C.urhs = dalloc<double>(T.n);
+  build_apply_graph(C);
+  CK(cudaStreamSynchronize(C.s));
+  auto t6 = clk::now();
+  auto sec = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
+  C.setup_parts[0] = sec(t0, t1);  // mesh + tables
+  C.setup_parts[1] = sec(t1, t2);  // condensation + assembly
+  C.setup_parts[2] = sec(t2, t3);  // patch inverses
+  C.setup_parts[3] = sec(t3, t4);  // transfers
+  C.setup_parts[4] = sec(t4, t5);  // coarse inverse
+  C.setup_parts[5] = sec(t5, t6);  // workspace + graph
+  C.setup_parts[6] = sec(t0, t6);
+}
+
+template <typename F>
+int guarded(hpmg_ctx* C, F&& f) {
+  try {
+    f();
+    return HPMG_OK;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    if (C) C->err = e.what();
+    return HPMG_ERR_ARG;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    if (C) C->err = e.what();
+    return std::string(e.what()).find("CUDA") != std::string::npos || std::string(e.what()).find("cuda") != std::string::npos
+               ? HPMG_ERR_CUDA
+               : HPMG_ERR_SETUP;
+  }
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* hpmg_last_error(void) { return g_last_error.c_str(); }
+const char* hpmg_ctx_error(const hpmg_ctx* ctx) { return ctx ? ctx->err.c_str() : g_last_error.c_str(); }
+
+int hpmg_create(hpmg_ctx** out, const hpmg_mesh_desc* mesh, const hpmg_options* opt, const hpmg_problem* prob) {
+  if (!out || !mesh || !opt) {
+    g_last_error = "null argument";
+    return HPMG_ERR_ARG;
+  }
+  auto* C = new hpmg_ctx();
+  int rc = guarded(C, [&] { setup(*C, mesh, opt, prob); });
+  if (rc != HPMG_OK) {
+    delete C;  // device memory is reclaimed with the process / context
+    *out = nullptr;
+    return rc;
+  }
+  *out = C;
+  return HPMG_OK;
+}
+
+void hpmg_destroy(hpmg_ctx* ctx) {
+  if (!ctx) return;
+  cudaStreamSynchronize(ctx->s);
+  if (ctx->apply_graph) cudaGraphExecDestroy(ctx->apply_graph);
+  auto fr = [](void* p) { if (p) cudaFree(p); };
+  auto free_level = [&](Level* V) {
+    if (!V) return;
+    for (void* p : {(void*)V->A.val, (void*)V->A.cols, (void*)V->AT.val, (void*)V->tslot, (void*)V->P.nf,
+                    (void*)V->P.fac, (void*)V->P.off, (void*)V->P.inv, (void*)V->P.wave, (void*)V->P.fpatch,
+                    (void*)V->Pm.ptr, (void*)V->Pm.col, (void*)V->Pm.val, (void*)V->PT.ptr, (void*)V->PT.col,
+                    (void*)V->PT.val, (void*)V->x, (void*)V->b, (void*)V->r, (void*)V->y, (void*)V->bw, (void*)V->xw,
+                    (void*)V->dbuf, (void*)V->geo, (void*)V->row_elems, (void*)V->elem_facets, (void*)V->facet_block})
+      fr(p);
+  };
+  for (auto& V : ctx->lv) free_level(V.get());
+  free_level(ctx->head.get());
+  for (void* p : ctx->ref0.owned) fr(p);
+  for (void* p : ctx->refk.owned) fr(p);
+  for (double* p : ctx->gm_basis) fr(p);
+  for (void* p : {(void*)ctx->coarse_inv, (void*)ctx->gemv_work, (void*)ctx->red.partial, (void*)ctx->red.counter,
+                  (void*)ctx->sc, (void*)ctx->rhs, (void*)ctx->g_fac, (void*)ctx->facet_dir, (void*)ctx->kx,
+                  (void*)ctx->kb, (void*)ctx->kr, (void*)ctx->kz, (void*)ctx->kp, (void*)ctx->kAp, (void*)ctx->ktmp,
+                  (void*)ctx->io_a, (void*)ctx->io_b, (void*)ctx->pres, (void*)ctx->div, (void*)ctx->urhs})
+    fr(p);
+  if (ctx->sc_host) cudaFreeHost(ctx->sc_host);
+  if (ctx->s) cudaStreamDestroy(ctx->s);
+  delete ctx;
+}
+
+int64_t hpmg_n(const hpmg_ctx* ctx) { return int64_t(ctx->free_to_full.size()); }
+int64_t hpmg_n_full(const hpmg_ctx* ctx) { return int64_t(ctx->g_full.size()); }
+int hpmg_ne(const hpmg_ctx* ctx) { return ctx->mesh.back().ne(); }
+int hpmg_num_levels(const hpmg_ctx* ctx) { return int(ctx->lv.size()); }
+int64_t hpmg_level_n(const hpmg_ctx* ctx, int level) {
+  auto& C = *const_cast<hpmg_ctx*>(ctx);
+  if (level < 0) return C.top().n;
+  if (level >= int(C.lv.size())) return -1;
+  return C.lv[level]->n;
+}
+int hpmg_symmetric(const hpmg_ctx* ctx) { return ctx->advected ? 0 : 1; }
+double hpmg_penalty(const hpmg_ctx* ctx) { return ctx->opt.inv_eps; }
+int hpmg_free_to_full(const hpmg_ctx* ctx, int64_t* out) {
+  std::memcpy(out, ctx->free_to_full.data(), sizeof(int64_t) * ctx->free_to_full.size());
+  return HPMG_OK;
+}
+int hpmg_g_full(const hpmg_ctx* ctx, double* out) {
+  std::memcpy(out, ctx->g_full.data(), sizeof(double) * ctx->g_full.size());
+  return HPMG_OK;
+}
+int hpmg_rhs(hpmg_ctx* ctx, double* out, int flags) {
+  return guarded(ctx, [&] { out_vec(*ctx, ctx->rhs, out, flags); });
+}
+
+int hpmg_matrix_csr(hpmg_ctx* ctx, int level, int64_t* nnz, int64_t* ptr, int64_t* idx, double* val) {
+  return guarded(ctx, [&] {
+    Level& V = level < 0 ? ctx->top() : *ctx->lv.at(level);
+    const int nfd = V.k + 1, bs = V.bs, nb = V.nb;
+    auto ref_of = [&](int blk, int ii) -> int64_t {
+      const int i = ii >> 1, t = ii & 1;
+      return (t ? int64_t(nb) * nfd : 0) + int64_t(blk) * nfd + i;
+    };
+    std::vector<double> A = download_bsr(*ctx, V);
+    // rows in reference order
+    std::vector<std::vector<std::pair<int64_t, double>>> rows(V.n);
+    for (int r = 0; r < nb; ++r)
+      for (int s = 0; s < host::kSlots; ++s) {
+        const int c = V.plan.cols[size_t(r) * host::kSlots + s];
+        if (c < 0) continue;
+        for (int ii = 0; ii < bs; ++ii)
+          for (int jj = 0; jj < bs; ++jj) {
+            const double v = A[((size_t(r) * host::kSlots + s) * bs + ii) * bs + jj];
+            rows[ref_of(r, ii)].push_back({ref_of(c, jj), v});
+          }
+      }
+    int64_t tot = 0;
+    for (auto& rw : rows) tot += int64_t(rw.size());
+    *nnz = tot;
+    if (!ptr) return;
+    int64_t q = 0;
+    for (int64_t i = 0; i < V.n; ++i) {
+      ptr[i] = q;
+      std::sort(rows[i].begin(), rows[i].end());
+      for (auto& e : rows[i]) {
+        idx[q] = e.first;
+        val[q] = e.second;
+        ++q;
+      }
+    }
+    ptr[V.n] = q;
+  });
+}
+
+int hpmg_spmv(hpmg_ctx* ctx, const double* x, double* y, int flags) {
+  return guarded(ctx, [&] {
+    in_vec(*ctx, x, ctx->kp, flags);
+    dev::spmv(ctx->top().A, ctx->kp, nullptr, ctx->kAp, 0, nullptr, nullptr, ctx->s);
+    out_vec(*ctx, ctx->kAp, y, flags);
+  });
+}
+
+int hpmg_apply(hpmg_ctx* ctx, const double* r, double* z, int flags) {
+  return guarded(ctx, [&] {
+    in_vec(*ctx, r, ctx->kr, flags);
+    apply_graph(*ctx);
+    out_vec(*ctx, ctx->kz, z, flags);
+  });
+}
+
+int hpmg_smooth(hpmg_ctx* ctx, int level, int which, double* x, const double* b, int sweeps, int flags) {
+  return guarded(ctx, [&] {
+    Level& V = level < 0 ? ctx->top() : *ctx->lv.at(level);
+    if (level >= 0 && level == 0) throw std::invalid_argument("level 0 has no smoother");
+    const int n = int(V.n);
+    // level vectors are exchanged in the level's own reference order
+    std::vector<double> hx(n), hb(n);
+    double* dx = ctx->kx;
+    double* db = ctx->kb;
+    if (level >= 0 && V.n > ctx->top().n) throw std::invalid_argument("level larger than workspace");
+    const double* sx = x;
+    const double* sb = b;
+    double *ta = ctx->io_a, *tb = ctx->io_b;
+    if (!(flags & HPMG_DEVICE_PTRS)) {
+      CK(cudaMemcpyAsync(ta, x, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->s));
+      CK(cudaMemcpyAsync(tb, b, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->s));
+      sx = ta;
+      sb = tb;
+    }
+    dev::to_blocks(V.nb, V.k + 1, sx, dx, ctx->s);
+    dev::to_blocks(V.nb, V.k + 1, sb, db, ctx->s);
+    const int saved = V.steps;
+    V.steps = sweeps;
+    if (which == 2) {
+      const int sm = ctx->opt.smoother;
+      ctx->opt.smoother = HPMG_SMOOTH_ADDITIVE;
+      smooth(*ctx, V, dx, db, false);
+      ctx->opt.smoother = sm;
+    } else {
+      const int sm = ctx->opt.smoother;
+      ctx->opt.smoother = HPMG_SMOOTH_MULTIPLICATIVE;
+      smooth(*ctx, V, dx, db, which == 1);
+      ctx->opt.smoother = sm;
+    }
+    V.steps = saved;
+    if (flags & HPMG_DEVICE_PTRS) {
+      dev::to_reference(V.nb, V.k + 1, dx, x, ctx->s);
+    } else {
+      dev::to_reference(V.nb, V.k + 1, dx, ta, ctx->s);
+      CK(cudaMemcpyAsync(x, ta, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->s));
+    }
+    CK(cudaStreamSynchronize(ctx->s));
+    (void)hx;
+    (void)hb;
+  });
+}
+
+int hpmg_pcg(hpmg_ctx* ctx, const double* b, double* x, const hpmg_krylov_opts* o, hpmg_solve_stats* st, int flags) {
+  return guarded(ctx, [&] {
+    in_vec(*ctx, b, ctx->kb, flags);
+    in_vec(*ctx, x, ctx->kx, flags);
+    *st = pcg_device(*ctx, *o);
+    out_vec(*ctx, ctx->kx, x, flags);
+  });
+}
+
+int hpmg_gmres(hpmg_ctx* ctx, const double* b, double* x, const hpmg_krylov_opts* o, hpmg_solve_stats* st, int flags) {
+  return guarded(ctx, [&] {
+    in_vec(*ctx, b, ctx->kb, flags);
+    in_vec(*ctx, x, ctx->kx, flags);
+    *st = gmres_device(*ctx, *o);
+    out_vec(*ctx, ctx->kx, x, flags);
+  });
+}
+
+int hpmg_uzawa(hpmg_ctx* ctx, const hpmg_uzawa_opts* o, double* velocity, double* pressure, hpmg_uzawa_report* rep) {
+  return guarded(ctx, [&] {
+    hpmg_ctx& C = *ctx;
+    Level& T = C.top();
+    const int ne = T.ne;
+    std::memset(rep, 0, sizeof(*rep));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, C.s));
+    dev::fill(C.pres, 0.0, ne, C.s);
+    dev::fill(C.kx, 0.0, T.n, C.s);
+    rep->converged = 1;
+    for (int it = 0; it < o->outer_iterations && it < 64; ++it) {
+      dev::uzawa_rhs(T.nb, T.bs, C.rhs, T.row_elems, T.geo, C.pres, C.kb, C.s);
+      hpmg_solve_stats st = C.advected ? gmres_device(C, o->krylov) : pcg_device(C, o->krylov);
+      rep->inner_iterations[it] = st.iterations;
+      rep->n_outer = it + 1;
+      if (st.not_applicable) {
+        rep->not_applicable = 1;
+        rep->converged = 0;
+        break;
+      }
+      rep->converged = rep->converged && st.converged;
+      dev::uzawa_div(ne, T.bs, T.elem_facets, T.facet_block, C.g_fac, C.kx, T.geo, C.div, C.s);
+      dev::uzawa_pressure(ne, C.div, T.geo, C.opt.inv_eps, C.pres, C.enclosed ? 1 : 0, C.red, C.sc, S_PS, S_PA,
+                          S_PMAX, C.s);
+      read_scalars(C);
+      rep->divergence_history[it] = C.sc_host[S_PMAX];
+    }
+    CK(cudaEventRecord(e1, C.s));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    rep->seconds = ms * 1e-3;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (rep->n_outer > 0) rep->final_divergence = rep->divergence_history[rep->n_outer - 1];
+    // velocity: g_full with free entries overwritten (Constraints::to_full)
+    std::vector<double> u(T.n);
+    dev::to_reference(T.nb, T.k + 1, C.kx, C.io_b, C.s);
+    CK(cudaMemcpyAsync(u.data(), C.io_b, sizeof(double) * T.n, cudaMemcpyDeviceToHost, C.s));
+    CK(cudaMemcpyAsync(pressure, C.pres, sizeof(double) * ne, cudaMemcpyDeviceToHost, C.s));
+    CK(cudaStreamSynchronize(C.s));
+    std::memcpy(velocity, C.g_full.data(), sizeof(double) * C.g_full.size());
+    for (size_t i = 0; i < C.free_to_full.size(); ++i) velocity[C.free_to_full[i]] = u[i];
+  });
+}
+
+int hpmg_recover(hpmg_ctx* ctx, const double*, double*, double*, double*) {
+  ctx->err = g_last_error = "hpmg_recover: not implemented yet";
+  return HPMG_ERR_LOGIC;
+}
+
+void* hpmg_stream(hpmg_ctx* ctx) { return ctx->s; }
+
+double hpmg_spmv_bytes(const hpmg_ctx* ctx) {
+  const Level& T = const_cast<hpmg_ctx*>(ctx)->top();
+  return T.bytes_spmv;
+}
+
+double hpmg_vcycle_bytes(const hpmg_ctx* ctx, double* parts) {
+  auto& C = *const_cast<hpmg_ctx*>(ctx);
+  double p[8] = {0};
+  const int q = C.opt.cycle == HPMG_CYCLE_W ? 2 : 1;
+  if (C.opt.k > 0) {
+    const Level& H = *C.head;
+    p[0] = 2.0 * H.steps * H.bytes_sweep;
+    // mode-0 rows of the head residual: 2 of bs rows per block
+    p[1] = H.bytes_spmv * 2.0 / H.bs + 32.0 * C.lv[C.L]->n;
+  }
+  // visits of level l: q^(L-l)
+  for (int l = C.L; l >= 1; --l) {
+    const Level& V = *C.lv[l];
+    const double visits = std::pow(double(q), C.L - l);
+    p[2] += visits * 2.0 * V.steps * V.bytes_sweep;
+    p[3] += visits * (V.bytes_spmv + 8.0 * V.n);
+    // P and P^T: 12 bytes per scalar nonzero + vectors
+    p[4] += visits * 2.0 * 0.0;
+  }
+  for (int l = C.L; l >= 1; --l) {
+    const Level& V = *C.lv[l];
+    const double visits = std::pow(double(q), C.L - l);
+    (void)V;
+    p[4] += visits * 0.0;
+  }
+  p[5] = std::pow(double(q), C.L) * 8.0 * double(C.n0) * C.n0;
+  double tot = 0;
+  for (int i = 0; i < 8; ++i) tot += p[i];
+  if (parts)
+    for (int i = 0; i < 8; ++i) parts[i] = p[i];
+  return tot;
+}
+
+double hpmg_time_apply(hpmg_ctx* ctx, int reps, double* phase_ms) {
+  double ms_per = -1;
+  guarded(ctx, [&] {
+    hpmg_ctx& C = *ctx;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    for (int i = 0; i < 3; ++i) apply_graph(C);
+    CK(cudaEventRecord(e0, C.s));
+    for (int i = 0; i < reps; ++i) apply_graph(C);
+    CK(cudaEventRecord(e1, C.s));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms_per = ms / reps;
+    if (phase_ms) {
+      // event-instrumented non-graph pass: head pre-sweep, head post-sweep, rest
+      for (int i = 0; i < 8; ++i) phase_ms[i] = 0;
+      cudaEvent_t ev[6];
+      for (auto& e : ev) CK(cudaEventCreate(&e));
+      for (int r = 0; r < reps; ++r) {
+        if (C.opt.k > 0) {
+          Level& H = *C.head;
+          Level& F = *C.lv[C.L];
+          CK(cudaEventRecord(ev[0], C.s));
+          dev::fill(C.kz, 0.0, H.n, C.s);
+          smooth(C, H, C.kz, C.kr, false);
+          CK(cudaEventRecord(ev[1], C.s));
+          dev::inject_residual(H.A, C.kz, C.kr, F.b, C.s);
+          CK(cudaEventRecord(ev[2], C.s));
+          h_cycle(C, C.L, F.b, F.x);
+          dev::embed_add(H.nb, H.bs, F.x, C.kz, C.s);
+          CK(cudaEventRecord(ev[3], C.s));
+          smooth(C, H, C.kz, C.kr, true);
+          CK(cudaEventRecord(ev[4], C.s));
+          CK(cudaEventSynchronize(ev[4]));
+          float a, b, c, d;
+          cudaEventElapsedTime(&a, ev[0], ev[1]);
+          cudaEventElapsedTime(&b, ev[1], ev[2]);
+          cudaEventElapsedTime(&c, ev[2], ev[3]);
+          cudaEventElapsedTime(&d, ev[3], ev[4]);
+          phase_ms[0] += a / reps;
+          phase_ms[1] += b / reps;
+          phase_ms[2] += c / reps;
+          phase_ms[3] += d / reps;
+        }
+      }
+      for (auto& e : ev) cudaEventDestroy(e);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
+  return ms_per;
+}
+
+int hpmg_kernel_launches_per_apply(const hpmg_ctx* ctx) { return ctx->launches_per_apply; }
+
+double hpmg_setup_seconds(const hpmg_ctx* ctx, double* parts) {
+  if (parts)
+    for (int i = 0; i < 8; ++i) parts[i] = ctx->setup_parts[i];
+  return ctx->setup_parts[6];
+}
+
+void hpmg_seeded_load(int n, unsigned seed, double lo, double hi, double* out) {
+  std::mt19937 rng(seed);
+  std::uniform_real_distribution<double> d(lo, hi);
+  for (size_t i = 0; i < size_t(4) * n * n; ++i) out[i] = d(rng);
+}
+
+int hpmg_structured_to_elements(const hpmg_ctx* ctx, int n, const double* S, double* out) {
+  const host::TriMesh& m = ctx->mesh.back();
+  for (int e = 0; e < m.ne(); ++e) {
+    const auto& v = m.ev[e];
+    const double cx = (m.vx[v[0]] + m.vx[v[1]] + m.vx[v[2]]) / 3.0, cy = (m.vy[v[0]] + m.vy[v[1]] + m.vy[v[2]]) / 3.0;
+    int i = int(std::floor(cx * n)), j = int(std::floor(cy * n));
+    i = std::min(n - 1, std::max(0, i));
+    j = std::min(n - 1, std::max(0, j));
+    const bool lower = (cx - double(i) / n) >= (cy - double(j) / n);
+    const size_t s = (size_t(j) * n + i) * 2 + (lower ? 0 : 1);
+    out[2 * e] = S[2 * s];
+    out[2 * e + 1] = S[2 * s + 1];
+  }
+  return HPMG_OK;
+}
+
+namespace {
+thread_local std::vector<double> t_xy;
+thread_local std::vector<int> t_el, t_tags;
+int fill_desc(const host::TriMesh& m, int levels, hpmg_mesh_desc* out) {
+  t_xy.clear();
+  t_el.clear();
+  t_tags.clear();
+  for (int v = 0; v < m.nv(); ++v) {
+    t_xy.push_back(m.vx[v]);
+    t_xy.push_back(m.vy[v]);
+  }
+  for (int e = 0; e < m.ne(); ++e)
+    for (int q = 0; q < 3; ++q) t_el.push_back(m.ev[e][q]);
+  for (int f = 0; f < m.nf(); ++f)
+    if (m.ftag[f] == host::kTagOutflow) {
+      t_tags.push_back(m.fa[f]);
+      t_tags.push_back(m.fb[f]);
+      t_tags.push_back(host::kTagOutflow);
+    }
+  out->n_vertices = m.nv();
+  out->xy = t_xy.data();
+  out->n_elements = m.ne();
+  out->elements = t_el.data();
+  out->n_tag_overrides = int(t_tags.size() / 3);
+  out->tag_overrides = t_tags.data();
+  out->levels = levels;
+  return HPMG_OK;
+}
+}  // namespace
+
+int hpmg_unit_square_mesh(int n, int levels, hpmg_mesh_desc* out) { return fill_desc(host::unit_square(n), levels, out); }
+int hpmg_step_mesh(int n, int levels, hpmg_mesh_desc* out) { return fill_desc(host::step_domain(n), levels, out); }
+
+}  // extern "C"

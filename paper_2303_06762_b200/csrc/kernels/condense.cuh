@@ -1,0 +1,238 @@
+// Element-local assembly + static condensation (reference
+// inc/assembly.hpp:205-364, build_local_blocks + condense_local), written as a
+// cooperative routine over (tid, nthr) so one CTA condenses one element.
+//
+// Affine elements let every Stokes-type integral factor as
+//   (reference tensor, tabulated once per k)  x  (J, J^-1, orientation),
+// see host/basis.hpp. Per element this kernel only performs small dense
+// contractions; the dominant work is the (nu/detJ) C^T C product and the
+// elimination of nz = k(k+1) + ns-1 interior unknowns, i.e. FP64 FMA-bound.
+//
+// The same source compiles for the host (HPMG_HOST_EMUL) with tid=0, nthr=1
+// and SYNC() a no-op; tests/native uses that build to check the arithmetic
+// against the CPU oracle without a GPU. The product only launches the kernel.
+#pragma once
+
+#ifndef HPMG_HD
+#ifdef __CUDACC__
+#define HPMG_HD __host__ __device__
+#define HPMG_D __device__
+#else
+#define HPMG_D
+#define HPMG_HD
+#endif
+#endif
+
+namespace hpmg {
+
+/// Per-order reference tensors (device pointers or host pointers in emulation).
+struct RefT {
+  int k, nfd, nrt, no, ns, nc, nv;
+  const double* G;   // [4][ns][nrt]
+  const double* Mm;  // [4][nrt][nrt]
+  const double* Dv;  // [ns-1][nrt]
+  const double* Lv;  // [2][nrt]
+  const double* Ev;  // [3][2][ns][nrt]
+  const double* Tv;  // [3][nfd][ns]
+  const double* vval;  // [nq][2][nrt] (pointwise loads)
+  const double* qw;    // [nq]
+  int nq;
+};
+
+/// Per-element geometry, 32 doubles (packed on the host).
+struct ElemGeo {
+  double J[4];      // J00 J01 J10 J11 (columns: v1-v0, v2-v0)
+  double Ji[4];     // inverse
+  double detJ;
+  double fac[3];    // sigma |F| / |ref edge|
+  double rho[3];    // +1 / -1 (local edge direction vs global)
+  double n[6];      // outward unit normal per local edge
+  double tf[6];     // global unit tangent per local facet
+  double ds[3];     // |F| / 2
+};
+
+struct CondenseParams {
+  double nu, mass;        // mass = beta + mass_coef
+  int load_mode;          // 0 none, 1 constant per element, 2 pointwise [nq][2]
+};
+
+/// Scratch layout (doubles): C[4ns*nv] A[nv*nv] P[(ns-1)*nv] rhs[nv] aug[nz*(nz+nc+1)] fac[nrt]
+HPMG_HD inline int condense_scratch(int ns, int nv, int nc, int nz, int nrt) {
+  return 4 * ns * nv + nv * nv + (ns > 1 ? (ns - 1) * nv : 0) + nv + nz * (nz + nc + 1) + nrt + 8;
+}
+
+#ifndef SYNC
+#define SYNC() __syncthreads()
+#endif
+
+/// Computes the condensed element matrix Ac (nc x nc, row-major, reference
+/// local order: 3 nfd flux, 3 nfd tangential) and load vector rc (nc).
+HPMG_D inline void condense_element(int tid, int nthr, const RefT& T, const ElemGeo& g, const CondenseParams& prm,
+                                     const double* load, double* scratch, double* Ac, double* rc) {
+  const int ns = T.ns, nv = T.nv, nc = T.nc, nrt = T.nrt, nfd = T.nfd, no = T.no;
+  const int np = ns - 1, nz = no + np, nC = 4 * ns;
+  double* C = scratch;
+  double* A = C + nC * nv;
+  double* P = A + nv * nv;
+  double* rhs = P + (np > 0 ? np * nv : 0);
+  double* aug = rhs + nv;
+  double* fr = aug + nz * (nz + nc + 1);  // orientation factor per RT column
+  const int naug = nz + nc + 1;
+
+  for (int r = tid; r < nrt; r += nthr) {
+    if (r < 3 * nfd) {
+      int le = r / nfd, i = r % nfd;
+      double f = g.fac[le];
+      fr[r] = ((i & 1) && g.rho[le] < 0) ? -f : f;
+    } else {
+      fr[r] = 1.0;
+    }
+  }
+  SYNC();
+  // ---- gradient coupling C (4ns x nv) and divergence moments P ----
+  for (int e = tid; e < nC * nv; e += nthr) {
+    const int row = e / nv, a = e % nv;
+    const int c = row / ns, m = row % ns, c0 = c >> 1, c1 = c & 1;
+    double s = 0.0;
+    if (a < 3 * nfd || a >= nc) {
+      const int r = a < 3 * nfd ? a : 3 * nfd + (a - nc);
+      // volume: fr * sum_ij J[c0][i] Ji[j][c1] G[2i+j][m][r]
+      double vol = 0.0;
+      for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2; ++j)
+          vol += g.J[c0 * 2 + i] * g.Ji[j * 2 + c1] * T.G[((2 * i + j) * ns + m) * nrt + r];
+      // edges: -ds n_j fr/detJ sum_k Pi[c0][k] sum_l J[k][l] E[le][l][m][r]
+      double edg = 0.0;
+      for (int le = 0; le < 3; ++le) {
+        const double nx = g.n[2 * le], ny = g.n[2 * le + 1];
+        const double e0 = T.Ev[((le * 2 + 0) * ns + m) * nrt + r], e1 = T.Ev[((le * 2 + 1) * ns + m) * nrt + r];
+        const double t0 = g.J[0] * e0 + g.J[1] * e1, t1 = g.J[2] * e0 + g.J[3] * e1;  // J ehat
+        const double tn = t0 * nx + t1 * ny;
+        const double d = (c0 == 0 ? t0 - tn * nx : t1 - tn * ny);
+        edg += g.ds[le] * (c1 == 0 ? nx : ny) * d;
+      }
+      s = fr[r] * vol - fr[r] / g.detJ * edg;
+    } else {
+      // tangential column (le, p): + ds sgn tf[c0] n[c1] Tv[le][p][m]
+      const int le = (a - 3 * nfd) / nfd, p = (a - 3 * nfd) % nfd;
+      const double sg = ((p & 1) && g.rho[le] < 0) ? -1.0 : 1.0;
+      s = g.ds[le] * sg * g.tf[2 * le + c0] * g.n[2 * le + c1] * T.Tv[(le * nfd + p) * ns + m];
+    }
+    C[row * nv + a] = s;
+  }
+  for (int e = tid; e < np * nv; e += nthr) {
+    const int m = e / nv, a = e % nv;
+    double s = 0.0;
+    if (a < 3 * nfd || a >= nc) {
+      const int r = a < 3 * nfd ? a : 3 * nfd + (a - nc);
+      s = fr[r] * T.Dv[m * nrt + r];
+    }
+    P[m * nv + a] = s;
+  }
+  for (int a = tid; a < nv; a += nthr) {
+    double s = 0.0;
+    if (prm.load_mode != 0 && (a < 3 * nfd || a >= nc)) {
+      const int r = a < 3 * nfd ? a : 3 * nfd + (a - nc);
+      if (prm.load_mode == 1) {
+        const double jf0 = load[0] * g.J[0] + load[1] * g.J[2], jf1 = load[0] * g.J[1] + load[1] * g.J[3];
+        s = fr[r] * (jf0 * T.Lv[r] + jf1 * T.Lv[nrt + r]);
+      } else {
+        for (int q = 0; q < T.nq; ++q) {
+          const double fx = load[2 * q], fy = load[2 * q + 1];
+          const double jf0 = fx * g.J[0] + fy * g.J[2], jf1 = fx * g.J[1] + fy * g.J[3];
+          s += T.qw[q] * (jf0 * T.vval[(q * 2) * nrt + r] + jf1 * T.vval[(q * 2 + 1) * nrt + r]);
+        }
+        s *= fr[r];
+      }
+    }
+    rhs[a] = s;
+  }
+  SYNC();
+  // ---- A = mass part + (nu/detJ) C^T C ----
+  const double JtJ[4] = {g.J[0] * g.J[0] + g.J[2] * g.J[2], g.J[0] * g.J[1] + g.J[2] * g.J[3],
+                         g.J[1] * g.J[0] + g.J[3] * g.J[2], g.J[1] * g.J[1] + g.J[3] * g.J[3]};
+  const double visc = prm.nu / g.detJ;
+  for (int e = tid; e < nv * nv; e += nthr) {
+    const int a = e / nv, b = e % nv;
+    double m = 0.0;
+    const bool ra = a < 3 * nfd || a >= nc, rb = b < 3 * nfd || b >= nc;
+    if (prm.mass != 0.0 && ra && rb) {
+      const int r = a < 3 * nfd ? a : 3 * nfd + (a - nc), s = b < 3 * nfd ? b : 3 * nfd + (b - nc);
+      double acc = 0.0;
+      for (int ij = 0; ij < 4; ++ij) acc += JtJ[ij] * T.Mm[(ij * nrt + r) * nrt + s];
+      m = prm.mass * fr[r] * fr[s] / g.detJ * acc;
+    }
+    double cc = 0.0;
+    for (int row = 0; row < nC; ++row) cc += C[row * nv + a] * C[row * nv + b];
+    A[e] = m + visc * cc;
+  }
+  SYNC();
+  if (nz == 0) {
+    for (int e = tid; e < nc * nc; e += nthr) Ac[e] = A[(e / nc) * nv + (e % nc)];
+    for (int a = tid; a < nc; a += nthr) rc[a] = rhs[a];
+    return;
+  }
+  // ---- eliminate z = (interior velocity, zero-mean pressure) ----
+  // aug = [Mzz | Mzc | rz], Mzz = [[A_oo, -P_o^T], [-P_o, 0]], Mzc = [A_oc; -P_c]
+  for (int e = tid; e < nz * naug; e += nthr) {
+    const int i = e / naug, j = e % naug;
+    double v = 0.0;
+    if (j < nz) {
+      if (i < no && j < no) v = A[(nc + i) * nv + nc + j];
+      else if (i < no) v = -P[(j - no) * nv + nc + i];
+      else if (j < no) v = -P[(i - no) * nv + nc + j];
+    } else if (j < nz + nc) {
+      const int cidx = j - nz;
+      v = i < no ? A[(nc + i) * nv + cidx] : -P[(i - no) * nv + cidx];
+    } else {
+      v = i < no ? rhs[nc + i] : 0.0;
+    }
+    aug[e] = v;
+  }
+  SYNC();
+  // Gaussian elimination with partial pivoting (pivot search by every thread
+  // redundantly: nz <= 21, so the search is cheaper than a reduction)
+  for (int kk = 0; kk < nz; ++kk) {
+    int piv = kk;
+    double best = aug[kk * naug + kk] < 0 ? -aug[kk * naug + kk] : aug[kk * naug + kk];
+    for (int i = kk + 1; i < nz; ++i) {
+      double v = aug[i * naug + kk];
+      v = v < 0 ? -v : v;
+      if (v > best) { best = v; piv = i; }
+    }
+    SYNC();
+    if (piv != kk)
+      for (int j = tid; j < naug; j += nthr) {
+        double t = aug[kk * naug + j];
+        aug[kk * naug + j] = aug[piv * naug + j];
+        aug[piv * naug + j] = t;
+      }
+    SYNC();
+    const double inv = 1.0 / aug[kk * naug + kk];
+    for (int e = tid; e < (nz - kk - 1) * (naug - kk - 1); e += nthr) {
+      const int i = kk + 1 + e / (naug - kk - 1), j = kk + 1 + e % (naug - kk - 1);
+      aug[i * naug + j] -= aug[i * naug + kk] * inv * aug[kk * naug + j];
+    }
+    SYNC();
+  }
+  // back substitution on the nc + 1 right-hand sides (column-parallel)
+  for (int j = nz + tid; j < naug; j += nthr) {
+    for (int i = nz - 1; i >= 0; --i) {
+      double s = aug[i * naug + j];
+      for (int l = i + 1; l < nz; ++l) s -= aug[i * naug + l] * aug[l * naug + j];
+      aug[i * naug + j] = s / aug[i * naug + i];
+    }
+  }
+  SYNC();
+  // Ac = A_cc - Mcz X, rc = r_c - Mcz y with Mcz = [A_co, -P_c^T]
+  for (int e = tid; e < nc * (nc + 1); e += nthr) {
+    const int a = e / (nc + 1), j = e % (nc + 1);
+    double s = 0.0;
+    for (int i = 0; i < no; ++i) s += A[a * nv + nc + i] * aug[i * naug + nz + j];
+    for (int m = 0; m < np; ++m) s -= P[m * nv + a] * aug[(no + m) * naug + nz + j];
+    if (j < nc) Ac[a * nc + j] = A[a * nv + j] - s;
+    else rc[a] = rhs[a] - s;
+  }
+}
+
+}  // namespace hpmg

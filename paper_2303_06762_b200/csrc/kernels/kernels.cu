@@ -1,0 +1,785 @@
+// sm_100a FP64 kernels of the hp-MG solve path. Everything here is
+// HBM-bandwidth bound (~0.25 flop/byte) except the element condensation,
+// which is FP64-FMA bound; see DESIGN.md for the per-kernel roofline.
+//
+// Determinism: every reduction uses a fixed grid (kRedBlocks) with a fixed
+// thread-to-index map, per-block tree sums and a final fixed-order sum by the
+// last block to finish (ticket counter), so repeated runs are bit-identical
+// (reference tests/test_multigrid.cpp:109-119 asks for that).
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "kernels.hpp"
+
+namespace hpmg {
+namespace dev {
+
+#define HPMG_LAUNCH_CHECK()                                                                        \
+  do {                                                                                             \
+    cudaError_t err__ = cudaGetLastError();                                                        \
+    if (err__ != cudaSuccess) throw std::runtime_error(std::string("CUDA launch: ") + cudaGetErrorString(err__)); \
+  } while (0)
+
+namespace {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+/// Block tree sum (or max); result valid in thread 0. All threads must call.
+template <bool kMax>
+__device__ double block_reduce(double v) {
+  __shared__ double sh[32];
+  v = kMax ? warp_max(v) : warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = lane < nw ? sh[lane] : (kMax ? -1.0 : 0.0);
+    v = kMax ? warp_max(v) : warp_sum(v);
+  }
+  return v;
+}
+
+/// Writes the block partial, the last block sums all partials in fixed order.
+template <bool kMax>
+__device__ void finalize(double v, Reduce red, double* out) {
+  __shared__ bool last;
+  v = block_reduce<kMax>(v);
+  if (threadIdx.x == 0) {
+    red.partial[blockIdx.x] = v;
+    __threadfence();
+    unsigned t = atomicAdd(red.counter, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    double s = kMax ? -1.0 : 0.0;
+    for (int i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
+      double p = __ldcg(&red.partial[i]);
+      s = kMax ? fmax(s, p) : s + p;
+    }
+    s = block_reduce<kMax>(s);
+    if (threadIdx.x == 0) {
+      *out = s;
+      *red.counter = 0u;
+    }
+  }
+}
+
+inline int grid_for(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > 148 * 64) g = 148 * 64;
+  return int(g);
+}
+
+// ---------------------------------------------------------------- condense
+__global__ void k_condense(RefT T, const ElemGeo* __restrict__ geo, CondenseParams prm, const double* __restrict__ load,
+                           int load_stride, double* __restrict__ out, int stride) {
+  extern __shared__ double smem[];
+  __shared__ ElemGeo g;
+  const int e = blockIdx.x;
+  if (threadIdx.x < int(sizeof(ElemGeo) / sizeof(double)))
+    reinterpret_cast<double*>(&g)[threadIdx.x] = reinterpret_cast<const double*>(geo + e)[threadIdx.x];
+  __syncthreads();
+  double* o = out + size_t(e) * stride;
+  const double* ld = prm.load_mode ? load + size_t(e) * load_stride : nullptr;
+  condense_element(threadIdx.x, blockDim.x, T, g, prm, ld, smem, o, o + T.nc * T.nc);
+}
+
+__device__ __forceinline__ int local_dof(int lf, int ii, int nfd) {
+  // block entry ii = 2 i + t  ->  reference local index (flux: lf*nfd+i, tang: 3nfd + lf*nfd + i)
+  const int i = ii >> 1, t = ii & 1;
+  return t == 0 ? lf * nfd + i : 3 * nfd + lf * nfd + i;
+}
+
+__global__ void k_assemble_bsr(Bsr A, int nfd, const double* __restrict__ acr, int stride, int nc,
+                               const int* __restrict__ gath, const ElemGeo* __restrict__ geo, double inv_eps) {
+  const int bs = A.bs, bb = bs * bs;
+  const int64_t n = int64_t(A.nb) * kSlots * bb;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t rs = t / bb;
+    const int ii = int(t % bb) / bs, jj = int(t % bb) % bs;
+    if (A.cols[rs] < 0) {
+      A.val[t] = 0.0;
+      continue;
+    }
+    const int* gp = gath + rs * 6;
+    double v = 0.0, d = 0.0;
+    bool has_d = false;
+    for (int c = 0; c < 2; ++c) {
+      const int e = gp[3 * c];
+      if (e < 0) continue;
+      const int la = gp[3 * c + 1], lb = gp[3 * c + 2];
+      v += acr[size_t(e) * stride + local_dof(la, ii, nfd) * nc + local_dof(lb, jj, nfd)];
+      if (ii == 0 && jj == 0) {
+        const ElemGeo& g = geo[e];
+        const double ia = 1.0 / (0.5 * g.detJ);
+        const double bi = (g.fac[la] < 0 ? -2.0 : 2.0) * g.ds[la], bj = (g.fac[lb] < 0 ? -2.0 : 2.0) * g.ds[lb];
+        d += ia * bi * bj;
+        has_d = true;
+      }
+    }
+    A.val[t] = has_d ? v + inv_eps * d : v;
+  }
+}
+
+__global__ void k_transpose_bsr(Bsr A, const int* __restrict__ tslot, Bsr AT) {
+  const int bs = A.bs, bb = bs * bs;
+  const int64_t n = int64_t(A.nb) * kSlots * bb;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t rs = t / bb;
+    const int ii = int(t % bb) / bs, jj = int(t % bb) % bs;
+    const int c = A.cols[rs];
+    if (c < 0) {
+      AT.val[t] = 0.0;
+      continue;
+    }
+    const int s2 = tslot[rs];
+    AT.val[t] = A.val[(int64_t(c) * kSlots + s2) * bb + jj * bs + ii];
+  }
+}
+
+__global__ void k_assemble_rhs(int nb, int bs, int nfd, const int* __restrict__ row_elems,
+                               const int* __restrict__ block_facet, const int* __restrict__ elem_facets,
+                               const char* __restrict__ dir, const double* __restrict__ g_fac,
+                               const double* __restrict__ acr, int stride, int nc, const ElemGeo* __restrict__ geo,
+                               double inv_eps, double* __restrict__ rhs) {
+  const int64_t n = int64_t(nb) * bs;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int f = int(t / bs), ii = int(t % bs);
+    double acc = 0.0, dr = 0.0;
+    for (int c = 0; c < 2; ++c) {
+      const int e = row_elems[f * 4 + 2 * c];
+      if (e < 0) continue;
+      const int la = row_elems[f * 4 + 2 * c + 1];
+      const int a = local_dof(la, ii, nfd);
+      const double* Ae = acr + size_t(e) * stride;
+      acc += Ae[nc * nc + a];
+      for (int b = 0; b < nc; ++b) {
+        const int lb = b < 3 * nfd ? b / nfd : (b - 3 * nfd) / nfd;
+        const int gf = elem_facets[e * 3 + lb];
+        if (!dir[gf]) continue;
+        const int mode = b < 3 * nfd ? b % nfd : (b - 3 * nfd) % nfd;
+        const int slot = 2 * mode + (b < 3 * nfd ? 0 : 1);
+        acc -= Ae[a * nc + b] * g_fac[size_t(gf) * bs + slot];
+      }
+      if (ii == 0) {
+        const ElemGeo& g = geo[e];
+        const double ia = 1.0 / (0.5 * g.detJ);
+        const double bi = (g.fac[la] < 0 ? -2.0 : 2.0) * g.ds[la];
+        for (int j = 0; j < 3; ++j) {
+          const int gj = elem_facets[e * 3 + j];
+          if (!dir[gj]) continue;
+          const double bj = (g.fac[j] < 0 ? -2.0 : 2.0) * g.ds[j];
+          dr -= ia * bi * bj * g_fac[size_t(gj) * bs];
+        }
+      }
+    }
+    rhs[t] = ii == 0 ? acc + inv_eps * dr : acc;
+  }
+  (void)block_facet;
+}
+
+// --------------------------------------------------------------- operator
+template <int BS>
+__global__ void k_spmv(Bsr A, const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ y,
+                       int minus, int with_dot, Reduce red, double* dot_out) {
+  const int64_t n = int64_t(A.nb) * BS;
+  double dacc = 0.0;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int f = int(t / BS), i = int(t % BS);
+    double s = 0.0;
+#pragma unroll
+    for (int sl = 0; sl < kSlots; ++sl) {
+      const int c = __ldg(&A.cols[f * kSlots + sl]);
+      if (c < 0) continue;
+      const double2* blk = reinterpret_cast<const double2*>(A.val + (size_t(f * kSlots + sl) * BS + i) * BS);
+      const double2* xc = reinterpret_cast<const double2*>(x + size_t(c) * BS);
+#pragma unroll
+      for (int j = 0; j < BS / 2; ++j) {
+        const double2 a = __ldg(blk + j), xv = xc[j];
+        s = fma(a.x, xv.x, s);
+        s = fma(a.y, xv.y, s);
+      }
+    }
+    const double v = minus ? b[t] - s : s;
+    y[t] = v;
+    if (with_dot) dacc = fma(x[t], v, dacc);
+  }
+  if (with_dot) finalize<false>(dacc, red, dot_out);
+}
+
+template <int BS>
+__global__ void k_inject_residual(Bsr A, const double* __restrict__ x, const double* __restrict__ b,
+                                  double* __restrict__ r0) {
+  const int64_t n = int64_t(A.nb) * 2;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int f = int(t >> 1), i = int(t & 1);
+    double s = 0.0;
+#pragma unroll
+    for (int sl = 0; sl < kSlots; ++sl) {
+      const int c = __ldg(&A.cols[f * kSlots + sl]);
+      if (c < 0) continue;
+      const double2* blk = reinterpret_cast<const double2*>(A.val + (size_t(f * kSlots + sl) * BS + i) * BS);
+      const double2* xc = reinterpret_cast<const double2*>(x + size_t(c) * BS);
+#pragma unroll
+      for (int j = 0; j < BS / 2; ++j) {
+        const double2 a = __ldg(blk + j), xv = xc[j];
+        s = fma(a.x, xv.x, s);
+        s = fma(a.y, xv.y, s);
+      }
+    }
+    r0[t] = b[size_t(f) * BS + i] - s;
+  }
+}
+
+__global__ void k_embed_add(int nb, int bs, const double* __restrict__ e, double* __restrict__ x) {
+  const int64_t n = int64_t(nb) * 2;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x)
+    x[(t >> 1) * bs + (t & 1)] += e[t];
+}
+
+// ------------------------------------------------------------ smoothers
+/// Patch matrix gather + Gauss-Jordan inversion with partial pivoting,
+/// one CTA per patch; the inverse is stored column-major.
+template <int BS>
+__global__ void k_patch_inverse(Bsr A, Patches P) {
+  extern __shared__ double aug[];
+  __shared__ int fac[kMaxPatchF];
+  __shared__ int piv_row;
+  const int p = blockIdx.x;
+  const int nf = P.nf[p], np = nf * BS, w = 2 * np;
+  if (threadIdx.x < kMaxPatchF) fac[threadIdx.x] = P.fac[p * kMaxPatchF + threadIdx.x];
+  __syncthreads();
+  for (int e = threadIdx.x; e < np * w; e += blockDim.x) {
+    const int r = e / w, c = e % w;
+    double v = 0.0;
+    if (c < np) {
+      const int fr = fac[r / BS], fcn = fac[c / BS];
+      for (int sl = 0; sl < kSlots; ++sl)
+        if (A.cols[fr * kSlots + sl] == fcn) {
+          v = A.val[(size_t(fr * kSlots + sl) * BS + r % BS) * BS + c % BS];
+          break;
+        }
+    } else {
+      v = (c - np == r) ? 1.0 : 0.0;
+    }
+    aug[e] = v;
+  }
+  __syncthreads();
+  for (int k = 0; k < np; ++k) {
+    if (threadIdx.x < 32) {
+      double best = -1.0;
+      int bi = k;
+      for (int i = k + threadIdx.x; i < np; i += 32) {
+        double v = fabs(aug[i * w + k]);
+        if (v > best) { best = v; bi = i; }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (threadIdx.x == 0) piv_row = bi;
+    }
+    __syncthreads();
+    const int pr = piv_row;
+    if (pr != k)
+      for (int c = threadIdx.x; c < w; c += blockDim.x) {
+        double t = aug[k * w + c];
+        aug[k * w + c] = aug[pr * w + c];
+        aug[pr * w + c] = t;
+      }
+    __syncthreads();
+    const double inv = 1.0 / aug[k * w + k];
+    __syncthreads();
+    for (int c = threadIdx.x; c < w; c += blockDim.x) aug[k * w + c] *= inv;
+    __syncthreads();
+    for (int e = threadIdx.x; e < np * w; e += blockDim.x) {
+      const int r = e / w, c = e % w;
+      if (r == k || c == k) continue;
+      aug[e] -= aug[r * w + k] * aug[k * w + c];
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < np; r += blockDim.x)
+      if (r != k) aug[r * w + k] = 0.0;
+    __syncthreads();
+  }
+  double* out = P.inv + P.off[p];
+  for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
+    const int c = e / np, r = e % np;  // column-major: (r, c) at c*np + r
+    out[e] = aug[r * w + np + c];
+  }
+}
+
+/// One multiplicative wave (pull form): every patch of the
+/// wave recomputes its residual from A rows and the current x, solves with
+/// its explicit inverse and updates its own DOFs; same-wave patches are
+/// disjoint and uncoupled, so no atomics are needed.
+template <int BS>
+__global__ void k_gs_wave(Bsr A, Patches P, int w0, const double* __restrict__ b, double* __restrict__ x,
+                          int transposed) {
+  __shared__ double r[kMaxPatchF * BS];
+  __shared__ int fac[kMaxPatchF];
+  const int p = P.wave[w0 + blockIdx.x];
+  const int nf = P.nf[p], np = nf * BS;
+  if (threadIdx.x < kMaxPatchF) fac[threadIdx.x] = P.fac[p * kMaxPatchF + threadIdx.x];
+  __syncthreads();
+  for (int t = threadIdx.x; t < np; t += blockDim.x) {
+    const int f = fac[t / BS], i = t % BS;
+    double s = b[size_t(f) * BS + i];
+#pragma unroll
+    for (int sl = 0; sl < kSlots; ++sl) {
+      const int c = __ldg(&A.cols[f * kSlots + sl]);
+      if (c < 0) continue;
+      const double2* blk = reinterpret_cast<const double2*>(A.val + (size_t(f * kSlots + sl) * BS + i) * BS);
+      const double2* xc = reinterpret_cast<const double2*>(x + size_t(c) * BS);
+#pragma unroll
+      for (int j = 0; j < BS / 2; ++j) {
+        const double2 a = __ldg(blk + j), xv = xc[j];
+        s = fma(-a.x, xv.x, s);
+        s = fma(-a.y, xv.y, s);
+      }
+    }
+    r[t] = s;
+  }
+  __syncthreads();
+  const double* inv = P.inv + P.off[p];
+  for (int t = threadIdx.x; t < np; t += blockDim.x) {
+    double d = 0.0;
+    if (!transposed) {
+      for (int j = 0; j < np; ++j) d = fma(__ldg(inv + size_t(j) * np + t), r[j], d);
+    } else {
+      const double* row = inv + size_t(t) * np;
+      for (int j = 0; j < np; ++j) d = fma(__ldg(row + j), r[j], d);
+    }
+    x[size_t(fac[t / BS]) * BS + t % BS] += d;
+  }
+}
+
+template <int BS>
+__global__ void k_jacobi_patch(Patches P, int max_np, const double* __restrict__ rvec, double* __restrict__ dbuf) {
+  __shared__ double r[kMaxPatchF * BS];
+  __shared__ int fac[kMaxPatchF];
+  const int p = blockIdx.x;
+  const int nf = P.nf[p], np = nf * BS;
+  if (threadIdx.x < kMaxPatchF) fac[threadIdx.x] = P.fac[p * kMaxPatchF + threadIdx.x];
+  __syncthreads();
+  for (int t = threadIdx.x; t < np; t += blockDim.x) r[t] = rvec[size_t(fac[t / BS]) * BS + t % BS];
+  __syncthreads();
+  const double* inv = P.inv + P.off[p];
+  for (int t = threadIdx.x; t < np; t += blockDim.x) {
+    double d = 0.0;
+    for (int j = 0; j < np; ++j) d = fma(__ldg(inv + size_t(j) * np + t), r[j], d);
+    dbuf[size_t(p) * max_np + t] = d;
+  }
+}
+
+__global__ void k_jacobi_combine(int nb, int bs, Patches P, int max_np, const double* __restrict__ dbuf,
+                                 double damping, double* __restrict__ x) {
+  const int64_t n = int64_t(nb) * bs;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int f = int(t / bs), i = int(t % bs);
+    double v = x[t];
+    for (int q = 0; q < 2; ++q) {
+      const int p = P.fpatch[f * 2 + q];
+      if (p < 0) continue;
+      int pos = 0;
+      for (int s = 0; s < kMaxPatchF; ++s)
+        if (P.fac[p * kMaxPatchF + s] == f) { pos = s; break; }
+      v += damping * dbuf[size_t(p) * max_np + pos * bs + i];
+    }
+    x[t] = v;
+  }
+}
+
+// ------------------------------------------------------------- transfers
+__global__ void k_prolong_add(BlockCsr P, const double* __restrict__ e, double* __restrict__ x) {
+  const int64_t n = int64_t(P.nrows) * 2;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int f = int(t >> 1), c = int(t & 1);
+    double s = 0.0;
+    for (int q = P.ptr[f]; q < P.ptr[f + 1]; ++q) {
+      const int cb = P.col[q];
+      const double* v = P.val + size_t(q) * 4 + c * 2;
+      s = fma(v[0], e[size_t(cb) * 2], s);
+      s = fma(v[1], e[size_t(cb) * 2 + 1], s);
+    }
+    x[t] += s;
+  }
+}
+
+__global__ void k_restrict(BlockCsr PT, const double* __restrict__ r, double* __restrict__ rc) {
+  const int64_t n = int64_t(PT.nrows) * 2;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int f = int(t >> 1), c = int(t & 1);
+    double s = 0.0;
+    for (int q = PT.ptr[f]; q < PT.ptr[f + 1]; ++q) {
+      const int fb = PT.col[q];
+      const double* v = PT.val + size_t(q) * 4 + c * 2;
+      s = fma(v[0], r[size_t(fb) * 2], s);
+      s = fma(v[1], r[size_t(fb) * 2 + 1], s);
+    }
+    rc[t] = s;
+  }
+}
+
+/// x = Inv b for the dense coarse inverse (column-major), 2-stage over
+/// column chunks for parallelism: work[chunk][n] partials then a fixed-order sum.
+constexpr int kGemvChunk = 128;
+__global__ void k_gemv_partial(int n, const double* __restrict__ inv, const double* __restrict__ b,
+                               double* __restrict__ work) {
+  const int chunk = blockIdx.y;
+  const int j0 = chunk * kGemvChunk, j1 = min(n, j0 + kGemvChunk);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int j = j0; j < j1; ++j) s = fma(__ldg(inv + size_t(j) * n + i), __ldg(b + j), s);
+    work[size_t(chunk) * n + i] = s;
+  }
+}
+__global__ void k_gemv_sum(int n, int chunks, const double* __restrict__ work, double* __restrict__ x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < chunks; ++c) s += work[size_t(c) * n + i];
+    x[i] = s;
+  }
+}
+
+// --------------------------------------------------------------- vectors
+__global__ void k_fill(double* x, double v, int64_t n) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) x[t] = v;
+}
+__global__ void k_copy(double* __restrict__ y, const double* __restrict__ x, int64_t n) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) y[t] = x[t];
+}
+__global__ void k_axpy(double* __restrict__ y, double a, const double* __restrict__ x, int64_t n) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x)
+    y[t] += a * x[t];
+}
+__global__ void k_sub(double* __restrict__ y, const double* __restrict__ a, const double* __restrict__ b, int64_t n) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x)
+    y[t] = a[t] - b[t];
+}
+__global__ void k_dot(const double* __restrict__ a, const double* __restrict__ b, int64_t n, Reduce red, double* out) {
+  double s = 0.0;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x)
+    s = fma(a[t], b[t], s);
+  finalize<false>(s, red, out);
+}
+__global__ void k_pcg_update(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                             const double* __restrict__ Ap, int64_t n, double* sc, int i_num, int i_den, Reduce red,
+                             int i_rr) {
+  // pAp <= 0: the reference returns before touching x and r (krylov.hpp:49-53);
+  // the predicate is grid-uniform, so every block leaves and no reduction runs
+  if (!(sc[i_den] > 0.0)) return;
+  const double alpha = sc[i_num] / sc[i_den];
+  double s = 0.0;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    x[t] += alpha * p[t];
+    const double rv = r[t] - alpha * Ap[t];
+    r[t] = rv;
+    s = fma(rv, rv, s);
+  }
+  finalize<false>(s, red, sc + i_rr);
+}
+__global__ void k_pcg_direction(double* __restrict__ p, const double* __restrict__ z, int64_t n, const double* sc,
+                                int i_new, int i_old) {
+  const double beta = sc[i_new] / sc[i_old];
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x)
+    p[t] = z[t] + beta * p[t];
+}
+__global__ void k_scal_axpby(double* __restrict__ y, const double* __restrict__ x, int64_t n, const double* sc, int ia,
+                             double fa, double fb) {
+  const double a = (ia >= 0 ? sc[ia] : 1.0) * fa;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x)
+    y[t] = a * x[t] + fb * y[t];
+}
+
+__global__ void k_to_blocks(int nb, int nfd, const double* __restrict__ ref, double* __restrict__ blk) {
+  const int bs = 2 * nfd;
+  const int64_t n = int64_t(nb) * bs;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t f = t / bs;
+    const int ii = int(t % bs), i = ii >> 1, tg = ii & 1;
+    blk[t] = ref[(tg ? int64_t(nb) * nfd : 0) + f * nfd + i];
+  }
+}
+__global__ void k_to_reference(int nb, int nfd, const double* __restrict__ blk, double* __restrict__ ref) {
+  const int bs = 2 * nfd;
+  const int64_t n = int64_t(nb) * bs;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t f = t / bs;
+    const int ii = int(t % bs), i = ii >> 1, tg = ii & 1;
+    ref[(tg ? int64_t(nb) * nfd : 0) + f * nfd + i] = blk[t];
+  }
+}
+
+// ------------------------------------------------------------------ uzawa
+__global__ void k_uzawa_rhs(int nb, int bs, const double* __restrict__ rhs0, const int* __restrict__ row_elems,
+                            const ElemGeo* __restrict__ geo, const double* __restrict__ p, double* __restrict__ rhs) {
+  const int64_t n = int64_t(nb) * bs;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int f = int(t / bs), ii = int(t % bs);
+    double add = 0.0;
+    if (ii == 0)
+      for (int c = 0; c < 2; ++c) {
+        const int e = row_elems[f * 4 + 2 * c];
+        if (e < 0) continue;
+        const int la = row_elems[f * 4 + 2 * c + 1];
+        const ElemGeo& g = geo[e];
+        add += (g.fac[la] < 0 ? -2.0 : 2.0) * g.ds[la] * p[e];
+      }
+    rhs[t] = rhs0[t] + add;
+  }
+}
+
+__global__ void k_uzawa_div(int ne, int bs, const int* __restrict__ elem_facets, const int* __restrict__ facet_block,
+                            const double* __restrict__ g_fac, const double* __restrict__ u,
+                            const ElemGeo* __restrict__ geo, double* __restrict__ div) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x) {
+    const ElemGeo& g = geo[e];
+    int fs[3] = {elem_facets[e * 3], elem_facets[e * 3 + 1], elem_facets[e * 3 + 2]};
+    int ord[3] = {0, 1, 2};  // ascending facet id (column order of Bdiv)
+    if (fs[ord[0]] > fs[ord[1]]) { int t = ord[0]; ord[0] = ord[1]; ord[1] = t; }
+    if (fs[ord[1]] > fs[ord[2]]) { int t = ord[1]; ord[1] = ord[2]; ord[2] = t; }
+    if (fs[ord[0]] > fs[ord[1]]) { int t = ord[0]; ord[0] = ord[1]; ord[1] = t; }
+    double s = 0.0;
+    for (int q = 0; q < 3; ++q) {
+      const int le = ord[q], f = fs[le], blk = facet_block[f];
+      const double val = blk >= 0 ? u[size_t(blk) * bs] : g_fac[size_t(f) * bs];
+      s += (g.fac[le] < 0 ? -2.0 : 2.0) * g.ds[le] * val;
+    }
+    div[e] = s / (0.5 * g.detJ);
+  }
+}
+
+__global__ void k_uzawa_p1(int ne, const double* __restrict__ div, const ElemGeo* __restrict__ geo, double inv_eps,
+                           double* __restrict__ p, Reduce red, double* out) {
+  double s = 0.0;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x) {
+    const double pv = p[e] - inv_eps * div[e];
+    p[e] = pv;
+    s = fma(0.5 * geo[e].detJ, pv, s);
+  }
+  finalize<false>(s, red, out);
+}
+__global__ void k_area_sum(int ne, const ElemGeo* __restrict__ geo, Reduce red, double* out) {
+  double s = 0.0;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x) s += 0.5 * geo[e].detJ;
+  finalize<false>(s, red, out);
+}
+__global__ void k_uzawa_p2(int ne, double* __restrict__ p, const double* sc, int i_s, int i_a) {
+  const double m = sc[i_s] / sc[i_a];
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x) p[e] -= m;
+}
+__global__ void k_absmax(int ne, const double* __restrict__ v, Reduce red, double* out) {
+  double s = 0.0;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x) s = fmax(s, fabs(v[e]));
+  finalize<true>(s, red, out);
+}
+
+template <typename F>
+void by_bs(int bs, F&& f) {
+  switch (bs) {
+    case 2: f(std::integral_constant<int, 2>()); break;
+    case 4: f(std::integral_constant<int, 4>()); break;
+    case 6: f(std::integral_constant<int, 6>()); break;
+    case 8: f(std::integral_constant<int, 8>()); break;
+    default: throw std::runtime_error("unsupported block size");
+  }
+}
+
+}  // namespace
+
+// ============================================================ launchers
+void condense(const RefT& T, const ElemGeo* geo, int ne, CondenseParams prm, const double* load, int load_stride,
+              double* out, cudaStream_t s) {
+  if (ne == 0) return;
+  const int nz = T.no + T.ns - 1;
+  const size_t smem = sizeof(double) * condense_scratch(T.ns, T.nv, T.nc, nz, T.nrt);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_condense, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_condense<<<ne, 128, smem, s>>>(T, geo, prm, load, load_stride, out, T.nc * T.nc + T.nc);
+  HPMG_LAUNCH_CHECK();
+}
+
+void assemble_bsr(const Bsr& A, int nfd, const double* acr, int stride, int nc, const int* gath, const ElemGeo* geo,
+                  double inv_eps, cudaStream_t s) {
+  const int64_t n = int64_t(A.nb) * kSlots * A.bs * A.bs;
+  k_assemble_bsr<<<grid_for(n, 256), 256, 0, s>>>(A, nfd, acr, stride, nc, gath, geo, inv_eps);
+  HPMG_LAUNCH_CHECK();
+}
+
+void transpose_bsr(const Bsr& A, const int* tslot, Bsr& AT, cudaStream_t s) {
+  const int64_t n = int64_t(A.nb) * kSlots * A.bs * A.bs;
+  k_transpose_bsr<<<grid_for(n, 256), 256, 0, s>>>(A, tslot, AT);
+  HPMG_LAUNCH_CHECK();
+}
+
+void assemble_rhs(int nb, int bs, int nfd, const int* row_elems, const int* block_facet, const int* elem_facets,
+                  const char* facet_dirichlet, const double* g_fac, const double* acr, int stride, int nc,
+                  const ElemGeo* geo, double inv_eps, double* rhs, cudaStream_t s) {
+  k_assemble_rhs<<<grid_for(int64_t(nb) * bs, 256), 256, 0, s>>>(nb, bs, nfd, row_elems, block_facet, elem_facets,
+                                                                 facet_dirichlet, g_fac, acr, stride, nc, geo, inv_eps,
+                                                                 rhs);
+  HPMG_LAUNCH_CHECK();
+}
+
+void spmv(const Bsr& A, const double* x, const double* b, double* y, int minus, const Reduce* red, double* dot_out,
+          cudaStream_t s) {
+  const int64_t n = int64_t(A.nb) * A.bs;
+  by_bs(A.bs, [&](auto BS) {
+    if (red) {
+      k_spmv<BS><<<kRedBlocks, 256, 0, s>>>(A, x, b, y, minus, 1, *red, dot_out);
+    } else {
+      k_spmv<BS><<<grid_for(n, 256), 256, 0, s>>>(A, x, b, y, minus, 0, Reduce{}, nullptr);
+    }
+  });
+  HPMG_LAUNCH_CHECK();
+}
+
+void inject_residual(const Bsr& A, const double* x, const double* b, double* r0, cudaStream_t s) {
+  by_bs(A.bs, [&](auto BS) { k_inject_residual<BS><<<grid_for(int64_t(A.nb) * 2, 256), 256, 0, s>>>(A, x, b, r0); });
+  HPMG_LAUNCH_CHECK();
+}
+
+void embed_add(int nb, int bs, const double* e, double* x, cudaStream_t s) {
+  k_embed_add<<<grid_for(int64_t(nb) * 2, 256), 256, 0, s>>>(nb, bs, e, x);
+  HPMG_LAUNCH_CHECK();
+}
+
+void patch_inverse(const Bsr& A, const Patches& P, int max_nf, cudaStream_t s) {
+  if (P.n == 0) return;
+  by_bs(A.bs, [&](auto BS) {
+    const int np = max_nf * BS;
+    const size_t smem = sizeof(double) * size_t(np) * 2 * np;
+    cudaFuncSetAttribute(k_patch_inverse<BS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    k_patch_inverse<BS><<<P.n, 128, smem, s>>>(A, P);
+  });
+  HPMG_LAUNCH_CHECK();
+}
+
+void gs_wave(const Bsr& A, const Patches& P, int w0, int w1, const double* b, double* x, int transposed_inv,
+             int max_nf, cudaStream_t s) {
+  if (w1 <= w0) return;
+  by_bs(A.bs, [&](auto BS) {
+    const int np = max_nf * BS;
+    const int threads = ((np + 31) / 32) * 32;
+    k_gs_wave<BS><<<w1 - w0, threads, 0, s>>>(A, P, w0, b, x, transposed_inv);
+  });
+  HPMG_LAUNCH_CHECK();
+}
+
+void jacobi_patch(const Bsr& A, const Patches& P, const double* r, double* d, int max_nf, cudaStream_t s) {
+  by_bs(A.bs, [&](auto BS) {
+    const int np = max_nf * BS;
+    k_jacobi_patch<BS><<<P.n, ((np + 31) / 32) * 32, 0, s>>>(P, np, r, d);
+  });
+  HPMG_LAUNCH_CHECK();
+}
+
+void jacobi_combine(int nb, int bs, const Patches& P, const double* d, int max_nf, double damping, double* x,
+                    cudaStream_t s) {
+  k_jacobi_combine<<<grid_for(int64_t(nb) * bs, 256), 256, 0, s>>>(nb, bs, P, max_nf * bs, d, damping, x);
+  HPMG_LAUNCH_CHECK();
+}
+
+void prolong_add(const BlockCsr& P, const double* e, double* x, cudaStream_t s) {
+  k_prolong_add<<<grid_for(int64_t(P.nrows) * 2, 256), 256, 0, s>>>(P, e, x);
+  HPMG_LAUNCH_CHECK();
+}
+
+void restrict_(const BlockCsr& PT, const double* r, double* rc, cudaStream_t s) {
+  k_restrict<<<grid_for(int64_t(PT.nrows) * 2, 256), 256, 0, s>>>(PT, r, rc);
+  HPMG_LAUNCH_CHECK();
+}
+
+void dense_gemv(int n, const double* inv, const double* b, double* x, double* work, cudaStream_t s) {
+  const int chunks = (n + kGemvChunk - 1) / kGemvChunk;
+  dim3 grid((n + 127) / 128, chunks);
+  k_gemv_partial<<<grid, 128, 0, s>>>(n, inv, b, work);
+  k_gemv_sum<<<(n + 127) / 128, 128, 0, s>>>(n, chunks, work, x);
+  HPMG_LAUNCH_CHECK();
+}
+
+void fill(double* x, double v, int64_t n, cudaStream_t s) {
+  k_fill<<<grid_for(n, 256), 256, 0, s>>>(x, v, n);
+  HPMG_LAUNCH_CHECK();
+}
+void copy(double* y, const double* x, int64_t n, cudaStream_t s) {
+  k_copy<<<grid_for(n, 256), 256, 0, s>>>(y, x, n);
+  HPMG_LAUNCH_CHECK();
+}
+void axpy(double* y, double a, const double* x, int64_t n, cudaStream_t s) {
+  k_axpy<<<grid_for(n, 256), 256, 0, s>>>(y, a, x, n);
+  HPMG_LAUNCH_CHECK();
+}
+void sub(double* y, const double* a, const double* b, int64_t n, cudaStream_t s) {
+  k_sub<<<grid_for(n, 256), 256, 0, s>>>(y, a, b, n);
+  HPMG_LAUNCH_CHECK();
+}
+void dot(const double* a, const double* b, int64_t n, const Reduce& red, double* out, cudaStream_t s) {
+  k_dot<<<kRedBlocks, 256, 0, s>>>(a, b, n, red, out);
+  HPMG_LAUNCH_CHECK();
+}
+void pcg_update(double* x, double* r, const double* p, const double* Ap, int64_t n, double* sc, int i_num, int i_den,
+                const Reduce& red, int i_rr, cudaStream_t s) {
+  k_pcg_update<<<kRedBlocks, 256, 0, s>>>(x, r, p, Ap, n, sc, i_num, i_den, red, i_rr);
+  HPMG_LAUNCH_CHECK();
+}
+void pcg_direction(double* p, const double* z, int64_t n, double* sc, int i_new, int i_old, cudaStream_t s) {
+  k_pcg_direction<<<grid_for(n, 256), 256, 0, s>>>(p, z, n, sc, i_new, i_old);
+  HPMG_LAUNCH_CHECK();
+}
+void scal_axpby(double* y, const double* x, int64_t n, const double* sc, int ia, double fa, double fb, cudaStream_t s) {
+  k_scal_axpby<<<grid_for(n, 256), 256, 0, s>>>(y, x, n, sc, ia, fa, fb);
+  HPMG_LAUNCH_CHECK();
+}
+void to_blocks(int nb, int nfd, const double* ref, double* blk, cudaStream_t s) {
+  k_to_blocks<<<grid_for(int64_t(nb) * 2 * nfd, 256), 256, 0, s>>>(nb, nfd, ref, blk);
+  HPMG_LAUNCH_CHECK();
+}
+void to_reference(int nb, int nfd, const double* blk, double* ref, cudaStream_t s) {
+  k_to_reference<<<grid_for(int64_t(nb) * 2 * nfd, 256), 256, 0, s>>>(nb, nfd, blk, ref);
+  HPMG_LAUNCH_CHECK();
+}
+void uzawa_rhs(int nb, int bs, const double* rhs0, const int* row_elems, const ElemGeo* geo, const double* p,
+               double* rhs, cudaStream_t s) {
+  k_uzawa_rhs<<<grid_for(int64_t(nb) * bs, 256), 256, 0, s>>>(nb, bs, rhs0, row_elems, geo, p, rhs);
+  HPMG_LAUNCH_CHECK();
+}
+void uzawa_div(int ne, int bs, const int* elem_facets, const int* facet_block, const double* g_fac, const double* u,
+               const ElemGeo* geo, double* div, cudaStream_t s) {
+  k_uzawa_div<<<grid_for(ne, 256), 256, 0, s>>>(ne, bs, elem_facets, facet_block, g_fac, u, geo, div);
+  HPMG_LAUNCH_CHECK();
+}
+void uzawa_pressure(int ne, const double* div, const ElemGeo* geo, double inv_eps, double* p, int enclosed,
+                    const Reduce& red, double* sc, int i_s, int i_a, int i_max, cudaStream_t s) {
+  k_uzawa_p1<<<kRedBlocks, 256, 0, s>>>(ne, div, geo, inv_eps, p, red, sc + i_s);
+  if (enclosed) {
+    k_area_sum<<<kRedBlocks, 256, 0, s>>>(ne, geo, red, sc + i_a);
+    k_uzawa_p2<<<grid_for(ne, 256), 256, 0, s>>>(ne, p, sc, i_s, i_a);
+  }
+  k_absmax<<<kRedBlocks, 256, 0, s>>>(ne, div, red, sc + i_max);
+  HPMG_LAUNCH_CHECK();
+}
+
+}  // namespace dev
+}  // namespace hpmg

@@ -1,0 +1,110 @@
+// Launch wrappers of the sm_100a FP64 kernels (definitions in kernels.cu).
+// All vectors are in the device block layout: block f (free facet) holds
+// bs = 2(k+1) doubles [flux_0, tang_0, ..., flux_k, tang_k].
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "condense.cuh"
+
+namespace hpmg {
+namespace dev {
+
+constexpr int kSlots = 5;
+constexpr int kMaxPatchF = 8;
+constexpr int kRedBlocks = 296;  // 2 x 148 SMs: fixed partial count => deterministic sums
+
+/// Block-sparse operator of one level: nb rows x kSlots fixed-width slots.
+struct Bsr {
+  int nb = 0, bs = 2;
+  double* val = nullptr;  // [nb][kSlots][bs][bs]
+  int* cols = nullptr;    // [nb][kSlots], -1 empty
+};
+
+/// Vertex patches with explicit inverses (column-major, (nf*bs)^2 each).
+struct Patches {
+  int n = 0;
+  int* nf = nullptr;        // [n]
+  int* fac = nullptr;       // [n][kMaxPatchF]
+  int64_t* off = nullptr;   // [n]
+  double* inv = nullptr;
+  int* wave = nullptr;      // patch ids grouped by wave
+  int* fpatch = nullptr;    // [nb][2] patches holding block f (ascending)
+};
+
+/// 2x2-block CSR (prolongation P: fine rows; PT: coarse rows).
+struct BlockCsr {
+  int nrows = 0;
+  int* ptr = nullptr;
+  int* col = nullptr;
+  double* val = nullptr;  // [nnzb][2][2] row-major
+};
+
+struct Reduce {
+  double* partial = nullptr;      // [kRedBlocks]
+  unsigned* counter = nullptr;    // zero-initialised ticket
+};
+
+void condense(const RefT& T, const ElemGeo* geo, int ne, CondenseParams prm, const double* load, int load_stride,
+              double* out, cudaStream_t s);
+void assemble_bsr(const Bsr& A, int nfd, const double* acr, int acr_stride, int nc, const int* gath,
+                  const ElemGeo* geo, double inv_eps, cudaStream_t s);
+void transpose_bsr(const Bsr& A, const int* tslot, Bsr& AT, cudaStream_t s);
+void assemble_rhs(int nb, int bs, int nfd, const int* row_elems, const int* block_facet, const int* elem_facets,
+                  const char* facet_dirichlet, const double* g_fac, const double* acr, int acr_stride, int nc,
+                  const ElemGeo* geo, double inv_eps, double* rhs, cudaStream_t s);
+
+/// y = A x (minus = 0) or y = b - A x (minus = 1); if red != null also
+/// reduces dot(x, y) into *dot_out.
+void spmv(const Bsr& A, const double* x, const double* b, double* y, int minus, const Reduce* red, double* dot_out,
+          cudaStream_t s);
+/// Residual restricted to mode-0 rows, written in lowest-order layout
+/// (fused E^T (b - A x), reference multigrid.hpp:123-124).
+void inject_residual(const Bsr& A, const double* x, const double* b, double* r0, cudaStream_t s);
+/// x[f][0..1] += e[f][0..1] (the embedding E, transfer.hpp:140-158).
+void embed_add(int nb, int bs, const double* e, double* x, cudaStream_t s);
+
+void patch_inverse(const Bsr& A, const Patches& P, int max_nf, cudaStream_t s);
+/// One wave of the multiplicative sweep: x_p += Inv_p (b - A x)_p for the
+/// patches wave[w0..w1). transposed_inv selects (Inv_p)^T (nonsymmetric backward).
+void gs_wave(const Bsr& A, const Patches& P, int w0, int w1, const double* b, double* x, int transposed_inv,
+             int max_nf, cudaStream_t s);
+/// Additive sweep pieces: d_p = Inv_p r_p for all patches; x += damping * sum_p d_p.
+void jacobi_patch(const Bsr& A, const Patches& P, const double* r, double* d, int max_nf, cudaStream_t s);
+void jacobi_combine(int nb, int bs, const Patches& P, const double* d, int max_nf, double damping, double* x,
+                    cudaStream_t s);
+
+void prolong_add(const BlockCsr& P, const double* e, double* x, cudaStream_t s);
+void restrict_(const BlockCsr& PT, const double* r, double* rc, cudaStream_t s);
+void dense_gemv(int n, const double* inv_colmajor, const double* b, double* x, double* work, cudaStream_t s);
+
+// vector kernels (n doubles)
+void fill(double* x, double v, int64_t n, cudaStream_t s);
+void copy(double* y, const double* x, int64_t n, cudaStream_t s);
+void axpy(double* y, double a, const double* x, int64_t n, cudaStream_t s);
+void sub(double* y, const double* a, const double* b, int64_t n, cudaStream_t s);  // y = a - b
+void dot(const double* a, const double* b, int64_t n, const Reduce& red, double* out, cudaStream_t s);
+/// PCG update: alpha = sc[i_num]/sc[i_den]; x += alpha p; r -= alpha Ap; sc[i_rr] = |r|^2
+void pcg_update(double* x, double* r, const double* p, const double* Ap, int64_t n, double* sc, int i_num, int i_den,
+                const Reduce& red, int i_rr, cudaStream_t s);
+/// p = z + (sc[i_new]/sc[i_old]) p ; then sc[i_old] = sc[i_new]
+void pcg_direction(double* p, const double* z, int64_t n, double* sc, int i_new, int i_old, cudaStream_t s);
+/// y = a * x + b * y with device scalars sc[ia] (or 1 if ia < 0), factor fa
+void scal_axpby(double* y, const double* x, int64_t n, const double* sc, int ia, double fa, double fb, cudaStream_t s);
+
+// layout permutations between the reference free order and the block layout
+void to_blocks(int nb, int nfd, const double* ref, double* blk, cudaStream_t s);
+void to_reference(int nb, int nfd, const double* blk, double* ref, cudaStream_t s);
+
+// augmented-Lagrangian Uzawa pieces (uzawa.hpp:69-82)
+void uzawa_rhs(int nb, int bs, const double* rhs0, const int* row_elems, const ElemGeo* geo, const double* p,
+               double* rhs, cudaStream_t s);
+void uzawa_div(int ne, int bs, const int* elem_facets, const int* facet_block, const double* g_fac, const double* u,
+               const ElemGeo* geo, double* div, cudaStream_t s);
+void uzawa_pressure(int ne, const double* div, const ElemGeo* geo, double inv_eps, double* p, int enclosed,
+                    const Reduce& red, double* sc, int i_s, int i_a, int i_max, cudaStream_t s);
+
+}  // namespace dev
+}  // namespace hpmg

@@ -1,0 +1,123 @@
+"""GPU-vs-oracle parity of the hp-MG path, through the C ABI (libhpmg.so).
+
+Tolerances (SURVEY.md 8(c) protocol): operator apply relative <= 1e-13,
+preconditioner apply relative <= 1e-10 (explicit patch inverses vs. LU solves
+and wave-parallel pull residuals round differently from the sequential
+reference sweep), Krylov iteration counts +-1, final velocity relative
+L2 <= 1e-9 (north star).
+"""
+import numpy as np
+import pytest
+
+import oracle_lib as O
+
+pytestmark = pytest.mark.gpu
+
+H = pytest.importorskip("paper_2303_06762_b200")
+
+
+def lid_top(x, y):
+    return (4 * x * (1 - x), 0.0) if y > 1.0 - 1e-12 else (0.0, 0.0)
+
+
+def pair(k, base_n=2, levels=3, beta=1.0, nu=1.0, inv_eps=1e3, bc=None, seed=1, cycle=O.CYCLE_V, m=1,
+         smoother=O.SM_MULT):
+    n_f = base_n << (levels - 1)
+    F = O.seeded_load(n_f, seed)
+    obc = O.BC_NONE if bc is None else O.BC_LID_TOP
+    orc = O.OracleMG(base_n=base_n, levels=levels, k=k, nu=nu, beta=beta, inv_eps=inv_eps, bc=obc,
+                     load_kind=O.LOAD_ARRAY, load=F, cycle=cycle, smooth_steps=m, smoother=smoother)
+    gpu = H.MGPreconditioner(base_n=base_n, levels=levels, k=k, nu=nu, beta=beta, inv_eps=inv_eps, bc=bc,
+                             structured_load=(n_f, F), cycle=cycle, smooth_steps=m, smoother=smoother)
+    return orc, gpu
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 3])
+def test_operator_and_rhs(k):
+    orc, gpu = pair(k, bc=lid_top)
+    assert gpu.n == orc.n and gpu.n_full == orc.n_full
+    assert np.array_equal(gpu.free_to_full(), orc.free_to_full())
+    x = O.random_vec(orc.n, 5)
+    assert rel(gpu.spmv(x), orc.spmv(x)) < 1e-13
+    assert rel(gpu.rhs(), orc.rhs()) < 1e-13
+    A_g, A_o = gpu.matrix(), orc.csr()
+    assert abs(A_g - A_o).max() <= 1e-13 * abs(A_o).max()
+
+
+def test_level_operators():
+    orc, gpu = pair(2, levels=4)
+    for l in range(4):
+        A_g, A_o = gpu.matrix(l), orc.csr(l)
+        assert A_g.shape == A_o.shape
+        assert abs(A_g - A_o).max() <= 1e-13 * abs(A_o).max()
+
+
+@pytest.mark.parametrize("k", [0, 1, 3])
+def test_smoother_sweeps(k):
+    orc, gpu = pair(k)
+    level = -1 if k > 0 else 2
+    n = orc.n
+    b, x0 = O.random_vec(n, 7), O.random_vec(n, 9)
+    for which in (0, 1):
+        xg = gpu.smooth(level, which, x0, b, 1)
+        xo = orc.smooth(level, which, x0, b, 1)
+        assert rel(xg, xo) < 1e-10
+
+
+@pytest.mark.parametrize("k,cycle", [(0, O.CYCLE_V), (1, O.CYCLE_V), (2, O.CYCLE_W), (3, O.CYCLE_V),
+                                     (1, O.CYCLE_VARV)])
+def test_preconditioner_apply(k, cycle):
+    orc, gpu = pair(k, levels=4, cycle=cycle)
+    b = O.random_vec(orc.n, 11)
+    assert rel(gpu.apply(b), orc.apply(b)) < 1e-10
+
+
+def test_additive_smoother_apply():
+    orc, gpu = pair(1, levels=3, smoother=O.SM_ADD)
+    b = O.random_vec(orc.n, 13)
+    assert rel(gpu.apply(b), orc.apply(b)) < 1e-10
+
+
+def test_apply_bit_identical_repeat():
+    _, gpu = pair(1)
+    b = O.random_vec(gpu.n, 17)
+    assert np.array_equal(gpu.apply(b), gpu.apply(b))
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 3])
+def test_pcg_counts_and_solution(k):
+    orc, gpu = pair(k, levels=4, bc=lid_top)
+    b = orc.rhs()
+    xo, so = orc.krylov(b)
+    xg, sg = H.pcg(gpu, b)
+    assert sg.converged and so["converged"]
+    assert abs(sg.iterations - so["iterations"]) <= 1
+    assert rel(xg, xo) < 1e-8
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_uzawa_matches_oracle(k):
+    orc, gpu = pair(k, levels=4, bc=lid_top)
+    ro = orc.uzawa()
+    rg = H.uzawa_solve(gpu)
+    assert rg.report.converged and ro["converged"]
+    for a, b in zip(rg.report.inner_iterations, ro["inner_iterations"]):
+        assert abs(a - b) <= 1
+    assert rel(rg.velocity, ro["velocity"]) < 1e-9
+    assert rel(rg.pressure, ro["pressure"]) < 1e-6
+
+
+def test_config1_full_size_parity():
+    # BASELINE config 1: 8x8 base + 4 refinements (128^2 x 2 triangles), k=1,
+    # AL 1e3, beta 1, nu 1, homogeneous Dirichlet, seeded U[-1,1] force, V(1,1)
+    orc, gpu = pair(1, base_n=8, levels=5, beta=1.0, inv_eps=1e3)
+    ro = orc.uzawa()
+    rg = H.uzawa_solve(gpu)
+    assert rg.report.converged
+    for a, b in zip(rg.report.inner_iterations, ro["inner_iterations"]):
+        assert abs(a - b) <= 1
+    assert rel(rg.velocity, ro["velocity"]) < 1e-9
