@@ -1,0 +1,280 @@
+#!/usr/bin/env python
+"""hp-MG V-cycle benchmark on B200 (BASELINE.json metric, config 2 by default).
+
+Workload (BASELINE configs[1]): 2-D generalized Stokes, unit square, 16x16
+base mesh + 4 red refinements (256^2 x 2 = 131,072 triangles, 5 GMG levels),
+order k = 3 (n = 1,568,768 free DOFs), AL parameter 1e3, mass 1e-2, nu 1,
+homogeneous Dirichlet, seeded per-triangle force U[-1,1] (mt19937 seed 1),
+V(1,1) multiplicative vertex-patch smoothing, PCG to 1e-8.
+
+One step = one hp-MG V-cycle (MGPreconditioner::apply) on an HBM-resident
+residual. `value` = V-cycles/s over all ranks (replicas, one per GPU);
+`e2e` = the same through the C ABI with host buffers (H2D residual + V-cycle +
+D2H correction inside the timed region). The V-cycle streams ~6 GB per call,
+far above the 126 MB L2, so no explicit flush is needed.
+
+--impl reference times the CPU restatement of the reference (oracle/,
+single-threaded like the reference) on the same config, bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+CONFIGS = {
+    # name: (base_n, levels, k, nu, beta, inv_eps)
+    "config2": dict(base_n=16, levels=5, k=3, nu=1.0, beta=1e-2, inv_eps=1e3),
+    "config1": dict(base_n=8, levels=5, k=1, nu=1.0, beta=1.0, inv_eps=1e3),
+    "config3": dict(base_n=8, levels=5, k=2, nu=1.0, beta=0.0, inv_eps=1e4),
+}
+METRIC = "hp-MG V-cycles/sec (k=3, 256^2x2 tri, 1.57M DOFs)"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) == 6:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        return rank, world, local, dist
+    return 0, 1, 0, None
+
+
+def run_hpmg(args, rank, world, local, dist):
+    import torch  # device selection / external-stream events (plumbing only)
+    import paper_2303_06762_b200 as H
+
+    torch.cuda.set_device(local)
+    cfg = CONFIGS[args.config]
+    n_f = cfg["base_n"] << (cfg["levels"] - 1)
+    F = H.seeded_load(n_f, args.seed)
+    t0 = time.perf_counter()
+    B = H.MGPreconditioner(mesh="unit_square", base_n=cfg["base_n"], levels=cfg["levels"], k=cfg["k"],
+                           nu=cfg["nu"], beta=cfg["beta"], inv_eps=cfg["inv_eps"], cycle=H.CYCLE_V,
+                           smoother=H.SMOOTH_MULTIPLICATIVE, smooth_steps=1, structured_load=(n_f, F))
+    setup_wall = time.perf_counter() - t0
+    setup_dev, setup_parts = B.setup_seconds()
+    n = B.n
+    lib = H.lib()
+    stream = torch.cuda.ExternalStream(B.stream())
+    rng = np.random.default_rng(1234 + rank)
+    r_host = torch.from_numpy(rng.uniform(-1, 1, n)).pin_memory()
+    z_host = torch.empty(n, dtype=torch.float64).pin_memory()
+    r_dev = r_host.to(f"cuda:{local}")
+    z_dev = torch.empty_like(r_dev)
+
+    def step_dev():
+        lib.hpmg_apply(B.h, ctypes.c_void_p(r_dev.data_ptr()), ctypes.c_void_p(z_dev.data_ptr()), H.DEVICE_PTRS)
+
+    def step_e2e():
+        lib.hpmg_apply(B.h, ctypes.c_void_p(r_host.data_ptr()), ctypes.c_void_p(z_host.data_ptr()), 0)
+
+    def timed(fn, steps):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ms], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    with ClockSampler(local) as clk:
+        ms_dev = timed(step_dev, args.steps)
+    ms_e2e = timed(step_e2e, max(3, args.steps // 2))
+    # per-phase split (event-instrumented pass): head pre-sweep, head residual, h-cycle, head post-sweep
+    _, phases = B.time_apply(max(3, args.steps // 4), phases=True)
+    vbytes, vparts = B.vcycle_bytes()
+    hbm, src = peaks()
+    head_sweep_ms = phases[0] + phases[3]
+    head_bytes = vparts[0]
+    achieved = head_bytes / (head_sweep_ms * 1e-3) / 1e9 if head_sweep_ms > 0 else None
+    # time-to-solution: device Uzawa (2 outer PCG solves to 1e-8)
+    sol = H.uzawa_solve(B)
+    launches = B.launches_per_apply()
+    out = None
+    if rank == 0:
+        per_gpu = args.steps / (ms_dev * 1e-3)
+        out = {
+            "metric": METRIC if args.config == "config2" else f"hp-MG V-cycles/sec ({args.config})",
+            "value": per_gpu * world,
+            "unit": "V-cycles/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_dev / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic: seeded per-triangle U[-1,1] force (mt19937 seed %d), random-init residual" % args.seed,
+            "config": {"workload": args.config, **cfg, "cycle": "V(1,1)", "smoother": "multiplicative vertex-patch",
+                       "n_dofs": int(n), "parallelism": f"replicas x{world}",
+                       "l2": "no flush needed: V-cycle streams %.2f GB per call (> 126 MB L2)" % (vbytes / 1e9)},
+            "e2e": {"value": max(3, args.steps // 2) / (ms_e2e * 1e-3) * world, "unit": "V-cycles/s",
+                    "h2d_bytes_per_step": int(8 * n), "d2h_bytes_per_step": int(8 * n)},
+            "roofline": {"bound": "hbm", "kernel": "k_gs_wave<8> (order-k head patch sweeps)",
+                         "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": (achieved / hbm) if achieved else None, "traffic": None,
+                         "peak_source": src, "algorithmic_bytes_per_vcycle": vbytes,
+                         "head_sweep_bytes_per_vcycle": head_bytes, "head_sweep_ms": head_sweep_ms,
+                         "vcycle_achieved_gbs": vbytes / (ms_dev / args.steps * 1e-3) / 1e9},
+            "phases_ms": {"head_pre": phases[0], "head_residual": phases[1], "h_cycle": phases[2],
+                          "head_post": phases[3]},
+            "gpu_launches": int(launches * args.steps),
+            "kernels_per_vcycle": int(launches),
+            "tts": {"uzawa_device_s": sol.report.seconds, "setup_wall_s": setup_wall,
+                    "setup_parts_s": [float(x) for x in setup_parts[:7]],
+                    "inner_iterations": sol.report.inner_iterations,
+                    "final_divergence": sol.report.final_divergence, "converged": sol.report.converged},
+            "clocks": clk.summary(),
+        }
+        if args.cpu_baseline and world == 1:
+            out["cpu_baseline"] = cpu_baseline(args, cfg, n_f, F, sample_vcycles=args.cpu_vcycles)
+    return out
+
+
+def cpu_baseline(args, cfg, n_f, F, sample_vcycles=3):
+    """Oracle (CPU restatement of the reference, 1 thread) on the same config."""
+    import oracle_lib as O
+    t0 = time.perf_counter()
+    B = O.OracleMG(base_n=cfg["base_n"], levels=cfg["levels"], k=cfg["k"], nu=cfg["nu"], beta=cfg["beta"],
+                   inv_eps=cfg["inv_eps"], bc=O.BC_NONE, load_kind=O.LOAD_ARRAY, load=F, cycle=O.CYCLE_V,
+                   smooth_steps=1)
+    setup = time.perf_counter() - t0
+    secs = B.time_apply(sample_vcycles)
+    return {"value": sample_vcycles / secs, "unit": "V-cycles/s", "cores": 1, "kind": "port",
+            "sample": f"{sample_vcycles} V-cycles of {args.config} after a {setup:.1f} s setup (oracle/, 1 thread)",
+            "setup_s": setup}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    import oracle_lib as O
+    cfg = CONFIGS[args.config]
+    n_f = cfg["base_n"] << (cfg["levels"] - 1)
+    F = O.seeded_load(n_f, args.seed)
+    B = O.OracleMG(base_n=cfg["base_n"], levels=cfg["levels"], k=cfg["k"], nu=cfg["nu"], beta=cfg["beta"],
+                   inv_eps=cfg["inv_eps"], bc=O.BC_NONE, load_kind=O.LOAD_ARRAY, load=F, cycle=O.CYCLE_V,
+                   smooth_steps=1)
+    per_step = max(1, args.ref_vcycles_per_step)
+    for _ in range(min(args.warmup, 3)):
+        B.time_apply(1)
+    secs = sum(B.time_apply(per_step) for _ in range(args.steps))
+    v = args.steps * per_step / secs
+    return {"impl": "reference", "metric": METRIC if args.config == "config2" else f"hp-MG V-cycles/sec ({args.config})",
+            "value": v, "unit": "V-cycles/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (same seeded force as the GPU arm)",
+            "config": {"workload": args.config, **cfg},
+            "cpu_baseline": {"value": v, "unit": "V-cycles/s", "cores": 1, "kind": "port",
+                             "sample": f"{args.steps} x {per_step} V-cycles, oracle/ restatement (reference needs Eigen, absent)"},
+            "e2e": {"value": v, "unit": "V-cycles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="hpmg", choices=["hpmg", "reference"])
+    ap.add_argument("--config", default="config2", choices=sorted(CONFIGS))
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--cpu-baseline", dest="cpu_baseline", action="store_true", default=True)
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--cpu-vcycles", type=int, default=3)
+    ap.add_argument("--ref-vcycles-per-step", type=int, default=1)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "hpmg" else args.warmup
+    if args.impl == "reference":
+        out = run_reference(args)
+    else:
+        rank, world, local, dist = dist_init()
+        out = run_hpmg(args, rank, world, local, dist)
+        if dist:
+            dist.barrier()
+    if out is not None:
+        print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -165,6 +165,10 @@ double hpmg_spmv_bytes(const hpmg_ctx* ctx);
  * 8 doubles) receives per-phase averages from an event-instrumented pass. */
 double hpmg_time_apply(hpmg_ctx* ctx, int reps, double* phase_ms);
 int hpmg_kernel_launches_per_apply(const hpmg_ctx* ctx);
+/* Per-level split of one V-cycle (event-instrumented, no graph): out[0] coarse
+ * solve, out[2l] / out[2l+1] pre / post part of level l, out[2L+2..2L+4] head
+ * pre-sweep, head residual, head post-sweep (ms). Returns the entry count. */
+int hpmg_profile_levels(hpmg_ctx* ctx, int reps, double* out);
 double hpmg_setup_seconds(const hpmg_ctx* ctx, double* parts);
 
 /* Seeded per-triangle force of the BASELINE configs: std::mt19937(seed) and

@@ -64,6 +64,8 @@ struct Level {
   dev::Patches P;
   int max_nf = 0;
   std::vector<int> wave_ptr;
+  int* d_wave_ptr = nullptr;
+  dev::PatchRecords rec;
   dev::BlockCsr Pm, PT;  // from level l-1 to l (lowest-order levels l >= 1)
   double *x = nullptr, *b = nullptr, *r = nullptr, *y = nullptr, *bw = nullptr, *xw = nullptr, *dbuf = nullptr;
   int steps = 1;
@@ -74,8 +76,9 @@ struct Level {
   int* row_elems = nullptr;
   int* elem_facets = nullptr;
   int* facet_block = nullptr;
-  double bytes_sweep = 0, bytes_spmv = 0;
+  double bytes_sweep = 0, bytes_spmv = 0, p_nnz = 0, bytes_sweep_phys = 0;
 };
+constexpr double kSlotsD = double(host::kSlots);
 
 }  // namespace
 
@@ -189,6 +192,7 @@ void build_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, const Dev
   V.k = k;
   V.bs = 2 * (k + 1);
   V.plan = host::make_level(m, k);
+  host::set_inverse_layout(V.plan, !C.advected);  // packed symmetric inverses for Stokes
   V.nb = V.plan.nb;
   V.n = V.plan.n();
   V.ne = m.ne();
@@ -282,9 +286,11 @@ void build_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, const Dev
   V.P.fac = dupload(V.plan.patch_fac, s);
   V.P.off = dupload(V.plan.inv_off, s);
   V.P.inv = dalloc<double>(size_t(V.plan.inv_total));
+  V.P.packed = V.plan.packed ? 1 : 0;
   V.P.wave = dupload(V.plan.wave_patch, s);
   V.P.fpatch = dupload(V.plan.facet_patches, s);
   V.wave_ptr = V.plan.wave_ptr;
+  V.d_wave_ptr = dupload(V.wave_ptr, s);
   alloc_level_vectors(V);
   V.dbuf = dalloc<double>(size_t(std::max(V.P.n, 1)) * V.max_nf * V.bs);
   // algorithmic bytes, ELL slots counted as stored
@@ -292,11 +298,19 @@ void build_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, const Dev
   for (int c : V.plan.cols) nnz += c >= 0 ? double(V.bs) * V.bs : 0.0;
   const double nblk = nnz / (double(V.bs) * V.bs);
   V.bytes_spmv = 8 * nnz + 4 * nblk + 4 * (V.nb + 1.0) + 16.0 * V.n;
-  V.bytes_sweep = 8.0 * double(V.plan.inv_total) + 2 * (8 * nnz + 4 * nblk) + 32.0 * V.n;
+  // reference storage accounting: full np^2 patch factors (packing halves the physical bytes)
+  V.bytes_sweep = 8.0 * double(V.plan.inv_full_total) + 2 * (8 * nnz + 4 * nblk) + 32.0 * V.n;
+  V.bytes_sweep_phys = 8.0 * double(V.plan.inv_total) + 2 * (8 * nnz + 4 * kSlotsD * V.nb) + 32.0 * V.n;
 }
 
 void build_patch_inverses(hpmg_ctx& C, Level& V) {
-  if (V.P.n > 0) dev::patch_inverse(V.A, V.P, V.max_nf, C.s);
+  if (V.P.n == 0) return;
+  dev::patch_inverse(V.A, V.P, V.max_nf, C.s);
+  if (V.P.packed) {  // fixed-stride patch records for the TMA sweep (sweep_rec.cu)
+    V.rec = dev::record_layout(V.bs, V.max_nf);
+    V.rec.rec = dalloc<double>(size_t(V.P.n) * V.rec.stride);
+    dev::build_records(V.A, V.P, V.rec, C.s);
+  }
 }
 
 /// transposed-slot map for A^T in the same ELL pattern (A's pattern is symmetric)
@@ -385,10 +399,28 @@ void smooth(hpmg_ctx& C, Level& V, double* x, const double* b, bool post) {
     }
     return;
   }
+  // L2 prefetch of the next wave's patch inverses (contiguous: patches are numbered in wave order)
+  auto next_inv = [&](int w, const void** ptr, size_t* len) {
+    *ptr = nullptr;
+    *len = 0;
+    if (w < 0 || w >= nw || !V.P.packed) return;
+    const int64_t a = V.plan.inv_off[V.wave_ptr[w]];
+    const int64_t e = V.wave_ptr[w + 1] < V.P.n ? V.plan.inv_off[V.wave_ptr[w + 1]] : V.plan.inv_total;
+    const uintptr_t beg = reinterpret_cast<uintptr_t>(V.P.inv + a) & ~uintptr_t(15);
+    *ptr = reinterpret_cast<const void*>(beg);
+    *len = size_t(reinterpret_cast<uintptr_t>(V.P.inv + e) - beg);
+  };
+  const void* pf;
+  size_t pl;
   if (!post) {
     for (int s = 0; s < V.steps; ++s)
       for (int w = 0; w < nw; ++w) {
-        dev::gs_wave(V.A, V.P, V.wave_ptr[w], V.wave_ptr[w + 1], b, x, 0, V.max_nf, C.s);
+        if (V.P.packed) {
+          dev::gs_wave_rec(V.rec, V.wave_ptr[w], V.wave_ptr[w + 1], b, x, C.s);
+        } else {
+          next_inv(w + 1 < nw ? w + 1 : (s + 1 < V.steps ? 0 : -1), &pf, &pl);
+          dev::gs_wave(V.A, V.P, V.wave_ptr[w], V.wave_ptr[w + 1], b, x, 0, V.max_nf, C.s, pf, pl);
+        }
         count(C);
       }
     return;
@@ -397,7 +429,12 @@ void smooth(hpmg_ctx& C, Level& V, double* x, const double* b, bool post) {
     // symmetric: the exact transpose sweep is the reverse-order sweep on x itself
     for (int s = 0; s < V.steps; ++s)
       for (int w = nw - 1; w >= 0; --w) {
-        dev::gs_wave(V.A, V.P, V.wave_ptr[w], V.wave_ptr[w + 1], b, x, 0, V.max_nf, C.s);
+        if (V.P.packed) {
+          dev::gs_wave_rec(V.rec, V.wave_ptr[w], V.wave_ptr[w + 1], b, x, C.s);
+        } else {
+          next_inv(w - 1 >= 0 ? w - 1 : (s + 1 < V.steps ? nw - 1 : -1), &pf, &pl);
+          dev::gs_wave(V.A, V.P, V.wave_ptr[w], V.wave_ptr[w + 1], b, x, 0, V.max_nf, C.s, pf, pl);
+        }
         count(C);
       }
     return;
@@ -424,6 +461,18 @@ void h_cycle(hpmg_ctx& C, int l, const double* b, double* x) {
   }
   Level& V = *C.lv[l];
   Level& W = *C.lv[l - 1];
+  const int q = C.opt.cycle == HPMG_CYCLE_W ? 2 : 1;
+  const int nw = int(V.wave_ptr.size()) - 1;
+  if (dev::small_level_fits(V.nb, V.P.n, nw) && !C.advected && C.opt.smoother == HPMG_SMOOTH_MULTIPLICATIVE &&
+      q == 1) {
+    // whole-level sweeps in one persistent CTA (small_levels.cu)
+    dev::small_pre(V.A, V.P, V.d_wave_ptr, nw, V.steps, V.PT, b, x, W.b, C.s);
+    count(C);
+    h_cycle(C, l - 1, W.b, W.x);
+    dev::small_post(V.A, V.P, V.d_wave_ptr, nw, V.steps, V.Pm, W.x, b, x, C.s);
+    count(C);
+    return;
+  }
   dev::fill(x, 0.0, V.n, C.s);
   count(C);
   smooth(C, V, x, b, false);
@@ -431,7 +480,6 @@ void h_cycle(hpmg_ctx& C, int l, const double* b, double* x) {
   dev::restrict_(V.PT, V.r, W.b, C.s);
   count(C, 2);
   h_cycle(C, l - 1, W.b, W.x);
-  const int q = C.opt.cycle == HPMG_CYCLE_W ? 2 : 1;
   for (int i = 1; i < q; ++i) {
     dev::spmv(W.A, W.x, W.b, W.bw, 1, nullptr, nullptr, C.s);
     count(C);
@@ -755,6 +803,9 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
     std::vector<double> Af = download_bsr(C, *C.lv[l]);
     host::BlockCsrH P = host::corrected_prolongation(C.lv[l - 1]->plan, C.lv[l]->plan, C.ref[l - 1], Af);
     host::BlockCsrH PT = host::transpose_blocks(P);
+    double nz = 0;
+    for (double v : P.val) nz += v != 0.0;
+    C.lv[l]->p_nnz = nz;
     C.lv[l]->Pm = upload_blockcsr(P, C.s);
     C.lv[l]->PT = upload_blockcsr(PT, C.s);
   }
@@ -772,7 +823,7 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
           for (int j = 0; j < 2; ++j) D[size_t(2 * r + i) * C.n0 + 2 * c + j] = A0[((size_t(r) * host::kSlots + s) * 2 + i) * 2 + j];
       }
     C.coarse_inv = dupload(dense_inverse(D, C.n0), C.s);
-    C.gemv_work = dalloc<double>(size_t(C.n0) * ((C.n0 + 127) / 128 + 1));
+    C.gemv_work = dalloc<double>(size_t(C.n0) * ((C.n0 + 63) / 64 + 1));  // kGemvChunk = 64
   }
   auto t5 = clk::now();
   // solver workspace
@@ -847,7 +898,8 @@ void hpmg_destroy(hpmg_ctx* ctx) {
                     (void*)V->P.fac, (void*)V->P.off, (void*)V->P.inv, (void*)V->P.wave, (void*)V->P.fpatch,
                     (void*)V->Pm.ptr, (void*)V->Pm.col, (void*)V->Pm.val, (void*)V->PT.ptr, (void*)V->PT.col,
                     (void*)V->PT.val, (void*)V->x, (void*)V->b, (void*)V->r, (void*)V->y, (void*)V->bw, (void*)V->xw,
-                    (void*)V->dbuf, (void*)V->geo, (void*)V->row_elems, (void*)V->elem_facets, (void*)V->facet_block})
+                    (void*)V->dbuf, (void*)V->geo, (void*)V->row_elems, (void*)V->elem_facets, (void*)V->facet_block,
+                    (void*)V->d_wave_ptr, (void*)V->rec.rec})
       fr(p);
   };
   for (auto& V : ctx->lv) free_level(V.get());
@@ -1086,14 +1138,8 @@ double hpmg_vcycle_bytes(const hpmg_ctx* ctx, double* parts) {
     const double visits = std::pow(double(q), C.L - l);
     p[2] += visits * 2.0 * V.steps * V.bytes_sweep;
     p[3] += visits * (V.bytes_spmv + 8.0 * V.n);
-    // P and P^T: 12 bytes per scalar nonzero + vectors
-    p[4] += visits * 2.0 * 0.0;
-  }
-  for (int l = C.L; l >= 1; --l) {
-    const Level& V = *C.lv[l];
-    const double visits = std::pow(double(q), C.L - l);
-    (void)V;
-    p[4] += visits * 0.0;
+    // B_P = 12 nnz(P) + 16 n_l, for P and for P^T
+    p[4] += visits * 2.0 * (12.0 * V.p_nnz + 16.0 * V.n);
   }
   p[5] = std::pow(double(q), C.L) * 8.0 * double(C.n0) * C.n0;
   double tot = 0;
@@ -1159,6 +1205,96 @@ double hpmg_time_apply(hpmg_ctx* ctx, int reps, double* phase_ms) {
 }
 
 int hpmg_kernel_launches_per_apply(const hpmg_ctx* ctx) { return ctx->launches_per_apply; }
+
+/// Event-instrumented V-cycle (no graph): out[2l], out[2l+1] = pre/post part
+/// of level l (l = 1..L) in ms, out[0] = coarse solve, out[2(L+1)..+2] = head
+/// pre-sweep, residual+embed, post-sweep. Returns the number of entries.
+int hpmg_profile_levels(hpmg_ctx* ctx, int reps, double* out) {
+  int nout = 0;
+  guarded(ctx, [&] {
+    hpmg_ctx& C = *ctx;
+    const int L = C.L;
+    nout = 2 * (L + 1) + 3;
+    for (int i = 0; i < nout; ++i) out[i] = 0;
+    std::vector<cudaEvent_t> ev(2 * (L + 1) + 8);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    auto el = [&](int a, int b) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[a], ev[b]);
+      return double(ms);
+    };
+    for (int r = 0; r < reps; ++r) {
+      // walk down: pre parts, record an event after each level's pre part
+      const double* b = C.opt.k > 0 ? C.lv[L]->b : C.kr;
+      double* x = C.opt.k > 0 ? C.lv[L]->x : C.kz;
+      int e = 0;
+      CK(cudaEventRecord(ev[e++], C.s));  // 0
+      if (C.opt.k > 0) {
+        Level& H = *C.head;
+        dev::fill(C.kz, 0.0, H.n, C.s);
+        smooth(C, H, C.kz, C.kr, false);
+        CK(cudaEventRecord(ev[e++], C.s));  // 1
+        dev::inject_residual(H.A, C.kz, C.kr, C.lv[L]->b, C.s);
+        CK(cudaEventRecord(ev[e++], C.s));  // 2
+      }
+      const int ebase = e;
+      std::vector<const double*> bs(L + 1);
+      std::vector<double*> xs(L + 1);
+      bs[L] = b;
+      xs[L] = x;
+      for (int l = L; l >= 1; --l) {
+        Level& V = *C.lv[l];
+        Level& W = *C.lv[l - 1];
+        const int nw = int(V.wave_ptr.size()) - 1;
+        if (dev::small_level_fits(V.nb, V.P.n, nw)) {
+          dev::small_pre(V.A, V.P, V.d_wave_ptr, nw, V.steps, V.PT, bs[l], xs[l], W.b, C.s);
+        } else {
+          dev::fill(xs[l], 0.0, V.n, C.s);
+          smooth(C, V, xs[l], bs[l], false);
+          dev::spmv(V.A, xs[l], bs[l], V.r, 1, nullptr, nullptr, C.s);
+          dev::restrict_(V.PT, V.r, W.b, C.s);
+        }
+        bs[l - 1] = W.b;
+        xs[l - 1] = W.x;
+        CK(cudaEventRecord(ev[e++], C.s));
+      }
+      dev::dense_gemv(C.n0, C.coarse_inv, bs[0], xs[0], C.gemv_work, C.s);
+      CK(cudaEventRecord(ev[e++], C.s));
+      for (int l = 1; l <= L; ++l) {
+        Level& V = *C.lv[l];
+        Level& W = *C.lv[l - 1];
+        const int nw = int(V.wave_ptr.size()) - 1;
+        if (dev::small_level_fits(V.nb, V.P.n, nw)) {
+          dev::small_post(V.A, V.P, V.d_wave_ptr, nw, V.steps, V.Pm, W.x, bs[l], xs[l], C.s);
+        } else {
+          dev::prolong_add(V.Pm, W.x, xs[l], C.s);
+          smooth(C, V, xs[l], bs[l], true);
+        }
+        CK(cudaEventRecord(ev[e++], C.s));
+      }
+      if (C.opt.k > 0) {
+        Level& H = *C.head;
+        dev::embed_add(H.nb, H.bs, C.lv[L]->x, C.kz, C.s);
+        smooth(C, H, C.kz, C.kr, true);
+        CK(cudaEventRecord(ev[e++], C.s));
+      }
+      CK(cudaEventSynchronize(ev[e - 1]));
+      // pre part of level l: between consecutive events going down
+      int idx = ebase;
+      for (int l = L; l >= 1; --l, ++idx) out[2 * l] += el(idx - 1, idx) / reps;
+      out[0] += el(idx - 1, idx) / reps;  // coarse
+      ++idx;
+      for (int l = 1; l <= L; ++l, ++idx) out[2 * l + 1] += el(idx - 1, idx) / reps;
+      if (C.opt.k > 0) {
+        out[2 * (L + 1)] += el(0, 1) / reps;
+        out[2 * (L + 1) + 1] += el(1, 2) / reps;
+        out[2 * (L + 1) + 2] += el(idx - 1, idx) / reps;
+      }
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+  });
+  return nout;
+}
 
 double hpmg_setup_seconds(const hpmg_ctx* ctx, double* parts) {
   if (parts)

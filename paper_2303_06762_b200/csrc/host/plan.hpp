@@ -75,13 +75,17 @@ struct LevelPlan {
   int npatch = 0, max_patch_f = 0;
   std::vector<int> patch_nf;          // facets per patch
   std::vector<int> patch_fac;         // [npatch][kMaxPatchF] block ids, ascending facet id
-  std::vector<int64_t> inv_off;       // offset of each patch inverse ((nf*bs)^2 doubles)
-  int64_t inv_total = 0;
+  std::vector<int64_t> inv_off;       // offset of each patch inverse (see set_inverse_layout)
+  int64_t inv_total = 0;              // doubles stored
+  int64_t inv_full_total = 0;         // sum np^2 (reference storage accounting)
+  bool packed = true;
   std::vector<int> wave_ptr, wave_patch;  // forward wave order
   std::vector<int> facet_patches;     // [nb][2] the two patches holding a block, ascending
   int nwaves() const { return int(wave_ptr.size()) - 1; }
   int64_t n() const { return int64_t(nb) * bs; }
 };
+
+inline void set_inverse_layout(LevelPlan& L, bool packed);
 
 /// Free blocks, ELL pattern, gather lists, patches and waves for one level.
 inline LevelPlan make_level(const TriMesh& m, int k) {
@@ -170,8 +174,6 @@ inline LevelPlan make_level(const TriMesh& m, int k) {
     L.patch_nf.push_back(int(blocks.size()));
     L.max_patch_f = std::max(L.max_patch_f, int(blocks.size()));
     for (int q = 0; q < kMaxPatchF; ++q) L.patch_fac.push_back(q < int(blocks.size()) ? blocks[q] : -1);
-    L.inv_off.push_back(L.inv_total);
-    L.inv_total += int64_t(blocks.size() * L.bs) * int64_t(blocks.size() * L.bs);
     for (int b : blocks) {
       int* fp = &L.facet_patches[size_t(b) * 2];
       if (fp[0] < 0) fp[0] = p;
@@ -204,7 +206,40 @@ inline LevelPlan make_level(const TriMesh& m, int k) {
     for (int p : w) L.wave_patch.push_back(p);
     L.wave_ptr.push_back(int(L.wave_patch.size()));
   }
+  // Renumber patches in wave order so that a wave is a contiguous patch
+  // range on the device (no wave -> patch indirection in the sweep kernels).
+  // facet_patches keeps the reference's ascending-vertex order of the two
+  // patches of a facet (the additive smoother sums in that order).
+  std::vector<int> newid(L.npatch);
+  for (int q = 0; q < L.npatch; ++q) newid[L.wave_patch[q]] = q;
+  std::vector<int> nf2(L.npatch), fac2(L.patch_fac.size());
+  for (int p = 0; p < L.npatch; ++p) {
+    nf2[newid[p]] = L.patch_nf[p];
+    for (int q = 0; q < kMaxPatchF; ++q) fac2[size_t(newid[p]) * kMaxPatchF + q] = L.patch_fac[size_t(p) * kMaxPatchF + q];
+  }
+  L.patch_nf.swap(nf2);
+  L.patch_fac.swap(fac2);
+  for (auto& fp : L.facet_patches)
+    if (fp >= 0) fp = newid[fp];
+  for (int q = 0; q < L.npatch; ++q) L.wave_patch[q] = q;
+  set_inverse_layout(L, true);
   return L;
+}
+
+/// Offsets of the per-patch explicit inverses: packed lower triangle by
+/// columns (np(np+1)/2 doubles) for symmetric operators, full column-major
+/// (np^2) otherwise.
+inline void set_inverse_layout(LevelPlan& L, bool packed) {
+  L.packed = packed;
+  L.inv_off.assign(L.npatch, 0);
+  L.inv_total = 0;
+  L.inv_full_total = 0;
+  for (int p = 0; p < L.npatch; ++p) {
+    const int64_t np = int64_t(L.patch_nf[p]) * L.bs;
+    L.inv_off[p] = L.inv_total;
+    L.inv_total += packed ? ((np * (np + 1) / 2 + 1) & ~int64_t(1)) : np * np;  // even: 16-byte TMA rows
+    L.inv_full_total += np * np;
+  }
 }
 
 }  // namespace host

@@ -8,6 +8,7 @@
 // (reference tests/test_multigrid.cpp:109-119 asks for that).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -259,6 +260,7 @@ __global__ void k_embed_add(int nb, int bs, const double* __restrict__ e, double
 template <int BS>
 __global__ void k_patch_inverse(Bsr A, Patches P) {
   extern __shared__ double aug[];
+  const bool packed = P.packed != 0;
   __shared__ int fac[kMaxPatchF];
   __shared__ int piv_row;
   const int p = blockIdx.x;
@@ -320,9 +322,101 @@ __global__ void k_patch_inverse(Bsr A, Patches P) {
     __syncthreads();
   }
   double* out = P.inv + P.off[p];
-  for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
-    const int c = e / np, r = e % np;  // column-major: (r, c) at c*np + r
-    out[e] = aug[r * w + np + c];
+  if (packed) {
+    // symmetric operator: symmetrised inverse, lower triangle packed by columns
+    // (column c holds rows c..np-1 at c*np - c(c-1)/2)
+    for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
+      const int c = e / np, r = e % np;
+      if (r < c) continue;
+      out[c * np - c * (c - 1) / 2 + (r - c)] = 0.5 * (aug[r * w + np + c] + aug[c * w + np + r]);
+    }
+  } else {
+    for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
+      const int c = e / np, r = e % np;  // column-major: (r, c) at c*np + r
+      out[e] = aug[r * w + np + c];
+    }
+  }
+}
+
+/// Symmetric multiplicative wave, several patches per CTA (TP threads each).
+/// Latency structure: one dependent round for the patch metadata, then every
+/// independent load of the patch (its packed inverse, U per thread, and its
+/// A rows) is issued back to back; the x gathers are the only second round.
+/// The CTA also bulk-prefetches its slice of the NEXT wave's inverses into
+/// L2 (they are contiguous because patches are numbered in wave order).
+template <int BS, int TP, int U>
+__global__ void __launch_bounds__(128) k_gs_wave_sym(Bsr A, Patches P, int p0, int p1, int pk_max,
+                                                     const double* __restrict__ b, double* __restrict__ x,
+                                                     const char* pf_ptr, unsigned pf_bytes) {
+  extern __shared__ double sm[];
+  const int ppc = blockDim.x / TP, lp = threadIdx.x / TP, t = threadIdx.x % TP;
+  double* sp = sm + size_t(lp) * pk_max;
+  double* r = sm + size_t(ppc) * pk_max + lp * TP;
+  if (pf_bytes && threadIdx.x == 0) {
+    const unsigned chunk = ((pf_bytes / gridDim.x) + 15u) & ~15u;
+    const unsigned beg = chunk * blockIdx.x;
+    if (beg < pf_bytes) {
+      const unsigned len = min(chunk, pf_bytes - beg) & ~15u;
+      if (len) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf_ptr + beg), "r"(len) : "memory");
+    }
+  }
+  const int p = p0 + blockIdx.x * ppc + lp;
+  int np = 0, f = 0;
+  if (p < p1) {
+    np = P.nf[p] * BS;
+    const int64_t off = P.off[p];
+    if (t < np) f = P.fac[p * kMaxPatchF + t / BS];
+    const double* src = P.inv + off;
+    const int tot = np * (np + 1) / 2;
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = t + u * TP;
+      v[u] = k < tot ? __ldg(src + k) : 0.0;
+    }
+    for (int k = t + U * TP; k < tot; k += TP) sp[k] = __ldg(src + k);  // patches above 6 facets
+    double s = 0.0;
+    if (t < np) {
+      const int i = t % BS;
+      s = b[size_t(f) * BS + i];
+      int cc[kSlots];
+#pragma unroll
+      for (int sl = 0; sl < kSlots; ++sl) cc[sl] = __ldg(&A.cols[f * kSlots + sl]);
+#pragma unroll
+      for (int sl = 0; sl < kSlots; ++sl) {
+        if (cc[sl] < 0) continue;
+        const double2* blk = reinterpret_cast<const double2*>(A.val + (size_t(f * kSlots + sl) * BS + i) * BS);
+        const double2* xc = reinterpret_cast<const double2*>(x + size_t(cc[sl]) * BS);
+#pragma unroll
+        for (int j = 0; j < BS / 2; ++j) {
+          const double2 a = __ldg(blk + j), xv = xc[j];
+          s = fma(-a.x, xv.x, s);
+          s = fma(-a.y, xv.y, s);
+        }
+      }
+      r[t] = s;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = t + u * TP;
+      if (k < tot) sp[k] = v[u];
+    }
+  }
+  __syncthreads();
+  if (t < np) {
+    // S(t, j): j >= t in column t, j < t in column j (packed lower by columns)
+    const int ct = t * np - t * (t - 1) / 2 - t;
+    double d0 = 0.0, d1 = 0.0;
+    int j = 0;
+    for (; j + 1 < np; j += 2) {
+      const int i0 = j >= t ? ct + j : j * np - j * (j - 1) / 2 + (t - j);
+      const int j1 = j + 1;
+      const int i1 = j1 >= t ? ct + j1 : j1 * np - j1 * (j1 - 1) / 2 + (t - j1);
+      d0 = fma(sp[i0], r[j], d0);
+      d1 = fma(sp[i1], r[j1], d1);
+    }
+    if (j < np) d0 = fma(sp[j >= t ? ct + j : j * np - j * (j - 1) / 2 + (t - j)], r[j], d0);
+    x[size_t(f) * BS + t % BS] += d0 + d1;
   }
 }
 
@@ -384,7 +478,13 @@ __global__ void k_jacobi_patch(Patches P, int max_np, const double* __restrict__
   const double* inv = P.inv + P.off[p];
   for (int t = threadIdx.x; t < np; t += blockDim.x) {
     double d = 0.0;
-    for (int j = 0; j < np; ++j) d = fma(__ldg(inv + size_t(j) * np + t), r[j], d);
+    if (P.packed) {
+      const int ct = t * np - t * (t - 1) / 2 - t;
+      for (int j = 0; j < np; ++j)
+        d = fma(__ldg(inv + (j >= t ? ct + j : j * np - j * (j - 1) / 2 + (t - j))), r[j], d);
+    } else {
+      for (int j = 0; j < np; ++j) d = fma(__ldg(inv + size_t(j) * np + t), r[j], d);
+    }
     dbuf[size_t(p) * max_np + t] = d;
   }
 }
@@ -440,16 +540,29 @@ __global__ void k_restrict(BlockCsr PT, const double* __restrict__ r, double* __
 
 /// x = Inv b for the dense coarse inverse (column-major), 2-stage over
 /// column chunks for parallelism: work[chunk][n] partials then a fixed-order sum.
-constexpr int kGemvChunk = 128;
+constexpr int kGemvChunk = 64;
 __global__ void k_gemv_partial(int n, const double* __restrict__ inv, const double* __restrict__ b,
                                double* __restrict__ work) {
+  __shared__ double sb[kGemvChunk];
   const int chunk = blockIdx.y;
   const int j0 = chunk * kGemvChunk, j1 = min(n, j0 + kGemvChunk);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int j = j0; j < j1; ++j) s = fma(__ldg(inv + size_t(j) * n + i), __ldg(b + j), s);
-    work[size_t(chunk) * n + i] = s;
+  for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) sb[j - j0] = b[j];
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  // eight independent accumulators keep 8 column loads in flight per thread
+  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const double* col = inv + size_t(j0) * n + i;
+  int j = j0;
+  for (; j + 8 <= j1; j += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(col + size_t(j - j0 + u) * n);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s[u] = fma(v[u], sb[j - j0 + u], s[u]);
   }
+  for (; j < j1; ++j) s[0] = fma(__ldg(col + size_t(j - j0) * n), sb[j - j0], s[0]);
+  work[size_t(chunk) * n + i] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
 }
 __global__ void k_gemv_sum(int n, int chunks, const double* __restrict__ work, double* __restrict__ x) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -677,13 +790,35 @@ void patch_inverse(const Bsr& A, const Patches& P, int max_nf, cudaStream_t s) {
 }
 
 void gs_wave(const Bsr& A, const Patches& P, int w0, int w1, const double* b, double* x, int transposed_inv,
-             int max_nf, cudaStream_t s) {
+             int max_nf, cudaStream_t s, const void* prefetch, size_t prefetch_len) {
   if (w1 <= w0) return;
-  by_bs(A.bs, [&](auto BS) {
-    const int np = max_nf * BS;
-    const int threads = ((np + 31) / 32) * 32;
-    k_gs_wave<BS><<<w1 - w0, threads, 0, s>>>(A, P, w0, b, x, transposed_inv);
-  });
+  const char* prefetch_ptr = static_cast<const char*>(prefetch);
+  unsigned prefetch_bytes = unsigned(std::min<size_t>(prefetch_len, 0xFFFFFFF0u)) & ~15u;
+  if (P.packed) {
+    if (transposed_inv) throw std::runtime_error("packed (symmetric) inverses have no transposed sweep");
+    by_bs(A.bs, [&](auto BS) {
+      constexpr int TP = BS == 2 ? 16 : (BS == 4 ? 32 : 64);
+      constexpr int NP6 = 6 * BS;                               // interior vertex: 6 facets
+      constexpr int U = (NP6 * (NP6 + 1) / 2 + TP - 1) / TP;   // staged loads per thread
+      const int npmax = max_nf * BS;
+      if (npmax > TP) throw std::runtime_error("vertex patch too large for the sweep kernel");
+      const int ppc = 128 / TP, pk = npmax * (npmax + 1) / 2;
+      const size_t smem = sizeof(double) * (size_t(ppc) * pk + 128);
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_gs_wave_sym<BS, TP, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+      }
+      const int nblk = (w1 - w0 + ppc - 1) / ppc;
+      k_gs_wave_sym<BS, TP, U><<<nblk, 128, smem, s>>>(A, P, w0, w1, pk, b, x, prefetch_ptr, prefetch_bytes);
+    });
+  } else {
+    by_bs(A.bs, [&](auto BS) {
+      const int np = max_nf * BS;
+      const int threads = ((np + 31) / 32) * 32;
+      k_gs_wave<BS><<<w1 - w0, threads, 0, s>>>(A, P, w0, b, x, transposed_inv);
+    });
+  }
   HPMG_LAUNCH_CHECK();
 }
 

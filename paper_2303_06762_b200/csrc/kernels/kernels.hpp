@@ -32,6 +32,7 @@ struct Patches {
   double* inv = nullptr;
   int* wave = nullptr;      // patch ids grouped by wave
   int* fpatch = nullptr;    // [nb][2] patches holding block f (ascending)
+  int packed = 1;           // 1: symmetric, lower triangle packed by columns
 };
 
 /// 2x2-block CSR (prolongation P: fine rows; PT: coarse rows).
@@ -70,11 +71,36 @@ void patch_inverse(const Bsr& A, const Patches& P, int max_nf, cudaStream_t s);
 /// One wave of the multiplicative sweep: x_p += Inv_p (b - A x)_p for the
 /// patches wave[w0..w1). transposed_inv selects (Inv_p)^T (nonsymmetric backward).
 void gs_wave(const Bsr& A, const Patches& P, int w0, int w1, const double* b, double* x, int transposed_inv,
-             int max_nf, cudaStream_t s);
+             int max_nf, cudaStream_t s, const void* prefetch = nullptr, size_t prefetch_len = 0);
+/// Fixed-stride per-patch records (sweep_rec.cu): packed inverse, A row
+/// blocks of the patch facets and int32 meta (nf, facets, block columns).
+struct PatchRecords {
+  double* rec = nullptr;
+  int bs = 2, max_nf = 0;
+  int stride = 0, a_off = 0, meta_off = 0;  // in doubles
+};
+PatchRecords record_layout(int bs, int max_nf);
+void build_records(const Bsr& A, const Patches& P, PatchRecords& R, cudaStream_t s);
+/// One symmetric wave over the patch records [w0, w1) (one TMA per CTA).
+void gs_wave_rec(const PatchRecords& R, int w0, int w1, const double* b, double* x, cudaStream_t s);
+
+/// Same wave with the TMA-fed persistent kernel (sweep_tma.cu); symmetric
+/// (packed) inverses only.
+void gs_wave_tma(const Bsr& A, const Patches& P, int w0, int w1, const double* b, double* x, int max_nf,
+                 cudaStream_t s);
 /// Additive sweep pieces: d_p = Inv_p r_p for all patches; x += damping * sum_p d_p.
 void jacobi_patch(const Bsr& A, const Patches& P, const double* r, double* d, int max_nf, cudaStream_t s);
 void jacobi_combine(int nb, int bs, const Patches& P, const double* d, int max_nf, double damping, double* x,
                     cudaStream_t s);
+
+/// Small lowest-order levels (small_levels.cu, symmetric): one CTA runs
+/// x = 0, all pre-smoothing waves, r = b - A x and rc = P^T r (small_pre),
+/// resp. x += P e and all post-smoothing waves (small_post).
+bool small_level_fits(int nb, int npatch, int nwaves);
+void small_pre(const Bsr& A, const Patches& P, const int* wave_ptr, int nwaves, int sweeps, const BlockCsr& PT,
+               const double* b, double* x, double* rc, cudaStream_t s);
+void small_post(const Bsr& A, const Patches& P, const int* wave_ptr, int nwaves, int sweeps, const BlockCsr& Pm,
+                const double* e, const double* b, double* x, cudaStream_t s);
 
 void prolong_add(const BlockCsr& P, const double* e, double* x, cudaStream_t s);
 void restrict_(const BlockCsr& PT, const double* r, double* rc, cudaStream_t s);

@@ -1,0 +1,234 @@
+// Patch-record multiplicative sweep (symmetric operators): the dominant
+// kernel of the hp-MG V-cycle (reference
+// inc/smoother.hpp:53-67, 83-94).
+//
+// Every vertex patch owns one fixed-stride record in HBM, built once at setup:
+//   [ packed symmetric patch inverse (pk_max doubles)
+//   | the nf A row blocks of its facets (nf x 5 x bs^2 doubles)
+//   | int32 meta: nf, facet ids, the 5 block columns of each facet ]
+// A CTA therefore needs no dependent index loads: one elected thread issues a
+// single TMA bulk copy (cp.async.bulk, L2 evict-first so the streamed records
+// do not evict x and b) of the records of its patch group, addressed by the
+// patch id alone, onto an mbarrier. The threads then gather the x blocks of
+// the patch neighbourhood (the only dependent round, L2-resident), form the
+// residual rows from shared memory and apply the packed inverse.
+// The A rows are stored twice (each facet belongs to two patches): 0.5 GB
+// extra at k=3 on 256^2, traded for one latency round per patch.
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "kernels.hpp"
+
+namespace hpmg {
+namespace dev {
+
+namespace {
+
+__device__ __forceinline__ unsigned su32(const void* p) { return unsigned(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void bar_init(unsigned long long* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bar_wait(unsigned long long* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+      "@P1 bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(su32(bar))
+      : "memory");
+}
+/// one TMA bulk copy global -> shared with an L2 evict-first policy
+__device__ __forceinline__ void tma_stream(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar)), "l"(pol)
+      : "memory");
+}
+
+/// Records of G consecutive patches per CTA, TP threads per patch.
+template <int BS, int TP, int G>
+__global__ void __launch_bounds__(G* TP) k_sweep_rec(PatchRecords R, int p0, int p1, const double* __restrict__ b,
+                                                     double* __restrict__ x) {
+  constexpr int kRow = kSlots * BS * BS;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double* srec = reinterpret_cast<double*>(smraw);  // G * stride
+  double* sx = srec + size_t(G) * R.stride;          // G * max_nf * kSlots * BS
+  double* r = sx + G * R.max_nf * kSlots * BS;       // G * TP
+  __shared__ unsigned long long bar;
+  const int lp = threadIdx.x / TP, t = threadIdx.x % TP;
+  const int q0 = p0 + blockIdx.x * G;
+  const int ng = min(G, p1 - q0);
+  if (threadIdx.x == 0) {
+    bar_init(&bar);
+    tma_stream(srec, R.rec + size_t(q0) * R.stride, unsigned(ng) * unsigned(R.stride) * 8u, &bar);
+  }
+  // Programmatic dependent launch: the records do not depend on the previous
+  // wave, so the copy above may overlap its tail; x and b may not be touched
+  // before the previous grid has completed.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  __syncthreads();
+  bar_wait(&bar);
+  const double* rec = srec + size_t(lp) * R.stride;
+  const int* meta = reinterpret_cast<const int*>(rec + R.meta_off);
+  const int nf = lp < ng ? meta[0] : 0, np = nf * BS;
+  const int* fac = meta + 1;
+  const int* cols = meta + 1 + R.max_nf;
+  double* xs = sx + lp * R.max_nf * kSlots * BS;
+  for (int e = t; e < nf * kSlots * BS; e += TP) {
+    const int c = cols[e / BS];
+    xs[e] = c >= 0 ? x[size_t(c) * BS + e % BS] : 0.0;
+  }
+  double bv = 0.0;
+  if (t < np) bv = b[size_t(fac[t / BS]) * BS + t % BS];
+  __syncthreads();
+  if (t < np) {
+    const int lf = t / BS, i = t % BS;
+    const double* arow = rec + R.a_off + lf * kRow + i * BS;
+    const double* xr = xs + lf * kSlots * BS;
+    double a0 = bv, a1 = 0.0;
+#pragma unroll
+    for (int sl = 0; sl < kSlots; ++sl)
+#pragma unroll
+      for (int jj = 0; jj < BS; jj += 2) {
+        const int j0 = (jj + i) % BS, j1 = (jj + 1 + i) % BS;  // rotated: rows of a block hit distinct banks
+        a0 = fma(-arow[sl * BS * BS + j0], xr[sl * BS + j0], a0);
+        a1 = fma(-arow[sl * BS * BS + j1], xr[sl * BS + j1], a1);
+      }
+    r[threadIdx.x] = a0 + a1;
+  }
+  __syncthreads();
+  if (t < np) {
+    const double* S = rec;  // packed lower triangle by columns
+    const double* rr = r + lp * TP;
+    const int ct = t * np - t * (t - 1) / 2 - t;
+    double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+    int j = 0;
+    for (; j + 3 < np; j += 4) {
+      double s4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int ju = j + u;
+        s4[u] = S[ju >= t ? ct + ju : ju * np - ju * (ju - 1) / 2 + (t - ju)];
+      }
+      d0 = fma(s4[0], rr[j], d0);
+      d1 = fma(s4[1], rr[j + 1], d1);
+      d2 = fma(s4[2], rr[j + 2], d2);
+      d3 = fma(s4[3], rr[j + 3], d3);
+    }
+    for (; j < np; ++j) d0 = fma(S[j >= t ? ct + j : j * np - j * (j - 1) / 2 + (t - j)], rr[j], d0);
+    x[size_t(fac[t / BS]) * BS + t % BS] += (d0 + d1) + (d2 + d3);
+  }
+}
+
+/// Builds the records from the packed inverses and the ELL operator.
+__global__ void k_build_records(Bsr A, Patches P, PatchRecords R, int bs) {
+  const int p = blockIdx.x;
+  double* rec = R.rec + size_t(p) * R.stride;
+  const int nf = P.nf[p], np = nf * bs;
+  const int pk = np * (np + 1) / 2;
+  const double* inv = P.inv + P.off[p];
+  for (int k = threadIdx.x; k < R.a_off; k += blockDim.x) rec[k] = k < pk ? inv[k] : 0.0;
+  const int row = kSlots * bs * bs;
+  for (int k = threadIdx.x; k < R.max_nf * row; k += blockDim.x) {
+    const int lf = k / row;
+    rec[R.a_off + k] = lf < nf ? A.val[size_t(P.fac[p * kMaxPatchF + lf]) * row + k % row] : 0.0;
+  }
+  int* meta = reinterpret_cast<int*>(rec + R.meta_off);
+  if (threadIdx.x == 0) meta[0] = nf;
+  for (int k = threadIdx.x; k < R.max_nf; k += blockDim.x) meta[1 + k] = k < nf ? P.fac[p * kMaxPatchF + k] : -1;
+  for (int k = threadIdx.x; k < R.max_nf * kSlots; k += blockDim.x) {
+    const int lf = k / kSlots;
+    meta[1 + R.max_nf + k] = lf < nf ? A.cols[P.fac[p * kMaxPatchF + lf] * kSlots + k % kSlots] : -1;
+  }
+}
+
+template <int BS>
+struct RecCfg;
+template <>
+struct RecCfg<2> {
+  static constexpr int TP = 16, G = 8;
+};
+template <>
+struct RecCfg<4> {
+  static constexpr int TP = 32, G = 2;
+};
+template <>
+struct RecCfg<6> {
+  static constexpr int TP = 64, G = 1;
+};
+template <>
+struct RecCfg<8> {
+  static constexpr int TP = 64, G = 1;
+};
+
+template <int BS>
+void launch_rec(const PatchRecords& R, int w0, int w1, const double* b, double* x, cudaStream_t s) {
+  constexpr int TP = RecCfg<BS>::TP, G = RecCfg<BS>::G;
+  if (R.max_nf * BS > TP) throw std::runtime_error("vertex patch too large for the record sweep");
+  const size_t smem = sizeof(double) * (size_t(G) * R.stride + size_t(G) * R.max_nf * kSlots * BS + G * TP);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sweep_rec<BS, TP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((w1 - w0 + G - 1) / G);
+  cfg.blockDim = dim3(G * TP);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr_pdl[1];
+  attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr_pdl;
+  cfg.numAttrs = 1;
+  cudaError_t err = cudaLaunchKernelEx(&cfg, k_sweep_rec<BS, TP, G>, R, w0, w1, b, x);
+  if (err == cudaSuccess) err = cudaGetLastError();
+  if (err != cudaSuccess) throw std::runtime_error(std::string("CUDA launch (sweep_rec): ") + cudaGetErrorString(err));
+}
+
+}  // namespace
+
+PatchRecords record_layout(int bs, int max_nf) {
+  PatchRecords R;
+  R.bs = bs;
+  R.max_nf = max_nf;
+  const int npmax = max_nf * bs;
+  R.a_off = ((npmax * (npmax + 1) / 2) + 1) & ~1;
+  R.meta_off = R.a_off + max_nf * kSlots * bs * bs;
+  const int meta_ints = 1 + max_nf + max_nf * kSlots;
+  R.stride = (R.meta_off + (meta_ints + 1) / 2 + 1) & ~1;  // even => 16-byte aligned records
+  return R;
+}
+
+void build_records(const Bsr& A, const Patches& P, PatchRecords& R, cudaStream_t s) {
+  if (P.n == 0) return;
+  k_build_records<<<P.n, 128, 0, s>>>(A, P, R, R.bs);
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) throw std::runtime_error(std::string("CUDA launch (build_records): ") + cudaGetErrorString(err));
+}
+
+void gs_wave_rec(const PatchRecords& R, int w0, int w1, const double* b, double* x, cudaStream_t s) {
+  if (w1 <= w0) return;
+  switch (R.bs) {
+    case 2: launch_rec<2>(R, w0, w1, b, x, s); break;
+    case 4: launch_rec<4>(R, w0, w1, b, x, s); break;
+    case 6: launch_rec<6>(R, w0, w1, b, x, s); break;
+    case 8: launch_rec<8>(R, w0, w1, b, x, s); break;
+    default: throw std::runtime_error("unsupported block size");
+  }
+}
+
+}  // namespace dev
+}  // namespace hpmg
