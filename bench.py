@@ -190,7 +190,11 @@ def run_hpmg(args, rank, world, local, dist):
                        "l2": "no flush needed: V-cycle streams %.2f GB per call (> 126 MB L2)" % (vbytes / 1e9)},
             "e2e": {"value": max(3, args.steps // 2) / (ms_e2e * 1e-3) * world, "unit": "V-cycles/s",
                     "h2d_bytes_per_step": int(8 * n), "d2h_bytes_per_step": int(8 * n)},
-            "roofline": {"bound": "hbm", "kernel": "k_gs_wave<8> (order-k head patch sweeps)",
+            "roofline": {"bound": "hbm",
+                         "kernel": "k_sweep_rec<8,64,1> (order-k head patch sweeps, TMA patch records)",
+                         "bytes_note": "achieved = reference-storage algorithmic bytes (full np^2 patch factors, "
+                                       "A rows twice, x/b) / measured head-sweep time; physical traffic is lower "
+                                       "(packed symmetric inverses)",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": (achieved / hbm) if achieved else None, "traffic": None,
                          "peak_source": src, "algorithmic_bytes_per_vcycle": vbytes,

@@ -178,6 +178,15 @@ double hpmg_setup_seconds(const hpmg_ctx* ctx, double* parts);
 void hpmg_seeded_load(int n, unsigned seed, double lo, double hi, double* out);
 int hpmg_structured_to_elements(const hpmg_ctx* ctx, int n, const double* structured, double* per_element);
 
+/* Host-only (no GPU needed): builds the hierarchy and the level-`level` plan
+ * (-1: order-k head on the finest mesh) and checks the wave schedule.
+ * out[0] free DOFs, out[1] patches, out[2] waves, out[3] 1 if every free DOF
+ * lies in exactly two patches (smoother.hpp:13-28), out[4] 1 if no two
+ * patches of a wave share a facet or an operator coupling, out[5] 1 if the
+ * waves respect every ascending-order dependency, out[6] max patch facets,
+ * out[7..7+waves) wave sizes (up to out_len). Returns entries written. */
+int hpmg_plan_check(const hpmg_mesh_desc* mesh, int k, int level, int64_t* out, int out_len);
+
 /* Base meshes of the reference (mesh.hpp:220-279): fills a descriptor whose
  * arrays stay valid until the next call from the same thread. */
 int hpmg_unit_square_mesh(int n, int levels, hpmg_mesh_desc* out);

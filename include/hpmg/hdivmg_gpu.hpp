@@ -1,0 +1,191 @@
+// Drop-in C++ adapter: the reference hdivmg operator interface on top of the
+// hpmg C ABI. Compile it inside the reference tree (it includes the
+// reference headers, i.e. Eigen); swap
+//     hdivmg::MGPreconditioner B(hier, k, bc, opt, inv_eps, mg);
+//     auto sol = hdivmg::uzawa_solve(B);
+// for
+//     hpmg::MGPreconditioner B(hier, k, bc, opt, inv_eps, mg);
+//     auto sol = hpmg::uzawa_solve(B);
+// Signatures and semantics follow proj/include/hdivmg/multigrid.hpp:43-146,
+// krylov.hpp:30-144 and uzawa.hpp:23-91. Setup errors are rethrown as the
+// reference's exception types; Krylov breakdown stays in-band.
+#pragma once
+
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "hdivmg/multigrid.hpp"
+#include "hdivmg/uzawa.hpp"
+#include "hpmg/capi.h"
+
+namespace hpmg {
+
+using hdivmg::Index;
+using hdivmg::Real;
+using hdivmg::Vec;
+using hdivmg::Vec2;
+
+namespace detail {
+inline void check(int rc, const hpmg_ctx* ctx = nullptr) {
+  if (rc == HPMG_OK) return;
+  std::string msg = ctx ? hpmg_ctx_error(ctx) : hpmg_last_error();
+  if (rc == HPMG_ERR_ARG) throw std::invalid_argument(msg);
+  if (rc == HPMG_ERR_LOGIC) throw std::logic_error(msg);
+  throw std::runtime_error(msg);
+}
+inline void field_trampoline(double x, double y, double* out, void* user) {
+  const auto& f = *static_cast<const std::function<Vec2(const Vec2&)>*>(user);
+  Vec2 v = f(Vec2(x, y));
+  out[0] = v.x();
+  out[1] = v.y();
+}
+}  // namespace detail
+
+class MGPreconditioner {
+ public:
+  MGPreconditioner(const hdivmg::MeshHierarchy& hier, int k, const hdivmg::VelocityBC& bc,
+                   const hdivmg::AssemblyOptions& fine_opt, Real inv_eps, const hdivmg::MGOptions& mg)
+      : bc_(bc.g), load_(fine_opt.load) {
+    const hdivmg::Mesh& base = hier.levels.front();
+    for (const auto& v : base.vertices) {
+      xy_.push_back(v.x());
+      xy_.push_back(v.y());
+    }
+    for (const auto& e : base.elements)
+      for (int i = 0; i < 3; ++i) el_.push_back(e.v[i]);
+    for (const auto& f : base.facets)
+      if (f.tag == hdivmg::bc::kOutflow) {
+        tags_.push_back(f.a);
+        tags_.push_back(f.b);
+        tags_.push_back(HPMG_TAG_OUTFLOW);
+      }
+    hpmg_mesh_desc md{base.nv(), xy_.data(), base.ne(), el_.data(), int(tags_.size() / 3), tags_.data(),
+                      int(hier.levels.size())};
+    hpmg_options o{k, fine_opt.nu, fine_opt.beta, fine_opt.mass_coef, inv_eps,
+                   mg.cycle == hdivmg::CycleKind::V ? HPMG_CYCLE_V
+                   : mg.cycle == hdivmg::CycleKind::W ? HPMG_CYCLE_W
+                                                      : HPMG_CYCLE_VARIABLE_V,
+                   mg.smoother == hdivmg::SmootherKind::Multiplicative ? HPMG_SMOOTH_MULTIPLICATIVE
+                                                                       : HPMG_SMOOTH_ADDITIVE,
+                   mg.smooth_steps, mg.jacobi_damping};
+    hpmg_problem p{};
+    if (bc_) {
+      p.bc = &detail::field_trampoline;
+      p.bc_user = &bc_;
+    }
+    if (load_) {
+      p.load = &detail::field_trampoline;
+      p.load_user = &load_;
+    }
+    if (fine_opt.advection) {
+      wind_c_ = fine_opt.advection->compound;
+      wind_i_ = fine_opt.advection->interior;
+      p.wind_compound = wind_c_.data();
+      p.wind_interior = wind_i_.data();
+      p.newton = fine_opt.newton;
+    }
+    hpmg_ctx* c = nullptr;
+    detail::check(hpmg_create(&c, &md, &o, &p));
+    ctx_.reset(c);
+  }
+  MGPreconditioner(const MGPreconditioner&) = delete;
+  MGPreconditioner& operator=(const MGPreconditioner&) = delete;
+
+  /// One cycle, zero initial guess (multigrid.hpp:117-128).
+  Vec apply(const Vec& b) const {
+    Vec z(b.size());
+    detail::check(hpmg_apply(ctx_.get(), b.data(), z.data(), 0), ctx_.get());
+    return z;
+  }
+  hdivmg::LinearOperator as_operator() const {
+    return [this](const Vec& v) { return apply(v); };
+  }
+  /// matrix() * v on the device (uzawa.hpp:42)
+  Vec spmv(const Vec& v) const {
+    Vec y(v.size());
+    detail::check(hpmg_spmv(ctx_.get(), v.data(), y.data(), 0), ctx_.get());
+    return y;
+  }
+  /// host mirror of the finest operator (multigrid.hpp:133)
+  hdivmg::SpMat matrix() const {
+    int64_t nnz = 0;
+    detail::check(hpmg_matrix_csr(ctx_.get(), -1, &nnz, nullptr, nullptr, nullptr), ctx_.get());
+    const int64_t n = hpmg_n(ctx_.get());
+    std::vector<int64_t> ptr(n + 1), idx(nnz);
+    std::vector<double> val(nnz);
+    detail::check(hpmg_matrix_csr(ctx_.get(), -1, &nnz, ptr.data(), idx.data(), val.data()), ctx_.get());
+    std::vector<hdivmg::Triplet> t;
+    t.reserve(nnz);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t q = ptr[i]; q < ptr[i + 1]; ++q) t.emplace_back(int(i), int(idx[q]), val[q]);
+    hdivmg::SpMat A(int(n), int(n));
+    A.setFromTriplets(t.begin(), t.end());
+    return A;
+  }
+  Vec rhs() const {
+    Vec r(hpmg_n(ctx_.get()));
+    detail::check(hpmg_rhs(ctx_.get(), r.data(), 0), ctx_.get());
+    return r;
+  }
+  bool symmetric() const { return hpmg_symmetric(ctx_.get()) != 0; }
+  Real penalty() const { return hpmg_penalty(ctx_.get()); }
+  hpmg_ctx* handle() const { return ctx_.get(); }
+
+ private:
+  struct Del {
+    void operator()(hpmg_ctx* c) const { hpmg_destroy(c); }
+  };
+  std::function<Vec2(const Vec2&)> bc_, load_;
+  std::vector<double> xy_, wind_c_, wind_i_;
+  std::vector<int> el_, tags_;
+  std::unique_ptr<hpmg_ctx, Del> ctx_;
+};
+
+/// Device PCG with B.matrix() and B.apply (krylov.hpp:30-73).
+inline hdivmg::SolveStats pcg(const MGPreconditioner& B, const Vec& b, Vec& x, const hdivmg::KrylovOptions& opt = {}) {
+  hpmg_krylov_opts o{opt.rel_tol, opt.abs_tol, opt.max_iterations, 0};
+  hpmg_solve_stats st{};
+  detail::check(hpmg_pcg(B.handle(), b.data(), x.data(), &o, &st, 0), B.handle());
+  hdivmg::SolveStats s;
+  s.iterations = st.iterations;
+  s.converged = st.converged != 0;
+  s.not_applicable = st.not_applicable != 0;
+  s.residual = st.residual;
+  return s;
+}
+
+/// Device right-preconditioned GMRES (krylov.hpp:79-144).
+inline hdivmg::SolveStats gmres(const MGPreconditioner& B, const Vec& b, Vec& x,
+                                const hdivmg::KrylovOptions& opt = {}) {
+  hpmg_krylov_opts o{opt.rel_tol, opt.abs_tol, opt.max_iterations, 0};
+  hpmg_solve_stats st{};
+  detail::check(hpmg_gmres(B.handle(), b.data(), x.data(), &o, &st, 0), B.handle());
+  hdivmg::SolveStats s;
+  s.iterations = st.iterations;
+  s.converged = st.converged != 0;
+  s.not_applicable = st.not_applicable != 0;
+  s.residual = st.residual;
+  return s;
+}
+
+/// Augmented-Lagrangian Uzawa on the device (uzawa.hpp:51-91).
+inline hdivmg::StokesSolution uzawa_solve(const MGPreconditioner& B, const hdivmg::UzawaOptions& opt = {}) {
+  hpmg_uzawa_opts o{opt.outer_iterations, {opt.krylov.rel_tol, opt.krylov.abs_tol, opt.krylov.max_iterations, 0}};
+  hdivmg::StokesSolution sol;
+  sol.velocity.resize(hpmg_n_full(B.handle()));
+  sol.pressure.resize(hpmg_ne(B.handle()));
+  hpmg_uzawa_report rep{};
+  detail::check(hpmg_uzawa(B.handle(), &o, sol.velocity.data(), sol.pressure.data(), &rep), B.handle());
+  for (int i = 0; i < rep.n_outer; ++i) {
+    sol.report.inner_iterations.push_back(rep.inner_iterations[i]);
+    sol.report.divergence_history.push_back(rep.divergence_history[i]);
+  }
+  sol.report.converged = rep.converged != 0;
+  sol.report.not_applicable = rep.not_applicable != 0;
+  sol.report.final_divergence = rep.final_divergence;
+  return sol;
+}
+
+}  // namespace hpmg

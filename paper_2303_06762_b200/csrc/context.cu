@@ -66,6 +66,9 @@ struct Level {
   std::vector<int> wave_ptr;
   int* d_wave_ptr = nullptr;
   dev::PatchRecords rec;
+  bool small = false;  // whole pre/post phase in one CTA (small_levels.cu)
+  int2* d_passes = nullptr;
+  int npass = 0;
   dev::BlockCsr Pm, PT;  // from level l-1 to l (lowest-order levels l >= 1)
   double *x = nullptr, *b = nullptr, *r = nullptr, *y = nullptr, *bw = nullptr, *xw = nullptr, *dbuf = nullptr;
   int steps = 1;
@@ -310,6 +313,16 @@ void build_patch_inverses(hpmg_ctx& C, Level& V) {
     V.rec = dev::record_layout(V.bs, V.max_nf);
     V.rec.rec = dalloc<double>(size_t(V.P.n) * V.rec.stride);
     dev::build_records(V.A, V.P, V.rec, C.s);
+    std::vector<int2> passes;
+    const int pp = dev::small_pass_patches();
+    for (size_t w = 0; w + 1 < V.wave_ptr.size(); ++w)
+      for (int a = V.wave_ptr[w]; a < V.wave_ptr[w + 1]; a += pp)
+        passes.push_back(make_int2(a, std::min(pp, V.wave_ptr[w + 1] - a)));
+    if (V.k == 0 && dev::small_level_fits(V.nb, V.rec.stride, int(passes.size()))) {
+      V.npass = int(passes.size());
+      V.d_passes = dupload(passes, C.s);
+      V.small = true;
+    }
   }
 }
 
@@ -462,14 +475,12 @@ void h_cycle(hpmg_ctx& C, int l, const double* b, double* x) {
   Level& V = *C.lv[l];
   Level& W = *C.lv[l - 1];
   const int q = C.opt.cycle == HPMG_CYCLE_W ? 2 : 1;
-  const int nw = int(V.wave_ptr.size()) - 1;
-  if (dev::small_level_fits(V.nb, V.P.n, nw) && !C.advected && C.opt.smoother == HPMG_SMOOTH_MULTIPLICATIVE &&
-      q == 1) {
+  if (V.small && C.opt.smoother == HPMG_SMOOTH_MULTIPLICATIVE && q == 1) {
     // whole-level sweeps in one persistent CTA (small_levels.cu)
-    dev::small_pre(V.A, V.P, V.d_wave_ptr, nw, V.steps, V.PT, b, x, W.b, C.s);
+    dev::small_pre(V.A, V.rec, V.d_passes, V.npass, V.steps, V.PT, b, x, W.b, C.s);
     count(C);
     h_cycle(C, l - 1, W.b, W.x);
-    dev::small_post(V.A, V.P, V.d_wave_ptr, nw, V.steps, V.Pm, W.x, b, x, C.s);
+    dev::small_post(V.A, V.rec, V.d_passes, V.npass, V.steps, V.Pm, W.x, b, x, C.s);
     count(C);
     return;
   }
@@ -899,7 +910,7 @@ void hpmg_destroy(hpmg_ctx* ctx) {
                     (void*)V->Pm.ptr, (void*)V->Pm.col, (void*)V->Pm.val, (void*)V->PT.ptr, (void*)V->PT.col,
                     (void*)V->PT.val, (void*)V->x, (void*)V->b, (void*)V->r, (void*)V->y, (void*)V->bw, (void*)V->xw,
                     (void*)V->dbuf, (void*)V->geo, (void*)V->row_elems, (void*)V->elem_facets, (void*)V->facet_block,
-                    (void*)V->d_wave_ptr, (void*)V->rec.rec})
+                    (void*)V->d_wave_ptr, (void*)V->rec.rec, (void*)V->d_passes})
       fr(p);
   };
   for (auto& V : ctx->lv) free_level(V.get());
@@ -1245,9 +1256,8 @@ int hpmg_profile_levels(hpmg_ctx* ctx, int reps, double* out) {
       for (int l = L; l >= 1; --l) {
         Level& V = *C.lv[l];
         Level& W = *C.lv[l - 1];
-        const int nw = int(V.wave_ptr.size()) - 1;
-        if (dev::small_level_fits(V.nb, V.P.n, nw)) {
-          dev::small_pre(V.A, V.P, V.d_wave_ptr, nw, V.steps, V.PT, bs[l], xs[l], W.b, C.s);
+        if (V.small) {
+          dev::small_pre(V.A, V.rec, V.d_passes, V.npass, V.steps, V.PT, bs[l], xs[l], W.b, C.s);
         } else {
           dev::fill(xs[l], 0.0, V.n, C.s);
           smooth(C, V, xs[l], bs[l], false);
@@ -1263,9 +1273,8 @@ int hpmg_profile_levels(hpmg_ctx* ctx, int reps, double* out) {
       for (int l = 1; l <= L; ++l) {
         Level& V = *C.lv[l];
         Level& W = *C.lv[l - 1];
-        const int nw = int(V.wave_ptr.size()) - 1;
-        if (dev::small_level_fits(V.nb, V.P.n, nw)) {
-          dev::small_post(V.A, V.P, V.d_wave_ptr, nw, V.steps, V.Pm, W.x, bs[l], xs[l], C.s);
+        if (V.small) {
+          dev::small_post(V.A, V.rec, V.d_passes, V.npass, V.steps, V.Pm, W.x, bs[l], xs[l], C.s);
         } else {
           dev::prolong_add(V.Pm, W.x, xs[l], C.s);
           smooth(C, V, xs[l], bs[l], true);
@@ -1355,6 +1364,70 @@ int fill_desc(const host::TriMesh& m, int levels, hpmg_mesh_desc* out) {
 }  // namespace
 
 int hpmg_unit_square_mesh(int n, int levels, hpmg_mesh_desc* out) { return fill_desc(host::unit_square(n), levels, out); }
+
+int hpmg_plan_check(const hpmg_mesh_desc* md, int k, int level, int64_t* out, int out_len) {
+  try {
+    host::TriMesh m;
+    for (int v = 0; v < md->n_vertices; ++v) {
+      m.vx.push_back(md->xy[2 * v]);
+      m.vy.push_back(md->xy[2 * v + 1]);
+    }
+    for (int e = 0; e < md->n_elements; ++e)
+      m.ev.push_back({md->elements[3 * e], md->elements[3 * e + 1], md->elements[3 * e + 2]});
+    m.build_facets();
+    const int target = level < 0 ? md->levels - 1 : level;
+    for (int l = 0; l < target; ++l) {
+      host::Refinement R;
+      m = host::refine(m, R);
+    }
+    host::LevelPlan P = host::make_level(m, level < 0 ? k : 0);
+    // double cover
+    std::vector<int> seen(P.nb, 0);
+    for (int p = 0; p < P.npatch; ++p)
+      for (int q = 0; q < P.patch_nf[p]; ++q) seen[P.patch_fac[size_t(p) * host::kMaxPatchF + q]]++;
+    bool cover = true;
+    for (int c : seen) cover = cover && c == 2;
+    // independence inside a wave: no shared block, no coupling between blocks
+    std::vector<int> owner(P.nb, -1), wave_of(P.npatch, -1);
+    bool indep = true;
+    for (int w = 0; w + 1 < int(P.wave_ptr.size()); ++w) {
+      std::vector<int> touched;
+      for (int p = P.wave_ptr[w]; p < P.wave_ptr[w + 1]; ++p) {
+        wave_of[p] = w;
+        for (int q = 0; q < P.patch_nf[p]; ++q) {
+          const int f = P.patch_fac[size_t(p) * host::kMaxPatchF + q];
+          if (owner[f] >= 0 && owner[f] != p) indep = false;
+          owner[f] = p;
+          touched.push_back(f);
+        }
+      }
+      for (int p = P.wave_ptr[w]; p < P.wave_ptr[w + 1]; ++p)
+        for (int q = 0; q < P.patch_nf[p]; ++q) {
+          const int f = P.patch_fac[size_t(p) * host::kMaxPatchF + q];
+          for (int s = 0; s < host::kSlots; ++s) {
+            const int c = P.cols[size_t(f) * host::kSlots + s];
+            if (c >= 0 && owner[c] >= 0 && owner[c] != p) indep = false;
+          }
+        }
+      for (int f : touched) owner[f] = -1;
+    }
+    // ordering: two coupled patches must run in ascending vertex order; the
+    // facet's two patches are stored (lower vertex, higher vertex)
+    bool order = true;
+    for (int f = 0; f < P.nb; ++f) {
+      const int a = P.facet_patches[size_t(f) * 2], b = P.facet_patches[size_t(f) * 2 + 1];
+      if (a >= 0 && b >= 0 && !(wave_of[a] < wave_of[b])) order = false;
+    }
+    int64_t vals[7] = {P.n(), P.npatch, P.nwaves(), cover, indep, order, P.max_patch_f};
+    int w = 0;
+    for (; w < 7 && w < out_len; ++w) out[w] = vals[w];
+    for (int i = 0; i < P.nwaves() && w < out_len; ++i, ++w) out[w] = P.wave_ptr[i + 1] - P.wave_ptr[i];
+    return w;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return -1;
+  }
+}
 int hpmg_step_mesh(int n, int levels, hpmg_mesh_desc* out) { return fill_desc(host::step_domain(n), levels, out); }
 
 }  // extern "C"

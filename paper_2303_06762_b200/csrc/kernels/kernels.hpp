@@ -96,10 +96,14 @@ void jacobi_combine(int nb, int bs, const Patches& P, const double* d, int max_n
 /// Small lowest-order levels (small_levels.cu, symmetric): one CTA runs
 /// x = 0, all pre-smoothing waves, r = b - A x and rc = P^T r (small_pre),
 /// resp. x += P e and all post-smoothing waves (small_post).
-bool small_level_fits(int nb, int npatch, int nwaves);
-void small_pre(const Bsr& A, const Patches& P, const int* wave_ptr, int nwaves, int sweeps, const BlockCsr& PT,
+/// Passes are (first patch, count) ranges of <= small_pass_patches() patches
+/// inside one wave, in forward sweep order.
+struct PatchRecords;
+int small_pass_patches();
+bool small_level_fits(int nb, int record_stride, int npass);
+void small_pre(const Bsr& A, const PatchRecords& R, const int2* passes, int npass, int sweeps, const BlockCsr& PT,
                const double* b, double* x, double* rc, cudaStream_t s);
-void small_post(const Bsr& A, const Patches& P, const int* wave_ptr, int nwaves, int sweeps, const BlockCsr& Pm,
+void small_post(const Bsr& A, const PatchRecords& R, const int2* passes, int npass, int sweeps, const BlockCsr& Pm,
                 const double* e, const double* b, double* x, cudaStream_t s);
 
 void prolong_add(const BlockCsr& P, const double* e, double* x, cudaStream_t s);

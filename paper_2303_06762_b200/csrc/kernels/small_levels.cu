@@ -2,12 +2,13 @@
 //
 // Level 1 of a 16x16 base mesh needs 50 dependent waves per multiplicative
 // sweep (the reference's ascending-vertex order, smoother.hpp:53-57), each
-// only ~20 patches wide: launch latency, not bandwidth, bounds it. Here a
-// single 1024-thread CTA runs a whole pre- (resp. post-) smoothing phase of
-// the V-cycle: x, b and every index array of the level (wave lists, patch
-// facets, inverse offsets, block columns) are staged in shared memory once,
-// so a wave costs one L2 round trip for the A rows and patch inverses plus
-// two __syncthreads(). Symmetric operators only.
+// only ~20 patches wide: latency, not bandwidth, bounds it. One 256-thread
+// CTA runs a whole pre- (resp. post-) smoothing phase of the V-cycle with x
+// and b resident in shared memory. The sweep is cut into passes (<= kPass
+// patches of one wave, host-built list); the patch records of pass k+1..k+3
+// stream in by TMA bulk copies (a kStages-deep mbarrier ring) while pass k is
+// computed, so a wave costs two __syncthreads() and shared-memory arithmetic.
+// Symmetric operators only.
 #include <cuda_runtime.h>
 
 #include <stdexcept>
@@ -20,105 +21,143 @@ namespace dev {
 
 namespace {
 
-constexpr int kThreads = 1024;
-constexpr int kPerPass = kThreads / 16;  // 16 threads (rows) per patch
+constexpr int kThreads = 256;
+constexpr int kTP = 16;                   // threads (rows) per patch
+constexpr int kPass = kThreads / kTP;     // patches per pass
+constexpr int kStages = 4;
 
-struct SmallView {
-  double *sx, *sb, *rr;
-  int *wave_ptr, *wave, *nf, *fac, *off, *cols;
+__device__ __forceinline__ unsigned su32(const void* p) { return unsigned(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void ring_issue(unsigned long long* bar, double* dst, const double* src, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   su32(dst)),
+               "l"(src), "r"(bytes), "r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void ring_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(su32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+struct Smem {
+  double *sx, *sb, *ring, *r;
+  unsigned long long* bar;
 };
 
-__device__ SmallView stage(const Bsr& A, const Patches& P, const int* __restrict__ wave_ptr, int nwaves, double* sm) {
-  const int n = A.nb * 2, npch = P.n;
-  SmallView v;
+__device__ Smem carve(int n, int stride, double* sm) {
+  Smem v;
   v.sx = sm;
   v.sb = sm + n;
-  v.rr = v.sb + n;
-  int* ip = reinterpret_cast<int*>(v.rr + kThreads);
-  v.wave_ptr = ip;
-  v.wave = v.wave_ptr + (nwaves + 1);
-  v.nf = v.wave + npch;
-  v.off = v.nf + npch;
-  v.cols = v.off + npch;
-  v.fac = v.cols + A.nb * kSlots;
-  for (int i = threadIdx.x; i <= nwaves; i += blockDim.x) v.wave_ptr[i] = wave_ptr[i];
-  for (int i = threadIdx.x; i < npch; i += blockDim.x) {
-    v.wave[i] = P.wave[i];
-    v.nf[i] = P.nf[i];
-    v.off[i] = int(P.off[i]);
-  }
-  for (int i = threadIdx.x; i < npch * kMaxPatchF; i += blockDim.x) v.fac[i] = P.fac[i];
-  for (int i = threadIdx.x; i < A.nb * kSlots; i += blockDim.x) v.cols[i] = A.cols[i];
+  v.ring = v.sb + n;
+  v.r = v.ring + size_t(kStages) * kPass * stride;
+  v.bar = reinterpret_cast<unsigned long long*>(v.r + kThreads);
   return v;
 }
 
-__device__ void sweeps(const Bsr& A, const Patches& P, const SmallView& v, int nwaves, int nsweeps, bool reverse) {
-  const int pl = threadIdx.x >> 4, row = threadIdx.x & 15;
-  for (int s = 0; s < nsweeps; ++s)
-    for (int wi = 0; wi < nwaves; ++wi) {
-      const int w = reverse ? nwaves - 1 - wi : wi;
-      const int w0 = v.wave_ptr[w], w1 = v.wave_ptr[w + 1];
-      for (int base = w0; base < w1; base += kPerPass) {
-        const int q = base + pl;
-        int np = 0, g = 0;
-        double inv[2 * kMaxPatchF];
-        if (q < w1) {
-          const int p = v.wave[q];
-          np = 2 * v.nf[p];
-          if (row < np) {
-            const int f = v.fac[p * kMaxPatchF + (row >> 1)], i = row & 1;
-            g = 2 * f + i;
-            // row `row` of the packed symmetric inverse (lower triangle by columns)
-            const double* iv = P.inv + v.off[p];
-            const int ct = row * np - row * (row - 1) / 2 - row;
+/// All passes of `nsweeps` sweeps, forward or reversed, over the patch records.
+__device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, int npass, int nsweeps, bool reverse,
+                       const Smem& v) {
+  const int lp = threadIdx.x / kTP, t = threadIdx.x % kTP;
+  const int total = npass * nsweeps;
+  // the pass list lives in shared memory: a global load here would sit on
+  // the critical path of every pass
+  int2* spass = reinterpret_cast<int2*>(v.bar + kStages);
+  for (int i = threadIdx.x; i < npass; i += blockDim.x) spass[i] = passes[i];
+  __syncthreads();
+  auto pass_of = [&](int k) {
+    const int q = k % npass;
+    return spass[reverse ? npass - 1 - q : q];
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&v.bar[s])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int k = 0; k < kStages - 1 && k < total; ++k) {
+      const int2 ps = pass_of(k);
+      ring_issue(&v.bar[k % kStages], v.ring + size_t(k % kStages) * kPass * R.stride, R.rec + size_t(ps.x) * R.stride,
+                 unsigned(ps.y) * unsigned(R.stride) * 8u);
+    }
+  }
+  __syncthreads();
+  for (int k = 0; k < total; ++k) {
+    if (threadIdx.x == 0 && k + kStages - 1 < total) {
+      // the slot refilled here was released by the __syncthreads() that closed pass k-1
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const int kk = k + kStages - 1;
+      const int2 ps = pass_of(kk);
+      ring_issue(&v.bar[kk % kStages], v.ring + size_t(kk % kStages) * kPass * R.stride,
+                 R.rec + size_t(ps.x) * R.stride, unsigned(ps.y) * unsigned(R.stride) * 8u);
+    }
+    const int2 ps = pass_of(k);
+    ring_wait(&v.bar[k % kStages], unsigned((k / kStages) & 1));
+    const double* rec = v.ring + (size_t(k % kStages) * kPass + lp) * R.stride;
+    int np = 0, g = 0;
+    if (lp < ps.y) {
+      const int* meta = reinterpret_cast<const int*>(rec + R.meta_off);
+      np = 2 * meta[0];
+      if (t < np) {
+        const int lf = t >> 1, i = t & 1;
+        g = 2 * meta[1 + lf] + i;
+        const int* cols = meta + 1 + R.max_nf + lf * kSlots;
+        const double* arow = rec + R.a_off + lf * kSlots * 4 + i * 2;
+        double acc = v.sb[g];
 #pragma unroll
-            for (int j = 0; j < 2 * kMaxPatchF; ++j)
-              inv[j] = j < np ? __ldg(iv + (j >= row ? ct + j : j * np - j * (j - 1) / 2 + (row - j))) : 0.0;
-            double r = v.sb[g];
-#pragma unroll
-            for (int sl = 0; sl < kSlots; ++sl) {
-              const int c = v.cols[f * kSlots + sl];
-              if (c < 0) continue;
-              const double2 a = __ldg(reinterpret_cast<const double2*>(A.val + (size_t(f * kSlots + sl) * 2 + i) * 2));
-              r = fma(-a.x, v.sx[2 * c], r);
-              r = fma(-a.y, v.sx[2 * c + 1], r);
-            }
-            v.rr[threadIdx.x] = r;
-          }
+        for (int sl = 0; sl < kSlots; ++sl) {
+          const int c = cols[sl];
+          const double x0 = c >= 0 ? v.sx[2 * c] : 0.0, x1 = c >= 0 ? v.sx[2 * c + 1] : 0.0;
+          acc = fma(-arow[sl * 4], x0, acc);
+          acc = fma(-arow[sl * 4 + 1], x1, acc);
         }
-        __syncthreads();
-        if (row < np) {
-          double d = 0.0;
-#pragma unroll
-          for (int j = 0; j < 2 * kMaxPatchF; ++j)
-            if (j < np) d = fma(inv[j], v.rr[(pl << 4) + j], d);
-          v.sx[g] += d;
-        }
-        __syncthreads();
+        v.r[threadIdx.x] = acc;
       }
     }
+    __syncthreads();
+    if (t < np) {
+      const int ct = t * np - t * (t - 1) / 2 - t;
+      const double* rr = v.r + lp * kTP;
+      double d0 = 0.0, d1 = 0.0;
+      for (int j = 0; j < np; j += 2) {
+        d0 = fma(rec[j >= t ? ct + j : j * np - j * (j - 1) / 2 + (t - j)], rr[j], d0);
+        const int j1 = j + 1;
+        if (j1 < np) d1 = fma(rec[j1 >= t ? ct + j1 : j1 * np - j1 * (j1 - 1) / 2 + (t - j1)], rr[j1], d1);
+      }
+      v.sx[g] += d0 + d1;
+    }
+    __syncthreads();
+  }
 }
 
 /// x = 0; pre-smooth; r = b - A x; rc = P^T r (reference multigrid.hpp:174-178)
-__global__ void __launch_bounds__(kThreads) k_small_pre(Bsr A, Patches P, const int* __restrict__ wave_ptr, int nwaves,
-                                                        int nsweeps, BlockCsr PT, const double* __restrict__ b,
-                                                        double* __restrict__ x, double* __restrict__ rc) {
-  extern __shared__ double sm[];
+__global__ void __launch_bounds__(kThreads) k_small_pre(Bsr A, PatchRecords R, const int2* __restrict__ passes,
+                                                        int npass, int nsweeps, BlockCsr PT,
+                                                        const double* __restrict__ b, double* __restrict__ x,
+                                                        double* __restrict__ rc) {
+  extern __shared__ __align__(128) double sm[];
   const int n = A.nb * 2;
-  SmallView v = stage(A, P, wave_ptr, nwaves, sm);
+  Smem v = carve(n, R.stride, sm);
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     v.sx[i] = 0.0;
     v.sb[i] = b[i];
   }
   __syncthreads();
-  sweeps(A, P, v, nwaves, nsweeps, false);
+  sweeps(R, passes, npass, nsweeps, false, v);
   // residual in place of b (each row reads only its own b entry and x)
   for (int t = threadIdx.x; t < n; t += blockDim.x) {
     const int f = t >> 1, i = t & 1;
     double s = 0.0;
 #pragma unroll
     for (int sl = 0; sl < kSlots; ++sl) {
-      const int c = v.cols[f * kSlots + sl];
+      const int c = __ldg(&A.cols[f * kSlots + sl]);
       if (c < 0) continue;
       const double2 a = __ldg(reinterpret_cast<const double2*>(A.val + (size_t(f * kSlots + sl) * 2 + i) * 2));
       s = fma(a.x, v.sx[2 * c], s);
@@ -142,13 +181,13 @@ __global__ void __launch_bounds__(kThreads) k_small_pre(Bsr A, Patches P, const 
 }
 
 /// x += P e; post-smooth (reverse sweep) (reference multigrid.hpp:181-182)
-__global__ void __launch_bounds__(kThreads) k_small_post(Bsr A, Patches P, const int* __restrict__ wave_ptr,
-                                                         int nwaves, int nsweeps, BlockCsr Pm,
+__global__ void __launch_bounds__(kThreads) k_small_post(Bsr A, PatchRecords R, const int2* __restrict__ passes,
+                                                         int npass, int nsweeps, BlockCsr Pm,
                                                          const double* __restrict__ e, const double* __restrict__ b,
                                                          double* __restrict__ x) {
-  extern __shared__ double sm[];
+  extern __shared__ __align__(128) double sm[];
   const int n = A.nb * 2;
-  SmallView v = stage(A, P, wave_ptr, nwaves, sm);
+  Smem v = carve(n, R.stride, sm);
   for (int t = threadIdx.x; t < n; t += blockDim.x) {
     const int f = t >> 1, c = t & 1;
     double s = 0.0;
@@ -162,20 +201,24 @@ __global__ void __launch_bounds__(kThreads) k_small_post(Bsr A, Patches P, const
     v.sb[t] = b[t];
   }
   __syncthreads();
-  sweeps(A, P, v, nwaves, nsweeps, true);
+  sweeps(R, passes, npass, nsweeps, true, v);
   for (int t = threadIdx.x; t < n; t += blockDim.x) x[t] = v.sx[t];
 }
 
-size_t smem_bytes(int nb, int npatch, int nwaves) {
-  return sizeof(double) * (size_t(4) * nb + kThreads) +
-         sizeof(int) * (size_t(nwaves + 1) + size_t(npatch) * (3 + kMaxPatchF) + size_t(nb) * kSlots);
+size_t smem_bytes(int nb, int stride, int npass) {
+  return sizeof(double) * (size_t(4) * nb + size_t(kStages) * kPass * stride + kThreads) + 8 * kStages +
+         sizeof(int2) * size_t(npass);
 }
 
 }  // namespace
 
-bool small_level_fits(int nb, int npatch, int nwaves) { return smem_bytes(nb, npatch, nwaves) <= 220 * 1024; }
+int small_pass_patches() { return kPass; }
 
-void small_pre(const Bsr& A, const Patches& P, const int* wave_ptr, int nwaves, int sweeps, const BlockCsr& PT,
+bool small_level_fits(int nb, int record_stride, int npass) {
+  return smem_bytes(nb, record_stride, npass) <= 225 * 1024;
+}
+
+void small_pre(const Bsr& A, const PatchRecords& R, const int2* passes, int npass, int sweeps, const BlockCsr& PT,
                const double* b, double* x, double* rc, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
@@ -183,14 +226,14 @@ void small_pre(const Bsr& A, const Patches& P, const int* wave_ptr, int nwaves, 
     cudaFuncSetAttribute(k_small_post, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  k_small_pre<<<1, kThreads, smem_bytes(A.nb, P.n, nwaves), s>>>(A, P, wave_ptr, nwaves, sweeps, PT, b, x, rc);
+  k_small_pre<<<1, kThreads, smem_bytes(A.nb, R.stride, npass), s>>>(A, R, passes, npass, sweeps, PT, b, x, rc);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) throw std::runtime_error(std::string("CUDA launch: ") + cudaGetErrorString(err));
 }
 
-void small_post(const Bsr& A, const Patches& P, const int* wave_ptr, int nwaves, int sweeps, const BlockCsr& Pm,
+void small_post(const Bsr& A, const PatchRecords& R, const int2* passes, int npass, int sweeps, const BlockCsr& Pm,
                 const double* e, const double* b, double* x, cudaStream_t s) {
-  k_small_post<<<1, kThreads, smem_bytes(A.nb, P.n, nwaves), s>>>(A, P, wave_ptr, nwaves, sweeps, Pm, e, b, x);
+  k_small_post<<<1, kThreads, smem_bytes(A.nb, R.stride, npass), s>>>(A, R, passes, npass, sweeps, Pm, e, b, x);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) throw std::runtime_error(std::string("CUDA launch: ") + cudaGetErrorString(err));
 }
