@@ -100,6 +100,7 @@ def lib():
     L.hpmg_pcg.argtypes = [vp, vp, vp, C.POINTER(_KOpts), C.POINTER(_Stats), C.c_int]
     L.hpmg_gmres.argtypes = [vp, vp, vp, C.POINTER(_KOpts), C.POINTER(_Stats), C.c_int]
     L.hpmg_uzawa.argtypes = [vp, C.POINTER(_UOpts), dp, dp, C.POINTER(_UReport)]
+    L.hpmg_recover.argtypes = [vp, vp, vp, vp, vp]
     L.hpmg_stream.restype = vp
     L.hpmg_stream.argtypes = [vp]
     L.hpmg_vcycle_bytes.restype = C.c_double
@@ -305,6 +306,18 @@ class MGPreconditioner:
 
     def as_operator(self):
         return self.apply
+
+    def recover(self, velocity_full):
+        """recover_locals on the finest system (reference assembly.hpp:513-549):
+        returns (interior [ne, k(k+1)], p_ortho [ne, ns-1], grad [ne, 4 ns])."""
+        k = self.k
+        ns = (k + 1) * (k + 2) // 2
+        v = np.ascontiguousarray(velocity_full, dtype=np.float64)
+        interior = np.zeros((self.ne, max(k * (k + 1), 1)))
+        p = np.zeros((self.ne, max(ns - 1, 1)))
+        g = np.zeros((self.ne, 4 * ns))
+        self._check(lib().hpmg_recover(self.h, v.ctypes.data, interior.ctypes.data, p.ctypes.data, g.ctypes.data))
+        return interior[:, : k * (k + 1)], p[:, : ns - 1], g
 
     # -- measurement hooks
     def stream(self):

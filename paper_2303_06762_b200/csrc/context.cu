@@ -113,6 +113,10 @@ struct hpmg_ctx {
   std::vector<double*> gm_basis;
   // uzawa
   double *pres = nullptr, *div = nullptr, *urhs = nullptr;
+  // finest-system load and condensation parameters (recover_locals)
+  double* fine_load = nullptr;
+  int fine_lstride = 0;
+  CondenseParams fine_prm{};
   bool enclosed = true;
   int launches_per_apply = 0;
   bool counting = false;
@@ -281,7 +285,13 @@ void build_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, const Dev
   CK(cudaStreamSynchronize(s));
   cudaFree(acr);
   cudaFree(gath);
-  if (dload) cudaFree(dload);
+  if (finest) {  // kept for recover_locals
+    C.fine_load = dload;
+    C.fine_lstride = lstride;
+    C.fine_prm = prm;
+  } else if (dload) {
+    cudaFree(dload);
+  }
   // patches + explicit inverses
   V.P.n = V.plan.npatch;
   V.max_nf = V.plan.max_patch_f;
@@ -1121,9 +1131,26 @@ int hpmg_uzawa(hpmg_ctx* ctx, const hpmg_uzawa_opts* o, double* velocity, double
   });
 }
 
-int hpmg_recover(hpmg_ctx* ctx, const double*, double*, double*, double*) {
-  ctx->err = g_last_error = "hpmg_recover: not implemented yet";
-  return HPMG_ERR_LOGIC;
+int hpmg_recover(hpmg_ctx* ctx, const double* velocity_full, double* interior, double* p_ortho, double* grad) {
+  return guarded(ctx, [&] {
+    hpmg_ctx& C = *ctx;
+    Level& T = C.top();
+    const DevRef& R = C.opt.k > 0 ? C.refk : C.ref0;
+    const int ne = T.ne, no = R.T.no, np = R.T.ns - 1, ng = 4 * R.T.ns;
+    const size_t nfull = C.g_full.size();
+    double* comp = dalloc<double>(nfull);
+    double* di = dalloc<double>(size_t(ne) * std::max(no, 1));
+    double* dp = dalloc<double>(size_t(ne) * std::max(np, 1));
+    double* dg = dalloc<double>(size_t(ne) * ng);
+    CK(cudaMemcpyAsync(comp, velocity_full, sizeof(double) * nfull, cudaMemcpyHostToDevice, C.s));
+    dev::recover(R.T, T.geo, ne, C.fine_prm, C.fine_load, C.fine_lstride, T.elem_facets, (long long)(nfull / 2), comp,
+                 di, dp, dg, C.s);
+    if (no) CK(cudaMemcpyAsync(interior, di, sizeof(double) * ne * no, cudaMemcpyDeviceToHost, C.s));
+    if (np) CK(cudaMemcpyAsync(p_ortho, dp, sizeof(double) * ne * np, cudaMemcpyDeviceToHost, C.s));
+    CK(cudaMemcpyAsync(grad, dg, sizeof(double) * ne * ng, cudaMemcpyDeviceToHost, C.s));
+    CK(cudaStreamSynchronize(C.s));
+    for (double* p : {comp, di, dp, dg}) cudaFree(p);
+  });
 }
 
 void* hpmg_stream(hpmg_ctx* ctx) { return ctx->s; }

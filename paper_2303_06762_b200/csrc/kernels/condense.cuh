@@ -67,8 +67,14 @@ HPMG_HD inline int condense_scratch(int ns, int nv, int nc, int nz, int nrt) {
 
 /// Computes the condensed element matrix Ac (nc x nc, row-major, reference
 /// local order: 3 nfd flux, 3 nfd tangential) and load vector rc (nc).
+/// Recovery mode (reference recover_locals, inc/assembly.hpp:513-549): with
+/// xc != nullptr the element's skeleton coefficients are given and, instead of
+/// Ac / rc, z = M_zz^{-1}(r_z - M_zc xc) (interior RT coefficients then the
+/// zero-mean pressure modes) goes to zout and the gradient variable
+/// -(nu/detJ) C [xc; z_interior] to gout.
 HPMG_D inline void condense_element(int tid, int nthr, const RefT& T, const ElemGeo& g, const CondenseParams& prm,
-                                     const double* load, double* scratch, double* Ac, double* rc) {
+                                     const double* load, double* scratch, double* Ac, double* rc,
+                                     const double* xc = nullptr, double* zout = nullptr, double* gout = nullptr) {
   const int ns = T.ns, nv = T.nv, nc = T.nc, nrt = T.nrt, nfd = T.nfd, no = T.no;
   const int np = ns - 1, nz = no + np, nC = 4 * ns;
   double* C = scratch;
@@ -168,6 +174,14 @@ HPMG_D inline void condense_element(int tid, int nthr, const RefT& T, const Elem
   }
   SYNC();
   if (nz == 0) {
+    if (xc) {
+      for (int row = tid; row < nC; row += nthr) {
+        double s = 0.0;
+        for (int a = 0; a < nc; ++a) s += C[row * nv + a] * xc[a];
+        gout[row] = -visc * s;
+      }
+      return;
+    }
     for (int e = tid; e < nc * nc; e += nthr) Ac[e] = A[(e / nc) * nv + (e % nc)];
     for (int a = tid; a < nc; a += nthr) rc[a] = rhs[a];
     return;
@@ -224,6 +238,23 @@ HPMG_D inline void condense_element(int tid, int nthr, const RefT& T, const Elem
     }
   }
   SYNC();
+  if (xc) {
+    // z = y - X xc, xv = [xc; z_interior] staged in rhs[], then L = -(nu/detJ) C xv
+    for (int i = tid; i < nz; i += nthr) {
+      double s = aug[i * naug + nz + nc];
+      for (int j = 0; j < nc; ++j) s -= aug[i * naug + nz + j] * xc[j];
+      zout[i] = s;
+      if (i < no) rhs[nc + i] = s;
+    }
+    for (int a = tid; a < nc; a += nthr) rhs[a] = xc[a];
+    SYNC();
+    for (int row = tid; row < nC; row += nthr) {
+      double s = 0.0;
+      for (int a = 0; a < nv; ++a) s += C[row * nv + a] * rhs[a];
+      gout[row] = -visc * s;
+    }
+    return;
+  }
   // Ac = A_cc - Mcz X, rc = r_c - Mcz y with Mcz = [A_co, -P_c^T]
   for (int e = tid; e < nc * (nc + 1); e += nthr) {
     const int a = e / (nc + 1), j = e % (nc + 1);

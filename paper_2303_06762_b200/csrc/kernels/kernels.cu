@@ -101,6 +101,38 @@ __global__ void k_condense(RefT T, const ElemGeo* __restrict__ geo, CondensePara
   condense_element(threadIdx.x, blockDim.x, T, g, prm, ld, smem, o, o + T.nc * T.nc);
 }
 
+/// recover_locals (reference inc/assembly.hpp:513-549) for every element:
+/// gathers the element's skeleton coefficients from the full compound vector
+/// (reference layout: all flux modes, then all tangential modes).
+__global__ void k_recover(RefT T, const ElemGeo* __restrict__ geo, CondenseParams prm, const double* __restrict__ load,
+                          int load_stride, const int* __restrict__ elem_facets, long long nflux,
+                          const double* __restrict__ compound, double* __restrict__ interior,
+                          double* __restrict__ pres, double* __restrict__ grad) {
+  extern __shared__ double smem[];
+  __shared__ ElemGeo g;
+  const int e = blockIdx.x;
+  const int nfd = T.nfd, nc = T.nc, nz = T.no + T.ns - 1;
+  double* xc = smem;
+  double* zb = xc + nc;
+  double* gb = zb + nz + 1;
+  double* scratch = gb + 4 * T.ns;
+  if (threadIdx.x < int(sizeof(ElemGeo) / sizeof(double)))
+    reinterpret_cast<double*>(&g)[threadIdx.x] = reinterpret_cast<const double*>(geo + e)[threadIdx.x];
+  for (int a = threadIdx.x; a < nc; a += blockDim.x) {
+    const bool tang = a >= 3 * nfd;
+    const int la = tang ? a - 3 * nfd : a;
+    const long long f = elem_facets[e * 3 + la / nfd];
+    xc[a] = compound[(tang ? nflux : 0) + f * nfd + la % nfd];
+  }
+  __syncthreads();
+  const double* ld = prm.load_mode ? load + size_t(e) * load_stride : nullptr;
+  condense_element(threadIdx.x, blockDim.x, T, g, prm, ld, scratch, nullptr, nullptr, xc, zb, gb);
+  __syncthreads();
+  for (int j = threadIdx.x; j < T.no; j += blockDim.x) interior[size_t(e) * T.no + j] = zb[j];
+  for (int m = threadIdx.x; m < T.ns - 1; m += blockDim.x) pres[size_t(e) * (T.ns - 1) + m] = zb[T.no + m];
+  for (int r = threadIdx.x; r < 4 * T.ns; r += blockDim.x) grad[size_t(e) * 4 * T.ns + r] = gb[r];
+}
+
 __device__ __forceinline__ int local_dof(int lf, int ii, int nfd) {
   // block entry ii = 2 i + t  ->  reference local index (flux: lf*nfd+i, tang: 3nfd + lf*nfd + i)
   const int i = ii >> 1, t = ii & 1;
@@ -730,6 +762,22 @@ void condense(const RefT& T, const ElemGeo* geo, int ne, CondenseParams prm, con
     attr = true;
   }
   k_condense<<<ne, 128, smem, s>>>(T, geo, prm, load, load_stride, out, T.nc * T.nc + T.nc);
+  HPMG_LAUNCH_CHECK();
+}
+
+void recover(const RefT& T, const ElemGeo* geo, int ne, CondenseParams prm, const double* load, int load_stride,
+             const int* elem_facets, long long nflux, const double* compound, double* interior, double* pres,
+             double* grad, cudaStream_t s) {
+  if (ne == 0) return;
+  const int nz = T.no + T.ns - 1;
+  const size_t smem =
+      sizeof(double) * (condense_scratch(T.ns, T.nv, T.nc, nz, T.nrt) + T.nc + nz + 1 + 4 * T.ns);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_recover, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_recover<<<ne, 128, smem, s>>>(T, geo, prm, load, load_stride, elem_facets, nflux, compound, interior, pres, grad);
   HPMG_LAUNCH_CHECK();
 }
 

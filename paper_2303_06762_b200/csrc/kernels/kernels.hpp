@@ -50,6 +50,10 @@ struct Reduce {
 
 void condense(const RefT& T, const ElemGeo* geo, int ne, CondenseParams prm, const double* load, int load_stride,
               double* out, cudaStream_t s);
+/// recover_locals on every element from the full compound skeleton vector.
+void recover(const RefT& T, const ElemGeo* geo, int ne, CondenseParams prm, const double* load, int load_stride,
+             const int* elem_facets, long long nflux, const double* compound, double* interior, double* pres,
+             double* grad, cudaStream_t s);
 void assemble_bsr(const Bsr& A, int nfd, const double* acr, int acr_stride, int nc, const int* gath,
                   const ElemGeo* geo, double inv_eps, cudaStream_t s);
 void transpose_bsr(const Bsr& A, const int* tslot, Bsr& AT, cudaStream_t s);

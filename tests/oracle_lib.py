@@ -213,6 +213,16 @@ class OracleMG:
                     divergence_history=list(hist[:done]), converged=bool(flags[0]),
                     not_applicable=bool(flags[1]), seconds=float(secs[0]))
 
+    def recover(self, velocity_full):
+        k = self.k
+        ns = (k + 1) * (k + 2) // 2
+        v = np.ascontiguousarray(velocity_full, dtype=np.float64)
+        interior = np.zeros((self.ne, max(k * (k + 1), 1)))
+        p = np.zeros((self.ne, max(ns - 1, 1)))
+        g = np.zeros((self.ne, 4 * ns))
+        lib().orc_mg_recover(self.h, _dp(v), _dp(interior), _dp(p), _dp(g))
+        return interior[:, : k * (k + 1)], p[:, : ns - 1], g
+
     def time_apply(self, reps):
         return lib().orc_mg_time_apply(self.h, reps)
 

@@ -121,3 +121,44 @@ def test_config1_full_size_parity():
     for a, b in zip(rg.report.inner_iterations, ro["inner_iterations"]):
         assert abs(a - b) <= 1
     assert rel(rg.velocity, ro["velocity"]) < 1e-9
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 3])
+def test_recover_locals(k):
+    # reference assembly.hpp:513-549 on the Uzawa velocity; the zero-mean pressure
+    # modes and the gradient variable are basis-independent; interior RT
+    # coefficients match for the min-norm divergence functions, and up to the
+    # sign / rotation of the divergence-free bubbles (k(k-1)/2 of them) otherwise
+    orc, gpu = pair(k, levels=3, bc=lid_top)
+    vel = orc.uzawa()["velocity"]
+    ig, pg, gg = gpu.recover(vel)
+    io, po, go = orc.recover(vel)
+    assert rel(gg.ravel(), go.ravel()) < 1e-10
+    if k > 0:
+        assert rel(pg.ravel(), po.ravel()) < 1e-10
+        nb = k * (k - 1) // 2
+        # the interior coefficients of a (discretely) divergence-free solution are
+        # O(1e-18) here, so they are compared against the velocity scale
+        scale = np.abs(vel).max()
+        assert np.abs(ig[:, nb:] - io[:, nb:]).max() <= 1e-10 * scale
+        if nb == 1:
+            assert np.abs(np.abs(ig[:, 0]) - np.abs(io[:, 0])).max() <= 1e-10 * scale
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_recover_locals_random_skeleton(k):
+    # a non-solenoidal skeleton vector makes every interior coefficient O(1)
+    orc, gpu = pair(k, levels=2, bc=lid_top)
+    vel = O.random_vec(orc.n_full, 29)
+    ig, pg, gg = gpu.recover(vel)
+    io, po, go = orc.recover(vel)
+    assert rel(gg.ravel(), go.ravel()) < 1e-10
+    assert rel(pg.ravel(), po.ravel()) < 1e-10
+    nb = k * (k - 1) // 2
+    # the divergence-reproducing interior functions carry the zero-mean part of
+    # div u, which the elimination forces to zero; bubbles carry O(1) values
+    scale = np.abs(vel).max()
+    assert np.abs(ig[:, nb:] - io[:, nb:]).max() <= 1e-10 * scale
+    if nb == 1:
+        assert np.abs(io[:, 0]).max() > 1e-3 * scale
+        assert rel(np.abs(ig[:, 0]), np.abs(io[:, 0])) < 1e-10
