@@ -13,6 +13,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/hpmg/capi.h"
@@ -820,15 +821,32 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
   CK(cudaStreamSynchronize(C.s));
   auto t3 = clk::now();
   // transfers (host correction from the downloaded fine operators)
-  for (int l = 1; l <= C.L; ++l) {
-    std::vector<double> Af = download_bsr(C, *C.lv[l]);
-    host::BlockCsrH P = host::corrected_prolongation(C.lv[l - 1]->plan, C.lv[l]->plan, C.ref[l - 1], Af);
-    host::BlockCsrH PT = host::transpose_blocks(P);
-    double nz = 0;
-    for (double v : P.val) nz += v != 0.0;
-    C.lv[l]->p_nnz = nz;
-    C.lv[l]->Pm = upload_blockcsr(P, C.s);
-    C.lv[l]->PT = upload_blockcsr(PT, C.s);
+  {
+    // levels are independent: one host thread per level
+    std::vector<std::vector<double>> Af(C.L + 1);
+    for (int l = 1; l <= C.L; ++l) Af[l] = download_bsr(C, *C.lv[l]);
+    std::vector<host::BlockCsrH> Ps(C.L + 1), PTs(C.L + 1);
+    std::vector<std::thread> pool;
+    std::vector<std::string> errs(C.L + 1);
+    for (int l = 1; l <= C.L; ++l)
+      pool.emplace_back([&, l] {
+        try {
+          Ps[l] = host::corrected_prolongation(C.lv[l - 1]->plan, C.lv[l]->plan, C.ref[l - 1], Af[l]);
+          PTs[l] = host::transpose_blocks(Ps[l]);
+        } catch (const std::exception& e) {
+          errs[l] = e.what();
+        }
+      });
+    for (auto& t : pool) t.join();
+    for (int l = 1; l <= C.L; ++l) {
+      if (!errs[l].empty()) throw std::runtime_error(errs[l]);
+      double nz = 0;
+      for (double v : Ps[l].val) nz += v != 0.0;
+      C.lv[l]->p_nnz = nz;
+      C.lv[l]->Pm = upload_blockcsr(Ps[l], C.s);
+      C.lv[l]->PT = upload_blockcsr(PTs[l], C.s);
+    }
+    CK(cudaStreamSynchronize(C.s));
   }
   auto t4 = clk::now();
   // coarse dense inverse
@@ -843,7 +861,11 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
         for (int i = 0; i < 2; ++i)
           for (int j = 0; j < 2; ++j) D[size_t(2 * r + i) * C.n0 + 2 * c + j] = A0[((size_t(r) * host::kSlots + s) * 2 + i) * 2 + j];
       }
-    C.coarse_inv = dupload(dense_inverse(D, C.n0), C.s);
+    // Gauss-Jordan on the device (host LU: dense_inverse(), kept for reference)
+    double* dA = dupload(D, C.s);
+    C.coarse_inv = dalloc<double>(size_t(C.n0) * C.n0);
+    dev::dense_invert(C.n0, dA, C.coarse_inv, C.s);
+    cudaFree(dA);
     C.gemv_work = dalloc<double>(size_t(C.n0) * ((C.n0 + 63) / 64 + 1));  // kGemvChunk = 64
   }
   auto t5 = clk::now();

@@ -4,11 +4,12 @@
 //   interior patches    (inc/transfer.hpp:75-88)
 //   harmonic correction P_T = I_T - A_TT^{-1} (A I)_T  (inc/transfer.hpp:95-133)
 // The correction reads the assembled fine operator (downloaded once from the
-// device). Setup-only work; its apply runs on the device (dev::prolong_add /
-// dev::restrict_).
+// device). Setup-only work on small fixed-capacity row buffers (a fine row
+// touches at most 5 coarse facets, a corrected row at most 9); the apply runs
+// on the device (dev::prolong_add / dev::restrict_).
 #pragma once
 
-#include <map>
+#include <array>
 #include <vector>
 
 #include "plan.hpp"
@@ -34,12 +35,36 @@ inline double cr_basis(const TriMesh& m, int e, int lf, double x, double y) {
   return 1.0 - 2.0 * part / full;
 }
 
-/// Rows of the averaging transfer as block maps (sorted by coarse block).
-inline std::vector<std::map<int, std::array<double, 4>>> averaging_blocks(const LevelPlan& C, const LevelPlan& F,
-                                                                          const Refinement& R) {
+/// Sparse block row with a small fixed capacity, columns kept sorted.
+template <int N>
+struct BlockRow {
+  int n = 0;
+  std::array<int, N> col;
+  std::array<std::array<double, 4>, N> v;
+  std::array<double, 4>& at(int c) {
+    int i = 0;
+    while (i < n && col[i] < c) ++i;
+    if (i < n && col[i] == c) return v[i];
+    if (n == N) throw std::runtime_error("transfer row capacity exceeded");
+    for (int j = n; j > i; --j) {
+      col[j] = col[j - 1];
+      v[j] = v[j - 1];
+    }
+    col[i] = c;
+    v[i] = {0.0, 0.0, 0.0, 0.0};
+    ++n;
+    return v[i];
+  }
+};
+
+constexpr int kAvgCap = 8;   // fine row of the averaging transfer: <= 5 coarse facets
+constexpr int kCorrCap = 16; // corrected row: facets of a coarse element and its neighbours (<= 9)
+
+/// Rows of the averaging transfer (reference inc/transfer.hpp:19-71).
+inline std::vector<BlockRow<kAvgCap>> averaging_blocks(const LevelPlan& C, const LevelPlan& F, const Refinement& R) {
   const TriMesh& cm = *C.mesh;
   const TriMesh& fm = *F.mesh;
-  std::vector<std::map<int, std::array<double, 4>>> rows(F.nb);
+  std::vector<BlockRow<kAvgCap>> rows(F.nb);
   for (int rf = 0; rf < F.nb; ++rf) {
     const int ff = F.block_facet[rf];
     int se[2] = {-1, -1};
@@ -72,7 +97,7 @@ inline std::vector<std::map<int, std::array<double, 4>>> averaging_blocks(const 
         double ncx, ncy, tcx, tcy;
         cm.fnormal(fc, ncx, ncy);
         cm.ftan(fc, tcx, tcy);
-        auto& b = rows[rf][cb];  // zero-initialised on first touch
+        auto& b = rows[rf].at(cb);
         b[0] += phi * (nfx * ncx + nfy * ncy);  // (flux, flux)
         b[3] += phi * (tfx * tcx + tfy * tcy);  // (tang, tang)
         b[1] += phi * (nfx * tcx + nfy * tcy);  // (flux, tang)
@@ -86,8 +111,6 @@ inline std::vector<std::map<int, std::array<double, 4>>> averaging_blocks(const 
 /// Small dense LU solve with partial pivoting, multiple right-hand sides
 /// (row-major A n x n, B n x m overwritten by the solution).
 inline void lu_solve_multi(std::vector<double> A, int n, std::vector<double>& B, int m) {
-  std::vector<int> perm(n);
-  for (int i = 0; i < n; ++i) perm[i] = i;
   for (int k = 0; k < n; ++k) {
     int p = k;
     for (int i = k + 1; i < n; ++i)
@@ -119,58 +142,62 @@ inline BlockCsrH corrected_prolongation(const LevelPlan& C, const LevelPlan& F, 
   auto rows = averaging_blocks(C, F, R);
   const TriMesh& fm = *F.mesh;
   // interior patches: medial fine facets per coarse element, ascending facet id
-  std::vector<std::vector<int>> med(R.children.size());
+  std::vector<std::array<int, 3>> med(R.children.size(), {-1, -1, -1});
+  std::vector<int> nmed(R.children.size(), 0);
   for (int ff = 0; ff < fm.nf(); ++ff)
-    if (R.fclass[ff] == kMedial && F.facet_block[ff] >= 0) med[R.parent_elem[ff]].push_back(F.facet_block[ff]);
+    if (R.fclass[ff] == kMedial && F.facet_block[ff] >= 0) {
+      const int e = R.parent_elem[ff];
+      med[e][nmed[e]++] = F.facet_block[ff];
+    }
   auto Aent = [&](int rb, int rt, int cb, int ct) -> double {
     for (int s = 0; s < kSlots; ++s)
       if (F.cols[size_t(rb) * kSlots + s] == cb) return Aval[((size_t(rb) * kSlots + s) * 2 + rt) * 2 + ct];
     return 0.0;
   };
-  std::vector<std::map<int, std::array<double, 4>>> corr(F.nb);
-  for (const auto& T : med) {
-    const int nt = 2 * int(T.size());
+  std::vector<BlockRow<kCorrCap>> corr(F.nb);
+  std::vector<double> Att, B;
+  for (size_t e = 0; e < med.size(); ++e) {
+    const int nt = 2 * nmed[e];
     if (nt == 0) continue;
-    // W_T = (A I_avg) restricted to the rows of T
-    std::map<int, std::array<double, 2>> dummy;
-    std::vector<std::map<int, std::array<double, 2>>> W(nt);  // per T-row: coarse block -> (flux, tang) cols
+    // W_T = (A I_avg) restricted to the rows of T: per T-row, coarse block -> (flux, tang)
+    BlockRow<kCorrCap> W[6];
     for (int r = 0; r < nt; ++r) {
-      const int rb = T[r / 2], rt = r % 2;
+      const int rb = med[e][r / 2], rt = r % 2;
       for (int s = 0; s < kSlots; ++s) {
         const int jb = F.cols[size_t(rb) * kSlots + s];
         if (jb < 0) continue;
         for (int jt = 0; jt < 2; ++jt) {
           const double a = Aval[((size_t(rb) * kSlots + s) * 2 + rt) * 2 + jt];
           if (a == 0.0) continue;
-          for (const auto& kv : rows[jb]) {
-            auto& w = W[r][kv.first];
-            w[0] += a * kv.second[jt * 2 + 0];
-            w[1] += a * kv.second[jt * 2 + 1];
+          const auto& ar = rows[jb];
+          for (int q = 0; q < ar.n; ++q) {
+            auto& w = W[r].at(ar.col[q]);
+            w[0] += a * ar.v[q][jt * 2 + 0];
+            w[1] += a * ar.v[q][jt * 2 + 1];
           }
         }
       }
     }
-    std::vector<int> cols;
+    BlockRow<kCorrCap> cols;  // union of W columns
     for (int r = 0; r < nt; ++r)
-      for (const auto& kv : W[r]) cols.push_back(kv.first);
-    std::sort(cols.begin(), cols.end());
-    cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
-    if (cols.empty()) continue;
-    const int m = 2 * int(cols.size());
-    std::vector<double> Att(size_t(nt) * nt), B(size_t(nt) * m, 0.0);
+      for (int q = 0; q < W[r].n; ++q) cols.at(W[r].col[q]);
+    if (cols.n == 0) continue;
+    const int m = 2 * cols.n;
+    Att.assign(size_t(nt) * nt, 0.0);
+    B.assign(size_t(nt) * m, 0.0);
     for (int r = 0; r < nt; ++r) {
-      for (int c = 0; c < nt; ++c) Att[size_t(r) * nt + c] = Aent(T[r / 2], r % 2, T[c / 2], c % 2);
-      for (size_t j = 0; j < cols.size(); ++j) {
-        auto it = W[r].find(cols[j]);
-        if (it == W[r].end()) continue;
-        B[size_t(r) * m + 2 * j] = it->second[0];
-        B[size_t(r) * m + 2 * j + 1] = it->second[1];
+      for (int c = 0; c < nt; ++c) Att[size_t(r) * nt + c] = Aent(med[e][r / 2], r % 2, med[e][c / 2], c % 2);
+      for (int q = 0; q < W[r].n; ++q) {
+        int j = 0;
+        while (cols.col[j] != W[r].col[q]) ++j;
+        B[size_t(r) * m + 2 * j] = W[r].v[q][0];
+        B[size_t(r) * m + 2 * j + 1] = W[r].v[q][1];
       }
     }
     lu_solve_multi(Att, nt, B, m);
     for (int r = 0; r < nt; ++r)
-      for (size_t j = 0; j < cols.size(); ++j) {
-        auto& b = corr[T[r / 2]][cols[j]];
+      for (int j = 0; j < cols.n; ++j) {
+        auto& b = corr[med[e][r / 2]].at(cols.col[j]);
         b[(r % 2) * 2 + 0] -= B[size_t(r) * m + 2 * j];
         b[(r % 2) * 2 + 1] -= B[size_t(r) * m + 2 * j + 1];
       }
@@ -178,16 +205,20 @@ inline BlockCsrH corrected_prolongation(const LevelPlan& C, const LevelPlan& F, 
   BlockCsrH P;
   P.nrows = F.nb;
   P.ncols = C.nb;
+  P.col.reserve(size_t(F.nb) * 6);
+  P.val.reserve(size_t(F.nb) * 24);
   for (int rf = 0; rf < F.nb; ++rf) {
-    std::map<int, std::array<double, 4>> merged = rows[rf];
-    for (const auto& kv : corr[rf]) {
-      auto& b = merged[kv.first];
-      for (int q = 0; q < 4; ++q) b[q] += kv.second[q];
+    BlockRow<kCorrCap> merged;
+    for (int q = 0; q < rows[rf].n; ++q) merged.at(rows[rf].col[q]) = rows[rf].v[q];
+    for (int q = 0; q < corr[rf].n; ++q) {
+      auto& b = merged.at(corr[rf].col[q]);
+      for (int t = 0; t < 4; ++t) b[t] += corr[rf].v[q][t];
     }
-    for (const auto& kv : merged) {
-      if (kv.second[0] == 0.0 && kv.second[1] == 0.0 && kv.second[2] == 0.0 && kv.second[3] == 0.0) continue;
-      P.col.push_back(kv.first);
-      for (int q = 0; q < 4; ++q) P.val.push_back(kv.second[q]);
+    for (int q = 0; q < merged.n; ++q) {
+      const auto& v = merged.v[q];
+      if (v[0] == 0.0 && v[1] == 0.0 && v[2] == 0.0 && v[3] == 0.0) continue;
+      P.col.push_back(merged.col[q]);
+      for (int t = 0; t < 4; ++t) P.val.push_back(v[t]);
     }
     P.ptr.push_back(int(P.col.size()));
   }

@@ -604,6 +604,80 @@ __global__ void k_gemv_sum(int n, int chunks, const double* __restrict__ work, d
   }
 }
 
+// ---------------------------------------------- dense coarse inverse (setup)
+/// Gauss-Jordan step k on aug = [A | I] (n x 2n row-major): pivot search
+/// (largest |a_ik|, lowest index on ties), row swap, and copies of the pivot
+/// row and column so the elimination kernel never reads what it writes.
+__global__ void k_gj_pivot(int n, int k, double* __restrict__ aug, double* __restrict__ rowk,
+                           double* __restrict__ colk, int* __restrict__ status) {
+  __shared__ double bv[32];
+  __shared__ int bi[32];
+  const int w = 2 * n;
+  double best = -1.0;
+  int besti = k;
+  for (int i = k + threadIdx.x; i < n; i += blockDim.x) {
+    const double v = fabs(aug[size_t(i) * w + k]);
+    if (v > best) { best = v; besti = i; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, besti, o);
+    if (ob > best || (ob == best && oi < besti)) { best = ob; besti = oi; }
+  }
+  if ((threadIdx.x & 31) == 0) { bv[threadIdx.x >> 5] = best; bi[threadIdx.x >> 5] = besti; }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int nw = blockDim.x >> 5;
+    best = threadIdx.x < nw ? bv[threadIdx.x] : -1.0;
+    besti = threadIdx.x < nw ? bi[threadIdx.x] : n;
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, besti, o);
+      if (ob > best || (ob == best && oi < besti)) { best = ob; besti = oi; }
+    }
+    if (threadIdx.x == 0) { bi[0] = besti; bv[0] = best; }
+  }
+  __syncthreads();
+  const int p = bi[0];
+  if (threadIdx.x == 0 && !(bv[0] > 0.0)) *status = 1;  // singular
+  for (int j = threadIdx.x; j < w; j += blockDim.x) {
+    const double a = aug[size_t(k) * w + j], b = aug[size_t(p) * w + j];
+    aug[size_t(k) * w + j] = b;
+    aug[size_t(p) * w + j] = a;
+    rowk[j] = b;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) colk[i] = i == k ? 0.0 : aug[size_t(i) * w + k];
+}
+
+__global__ void k_gj_eliminate(int n, int k, double* __restrict__ aug, const double* __restrict__ rowk,
+                               const double* __restrict__ colk) {
+  const int w = 2 * n;
+  const double inv = 1.0 / rowk[k];
+  const int64_t tot = int64_t(n) * w;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(e / w), j = int(e % w);
+    const double r = rowk[j] * inv;
+    aug[e] = i == k ? r : aug[e] - colk[i] * r;
+  }
+}
+
+__global__ void k_gj_extract(int n, const double* __restrict__ aug, double* __restrict__ inv) {
+  const int64_t tot = int64_t(n) * n;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
+    const int j = int(e / n), i = int(e % n);  // column-major output
+    inv[e] = aug[size_t(i) * 2 * n + n + j];
+  }
+}
+
+__global__ void k_gj_init(int n, const double* __restrict__ A, double* __restrict__ aug) {
+  const int64_t tot = int64_t(n) * 2 * n;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(e / (2 * n)), j = int(e % (2 * n));
+    aug[e] = j < n ? A[size_t(i) * n + j] : (j - n == i ? 1.0 : 0.0);
+  }
+}
+
 // --------------------------------------------------------------- vectors
 __global__ void k_fill(double* x, double v, int64_t n) {
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) x[t] = v;
@@ -900,6 +974,32 @@ void dense_gemv(int n, const double* inv, const double* b, double* x, double* wo
   k_gemv_partial<<<grid, 128, 0, s>>>(n, inv, b, work);
   k_gemv_sum<<<(n + 127) / 128, 128, 0, s>>>(n, chunks, work, x);
   HPMG_LAUNCH_CHECK();
+}
+
+void dense_invert(int n, const double* A_rowmajor, double* inv_colmajor, cudaStream_t s) {
+  double *aug = nullptr, *rowk = nullptr, *colk = nullptr;
+  int* status = nullptr;
+  if (cudaMalloc(&aug, sizeof(double) * size_t(n) * 2 * n) != cudaSuccess ||
+      cudaMalloc(&rowk, sizeof(double) * 2 * n) != cudaSuccess || cudaMalloc(&colk, sizeof(double) * n) != cudaSuccess ||
+      cudaMalloc(&status, sizeof(int)) != cudaSuccess)
+    throw std::runtime_error("CUDA allocation failed (dense_invert)");
+  cudaMemsetAsync(status, 0, sizeof(int), s);
+  const int64_t tot = int64_t(n) * 2 * n;
+  k_gj_init<<<grid_for(tot, 256), 256, 0, s>>>(n, A_rowmajor, aug);
+  for (int k = 0; k < n; ++k) {
+    k_gj_pivot<<<1, 1024, 0, s>>>(n, k, aug, rowk, colk, status);
+    k_gj_eliminate<<<grid_for(tot, 256), 256, 0, s>>>(n, k, aug, rowk, colk);
+  }
+  k_gj_extract<<<grid_for(int64_t(n) * n, 256), 256, 0, s>>>(n, aug, inv_colmajor);
+  HPMG_LAUNCH_CHECK();
+  int hs = 0;
+  cudaMemcpyAsync(&hs, status, sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  cudaFree(aug);
+  cudaFree(rowk);
+  cudaFree(colk);
+  cudaFree(status);
+  if (hs) throw std::runtime_error("singular coarse operator");
 }
 
 void fill(double* x, double v, int64_t n, cudaStream_t s) {

@@ -113,6 +113,8 @@ void small_post(const Bsr& A, const PatchRecords& R, const int2* passes, int npa
 void prolong_add(const BlockCsr& P, const double* e, double* x, cudaStream_t s);
 void restrict_(const BlockCsr& PT, const double* r, double* rc, cudaStream_t s);
 void dense_gemv(int n, const double* inv_colmajor, const double* b, double* x, double* work, cudaStream_t s);
+/// Gauss-Jordan inverse with partial pivoting of a dense row-major matrix (setup).
+void dense_invert(int n, const double* A_rowmajor, double* inv_colmajor, cudaStream_t s);
 
 // vector kernels (n doubles)
 void fill(double* x, double v, int64_t n, cudaStream_t s);

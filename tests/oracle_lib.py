@@ -74,6 +74,22 @@ def lib():
                      "orc_mg_setup_seconds"]:
             getattr(L, name).argtypes = [P]
         L.orc_mg_time_apply.argtypes = [P, C.c_int]
+        # every handle-taking entry point gets an explicit void* first argument
+        # (an untyped Python int would be truncated to 32 bits)
+        L.orc_mg_rows.argtypes = [P, C.c_int]
+        L.orc_mg_nnz.argtypes = [P, C.c_int]
+        L.orc_mg_P_nnz.argtypes = [P, C.c_int]
+        L.orc_mg_csr.argtypes = [P, C.c_int, lp, lp, dp]
+        L.orc_mg_P_csr.argtypes = [P, C.c_int, lp, lp, dp]
+        L.orc_mg_rhs.argtypes = [P, dp]
+        L.orc_mg_free_to_full.argtypes = [P, lp]
+        L.orc_mg_g_full.argtypes = [P, dp]
+        L.orc_mg_apply.argtypes = [P, dp, dp]
+        L.orc_mg_spmv.argtypes = [P, dp, dp]
+        L.orc_mg_num_patches.argtypes = [P, C.c_int]
+        L.orc_mg_patches.argtypes = [P, C.c_int, lp, lp]
+        L.orc_mg_recover.argtypes = [P, dp, dp, dp, dp]
+        L.orc_mg_wind.argtypes = [P, dp, dp]
         _lib = L
     return _lib
 
