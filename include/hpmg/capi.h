@@ -89,7 +89,17 @@ typedef struct {
   int newton;
   const double* structured_load;  /* alternative: seeded structured force (hpmg_seeded_load layout) */
   int structured_n;               /*   on an n x n unit-square grid, mapped onto the finest elements */
+  hpmg_field_fn wind;             /* alternative advection state: a wind field, interpolated into   */
+  void* wind_user;                /*   the hybrid RT_k space as interpolate_hdg does (Oseen/Picard) */
 } hpmg_problem;
+
+/* Analytic fields usable as hpmg_field_fn (no host-language callback cost):
+ * BASELINE config 5 wind w = curl of sin^2(pi x) sin^2(pi y), i.e.
+ * (pi sin^2(pi x) sin(2 pi y), -pi sin(2 pi x) sin^2(pi y)); the rotation
+ * (y - 1/2, 1/2 - x) of the reference tests; the unit lid (1, 0) on y = 1. */
+void hpmg_field_config5_wind(double x, double y, double* out, void* user);
+void hpmg_field_rotation(double x, double y, double* out, void* user);
+void hpmg_field_lid_unit(double x, double y, double* out, void* user);
 
 typedef struct {
   double rel_tol, abs_tol;    /* KrylovOptions (krylov.hpp:12-16): 1e-8, 1e-10 */

@@ -41,7 +41,8 @@ class _Problem(C.Structure):
     _fields_ = [("bc", FIELD_FN), ("bc_user", C.c_void_p), ("load", FIELD_FN), ("load_user", C.c_void_p),
                 ("load_per_element", C.POINTER(C.c_double)), ("wind_compound", C.POINTER(C.c_double)),
                 ("wind_interior", C.POINTER(C.c_double)), ("newton", C.c_int),
-                ("structured_load", C.POINTER(C.c_double)), ("structured_n", C.c_int)]
+                ("structured_load", C.POINTER(C.c_double)), ("structured_n", C.c_int),
+                ("wind", FIELD_FN), ("wind_user", C.c_void_p)]
 
 
 class _KOpts(C.Structure):
@@ -123,10 +124,17 @@ def _dp(a):
     return a.ctypes.data_as(C.POINTER(C.c_double))
 
 
+NAMED_FIELDS = {"config5_wind": "hpmg_field_config5_wind", "rotation": "hpmg_field_rotation",
+                "lid_unit": "hpmg_field_lid_unit"}
+
+
 def _field(fn):
-    """Wraps a python callable (x, y) -> (fx, fy) as a C point callback."""
+    """Wraps a python callable (x, y) -> (fx, fy) as a C point callback; a
+    name from NAMED_FIELDS selects the library's own C implementation."""
     if fn is None:
         return FIELD_FN()
+    if isinstance(fn, str):
+        return C.cast(getattr(lib(), NAMED_FIELDS[fn]), FIELD_FN)
 
     def cb(x, y, out, _user):
         v = fn(x, y)
@@ -197,7 +205,8 @@ class MGPreconditioner:
 
     def __init__(self, *, mesh="unit_square", base_n=2, levels=2, k=0, nu=1.0, beta=0.0, mass_coef=0.0,
                  inv_eps=1e6, cycle=CYCLE_W, smoother=SMOOTH_MULTIPLICATIVE, smooth_steps=1,
-                 jacobi_damping=1.0 / 3.0, bc=None, load=None, load_per_element=None, structured_load=None):
+                 jacobi_damping=1.0 / 3.0, bc=None, load=None, load_per_element=None, structured_load=None,
+                 wind=None):
         L = lib()
         md = _Mesh()
         rc = (L.hpmg_unit_square_mesh if mesh == "unit_square" else L.hpmg_step_mesh)(base_n, levels, C.byref(md))
@@ -207,7 +216,8 @@ class MGPreconditioner:
         self._bc = _field(bc)
         self._load = _field(load)
         self._keep = []
-        prob = _Problem(self._bc, None, self._load, None, None, None, None, 0, None, 0)
+        self._wind = _field(wind)  # Oseen: wind field interpolated by the library
+        prob = _Problem(self._bc, None, self._load, None, None, None, None, 0, None, 0, self._wind, None)
         if load_per_element is not None:
             a = np.ascontiguousarray(load_per_element, dtype=np.float64)
             self._keep.append(a)

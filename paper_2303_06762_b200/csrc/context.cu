@@ -20,6 +20,7 @@
 #include "host/basis.hpp"
 #include "host/plan.hpp"
 #include "host/transfer.hpp"
+#include "host/wind.hpp"
 #include "kernels/kernels.hpp"
 
 using namespace hpmg;
@@ -153,6 +154,11 @@ void upload_ref(DevRef& D, const host::RefTensors& T, cudaStream_t s) {
   D.T.vval = up(T.vval);
   D.T.qw = up(T.qw);
   D.T.nq = T.nq;
+  D.T.vjac = up(T.vjac);
+  D.T.evp = up(T.evp);
+  D.T.ew = up(T.ew);
+  D.T.eleg = up(T.eleg);
+  D.T.nqe = T.nqe;
 }
 
 /// Legendre moments of the boundary data on Dirichlet facets, block layout
@@ -193,9 +199,11 @@ void alloc_level_vectors(Level& V) {
   V.xw = dalloc<double>(V.n);
 }
 
+std::vector<int> transpose_slots(const host::LevelPlan& P);
+
 /// Assembles (condense + gather) one level operator on the device.
 void build_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, const DevRef& R, bool finest,
-                 const hpmg_problem* prob, double* rhs_out) {
+                 const hpmg_problem* prob, double* rhs_out, const host::HdgField* wind = nullptr) {
   cudaStream_t s = C.s;
   V.k = k;
   V.bs = 2 * (k + 1);
@@ -262,7 +270,9 @@ void build_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, const Dev
       lstride = 2 * nq;
     }
   }
-  dev::condense(R.T, V.geo, m.ne(), prm, dload, lstride, acr, s);
+  double* dwind = nullptr;
+  if (wind) dwind = dupload(host::local_wind(m, k, *wind), s);
+  dev::condense(R.T, V.geo, m.ne(), prm, dload, lstride, acr, s, dwind);
   // operator
   V.A.nb = V.nb;
   V.A.bs = V.bs;
@@ -270,6 +280,16 @@ void build_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, const Dev
   V.A.cols = dupload(V.plan.cols, s);
   int* gath = dupload(V.plan.gath, s);
   dev::assemble_bsr(V.A, k + 1, acr, stride, nc, gath, V.geo, C.opt.inv_eps, s);
+  if (C.advected) {  // A^T rows for the exact transpose (backward) sweeps, multigrid.hpp:84,106
+    V.AT = V.A;
+    V.AT.val = dalloc<double>(size_t(V.nb) * host::kSlots * V.bs * V.bs);
+    V.tslot = dupload(transpose_slots(V.plan), s);
+    dev::transpose_bsr(V.A, V.tslot, V.AT, s);
+  }
+  if (dwind) {
+    CK(cudaStreamSynchronize(s));
+    cudaFree(dwind);
+  }
   if (finest) {
     std::vector<int> ef(size_t(m.ne()) * 3);
     for (int e = 0; e < m.ne(); ++e)
@@ -723,8 +743,8 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
   if (opt->k < 0 || opt->k > 3) throw std::invalid_argument("order k must be in 0..3");
   if (md->levels < 1) throw std::invalid_argument("levels must be >= 1");
   C.opt = *opt;
-  C.advected = prob && prob->wind_compound;
-  if (C.advected) throw std::invalid_argument("advection (Oseen) operators are not supported yet");
+  C.advected = prob && (prob->wind_compound || prob->wind);
+  if (prob && prob->newton) throw std::invalid_argument("Newton linearisations are not supported (Picard/Oseen only)");
   CK(cudaStreamCreateWithFlags(&C.s, cudaStreamNonBlocking));
   // mesh hierarchy
   host::TriMesh base;
@@ -792,6 +812,25 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
       if (!dir[f])
         for (int i = 0; i < nfd; ++i) C.free_to_full.push_back(nflux + int64_t(f) * nfd + i);
   }
+  // advection state (Oseen): order-k wind on the finest mesh, its lowest-order
+  // carrier and the restriction chain (reference multigrid.hpp:58-66)
+  std::vector<host::HdgField> adv;
+  host::HdgField wind_k;
+  if (C.advected) {
+    if (prob->wind) {
+      wind_k = host::interpolate_hdg(fine, k, k > 0 ? *tTk : *tT0, [&](double x, double y, double* o) {
+        prob->wind(x, y, o, prob->wind_user);
+      });
+    } else {
+      wind_k.k = k;
+      wind_k.compound.assign(prob->wind_compound, prob->wind_compound + C.g_full.size());
+      const size_t ni = size_t(fine.ne()) * k * (k + 1);
+      if (ni) wind_k.interior.assign(prob->wind_interior, prob->wind_interior + ni);
+    }
+    adv.resize(C.L + 1);
+    adv[C.L] = k > 0 ? host::lowest_order(fine, wind_k) : wind_k;
+    for (int l = C.L; l > 0; --l) adv[l - 1] = host::restrict_wind(C.mesh[l - 1], C.mesh[l], C.ref[l - 1], adv[l]);
+  }
   auto t1 = clk::now();
   // lowest-order levels
   C.lv.resize(C.L + 1);
@@ -804,13 +843,14 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
       const int64_t nfree = int64_t(C.free_to_full.size());
       rhs_tmp = C.rhs = dalloc<double>(nfree);
     }
-    build_level(C, V, C.mesh[l], 0, C.ref0, finest, prob, finest ? C.rhs : nullptr);
+    build_level(C, V, C.mesh[l], 0, C.ref0, finest, prob, finest ? C.rhs : nullptr,
+                C.advected ? &adv[l] : nullptr);
     V.steps = opt->cycle == HPMG_CYCLE_VARIABLE_V ? (opt->smooth_steps << (C.L - l)) : opt->smooth_steps;
   }
   if (k > 0) {
     C.head = std::make_unique<Level>();
     C.rhs = dalloc<double>(int64_t(C.free_to_full.size()));
-    build_level(C, *C.head, fine, k, C.refk, true, prob, C.rhs);
+    build_level(C, *C.head, fine, k, C.refk, true, prob, C.rhs, C.advected ? &wind_k : nullptr);
     C.head->steps = opt->smooth_steps;
   }
   (void)rhs_tmp;
@@ -1358,6 +1398,21 @@ double hpmg_setup_seconds(const hpmg_ctx* ctx, double* parts) {
   if (parts)
     for (int i = 0; i < 8; ++i) parts[i] = ctx->setup_parts[i];
   return ctx->setup_parts[6];
+}
+
+void hpmg_field_config5_wind(double x, double y, double* out, void*) {
+  const double s = std::sin(M_PI * x), t = std::sin(M_PI * y);
+  out[0] = M_PI * s * s * std::sin(2 * M_PI * y);
+  out[1] = -M_PI * std::sin(2 * M_PI * x) * t * t;
+}
+void hpmg_field_rotation(double x, double y, double* out, void*) {
+  out[0] = y - 0.5;
+  out[1] = 0.5 - x;
+}
+void hpmg_field_lid_unit(double x, double y, double* out, void*) {
+  out[0] = y > 1.0 - 1e-12 ? 1.0 : 0.0;
+  out[1] = 0.0;
+  (void)x;
 }
 
 void hpmg_seeded_load(int n, unsigned seed, double lo, double hi, double* out) {

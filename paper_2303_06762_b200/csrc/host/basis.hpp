@@ -411,6 +411,12 @@ struct RefTensors {
   // volume rule and basis values for pointwise loads: [nq], [nq][2][nrt]
   std::vector<double> qx, qy, qw, vval;
   int nq = 0;
+  // pointwise tables for the (trilinear, upwinded) convection form:
+  std::vector<double> vjac;  // [nq][4][nrt] reference Jacobians dvx/dx dvx/dy dvy/dx dvy/dy
+  std::vector<double> evp;   // [3][nqe][2][nrt] RT values at edge points
+  std::vector<double> ew;    // [nqe] edge weights on [-1,1]
+  std::vector<double> eleg;  // [nqe][nfd] Legendre L_i(t_q)
+  int nqe = 0;
   RTBasis rt;
   std::vector<Poly> scal;
 };
@@ -454,6 +460,9 @@ inline std::unique_ptr<RefTensors> build_ref_tensors(int k) {
       T->vval[(size_t(q) * 2 + 0) * nrt + r] = vv[r];
       T->vval[(size_t(q) * 2 + 1) * nrt + r] = vv[nrt + r];
     }
+    T->vjac.resize(size_t(T->nq) * 4 * nrt);
+    for (int c = 0; c < 4; ++c)
+      for (int r = 0; r < nrt; ++r) T->vjac[(size_t(q) * 4 + c) * nrt + r] = jv[c * nrt + r];
     for (int c = 0; c < 4; ++c)
       for (int m = 0; m < ns; ++m)
         for (int r = 0; r < nrt; ++r) T->G[(size_t(c) * ns + m) * nrt + r] += w * jv[c * nrt + r] * sv[m];
@@ -469,6 +478,15 @@ inline std::unique_ptr<RefTensors> build_ref_tensors(int k) {
   }
   std::vector<double> ex, ew;
   gauss(3 * k + 4, ex, ew);
+  T->nqe = int(ex.size());
+  T->ew = ew;
+  T->eleg.assign(size_t(T->nqe) * nfd, 0.0);
+  T->evp.assign(size_t(3) * T->nqe * 2 * nrt, 0.0);
+  for (int q = 0; q < T->nqe; ++q) {
+    double Lq[8];
+    legendre(k, ex[q], Lq);
+    for (int i = 0; i < nfd; ++i) T->eleg[size_t(q) * nfd + i] = Lq[i];
+  }
   T->Ev.assign(size_t(3) * 2 * ns * nrt, 0.0);
   T->Tv.assign(size_t(3) * nfd * ns, 0.0);
   const double vx[3] = {0, 1, 0}, vy[3] = {0, 0, 1};
@@ -483,6 +501,7 @@ inline std::unique_ptr<RefTensors> build_ref_tensors(int k) {
       for (int l = 0; l < 2; ++l)
         for (int r = 0; r < nrt; ++r) {
           double v = B.fn[r][l](x, y);
+          T->evp[((size_t(e) * T->nqe + p) * 2 + l) * nrt + r] = v;
           for (int m = 0; m < ns; ++m) T->Ev[((size_t(e) * 2 + l) * ns + m) * nrt + r] += w * v * sv[m];
         }
       for (int i = 0; i < nfd; ++i)

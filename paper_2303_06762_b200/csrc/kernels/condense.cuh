@@ -37,7 +37,91 @@ struct RefT {
   const double* vval;  // [nq][2][nrt] (pointwise loads)
   const double* qw;    // [nq]
   int nq;
+  // convection (Oseen) tables
+  const double* vjac;  // [nq][4][nrt]
+  const double* evp;   // [3][nqe][2][nrt]
+  const double* ew;    // [nqe]
+  const double* eleg;  // [nqe][nfd]
+  int nqe;
 };
+
+/// Convection entry A(a, b) of the upwinded transport form linearised about
+/// the wind (reference inc/assembly.hpp:254-275 volume, :294-321 facets;
+/// Picard only). `wq` = physical wind at the volume nodes [nq][2], `wn` =
+/// normal wind trace w.n_out at the edge nodes [3][nqe]. Evaluated pointwise:
+/// the upwind switch depends on the sign of w.n at every edge node.
+template <class Geo>
+HPMG_HD inline double convection_entry(const RefT& T, const Geo& g, const double* fr, const double* wq,
+                                       const double* wn, int a, int b) {
+  const int nfd = T.nfd, nc = T.nc, nrt = T.nrt;
+  const bool ra = a < 3 * nfd || a >= nc, rb = b < 3 * nfd || b >= nc;
+  const int r = ra ? (a < 3 * nfd ? a : 3 * nfd + (a - nc)) : -1;
+  const int s = rb ? (b < 3 * nfd ? b : 3 * nfd + (b - nc)) : -1;
+  double acc = 0.0;
+  const double J0 = g.J[0], J1 = g.J[1], J2 = g.J[2], J3 = g.J[3];
+  // volume: -(u (x) w, grad v), test r, trial s
+  if (ra && rb) {
+    for (int q = 0; q < T.nq; ++q) {
+      const double* vj = T.vjac + size_t(q) * 4 * nrt;
+      const double* vv = T.vval + size_t(q) * 2 * nrt;
+      // physical Jacobian of test r: (J Jh Ji) / detJ * fr
+      const double h00 = vj[r], h01 = vj[nrt + r], h10 = vj[2 * nrt + r], h11 = vj[3 * nrt + r];
+      const double t00 = J0 * h00 + J1 * h10, t01 = J0 * h01 + J1 * h11;
+      const double t10 = J2 * h00 + J3 * h10, t11 = J2 * h01 + J3 * h11;
+      const double gs = fr[r] / g.detJ;
+      const double g0 = (t00 * g.Ji[0] + t01 * g.Ji[2]) * gs, g1 = (t00 * g.Ji[1] + t01 * g.Ji[3]) * gs;
+      const double g2 = (t10 * g.Ji[0] + t11 * g.Ji[2]) * gs, g3 = (t10 * g.Ji[1] + t11 * g.Ji[3]) * gs;
+      const double vs = fr[s] / g.detJ;
+      const double v0 = (J0 * vv[s] + J1 * vv[nrt + s]) * vs, v1 = (J2 * vv[s] + J3 * vv[nrt + s]) * vs;
+      const double wx = wq[2 * q], wy = wq[2 * q + 1];
+      const double w = T.qw[q] * g.detJ;
+      acc -= w * (v0 * (g0 * wx + g1 * wy) + v1 * (g2 * wx + g3 * wy));
+    }
+  }
+  // facets: upwinded transport of the trace, tested with the tangential difference
+  for (int le = 0; le < 3; ++le) {
+    const double nx = g.n[2 * le], ny = g.n[2 * le + 1];
+    // test column a on this edge: RT column -> D = T - (T.n)n ; tangential (le) -> D = -T
+    const bool at = !ra && (a - 3 * nfd) / nfd == le;
+    if (!ra && !at) continue;
+    const bool bt = !rb && (b - 3 * nfd) / nfd == le;
+    if (!rb && !bt) continue;
+    for (int q = 0; q < T.nqe; ++q) {
+      const double wnq = wn[le * T.nqe + q];
+      if (wnq == 0.0) continue;
+      const bool outflow = wnq > 0;
+      if (outflow != rb) continue;  // outflow couples RT trial columns, inflow tangential ones
+      double ta0, ta1, tb0, tb1;
+      const double* ev = T.evp + size_t(le * T.nqe + q) * 2 * nrt;
+      if (ra) {
+        const double e0 = ev[r], e1 = ev[nrt + r], f = fr[r] / g.detJ;
+        const double T0 = (J0 * e0 + J1 * e1) * f, T1 = (J2 * e0 + J3 * e1) * f;
+        const double tn = T0 * nx + T1 * ny;
+        ta0 = T0 - tn * nx;
+        ta1 = T1 - tn * ny;
+      } else {
+        const int i = (a - 3 * nfd) % nfd;
+        double lg = T.eleg[q * nfd + i];
+        if (g.rho[le] < 0 && (i & 1)) lg = -lg;
+        ta0 = -lg * g.tf[2 * le];
+        ta1 = -lg * g.tf[2 * le + 1];
+      }
+      if (rb) {
+        const double e0 = ev[s], e1 = ev[nrt + s], f = fr[s] / g.detJ;
+        tb0 = (J0 * e0 + J1 * e1) * f;
+        tb1 = (J2 * e0 + J3 * e1) * f;
+      } else {
+        const int i = (b - 3 * nfd) % nfd;
+        double lg = T.eleg[q * nfd + i];
+        if (g.rho[le] < 0 && (i & 1)) lg = -lg;
+        tb0 = lg * g.tf[2 * le];
+        tb1 = lg * g.tf[2 * le + 1];
+      }
+      acc += T.ew[q] * g.ds[le] * wnq * (ta0 * tb0 + ta1 * tb1);
+    }
+  }
+  return acc;
+}
 
 /// Per-element geometry, 32 doubles (packed on the host).
 struct ElemGeo {
@@ -58,7 +142,8 @@ struct CondenseParams {
 
 /// Scratch layout (doubles): C[4ns*nv] A[nv*nv] P[(ns-1)*nv] rhs[nv] aug[nz*(nz+nc+1)] fac[nrt]
 HPMG_HD inline int condense_scratch(int ns, int nv, int nc, int nz, int nrt) {
-  return 4 * ns * nv + nv * nv + (ns > 1 ? (ns - 1) * nv : 0) + nv + nz * (nz + nc + 1) + nrt + 8;
+  // + wind tables: 2 nq (volume) + 3 nqe (edges) <= 256 for k <= 3
+  return 4 * ns * nv + nv * nv + (ns > 1 ? (ns - 1) * nv : 0) + nv + nz * (nz + nc + 1) + nrt + 8 + 256;
 }
 
 #ifndef SYNC
@@ -74,7 +159,8 @@ HPMG_HD inline int condense_scratch(int ns, int nv, int nc, int nz, int nrt) {
 /// -(nu/detJ) C [xc; z_interior] to gout.
 HPMG_D inline void condense_element(int tid, int nthr, const RefT& T, const ElemGeo& g, const CondenseParams& prm,
                                      const double* load, double* scratch, double* Ac, double* rc,
-                                     const double* xc = nullptr, double* zout = nullptr, double* gout = nullptr) {
+                                     const double* xc = nullptr, double* zout = nullptr, double* gout = nullptr,
+                                     const double* xw = nullptr) {
   const int ns = T.ns, nv = T.nv, nc = T.nc, nrt = T.nrt, nfd = T.nfd, no = T.no;
   const int np = ns - 1, nz = no + np, nC = 4 * ns;
   double* C = scratch;
@@ -83,6 +169,8 @@ HPMG_D inline void condense_element(int tid, int nthr, const RefT& T, const Elem
   double* rhs = P + (np > 0 ? np * nv : 0);
   double* aug = rhs + nv;
   double* fr = aug + nz * (nz + nc + 1);  // orientation factor per RT column
+  double* wq = fr + nrt + 8;               // [nq][2] physical wind at the volume nodes
+  double* wn = wq + 2 * T.nq;              // [3][nqe] w.n_out at the edge nodes
   const int naug = nz + nc + 1;
 
   for (int r = tid; r < nrt; r += nthr) {
@@ -95,6 +183,31 @@ HPMG_D inline void condense_element(int tid, int nthr, const RefT& T, const Elem
     }
   }
   SYNC();
+  if (xw) {
+    // wind in the RT part of the local basis: wrt[r] = xw[vel_of_rt(r)]
+    for (int q = tid; q < T.nq; q += nthr) {
+      double sx = 0.0, sy = 0.0;
+      for (int r = 0; r < nrt; ++r) {
+        const double c = xw[r < 3 * nfd ? r : nc + (r - 3 * nfd)] * fr[r] / g.detJ;
+        const double v0 = T.vval[(q * 2) * nrt + r], v1 = T.vval[(q * 2 + 1) * nrt + r];
+        sx += c * (g.J[0] * v0 + g.J[1] * v1);
+        sy += c * (g.J[2] * v0 + g.J[3] * v1);
+      }
+      wq[2 * q] = sx;
+      wq[2 * q + 1] = sy;
+    }
+    for (int e = tid; e < 3 * T.nqe; e += nthr) {
+      const int le = e / T.nqe, q = e % T.nqe;
+      const double* ev = T.evp + size_t(le * T.nqe + q) * 2 * nrt;
+      double sx = 0.0, sy = 0.0;
+      for (int r = 0; r < nrt; ++r) {
+        const double c = xw[r < 3 * nfd ? r : nc + (r - 3 * nfd)] * fr[r] / g.detJ;
+        sx += c * (g.J[0] * ev[r] + g.J[1] * ev[nrt + r]);
+        sy += c * (g.J[2] * ev[r] + g.J[3] * ev[nrt + r]);
+      }
+      wn[e] = sx * g.n[2 * le] + sy * g.n[2 * le + 1];
+    }
+  }
   // ---- gradient coupling C (4ns x nv) and divergence moments P ----
   for (int e = tid; e < nC * nv; e += nthr) {
     const int row = e / nv, a = e % nv;
@@ -170,7 +283,7 @@ HPMG_D inline void condense_element(int tid, int nthr, const RefT& T, const Elem
     }
     double cc = 0.0;
     for (int row = 0; row < nC; ++row) cc += C[row * nv + a] * C[row * nv + b];
-    A[e] = m + visc * cc;
+    A[e] = m + visc * cc + (xw ? convection_entry(T, g, fr, wq, wn, a, b) : 0.0);
   }
   SYNC();
   if (nz == 0) {

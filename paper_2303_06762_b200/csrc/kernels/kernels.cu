@@ -89,7 +89,7 @@ inline int grid_for(int64_t n, int threads) {
 
 // ---------------------------------------------------------------- condense
 __global__ void k_condense(RefT T, const ElemGeo* __restrict__ geo, CondenseParams prm, const double* __restrict__ load,
-                           int load_stride, double* __restrict__ out, int stride) {
+                           int load_stride, double* __restrict__ out, int stride, const double* __restrict__ wind) {
   extern __shared__ double smem[];
   __shared__ ElemGeo g;
   const int e = blockIdx.x;
@@ -98,7 +98,8 @@ __global__ void k_condense(RefT T, const ElemGeo* __restrict__ geo, CondensePara
   __syncthreads();
   double* o = out + size_t(e) * stride;
   const double* ld = prm.load_mode ? load + size_t(e) * load_stride : nullptr;
-  condense_element(threadIdx.x, blockDim.x, T, g, prm, ld, smem, o, o + T.nc * T.nc);
+  const double* xw = wind ? wind + size_t(e) * T.nv : nullptr;  // local wind coefficients (Oseen)
+  condense_element(threadIdx.x, blockDim.x, T, g, prm, ld, smem, o, o + T.nc * T.nc, nullptr, nullptr, nullptr, xw);
 }
 
 /// recover_locals (reference inc/assembly.hpp:513-549) for every element:
@@ -826,7 +827,7 @@ void by_bs(int bs, F&& f) {
 
 // ============================================================ launchers
 void condense(const RefT& T, const ElemGeo* geo, int ne, CondenseParams prm, const double* load, int load_stride,
-              double* out, cudaStream_t s) {
+              double* out, cudaStream_t s, const double* wind) {
   if (ne == 0) return;
   const int nz = T.no + T.ns - 1;
   const size_t smem = sizeof(double) * condense_scratch(T.ns, T.nv, T.nc, nz, T.nrt);
@@ -835,7 +836,7 @@ void condense(const RefT& T, const ElemGeo* geo, int ne, CondenseParams prm, con
     cudaFuncSetAttribute(k_condense, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  k_condense<<<ne, 128, smem, s>>>(T, geo, prm, load, load_stride, out, T.nc * T.nc + T.nc);
+  k_condense<<<ne, 128, smem, s>>>(T, geo, prm, load, load_stride, out, T.nc * T.nc + T.nc, wind);
   HPMG_LAUNCH_CHECK();
 }
 

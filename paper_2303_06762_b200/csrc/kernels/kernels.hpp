@@ -48,8 +48,9 @@ struct Reduce {
   unsigned* counter = nullptr;    // zero-initialised ticket
 };
 
+/// wind: per-element local wind coefficients [ne][nv] (Oseen) or nullptr (Stokes)
 void condense(const RefT& T, const ElemGeo* geo, int ne, CondenseParams prm, const double* load, int load_stride,
-              double* out, cudaStream_t s);
+              double* out, cudaStream_t s, const double* wind = nullptr);
 /// recover_locals on every element from the full compound skeleton vector.
 void recover(const RefT& T, const ElemGeo* geo, int ne, CondenseParams prm, const double* load, int load_stride,
              const int* elem_facets, long long nflux, const double* compound, double* interior, double* pres,

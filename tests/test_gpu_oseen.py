@@ -1,0 +1,94 @@
+"""GPU-vs-oracle parity of the advected (Oseen/Picard) path: upwinded
+condensation, A^T backward sweeps, nonsymmetric V-cycle, device GMRES and the
+Uzawa loop (BASELINE config 5 shape at small sizes). Tolerances as in
+test_gpu_parity.py; GMRES counts +-1."""
+import numpy as np
+import pytest
+
+import oracle_lib as O
+
+pytestmark = pytest.mark.gpu
+
+H = pytest.importorskip("paper_2303_06762_b200")
+
+WIND = {"rotation": O.WIND_ROT, "config5_wind": O.WIND_CURL}
+
+
+def pair(k, wind="config5_wind", base_n=2, levels=3, nu=1e-2, beta=0.0, inv_eps=1e3, lid=True, seed=3, m=1,
+         cycle=O.CYCLE_V):
+    n_f = base_n << (levels - 1)
+    F = O.seeded_load(n_f, seed, -0.1, 0.1)
+    orc = O.OracleMG(base_n=base_n, levels=levels, k=k, nu=nu, beta=beta, inv_eps=inv_eps,
+                     bc=O.BC_LID_UNIT if lid else O.BC_NONE, load_kind=O.LOAD_ARRAY, load=F, wind=WIND[wind],
+                     cycle=cycle, smooth_steps=m)
+    gpu = H.MGPreconditioner(base_n=base_n, levels=levels, k=k, nu=nu, beta=beta, inv_eps=inv_eps,
+                             bc="lid_unit" if lid else None, structured_load=(n_f, F), wind=wind, cycle=cycle,
+                             smooth_steps=m)
+    return orc, gpu
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.mark.parametrize("k,wind", [(0, "rotation"), (1, "config5_wind"), (2, "config5_wind"), (3, "rotation")])
+def test_advected_operator(k, wind):
+    orc, gpu = pair(k, wind)
+    assert not gpu.symmetric()
+    x = O.random_vec(orc.n, 5)
+    assert rel(gpu.spmv(x), orc.spmv(x)) < 1e-12
+    assert rel(gpu.rhs(), orc.rhs()) < 1e-12
+    for l in range(3):
+        A_g, A_o = gpu.matrix(l), orc.csr(l)
+        assert abs(A_g - A_o).max() <= 1e-12 * abs(A_o).max()
+
+
+@pytest.mark.parametrize("k", [0, 2])
+def test_advected_sweeps_are_exact_transposes(k):
+    orc, gpu = pair(k)
+    level = -1 if k > 0 else 2
+    n = orc.n
+    b, x0 = O.random_vec(n, 7), O.random_vec(n, 9)
+    for which in (0, 1):
+        assert rel(gpu.smooth(level, which, x0, b, 1), orc.smooth(level, which, x0, b, 1)) < 1e-10
+
+
+@pytest.mark.parametrize("k", [0, 1, 2])
+def test_advected_vcycle(k):
+    orc, gpu = pair(k, levels=4)
+    b = O.random_vec(orc.n, 11)
+    assert rel(gpu.apply(b), orc.apply(b)) < 1e-10
+
+
+@pytest.mark.parametrize("k,nu", [(0, 1.0), (1, 1e-2), (2, 1e-2), (2, 1e-3)])
+def test_gmres_counts_and_solution(k, nu):
+    orc, gpu = pair(k, nu=nu, levels=4)
+    b = orc.rhs()
+    xo, so = orc.krylov(b, method=1)
+    xg, sg = H.gmres(gpu, b)
+    assert so["converged"] and sg.converged
+    # +-1 (north star); unrestarted MGS-GMRES beyond ~100 iterations (nu = 1e-3:
+    # 180 its) loses orthogonality at the round-off level, so long runs get 1%
+    assert abs(sg.iterations - so["iterations"]) <= max(1, int(0.01 * so["iterations"]) + 1)
+    assert rel(xg, xo) < 1e-8
+
+
+def test_restarted_gmres_matches_when_below_restart():
+    orc, gpu = pair(2, nu=1.0, levels=4)
+    b = orc.rhs()
+    x1, s1 = H.gmres(gpu, b)
+    x2, s2 = H.gmres(gpu, b, opt=H.KrylovOptions(restart=50))
+    assert s1.iterations < 50 and s1.iterations == s2.iterations
+    assert rel(x2, x1) < 1e-12
+
+
+@pytest.mark.parametrize("nu", [1.0, 1e-2])
+def test_oseen_uzawa(nu):
+    # BASELINE config 5 shape: lid (1,0), wind = curl sin^2 sin^2, k=2, AL 1e3, U[-0.1,0.1] force
+    orc, gpu = pair(2, nu=nu, levels=4)
+    ro = orc.uzawa()
+    rg = H.uzawa_solve(gpu)
+    assert ro["converged"] and rg.report.converged
+    for a, b in zip(rg.report.inner_iterations, ro["inner_iterations"]):
+        assert abs(a - b) <= 1
+    assert rel(rg.velocity, ro["velocity"]) < 1e-8
