@@ -179,6 +179,8 @@ int hpmg_kernel_launches_per_apply(const hpmg_ctx* ctx);
  * solve, out[2l] / out[2l+1] pre / post part of level l, out[2L+2..2L+4] head
  * pre-sweep, head residual, head post-sweep (ms). Returns the entry count. */
 int hpmg_profile_levels(hpmg_ctx* ctx, int reps, double* out);
+/* Development hook: clock64 timeline of the one-CTA small-level sweep. */
+void hpmg_debug_small_trace(int arm, long long* out);
 double hpmg_setup_seconds(const hpmg_ctx* ctx, double* parts);
 
 /* Seeded per-triangle force of the BASELINE configs: std::mt19937(seed) and

@@ -8,6 +8,7 @@
 
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <random>
@@ -40,6 +41,12 @@ T* dalloc(size_t n) {
   void* p = nullptr;
   if (n == 0) n = 1;
   CK(cudaMalloc(&p, n * sizeof(T)));
+  // HPMG_POISON=1: every allocation starts as NaN / -1 bytes (uninitialised-read check)
+  static const bool poison = std::getenv("HPMG_POISON") != nullptr;
+  if (poison) {
+    CK(cudaMemset(p, 0xff, n * sizeof(T)));
+    CK(cudaDeviceSynchronize());  // ordered before any non-blocking-stream use
+  }
   return static_cast<T*>(p);
 }
 template <typename T>
@@ -68,7 +75,8 @@ struct Level {
   std::vector<int> wave_ptr;
   int* d_wave_ptr = nullptr;
   dev::PatchRecords rec;
-  bool small = false;  // whole pre/post phase in one CTA (small_levels.cu)
+  dev::PatchRecords srec;  // full-inverse records of the one-CTA path
+  bool small = false;      // whole pre/post phase in one CTA (small_levels.cu)
   int2* d_passes = nullptr;
   int npass = 0;
   dev::BlockCsr Pm, PT;  // from level l-1 to l (lowest-order levels l >= 1)
@@ -349,7 +357,14 @@ void build_patch_inverses(hpmg_ctx& C, Level& V) {
     for (size_t w = 0; w + 1 < V.wave_ptr.size(); ++w)
       for (int a = V.wave_ptr[w]; a < V.wave_ptr[w + 1]; a += pp)
         passes.push_back(make_int2(a, std::min(pp, V.wave_ptr[w + 1] - a)));
-    if (V.k == 0 && dev::small_level_fits(V.nb, V.rec.stride, int(passes.size()))) {
+    // one-CTA path only where the wave count (not the width) dominates: level 1
+    // of a coarse base mesh (26 / 50 waves); refined levels have 9 wide waves
+    const int nwaves = int(V.wave_ptr.size()) - 1;
+    const dev::PatchRecords full = dev::record_layout(V.bs, V.max_nf, true);
+    if (V.k == 0 && nwaves > 12 && dev::small_level_fits(V.nb, full.stride, int(passes.size()))) {
+      V.srec = full;
+      V.srec.rec = dalloc<double>(size_t(V.P.n) * V.srec.stride);
+      dev::build_records(V.A, V.P, V.srec, C.s);
       V.npass = int(passes.size());
       V.d_passes = dupload(passes, C.s);
       V.small = true;
@@ -508,10 +523,10 @@ void h_cycle(hpmg_ctx& C, int l, const double* b, double* x) {
   const int q = C.opt.cycle == HPMG_CYCLE_W ? 2 : 1;
   if (V.small && C.opt.smoother == HPMG_SMOOTH_MULTIPLICATIVE && q == 1) {
     // whole-level sweeps in one persistent CTA (small_levels.cu)
-    dev::small_pre(V.A, V.rec, V.d_passes, V.npass, V.steps, V.PT, b, x, W.b, C.s);
+    dev::small_pre(V.A, V.srec, V.d_passes, V.npass, V.steps, V.PT, b, x, W.b, C.s);
     count(C);
     h_cycle(C, l - 1, W.b, W.x);
-    dev::small_post(V.A, V.rec, V.d_passes, V.npass, V.steps, V.Pm, W.x, b, x, C.s);
+    dev::small_post(V.A, V.srec, V.d_passes, V.npass, V.steps, V.Pm, W.x, b, x, C.s);
     count(C);
     return;
   }
@@ -905,6 +920,7 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
     double* dA = dupload(D, C.s);
     C.coarse_inv = dalloc<double>(size_t(C.n0) * C.n0);
     dev::dense_invert(C.n0, dA, C.coarse_inv, C.s);
+    CK(cudaStreamSynchronize(C.s));
     cudaFree(dA);
     C.gemv_work = dalloc<double>(size_t(C.n0) * ((C.n0 + 63) / 64 + 1));  // kGemvChunk = 64
   }
@@ -982,7 +998,7 @@ void hpmg_destroy(hpmg_ctx* ctx) {
                     (void*)V->Pm.ptr, (void*)V->Pm.col, (void*)V->Pm.val, (void*)V->PT.ptr, (void*)V->PT.col,
                     (void*)V->PT.val, (void*)V->x, (void*)V->b, (void*)V->r, (void*)V->y, (void*)V->bw, (void*)V->xw,
                     (void*)V->dbuf, (void*)V->geo, (void*)V->row_elems, (void*)V->elem_facets, (void*)V->facet_block,
-                    (void*)V->d_wave_ptr, (void*)V->rec.rec, (void*)V->d_passes})
+                    (void*)V->d_wave_ptr, (void*)V->rec.rec, (void*)V->srec.rec, (void*)V->d_passes})
       fr(p);
   };
   for (auto& V : ctx->lv) free_level(V.get());
@@ -1306,6 +1322,10 @@ double hpmg_time_apply(hpmg_ctx* ctx, int reps, double* phase_ms) {
 
 int hpmg_kernel_launches_per_apply(const hpmg_ctx* ctx) { return ctx->launches_per_apply; }
 
+/// Development hook: arm (1) / disarm (0) the one-CTA sweep timeline and copy
+/// it out (4096 clock64 stamps: per pass start, data ready, residual done, end).
+void hpmg_debug_small_trace(int arm, long long* out) { dev::small_trace(arm, out); }
+
 /// Event-instrumented V-cycle (no graph): out[2l], out[2l+1] = pre/post part
 /// of level l (l = 1..L) in ms, out[0] = coarse solve, out[2(L+1)..+2] = head
 /// pre-sweep, residual+embed, post-sweep. Returns the number of entries.
@@ -1346,7 +1366,7 @@ int hpmg_profile_levels(hpmg_ctx* ctx, int reps, double* out) {
         Level& V = *C.lv[l];
         Level& W = *C.lv[l - 1];
         if (V.small) {
-          dev::small_pre(V.A, V.rec, V.d_passes, V.npass, V.steps, V.PT, bs[l], xs[l], W.b, C.s);
+          dev::small_pre(V.A, V.srec, V.d_passes, V.npass, V.steps, V.PT, bs[l], xs[l], W.b, C.s);
         } else {
           dev::fill(xs[l], 0.0, V.n, C.s);
           smooth(C, V, xs[l], bs[l], false);
@@ -1363,7 +1383,7 @@ int hpmg_profile_levels(hpmg_ctx* ctx, int reps, double* out) {
         Level& V = *C.lv[l];
         Level& W = *C.lv[l - 1];
         if (V.small) {
-          dev::small_post(V.A, V.rec, V.d_passes, V.npass, V.steps, V.Pm, W.x, bs[l], xs[l], C.s);
+          dev::small_post(V.A, V.srec, V.d_passes, V.npass, V.steps, V.Pm, W.x, bs[l], xs[l], C.s);
         } else {
           dev::prolong_add(V.Pm, W.x, xs[l], C.s);
           smooth(C, V, xs[l], bs[l], true);

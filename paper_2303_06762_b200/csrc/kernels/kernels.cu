@@ -725,8 +725,9 @@ __global__ void k_pcg_direction(double* __restrict__ p, const double* __restrict
 __global__ void k_scal_axpby(double* __restrict__ y, const double* __restrict__ x, int64_t n, const double* sc, int ia,
                              double fa, double fb) {
   const double a = (ia >= 0 ? sc[ia] : 1.0) * fa;
+  // fb == 0 overwrites y without reading it (fresh GMRES basis vectors hold garbage, 0 * NaN = NaN)
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x)
-    y[t] = a * x[t] + fb * y[t];
+    y[t] = fb == 0.0 ? a * x[t] : a * x[t] + fb * y[t];
 }
 
 __global__ void k_to_blocks(int nb, int nfd, const double* __restrict__ ref, double* __restrict__ blk) {

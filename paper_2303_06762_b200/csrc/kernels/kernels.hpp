@@ -83,8 +83,9 @@ struct PatchRecords {
   double* rec = nullptr;
   int bs = 2, max_nf = 0;
   int stride = 0, a_off = 0, meta_off = 0;  // in doubles
+  int full = 0;  // 1: full np x np column-major inverse instead of the packed triangle
 };
-PatchRecords record_layout(int bs, int max_nf);
+PatchRecords record_layout(int bs, int max_nf, bool full = false);
 void build_records(const Bsr& A, const Patches& P, PatchRecords& R, cudaStream_t s);
 /// One symmetric wave over the patch records [w0, w1) (one TMA per CTA).
 void gs_wave_rec(const PatchRecords& R, int w0, int w1, const double* b, double* x, cudaStream_t s);
@@ -105,6 +106,7 @@ void jacobi_combine(int nb, int bs, const Patches& P, const double* d, int max_n
 /// inside one wave, in forward sweep order.
 struct PatchRecords;
 int small_pass_patches();
+void small_trace(int arm, long long* out);  // development timeline (clock64 per pass phase)
 bool small_level_fits(int nb, int record_stride, int npass);
 void small_pre(const Bsr& A, const PatchRecords& R, const int2* passes, int npass, int sweeps, const BlockCsr& PT,
                const double* b, double* x, double* rc, cudaStream_t s);

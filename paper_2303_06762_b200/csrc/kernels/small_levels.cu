@@ -2,12 +2,15 @@
 //
 // Level 1 of a 16x16 base mesh needs 50 dependent waves per multiplicative
 // sweep (the reference's ascending-vertex order, smoother.hpp:53-57), each
-// only ~20 patches wide: latency, not bandwidth, bounds it. One 256-thread
-// CTA runs a whole pre- (resp. post-) smoothing phase of the V-cycle with x
-// and b resident in shared memory. The sweep is cut into passes (<= kPass
-// patches of one wave, host-built list); the patch records of pass k+1..k+3
-// stream in by TMA bulk copies (a kStages-deep mbarrier ring) while pass k is
-// computed, so a wave costs two __syncthreads() and shared-memory arithmetic.
+// only ~16 patches wide: latency, not bandwidth, bounds it. One CTA runs a
+// whole pre- (resp. post-) smoothing phase of the V-cycle with x and b
+// resident in shared memory. The sweep is cut into passes (<= kPass patches
+// of one wave, host-built list). Warp-specialised: a producer warp streams the
+// patch records of pass k+1 by a TMA bulk copy (L2 evict-last, so they stay
+// L2-resident across V-cycles) into a 2-slot mbarrier ring while the kPass x 16
+// consumer threads compute pass k: residual row from the staged A rows and x,
+// then d = S r with the FULL patch inverse (column-major in the record, so the
+// GEMV reads are bank-conflict free). A wave costs two __syncthreads().
 // Symmetric operators only.
 #include <cuda_runtime.h>
 
@@ -21,19 +24,28 @@ namespace dev {
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kTP = 16;                   // threads (rows) per patch
-constexpr int kPass = kThreads / kTP;     // patches per pass
-constexpr int kStages = 4;
+constexpr int kTP = 16;                      // threads (rows) per patch
+constexpr int kPass = 24;                    // patches per pass (level-1 waves are 16-17 wide)
+constexpr int kConsumers = kPass * kTP;      // 384
+constexpr int kThreads = kConsumers + 32;    // + one producer warp
+constexpr int kStages = 2;
 
 __device__ __forceinline__ unsigned su32(const void* p) { return unsigned(__cvta_generic_to_shared(p)); }
 
+// development timeline of the one-CTA sweep (off unless hpmg_debug_small_trace arms it)
+__device__ int d_trace_on = 0;
+__device__ long long d_trace[4096];
+
+/// TMA bulk copy with an L2 evict-last hint.
 __device__ __forceinline__ void ring_issue(unsigned long long* bar, double* dst, const double* src, unsigned bytes) {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   su32(dst)),
-               "l"(src), "r"(bytes), "r"(su32(bar))
-               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar)), "l"(pol)
+      : "memory");
 }
 __device__ __forceinline__ void ring_wait(unsigned long long* bar, unsigned phase) {
   asm volatile(
@@ -52,6 +64,7 @@ __device__ __forceinline__ void ring_wait(unsigned long long* bar, unsigned phas
 struct Smem {
   double *sx, *sb, *ring, *r;
   unsigned long long* bar;
+  int2* pass;
 };
 
 __device__ Smem carve(int n, int stride, double* sm) {
@@ -60,7 +73,8 @@ __device__ Smem carve(int n, int stride, double* sm) {
   v.sb = sm + n;
   v.ring = v.sb + n;
   v.r = v.ring + size_t(kStages) * kPass * stride;
-  v.bar = reinterpret_cast<unsigned long long*>(v.r + kThreads);
+  v.bar = reinterpret_cast<unsigned long long*>(v.r + kConsumers);
+  v.pass = reinterpret_cast<int2*>(v.bar + kStages);
   return v;
 }
 
@@ -68,38 +82,41 @@ __device__ Smem carve(int n, int stride, double* sm) {
 __device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, int npass, int nsweeps, bool reverse,
                        const Smem& v) {
   const int lp = threadIdx.x / kTP, t = threadIdx.x % kTP;
+  const bool producer = threadIdx.x >= kConsumers;
   const int total = npass * nsweeps;
-  // the pass list lives in shared memory: a global load here would sit on
-  // the critical path of every pass
-  int2* spass = reinterpret_cast<int2*>(v.bar + kStages);
-  for (int i = threadIdx.x; i < npass; i += blockDim.x) spass[i] = passes[i];
-  __syncthreads();
-  auto pass_of = [&](int k) {
-    const int q = k % npass;
-    return spass[reverse ? npass - 1 - q : q];
-  };
+  for (int i = threadIdx.x; i < npass; i += blockDim.x) v.pass[i] = passes[i];
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&v.bar[s])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int k = 0; k < kStages - 1 && k < total; ++k) {
-      const int2 ps = pass_of(k);
-      ring_issue(&v.bar[k % kStages], v.ring + size_t(k % kStages) * kPass * R.stride, R.rec + size_t(ps.x) * R.stride,
-                 unsigned(ps.y) * unsigned(R.stride) * 8u);
-    }
   }
   __syncthreads();
+  auto pass_of = [&](int k) {
+    const int q = k % npass;
+    return v.pass[reverse ? npass - 1 - q : q];
+  };
+  auto issue = [&](int k) {
+    const int2 ps = pass_of(k);
+    ring_issue(&v.bar[k % kStages], v.ring + size_t(k % kStages) * kPass * R.stride, R.rec + size_t(ps.x) * R.stride,
+               unsigned(ps.y) * unsigned(R.stride) * 8u);
+  };
+  if (producer && threadIdx.x == kConsumers)
+    for (int k = 0; k < kStages - 1 && k < total; ++k) issue(k);
   for (int k = 0; k < total; ++k) {
-    if (threadIdx.x == 0 && k + kStages - 1 < total) {
-      // the slot refilled here was released by the __syncthreads() that closed pass k-1
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      const int kk = k + kStages - 1;
-      const int2 ps = pass_of(kk);
-      ring_issue(&v.bar[kk % kStages], v.ring + size_t(kk % kStages) * kPass * R.stride,
-                 R.rec + size_t(ps.x) * R.stride, unsigned(ps.y) * unsigned(R.stride) * 8u);
+    if (producer) {
+      // slot (k+1) % 2 was released by the __syncthreads() that closed pass k-1
+      if (threadIdx.x == kConsumers && k + kStages - 1 < total) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(k + kStages - 1);
+      }
+      __syncthreads();
+      __syncthreads();
+      continue;
     }
     const int2 ps = pass_of(k);
+    if (d_trace_on && threadIdx.x == 0 && k < 1024) d_trace[4 * k] = clock64();
     ring_wait(&v.bar[k % kStages], unsigned((k / kStages) & 1));
+    if (d_trace_on && threadIdx.x == 0 && k < 1024) d_trace[4 * k + 1] = clock64();
     const double* rec = v.ring + (size_t(k % kStages) * kPass + lp) * R.stride;
     int np = 0, g = 0;
     if (lp < ps.y) {
@@ -110,30 +127,30 @@ __device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, i
         g = 2 * meta[1 + lf] + i;
         const int* cols = meta + 1 + R.max_nf + lf * kSlots;
         const double* arow = rec + R.a_off + lf * kSlots * 4 + i * 2;
-        double acc = v.sb[g];
+        double a0 = v.sb[g], a1 = 0.0;
 #pragma unroll
         for (int sl = 0; sl < kSlots; ++sl) {
           const int c = cols[sl];
-          const double x0 = c >= 0 ? v.sx[2 * c] : 0.0, x1 = c >= 0 ? v.sx[2 * c + 1] : 0.0;
-          acc = fma(-arow[sl * 4], x0, acc);
-          acc = fma(-arow[sl * 4 + 1], x1, acc);
+          const int cc = c >= 0 ? c : 0;  // empty slots hold zero blocks
+          a0 = fma(-arow[sl * 4], v.sx[2 * cc], a0);
+          a1 = fma(-arow[sl * 4 + 1], v.sx[2 * cc + 1], a1);
         }
-        v.r[threadIdx.x] = acc;
+        v.r[threadIdx.x] = a0 + a1;
       }
     }
     __syncthreads();
+    if (d_trace_on && threadIdx.x == 0 && k < 1024) d_trace[4 * k + 2] = clock64();
     if (t < np) {
-      const int ct = t * np - t * (t - 1) / 2 - t;
+      // full column-major inverse: S(t, j) at j*np + t
       const double* rr = v.r + lp * kTP;
-      double d0 = 0.0, d1 = 0.0;
-      for (int j = 0; j < np; j += 2) {
-        d0 = fma(rec[j >= t ? ct + j : j * np - j * (j - 1) / 2 + (t - j)], rr[j], d0);
-        const int j1 = j + 1;
-        if (j1 < np) d1 = fma(rec[j1 >= t ? ct + j1 : j1 * np - j1 * (j1 - 1) / 2 + (t - j1)], rr[j1], d1);
-      }
-      v.sx[g] += d0 + d1;
+      double d[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int j = 0; j < 2 * kMaxPatchF; ++j)
+        if (j < np) d[j & 3] = fma(rec[j * np + t], rr[j], d[j & 3]);
+      v.sx[g] += (d[0] + d[1]) + (d[2] + d[3]);
     }
     __syncthreads();
+    if (d_trace_on && threadIdx.x == 0 && k < 1024) d_trace[4 * k + 3] = clock64();
   }
 }
 
@@ -206,7 +223,7 @@ __global__ void __launch_bounds__(kThreads) k_small_post(Bsr A, PatchRecords R, 
 }
 
 size_t smem_bytes(int nb, int stride, int npass) {
-  return sizeof(double) * (size_t(4) * nb + size_t(kStages) * kPass * stride + kThreads) + 8 * kStages +
+  return sizeof(double) * (size_t(4) * nb + size_t(kStages) * kPass * stride + kConsumers) + 8 * kStages +
          sizeof(int2) * size_t(npass);
 }
 
@@ -214,12 +231,18 @@ size_t smem_bytes(int nb, int stride, int npass) {
 
 int small_pass_patches() { return kPass; }
 
+void small_trace(int arm, long long* out) {
+  cudaMemcpyToSymbol(d_trace_on, &arm, sizeof(int));
+  if (out) cudaMemcpyFromSymbol(out, d_trace, sizeof(long long) * 4096);
+}
+
 bool small_level_fits(int nb, int record_stride, int npass) {
   return smem_bytes(nb, record_stride, npass) <= 225 * 1024;
 }
 
 void small_pre(const Bsr& A, const PatchRecords& R, const int2* passes, int npass, int sweeps, const BlockCsr& PT,
                const double* b, double* x, double* rc, cudaStream_t s) {
+  if (!R.full) throw std::runtime_error("small-level sweeps need full-inverse patch records");
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_small_pre, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);

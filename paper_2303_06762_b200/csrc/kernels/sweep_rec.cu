@@ -139,7 +139,18 @@ __global__ void k_build_records(Bsr A, Patches P, PatchRecords R, int bs) {
   const int nf = P.nf[p], np = nf * bs;
   const int pk = np * (np + 1) / 2;
   const double* inv = P.inv + P.off[p];
-  for (int k = threadIdx.x; k < R.a_off; k += blockDim.x) rec[k] = k < pk ? inv[k] : 0.0;
+  if (R.full) {  // unpack the symmetric triangle: (r, c) at c*np + r
+    for (int k = threadIdx.x; k < R.a_off; k += blockDim.x) {
+      double v = 0.0;
+      if (k < np * np) {
+        const int c = k / np, r = k % np, lo = r > c ? c : r, hi = r > c ? r : c;
+        v = inv[lo * np - lo * (lo - 1) / 2 + (hi - lo)];
+      }
+      rec[k] = v;
+    }
+  } else {
+    for (int k = threadIdx.x; k < R.a_off; k += blockDim.x) rec[k] = k < pk ? inv[k] : 0.0;
+  }
   const int row = kSlots * bs * bs;
   for (int k = threadIdx.x; k < R.max_nf * row; k += blockDim.x) {
     const int lf = k / row;
@@ -200,12 +211,13 @@ void launch_rec(const PatchRecords& R, int w0, int w1, const double* b, double* 
 
 }  // namespace
 
-PatchRecords record_layout(int bs, int max_nf) {
+PatchRecords record_layout(int bs, int max_nf, bool full) {
   PatchRecords R;
   R.bs = bs;
   R.max_nf = max_nf;
+  R.full = full ? 1 : 0;
   const int npmax = max_nf * bs;
-  R.a_off = ((npmax * (npmax + 1) / 2) + 1) & ~1;
+  R.a_off = full ? ((npmax * npmax + 1) & ~1) : (((npmax * (npmax + 1) / 2) + 1) & ~1);
   R.meta_off = R.a_off + max_nf * kSlots * bs * bs;
   const int meta_ints = 1 + max_nf + max_nf * kSlots;
   R.stride = (R.meta_off + (meta_ints + 1) / 2 + 1) & ~1;  // even => 16-byte aligned records

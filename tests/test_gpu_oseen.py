@@ -92,3 +92,19 @@ def test_oseen_uzawa(nu):
     for a, b in zip(rg.report.inner_iterations, ro["inner_iterations"]):
         assert abs(a - b) <= 1
     assert rel(rg.velocity, ro["velocity"]) < 1e-8
+
+
+def test_gmres_on_dirty_device_memory():
+    # fresh cudaMalloc blocks may hold NaN bit patterns from earlier work: the
+    # GMRES basis vectors must be overwritten, never scaled (0 * NaN = NaN)
+    torch = pytest.importorskip("torch")
+    junk = torch.full((64 << 20,), float("nan"), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    del junk
+    torch.cuda.empty_cache()
+    orc, gpu = pair(1, nu=1e-2, levels=4)
+    b = orc.rhs()
+    xo, so = orc.krylov(b, method=1)
+    xg, sg = H.gmres(gpu, b)
+    assert sg.converged and abs(sg.iterations - so["iterations"]) <= 1
+    assert rel(xg, xo) < 1e-8
