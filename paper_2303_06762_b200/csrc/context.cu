@@ -523,11 +523,11 @@ void h_cycle(hpmg_ctx& C, int l, const double* b, double* x) {
   const int q = C.opt.cycle == HPMG_CYCLE_W ? 2 : 1;
   if (V.small && C.opt.smoother == HPMG_SMOOTH_MULTIPLICATIVE && q == 1) {
     // whole-level sweeps in one persistent CTA (small_levels.cu)
-    dev::small_pre(V.A, V.srec, V.d_passes, V.npass, V.steps, V.PT, b, x, W.b, C.s);
-    count(C);
+    dev::small_pre(V.A, V.srec, V.d_passes, V.npass, V.steps, V.PT, b, x, V.r, W.b, C.s);
+    count(C, 3);
     h_cycle(C, l - 1, W.b, W.x);
     dev::small_post(V.A, V.srec, V.d_passes, V.npass, V.steps, V.Pm, W.x, b, x, C.s);
-    count(C);
+    count(C, 2);
     return;
   }
   dev::fill(x, 0.0, V.n, C.s);
@@ -1366,7 +1366,7 @@ int hpmg_profile_levels(hpmg_ctx* ctx, int reps, double* out) {
         Level& V = *C.lv[l];
         Level& W = *C.lv[l - 1];
         if (V.small) {
-          dev::small_pre(V.A, V.srec, V.d_passes, V.npass, V.steps, V.PT, bs[l], xs[l], W.b, C.s);
+          dev::small_pre(V.A, V.srec, V.d_passes, V.npass, V.steps, V.PT, bs[l], xs[l], V.r, W.b, C.s);
         } else {
           dev::fill(xs[l], 0.0, V.n, C.s);
           smooth(C, V, xs[l], bs[l], false);

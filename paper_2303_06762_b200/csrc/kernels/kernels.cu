@@ -541,33 +541,43 @@ __global__ void k_jacobi_combine(int nb, int bs, Patches P, int max_np, const do
 }
 
 // ------------------------------------------------------------- transfers
-__global__ void k_prolong_add(BlockCsr P, const double* __restrict__ e, double* __restrict__ x) {
-  const int64_t n = int64_t(P.nrows) * 2;
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
-    const int f = int(t >> 1), c = int(t & 1);
-    double s = 0.0;
-    for (int q = P.ptr[f]; q < P.ptr[f + 1]; ++q) {
-      const int cb = P.col[q];
-      const double* v = P.val + size_t(q) * 4 + c * 2;
-      s = fma(v[0], e[size_t(cb) * 2], s);
-      s = fma(v[1], e[size_t(cb) * 2 + 1], s);
+/// y (+)= M v for a 2x2-block CSR, G lanes per block row (q strided by G,
+/// fixed-order butterfly): PT rows hold ~25 blocks, P rows ~6, so one thread
+/// per row would serialise that many dependent L2 round trips.
+template <int G, bool ACC>
+__global__ void k_bcsr_group(BlockCsr M, const double* __restrict__ v, double* __restrict__ y) {
+  // warp-uniform grid stride: every lane of a warp runs the same trip count (shuffles)
+  const int64_t total = int64_t(M.nrows) * G, stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t base = blockIdx.x * int64_t(blockDim.x) + (threadIdx.x & ~31); base < total; base += stride) {
+  const int64_t gt = base + (threadIdx.x & 31);
+  const int row = int(gt / G), lane = int(gt % G);
+  const bool live = row < M.nrows;
+  double s0 = 0.0, s1 = 0.0;
+  if (live) {
+    const int q1 = __ldg(&M.ptr[row + 1]);
+    for (int q = __ldg(&M.ptr[row]) + lane; q < q1; q += G) {
+      const int c = __ldg(&M.col[q]);
+      const double2 a0 = __ldg(reinterpret_cast<const double2*>(M.val) + size_t(q) * 2);
+      const double2 a1 = __ldg(reinterpret_cast<const double2*>(M.val) + size_t(q) * 2 + 1);
+      const double2 w = __ldg(reinterpret_cast<const double2*>(v) + c);
+      s0 = fma(a0.x, w.x, fma(a0.y, w.y, s0));
+      s1 = fma(a1.x, w.x, fma(a1.y, w.y, s1));
     }
-    x[t] += s;
   }
-}
-
-__global__ void k_restrict(BlockCsr PT, const double* __restrict__ r, double* __restrict__ rc) {
-  const int64_t n = int64_t(PT.nrows) * 2;
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
-    const int f = int(t >> 1), c = int(t & 1);
-    double s = 0.0;
-    for (int q = PT.ptr[f]; q < PT.ptr[f + 1]; ++q) {
-      const int fb = PT.col[q];
-      const double* v = PT.val + size_t(q) * 4 + c * 2;
-      s = fma(v[0], r[size_t(fb) * 2], s);
-      s = fma(v[1], r[size_t(fb) * 2 + 1], s);
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o, G);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o, G);
+  }
+  if (live && lane == 0) {
+    double2* yr = reinterpret_cast<double2*>(y) + row;
+    if (ACC) {
+      const double2 o = *yr;
+      *yr = make_double2(o.x + s0, o.y + s1);
+    } else {
+      *yr = make_double2(s0, s1);
     }
-    rc[t] = s;
+  }
   }
 }
 
@@ -961,12 +971,14 @@ void jacobi_combine(int nb, int bs, const Patches& P, const double* d, int max_n
 }
 
 void prolong_add(const BlockCsr& P, const double* e, double* x, cudaStream_t s) {
-  k_prolong_add<<<grid_for(int64_t(P.nrows) * 2, 256), 256, 0, s>>>(P, e, x);
+  constexpr int G = 4;
+  k_bcsr_group<G, true><<<grid_for(int64_t(P.nrows) * G, 256), 256, 0, s>>>(P, e, x);
   HPMG_LAUNCH_CHECK();
 }
 
 void restrict_(const BlockCsr& PT, const double* r, double* rc, cudaStream_t s) {
-  k_restrict<<<grid_for(int64_t(PT.nrows) * 2, 256), 256, 0, s>>>(PT, r, rc);
+  constexpr int G = 8;
+  k_bcsr_group<G, false><<<grid_for(int64_t(PT.nrows) * G, 256), 256, 0, s>>>(PT, r, rc);
   HPMG_LAUNCH_CHECK();
 }
 

@@ -100,8 +100,9 @@ void jacobi_combine(int nb, int bs, const Patches& P, const double* d, int max_n
                     cudaStream_t s);
 
 /// Small lowest-order levels (small_levels.cu, symmetric): one CTA runs
-/// x = 0, all pre-smoothing waves, r = b - A x and rc = P^T r (small_pre),
-/// resp. x += P e and all post-smoothing waves (small_post).
+/// x = 0 and all pre-smoothing waves, then r = b - A x and rc = P^T r run
+/// grid-wide (small_pre, 3 launches); x += P e grid-wide, then one CTA runs
+/// all post-smoothing waves (small_post, 2 launches).
 /// Passes are (first patch, count) ranges of <= small_pass_patches() patches
 /// inside one wave, in forward sweep order.
 struct PatchRecords;
@@ -109,7 +110,7 @@ int small_pass_patches();
 void small_trace(int arm, long long* out);  // development timeline (clock64 per pass phase)
 bool small_level_fits(int nb, int record_stride, int npass);
 void small_pre(const Bsr& A, const PatchRecords& R, const int2* passes, int npass, int sweeps, const BlockCsr& PT,
-               const double* b, double* x, double* rc, cudaStream_t s);
+               const double* b, double* x, double* r, double* rc, cudaStream_t s);
 void small_post(const Bsr& A, const PatchRecords& R, const int2* passes, int npass, int sweeps, const BlockCsr& Pm,
                 const double* e, const double* b, double* x, cudaStream_t s);
 

@@ -35,6 +35,13 @@ __device__ __forceinline__ unsigned su32(const void* p) { return unsigned(__cvta
 // development timeline of the one-CTA sweep (off unless hpmg_debug_small_trace arms it)
 __device__ int d_trace_on = 0;
 __device__ long long d_trace[4096];
+__device__ __forceinline__ void stamp(int slot) {
+  if (d_trace_on && threadIdx.x == 0) {
+    long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    d_trace[slot] = t;
+  }
+}
 
 /// TMA bulk copy with an L2 evict-last hint.
 __device__ __forceinline__ void ring_issue(unsigned long long* bar, double* dst, const double* src, unsigned bytes) {
@@ -114,9 +121,9 @@ __device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, i
       continue;
     }
     const int2 ps = pass_of(k);
-    if (d_trace_on && threadIdx.x == 0 && k < 1024) d_trace[4 * k] = clock64();
+    if (d_trace_on && threadIdx.x == 0 && k < 1000) d_trace[4 * k] = clock64();
     ring_wait(&v.bar[k % kStages], unsigned((k / kStages) & 1));
-    if (d_trace_on && threadIdx.x == 0 && k < 1024) d_trace[4 * k + 1] = clock64();
+    if (d_trace_on && threadIdx.x == 0 && k < 1000) d_trace[4 * k + 1] = clock64();
     const double* rec = v.ring + (size_t(k % kStages) * kPass + lp) * R.stride;
     int np = 0, g = 0;
     if (lp < ps.y) {
@@ -139,7 +146,7 @@ __device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, i
       }
     }
     __syncthreads();
-    if (d_trace_on && threadIdx.x == 0 && k < 1024) d_trace[4 * k + 2] = clock64();
+    if (d_trace_on && threadIdx.x == 0 && k < 1000) d_trace[4 * k + 2] = clock64();
     if (t < np) {
       // full column-major inverse: S(t, j) at j*np + t
       const double* rr = v.r + lp * kTP;
@@ -150,76 +157,48 @@ __device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, i
       v.sx[g] += (d[0] + d[1]) + (d[2] + d[3]);
     }
     __syncthreads();
-    if (d_trace_on && threadIdx.x == 0 && k < 1024) d_trace[4 * k + 3] = clock64();
+    if (d_trace_on && threadIdx.x == 0 && k < 1000) d_trace[4 * k + 3] = clock64();
   }
 }
 
-/// x = 0; pre-smooth; r = b - A x; rc = P^T r (reference multigrid.hpp:174-178)
-__global__ void __launch_bounds__(kThreads) k_small_pre(Bsr A, PatchRecords R, const int2* __restrict__ passes,
-                                                        int npass, int nsweeps, BlockCsr PT,
-                                                        const double* __restrict__ b, double* __restrict__ x,
-                                                        double* __restrict__ rc) {
+/// x = 0; pre-smooth (reference multigrid.hpp:174-175). The residual and the
+/// restriction run grid-wide after it (small_pre): their latency-bound CSR
+/// loops cost ~90 us in one CTA.
+__global__ void __launch_bounds__(kThreads) k_small_pre(int n, PatchRecords R, const int2* __restrict__ passes,
+                                                        int npass, int nsweeps, const double* __restrict__ b,
+                                                        double* __restrict__ x) {
   extern __shared__ __align__(128) double sm[];
-  const int n = A.nb * 2;
   Smem v = carve(n, R.stride, sm);
+  stamp(4088);
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     v.sx[i] = 0.0;
     v.sb[i] = b[i];
   }
   __syncthreads();
+  stamp(4089);
   sweeps(R, passes, npass, nsweeps, false, v);
-  // residual in place of b (each row reads only its own b entry and x)
-  for (int t = threadIdx.x; t < n; t += blockDim.x) {
-    const int f = t >> 1, i = t & 1;
-    double s = 0.0;
-#pragma unroll
-    for (int sl = 0; sl < kSlots; ++sl) {
-      const int c = __ldg(&A.cols[f * kSlots + sl]);
-      if (c < 0) continue;
-      const double2 a = __ldg(reinterpret_cast<const double2*>(A.val + (size_t(f * kSlots + sl) * 2 + i) * 2));
-      s = fma(a.x, v.sx[2 * c], s);
-      s = fma(a.y, v.sx[2 * c + 1], s);
-    }
-    x[t] = v.sx[t];
-    v.sb[t] = v.sb[t] - s;
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < PT.nrows * 2; t += blockDim.x) {
-    const int cb = t >> 1, c = t & 1;
-    double s = 0.0;
-    for (int q = PT.ptr[cb]; q < PT.ptr[cb + 1]; ++q) {
-      const int fb = PT.col[q];
-      const double* pv = PT.val + size_t(q) * 4 + c * 2;
-      s = fma(pv[0], v.sb[2 * fb], s);
-      s = fma(pv[1], v.sb[2 * fb + 1], s);
-    }
-    rc[t] = s;
-  }
+  stamp(4090);
+  for (int t = threadIdx.x; t < n; t += blockDim.x) x[t] = v.sx[t];
+  stamp(4091);
 }
 
-/// x += P e; post-smooth (reverse sweep) (reference multigrid.hpp:181-182)
-__global__ void __launch_bounds__(kThreads) k_small_post(Bsr A, PatchRecords R, const int2* __restrict__ passes,
-                                                         int npass, int nsweeps, BlockCsr Pm,
-                                                         const double* __restrict__ e, const double* __restrict__ b,
+/// post-smooth (reverse sweep) of x, after the grid-wide x += P e (multigrid.hpp:181-182)
+__global__ void __launch_bounds__(kThreads) k_small_post(int n, PatchRecords R, const int2* __restrict__ passes,
+                                                         int npass, int nsweeps, const double* __restrict__ b,
                                                          double* __restrict__ x) {
   extern __shared__ __align__(128) double sm[];
-  const int n = A.nb * 2;
   Smem v = carve(n, R.stride, sm);
+  stamp(4092);
   for (int t = threadIdx.x; t < n; t += blockDim.x) {
-    const int f = t >> 1, c = t & 1;
-    double s = 0.0;
-    for (int q = Pm.ptr[f]; q < Pm.ptr[f + 1]; ++q) {
-      const int cb = Pm.col[q];
-      const double* pv = Pm.val + size_t(q) * 4 + c * 2;
-      s = fma(pv[0], e[size_t(cb) * 2], s);
-      s = fma(pv[1], e[size_t(cb) * 2 + 1], s);
-    }
-    v.sx[t] = x[t] + s;
+    v.sx[t] = x[t];
     v.sb[t] = b[t];
   }
   __syncthreads();
+  stamp(4093);
   sweeps(R, passes, npass, nsweeps, true, v);
+  stamp(4094);
   for (int t = threadIdx.x; t < n; t += blockDim.x) x[t] = v.sx[t];
+  stamp(4095);
 }
 
 size_t smem_bytes(int nb, int stride, int npass) {
@@ -241,7 +220,7 @@ bool small_level_fits(int nb, int record_stride, int npass) {
 }
 
 void small_pre(const Bsr& A, const PatchRecords& R, const int2* passes, int npass, int sweeps, const BlockCsr& PT,
-               const double* b, double* x, double* rc, cudaStream_t s) {
+               const double* b, double* x, double* r, double* rc, cudaStream_t s) {
   if (!R.full) throw std::runtime_error("small-level sweeps need full-inverse patch records");
   static bool attr = false;
   if (!attr) {
@@ -249,14 +228,17 @@ void small_pre(const Bsr& A, const PatchRecords& R, const int2* passes, int npas
     cudaFuncSetAttribute(k_small_post, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  k_small_pre<<<1, kThreads, smem_bytes(A.nb, R.stride, npass), s>>>(A, R, passes, npass, sweeps, PT, b, x, rc);
+  k_small_pre<<<1, kThreads, smem_bytes(A.nb, R.stride, npass), s>>>(A.nb * 2, R, passes, npass, sweeps, b, x);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) throw std::runtime_error(std::string("CUDA launch: ") + cudaGetErrorString(err));
+  spmv(A, x, b, r, 1, nullptr, nullptr, s);
+  restrict_(PT, r, rc, s);
 }
 
 void small_post(const Bsr& A, const PatchRecords& R, const int2* passes, int npass, int sweeps, const BlockCsr& Pm,
                 const double* e, const double* b, double* x, cudaStream_t s) {
-  k_small_post<<<1, kThreads, smem_bytes(A.nb, R.stride, npass), s>>>(A, R, passes, npass, sweeps, Pm, e, b, x);
+  prolong_add(Pm, e, x, s);
+  k_small_post<<<1, kThreads, smem_bytes(A.nb, R.stride, npass), s>>>(A.nb * 2, R, passes, npass, sweeps, b, x);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) throw std::runtime_error(std::string("CUDA launch: ") + cudaGetErrorString(err));
 }

@@ -13,7 +13,7 @@ CFG = {"config2": dict(base_n=16, levels=5, k=3, beta=1e-2, inv_eps=1e3),
        "config1": dict(base_n=8, levels=5, k=1, beta=1.0, inv_eps=1e3),
        "config3": dict(base_n=8, levels=5, k=2, beta=0.0, inv_eps=1e4)}
 
-for name in sys.argv[1:] or ["config2", "config1"]:
+for name in (sys.argv[1:] or ["config2", "config1"]) if __name__ == "__main__" else []:
     c = CFG[name]
     nf = c["base_n"] << (c["levels"] - 1)
     B = H.MGPreconditioner(base_n=c["base_n"], levels=c["levels"], k=c["k"], beta=c["beta"], inv_eps=c["inv_eps"],

@@ -29,3 +29,7 @@ print("wait  median %.0f mean %.0f" % (np.median(wait), wait.mean()))
 print("resid median %.0f mean %.0f" % (np.median(res), res.mean()))
 print("gemv  median %.0f mean %.0f" % (np.median(gemv), gemv.mean()))
 print("gap   median %.0f mean %.0f" % (np.median(gap), gap.mean()))
+g = out[4088:4096].astype(np.float64)
+print("pre  (ns): load %.0f sweeps %.0f resid+restrict %.0f" % (g[1] - g[0], g[2] - g[1], g[3] - g[2]))
+print("post (ns): prolong %.0f sweeps %.0f store %.0f" % (g[5] - g[4], g[6] - g[5], g[7] - g[6]))
+print("pre->post gap (ns) %.0f" % (g[4] - g[3]))
