@@ -17,7 +17,6 @@ LIB_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libhpmg.so")
 
 SOURCES = [os.path.join(CSRC, "kernels", "kernels.cu"), os.path.join(CSRC, "kernels", "small_levels.cu"),
-           os.path.join(CSRC, "kernels", "sweep_tma.cu"),
            os.path.join(CSRC, "kernels", "sweep_rec.cu"),
            os.path.join(CSRC, "context.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, d, f) for d in ("kernels", "host") for f in os.listdir(os.path.join(CSRC, d))] + [

@@ -89,9 +89,8 @@ struct Level {
   int* row_elems = nullptr;
   int* elem_facets = nullptr;
   int* facet_block = nullptr;
-  double bytes_sweep = 0, bytes_spmv = 0, p_nnz = 0, bytes_sweep_phys = 0;
+  double bytes_sweep = 0, bytes_spmv = 0, p_nnz = 0;
 };
-constexpr double kSlotsD = double(host::kSlots);
 
 }  // namespace
 
@@ -257,8 +256,6 @@ void build_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, const Dev
     } else if (prob->load) {
       // pointwise: evaluate the callback at the mapped volume nodes on the host
       const int nq = R.T.nq;
-      host::RefTensors* unused = nullptr;
-      (void)unused;
       std::vector<double> qx, qy, qw;
       host::duffy(3 * k + 4, qx, qy, qw);
       std::vector<double> l(size_t(m.ne()) * nq * 2);
@@ -342,13 +339,25 @@ void build_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, const Dev
   V.bytes_spmv = 8 * nnz + 4 * nblk + 4 * (V.nb + 1.0) + 16.0 * V.n;
   // reference storage accounting: full np^2 patch factors (packing halves the physical bytes)
   V.bytes_sweep = 8.0 * double(V.plan.inv_full_total) + 2 * (8 * nnz + 4 * nblk) + 32.0 * V.n;
-  V.bytes_sweep_phys = 8.0 * double(V.plan.inv_total) + 2 * (8 * nnz + 4 * kSlotsD * V.nb) + 32.0 * V.n;
 }
 
 void build_patch_inverses(hpmg_ctx& C, Level& V) {
   if (V.P.n == 0) return;
   dev::patch_inverse(V.A, V.P, V.max_nf, C.s);
   if (V.P.packed) {  // fixed-stride patch records for the TMA sweep (sweep_rec.cu)
+    // every patch facet couples to at most kExt facets outside the patch (triangle meshes)
+    for (int p = 0; p < V.P.n; ++p)
+      for (int lf = 0; lf < V.plan.patch_nf[p]; ++lf) {
+        const int f = V.plan.patch_fac[size_t(p) * dev::kMaxPatchF + lf];
+        int ne = 0;
+        for (int sl = 0; sl < host::kSlots; ++sl) {
+          const int c = V.plan.cols[size_t(f) * host::kSlots + sl];
+          bool inside = false;
+          for (int q = 0; q < V.plan.patch_nf[p]; ++q) inside |= V.plan.patch_fac[size_t(p) * dev::kMaxPatchF + q] == c;
+          ne += (c >= 0 && !inside) ? 1 : 0;
+        }
+        if (ne > dev::kExt) throw std::runtime_error("patch facet with more than 2 external couplings");
+      }
     V.rec = dev::record_layout(V.bs, V.max_nf);
     V.rec.rec = dalloc<double>(size_t(V.P.n) * V.rec.stride);
     dev::build_records(V.A, V.P, V.rec, C.s);
@@ -390,47 +399,6 @@ std::vector<double> download_bsr(hpmg_ctx& C, Level& V) {
   CK(cudaMemcpyAsync(h.data(), V.A.val, h.size() * sizeof(double), cudaMemcpyDeviceToHost, C.s));
   CK(cudaStreamSynchronize(C.s));
   return h;
-}
-
-/// Host LU inverse of the dense level-0 operator (block layout), column-major.
-std::vector<double> dense_inverse(const std::vector<double>& A, int n) {
-  std::vector<double> M = A;
-  std::vector<int> perm(n);
-  for (int i = 0; i < n; ++i) perm[i] = i;
-  for (int k = 0; k < n; ++k) {
-    int p = k;
-    for (int i = k + 1; i < n; ++i)
-      if (std::abs(M[size_t(i) * n + k]) > std::abs(M[size_t(p) * n + k])) p = i;
-    if (M[size_t(p) * n + k] == 0.0) throw std::runtime_error("singular coarse operator");
-    if (p != k) {
-      for (int j = 0; j < n; ++j) std::swap(M[size_t(k) * n + j], M[size_t(p) * n + j]);
-      std::swap(perm[k], perm[p]);
-    }
-    const double d = M[size_t(k) * n + k];
-    for (int i = k + 1; i < n; ++i) {
-      const double l = M[size_t(i) * n + k] / d;
-      M[size_t(i) * n + k] = l;
-      if (l == 0.0) continue;
-      for (int j = k + 1; j < n; ++j) M[size_t(i) * n + j] -= l * M[size_t(k) * n + j];
-    }
-  }
-  std::vector<double> inv(size_t(n) * n);  // column-major: column j = A^-1 e_j
-  std::vector<double> y(n);
-  for (int j = 0; j < n; ++j) {
-    for (int i = 0; i < n; ++i) y[i] = (perm[i] == j) ? 1.0 : 0.0;
-    for (int i = 0; i < n; ++i) {
-      double s = y[i];
-      for (int l = 0; l < i; ++l) s -= M[size_t(i) * n + l] * y[l];
-      y[i] = s;
-    }
-    for (int i = n - 1; i >= 0; --i) {
-      double s = y[i];
-      for (int l = i + 1; l < n; ++l) s -= M[size_t(i) * n + l] * y[l];
-      y[i] = s / M[size_t(i) * n + i];
-    }
-    for (int i = 0; i < n; ++i) inv[size_t(j) * n + i] = y[i];
-  }
-  return inv;
 }
 
 dev::BlockCsr upload_blockcsr(const host::BlockCsrH& H, cudaStream_t s) {
@@ -849,14 +817,13 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
   auto t1 = clk::now();
   // lowest-order levels
   C.lv.resize(C.L + 1);
-  double* rhs_tmp = nullptr;
   for (int l = 0; l <= C.L; ++l) {
     C.lv[l] = std::make_unique<Level>();
     Level& V = *C.lv[l];
     const bool finest = (k == 0 && l == C.L);
     if (finest) {
       const int64_t nfree = int64_t(C.free_to_full.size());
-      rhs_tmp = C.rhs = dalloc<double>(nfree);
+      C.rhs = dalloc<double>(nfree);
     }
     build_level(C, V, C.mesh[l], 0, C.ref0, finest, prob, finest ? C.rhs : nullptr,
                 C.advected ? &adv[l] : nullptr);
@@ -868,7 +835,6 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
     build_level(C, *C.head, fine, k, C.refk, true, prob, C.rhs, C.advected ? &wind_k : nullptr);
     C.head->steps = opt->smooth_steps;
   }
-  (void)rhs_tmp;
   CK(cudaStreamSynchronize(C.s));
   auto t2 = clk::now();
   for (int l = 1; l <= C.L; ++l) build_patch_inverses(C, *C.lv[l]);
@@ -916,7 +882,7 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
         for (int i = 0; i < 2; ++i)
           for (int j = 0; j < 2; ++j) D[size_t(2 * r + i) * C.n0 + 2 * c + j] = A0[((size_t(r) * host::kSlots + s) * 2 + i) * 2 + j];
       }
-    // Gauss-Jordan on the device (host LU: dense_inverse(), kept for reference)
+    // Gauss-Jordan with partial pivoting on the device (kernels.cu dense_invert)
     double* dA = dupload(D, C.s);
     C.coarse_inv = dalloc<double>(size_t(C.n0) * C.n0);
     dev::dense_invert(C.n0, dA, C.coarse_inv, C.s);

@@ -77,8 +77,12 @@ void patch_inverse(const Bsr& A, const Patches& P, int max_nf, cudaStream_t s);
 /// patches wave[w0..w1). transposed_inv selects (Inv_p)^T (nonsymmetric backward).
 void gs_wave(const Bsr& A, const Patches& P, int w0, int w1, const double* b, double* x, int transposed_inv,
              int max_nf, cudaStream_t s, const void* prefetch = nullptr, size_t prefetch_len = 0);
-/// Fixed-stride per-patch records (sweep_rec.cu): packed inverse, A row
-/// blocks of the patch facets and int32 meta (nf, facets, block columns).
+/// Fixed-stride per-patch records (sweep_rec.cu): the patch inverse (packed
+/// triangle or full), the <= 2 A blocks per patch facet that couple it to
+/// facets OUTSIDE the patch, and int32 meta (nf, facets, external columns).
+/// The sweep applies x_p = Inv_p (b_p - A_pe x_e), algebraically identical to
+/// x_p += Inv_p (b - A x)_p since Inv_p A_pp = I: A_pp is never read.
+constexpr int kExt = 2;  // external blocks per patch facet (the two far edges of its triangles)
 struct PatchRecords {
   double* rec = nullptr;
   int bs = 2, max_nf = 0;
@@ -90,10 +94,6 @@ void build_records(const Bsr& A, const Patches& P, PatchRecords& R, cudaStream_t
 /// One symmetric wave over the patch records [w0, w1) (one TMA per CTA).
 void gs_wave_rec(const PatchRecords& R, int w0, int w1, const double* b, double* x, cudaStream_t s);
 
-/// Same wave with the TMA-fed persistent kernel (sweep_tma.cu); symmetric
-/// (packed) inverses only.
-void gs_wave_tma(const Bsr& A, const Patches& P, int w0, int w1, const double* b, double* x, int max_nf,
-                 cudaStream_t s);
 /// Additive sweep pieces: d_p = Inv_p r_p for all patches; x += damping * sum_p d_p.
 void jacobi_patch(const Bsr& A, const Patches& P, const double* r, double* d, int max_nf, cudaStream_t s);
 void jacobi_combine(int nb, int bs, const Patches& P, const double* d, int max_nf, double damping, double* x,

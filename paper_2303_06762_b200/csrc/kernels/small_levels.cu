@@ -8,9 +8,9 @@
 // of one wave, host-built list). Warp-specialised: a producer warp streams the
 // patch records of pass k+1 by a TMA bulk copy (L2 evict-last, so they stay
 // L2-resident across V-cycles) into a 2-slot mbarrier ring while the kPass x 16
-// consumer threads compute pass k: residual row from the staged A rows and x,
-// then d = S r with the FULL patch inverse (column-major in the record, so the
-// GEMV reads are bank-conflict free). A wave costs two __syncthreads().
+// consumer threads compute pass k: r = b_p - A_pe x_e from the staged external
+// blocks (sweep_rec.cu), then x_p = S r with the FULL patch inverse
+// (column-major in the record, so the GEMV reads are bank-conflict free). A wave costs two __syncthreads().
 // Symmetric operators only.
 #include <cuda_runtime.h>
 
@@ -132,11 +132,11 @@ __device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, i
       if (t < np) {
         const int lf = t >> 1, i = t & 1;
         g = 2 * meta[1 + lf] + i;
-        const int* cols = meta + 1 + R.max_nf + lf * kSlots;
-        const double* arow = rec + R.a_off + lf * kSlots * 4 + i * 2;
+        const int* cols = meta + 1 + R.max_nf + lf * kExt;
+        const double* arow = rec + R.a_off + lf * kExt * 4 + i * 2;
         double a0 = v.sb[g], a1 = 0.0;
 #pragma unroll
-        for (int sl = 0; sl < kSlots; ++sl) {
+        for (int sl = 0; sl < kExt; ++sl) {
           const int c = cols[sl];
           const int cc = c >= 0 ? c : 0;  // empty slots hold zero blocks
           a0 = fma(-arow[sl * 4], v.sx[2 * cc], a0);
@@ -154,7 +154,7 @@ __device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, i
 #pragma unroll
       for (int j = 0; j < 2 * kMaxPatchF; ++j)
         if (j < np) d[j & 3] = fma(rec[j * np + t], rr[j], d[j & 3]);
-      v.sx[g] += (d[0] + d[1]) + (d[2] + d[3]);
+      v.sx[g] = (d[0] + d[1]) + (d[2] + d[3]);  // x_p = S_p (b_p - A_pe x_e), sweep_rec.cu
     }
     __syncthreads();
     if (d_trace_on && threadIdx.x == 0 && k < 1000) d_trace[4 * k + 3] = clock64();

@@ -3,17 +3,20 @@
 // inc/smoother.hpp:53-67, 83-94).
 //
 // Every vertex patch owns one fixed-stride record in HBM, built once at setup:
-//   [ packed symmetric patch inverse (pk_max doubles)
-//   | the nf A row blocks of its facets (nf x 5 x bs^2 doubles)
-//   | int32 meta: nf, facet ids, the 5 block columns of each facet ]
-// A CTA therefore needs no dependent index loads: one elected thread issues a
-// single TMA bulk copy (cp.async.bulk, L2 evict-first so the streamed records
-// do not evict x and b) of the records of its patch group, addressed by the
-// patch id alone, onto an mbarrier. The threads then gather the x blocks of
-// the patch neighbourhood (the only dependent round, L2-resident), form the
-// residual rows from shared memory and apply the packed inverse.
-// The A rows are stored twice (each facet belongs to two patches): 0.5 GB
-// extra at k=3 on 256^2, traded for one latency round per patch.
+//   [ patch inverse S_p (packed lower triangle by columns, or full)
+//   | A_pe: per patch facet the <= 2 blocks coupling it to facets outside the
+//     patch (facet (v,w) of the star of v couples to (v,a), (v,b) inside and
+//     to the far edges (w,a), (w,b) outside)
+//   | int32 meta: nf, facet ids, the external block columns ]
+// and the sweep sets x_p = S_p (b_p - A_pe x_e): with S_p A_pp = I this is the
+// reference update x_p += S_p (b - A x)_p without ever reading A_pp, which
+// cuts the A bytes per sweep from 10 to 4 blocks per facet (each facet sits in
+// two patches). A CTA needs no dependent index loads: one elected thread
+// issues a single TMA bulk copy (cp.async.bulk, L2 evict-first so the
+// streamed records do not evict x and b) of the records of its patch group,
+// addressed by the patch id alone, onto an mbarrier. The threads then gather
+// the external x blocks (the only dependent round, L2-resident), form the
+// right-hand side from shared memory and apply the inverse.
 #include <cuda_runtime.h>
 
 #include <stdexcept>
@@ -60,11 +63,11 @@ __device__ __forceinline__ void tma_stream(void* dst, const void* src, unsigned 
 template <int BS, int TP, int G>
 __global__ void __launch_bounds__(G* TP) k_sweep_rec(PatchRecords R, int p0, int p1, const double* __restrict__ b,
                                                      double* __restrict__ x) {
-  constexpr int kRow = kSlots * BS * BS;
+  constexpr int kRow = kExt * BS * BS;
   extern __shared__ __align__(128) unsigned char smraw[];
   double* srec = reinterpret_cast<double*>(smraw);  // G * stride
-  double* sx = srec + size_t(G) * R.stride;          // G * max_nf * kSlots * BS
-  double* r = sx + G * R.max_nf * kSlots * BS;       // G * TP
+  double* sx = srec + size_t(G) * R.stride;          // G * max_nf * kExt * BS
+  double* r = sx + G * R.max_nf * kExt * BS;         // G * TP
   __shared__ unsigned long long bar;
   const int lp = threadIdx.x / TP, t = threadIdx.x % TP;
   const int q0 = p0 + blockIdx.x * G;
@@ -84,10 +87,10 @@ __global__ void __launch_bounds__(G* TP) k_sweep_rec(PatchRecords R, int p0, int
   const int* meta = reinterpret_cast<const int*>(rec + R.meta_off);
   const int nf = lp < ng ? meta[0] : 0, np = nf * BS;
   const int* fac = meta + 1;
-  const int* cols = meta + 1 + R.max_nf;
-  double* xs = sx + lp * R.max_nf * kSlots * BS;
-  for (int e = t; e < nf * kSlots * BS; e += TP) {
-    const int c = cols[e / BS];
+  const int* ecol = meta + 1 + R.max_nf;
+  double* xs = sx + lp * R.max_nf * kExt * BS;
+  for (int e = t; e < nf * kExt * BS; e += TP) {
+    const int c = ecol[e / BS];
     xs[e] = c >= 0 ? x[size_t(c) * BS + e % BS] : 0.0;
   }
   double bv = 0.0;
@@ -96,10 +99,10 @@ __global__ void __launch_bounds__(G* TP) k_sweep_rec(PatchRecords R, int p0, int
   if (t < np) {
     const int lf = t / BS, i = t % BS;
     const double* arow = rec + R.a_off + lf * kRow + i * BS;
-    const double* xr = xs + lf * kSlots * BS;
+    const double* xr = xs + lf * kExt * BS;
     double a0 = bv, a1 = 0.0;
 #pragma unroll
-    for (int sl = 0; sl < kSlots; ++sl)
+    for (int sl = 0; sl < kExt; ++sl)
 #pragma unroll
       for (int jj = 0; jj < BS; jj += 2) {
         const int j0 = (jj + i) % BS, j1 = (jj + 1 + i) % BS;  // rotated: rows of a block hit distinct banks
@@ -128,7 +131,7 @@ __global__ void __launch_bounds__(G* TP) k_sweep_rec(PatchRecords R, int p0, int
       d3 = fma(s4[3], rr[j + 3], d3);
     }
     for (; j < np; ++j) d0 = fma(S[j >= t ? ct + j : j * np - j * (j - 1) / 2 + (t - j)], rr[j], d0);
-    x[size_t(fac[t / BS]) * BS + t % BS] += (d0 + d1) + (d2 + d3);
+    x[size_t(fac[t / BS]) * BS + t % BS] = (d0 + d1) + (d2 + d3);
   }
 }
 
@@ -151,17 +154,33 @@ __global__ void k_build_records(Bsr A, Patches P, PatchRecords R, int bs) {
   } else {
     for (int k = threadIdx.x; k < R.a_off; k += blockDim.x) rec[k] = k < pk ? inv[k] : 0.0;
   }
-  const int row = kSlots * bs * bs;
-  for (int k = threadIdx.x; k < R.max_nf * row; k += blockDim.x) {
-    const int lf = k / row;
-    rec[R.a_off + k] = lf < nf ? A.val[size_t(P.fac[p * kMaxPatchF + lf]) * row + k % row] : 0.0;
-  }
+  // external blocks: slots whose column is a facet outside the patch, in slot order
+  const int* pf = P.fac + p * kMaxPatchF;
+  const int blk = bs * bs;
   int* meta = reinterpret_cast<int*>(rec + R.meta_off);
+  for (int k = threadIdx.x; k < R.max_nf * kExt * blk; k += blockDim.x) rec[R.a_off + k] = 0.0;
   if (threadIdx.x == 0) meta[0] = nf;
-  for (int k = threadIdx.x; k < R.max_nf; k += blockDim.x) meta[1 + k] = k < nf ? P.fac[p * kMaxPatchF + k] : -1;
-  for (int k = threadIdx.x; k < R.max_nf * kSlots; k += blockDim.x) {
-    const int lf = k / kSlots;
-    meta[1 + R.max_nf + k] = lf < nf ? A.cols[P.fac[p * kMaxPatchF + lf] * kSlots + k % kSlots] : -1;
+  for (int k = threadIdx.x; k < R.max_nf; k += blockDim.x) meta[1 + k] = k < nf ? pf[k] : -1;
+  for (int k = threadIdx.x; k < R.max_nf * kExt; k += blockDim.x) meta[1 + R.max_nf + k] = -1;
+  __syncthreads();
+  for (int lf = threadIdx.x; lf < nf; lf += blockDim.x) {
+    const int f = pf[lf];
+    int ne = 0;
+    for (int sl = 0; sl < kSlots; ++sl) {
+      const int c = A.cols[f * kSlots + sl];
+      if (c < 0) continue;
+      bool inside = false;
+      for (int q = 0; q < nf; ++q) inside |= pf[q] == c;
+      if (inside) continue;
+      if (ne == kExt) {  // cannot happen on a triangle mesh: flag the record
+        meta[0] = -1;
+        break;
+      }
+      meta[1 + R.max_nf + lf * kExt + ne] = c;
+      for (int e = 0; e < blk; ++e)
+        rec[R.a_off + (lf * kExt + ne) * blk + e] = A.val[(size_t(f) * kSlots + sl) * blk + e];
+      ++ne;
+    }
   }
 }
 
@@ -188,7 +207,7 @@ template <int BS>
 void launch_rec(const PatchRecords& R, int w0, int w1, const double* b, double* x, cudaStream_t s) {
   constexpr int TP = RecCfg<BS>::TP, G = RecCfg<BS>::G;
   if (R.max_nf * BS > TP) throw std::runtime_error("vertex patch too large for the record sweep");
-  const size_t smem = sizeof(double) * (size_t(G) * R.stride + size_t(G) * R.max_nf * kSlots * BS + G * TP);
+  const size_t smem = sizeof(double) * (size_t(G) * R.stride + size_t(G) * R.max_nf * kExt * BS + G * TP);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_sweep_rec<BS, TP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -218,8 +237,8 @@ PatchRecords record_layout(int bs, int max_nf, bool full) {
   R.full = full ? 1 : 0;
   const int npmax = max_nf * bs;
   R.a_off = full ? ((npmax * npmax + 1) & ~1) : (((npmax * (npmax + 1) / 2) + 1) & ~1);
-  R.meta_off = R.a_off + max_nf * kSlots * bs * bs;
-  const int meta_ints = 1 + max_nf + max_nf * kSlots;
+  R.meta_off = R.a_off + max_nf * kExt * bs * bs;
+  const int meta_ints = 1 + max_nf + max_nf * kExt;
   R.stride = (R.meta_off + (meta_ints + 1) / 2 + 1) & ~1;  // even => 16-byte aligned records
   return R;
 }
