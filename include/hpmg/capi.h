@@ -167,7 +167,9 @@ int hpmg_recover(hpmg_ctx* ctx, const double* velocity_full, double* interior, d
 void* hpmg_stream(hpmg_ctx* ctx);               /* cudaStream_t the context launches on */
 /* Algorithmic bytes of one apply() / one spmv() in the reference storage
  * accounting; `parts` (optional, 8 doubles) splits the
- * V-cycle: head sweeps, head residual, level sweeps, level residuals, transfers, coarse. */
+ * V-cycle: head sweeps, head residual, level sweeps, level residuals, transfers, coarse;
+ * parts[6] / parts[7] = head / level sweep bytes as this implementation streams
+ * them (patch records + vector rows, not part of the returned total). */
 double hpmg_vcycle_bytes(const hpmg_ctx* ctx, double* parts);
 double hpmg_spmv_bytes(const hpmg_ctx* ctx);
 /* Device-resident timing of `reps` applies (graph-launched) on device buffers

@@ -90,6 +90,7 @@ struct Level {
   int* elem_facets = nullptr;
   int* facet_block = nullptr;
   double bytes_sweep = 0, bytes_spmv = 0, p_nnz = 0;
+  double bytes_stream = 0;  // one sweep as this implementation moves it: records + b/x rows + x_e gathers
 };
 
 }  // namespace
@@ -346,6 +347,7 @@ void build_patch_inverses(hpmg_ctx& C, Level& V) {
   dev::patch_inverse(V.A, V.P, V.max_nf, C.s);
   if (V.P.packed) {  // fixed-stride patch records for the TMA sweep (sweep_rec.cu)
     // every patch facet couples to at most kExt facets outside the patch (triangle meshes)
+    double vec_bytes = 0;
     for (int p = 0; p < V.P.n; ++p)
       for (int lf = 0; lf < V.plan.patch_nf[p]; ++lf) {
         const int f = V.plan.patch_fac[size_t(p) * dev::kMaxPatchF + lf];
@@ -357,6 +359,7 @@ void build_patch_inverses(hpmg_ctx& C, Level& V) {
           ne += (c >= 0 && !inside) ? 1 : 0;
         }
         if (ne > dev::kExt) throw std::runtime_error("patch facet with more than 2 external couplings");
+        vec_bytes += 8.0 * V.bs * (2 + ne);  // b row read, x row written, x_e blocks gathered
       }
     V.rec = dev::record_layout(V.bs, V.max_nf);
     V.rec.rec = dalloc<double>(size_t(V.P.n) * V.rec.stride);
@@ -378,6 +381,7 @@ void build_patch_inverses(hpmg_ctx& C, Level& V) {
       V.d_passes = dupload(passes, C.s);
       V.small = true;
     }
+    V.bytes_stream = 8.0 * double(V.P.n) * (V.small ? V.srec.stride : V.rec.stride) + vec_bytes;
   }
 }
 
@@ -1225,7 +1229,12 @@ double hpmg_vcycle_bytes(const hpmg_ctx* ctx, double* parts) {
   }
   p[5] = std::pow(double(q), C.L) * 8.0 * double(C.n0) * C.n0;
   double tot = 0;
-  for (int i = 0; i < 8; ++i) tot += p[i];
+  for (int i = 0; i < 6; ++i) tot += p[i];
+  // streamed bytes of this implementation's sweeps (records, not in `tot`)
+  auto stream = [](const Level& V) { return V.bytes_stream > 0 ? V.bytes_stream : V.bytes_sweep; };
+  if (C.opt.k > 0) p[6] = 2.0 * C.head->steps * stream(*C.head);
+  for (int l = C.L; l >= 1; --l)
+    p[7] += std::pow(double(q), C.L - l) * 2.0 * C.lv[l]->steps * stream(*C.lv[l]);
   if (parts)
     for (int i = 0; i < 8; ++i) parts[i] = p[i];
   return tot;
