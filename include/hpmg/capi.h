@@ -75,7 +75,12 @@ typedef struct {
   double nu, beta, mass_coef, inv_eps;
   int cycle, smoother, smooth_steps;
   double jacobi_damping;
+  int schedule;            /* multiplicative sweep schedule (symmetric operators):
+                              HPMG_SCHEDULE_WAVES (0, one launch per independent wave) or
+                              HPMG_SCHEDULE_DATAFLOW (1, one launch per sweep ordered by
+                              per-patch completion flags); identical results */
 } hpmg_options;
+enum { HPMG_SCHEDULE_WAVES = 0, HPMG_SCHEDULE_DATAFLOW = 1 };
 
 /* Problem data: boundary values, load and (Oseen) advection state. */
 typedef struct {
@@ -183,6 +188,8 @@ int hpmg_kernel_launches_per_apply(const hpmg_ctx* ctx);
 int hpmg_profile_levels(hpmg_ctx* ctx, int reps, double* out);
 /* Development hook: clock64 timeline of the one-CTA small-level sweep. */
 void hpmg_debug_small_trace(int arm, long long* out);
+/* development: per-CTA globaltimer stamps of the last wave-sweep launches (HPMG_DBG=4) */
+void hpmg_debug_sweep_trace(long long* out);
 double hpmg_setup_seconds(const hpmg_ctx* ctx, double* parts);
 
 /* Seeded per-triangle force of the BASELINE configs: std::mt19937(seed) and

@@ -31,10 +31,15 @@ class _Mesh(C.Structure):
                 ("tag_overrides", C.POINTER(C.c_int)), ("levels", C.c_int)]
 
 
+# multiplicative sweep schedules (identical results): one launch per wave, or
+# one dataflow launch per sweep ordered by per-patch completion flags
+SCHEDULES = {"waves": 0, "dataflow": 1}
+
+
 class _Options(C.Structure):
     _fields_ = [("k", C.c_int), ("nu", C.c_double), ("beta", C.c_double), ("mass_coef", C.c_double),
                 ("inv_eps", C.c_double), ("cycle", C.c_int), ("smoother", C.c_int), ("smooth_steps", C.c_int),
-                ("jacobi_damping", C.c_double)]
+                ("jacobi_damping", C.c_double), ("schedule", C.c_int)]
 
 
 class _Problem(C.Structure):
@@ -206,13 +211,16 @@ class MGPreconditioner:
     def __init__(self, *, mesh="unit_square", base_n=2, levels=2, k=0, nu=1.0, beta=0.0, mass_coef=0.0,
                  inv_eps=1e6, cycle=CYCLE_W, smoother=SMOOTH_MULTIPLICATIVE, smooth_steps=1,
                  jacobi_damping=1.0 / 3.0, bc=None, load=None, load_per_element=None, structured_load=None,
-                 wind=None):
+                 wind=None, schedule="waves"):
         L = lib()
         md = _Mesh()
         rc = (L.hpmg_unit_square_mesh if mesh == "unit_square" else L.hpmg_step_mesh)(base_n, levels, C.byref(md))
         if rc:
             raise HpmgError(L.hpmg_last_error().decode())
-        opt = _Options(k, nu, beta, mass_coef, inv_eps, cycle, smoother, smooth_steps, jacobi_damping)
+        if schedule not in SCHEDULES:
+            raise ValueError(f"schedule must be one of {sorted(SCHEDULES)}")
+        opt = _Options(k, nu, beta, mass_coef, inv_eps, cycle, smoother, smooth_steps, jacobi_damping,
+                       SCHEDULES[schedule])
         self._bc = _field(bc)
         self._load = _field(load)
         self._keep = []

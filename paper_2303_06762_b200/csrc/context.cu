@@ -76,6 +76,8 @@ struct Level {
   int* d_wave_ptr = nullptr;
   dev::PatchRecords rec;
   dev::PatchRecords srec;  // full-inverse records of the one-CTA path
+  unsigned* flow_flags = nullptr;  // [npatch] completion epochs of the dataflow sweep
+  unsigned* flow_ctl = nullptr;    // [2] epoch base, arrival counter
   bool small = false;      // whole pre/post phase in one CTA (small_levels.cu)
   int2* d_passes = nullptr;
   int npass = 0;
@@ -361,8 +363,17 @@ void build_patch_inverses(hpmg_ctx& C, Level& V) {
         if (ne > dev::kExt) throw std::runtime_error("patch facet with more than 2 external couplings");
         vec_bytes += 8.0 * V.bs * (2 + ne);  // b row read, x row written, x_e blocks gathered
       }
+    V.P.max_dep = V.plan.max_dep;
+    V.P.ndep = dupload(V.plan.patch_ndep, C.s);
+    V.P.dep = dupload(V.plan.patch_dep, C.s);
     V.rec = dev::record_layout(V.bs, V.max_nf);
     V.rec.rec = dalloc<double>(size_t(V.P.n) * V.rec.stride);
+    V.rec.n = V.P.n;
+    if (const char* d = std::getenv("HPMG_DBG")) V.rec.dbg = std::atoi(d);
+    V.flow_flags = dalloc<unsigned>(V.P.n);
+    V.flow_ctl = dalloc<unsigned>(2);
+    CK(cudaMemsetAsync(V.flow_flags, 0, sizeof(unsigned) * V.P.n, C.s));
+    CK(cudaMemsetAsync(V.flow_ctl, 0, sizeof(unsigned) * 2, C.s));
     dev::build_records(V.A, V.P, V.rec, C.s);
     std::vector<int2> passes;
     const int pp = dev::small_pass_patches();
@@ -443,6 +454,12 @@ void smooth(hpmg_ctx& C, Level& V, double* x, const double* b, bool post) {
   };
   const void* pf;
   size_t pl;
+  if (V.P.packed && C.opt.schedule == HPMG_SCHEDULE_DATAFLOW && nw <= dev::kMaxSweepWaves) {
+    // all waves of all steps in one dataflow launch (sweep_rec.cu)
+    dev::sweep_dag(V.rec, V.wave_ptr.data(), nw, V.P, V.steps, post, b, x, V.flow_flags, V.flow_ctl, C.s);
+    count(C, 2);
+    return;
+  }
   if (!post) {
     for (int s = 0; s < V.steps; ++s)
       for (int w = 0; w < nw; ++w) {
@@ -968,7 +985,7 @@ void hpmg_destroy(hpmg_ctx* ctx) {
                     (void*)V->Pm.ptr, (void*)V->Pm.col, (void*)V->Pm.val, (void*)V->PT.ptr, (void*)V->PT.col,
                     (void*)V->PT.val, (void*)V->x, (void*)V->b, (void*)V->r, (void*)V->y, (void*)V->bw, (void*)V->xw,
                     (void*)V->dbuf, (void*)V->geo, (void*)V->row_elems, (void*)V->elem_facets, (void*)V->facet_block,
-                    (void*)V->d_wave_ptr, (void*)V->rec.rec, (void*)V->srec.rec, (void*)V->d_passes})
+                    (void*)V->d_wave_ptr, (void*)V->rec.rec, (void*)V->srec.rec, (void*)V->flow_flags, (void*)V->flow_ctl, (void*)V->P.ndep, (void*)V->P.dep, (void*)V->d_passes})
       fr(p);
   };
   for (auto& V : ctx->lv) free_level(V.get());
@@ -1300,6 +1317,7 @@ int hpmg_kernel_launches_per_apply(const hpmg_ctx* ctx) { return ctx->launches_p
 /// Development hook: arm (1) / disarm (0) the one-CTA sweep timeline and copy
 /// it out (4096 clock64 stamps: per pass start, data ready, residual done, end).
 void hpmg_debug_small_trace(int arm, long long* out) { dev::small_trace(arm, out); }
+void hpmg_debug_sweep_trace(long long* out) { dev::sweep_trace(out); }
 
 /// Event-instrumented V-cycle (no graph): out[2l], out[2l+1] = pre/post part
 /// of level l (l = 1..L) in ms, out[0] = coarse solve, out[2(L+1)..+2] = head

@@ -81,6 +81,11 @@ struct LevelPlan {
   bool packed = true;
   std::vector<int> wave_ptr, wave_patch;  // forward wave order
   std::vector<int> facet_patches;     // [nb][2] the two patches holding a block, ascending
+  // dataflow sweep: patches of the mesh neighbours of each patch's vertex
+  // (renumbered ids; the forward sweep waits on the smaller, the reverse on the larger)
+  int max_dep = 0;
+  std::vector<int> patch_ndep;        // [npatch]
+  std::vector<int> patch_dep;         // [npatch][max_dep], -1 padded
   int nwaves() const { return int(wave_ptr.size()) - 1; }
   int64_t n() const { return int64_t(nb) * bs; }
 };
@@ -221,6 +226,24 @@ inline LevelPlan make_level(const TriMesh& m, int k) {
   L.patch_fac.swap(fac2);
   for (auto& fp : L.facet_patches)
     if (fp >= 0) fp = newid[fp];
+  {
+    std::vector<std::vector<int>> dep(L.npatch);
+    for (int v = 0; v < m.nv(); ++v) {
+      if (vertex_patch[v] < 0) continue;
+      auto& d = dep[newid[vertex_patch[v]]];
+      for (int u : nbr[v])
+        if (vertex_patch[u] >= 0) d.push_back(newid[vertex_patch[u]]);
+      std::sort(d.begin(), d.end());
+      d.erase(std::unique(d.begin(), d.end()), d.end());
+      L.max_dep = std::max(L.max_dep, int(d.size()));
+    }
+    L.patch_ndep.assign(L.npatch, 0);
+    L.patch_dep.assign(size_t(L.npatch) * std::max(L.max_dep, 1), -1);
+    for (int p = 0; p < L.npatch; ++p) {
+      L.patch_ndep[p] = int(dep[p].size());
+      for (size_t i = 0; i < dep[p].size(); ++i) L.patch_dep[size_t(p) * L.max_dep + i] = dep[p][i];
+    }
+  }
   for (int q = 0; q < L.npatch; ++q) L.wave_patch[q] = q;
   set_inverse_layout(L, true);
   return L;

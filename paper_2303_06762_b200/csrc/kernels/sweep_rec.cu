@@ -12,13 +12,28 @@
 // reference update x_p += S_p (b - A x)_p without ever reading A_pp, which
 // cuts the A bytes per sweep from 10 to 4 blocks per facet (each facet sits in
 // two patches). A CTA needs no dependent index loads: one elected thread
-// issues a single TMA bulk copy (cp.async.bulk, L2 evict-first so the
-// streamed records do not evict x and b) of the records of its patch group,
-// addressed by the patch id alone, onto an mbarrier. The threads then gather
-// the external x blocks (the only dependent round, L2-resident), form the
-// right-hand side from shared memory and apply the inverse.
+// issues TMA bulk copies (cp.async.bulk, L2 evict-first so the streamed
+// records do not evict x and b) of the records of its patch group, addressed
+// by the patch id alone, onto mbarriers. The threads then gather the external
+// x blocks (the only dependent round, L2-resident), form the right-hand side
+// from shared memory and apply the inverse.
+//
+// Ordering. The reference sweep is sequential in ascending vertex order; two
+// patches conflict iff their vertices are mesh neighbours.
+// Two schedules reproduce it exactly:
+//  - waves (gs_wave_rec): one launch per wave of mutually independent patches,
+//    chained by programmatic dependent launch;
+//  - dataflow (sweep_dag): ONE launch per sweep over all patches in sweep
+//    order (CTA index = position). A CTA waits only for the completion flags
+//    of its neighbours that precede it, so there is no wave boundary: the
+//    drain/fill of every wave disappears. Flags hold sweep epochs
+//    (ctl[0] + sweep + 1); a one-thread kernel advances ctl[0] after the
+//    launch, so the flags never need resetting. Like CUB's decoupled
+//    look-back, this relies on CTAs being dispatched in index order: every
+//    CTA waits only on lower indices, which are therefore resident or done.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <stdexcept>
 #include <string>
 
@@ -47,55 +62,149 @@ __device__ __forceinline__ void bar_wait(unsigned long long* bar) {
       "}\n" ::"r"(su32(bar))
       : "memory");
 }
-/// one TMA bulk copy global -> shared with an L2 evict-first policy
-__device__ __forceinline__ void tma_stream(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-  unsigned long long pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+__device__ __forceinline__ void bar_expect(unsigned long long* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+/// bulk copy completing on `bar` (whose expected bytes were announced by bar_expect)
+__device__ __forceinline__ void tma_part(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                         unsigned long long pol) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
           su32(dst)),
       "l"(src), "r"(bytes), "r"(su32(bar)), "l"(pol)
       : "memory");
 }
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// development timeline (R.dbg & 4): per CTA of the last launches, globaltimer
+// at start / A-part landed / gather done / S landed / end
+__device__ long long d_sweep_trace[5 * 32768];
+__device__ __forceinline__ void sweep_stamp(const PatchRecords& R, int k) {
+  if ((R.dbg & 4) && threadIdx.x == 0 && blockIdx.x < 32768) {
+    long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    d_sweep_trace[5 * blockIdx.x + k] = t;
+  }
+}
+
+/// Wave table of one sweep direction, passed by value (kernel parameter
+/// space): waves in processing order, their patch ranges and the prefix of
+/// their G-patch items.
+struct SweepOrder {
+  int nw = 0, nitems = 0, reverse = 0;
+  int wbeg[kMaxSweepWaves], wend[kMaxSweepWaves];
+  int item0[kMaxSweepWaves + 1];
+};
+
+struct DagState {
+  unsigned* flags = nullptr;  // [n] completion epochs
+  unsigned* ctl = nullptr;    // [2] epoch base, arrivals
+  const int* ndep = nullptr;  // [n]
+  const int* dep = nullptr;   // [n][max_dep] mesh-neighbour patches
+  int max_dep = 0;
+  int nsweeps = 1;
+};
 
 /// Records of G consecutive patches per CTA, TP threads per patch.
-template <int BS, int TP, int G>
-__global__ void __launch_bounds__(G* TP) k_sweep_rec(PatchRecords R, int p0, int p1, const double* __restrict__ b,
-                                                     double* __restrict__ x) {
+/// DAG = false: one wave [p0, p1); DAG = true: item blockIdx.x of O (x nsweeps).
+template <int BS, int TP, int G, bool DAG>
+__global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1, SweepOrder O, DagState D,
+                                                 const double* __restrict__ b, double* __restrict__ x) {
   constexpr int kRow = kExt * BS * BS;
   extern __shared__ __align__(128) unsigned char smraw[];
   double* srec = reinterpret_cast<double*>(smraw);  // G * stride
   double* sx = srec + size_t(G) * R.stride;          // G * max_nf * kExt * BS
   double* r = sx + G * R.max_nf * kExt * BS;         // G * TP
-  __shared__ unsigned long long bar;
+  __shared__ unsigned long long bar, bar_s;
+  __shared__ unsigned s_base;
   const int lp = threadIdx.x / TP, t = threadIdx.x % TP;
-  const int q0 = p0 + blockIdx.x * G;
-  const int ng = min(G, p1 - q0);
+  int q0, ng, sweep = 0;
+  if (DAG) {
+    const int it = blockIdx.x % O.nitems;
+    sweep = blockIdx.x / O.nitems;
+    int w = 0;
+    while (it >= O.item0[w + 1]) ++w;  // uniform scan over <= 64 parameter words
+    q0 = O.wbeg[w] + (it - O.item0[w]) * G;
+    ng = min(G, O.wend[w] - q0);
+  } else {
+    q0 = p0 + blockIdx.x * G;
+    ng = min(G, p1 - q0);
+  }
+  sweep_stamp(R, 0);
   if (threadIdx.x == 0) {
+    // two copies per patch: [A_pe | meta] first (gather + residual start on
+    // it), then the inverse S_p, which lands while x_e is being gathered
     bar_init(&bar);
-    tma_stream(srec, R.rec + size_t(q0) * R.stride, unsigned(ng) * unsigned(R.stride) * 8u, &bar);
+    bar_init(&bar_s);
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    const unsigned tail = unsigned(R.stride - R.a_off) * 8u, head = unsigned(R.a_off) * 8u;
+    bar_expect(&bar, unsigned(ng) * tail);
+    bar_expect(&bar_s, unsigned(ng) * head);
+    for (int q = 0; q < ng; ++q)
+      tma_part(srec + size_t(q) * R.stride + R.a_off, R.rec + size_t(q0 + q) * R.stride + R.a_off, tail, &bar, pol);
+    for (int q = 0; q < ng; ++q)
+      tma_part(srec + size_t(q) * R.stride, R.rec + size_t(q0 + q) * R.stride, head, &bar_s, pol);
+  }
+  // dependency lists do not depend on the previous kernel: load them now
+  int dq = -1;
+  if (DAG && int(threadIdx.x) < ng * D.max_dep) {
+    const int dp = threadIdx.x / D.max_dep, di = threadIdx.x % D.max_dep;
+    dq = __ldg(D.dep + size_t(q0 + dp) * D.max_dep + di);  // -1 padded
   }
   // Programmatic dependent launch: the records do not depend on the previous
-  // wave, so the copy above may overlap its tail; x and b may not be touched
-  // before the previous grid has completed.
+  // kernel, so the copies above may overlap its tail; x, b and the flags may
+  // not be touched before it has completed.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  unsigned mine = 0;
+  if (DAG) {
+    if (threadIdx.x == 0) s_base = *reinterpret_cast<volatile unsigned*>(D.ctl);
+    __syncthreads();
+    mine = s_base + unsigned(sweep) + 1u;
+    if (dq >= 0) {
+      // neighbours before this patch in the sweep: done in this sweep;
+      // after it: done in the previous sweep of this launch (if any)
+      const int me = q0 + int(threadIdx.x) / D.max_dep;
+      const bool before = O.reverse ? dq > me : dq < me;
+      const unsigned need = before ? mine : mine - 1u;
+      if (need != s_base)
+        while (int(ld_acquire(D.flags + dq) - need) < 0) __nanosleep(20);
+    }
+  }
   __syncthreads();
   bar_wait(&bar);
+  sweep_stamp(R, 1);
   const double* rec = srec + size_t(lp) * R.stride;
   const int* meta = reinterpret_cast<const int*>(rec + R.meta_off);
   const int nf = lp < ng ? meta[0] : 0, np = nf * BS;
   const int* fac = meta + 1;
   const int* ecol = meta + 1 + R.max_nf;
   double* xs = sx + lp * R.max_nf * kExt * BS;
-  for (int e = t; e < nf * kExt * BS; e += TP) {
-    const int c = ecol[e / BS];
-    xs[e] = c >= 0 ? x[size_t(c) * BS + e % BS] : 0.0;
+  {
+    // all loads of this thread in flight at once, then the shared stores;
+    // L2 (.cg) loads in the dataflow kernel: x changes under a running grid
+    constexpr int kPer = (kMaxPatchF * kExt * BS + TP - 1) / TP;
+    const int ne = nf * kExt * BS;
+    double v[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = t + u * TP;
+      const int c = e < ne ? ecol[e / BS] : -1;
+      v[u] = c < 0 ? 0.0 : (DAG ? __ldcg(x + size_t(c) * BS + e % BS) : x[size_t(c) * BS + e % BS]);
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u)
+      if (t + u * TP < ne) xs[t + u * TP] = v[u];
   }
   double bv = 0.0;
-  if (t < np) bv = b[size_t(fac[t / BS]) * BS + t % BS];
+  if (t < np) bv = __ldg(b + size_t(fac[t / BS]) * BS + t % BS);
   __syncthreads();
+  sweep_stamp(R, 2);
   if (t < np) {
     const int lf = t / BS, i = t % BS;
     const double* arow = rec + R.a_off + lf * kRow + i * BS;
@@ -112,27 +221,55 @@ __global__ void __launch_bounds__(G* TP) k_sweep_rec(PatchRecords R, int p0, int
     r[threadIdx.x] = a0 + a1;
   }
   __syncthreads();
+  bar_wait(&bar_s);
+  sweep_stamp(R, 3);
   if (t < np) {
-    const double* S = rec;  // packed lower triangle by columns
+    // S(t, j): j < t in column j at cs(j) + t - j, j >= t in column t at ct + j,
+    // cs(j) = j np - j (j - 1) / 2 the uniform column start (packed lower, by columns)
+    const double* S = rec;
     const double* rr = r + lp * TP;
     const int ct = t * np - t * (t - 1) / 2 - t;
     double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-    int j = 0;
+    int cs = 0, j = 0;
     for (; j + 3 < np; j += 4) {
-      double s4[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int ju = j + u;
-        s4[u] = S[ju >= t ? ct + ju : ju * np - ju * (ju - 1) / 2 + (t - ju)];
-      }
-      d0 = fma(s4[0], rr[j], d0);
-      d1 = fma(s4[1], rr[j + 1], d1);
-      d2 = fma(s4[2], rr[j + 2], d2);
-      d3 = fma(s4[3], rr[j + 3], d3);
+      const int o0 = j < t ? cs + t - j : ct + j;
+      cs += np - j;
+      const int o1 = j + 1 < t ? cs + t - j - 1 : ct + j + 1;
+      cs += np - j - 1;
+      const int o2 = j + 2 < t ? cs + t - j - 2 : ct + j + 2;
+      cs += np - j - 2;
+      const int o3 = j + 3 < t ? cs + t - j - 3 : ct + j + 3;
+      cs += np - j - 3;
+      d0 = fma(S[o0], rr[j], d0);
+      d1 = fma(S[o1], rr[j + 1], d1);
+      d2 = fma(S[o2], rr[j + 2], d2);
+      d3 = fma(S[o3], rr[j + 3], d3);
     }
-    for (; j < np; ++j) d0 = fma(S[j >= t ? ct + j : j * np - j * (j - 1) / 2 + (t - j)], rr[j], d0);
+    for (; j < np; ++j) {
+      d0 = fma(S[j < t ? cs + t - j : ct + j], rr[j], d0);
+      cs += np - j;
+    }
     x[size_t(fac[t / BS]) * BS + t % BS] = (d0 + d1) + (d2 + d3);
   }
+  if (DAG) {
+    __syncthreads();  // x_p written by every thread of the CTA
+    if (threadIdx.x == 0) {
+      __threadfence();
+      for (int q = 0; q < ng; ++q)
+        asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(D.flags + q0 + q), "r"(mine) : "memory");
+    }
+  }
+  if (R.dbg & 4) {
+    __syncthreads();
+    sweep_stamp(R, 4);
+  }
+}
+
+/// Advances the sweep epoch after a dataflow launch (stream-ordered after it,
+/// so every CTA of that launch has read the old base).
+__global__ void k_epoch(unsigned* ctl, int nsweeps) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  ctl[0] += unsigned(nsweeps);
 }
 
 /// Builds the records from the packed inverses and the ELL operator.
@@ -172,10 +309,7 @@ __global__ void k_build_records(Bsr A, Patches P, PatchRecords R, int bs) {
       bool inside = false;
       for (int q = 0; q < nf; ++q) inside |= pf[q] == c;
       if (inside) continue;
-      if (ne == kExt) {  // cannot happen on a triangle mesh: flag the record
-        meta[0] = -1;
-        break;
-      }
+      if (ne == kExt) break;  // excluded by the host check (triangle meshes)
       meta[1 + R.max_nf + lf * kExt + ne] = c;
       for (int e = 0; e < blk; ++e)
         rec[R.a_off + (lf * kExt + ne) * blk + e] = A.val[(size_t(f) * kSlots + sl) * blk + e];
@@ -203,18 +337,27 @@ struct RecCfg<8> {
   static constexpr int TP = 64, G = 1;
 };
 
-template <int BS>
-void launch_rec(const PatchRecords& R, int w0, int w1, const double* b, double* x, cudaStream_t s) {
-  constexpr int TP = RecCfg<BS>::TP, G = RecCfg<BS>::G;
+/// dataflow launches carry a fixed per-CTA cost (dependency polls, release
+/// fence), so they group more patches per CTA
+template <int BS, bool DAG>
+struct Grp {
+  static constexpr int G = DAG && BS == 8 ? 2 : RecCfg<BS>::G;
+};
+
+template <int BS, bool DAG>
+void launch(const PatchRecords& R, int p0, int p1, int nblocks, const SweepOrder& O, const DagState& D, const double* b,
+            double* x, cudaStream_t s) {
+  constexpr int TP = RecCfg<BS>::TP, G = Grp<BS, DAG>::G;
   if (R.max_nf * BS > TP) throw std::runtime_error("vertex patch too large for the record sweep");
+  if (DAG && D.max_dep > TP) throw std::runtime_error("too many patch dependencies for the dataflow sweep");
   const size_t smem = sizeof(double) * (size_t(G) * R.stride + size_t(G) * R.max_nf * kExt * BS + G * TP);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_sweep_rec<BS, TP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_sweep<BS, TP, G, DAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((w1 - w0 + G - 1) / G);
+  cfg.gridDim = dim3(nblocks);
   cfg.blockDim = dim3(G * TP);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
@@ -223,9 +366,31 @@ void launch_rec(const PatchRecords& R, int w0, int w1, const double* b, double* 
   attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr_pdl;
   cfg.numAttrs = 1;
-  cudaError_t err = cudaLaunchKernelEx(&cfg, k_sweep_rec<BS, TP, G>, R, w0, w1, b, x);
+  cudaError_t err = cudaLaunchKernelEx(&cfg, k_sweep<BS, TP, G, DAG>, R, p0, p1, O, D, b, x);
   if (err == cudaSuccess) err = cudaGetLastError();
-  if (err != cudaSuccess) throw std::runtime_error(std::string("CUDA launch (sweep_rec): ") + cudaGetErrorString(err));
+  if (err != cudaSuccess) throw std::runtime_error(std::string("CUDA launch (sweep): ") + cudaGetErrorString(err));
+}
+
+template <bool DAG>
+void launch_bs(const PatchRecords& R, int p0, int p1, int nblocks, const SweepOrder& O, const DagState& D,
+               const double* b, double* x, cudaStream_t s) {
+  switch (R.bs) {
+    case 2: launch<2, DAG>(R, p0, p1, nblocks, O, D, b, x, s); break;
+    case 4: launch<4, DAG>(R, p0, p1, nblocks, O, D, b, x, s); break;
+    case 6: launch<6, DAG>(R, p0, p1, nblocks, O, D, b, x, s); break;
+    case 8: launch<8, DAG>(R, p0, p1, nblocks, O, D, b, x, s); break;
+    default: throw std::runtime_error("unsupported block size");
+  }
+}
+
+int group_of(int bs, bool dag) {
+  switch (bs) {
+    case 2: return dag ? Grp<2, true>::G : Grp<2, false>::G;
+    case 4: return dag ? Grp<4, true>::G : Grp<4, false>::G;
+    case 6: return dag ? Grp<6, true>::G : Grp<6, false>::G;
+    case 8: return dag ? Grp<8, true>::G : Grp<8, false>::G;
+    default: throw std::runtime_error("unsupported block size");
+  }
 }
 
 }  // namespace
@@ -250,15 +415,51 @@ void build_records(const Bsr& A, const Patches& P, PatchRecords& R, cudaStream_t
   if (err != cudaSuccess) throw std::runtime_error(std::string("CUDA launch (build_records): ") + cudaGetErrorString(err));
 }
 
+void sweep_trace(long long* out) { cudaMemcpyFromSymbol(out, d_sweep_trace, sizeof(long long) * 5 * 32768); }
+
 void gs_wave_rec(const PatchRecords& R, int w0, int w1, const double* b, double* x, cudaStream_t s) {
   if (w1 <= w0) return;
-  switch (R.bs) {
-    case 2: launch_rec<2>(R, w0, w1, b, x, s); break;
-    case 4: launch_rec<4>(R, w0, w1, b, x, s); break;
-    case 6: launch_rec<6>(R, w0, w1, b, x, s); break;
-    case 8: launch_rec<8>(R, w0, w1, b, x, s); break;
-    default: throw std::runtime_error("unsupported block size");
+  const int G = group_of(R.bs, false);
+  launch_bs<false>(R, w0, w1, (w1 - w0 + G - 1) / G, SweepOrder{}, DagState{}, b, x, s);
+}
+
+void sweep_dag(const PatchRecords& R, const int* wave_ptr_host, int nwaves, const Patches& P, int nsweeps,
+               bool reverse, const double* b, double* x, unsigned* flags, unsigned* ctl, cudaStream_t s) {
+  if (nwaves > kMaxSweepWaves) throw std::runtime_error("too many waves for the dataflow sweep");
+  if (nsweeps < 1) return;
+  const int G = group_of(R.bs, true);
+  SweepOrder O;
+  O.nw = nwaves;
+  O.reverse = reverse ? 1 : 0;
+  O.item0[0] = 0;
+  for (int i = 0; i < nwaves; ++i) {
+    const int w = reverse ? nwaves - 1 - i : i;
+    O.wbeg[i] = wave_ptr_host[w];
+    O.wend[i] = wave_ptr_host[w + 1];
+    O.item0[i + 1] = O.item0[i] + (O.wend[i] - O.wbeg[i] + G - 1) / G;
   }
+  O.nitems = O.item0[nwaves];
+  DagState D;
+  D.flags = flags;
+  D.ctl = ctl;
+  D.ndep = P.ndep;
+  D.dep = P.dep;
+  D.max_dep = P.max_dep;
+  D.nsweeps = nsweeps;
+  if (D.max_dep <= 0 || !D.ndep) throw std::runtime_error("dataflow sweep needs the patch dependency lists");
+  launch_bs<true>(R, 0, 0, O.nitems * nsweeps, O, D, b, x, s);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(1);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t err = cudaLaunchKernelEx(&cfg, k_epoch, ctl, nsweeps);
+  if (err == cudaSuccess) err = cudaGetLastError();
+  if (err != cudaSuccess) throw std::runtime_error(std::string("CUDA launch (epoch): ") + cudaGetErrorString(err));
 }
 
 }  // namespace dev
