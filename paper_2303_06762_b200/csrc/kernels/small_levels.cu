@@ -36,7 +36,7 @@ __device__ __forceinline__ unsigned su32(const void* p) { return unsigned(__cvta
 __device__ int d_trace_on = 0;
 __device__ long long d_trace[4096];
 __device__ __forceinline__ void stamp(int slot) {
-  if (d_trace_on && threadIdx.x == 0) {
+  if (threadIdx.x == 0 && d_trace_on) {
     long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     d_trace[slot] = t;
@@ -91,6 +91,7 @@ __device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, i
   const int lp = threadIdx.x / kTP, t = threadIdx.x % kTP;
   const bool producer = threadIdx.x >= kConsumers;
   const int total = npass * nsweeps;
+  const bool trace = threadIdx.x == 0 && d_trace_on;  // read once: a global load per pass costs ~1 us
   for (int i = threadIdx.x; i < npass; i += blockDim.x) v.pass[i] = passes[i];
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s)
@@ -121,9 +122,9 @@ __device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, i
       continue;
     }
     const int2 ps = pass_of(k);
-    if (d_trace_on && threadIdx.x == 0 && k < 1000) d_trace[4 * k] = clock64();
+    if (trace && k < 1000) d_trace[4 * k] = clock64();
     ring_wait(&v.bar[k % kStages], unsigned((k / kStages) & 1));
-    if (d_trace_on && threadIdx.x == 0 && k < 1000) d_trace[4 * k + 1] = clock64();
+    if (trace && k < 1000) d_trace[4 * k + 1] = clock64();
     const double* rec = v.ring + (size_t(k % kStages) * kPass + lp) * R.stride;
     int np = 0, g = 0;
     if (lp < ps.y) {
@@ -146,7 +147,7 @@ __device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, i
       }
     }
     __syncthreads();
-    if (d_trace_on && threadIdx.x == 0 && k < 1000) d_trace[4 * k + 2] = clock64();
+    if (trace && k < 1000) d_trace[4 * k + 2] = clock64();
     if (t < np) {
       // full column-major inverse: S(t, j) at j*np + t
       const double* rr = v.r + lp * kTP;
@@ -157,7 +158,7 @@ __device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, i
       v.sx[g] = (d[0] + d[1]) + (d[2] + d[3]);  // x_p = S_p (b_p - A_pe x_e), sweep_rec.cu
     }
     __syncthreads();
-    if (d_trace_on && threadIdx.x == 0 && k < 1000) d_trace[4 * k + 3] = clock64();
+    if (trace && k < 1000) d_trace[4 * k + 3] = clock64();
   }
 }
 
