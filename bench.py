@@ -167,6 +167,16 @@ def run_hpmg(args, rank, world, local, dist):
     head_bytes = vparts[6]  # bytes the head sweeps stream (records + vector rows)
     achieved = head_bytes / (head_sweep_ms * 1e-3) / 1e9 if head_sweep_ms > 0 else None
     ref_equiv = vparts[0] / (head_sweep_ms * 1e-3) / 1e9 if head_sweep_ms > 0 else None
+    # DRAM traffic of the head sweeps from the committed ncu --set full capture
+    # (bytes per patch, cold cache) scaled to this V-cycle's patch visits
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                           "r01_head_sweep_ncu.json")))
+        if args.config == "config2":
+            traffic = prof["dram_bytes_per_patch"] * 2 * B.level_patches(-1)
+    except (OSError, KeyError, ValueError):
+        pass
     # time-to-solution: device Uzawa (2 outer PCG solves to 1e-8)
     sol = H.uzawa_solve(B)
     launches = B.launches_per_apply()
@@ -192,14 +202,16 @@ def run_hpmg(args, rank, world, local, dist):
             "e2e": {"value": max(3, args.steps // 2) / (ms_e2e * 1e-3) * world, "unit": "V-cycles/s",
                     "h2d_bytes_per_step": int(8 * n), "d2h_bytes_per_step": int(8 * n)},
             "roofline": {"bound": "hbm",
-                         "kernel": "k_sweep_rec<8,64,1> (order-k head patch sweeps, TMA patch records)",
+                         "kernel": "k_sweep<8,64,1,waves> (order-k head patch sweeps, TMA patch records)",
                          "bytes_note": "achieved = bytes the head sweeps must stream in this formulation "
                                        "(per patch: packed symmetric inverse, the <=2 external A blocks per facet, "
                                        "meta; b/x rows and x_e gathers) / measured head-sweep time. "
                                        "reference_storage_equiv_gbs uses SURVEY 8(d)'s reference bytes "
                                        "(full np^2 factors, A rows read twice) over the same time.",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": (achieved / hbm) if achieved else None, "traffic": None,
+                         "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
+                         "traffic_note": "bytes per V-cycle over the head sweeps: ncu dram read+write per "
+                                         "patch (profiles/r01_head_sweep_ncu.json) x 2 sweeps x patches",
                          "peak_source": src, "algorithmic_bytes_per_vcycle": vbytes,
                          "head_sweep_bytes_per_vcycle": head_bytes, "head_sweep_ms": head_sweep_ms,
                          "reference_storage_head_bytes_per_vcycle": vparts[0],

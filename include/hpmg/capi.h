@@ -143,6 +143,7 @@ int64_t hpmg_n_full(const hpmg_ctx* ctx);       /* compound DOFs */
 int hpmg_ne(const hpmg_ctx* ctx);               /* finest elements */
 int hpmg_num_levels(const hpmg_ctx* ctx);
 int64_t hpmg_level_n(const hpmg_ctx* ctx, int level); /* free DOFs of level l (-1: finest system) */
+int hpmg_level_patches(const hpmg_ctx* ctx, int level); /* vertex patches of level l (-1: finest system) */
 int hpmg_symmetric(const hpmg_ctx* ctx);
 double hpmg_penalty(const hpmg_ctx* ctx);
 int hpmg_free_to_full(const hpmg_ctx* ctx, int64_t* out);

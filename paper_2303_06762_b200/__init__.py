@@ -94,6 +94,8 @@ def lib():
         getattr(L, name).argtypes = [vp]
     L.hpmg_level_n.restype = C.c_int64
     L.hpmg_level_n.argtypes = [vp, C.c_int]
+    L.hpmg_level_patches.restype = C.c_int
+    L.hpmg_level_patches.argtypes = [vp, C.c_int]
     L.hpmg_penalty.restype = C.c_double
     L.hpmg_penalty.argtypes = [vp]
     L.hpmg_free_to_full.argtypes = [vp, lp]
@@ -288,6 +290,9 @@ class MGPreconditioner:
 
     def level_n(self, level=-1):
         return int(lib().hpmg_level_n(self.h, level))
+
+    def level_patches(self, level=-1):
+        return int(lib().hpmg_level_patches(self.h, level))
 
     def matrix(self, level=-1):
         """Host CSR mirror in the reference free order (multigrid.hpp:133)."""

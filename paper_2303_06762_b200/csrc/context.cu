@@ -1013,6 +1013,12 @@ int64_t hpmg_level_n(const hpmg_ctx* ctx, int level) {
   if (level >= int(C.lv.size())) return -1;
   return C.lv[level]->n;
 }
+int hpmg_level_patches(const hpmg_ctx* ctx, int level) {
+  auto& C = *const_cast<hpmg_ctx*>(ctx);
+  if (level < 0) return C.top().P.n;
+  if (level >= int(C.lv.size())) return -1;
+  return C.lv[level]->P.n;
+}
 int hpmg_symmetric(const hpmg_ctx* ctx) { return ctx->advected ? 0 : 1; }
 double hpmg_penalty(const hpmg_ctx* ctx) { return ctx->opt.inv_eps; }
 int hpmg_free_to_full(const hpmg_ctx* ctx, int64_t* out) {
