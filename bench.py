@@ -95,14 +95,37 @@ class ClockSampler:
 
 
 def dist_init():
+    """One process per GPU under torchrun: NCCL when CUDA is visible (the
+    plumbing for the barrier and the max-over-ranks), gloo otherwise (CPU
+    tests). Replicas only: no collective touches the data path."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        import torch
         import torch.distributed as dist
-        dist.init_process_group("gloo")
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
         return rank, world, local, dist
     return 0, 1, 0, None
+
+
+def max_over_ranks(ms, dist, device="cpu"):
+    """Device-timed milliseconds of this rank -> the max over all ranks."""
+    if dist is None:
+        return ms
+    import torch
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_rate(units_per_rank, ms_max, world):
+    """Weak scaling: every rank processes the same units; the job rate is the
+    total over ranks divided by the slowest rank's time."""
+    return units_per_rank * world / (ms_max * 1e-3)
 
 
 def run_hpmg(args, rank, world, local, dist):
@@ -150,11 +173,7 @@ def run_hpmg(args, rank, world, local, dist):
         e1.synchronize()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
-        if dist:
-            t = torch.tensor([ms], dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms
+        return max_over_ranks(ms, dist, f"cuda:{local}" if dist and dist.get_backend() == "nccl" else "cpu")
 
     with ClockSampler(local) as clk:
         ms_dev = timed(step_dev, args.steps)
@@ -182,10 +201,9 @@ def run_hpmg(args, rank, world, local, dist):
     launches = B.launches_per_apply()
     out = None
     if rank == 0:
-        per_gpu = args.steps / (ms_dev * 1e-3)
         out = {
             "metric": METRIC if args.config == "config2" else f"hp-MG V-cycles/sec ({args.config})",
-            "value": per_gpu * world,
+            "value": whole_job_rate(args.steps, ms_dev, world),
             "unit": "V-cycles/s",
             "n_gpus": world,
             "steps": args.steps,
@@ -199,7 +217,7 @@ def run_hpmg(args, rank, world, local, dist):
             "config": {"workload": args.config, **cfg, "cycle": "V(1,1)", "smoother": "multiplicative vertex-patch",
                        "n_dofs": int(n), "parallelism": f"replicas x{world}",
                        "l2": "no flush needed: V-cycle streams %.2f GB per call (> 126 MB L2)" % (vbytes / 1e9)},
-            "e2e": {"value": max(3, args.steps // 2) / (ms_e2e * 1e-3) * world, "unit": "V-cycles/s",
+            "e2e": {"value": whole_job_rate(max(3, args.steps // 2), ms_e2e, world), "unit": "V-cycles/s",
                     "h2d_bytes_per_step": int(8 * n), "d2h_bytes_per_step": int(8 * n)},
             "roofline": {"bound": "hbm",
                          "kernel": "k_sweep<8,64,1,waves> (order-k head patch sweeps, TMA patch records)",
