@@ -1,10 +1,14 @@
 """GPU-vs-oracle parity of the hp-MG path, through the C ABI (libhpmg.so).
 
-Tolerances (SURVEY.md 8(c) protocol): operator apply relative <= 1e-13,
-preconditioner apply relative <= 1e-10 (explicit patch inverses vs. LU solves
-and wave-parallel pull residuals round differently from the sequential
-reference sweep), Krylov iteration counts +-1, final velocity relative
-L2 <= 1e-9 (north star).
+Tolerances (SURVEY.md 8(c) protocol, measured margins in tools/parity_margins.py):
+operator apply and rhs relative <= 1e-14 (measured <= 2.3e-16 / 2.2e-15);
+level operators entrywise <= 1e-13 of max |A|; one preconditioner apply or
+sweep relative <= APPLY_TOL = 2e-12 at the BASELINE penalty inv_eps = 1e3
+(measured <= 7e-13: explicit patch inverses vs. LU solves and pull residuals
+round differently from the sequential reference sweep). The round-off grows
+with the AL penalty (cond(A_pp) ~ inv_eps): 1.5e-12 at 1e4, 2.3e-10 at 1e6,
+so penalised cases scale the bound by inv_eps / 1e3. Krylov iteration counts
++-1, final velocity relative L2 <= 1e-9 (north star).
 """
 import numpy as np
 import pytest
@@ -33,6 +37,13 @@ def pair(k, base_n=2, levels=3, beta=1.0, nu=1.0, inv_eps=1e3, bc=None, seed=1, 
     return orc, gpu
 
 
+APPLY_TOL = 2e-12  # at inv_eps = 1e3; see the module docstring
+
+
+def apply_tol(inv_eps=1e3):
+    return APPLY_TOL * max(1.0, inv_eps / 1e3)
+
+
 def rel(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
 
@@ -43,8 +54,8 @@ def test_operator_and_rhs(k):
     assert gpu.n == orc.n and gpu.n_full == orc.n_full
     assert np.array_equal(gpu.free_to_full(), orc.free_to_full())
     x = O.random_vec(orc.n, 5)
-    assert rel(gpu.spmv(x), orc.spmv(x)) < 1e-13
-    assert rel(gpu.rhs(), orc.rhs()) < 1e-13
+    assert rel(gpu.spmv(x), orc.spmv(x)) < 1e-14
+    assert rel(gpu.rhs(), orc.rhs()) < 1e-14
     A_g, A_o = gpu.matrix(), orc.csr()
     assert abs(A_g - A_o).max() <= 1e-13 * abs(A_o).max()
 
@@ -66,7 +77,7 @@ def test_smoother_sweeps(k):
     for which in (0, 1):
         xg = gpu.smooth(level, which, x0, b, 1)
         xo = orc.smooth(level, which, x0, b, 1)
-        assert rel(xg, xo) < 1e-10
+        assert rel(xg, xo) < apply_tol()
 
 
 @pytest.mark.parametrize("k,sweeps", [(0, 1), (1, 3), (3, 2)])
@@ -80,7 +91,7 @@ def test_dataflow_schedule_sweeps(k, sweeps):
     for rep in range(2):
         b, x0 = O.random_vec(n, 7 + rep), O.random_vec(n, 9 + rep)
         for which in (0, 1):
-            assert rel(gpu.smooth(level, which, x0, b, sweeps), orc.smooth(level, which, x0, b, sweeps)) < 1e-10
+            assert rel(gpu.smooth(level, which, x0, b, sweeps), orc.smooth(level, which, x0, b, sweeps)) < apply_tol()
 
 
 @pytest.mark.parametrize("k,cycle", [(0, O.CYCLE_V), (2, O.CYCLE_VARV), (3, O.CYCLE_V)])
@@ -88,7 +99,7 @@ def test_dataflow_schedule_apply(k, cycle):
     orc, gpu = pair(k, levels=4, cycle=cycle, schedule="dataflow")
     for seed in (11, 12):
         b = O.random_vec(orc.n, seed)
-        assert rel(gpu.apply(b), orc.apply(b)) < 1e-10
+        assert rel(gpu.apply(b), orc.apply(b)) < apply_tol()
 
 
 @pytest.mark.parametrize("k,cycle", [(0, O.CYCLE_V), (1, O.CYCLE_V), (2, O.CYCLE_W), (3, O.CYCLE_V),
@@ -96,13 +107,20 @@ def test_dataflow_schedule_apply(k, cycle):
 def test_preconditioner_apply(k, cycle):
     orc, gpu = pair(k, levels=4, cycle=cycle)
     b = O.random_vec(orc.n, 11)
-    assert rel(gpu.apply(b), orc.apply(b)) < 1e-10
+    assert rel(gpu.apply(b), orc.apply(b)) < apply_tol()
+
+
+@pytest.mark.parametrize("k,inv_eps", [(2, 1e4), (3, 1e6)])
+def test_preconditioner_apply_penalised(k, inv_eps):
+    orc, gpu = pair(k, levels=4, inv_eps=inv_eps)
+    b = O.random_vec(orc.n, 11)
+    assert rel(gpu.apply(b), orc.apply(b)) < apply_tol(inv_eps)
 
 
 def test_additive_smoother_apply():
     orc, gpu = pair(1, levels=3, smoother=O.SM_ADD)
     b = O.random_vec(orc.n, 13)
-    assert rel(gpu.apply(b), orc.apply(b)) < 1e-10
+    assert rel(gpu.apply(b), orc.apply(b)) < apply_tol()
 
 
 def test_apply_bit_identical_repeat():
