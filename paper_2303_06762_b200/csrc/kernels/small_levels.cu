@@ -134,14 +134,14 @@ __device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, i
         const int lf = t >> 1, i = t & 1;
         g = 2 * meta[1 + lf] + i;
         const int* cols = meta + 1 + R.max_nf + lf * kExt;
-        const double* arow = rec + R.a_off + lf * kExt * 4 + i * 2;
+        const double* acol = rec + R.a_off + lf * kExt * 4 + i;  // column-major 2x2 blocks
         double a0 = v.sb[g], a1 = 0.0;
 #pragma unroll
         for (int sl = 0; sl < kExt; ++sl) {
           const int c = cols[sl];
           const int cc = c >= 0 ? c : 0;  // empty slots hold zero blocks
-          a0 = fma(-arow[sl * 4], v.sx[2 * cc], a0);
-          a1 = fma(-arow[sl * 4 + 1], v.sx[2 * cc + 1], a1);
+          a0 = fma(-acol[sl * 4], v.sx[2 * cc], a0);
+          a1 = fma(-acol[sl * 4 + 2], v.sx[2 * cc + 1], a1);
         }
         v.r[threadIdx.x] = a0 + a1;
       }

@@ -6,7 +6,7 @@
 //   [ patch inverse S_p (packed lower triangle by columns, or full)
 //   | A_pe: per patch facet the <= 2 blocks coupling it to facets outside the
 //     patch (facet (v,w) of the star of v couples to (v,a), (v,b) inside and
-//     to the far edges (w,a), (w,b) outside)
+//     to the far edges (w,a), (w,b) outside), each block column-major
 //   | int32 meta: nf, facet ids, the external block columns ]
 // and the sweep sets x_p = S_p (b_p - A_pe x_e): with S_p A_pp = I this is the
 // reference update x_p += S_p (b - A x)_p without ever reading A_pp, which
@@ -207,16 +207,20 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
   sweep_stamp(R, 2);
   if (t < np) {
     const int lf = t / BS, i = t % BS;
-    const double* arow = rec + R.a_off + lf * kRow + i * BS;
+    // external blocks are stored column-major: A(i, j) at j*BS + i, so the
+    // rows of a block are consecutive words; the column order is rotated by
+    // the facet so the facets of a warp hit distinct banks, while all rows of
+    // one facet read the same x_e word (broadcast)
+    const double* acol = rec + R.a_off + lf * kRow + i;
     const double* xr = xs + lf * kExt * BS;
     double a0 = bv, a1 = 0.0;
 #pragma unroll
     for (int sl = 0; sl < kExt; ++sl)
 #pragma unroll
       for (int jj = 0; jj < BS; jj += 2) {
-        const int j0 = (jj + i) % BS, j1 = (jj + 1 + i) % BS;  // rotated: rows of a block hit distinct banks
-        a0 = fma(-arow[sl * BS * BS + j0], xr[sl * BS + j0], a0);
-        a1 = fma(-arow[sl * BS * BS + j1], xr[sl * BS + j1], a1);
+        const int j0 = (jj + lf) % BS, j1 = (jj + 1 + lf) % BS;
+        a0 = fma(-acol[sl * BS * BS + j0 * BS], xr[sl * BS + j0], a0);
+        a1 = fma(-acol[sl * BS * BS + j1 * BS], xr[sl * BS + j1], a1);
       }
     r[threadIdx.x] = a0 + a1;
   }
@@ -240,10 +244,12 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
       cs += np - j - 2;
       const int o3 = j + 3 < t ? cs + t - j - 3 : ct + j + 3;
       cs += np - j - 3;
-      d0 = fma(S[o0], rr[j], d0);
-      d1 = fma(S[o1], rr[j + 1], d1);
-      d2 = fma(S[o2], rr[j + 2], d2);
-      d3 = fma(S[o3], rr[j + 3], d3);
+      const double2 r01 = *reinterpret_cast<const double2*>(rr + j);  // broadcast, 16-byte words
+      const double2 r23 = *reinterpret_cast<const double2*>(rr + j + 2);
+      d0 = fma(S[o0], r01.x, d0);
+      d1 = fma(S[o1], r01.y, d1);
+      d2 = fma(S[o2], r23.x, d2);
+      d3 = fma(S[o3], r23.y, d3);
     }
     for (; j < np; ++j) {
       d0 = fma(S[j < t ? cs + t - j : ct + j], rr[j], d0);
@@ -311,8 +317,8 @@ __global__ void k_build_records(Bsr A, Patches P, PatchRecords R, int bs) {
       if (inside) continue;
       if (ne == kExt) break;  // excluded by the host check (triangle meshes)
       meta[1 + R.max_nf + lf * kExt + ne] = c;
-      for (int e = 0; e < blk; ++e)
-        rec[R.a_off + (lf * kExt + ne) * blk + e] = A.val[(size_t(f) * kSlots + sl) * blk + e];
+      for (int e = 0; e < blk; ++e)  // column-major block: (r, c) at c*bs + r
+        rec[R.a_off + (lf * kExt + ne) * blk + (e % bs) * bs + e / bs] = A.val[(size_t(f) * kSlots + sl) * blk + e];
       ++ne;
     }
   }
