@@ -91,11 +91,13 @@ typedef struct {
   const double* load_per_element; /* alternative: constant force per finest element (2*ne) */
   const double* wind_compound;    /* advection HDGVelocity on the finest mesh at order k: */
   const double* wind_interior;    /*   compound (n_full) and interior (ne*k(k+1)); NULL = Stokes */
-  int newton;
+  int newton;                     /* Newton linearisation about the wind (AssemblyOptions::newton) */
   const double* structured_load;  /* alternative: seeded structured force (hpmg_seeded_load layout) */
   int structured_n;               /*   on an n x n unit-square grid, mapped onto the finest elements */
   hpmg_field_fn wind;             /* alternative advection state: a wind field, interpolated into   */
   void* wind_user;                /*   the hybrid RT_k space as interpolate_hdg does (Oseen/Picard) */
+  const double* mass_compound;    /* pseudo-time mass field (AssemblyOptions::mass_field): HDG     */
+  const double* mass_interior;    /*   velocity at order k, load += mass_coef (m, v); NULL = none   */
 } hpmg_problem;
 
 /* Analytic fields usable as hpmg_field_fn (no host-language callback cost):
@@ -120,6 +122,7 @@ typedef struct {
 typedef struct {
   int outer_iterations;       /* UzawaOptions (uzawa.hpp:9-21): 2 */
   hpmg_krylov_opts krylov;
+  const double* initial_velocity; /* warm start, full compound (host); NULL = zero */
 } hpmg_uzawa_opts;
 
 typedef struct {
@@ -135,6 +138,7 @@ typedef struct {
 int hpmg_create(hpmg_ctx** out, const hpmg_mesh_desc* mesh, const hpmg_options* opt, const hpmg_problem* prob);
 void hpmg_destroy(hpmg_ctx* ctx);
 const char* hpmg_last_error(void);
+void hpmg_set_last_error(const char* msg); /* for drivers layered on this ABI (hpmg_ns_solve) */
 const char* hpmg_ctx_error(const hpmg_ctx* ctx);
 
 /* ---- sizes and host mirrors ---- */
@@ -164,6 +168,47 @@ int hpmg_pcg(hpmg_ctx* ctx, const double* b, double* x, const hpmg_krylov_opts* 
 int hpmg_gmres(hpmg_ctx* ctx, const double* b, double* x, const hpmg_krylov_opts* o, hpmg_solve_stats* st, int flags);
 /* velocity: full compound (n_full), pressure: element means (ne); host pointers */
 int hpmg_uzawa(hpmg_ctx* ctx, const hpmg_uzawa_opts* o, double* velocity, double* pressure, hpmg_uzawa_report* rep);
+/* rt_l2_norm (assembly.hpp:487-501) of the finest-space RT field given by its
+ * full compound and interior ([ne][k(k+1)]) coefficients; host pointers */
+double hpmg_rt_l2_norm(hpmg_ctx* ctx, const double* compound_full, const double* interior);
+/* interpolate_hdg (assembly.hpp:40-62) of a field into the finest space at
+ * order k in this library's interior basis: compound (n_full), interior (ne*k(k+1)) */
+int hpmg_interpolate_hdg(hpmg_ctx* ctx, hpmg_field_fn field, void* user, double* compound_full, double* interior);
+
+/* ---- stationary Navier-Stokes driver (ns.hpp:10-149) ---- */
+typedef struct {
+  double picard_tol;          /* 1e-4: Picard ends when ||u_n - u_{n-1}||_L2 < picard_tol */
+  double newton_rel_tol;      /* 1e-8 */
+  double newton_abs_tol;      /* 1e-10: Newton ends when the update < max(rel |u|, abs) */
+  int max_picard;             /* 60 */
+  int max_newton;             /* 25 */
+  double pseudo_time_inv;     /* 0: backward-Euler pseudo time step 1/pseudo_time_inv in Picard */
+  hpmg_uzawa_opts uzawa;      /* every linearised step (initial_velocity is set by the driver) */
+} hpmg_ns_opts;
+
+typedef struct {
+  int picard_iterations, newton_iterations;
+  int n_picard_inner, n_newton_inner;
+  int picard_inner[512];      /* Krylov counts of every Picard Uzawa step */
+  int newton_inner[256];
+  double picard_diffs[128];   /* consecutive velocity difference norms */
+  double newton_diffs[64];
+  int converged, not_applicable;
+  double final_divergence;
+  double seconds;             /* wall time of the whole driver */
+  double setup_seconds;       /* of which: preconditioner setups (one per linearised step) */
+} hpmg_ns_report;
+
+/* Stokes initial guess, Picard steps about the previous velocity, then
+ * total-update Newton steps; each step rebuilds the hp-MG hierarchy around the
+ * current velocity and warm-starts the AL-Uzawa solve from it. `opt` supplies
+ * k, nu, inv_eps and the MG options (beta and mass_coef are ignored as in the
+ * reference driver); `prob` supplies bc and load (its wind fields are ignored).
+ * Outputs: final velocity (full compound n_full), interior (ne*k(k+1)),
+ * pressure (ne); host pointers. */
+int hpmg_ns_solve(const hpmg_mesh_desc* mesh, const hpmg_options* opt, const hpmg_problem* prob,
+                  const hpmg_ns_opts* ns, double* velocity, double* interior, double* pressure,
+                  hpmg_ns_report* rep);
 /* recover_locals on the finest system: interior (ne*k(k+1)), p_ortho (ne*(ns-1)),
  * grad (ne*4*ns, element-major); interior coefficients refer to this library's
  * interior RT basis (same span as the reference's). */

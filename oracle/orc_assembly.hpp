@@ -313,14 +313,21 @@ inline LocalBlocks local_blocks(const ElemCtx& cx, int e, const AsmOpt& opt) {
         Real wtx = 0, wty = 0;
         for (int a = 0; a < 3 * nfd; ++a) { wtx += T(0, a) * xw[a]; wty += T(1, a) * xw[a]; }
         for (int j = 0; j < cx.no; ++j) { wtx += T(0, cx.nc + j) * xw[cx.nc + j]; wty += T(1, cx.nc + j) * xw[cx.nc + j]; }
-        const Real wn = wtx * n.x + wty * n.y;
+        Real wn = wtx * n.x + wty * n.y;
+        V2 tsk;  // tangential skeleton trace of the wind on this edge
+        for (int a = 3 * nfd; a < 6 * nfd; ++a) { tsk.x += T(0, a) * xw[a]; tsk.y += T(1, a) * xw[a]; }
+        // round-off guard: |w.n| below 1e-13 of the magnitude of the terms it
+        // is summed from (|RT coefficient| x |basis trace|, plus the
+        // tangential skeleton trace) is the exact-arithmetic w.n = 0 (inflow
+        // branch), not a basis-dependent round-off sign (no-slip walls, the lid,
+        // a solenoidal wind along the boundary, nodes where the wind vanishes)
+        Real wabs = std::sqrt(tsk.x * tsk.x + tsk.y * tsk.y);
+        for (int a = 0; a < 3 * nfd; ++a) wabs += std::abs(xw[a]) * std::sqrt(T(0, a) * T(0, a) + T(1, a) * T(1, a));
+        for (int j = 0; j < cx.no; ++j)
+          wabs += std::abs(xw[cx.nc + j]) * std::sqrt(T(0, cx.nc + j) * T(0, cx.nc + j) + T(1, cx.nc + j) * T(1, cx.nc + j));
+        if (std::abs(wn) <= 1e-13 * wabs) wn = 0.0;
         const bool outflow = wn > 0;
-        V2 up0;
-        if (outflow) {
-          up0 = V2(wtx, wty);
-        } else {
-          for (int a = 3 * nfd; a < 6 * nfd; ++a) { up0.x += T(0, a) * xw[a]; up0.y += T(1, a) * xw[a]; }
-        }
+        const V2 up0 = outflow ? V2(wtx, wty) : tsk;
         for (int a = 0; a < nv; ++a) {
           V2 ta(D(0, a), D(1, a));
           if (ta.x == 0.0 && ta.y == 0.0) continue;

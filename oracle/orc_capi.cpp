@@ -5,6 +5,7 @@
 #include <random>
 
 #include "orc_mg.hpp"
+#include "orc_ns.hpp"
 
 using namespace orc;
 
@@ -23,12 +24,33 @@ typedef struct {
   int wind_kind;   // 0 none, 1 rotation, 2 curl of sin^2(pi x) sin^2(pi y)
   int cycle, smoother, smooth_steps;
   double jacobi_damping;
+  int newton;      // Newton linearisation about the wind (AssemblyOptions::newton)
+  int mass_field;  // 1: pseudo-time mass field = the interpolated wind (AssemblyOptions::mass_field)
 } orc_problem;
 
 typedef struct {
   int iterations, converged, not_applicable;
   double residual;
 } orc_stats;
+
+/// NSOptions (inc/ns.hpp:10-28) + the Uzawa/Krylov options of every step.
+typedef struct {
+  double picard_tol, newton_rel_tol, newton_abs_tol;
+  int max_picard, max_newton;
+  double pseudo_time_inv;
+  int outer_iterations;
+  double rel_tol, abs_tol;
+  int max_iterations;
+} orc_ns_opts;
+
+/// NSReport (inc/ns.hpp:30-53), fixed capacity.
+typedef struct {
+  int picard_iterations, newton_iterations, n_picard_inner, n_newton_inner;
+  int picard_inner[512], newton_inner[256];
+  double picard_diffs[128], newton_diffs[64];
+  int converged, not_applicable;
+  double final_divergence, seconds;
+} orc_ns_report;
 }
 
 namespace {
@@ -129,6 +151,8 @@ void* orc_mg_create(const orc_problem* p) {
     if (p->wind_kind) {
       pr->wind = interpolate_hdg(fine, p->k, make_wind(p->wind_kind));
       pr->opt.advection = &pr->wind;
+      pr->opt.newton = p->newton != 0;
+      if (p->mass_field) pr->opt.mass_field = &pr->wind;
     }
     MGOpt mo;
     mo.cycle = p->cycle;
@@ -245,11 +269,16 @@ void orc_mg_krylov(void* h, int method, const double* b, double* x, double rel_t
 /// Runs uzawa_solve; velocity is full compound (n_full), pressure ne,
 /// inner[outer_max] iteration counts; returns number of outer steps done.
 int orc_mg_uzawa(void* h, int outer, double rel_tol, double abs_tol, int max_it, double* velocity, double* pressure,
-                 int* inner, double* div_hist, int* flags, double* seconds) {
+                 int* inner, double* div_hist, int* flags, double* seconds, const double* initial_full) {
   auto* p = static_cast<Problem*>(h);
   UzawaOpt o;
   o.outer_iterations = outer;
   o.krylov = {rel_tol, abs_tol, max_it};
+  Vec init;
+  if (initial_full) {  // warm start (UzawaOptions::initial_velocity)
+    init.assign(initial_full, initial_full + p->mg->constraints().n_full);
+    o.initial_velocity = &init;
+  }
   auto t0 = std::chrono::steady_clock::now();
   StokesSolution s = uzawa(*p->mg, o);
   if (seconds) *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -280,6 +309,73 @@ void orc_mg_wind(void* h, double* compound, double* interior) {
   auto* p = static_cast<Problem*>(h);
   std::memcpy(compound, p->wind.compound.data(), sizeof(double) * p->wind.compound.size());
   if (!p->wind.interior.empty()) std::memcpy(interior, p->wind.interior.data(), sizeof(double) * p->wind.interior.size());
+}
+
+/// rt_l2_norm (inc/assembly.hpp:487-501) on the problem's finest space.
+double orc_mg_rt_l2_norm(void* h, const double* compound_full, const double* interior) {
+  auto* p = static_cast<Problem*>(h);
+  const Space& V = p->mg->space();
+  Vec c(compound_full, compound_full + V.n_compound());
+  Vec i(interior, interior + V.n_interior());
+  return rt_l2_norm(*V.mesh, V, c, i);
+}
+
+/// navier_stokes_solve (inc/ns.hpp:69-149) for the problem description `p`
+/// (mesh, k, nu, inv_eps, bc, load, MG options; wind/beta/mass ignored as in
+/// the reference driver). Outputs the final compound velocity, interior
+/// coefficients and element pressures. Returns 0, or -1 on a setup error.
+int orc_ns_solve(const orc_problem* p, const orc_ns_opts* o, double* velocity, double* interior, double* pressure,
+                 orc_ns_report* rep) {
+  try {
+    auto t0 = std::chrono::steady_clock::now();
+    Hierarchy hier = Hierarchy::build(base_mesh(p), p->levels);
+    Vec loadcopy;
+    Field load;
+    if (p->load_kind == 1) {
+      int nf = p->base_n << (p->levels - 1);
+      loadcopy.assign(p->load, p->load + std::size_t(4) * nf * nf);
+      const double* F = loadcopy.data();
+      load = [F, nf](const V2& x) { return structured_load(F, nf, x); };
+    } else {
+      load = make_named_load(p->load_kind);
+    }
+    NSOpt no;
+    no.picard_tol = o->picard_tol;
+    no.newton_rel_tol = o->newton_rel_tol;
+    no.newton_abs_tol = o->newton_abs_tol;
+    no.max_picard = o->max_picard;
+    no.max_newton = o->max_newton;
+    no.pseudo_time_inv = o->pseudo_time_inv;
+    no.mg.cycle = p->cycle;
+    no.mg.smoother = p->smoother;
+    no.mg.smooth_steps = p->smooth_steps;
+    no.mg.jacobi_damping = p->jacobi_damping;
+    no.uzawa.outer_iterations = o->outer_iterations;
+    no.uzawa.krylov = {o->rel_tol, o->abs_tol, o->max_iterations};
+    NSSolution s = navier_stokes_solve(hier, p->k, make_bc(p->bc_kind), p->nu, load, p->inv_eps, no);
+    std::memset(rep, 0, sizeof(*rep));
+    rep->picard_iterations = s.report.picard_iterations;
+    rep->newton_iterations = s.report.newton_iterations;
+    rep->n_picard_inner = int(std::min<std::size_t>(s.report.picard_inner.size(), 512));
+    rep->n_newton_inner = int(std::min<std::size_t>(s.report.newton_inner.size(), 256));
+    for (int i = 0; i < rep->n_picard_inner; ++i) rep->picard_inner[i] = s.report.picard_inner[i];
+    for (int i = 0; i < rep->n_newton_inner; ++i) rep->newton_inner[i] = s.report.newton_inner[i];
+    for (std::size_t i = 0; i < s.report.picard_diffs.size() && i < 128; ++i) rep->picard_diffs[i] = s.report.picard_diffs[i];
+    for (std::size_t i = 0; i < s.report.newton_diffs.size() && i < 64; ++i) rep->newton_diffs[i] = s.report.newton_diffs[i];
+    rep->converged = s.report.converged;
+    rep->not_applicable = s.report.not_applicable;
+    rep->final_divergence = s.report.final_divergence;
+    if (!s.velocity.compound.empty()) {
+      std::memcpy(velocity, s.velocity.compound.data(), sizeof(double) * s.velocity.compound.size());
+      std::memcpy(interior, s.velocity.interior.data(), sizeof(double) * s.velocity.interior.size());
+      std::memcpy(pressure, s.pressure.data(), sizeof(double) * s.pressure.size());
+    }
+    rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
 }
 
 /// Time `reps` preconditioner applications on a fixed seeded vector (CPU baseline).

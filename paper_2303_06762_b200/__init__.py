@@ -47,7 +47,8 @@ class _Problem(C.Structure):
                 ("load_per_element", C.POINTER(C.c_double)), ("wind_compound", C.POINTER(C.c_double)),
                 ("wind_interior", C.POINTER(C.c_double)), ("newton", C.c_int),
                 ("structured_load", C.POINTER(C.c_double)), ("structured_n", C.c_int),
-                ("wind", FIELD_FN), ("wind_user", C.c_void_p)]
+                ("wind", FIELD_FN), ("wind_user", C.c_void_p),
+                ("mass_compound", C.POINTER(C.c_double)), ("mass_interior", C.POINTER(C.c_double))]
 
 
 class _KOpts(C.Structure):
@@ -60,7 +61,21 @@ class _Stats(C.Structure):
 
 
 class _UOpts(C.Structure):
-    _fields_ = [("outer_iterations", C.c_int), ("krylov", _KOpts)]
+    _fields_ = [("outer_iterations", C.c_int), ("krylov", _KOpts), ("initial_velocity", C.POINTER(C.c_double))]
+
+
+class _NSOpts(C.Structure):
+    _fields_ = [("picard_tol", C.c_double), ("newton_rel_tol", C.c_double), ("newton_abs_tol", C.c_double),
+                ("max_picard", C.c_int), ("max_newton", C.c_int), ("pseudo_time_inv", C.c_double),
+                ("uzawa", _UOpts)]
+
+
+class _NSReport(C.Structure):
+    _fields_ = [("picard_iterations", C.c_int), ("newton_iterations", C.c_int), ("n_picard_inner", C.c_int),
+                ("n_newton_inner", C.c_int), ("picard_inner", C.c_int * 512), ("newton_inner", C.c_int * 256),
+                ("picard_diffs", C.c_double * 128), ("newton_diffs", C.c_double * 64), ("converged", C.c_int),
+                ("not_applicable", C.c_int), ("final_divergence", C.c_double), ("seconds", C.c_double),
+                ("setup_seconds", C.c_double)]
 
 
 class _UReport(C.Structure):
@@ -109,6 +124,11 @@ def lib():
     L.hpmg_gmres.argtypes = [vp, vp, vp, C.POINTER(_KOpts), C.POINTER(_Stats), C.c_int]
     L.hpmg_uzawa.argtypes = [vp, C.POINTER(_UOpts), dp, dp, C.POINTER(_UReport)]
     L.hpmg_recover.argtypes = [vp, vp, vp, vp, vp]
+    L.hpmg_interpolate_hdg.argtypes = [vp, FIELD_FN, vp, dp, dp]
+    L.hpmg_rt_l2_norm.restype = C.c_double
+    L.hpmg_rt_l2_norm.argtypes = [vp, dp, dp]
+    L.hpmg_ns_solve.argtypes = [C.POINTER(_Mesh), C.POINTER(_Options), C.POINTER(_Problem), C.POINTER(_NSOpts),
+                                dp, dp, dp, C.POINTER(_NSReport)]
     L.hpmg_stream.restype = vp
     L.hpmg_stream.argtypes = [vp]
     L.hpmg_vcycle_bytes.restype = C.c_double
@@ -213,7 +233,7 @@ class MGPreconditioner:
     def __init__(self, *, mesh="unit_square", base_n=2, levels=2, k=0, nu=1.0, beta=0.0, mass_coef=0.0,
                  inv_eps=1e6, cycle=CYCLE_W, smoother=SMOOTH_MULTIPLICATIVE, smooth_steps=1,
                  jacobi_damping=1.0 / 3.0, bc=None, load=None, load_per_element=None, structured_load=None,
-                 wind=None, schedule="waves"):
+                 wind=None, newton=False, mass_field=None, schedule="waves"):
         L = lib()
         md = _Mesh()
         rc = (L.hpmg_unit_square_mesh if mesh == "unit_square" else L.hpmg_step_mesh)(base_n, levels, C.byref(md))
@@ -226,8 +246,22 @@ class MGPreconditioner:
         self._bc = _field(bc)
         self._load = _field(load)
         self._keep = []
-        self._wind = _field(wind)  # Oseen: wind field interpolated by the library
-        prob = _Problem(self._bc, None, self._load, None, None, None, None, 0, None, 0, self._wind, None)
+        # Oseen / Newton advection state: a wind field (callable or NAMED_FIELDS
+        # name) interpolated by the library, or an HDG velocity (compound, interior)
+        hdg_wind = isinstance(wind, tuple)
+        self._wind = _field(None if hdg_wind else wind)
+        prob = _Problem(self._bc, None, self._load, None, None, None, None, int(bool(newton)), None, 0, self._wind,
+                        None, None, None)
+        if hdg_wind:
+            wc, wi = (np.ascontiguousarray(a, dtype=np.float64) for a in wind)
+            self._keep += [wc, wi]
+            prob.wind_compound = _dp(wc)
+            prob.wind_interior = _dp(wi) if wi.size else None
+        if mass_field is not None:  # pseudo-time load mass_coef (m, v): HDG velocity (compound, interior)
+            mc, mi = (np.ascontiguousarray(a, dtype=np.float64) for a in mass_field)
+            self._keep += [mc, mi]
+            prob.mass_compound = _dp(mc)
+            prob.mass_interior = _dp(mi) if mi.size else None
         if load_per_element is not None:
             a = np.ascontiguousarray(load_per_element, dtype=np.float64)
             self._keep.append(a)
@@ -290,6 +324,24 @@ class MGPreconditioner:
 
     def level_n(self, level=-1):
         return int(lib().hpmg_level_n(self.h, level))
+
+    def interpolate(self, field):
+        """interpolate_hdg of a field (callable or NAMED_FIELDS name) into the
+        finest space: (compound full, interior [ne, k(k+1)])."""
+        f = _field(field)
+        c = np.zeros(self.n_full)
+        i = np.zeros(max(self.ne * self.k * (self.k + 1), 1))
+        self._check(lib().hpmg_interpolate_hdg(self.h, f, None, _dp(c), _dp(i)))
+        return c, i[: self.ne * self.k * (self.k + 1)].reshape(self.ne, self.k * (self.k + 1))
+
+    def rt_l2_norm(self, compound_full, interior):
+        """L2 norm of the finest-space RT field (reference assembly.hpp:487-501)."""
+        c = np.ascontiguousarray(compound_full, dtype=np.float64)
+        i = np.ascontiguousarray(interior, dtype=np.float64).ravel()
+        v = lib().hpmg_rt_l2_norm(self.h, _dp(c), _dp(i) if i.size else None)
+        if v < 0:
+            raise HpmgError(lib().hpmg_ctx_error(self.h).decode())
+        return v
 
     def level_patches(self, level=-1):
         return int(lib().hpmg_level_patches(self.h, level))
@@ -388,14 +440,92 @@ def gmres(B: MGPreconditioner, b, x=None, opt: KrylovOptions | None = None):
     return x, SolveStats(st.iterations, bool(st.converged), bool(st.not_applicable), st.residual)
 
 
-def uzawa_solve(B: MGPreconditioner, outer_iterations=2, krylov: KrylovOptions | None = None):
-    """Augmented-Lagrangian Uzawa loop on the device (reference uzawa.hpp:51-91)."""
+def uzawa_solve(B: MGPreconditioner, outer_iterations=2, krylov: KrylovOptions | None = None,
+                initial_velocity=None):
+    """Augmented-Lagrangian Uzawa loop on the device (reference uzawa.hpp:51-91);
+    `initial_velocity` (full compound) warm-starts the first Krylov solve."""
     krylov = krylov or KrylovOptions()
     vel = np.empty(B.n_full)
     p = np.empty(B.ne)
     rep = _UReport()
-    o = _UOpts(outer_iterations, krylov.c())
+    init = None if initial_velocity is None else np.ascontiguousarray(initial_velocity, dtype=np.float64)
+    o = _UOpts(outer_iterations, krylov.c(), None if init is None else _dp(init))
     B._check(lib().hpmg_uzawa(B.h, C.byref(o), _dp(vel), _dp(p), C.byref(rep)))
     r = UzawaReport(list(rep.inner_iterations[: rep.n_outer]), list(rep.divergence_history[: rep.n_outer]),
                     bool(rep.converged), bool(rep.not_applicable), rep.final_divergence, rep.seconds)
     return StokesSolution(vel, p, r)
+
+
+@dataclass
+class NSReport:
+    picard_iterations: int
+    newton_iterations: int
+    picard_inner: list
+    newton_inner: list
+    picard_diffs: list
+    newton_diffs: list
+    converged: bool
+    not_applicable: bool
+    final_divergence: float
+    seconds: float
+    setup_seconds: float
+
+
+@dataclass
+class NSSolution:
+    velocity: np.ndarray   # full compound
+    interior: np.ndarray   # [ne, k(k+1)] interior RT coefficients
+    pressure: np.ndarray   # element means
+    report: NSReport
+
+
+def navier_stokes_solve(*, mesh="unit_square", base_n=2, levels=2, k=0, nu=1.0, inv_eps=1e6, bc=None, load=None,
+                        load_per_element=None, structured_load=None, cycle=CYCLE_W, smoother=SMOOTH_MULTIPLICATIVE,
+                        smooth_steps=1, jacobi_damping=1.0 / 3.0, schedule="waves", picard_tol=1e-4,
+                        newton_rel_tol=1e-8, newton_abs_tol=1e-10, max_picard=60, max_newton=25,
+                        pseudo_time_inv=0.0, outer_iterations=2, krylov: KrylovOptions | None = None):
+    """Stationary Navier-Stokes driver (reference ns.hpp:69-149): Stokes guess,
+    Picard, then Newton, each linearised step on a device hp-MG hierarchy
+    rebuilt around the current velocity, warm-started AL-Uzawa."""
+    L = lib()
+    md = _Mesh()
+    rc = (L.hpmg_unit_square_mesh if mesh == "unit_square" else L.hpmg_step_mesh)(base_n, levels, C.byref(md))
+    if rc:
+        raise HpmgError(L.hpmg_last_error().decode())
+    opt = _Options(k, nu, 0.0, 0.0, inv_eps, cycle, smoother, smooth_steps, jacobi_damping, SCHEDULES[schedule])
+    keep = [_field(bc), _field(load)]
+    prob = _Problem(keep[0], None, keep[1], None, None, None, None, 0, None, 0, FIELD_FN(), None, None, None)
+    if load_per_element is not None:
+        a = np.ascontiguousarray(load_per_element, dtype=np.float64)
+        keep.append(a)
+        prob.load_per_element = _dp(a)
+    if structured_load is not None:
+        n, arr = structured_load
+        a = np.ascontiguousarray(arr, dtype=np.float64)
+        keep.append(a)
+        prob.structured_load = _dp(a)
+        prob.structured_n = int(n)
+    krylov = krylov or KrylovOptions()
+    o = _NSOpts(picard_tol, newton_rel_tol, newton_abs_tol, max_picard, max_newton, pseudo_time_inv,
+                _UOpts(outer_iterations, krylov.c(), None))
+    ne = md.n_elements * 4 ** (levels - 1)
+    # size of the compound space: 2 (k+1) per facet of the finest mesh (Euler: nf = nv + ne - 1)
+    nv = md.n_vertices
+    nf_base = nv + md.n_elements - 1
+    nf = nf_base
+    nv_l, ne_l = nv, md.n_elements
+    for _ in range(levels - 1):
+        nv_l, nf, ne_l = nv_l + nf, 2 * nf + 3 * ne_l, 4 * ne_l
+    vel = np.zeros(2 * (k + 1) * nf)
+    interior = np.zeros(max(ne * k * (k + 1), 1))
+    pres = np.zeros(ne)
+    rep = _NSReport()
+    rc = L.hpmg_ns_solve(C.byref(md), C.byref(opt), C.byref(prob), C.byref(o), _dp(vel), _dp(interior), _dp(pres),
+                         C.byref(rep))
+    if rc:
+        raise HpmgError(L.hpmg_last_error().decode())
+    r = NSReport(rep.picard_iterations, rep.newton_iterations, list(rep.picard_inner[: rep.n_picard_inner]),
+                 list(rep.newton_inner[: rep.n_newton_inner]), list(rep.picard_diffs[: rep.picard_iterations]),
+                 list(rep.newton_diffs[: rep.newton_iterations]), bool(rep.converged), bool(rep.not_applicable),
+                 rep.final_divergence, rep.seconds, rep.setup_seconds)
+    return NSSolution(vel, interior[: ne * k * (k + 1)].reshape(ne, k * (k + 1)), pres, r)

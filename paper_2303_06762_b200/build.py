@@ -18,7 +18,7 @@ LIB = os.path.join(LIB_DIR, "libhpmg.so")
 
 SOURCES = [os.path.join(CSRC, "kernels", "kernels.cu"), os.path.join(CSRC, "kernels", "small_levels.cu"),
            os.path.join(CSRC, "kernels", "sweep_rec.cu"),
-           os.path.join(CSRC, "context.cu")]
+           os.path.join(CSRC, "context.cu"), os.path.join(CSRC, "ns.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, d, f) for d in ("kernels", "host") for f in os.listdir(os.path.join(CSRC, d))] + [
     os.path.join(ROOT, "include", "hpmg", "capi.h")]
 
@@ -47,14 +47,17 @@ def build(force=False, verbose=False):
     if not force and up_to_date():
         return LIB
     os.makedirs(LIB_DIR, exist_ok=True)
-    objs = []
-    for src in SOURCES:
+    objs, procs = [], []
+    for src in SOURCES:  # translation units compile in parallel
         obj = os.path.join(LIB_DIR, os.path.basename(src) + ".o")
         cmd = [nvcc()] + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd))
-        subprocess.run(cmd, check=True)
+        procs.append((src, subprocess.Popen(cmd)))
         objs.append(obj)
+    for src, p in procs:
+        if p.wait() != 0:
+            raise RuntimeError(f"nvcc failed on {src}")
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB] + objs + ["-lcudart"]
     subprocess.run(cmd, check=True)
     for o in objs:

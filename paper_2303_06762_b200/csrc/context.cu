@@ -127,6 +127,8 @@ struct hpmg_ctx {
   double *pres = nullptr, *div = nullptr, *urhs = nullptr;
   // finest-system load and condensation parameters (recover_locals)
   double* fine_load = nullptr;
+  double* fine_wind = nullptr;  // finest-system local wind / mass field (recovery)
+  double* fine_mass = nullptr;
   int fine_lstride = 0;
   CondenseParams fine_prm{};
   bool enclosed = true;
@@ -228,7 +230,7 @@ void build_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, const Dev
   // condensation
   const int nc = R.T.nc, stride = nc * nc + nc;
   double* acr = dalloc<double>(size_t(m.ne()) * stride);
-  CondenseParams prm{C.opt.nu, C.opt.beta + C.opt.mass_coef, 0};
+  CondenseParams prm{C.opt.nu, C.opt.beta + C.opt.mass_coef, 0, (prob && prob->newton) ? 1 : 0, C.opt.mass_coef};
   double* dload = nullptr;
   int lstride = 0;
   if (finest && prob) {
@@ -280,7 +282,16 @@ void build_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, const Dev
   }
   double* dwind = nullptr;
   if (wind) dwind = dupload(host::local_wind(m, k, *wind), s);
-  dev::condense(R.T, V.geo, m.ne(), prm, dload, lstride, acr, s, dwind);
+  double* dmass = nullptr;  // pseudo-time mass field: a load, so on the finest system only
+  if (finest && prob && prob->mass_compound) {
+    host::HdgField mf;
+    mf.k = k;
+    mf.compound.assign(prob->mass_compound, prob->mass_compound + C.g_full.size());
+    const size_t ni = size_t(m.ne()) * k * (k + 1);
+    if (ni) mf.interior.assign(prob->mass_interior, prob->mass_interior + ni);
+    dmass = dupload(host::local_wind(m, k, mf), s);
+  }
+  dev::condense(R.T, V.geo, m.ne(), prm, dload, lstride, acr, s, dwind, dmass);
   // operator
   V.A.nb = V.nb;
   V.A.bs = V.bs;
@@ -294,7 +305,10 @@ void build_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, const Dev
     V.tslot = dupload(transpose_slots(V.plan), s);
     dev::transpose_bsr(V.A, V.tslot, V.AT, s);
   }
-  if (dwind) {
+  if (finest) {  // kept for recover_locals (same linearisation state)
+    C.fine_wind = dwind;
+    C.fine_mass = dmass;
+  } else if (dwind) {
     CK(cudaStreamSynchronize(s));
     cudaFree(dwind);
   }
@@ -748,7 +762,10 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
   if (md->levels < 1) throw std::invalid_argument("levels must be >= 1");
   C.opt = *opt;
   C.advected = prob && (prob->wind_compound || prob->wind);
-  if (prob && prob->newton) throw std::invalid_argument("Newton linearisations are not supported (Picard/Oseen only)");
+  if (prob && prob->newton && !(prob->wind_compound || prob->wind))
+    throw std::invalid_argument("a Newton linearisation needs the advection state (wind)");
+  if (prob && prob->mass_compound && (opt->k > 0 && !prob->mass_interior))
+    throw std::invalid_argument("mass field needs its interior coefficients at k > 0");
   CK(cudaStreamCreateWithFlags(&C.s, cudaStreamNonBlocking));
   // mesh hierarchy
   host::TriMesh base;
@@ -955,6 +972,7 @@ int guarded(hpmg_ctx* C, F&& f) {
 extern "C" {
 
 const char* hpmg_last_error(void) { return g_last_error.c_str(); }
+void hpmg_set_last_error(const char* msg) { g_last_error = msg ? msg : ""; }
 const char* hpmg_ctx_error(const hpmg_ctx* ctx) { return ctx ? ctx->err.c_str() : g_last_error.c_str(); }
 
 int hpmg_create(hpmg_ctx** out, const hpmg_mesh_desc* mesh, const hpmg_options* opt, const hpmg_problem* prob) {
@@ -985,7 +1003,8 @@ void hpmg_destroy(hpmg_ctx* ctx) {
                     (void*)V->Pm.ptr, (void*)V->Pm.col, (void*)V->Pm.val, (void*)V->PT.ptr, (void*)V->PT.col,
                     (void*)V->PT.val, (void*)V->x, (void*)V->b, (void*)V->r, (void*)V->y, (void*)V->bw, (void*)V->xw,
                     (void*)V->dbuf, (void*)V->geo, (void*)V->row_elems, (void*)V->elem_facets, (void*)V->facet_block,
-                    (void*)V->d_wave_ptr, (void*)V->rec.rec, (void*)V->srec.rec, (void*)V->flow_flags, (void*)V->flow_ctl, (void*)V->P.ndep, (void*)V->P.dep, (void*)V->d_passes})
+                    (void*)V->d_wave_ptr, (void*)V->rec.rec, (void*)V->srec.rec, (void*)V->flow_flags,
+                    (void*)V->flow_ctl, (void*)V->P.ndep, (void*)V->P.dep, (void*)V->d_passes})
       fr(p);
   };
   for (auto& V : ctx->lv) free_level(V.get());
@@ -996,7 +1015,8 @@ void hpmg_destroy(hpmg_ctx* ctx) {
   for (void* p : {(void*)ctx->coarse_inv, (void*)ctx->gemv_work, (void*)ctx->red.partial, (void*)ctx->red.counter,
                   (void*)ctx->sc, (void*)ctx->rhs, (void*)ctx->g_fac, (void*)ctx->facet_dir, (void*)ctx->kx,
                   (void*)ctx->kb, (void*)ctx->kr, (void*)ctx->kz, (void*)ctx->kp, (void*)ctx->kAp, (void*)ctx->ktmp,
-                  (void*)ctx->io_a, (void*)ctx->io_b, (void*)ctx->pres, (void*)ctx->div, (void*)ctx->urhs})
+                  (void*)ctx->io_a, (void*)ctx->io_b, (void*)ctx->pres, (void*)ctx->div, (void*)ctx->urhs,
+                  (void*)ctx->fine_load, (void*)ctx->fine_wind, (void*)ctx->fine_mass})
     fr(p);
   if (ctx->sc_host) cudaFreeHost(ctx->sc_host);
   if (ctx->s) cudaStreamDestroy(ctx->s);
@@ -1164,7 +1184,14 @@ int hpmg_uzawa(hpmg_ctx* ctx, const hpmg_uzawa_opts* o, double* velocity, double
     CK(cudaEventCreate(&e1));
     CK(cudaEventRecord(e0, C.s));
     dev::fill(C.pres, 0.0, ne, C.s);
-    dev::fill(C.kx, 0.0, T.n, C.s);
+    if (o->initial_velocity) {  // warm start: Constraints::to_free of the given full velocity
+      std::vector<double> u0(T.n);
+      for (size_t i = 0; i < C.free_to_full.size(); ++i) u0[i] = o->initial_velocity[C.free_to_full[i]];
+      in_vec(C, u0.data(), C.kx, 0);
+      CK(cudaStreamSynchronize(C.s));  // u0 is a host temporary
+    } else {
+      dev::fill(C.kx, 0.0, T.n, C.s);
+    }
     rep->converged = 1;
     for (int it = 0; it < o->outer_iterations && it < 64; ++it) {
       dev::uzawa_rhs(T.nb, T.bs, C.rhs, T.row_elems, T.geo, C.pres, C.kb, C.s);
@@ -1202,6 +1229,40 @@ int hpmg_uzawa(hpmg_ctx* ctx, const hpmg_uzawa_opts* o, double* velocity, double
   });
 }
 
+int hpmg_interpolate_hdg(hpmg_ctx* ctx, hpmg_field_fn field, void* user, double* compound_full, double* interior) {
+  return guarded(ctx, [&] {
+    if (!field) throw std::invalid_argument("interpolate_hdg needs a field");
+    hpmg_ctx& C = *ctx;
+    const int k = C.opt.k;
+    auto T = host::build_ref_tensors(k);
+    const host::HdgField u = host::interpolate_hdg(C.mesh.back(), k, *T, [&](double x, double y, double* o) {
+      field(x, y, o, user);
+    });
+    std::memcpy(compound_full, u.compound.data(), sizeof(double) * u.compound.size());
+    if (!u.interior.empty()) std::memcpy(interior, u.interior.data(), sizeof(double) * u.interior.size());
+  });
+}
+
+double hpmg_rt_l2_norm(hpmg_ctx* ctx, const double* compound_full, const double* interior) {
+  double out = -1.0;
+  const int rc = guarded(ctx, [&] {
+    hpmg_ctx& C = *ctx;
+    Level& T = C.top();
+    const DevRef& R = C.opt.k > 0 ? C.refk : C.ref0;
+    const size_t nfull = C.g_full.size(), ni = size_t(T.ne) * R.T.no;
+    double* comp = dalloc<double>(nfull);
+    double* di = dalloc<double>(std::max<size_t>(ni, 1));
+    CK(cudaMemcpyAsync(comp, compound_full, sizeof(double) * nfull, cudaMemcpyHostToDevice, C.s));
+    if (ni) CK(cudaMemcpyAsync(di, interior, sizeof(double) * ni, cudaMemcpyHostToDevice, C.s));
+    dev::rt_norm2(R.T, T.geo, T.ne, T.elem_facets, comp, di, C.red, C.sc + S_TMP, C.s);
+    read_scalars(C);
+    out = std::sqrt(C.sc_host[S_TMP]);
+    cudaFree(comp);
+    cudaFree(di);
+  });
+  return rc == 0 ? out : -1.0;
+}
+
 int hpmg_recover(hpmg_ctx* ctx, const double* velocity_full, double* interior, double* p_ortho, double* grad) {
   return guarded(ctx, [&] {
     hpmg_ctx& C = *ctx;
@@ -1215,7 +1276,7 @@ int hpmg_recover(hpmg_ctx* ctx, const double* velocity_full, double* interior, d
     double* dg = dalloc<double>(size_t(ne) * ng);
     CK(cudaMemcpyAsync(comp, velocity_full, sizeof(double) * nfull, cudaMemcpyHostToDevice, C.s));
     dev::recover(R.T, T.geo, ne, C.fine_prm, C.fine_load, C.fine_lstride, T.elem_facets, (long long)(nfull / 2), comp,
-                 di, dp, dg, C.s);
+                 di, dp, dg, C.s, C.fine_wind, C.fine_mass);
     if (no) CK(cudaMemcpyAsync(interior, di, sizeof(double) * ne * no, cudaMemcpyDeviceToHost, C.s));
     if (np) CK(cudaMemcpyAsync(p_ortho, dp, sizeof(double) * ne * np, cudaMemcpyDeviceToHost, C.s));
     CK(cudaMemcpyAsync(grad, dg, sizeof(double) * ne * ng, cudaMemcpyDeviceToHost, C.s));

@@ -13,6 +13,8 @@
 // against the CPU oracle without a GPU. The product only launches the kernel.
 #pragma once
 
+#include <cmath>
+
 #ifndef HPMG_HD
 #ifdef __CUDACC__
 #define HPMG_HD __host__ __device__
@@ -45,81 +47,146 @@ struct RefT {
   int nqe;
 };
 
+/// Wind tables of one element (scratch): physical wind at the volume nodes,
+/// and per edge node the normal wind w.n_out and (Newton) the upwind trace
+/// vector: the RT trace of the wind on outflow nodes, its tangential skeleton
+/// trace on inflow nodes (reference inc/assembly.hpp:300-321).
+struct WindTab {
+  const double* wq = nullptr;  // [nq][2]
+  const double* wn = nullptr;  // [3][nqe]
+  const double* up = nullptr;  // [3][nqe][2]
+  int newton = 0;
+};
+
+/// Physical Jacobian (row-major g0..g3) of RT local function r at volume node q.
+template <class Geo>
+HPMG_HD inline void rt_grad(const RefT& T, const Geo& g, const double* fr, int q, int r, double* gr) {
+  const int nrt = T.nrt;
+  const double* vj = T.vjac + size_t(q) * 4 * nrt;
+  const double h00 = vj[r], h01 = vj[nrt + r], h10 = vj[2 * nrt + r], h11 = vj[3 * nrt + r];
+  const double t00 = g.J[0] * h00 + g.J[1] * h10, t01 = g.J[0] * h01 + g.J[1] * h11;
+  const double t10 = g.J[2] * h00 + g.J[3] * h10, t11 = g.J[2] * h01 + g.J[3] * h11;
+  const double gs = fr[r] / g.detJ;
+  gr[0] = (t00 * g.Ji[0] + t01 * g.Ji[2]) * gs;
+  gr[1] = (t00 * g.Ji[1] + t01 * g.Ji[3]) * gs;
+  gr[2] = (t10 * g.Ji[0] + t11 * g.Ji[2]) * gs;
+  gr[3] = (t10 * g.Ji[1] + t11 * g.Ji[3]) * gs;
+}
+
+/// Test-function trace difference D on edge le at edge node q (RT column:
+/// T - (T.n)n; tangential column of this edge: -T; else zero). False if zero.
+template <class Geo>
+HPMG_HD inline bool test_trace(const RefT& T, const Geo& g, const double* fr, int le, int q, int a, double* ta) {
+  const int nfd = T.nfd, nc = T.nc, nrt = T.nrt;
+  const bool ra = a < 3 * nfd || a >= nc;
+  if (ra) {
+    const int r = a < 3 * nfd ? a : 3 * nfd + (a - nc);
+    const double* ev = T.evp + size_t(le * T.nqe + q) * 2 * nrt;
+    const double e0 = ev[r], e1 = ev[nrt + r], f = fr[r] / g.detJ;
+    const double T0 = (g.J[0] * e0 + g.J[1] * e1) * f, T1 = (g.J[2] * e0 + g.J[3] * e1) * f;
+    const double nx = g.n[2 * le], ny = g.n[2 * le + 1];
+    const double tn = T0 * nx + T1 * ny;
+    ta[0] = T0 - tn * nx;
+    ta[1] = T1 - tn * ny;
+    return true;
+  }
+  if ((a - 3 * nfd) / nfd != le) return false;
+  const int i = (a - 3 * nfd) % nfd;
+  double lg = T.eleg[q * nfd + i];
+  if (g.rho[le] < 0 && (i & 1)) lg = -lg;
+  ta[0] = -lg * g.tf[2 * le];
+  ta[1] = -lg * g.tf[2 * le + 1];
+  return true;
+}
+
 /// Convection entry A(a, b) of the upwinded transport form linearised about
 /// the wind (reference inc/assembly.hpp:254-275 volume, :294-321 facets;
-/// Picard only). `wq` = physical wind at the volume nodes [nq][2], `wn` =
-/// normal wind trace w.n_out at the edge nodes [3][nqe]. Evaluated pointwise:
-/// the upwind switch depends on the sign of w.n at every edge node.
+/// Picard, plus the Newton terms :265-273, :322-328 when W.newton). Evaluated
+/// pointwise: the upwind switch depends on the sign of w.n at every edge node.
 template <class Geo>
-HPMG_HD inline double convection_entry(const RefT& T, const Geo& g, const double* fr, const double* wq,
-                                       const double* wn, int a, int b) {
+HPMG_HD inline double convection_entry(const RefT& T, const Geo& g, const double* fr, const WindTab& W, int a,
+                                       int b) {
   const int nfd = T.nfd, nc = T.nc, nrt = T.nrt;
   const bool ra = a < 3 * nfd || a >= nc, rb = b < 3 * nfd || b >= nc;
   const int r = ra ? (a < 3 * nfd ? a : 3 * nfd + (a - nc)) : -1;
   const int s = rb ? (b < 3 * nfd ? b : 3 * nfd + (b - nc)) : -1;
   double acc = 0.0;
   const double J0 = g.J[0], J1 = g.J[1], J2 = g.J[2], J3 = g.J[3];
-  // volume: -(u (x) w, grad v), test r, trial s
+  // volume: -(u (x) w, grad v) [Picard] - (w (x) u, grad v) [Newton], test r, trial s
   if (ra && rb) {
     for (int q = 0; q < T.nq; ++q) {
-      const double* vj = T.vjac + size_t(q) * 4 * nrt;
       const double* vv = T.vval + size_t(q) * 2 * nrt;
-      // physical Jacobian of test r: (J Jh Ji) / detJ * fr
-      const double h00 = vj[r], h01 = vj[nrt + r], h10 = vj[2 * nrt + r], h11 = vj[3 * nrt + r];
-      const double t00 = J0 * h00 + J1 * h10, t01 = J0 * h01 + J1 * h11;
-      const double t10 = J2 * h00 + J3 * h10, t11 = J2 * h01 + J3 * h11;
-      const double gs = fr[r] / g.detJ;
-      const double g0 = (t00 * g.Ji[0] + t01 * g.Ji[2]) * gs, g1 = (t00 * g.Ji[1] + t01 * g.Ji[3]) * gs;
-      const double g2 = (t10 * g.Ji[0] + t11 * g.Ji[2]) * gs, g3 = (t10 * g.Ji[1] + t11 * g.Ji[3]) * gs;
+      double gr[4];
+      rt_grad(T, g, fr, q, r, gr);
       const double vs = fr[s] / g.detJ;
       const double v0 = (J0 * vv[s] + J1 * vv[nrt + s]) * vs, v1 = (J2 * vv[s] + J3 * vv[nrt + s]) * vs;
-      const double wx = wq[2 * q], wy = wq[2 * q + 1];
+      const double wx = W.wq[2 * q], wy = W.wq[2 * q + 1];
       const double w = T.qw[q] * g.detJ;
-      acc -= w * (v0 * (g0 * wx + g1 * wy) + v1 * (g2 * wx + g3 * wy));
+      acc -= w * (v0 * (gr[0] * wx + gr[1] * wy) + v1 * (gr[2] * wx + gr[3] * wy));
+      if (W.newton) acc -= w * (wx * (gr[0] * v0 + gr[1] * v1) + wy * (gr[2] * v0 + gr[3] * v1));
     }
   }
   // facets: upwinded transport of the trace, tested with the tangential difference
   for (int le = 0; le < 3; ++le) {
     const double nx = g.n[2 * le], ny = g.n[2 * le + 1];
-    // test column a on this edge: RT column -> D = T - (T.n)n ; tangential (le) -> D = -T
     const bool at = !ra && (a - 3 * nfd) / nfd == le;
     if (!ra && !at) continue;
     const bool bt = !rb && (b - 3 * nfd) / nfd == le;
-    if (!rb && !bt) continue;
+    const bool newton_col = W.newton && b < 3 * nfd;  // Newton couples the flux trial columns
+    if (!rb && !bt && !newton_col) continue;
     for (int q = 0; q < T.nqe; ++q) {
-      const double wnq = wn[le * T.nqe + q];
-      if (wnq == 0.0) continue;
-      const bool outflow = wnq > 0;
-      if (outflow != rb) continue;  // outflow couples RT trial columns, inflow tangential ones
-      double ta0, ta1, tb0, tb1;
+      const double wnq = W.wn[le * T.nqe + q];
+      double ta[2];
+      test_trace(T, g, fr, le, q, a, ta);
       const double* ev = T.evp + size_t(le * T.nqe + q) * 2 * nrt;
-      if (ra) {
-        const double e0 = ev[r], e1 = ev[nrt + r], f = fr[r] / g.detJ;
-        const double T0 = (J0 * e0 + J1 * e1) * f, T1 = (J2 * e0 + J3 * e1) * f;
-        const double tn = T0 * nx + T1 * ny;
-        ta0 = T0 - tn * nx;
-        ta1 = T1 - tn * ny;
-      } else {
-        const int i = (a - 3 * nfd) % nfd;
-        double lg = T.eleg[q * nfd + i];
-        if (g.rho[le] < 0 && (i & 1)) lg = -lg;
-        ta0 = -lg * g.tf[2 * le];
-        ta1 = -lg * g.tf[2 * le + 1];
-      }
+      double tb0 = 0.0, tb1 = 0.0;
       if (rb) {
         const double e0 = ev[s], e1 = ev[nrt + s], f = fr[s] / g.detJ;
         tb0 = (J0 * e0 + J1 * e1) * f;
         tb1 = (J2 * e0 + J3 * e1) * f;
-      } else {
+      } else if (bt) {
         const int i = (b - 3 * nfd) % nfd;
         double lg = T.eleg[q * nfd + i];
         if (g.rho[le] < 0 && (i & 1)) lg = -lg;
         tb0 = lg * g.tf[2 * le];
         tb1 = lg * g.tf[2 * le + 1];
       }
-      acc += T.ew[q] * g.ds[le] * wnq * (ta0 * tb0 + ta1 * tb1);
+      const double wds = T.ew[q] * g.ds[le];
+      // Picard: outflow couples RT trial columns, inflow tangential ones
+      if (wnq != 0.0 && (rb || bt) && (wnq > 0) == rb) acc += wds * wnq * (ta[0] * tb0 + ta[1] * tb1);
+      if (newton_col) {
+        const double tup = ta[0] * W.up[2 * (le * T.nqe + q)] + ta[1] * W.up[2 * (le * T.nqe + q) + 1];
+        if (tup != 0.0) acc += wds * tup * (tb0 * nx + tb1 * ny);
+      }
     }
   }
+  return acc;
+}
+
+/// Newton load of test column a: -(w (x) w, grad v) + <w.n (w_up . D(v))>
+/// (reference inc/assembly.hpp:273, :327).
+template <class Geo>
+HPMG_HD inline double newton_rhs(const RefT& T, const Geo& g, const double* fr, const WindTab& W, int a) {
+  const int nfd = T.nfd, nc = T.nc;
+  const bool ra = a < 3 * nfd || a >= nc;
+  double acc = 0.0;
+  if (ra) {
+    const int r = a < 3 * nfd ? a : 3 * nfd + (a - nc);
+    for (int q = 0; q < T.nq; ++q) {
+      double gr[4];
+      rt_grad(T, g, fr, q, r, gr);
+      const double wx = W.wq[2 * q], wy = W.wq[2 * q + 1];
+      acc -= T.qw[q] * g.detJ * (wx * (gr[0] * wx + gr[1] * wy) + wy * (gr[2] * wx + gr[3] * wy));
+    }
+  }
+  for (int le = 0; le < 3; ++le)
+    for (int q = 0; q < T.nqe; ++q) {
+      double ta[2];
+      if (!test_trace(T, g, fr, le, q, a, ta)) break;
+      const int e = le * T.nqe + q;
+      const double tup = ta[0] * W.up[2 * e] + ta[1] * W.up[2 * e + 1];
+      acc += T.ew[q] * g.ds[le] * W.wn[e] * tup;
+    }
   return acc;
 }
 
@@ -138,12 +205,15 @@ struct ElemGeo {
 struct CondenseParams {
   double nu, mass;        // mass = beta + mass_coef
   int load_mode;          // 0 none, 1 constant per element, 2 pointwise [nq][2]
+  int newton;             // Newton linearisation about the wind (needs the wind)
+  double mass_coef;       // pseudo-time coefficient multiplying the mass field load
 };
 
 /// Scratch layout (doubles): C[4ns*nv] A[nv*nv] P[(ns-1)*nv] rhs[nv] aug[nz*(nz+nc+1)] fac[nrt]
-HPMG_HD inline int condense_scratch(int ns, int nv, int nc, int nz, int nrt) {
-  // + wind tables: 2 nq (volume) + 3 nqe (edges) <= 256 for k <= 3
-  return 4 * ns * nv + nv * nv + (ns > 1 ? (ns - 1) * nv : 0) + nv + nz * (nz + nc + 1) + nrt + 8 + 256;
+/// + the tables wq[2nq] wn[3nqe] up[6nqe] mq[2nq].
+HPMG_HD inline int condense_scratch(int ns, int nv, int nc, int nz, int nrt, int nq, int nqe) {
+  return 4 * ns * nv + nv * nv + (ns > 1 ? (ns - 1) * nv : 0) + nv + nz * (nz + nc + 1) + nrt + 8 + 4 * nq +
+         9 * nqe + 8;
 }
 
 #ifndef SYNC
@@ -160,7 +230,7 @@ HPMG_HD inline int condense_scratch(int ns, int nv, int nc, int nz, int nrt) {
 HPMG_D inline void condense_element(int tid, int nthr, const RefT& T, const ElemGeo& g, const CondenseParams& prm,
                                      const double* load, double* scratch, double* Ac, double* rc,
                                      const double* xc = nullptr, double* zout = nullptr, double* gout = nullptr,
-                                     const double* xw = nullptr) {
+                                     const double* xw = nullptr, const double* xm = nullptr) {
   const int ns = T.ns, nv = T.nv, nc = T.nc, nrt = T.nrt, nfd = T.nfd, no = T.no;
   const int np = ns - 1, nz = no + np, nC = 4 * ns;
   double* C = scratch;
@@ -171,7 +241,14 @@ HPMG_D inline void condense_element(int tid, int nthr, const RefT& T, const Elem
   double* fr = aug + nz * (nz + nc + 1);  // orientation factor per RT column
   double* wq = fr + nrt + 8;               // [nq][2] physical wind at the volume nodes
   double* wn = wq + 2 * T.nq;              // [3][nqe] w.n_out at the edge nodes
+  double* up = wn + 3 * T.nqe;             // [3][nqe][2] upwind wind trace (Newton)
+  double* mq = up + 6 * T.nqe;             // [nq][2] physical mass field (pseudo-time load)
   const int naug = nz + nc + 1;
+  WindTab W;
+  W.wq = wq;
+  W.wn = wn;
+  W.up = up;
+  W.newton = xw ? prm.newton : 0;
 
   for (int r = tid; r < nrt; r += nthr) {
     if (r < 3 * nfd) {
@@ -199,15 +276,55 @@ HPMG_D inline void condense_element(int tid, int nthr, const RefT& T, const Elem
     for (int e = tid; e < 3 * T.nqe; e += nthr) {
       const int le = e / T.nqe, q = e % T.nqe;
       const double* ev = T.evp + size_t(le * T.nqe + q) * 2 * nrt;
-      double sx = 0.0, sy = 0.0;
+      double sx = 0.0, sy = 0.0, sabs = 0.0;
       for (int r = 0; r < nrt; ++r) {
         const double c = xw[r < 3 * nfd ? r : nc + (r - 3 * nfd)] * fr[r] / g.detJ;
-        sx += c * (g.J[0] * ev[r] + g.J[1] * ev[nrt + r]);
-        sy += c * (g.J[2] * ev[r] + g.J[3] * ev[nrt + r]);
+        const double tx = g.J[0] * ev[r] + g.J[1] * ev[nrt + r], ty = g.J[2] * ev[r] + g.J[3] * ev[nrt + r];
+        sx += c * tx;
+        sy += c * ty;
+        sabs += fabs(c) * sqrt(tx * tx + ty * ty);
       }
-      wn[e] = sx * g.n[2 * le] + sy * g.n[2 * le + 1];
+      // w.n_out, and the tangential skeleton trace of the wind on this edge
+      double lt = 0.0;
+      for (int i = 0; i < nfd; ++i) {
+        double lg = T.eleg[q * nfd + i];
+        if (g.rho[le] < 0 && (i & 1)) lg = -lg;
+        lt += xw[3 * nfd + le * nfd + i] * lg;
+      }
+      // A wind tangential to the edge (no-slip walls, the lid, a solenoidal
+      // field along the boundary, a node where it vanishes) has w.n = 0 in
+      // exact arithmetic but a round-off sign from the basis tables; the
+      // reference's upwind switch (w.n > 0, assembly.hpp:316) would pick the
+      // Newton upwind trace by that sign. |w.n| below 1e-13 of the magnitude
+      // of the terms it is summed from (plus the tangential trace) counts as
+      // the exact zero (inflow branch), in the oracle as well.
+      double wne = sx * g.n[2 * le] + sy * g.n[2 * le + 1];
+      if (fabs(wne) <= 1e-13 * (sabs + fabs(lt))) wne = 0.0;
+      wn[e] = wne;
+      if (wne > 0) {
+        up[2 * e] = sx;
+        up[2 * e + 1] = sy;
+      } else {  // inflow: the tangential skeleton trace
+        up[2 * e] = lt * g.tf[2 * le];
+        up[2 * e + 1] = lt * g.tf[2 * le + 1];
+      }
     }
   }
+  if (xm) {
+    // pseudo-time mass field, physical values at the volume nodes
+    for (int q = tid; q < T.nq; q += nthr) {
+      double sx = 0.0, sy = 0.0;
+      for (int r = 0; r < nrt; ++r) {
+        const double c = xm[r < 3 * nfd ? r : nc + (r - 3 * nfd)] * fr[r] / g.detJ;
+        const double v0 = T.vval[(q * 2) * nrt + r], v1 = T.vval[(q * 2 + 1) * nrt + r];
+        sx += c * (g.J[0] * v0 + g.J[1] * v1);
+        sy += c * (g.J[2] * v0 + g.J[3] * v1);
+      }
+      mq[2 * q] = sx;
+      mq[2 * q + 1] = sy;
+    }
+  }
+  SYNC();
   // ---- gradient coupling C (4ns x nv) and divergence moments P ----
   for (int e = tid; e < nC * nv; e += nthr) {
     const int row = e / nv, a = e % nv;
@@ -264,6 +381,18 @@ HPMG_D inline void condense_element(int tid, int nthr, const RefT& T, const Elem
         s *= fr[r];
       }
     }
+    if (xm && (a < 3 * nfd || a >= nc)) {
+      // + mass_coef (m_prev, v): backward-Euler pseudo-time load (reference assembly.hpp:273-276)
+      const int r = a < 3 * nfd ? a : 3 * nfd + (a - nc);
+      double sm = 0.0;
+      for (int q = 0; q < T.nq; ++q) {
+        const double fx = mq[2 * q], fy = mq[2 * q + 1];
+        const double jf0 = fx * g.J[0] + fy * g.J[2], jf1 = fx * g.J[1] + fy * g.J[3];
+        sm += T.qw[q] * (jf0 * T.vval[(q * 2) * nrt + r] + jf1 * T.vval[(q * 2 + 1) * nrt + r]);
+      }
+      s += prm.mass_coef * fr[r] * sm;
+    }
+    if (W.newton) s += newton_rhs(T, g, fr, W, a);
     rhs[a] = s;
   }
   SYNC();
@@ -283,7 +412,7 @@ HPMG_D inline void condense_element(int tid, int nthr, const RefT& T, const Elem
     }
     double cc = 0.0;
     for (int row = 0; row < nC; ++row) cc += C[row * nv + a] * C[row * nv + b];
-    A[e] = m + visc * cc + (xw ? convection_entry(T, g, fr, wq, wn, a, b) : 0.0);
+    A[e] = m + visc * cc + (xw ? convection_entry(T, g, fr, W, a, b) : 0.0);
   }
   SYNC();
   if (nz == 0) {

@@ -89,7 +89,8 @@ inline int grid_for(int64_t n, int threads) {
 
 // ---------------------------------------------------------------- condense
 __global__ void k_condense(RefT T, const ElemGeo* __restrict__ geo, CondenseParams prm, const double* __restrict__ load,
-                           int load_stride, double* __restrict__ out, int stride, const double* __restrict__ wind) {
+                           int load_stride, double* __restrict__ out, int stride, const double* __restrict__ wind,
+                           const double* __restrict__ mfield) {
   extern __shared__ double smem[];
   __shared__ ElemGeo g;
   const int e = blockIdx.x;
@@ -98,8 +99,10 @@ __global__ void k_condense(RefT T, const ElemGeo* __restrict__ geo, CondensePara
   __syncthreads();
   double* o = out + size_t(e) * stride;
   const double* ld = prm.load_mode ? load + size_t(e) * load_stride : nullptr;
-  const double* xw = wind ? wind + size_t(e) * T.nv : nullptr;  // local wind coefficients (Oseen)
-  condense_element(threadIdx.x, blockDim.x, T, g, prm, ld, smem, o, o + T.nc * T.nc, nullptr, nullptr, nullptr, xw);
+  const double* xw = wind ? wind + size_t(e) * T.nv : nullptr;      // local wind coefficients (Oseen)
+  const double* xm = mfield ? mfield + size_t(e) * T.nv : nullptr;  // local mass field (pseudo-time)
+  condense_element(threadIdx.x, blockDim.x, T, g, prm, ld, smem, o, o + T.nc * T.nc, nullptr, nullptr, nullptr, xw,
+                   xm);
 }
 
 /// recover_locals (reference inc/assembly.hpp:513-549) for every element:
@@ -108,7 +111,8 @@ __global__ void k_condense(RefT T, const ElemGeo* __restrict__ geo, CondensePara
 __global__ void k_recover(RefT T, const ElemGeo* __restrict__ geo, CondenseParams prm, const double* __restrict__ load,
                           int load_stride, const int* __restrict__ elem_facets, long long nflux,
                           const double* __restrict__ compound, double* __restrict__ interior,
-                          double* __restrict__ pres, double* __restrict__ grad) {
+                          double* __restrict__ pres, double* __restrict__ grad, const double* __restrict__ wind,
+                          const double* __restrict__ mfield) {
   extern __shared__ double smem[];
   __shared__ ElemGeo g;
   const int e = blockIdx.x;
@@ -127,7 +131,9 @@ __global__ void k_recover(RefT T, const ElemGeo* __restrict__ geo, CondenseParam
   }
   __syncthreads();
   const double* ld = prm.load_mode ? load + size_t(e) * load_stride : nullptr;
-  condense_element(threadIdx.x, blockDim.x, T, g, prm, ld, scratch, nullptr, nullptr, xc, zb, gb);
+  const double* xw = wind ? wind + size_t(e) * T.nv : nullptr;
+  const double* xm = mfield ? mfield + size_t(e) * T.nv : nullptr;
+  condense_element(threadIdx.x, blockDim.x, T, g, prm, ld, scratch, nullptr, nullptr, xc, zb, gb, xw, xm);
   __syncthreads();
   for (int j = threadIdx.x; j < T.no; j += blockDim.x) interior[size_t(e) * T.no + j] = zb[j];
   for (int m = threadIdx.x; m < T.ns - 1; m += blockDim.x) pres[size_t(e) * (T.ns - 1) + m] = zb[T.no + m];
@@ -710,6 +716,42 @@ __global__ void k_dot(const double* __restrict__ a, const double* __restrict__ b
     s = fma(a[t], b[t], s);
   finalize<false>(s, red, out);
 }
+/// Squared L2 norm of an RT velocity field (reference inc/assembly.hpp:487-501):
+/// one thread per element, local coefficients from the compound flux part and
+/// the interior part, sum over the volume nodes of w detJ |J v_hat c / detJ|^2.
+__global__ void k_rt_norm2(RefT T, const ElemGeo* __restrict__ geo, int ne, const int* __restrict__ elem_facets,
+                           const double* __restrict__ compound, const double* __restrict__ interior, Reduce red,
+                           double* out) {
+  double acc = 0.0;
+  const int nfd = T.nfd, nrt = T.nrt;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x) {
+    const ElemGeo& g = geo[e];
+    double c[kMaxRt];
+    for (int r = 0; r < nrt; ++r) {
+      if (r < 3 * nfd) {
+        const int le = r / nfd, i = r % nfd;
+        const double f = ((i & 1) && g.rho[le] < 0) ? -g.fac[le] : g.fac[le];
+        c[r] = f * compound[size_t(elem_facets[e * 3 + le]) * nfd + i];
+      } else {
+        c[r] = interior[size_t(e) * T.no + (r - 3 * nfd)];
+      }
+    }
+    double s = 0.0;
+    for (int q = 0; q < T.nq; ++q) {
+      const double* vv = T.vval + size_t(q) * 2 * nrt;
+      double h0 = 0.0, h1 = 0.0;
+      for (int r = 0; r < nrt; ++r) {
+        h0 = fma(vv[r], c[r], h0);
+        h1 = fma(vv[nrt + r], c[r], h1);
+      }
+      const double v0 = (g.J[0] * h0 + g.J[1] * h1) / g.detJ, v1 = (g.J[2] * h0 + g.J[3] * h1) / g.detJ;
+      s = fma(T.qw[q] * g.detJ, v0 * v0 + v1 * v1, s);
+    }
+    acc += s;
+  }
+  finalize<false>(acc, red, out);
+}
+
 __global__ void k_pcg_update(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
                              const double* __restrict__ Ap, int64_t n, double* sc, int i_num, int i_den, Reduce red,
                              int i_rr) {
@@ -838,32 +880,33 @@ void by_bs(int bs, F&& f) {
 
 // ============================================================ launchers
 void condense(const RefT& T, const ElemGeo* geo, int ne, CondenseParams prm, const double* load, int load_stride,
-              double* out, cudaStream_t s, const double* wind) {
+              double* out, cudaStream_t s, const double* wind, const double* mass_field) {
   if (ne == 0) return;
   const int nz = T.no + T.ns - 1;
-  const size_t smem = sizeof(double) * condense_scratch(T.ns, T.nv, T.nc, nz, T.nrt);
+  const size_t smem = sizeof(double) * condense_scratch(T.ns, T.nv, T.nc, nz, T.nrt, T.nq, T.nqe);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_condense, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  k_condense<<<ne, 128, smem, s>>>(T, geo, prm, load, load_stride, out, T.nc * T.nc + T.nc, wind);
+  k_condense<<<ne, 128, smem, s>>>(T, geo, prm, load, load_stride, out, T.nc * T.nc + T.nc, wind, mass_field);
   HPMG_LAUNCH_CHECK();
 }
 
 void recover(const RefT& T, const ElemGeo* geo, int ne, CondenseParams prm, const double* load, int load_stride,
              const int* elem_facets, long long nflux, const double* compound, double* interior, double* pres,
-             double* grad, cudaStream_t s) {
+             double* grad, cudaStream_t s, const double* wind, const double* mass_field) {
   if (ne == 0) return;
   const int nz = T.no + T.ns - 1;
   const size_t smem =
-      sizeof(double) * (condense_scratch(T.ns, T.nv, T.nc, nz, T.nrt) + T.nc + nz + 1 + 4 * T.ns);
+      sizeof(double) * (condense_scratch(T.ns, T.nv, T.nc, nz, T.nrt, T.nq, T.nqe) + T.nc + nz + 1 + 4 * T.ns);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_recover, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  k_recover<<<ne, 128, smem, s>>>(T, geo, prm, load, load_stride, elem_facets, nflux, compound, interior, pres, grad);
+  k_recover<<<ne, 128, smem, s>>>(T, geo, prm, load, load_stride, elem_facets, nflux, compound, interior, pres, grad,
+                                  wind, mass_field);
   HPMG_LAUNCH_CHECK();
 }
 
@@ -1030,6 +1073,12 @@ void axpy(double* y, double a, const double* x, int64_t n, cudaStream_t s) {
 }
 void sub(double* y, const double* a, const double* b, int64_t n, cudaStream_t s) {
   k_sub<<<grid_for(n, 256), 256, 0, s>>>(y, a, b, n);
+  HPMG_LAUNCH_CHECK();
+}
+void rt_norm2(const RefT& T, const ElemGeo* geo, int ne, const int* elem_facets, const double* compound,
+              const double* interior, const Reduce& red, double* out, cudaStream_t s) {
+  if (T.nrt > kMaxRt) throw std::runtime_error("RT space too large for rt_norm2");
+  k_rt_norm2<<<kRedBlocks, 256, 0, s>>>(T, geo, ne, elem_facets, compound, interior, red, out);
   HPMG_LAUNCH_CHECK();
 }
 void dot(const double* a, const double* b, int64_t n, const Reduce& red, double* out, cudaStream_t s) {

@@ -51,13 +51,15 @@ struct Reduce {
   unsigned* counter = nullptr;    // zero-initialised ticket
 };
 
-/// wind: per-element local wind coefficients [ne][nv] (Oseen) or nullptr (Stokes)
+/// wind: per-element local wind coefficients [ne][nv] (Oseen / Newton) or
+/// nullptr (Stokes); mass_field: same layout, pseudo-time load (prm.mass_coef)
 void condense(const RefT& T, const ElemGeo* geo, int ne, CondenseParams prm, const double* load, int load_stride,
-              double* out, cudaStream_t s, const double* wind = nullptr);
-/// recover_locals on every element from the full compound skeleton vector.
+              double* out, cudaStream_t s, const double* wind = nullptr, const double* mass_field = nullptr);
+/// recover_locals on every element from the full compound skeleton vector
+/// (same linearisation state as the condensation).
 void recover(const RefT& T, const ElemGeo* geo, int ne, CondenseParams prm, const double* load, int load_stride,
              const int* elem_facets, long long nflux, const double* compound, double* interior, double* pres,
-             double* grad, cudaStream_t s);
+             double* grad, cudaStream_t s, const double* wind = nullptr, const double* mass_field = nullptr);
 void assemble_bsr(const Bsr& A, int nfd, const double* acr, int acr_stride, int nc, const int* gath,
                   const ElemGeo* geo, double inv_eps, cudaStream_t s);
 void transpose_bsr(const Bsr& A, const int* tslot, Bsr& AT, cudaStream_t s);
@@ -139,6 +141,11 @@ void copy(double* y, const double* x, int64_t n, cudaStream_t s);
 void axpy(double* y, double a, const double* x, int64_t n, cudaStream_t s);
 void sub(double* y, const double* a, const double* b, int64_t n, cudaStream_t s);  // y = a - b
 void dot(const double* a, const double* b, int64_t n, const Reduce& red, double* out, cudaStream_t s);
+/// *out = ||u||^2_{L2} of the RT field with compound (flux part, reference
+/// layout) and interior [ne][no] coefficients (reference assembly.hpp:487-501)
+constexpr int kMaxRt = 24;  // 3(k+1) + k(k+1) at k = 3
+void rt_norm2(const RefT& T, const ElemGeo* geo, int ne, const int* elem_facets, const double* compound,
+              const double* interior, const Reduce& red, double* out, cudaStream_t s);
 /// PCG update: alpha = sc[i_num]/sc[i_den]; x += alpha p; r -= alpha Ap; sc[i_rr] = |r|^2
 void pcg_update(double* x, double* r, const double* p, const double* Ap, int64_t n, double* sc, int i_num, int i_den,
                 const Reduce& red, int i_rr, cudaStream_t s);

@@ -29,8 +29,23 @@ class Problem(C.Structure):
         ("nu", C.c_double), ("beta", C.c_double), ("mass_coef", C.c_double), ("inv_eps", C.c_double),
         ("bc_kind", C.c_int), ("load_kind", C.c_int), ("load", C.POINTER(C.c_double)),
         ("wind_kind", C.c_int), ("cycle", C.c_int), ("smoother", C.c_int), ("smooth_steps", C.c_int),
-        ("jacobi_damping", C.c_double),
+        ("jacobi_damping", C.c_double), ("newton", C.c_int), ("mass_field", C.c_int),
     ]
+
+
+class NSOpts(C.Structure):
+    _fields_ = [("picard_tol", C.c_double), ("newton_rel_tol", C.c_double), ("newton_abs_tol", C.c_double),
+                ("max_picard", C.c_int), ("max_newton", C.c_int), ("pseudo_time_inv", C.c_double),
+                ("outer_iterations", C.c_int), ("rel_tol", C.c_double), ("abs_tol", C.c_double),
+                ("max_iterations", C.c_int)]
+
+
+class NSReport(C.Structure):
+    _fields_ = [("picard_iterations", C.c_int), ("newton_iterations", C.c_int), ("n_picard_inner", C.c_int),
+                ("n_newton_inner", C.c_int), ("picard_inner", C.c_int * 512), ("newton_inner", C.c_int * 256),
+                ("picard_diffs", C.c_double * 128), ("newton_diffs", C.c_double * 64),
+                ("converged", C.c_int), ("not_applicable", C.c_int), ("final_divergence", C.c_double),
+                ("seconds", C.c_double)]
 
 
 class Stats(C.Structure):
@@ -66,7 +81,10 @@ def lib():
         L.orc_seeded_load.argtypes = [C.c_int, C.c_uint, C.c_double, C.c_double, dp]
         L.orc_mg_krylov.argtypes = [P, C.c_int, dp, dp, C.c_double, C.c_double, C.c_int, C.POINTER(Stats)]
         L.orc_mg_uzawa.argtypes = [P, C.c_int, C.c_double, C.c_double, C.c_int, dp, dp,
-                                   C.POINTER(C.c_int), dp, C.POINTER(C.c_int), dp]
+                                   C.POINTER(C.c_int), dp, C.POINTER(C.c_int), dp, dp]
+        L.orc_mg_rt_l2_norm.restype = C.c_double
+        L.orc_mg_rt_l2_norm.argtypes = [P, dp, dp]
+        L.orc_ns_solve.argtypes = [C.POINTER(Problem), C.POINTER(NSOpts), dp, dp, dp, C.POINTER(NSReport)]
         L.orc_mg_smooth.argtypes = [P, C.c_int, C.c_int, dp, dp, C.c_int, C.c_double]
         L.orc_check_cr_equivalence.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                                C.c_double, C.c_int, dp]
@@ -120,12 +138,13 @@ class OracleMG:
 
     def __init__(self, *, mesh_kind=0, base_n=2, levels=2, k=0, nu=1.0, beta=0.0, mass_coef=0.0,
                  inv_eps=1e6, bc=BC_NONE, load_kind=LOAD_NONE, load=None, wind=WIND_NONE,
-                 cycle=CYCLE_W, smoother=SM_MULT, smooth_steps=1, jacobi_damping=1.0 / 3.0):
+                 cycle=CYCLE_W, smoother=SM_MULT, smooth_steps=1, jacobi_damping=1.0 / 3.0, newton=False,
+                 mass_field=False):
         L = lib()
         self._load = None if load is None else np.ascontiguousarray(load, dtype=np.float64)
         p = Problem(mesh_kind, base_n, levels, k, nu, beta, mass_coef, inv_eps, bc, load_kind,
                     _dp(self._load) if self._load is not None else None, wind, cycle, smoother,
-                    smooth_steps, jacobi_damping)
+                    smooth_steps, jacobi_damping, int(newton), int(mass_field))
         self.h = L.orc_mg_create(C.byref(p))
         if not self.h:
             raise RuntimeError(L.orc_last_error().decode())
@@ -216,7 +235,8 @@ class OracleMG:
         return x, dict(iterations=st.iterations, converged=bool(st.converged),
                        not_applicable=bool(st.not_applicable), residual=st.residual)
 
-    def uzawa(self, outer=2, rel_tol=1e-8, abs_tol=1e-10, max_it=500):
+    def uzawa(self, outer=2, rel_tol=1e-8, abs_tol=1e-10, max_it=500, initial_velocity=None):
+        init = None if initial_velocity is None else np.ascontiguousarray(initial_velocity, dtype=np.float64)
         vel = np.empty(self.n_full)
         p = np.empty(self.ne)
         inner = (C.c_int * outer)()
@@ -224,7 +244,7 @@ class OracleMG:
         flags = (C.c_int * 2)()
         secs = np.zeros(1)
         done = lib().orc_mg_uzawa(self.h, outer, rel_tol, abs_tol, max_it, _dp(vel), _dp(p), inner,
-                                  _dp(hist), flags, _dp(secs))
+                                  _dp(hist), flags, _dp(secs), None if init is None else _dp(init))
         return dict(velocity=vel, pressure=p, inner_iterations=list(inner)[:done],
                     divergence_history=list(hist[:done]), converged=bool(flags[0]),
                     not_applicable=bool(flags[1]), seconds=float(secs[0]))
@@ -241,6 +261,49 @@ class OracleMG:
 
     def time_apply(self, reps):
         return lib().orc_mg_time_apply(self.h, reps)
+
+    def wind(self):
+        """The interpolated advection state (compound full, interior [ne][k(k+1)])."""
+        c = np.empty(self.n_full)
+        i = np.zeros(max(self.ne * self.k * (self.k + 1), 1))
+        lib().orc_mg_wind(self.h, _dp(c), _dp(i))
+        return c, i[: self.ne * self.k * (self.k + 1)]
+
+    def rt_l2_norm(self, compound_full, interior):
+        c = np.ascontiguousarray(compound_full, dtype=np.float64)
+        i = np.ascontiguousarray(interior, dtype=np.float64).ravel()
+        if i.size == 0:
+            i = np.zeros(1)
+        return lib().orc_mg_rt_l2_norm(self.h, _dp(c), _dp(i))
+
+
+def ns_solve(*, mesh_kind=0, base_n=2, levels=2, k=0, nu=1.0, inv_eps=1e3, bc=BC_LID_UNIT, load_kind=LOAD_NONE,
+             load=None, cycle=CYCLE_V, smoother=SM_MULT, smooth_steps=1, picard_tol=1e-4, newton_rel_tol=1e-8,
+             newton_abs_tol=1e-10, max_picard=60, max_newton=25, pseudo_time_inv=0.0, outer=2, rel_tol=1e-8,
+             abs_tol=1e-10, max_it=500):
+    """Oracle navier_stokes_solve (reference inc/ns.hpp:69-149)."""
+    L = lib()
+    ld = None if load is None else np.ascontiguousarray(load, dtype=np.float64)
+    p = Problem(mesh_kind, base_n, levels, k, nu, 0.0, 0.0, inv_eps, bc, load_kind,
+                _dp(ld) if ld is not None else None, WIND_NONE, cycle, smoother, smooth_steps, 1.0 / 3.0, 0, 0)
+    o = NSOpts(picard_tol, newton_rel_tol, newton_abs_tol, max_picard, max_newton, pseudo_time_inv, outer, rel_tol,
+               abs_tol, max_it)
+    # sizes from a throwaway problem of the same mesh and order
+    probe = OracleMG(mesh_kind=mesh_kind, base_n=base_n, levels=levels, k=k, nu=nu, inv_eps=inv_eps, bc=bc)
+    vel = np.zeros(probe.n_full)
+    interior = np.zeros(max(probe.ne * k * (k + 1), 1))
+    pres = np.zeros(probe.ne)
+    rep = NSReport()
+    if L.orc_ns_solve(C.byref(p), C.byref(o), _dp(vel), _dp(interior), _dp(pres), C.byref(rep)):
+        raise RuntimeError(L.orc_last_error().decode())
+    return dict(velocity=vel, interior=interior[: probe.ne * k * (k + 1)], pressure=pres,
+                picard_iterations=rep.picard_iterations, newton_iterations=rep.newton_iterations,
+                picard_inner=list(rep.picard_inner[: rep.n_picard_inner]),
+                newton_inner=list(rep.newton_inner[: rep.n_newton_inner]),
+                picard_diffs=list(rep.picard_diffs[: rep.picard_iterations]),
+                newton_diffs=list(rep.newton_diffs[: rep.newton_iterations]),
+                converged=bool(rep.converged), not_applicable=bool(rep.not_applicable),
+                final_divergence=rep.final_divergence, seconds=rep.seconds)
 
 
 def check(name, *args, n_out):

@@ -184,3 +184,41 @@ def test_cavity_counts_vs_paper(k):
             r = B.uzawa()
             assert r["converged"]
             assert max(r["inner_iterations"]) <= 1.5 * CAVITY[k][f][li]
+
+
+# ---------------------------------------------------------------- Navier-Stokes
+# (reference tests/test_ns.cpp; the manufactured NS load is replaced by a named
+# smooth load: the pinned properties hold for any load)
+
+def _field_gap(a, b, k, base_n, levels):
+    probe = O.OracleMG(base_n=base_n, levels=levels, k=k, bc=O.BC_ZERO)
+    return probe.rt_l2_norm(a["velocity"] - b["velocity"], a["interior"] - b["interior"])
+
+
+def test_ns_newton_updates_shrink_quadratically():
+    # test_ns.cpp:58-73: driven cavity, early hand-over to Newton, variable V
+    r = O.ns_solve(base_n=2, levels=3, k=0, nu=1e-2, inv_eps=1e4, bc=O.BC_LID_TOP, cycle=O.CYCLE_VARV,
+                   picard_tol=1e-1)
+    assert r["converged"]
+    d = r["newton_diffs"]
+    assert len(d) >= 3
+    assert d[1] < 5.0 * d[0] ** 2 and d[2] < 5.0 * d[1] ** 2
+    assert d[1] < 0.1 * d[0] and d[2] < 0.1 * d[1]
+
+
+def test_ns_tight_picard_lands_on_newton_fixed_point():
+    # test_ns.cpp:75-96
+    kw = dict(base_n=2, levels=2, k=0, nu=0.1, inv_eps=1e5, bc=O.BC_ZERO, load_kind=O.LOAD_SMOOTH_UZAWA)
+    picard = O.ns_solve(picard_tol=1e-11, max_picard=200, max_newton=0, **kw)
+    newton = O.ns_solve(**kw)
+    assert picard["converged"] and picard["newton_iterations"] == 0 and newton["converged"]
+    assert _field_gap(picard, newton, 0, 2, 2) < 1e-9
+
+
+def test_ns_pseudo_time_shares_the_fixed_point():
+    # test_ns.cpp:98-115
+    kw = dict(base_n=2, levels=2, k=0, nu=0.05, inv_eps=5e4, bc=O.BC_ZERO, load_kind=O.LOAD_SMOOTH_UZAWA)
+    marched = O.ns_solve(pseudo_time_inv=0.5, **kw)
+    plain = O.ns_solve(**kw)
+    assert marched["converged"] and plain["converged"]
+    assert _field_gap(marched, plain, 0, 2, 2) < 1e-9
