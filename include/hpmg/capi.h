@@ -137,6 +137,12 @@ typedef struct {
 /* ---- lifecycle ---- */
 int hpmg_create(hpmg_ctx** out, const hpmg_mesh_desc* mesh, const hpmg_options* opt, const hpmg_problem* prob);
 void hpmg_destroy(hpmg_ctx* ctx);
+/* Re-linearise in place (the reference rebuilds MGPreconditioner per
+ * Picard/Newton step, ns.hpp:84): new wind / Newton flag / mass field / load /
+ * boundary data and nu, beta, mass_coef, inv_eps; the mesh hierarchy, plans,
+ * patch structure, wave schedules and allocations are kept. Order, cycle,
+ * smoother, schedule and the symmetric/advected class must not change. */
+int hpmg_update(hpmg_ctx* ctx, const hpmg_options* opt, const hpmg_problem* prob);
 const char* hpmg_last_error(void);
 void hpmg_set_last_error(const char* msg); /* for drivers layered on this ABI (hpmg_ns_solve) */
 const char* hpmg_ctx_error(const hpmg_ctx* ctx);

@@ -125,6 +125,7 @@ def lib():
     L.hpmg_uzawa.argtypes = [vp, C.POINTER(_UOpts), dp, dp, C.POINTER(_UReport)]
     L.hpmg_recover.argtypes = [vp, vp, vp, vp, vp]
     L.hpmg_interpolate_hdg.argtypes = [vp, FIELD_FN, vp, dp, dp]
+    L.hpmg_update.argtypes = [vp, C.POINTER(_Options), C.POINTER(_Problem)]
     L.hpmg_rt_l2_norm.restype = C.c_double
     L.hpmg_rt_l2_norm.argtypes = [vp, dp, dp]
     L.hpmg_ns_solve.argtypes = [C.POINTER(_Mesh), C.POINTER(_Options), C.POINTER(_Problem), C.POINTER(_NSOpts),
@@ -241,10 +242,26 @@ class MGPreconditioner:
             raise HpmgError(L.hpmg_last_error().decode())
         if schedule not in SCHEDULES:
             raise ValueError(f"schedule must be one of {sorted(SCHEDULES)}")
-        opt = _Options(k, nu, beta, mass_coef, inv_eps, cycle, smoother, smooth_steps, jacobi_damping,
-                       SCHEDULES[schedule])
+        self._optargs = dict(k=k, nu=nu, beta=beta, mass_coef=mass_coef, inv_eps=inv_eps, cycle=cycle,
+                             smoother=smoother, smooth_steps=smooth_steps, jacobi_damping=jacobi_damping,
+                             schedule=SCHEDULES[schedule])
+        opt = _Options(**self._optargs)
         self._bc = _field(bc)
         self._load = _field(load)
+        self._static = dict(load_per_element=load_per_element, structured_load=structured_load)
+        prob = self._problem(wind, newton, mass_field)
+        h = C.c_void_p()
+        rc = L.hpmg_create(C.byref(h), C.byref(md), C.byref(opt), C.byref(prob))
+        if rc:
+            raise HpmgError(L.hpmg_last_error().decode())
+        self.h = h
+        self.k = k
+        self.n = L.hpmg_n(h)
+        self.n_full = L.hpmg_n_full(h)
+        self.ne = L.hpmg_ne(h)
+
+    def _problem(self, wind, newton, mass_field):
+        """_Problem for the stored bc / load and the given linearisation state."""
         self._keep = []
         # Oseen / Newton advection state: a wind field (callable or NAMED_FIELDS
         # name) interpolated by the library, or an HDG velocity (compound, interior)
@@ -262,25 +279,30 @@ class MGPreconditioner:
             self._keep += [mc, mi]
             prob.mass_compound = _dp(mc)
             prob.mass_interior = _dp(mi) if mi.size else None
-        if load_per_element is not None:
-            a = np.ascontiguousarray(load_per_element, dtype=np.float64)
+        if self._static["load_per_element"] is not None:
+            a = np.ascontiguousarray(self._static["load_per_element"], dtype=np.float64)
             self._keep.append(a)
             prob.load_per_element = _dp(a)
-        if structured_load is not None:
-            n, arr = structured_load
+        if self._static["structured_load"] is not None:
+            n, arr = self._static["structured_load"]
             a = np.ascontiguousarray(arr, dtype=np.float64)
             self._keep.append(a)
             prob.structured_load = _dp(a)
             prob.structured_n = int(n)
-        h = C.c_void_p()
-        rc = L.hpmg_create(C.byref(h), C.byref(md), C.byref(opt), C.byref(prob))
-        if rc:
-            raise HpmgError(L.hpmg_last_error().decode())
-        self.h = h
-        self.k = k
-        self.n = L.hpmg_n(h)
-        self.n_full = L.hpmg_n_full(h)
-        self.ne = L.hpmg_ne(h)
+        return prob
+
+    def update(self, *, wind=None, newton=False, mass_field=None, **opt_changes):
+        """Re-linearise in place (hpmg_update): new wind / Newton flag / mass
+        field and nu, beta, mass_coef, inv_eps, jacobi_damping; the hierarchy,
+        plans and wave schedules are kept."""
+        bad = set(opt_changes) - {"nu", "beta", "mass_coef", "inv_eps", "jacobi_damping"}
+        if bad:
+            raise ValueError(f"update cannot change {sorted(bad)}")
+        self._optargs.update(opt_changes)
+        opt = _Options(**self._optargs)
+        prob = self._problem(wind, newton, mass_field)
+        self._check(lib().hpmg_update(self.h, C.byref(opt), C.byref(prob)))
+        return self
 
     def close(self):
         if getattr(self, "h", None):

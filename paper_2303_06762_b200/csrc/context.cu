@@ -82,6 +82,7 @@ struct Level {
   int2* d_passes = nullptr;
   int npass = 0;
   dev::BlockCsr Pm, PT;  // from level l-1 to l (lowest-order levels l >= 1)
+  dev::TransferDev tdev;  // structure of Pm for its device construction
   double *x = nullptr, *b = nullptr, *r = nullptr, *y = nullptr, *bw = nullptr, *xw = nullptr, *dbuf = nullptr;
   int steps = 1;
   ElemGeo* geo = nullptr;
@@ -91,6 +92,9 @@ struct Level {
   int* row_elems = nullptr;
   int* elem_facets = nullptr;
   int* facet_block = nullptr;
+  int* block_facet = nullptr;
+  int* gath = nullptr;  // assembly gather lists (kept for re-linearisation)
+  bool finest = false;
   double bytes_sweep = 0, bytes_spmv = 0, p_nnz = 0;
   double bytes_stream = 0;  // one sweep as this implementation moves it: records + b/x rows + x_e gathers
 };
@@ -126,6 +130,9 @@ struct hpmg_ctx {
   // uzawa
   double *pres = nullptr, *div = nullptr, *urhs = nullptr;
   // finest-system load and condensation parameters (recover_locals)
+  double lin_parts[4] = {0, 0, 0, 0};  // last linearisation: patch inverses, transfers, coarse, condensation [s]
+  double* acr = nullptr;               // condensed element blocks (scratch of the linearisation)
+  size_t acr_cap = 0;
   double* fine_load = nullptr;
   double* fine_wind = nullptr;  // finest-system local wind / mass field (recovery)
   double* fine_mass = nullptr;
@@ -213,12 +220,13 @@ void alloc_level_vectors(Level& V) {
 
 std::vector<int> transpose_slots(const host::LevelPlan& P);
 
-/// Assembles (condense + gather) one level operator on the device.
-void build_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, const DevRef& R, bool finest,
-                 const hpmg_problem* prob, double* rhs_out, const host::HdgField* wind = nullptr) {
+/// Structure of one level: plan (patterns, patches, waves), geometry and every
+/// device allocation whose size does not depend on the linearisation state.
+void plan_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, bool finest) {
   cudaStream_t s = C.s;
   V.k = k;
   V.bs = 2 * (k + 1);
+  V.finest = finest;
   V.plan = host::make_level(m, k);
   host::set_inverse_layout(V.plan, !C.advected);  // packed symmetric inverses for Stokes
   V.nb = V.plan.nb;
@@ -227,9 +235,65 @@ void build_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, const Dev
   std::vector<ElemGeo> geo(m.ne());
   for (int e = 0; e < m.ne(); ++e) geo[e] = host::element_geometry(m, e);
   V.geo = dupload(geo, s);
-  // condensation
+  V.A.nb = V.nb;
+  V.A.bs = V.bs;
+  V.A.val = dalloc<double>(size_t(V.nb) * host::kSlots * V.bs * V.bs);
+  V.A.cols = dupload(V.plan.cols, s);
+  V.gath = dupload(V.plan.gath, s);
+  if (C.advected) {  // A^T rows for the exact transpose (backward) sweeps, multigrid.hpp:84,106
+    V.AT = V.A;
+    V.AT.val = dalloc<double>(size_t(V.nb) * host::kSlots * V.bs * V.bs);
+    V.tslot = dupload(transpose_slots(V.plan), s);
+  }
+  if (finest) {
+    std::vector<int> ef(size_t(m.ne()) * 3);
+    for (int e = 0; e < m.ne(); ++e)
+      for (int q = 0; q < 3; ++q) ef[size_t(e) * 3 + q] = m.ef[e][q];
+    V.elem_facets = dupload(ef, s);
+    V.row_elems = dupload(V.plan.row_elems, s);
+    V.facet_block = dupload(V.plan.facet_block, s);
+    V.block_facet = dupload(V.plan.block_facet, s);
+  }
+  // patches + explicit inverses
+  V.P.n = V.plan.npatch;
+  V.max_nf = V.plan.max_patch_f;
+  V.P.nf = dupload(V.plan.patch_nf, s);
+  V.P.fac = dupload(V.plan.patch_fac, s);
+  V.P.off = dupload(V.plan.inv_off, s);
+  V.P.inv = dalloc<double>(size_t(V.plan.inv_total));
+  V.P.packed = V.plan.packed ? 1 : 0;
+  V.P.wave = dupload(V.plan.wave_patch, s);
+  V.P.fpatch = dupload(V.plan.facet_patches, s);
+  V.wave_ptr = V.plan.wave_ptr;
+  V.d_wave_ptr = dupload(V.wave_ptr, s);
+  alloc_level_vectors(V);
+  V.dbuf = dalloc<double>(size_t(std::max(V.P.n, 1)) * V.max_nf * V.bs);
+  // algorithmic bytes (SURVEY.md 8(d)), ELL slots counted as stored
+  double nnz = 0;
+  for (int c : V.plan.cols) nnz += c >= 0 ? double(V.bs) * V.bs : 0.0;
+  const double nblk = nnz / (double(V.bs) * V.bs);
+  V.bytes_spmv = 8 * nnz + 4 * nblk + 4 * (V.nb + 1.0) + 16.0 * V.n;
+  // reference storage accounting: full np^2 patch factors (packing halves the physical bytes)
+  V.bytes_sweep = 8.0 * double(V.plan.inv_full_total) + 2 * (8 * nnz + 4 * nblk) + 32.0 * V.n;
+}
+
+/// Linearisation-dependent part of one level: condensation about the wind
+/// (Oseen / Newton, pseudo-time mass field), assembly into the level's
+/// operator arrays in place, A^T, and the finest system's rhs.
+void linearise_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, const DevRef& R, const hpmg_problem* prob,
+                     double* rhs_out, const host::HdgField* wind = nullptr) {
+  cudaStream_t s = C.s;
+  const int k = V.k;
+  const bool finest = V.finest;
   const int nc = R.T.nc, stride = nc * nc + nc;
-  double* acr = dalloc<double>(size_t(m.ne()) * stride);
+  // condensed element blocks: one persistent scratch sized for the largest level
+  const size_t need = size_t(m.ne()) * stride;
+  if (C.acr_cap < need) {
+    if (C.acr) cudaFree(C.acr);
+    C.acr = dalloc<double>(need);
+    C.acr_cap = need;
+  }
+  double* acr = C.acr;
   CondenseParams prm{C.opt.nu, C.opt.beta + C.opt.mass_coef, 0, (prob && prob->newton) ? 1 : 0, C.opt.mass_coef};
   double* dload = nullptr;
   int lstride = 0;
@@ -266,7 +330,7 @@ void build_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, const Dev
       std::vector<double> l(size_t(m.ne()) * nq * 2);
       double out[2];
       for (int e = 0; e < m.ne(); ++e) {
-        const ElemGeo& g = geo[e];
+        const ElemGeo g = host::element_geometry(m, e);
         const double x0 = m.vx[m.ev[e][0]], y0 = m.vy[m.ev[e][0]];
         for (int q = 0; q < nq; ++q) {
           const double x = x0 + g.J[0] * qx[q] + g.J[1] * qy[q], y = y0 + g.J[2] * qx[q] + g.J[3] * qy[q];
@@ -292,70 +356,24 @@ void build_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, const Dev
     dmass = dupload(host::local_wind(m, k, mf), s);
   }
   dev::condense(R.T, V.geo, m.ne(), prm, dload, lstride, acr, s, dwind, dmass);
-  // operator
-  V.A.nb = V.nb;
-  V.A.bs = V.bs;
-  V.A.val = dalloc<double>(size_t(V.nb) * host::kSlots * V.bs * V.bs);
-  V.A.cols = dupload(V.plan.cols, s);
-  int* gath = dupload(V.plan.gath, s);
-  dev::assemble_bsr(V.A, k + 1, acr, stride, nc, gath, V.geo, C.opt.inv_eps, s);
-  if (C.advected) {  // A^T rows for the exact transpose (backward) sweeps, multigrid.hpp:84,106
-    V.AT = V.A;
-    V.AT.val = dalloc<double>(size_t(V.nb) * host::kSlots * V.bs * V.bs);
-    V.tslot = dupload(transpose_slots(V.plan), s);
-    dev::transpose_bsr(V.A, V.tslot, V.AT, s);
-  }
+  dev::assemble_bsr(V.A, k + 1, acr, stride, nc, V.gath, V.geo, C.opt.inv_eps, s);
+  if (C.advected) dev::transpose_bsr(V.A, V.tslot, V.AT, s);
+  if (finest)
+    dev::assemble_rhs(V.nb, V.bs, k + 1, V.row_elems, V.block_facet, V.elem_facets, C.facet_dir, C.g_fac, acr,
+                      stride, nc, V.geo, C.opt.inv_eps, rhs_out, s);
+  CK(cudaStreamSynchronize(s));
   if (finest) {  // kept for recover_locals (same linearisation state)
+    for (void* p : {(void*)C.fine_load, (void*)C.fine_wind, (void*)C.fine_mass})
+      if (p) cudaFree(p);
     C.fine_wind = dwind;
     C.fine_mass = dmass;
-  } else if (dwind) {
-    CK(cudaStreamSynchronize(s));
-    cudaFree(dwind);
-  }
-  if (finest) {
-    std::vector<int> ef(size_t(m.ne()) * 3);
-    for (int e = 0; e < m.ne(); ++e)
-      for (int q = 0; q < 3; ++q) ef[size_t(e) * 3 + q] = m.ef[e][q];
-    V.elem_facets = dupload(ef, s);
-    V.row_elems = dupload(V.plan.row_elems, s);
-    V.facet_block = dupload(V.plan.facet_block, s);
-    int* bf = dupload(V.plan.block_facet, s);
-    dev::assemble_rhs(V.nb, V.bs, k + 1, V.row_elems, bf, V.elem_facets, C.facet_dir, C.g_fac, acr, stride, nc,
-                      V.geo, C.opt.inv_eps, rhs_out, s);
-    CK(cudaStreamSynchronize(s));
-    cudaFree(bf);
-  }
-  CK(cudaStreamSynchronize(s));
-  cudaFree(acr);
-  cudaFree(gath);
-  if (finest) {  // kept for recover_locals
     C.fine_load = dload;
     C.fine_lstride = lstride;
     C.fine_prm = prm;
-  } else if (dload) {
-    cudaFree(dload);
+  } else {
+    if (dwind) cudaFree(dwind);
+    if (dload) cudaFree(dload);
   }
-  // patches + explicit inverses
-  V.P.n = V.plan.npatch;
-  V.max_nf = V.plan.max_patch_f;
-  V.P.nf = dupload(V.plan.patch_nf, s);
-  V.P.fac = dupload(V.plan.patch_fac, s);
-  V.P.off = dupload(V.plan.inv_off, s);
-  V.P.inv = dalloc<double>(size_t(V.plan.inv_total));
-  V.P.packed = V.plan.packed ? 1 : 0;
-  V.P.wave = dupload(V.plan.wave_patch, s);
-  V.P.fpatch = dupload(V.plan.facet_patches, s);
-  V.wave_ptr = V.plan.wave_ptr;
-  V.d_wave_ptr = dupload(V.wave_ptr, s);
-  alloc_level_vectors(V);
-  V.dbuf = dalloc<double>(size_t(std::max(V.P.n, 1)) * V.max_nf * V.bs);
-  // algorithmic bytes (SURVEY.md 8(d)), ELL slots counted as stored
-  double nnz = 0;
-  for (int c : V.plan.cols) nnz += c >= 0 ? double(V.bs) * V.bs : 0.0;
-  const double nblk = nnz / (double(V.bs) * V.bs);
-  V.bytes_spmv = 8 * nnz + 4 * nblk + 4 * (V.nb + 1.0) + 16.0 * V.n;
-  // reference storage accounting: full np^2 patch factors (packing halves the physical bytes)
-  V.bytes_sweep = 8.0 * double(V.plan.inv_full_total) + 2 * (8 * nnz + 4 * nblk) + 32.0 * V.n;
 }
 
 void build_patch_inverses(hpmg_ctx& C, Level& V) {
@@ -377,6 +395,11 @@ void build_patch_inverses(hpmg_ctx& C, Level& V) {
         if (ne > dev::kExt) throw std::runtime_error("patch facet with more than 2 external couplings");
         vec_bytes += 8.0 * V.bs * (2 + ne);  // b row read, x row written, x_e blocks gathered
       }
+    if (V.rec.rec) {  // re-linearisation: same layout, rebuild the record contents in place
+      dev::build_records(V.A, V.P, V.rec, C.s);
+      if (V.small) dev::build_records(V.A, V.P, V.srec, C.s);
+      return;
+    }
     V.P.max_dep = V.plan.max_dep;
     V.P.ndep = dupload(V.plan.patch_ndep, C.s);
     V.P.dep = dupload(V.plan.patch_dep, C.s);
@@ -752,6 +775,8 @@ hpmg_solve_stats gmres_device(hpmg_ctx& C, const hpmg_krylov_opts& o) {
   return st;
 }
 
+void linearise(hpmg_ctx& C, const hpmg_problem* prob, const host::RefTensors* Tk);
+
 void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const hpmg_problem* prob) {
   using clk = std::chrono::steady_clock;
   auto t0 = clk::now();
@@ -833,13 +858,60 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
       if (!dir[f])
         for (int i = 0; i < nfd; ++i) C.free_to_full.push_back(nflux + int64_t(f) * nfd + i);
   }
-  // advection state (Oseen): order-k wind on the finest mesh, its lowest-order
-  // carrier and the restriction chain (reference multigrid.hpp:58-66)
+  auto t1 = clk::now();
+  // structure of every level
+  C.lv.resize(C.L + 1);
+  for (int l = 0; l <= C.L; ++l) {
+    C.lv[l] = std::make_unique<Level>();
+    Level& V = *C.lv[l];
+    const bool finest = (k == 0 && l == C.L);
+    plan_level(C, V, C.mesh[l], 0, finest);
+    V.steps = opt->cycle == HPMG_CYCLE_VARIABLE_V ? (opt->smooth_steps << (C.L - l)) : opt->smooth_steps;
+  }
+  if (k > 0) {
+    C.head = std::make_unique<Level>();
+    plan_level(C, *C.head, fine, k, true);
+    C.head->steps = opt->smooth_steps;
+  }
+  C.rhs = dalloc<double>(int64_t(C.free_to_full.size()));
+  // everything that depends on the linearisation state
+  linearise(C, prob, k > 0 ? tTk.get() : tT0.get());
+  auto t2 = clk::now();
+  C.setup_parts[2] = C.lin_parts[0];
+  C.setup_parts[3] = C.lin_parts[1];
+  C.setup_parts[4] = C.lin_parts[2];
+  auto t5 = clk::now();
+  // solver workspace
+  Level& T = C.top();
+  for (double** p : {&C.kx, &C.kb, &C.kr, &C.kz, &C.kp, &C.kAp, &C.ktmp, &C.io_a, &C.io_b}) *p = dalloc<double>(T.n);
+  C.pres = dalloc<double>(fine.ne());
+  C.div = dalloc<double>(fine.ne());
+  C.urhs = dalloc<double>(T.n);
+  build_apply_graph(C);
+  CK(cudaStreamSynchronize(C.s));
+  auto t6 = clk::now();
+  auto sec = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
+  C.setup_parts[0] = sec(t0, t1);                      // mesh + tables
+  C.setup_parts[1] = sec(t1, t2) - C.lin_parts[0] - C.lin_parts[1] - C.lin_parts[2];  // plans + condensation
+  C.setup_parts[5] = sec(t5, t6);                      // workspace + graph
+  C.setup_parts[6] = sec(t0, t6);
+}
+
+/// Everything that depends on the linearisation state (the reference rebuilds
+/// the whole MGPreconditioner per Picard / Newton step, ns.hpp:84): the wind
+/// chain (multigrid.hpp:58-66), condensation and assembly of every level, the
+/// patch inverses, the corrected prolongations and the coarse inverse.
+void linearise(hpmg_ctx& C, const hpmg_problem* prob, const host::RefTensors* Tk) {
+  using clk = std::chrono::steady_clock;
+  auto sec = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
+  const auto t0 = clk::now();
+  const int k = C.opt.k;
+  const host::TriMesh& fine = C.mesh[C.L];
   std::vector<host::HdgField> adv;
   host::HdgField wind_k;
   if (C.advected) {
     if (prob->wind) {
-      wind_k = host::interpolate_hdg(fine, k, k > 0 ? *tTk : *tT0, [&](double x, double y, double* o) {
+      wind_k = host::interpolate_hdg(fine, k, *Tk, [&](double x, double y, double* o) {
         prob->wind(x, y, o, prob->wind_user);
       });
     } else {
@@ -852,46 +924,27 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
     adv[C.L] = k > 0 ? host::lowest_order(fine, wind_k) : wind_k;
     for (int l = C.L; l > 0; --l) adv[l - 1] = host::restrict_wind(C.mesh[l - 1], C.mesh[l], C.ref[l - 1], adv[l]);
   }
-  auto t1 = clk::now();
-  // lowest-order levels
-  C.lv.resize(C.L + 1);
-  for (int l = 0; l <= C.L; ++l) {
-    C.lv[l] = std::make_unique<Level>();
-    Level& V = *C.lv[l];
-    const bool finest = (k == 0 && l == C.L);
-    if (finest) {
-      const int64_t nfree = int64_t(C.free_to_full.size());
-      C.rhs = dalloc<double>(nfree);
-    }
-    build_level(C, V, C.mesh[l], 0, C.ref0, finest, prob, finest ? C.rhs : nullptr,
-                C.advected ? &adv[l] : nullptr);
-    V.steps = opt->cycle == HPMG_CYCLE_VARIABLE_V ? (opt->smooth_steps << (C.L - l)) : opt->smooth_steps;
-  }
-  if (k > 0) {
-    C.head = std::make_unique<Level>();
-    C.rhs = dalloc<double>(int64_t(C.free_to_full.size()));
-    build_level(C, *C.head, fine, k, C.refk, true, prob, C.rhs, C.advected ? &wind_k : nullptr);
-    C.head->steps = opt->smooth_steps;
-  }
+  for (int l = 0; l <= C.L; ++l)
+    linearise_level(C, *C.lv[l], C.mesh[l], C.ref0, prob, C.lv[l]->finest ? C.rhs : nullptr,
+                    C.advected ? &adv[l] : nullptr);
+  if (k > 0) linearise_level(C, *C.head, fine, C.refk, prob, C.rhs, C.advected ? &wind_k : nullptr);
   CK(cudaStreamSynchronize(C.s));
-  auto t2 = clk::now();
+  const auto t1 = clk::now();
   for (int l = 1; l <= C.L; ++l) build_patch_inverses(C, *C.lv[l]);
   if (k > 0) build_patch_inverses(C, *C.head);
   CK(cudaStreamSynchronize(C.s));
-  auto t3 = clk::now();
-  // transfers (host correction from the downloaded fine operators)
-  {
-    // levels are independent: one host thread per level
-    std::vector<std::vector<double>> Af(C.L + 1);
-    for (int l = 1; l <= C.L; ++l) Af[l] = download_bsr(C, *C.lv[l]);
-    std::vector<host::BlockCsrH> Ps(C.L + 1), PTs(C.L + 1);
+  const auto t2 = clk::now();
+  // transfers: structure once on host threads (one per level), the harmonic
+  // correction from the current fine operators on the device
+  static_assert(host::TransferPlan::kColMax == dev::kTransferColMax, "transfer column capacity");
+  if (C.L >= 1 && !C.lv[1]->tdev.base) {
+    std::vector<host::TransferPlan> tp(C.L + 1);
     std::vector<std::thread> pool;
     std::vector<std::string> errs(C.L + 1);
     for (int l = 1; l <= C.L; ++l)
       pool.emplace_back([&, l] {
         try {
-          Ps[l] = host::corrected_prolongation(C.lv[l - 1]->plan, C.lv[l]->plan, C.ref[l - 1], Af[l]);
-          PTs[l] = host::transpose_blocks(Ps[l]);
+          tp[l] = host::transfer_plan(C.lv[l - 1]->plan, C.lv[l]->plan, C.ref[l - 1]);
         } catch (const std::exception& e) {
           errs[l] = e.what();
         }
@@ -899,53 +952,56 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
     for (auto& t : pool) t.join();
     for (int l = 1; l <= C.L; ++l) {
       if (!errs[l].empty()) throw std::runtime_error(errs[l]);
-      double nz = 0;
-      for (double v : Ps[l].val) nz += v != 0.0;
-      C.lv[l]->p_nnz = nz;
-      C.lv[l]->Pm = upload_blockcsr(Ps[l], C.s);
-      C.lv[l]->PT = upload_blockcsr(PTs[l], C.s);
+      Level& V = *C.lv[l];
+      const host::TransferPlan& T = tp[l];
+      V.Pm = upload_blockcsr(T.P, C.s);
+      V.PT = upload_blockcsr(T.PT, C.s);
+      V.Pm.nnz = V.PT.nnz = int(T.P.col.size());
+      dev::TransferDev& D = V.tdev;
+      D.nelem = T.nelem;
+      D.nnz = int(T.P.col.size());
+      D.nmed = dupload(T.nmed, C.s);
+      D.med = dupload(T.med, C.s);
+      D.ncol = dupload(T.ncol, C.s);
+      D.col = dupload(T.col, C.s);
+      D.pos = dupload(T.pos, C.s);
+      D.avg_ptr = dupload(T.avg.ptr, C.s);
+      D.avg_col = dupload(T.avg.col, C.s);
+      D.avg_val = dupload(T.avg.val, C.s);
+      D.base = dupload(T.P.val, C.s);
+      D.tperm = dupload(T.tperm, C.s);
+      V.p_nnz = 4.0 * double(T.P.col.size());
     }
     CK(cudaStreamSynchronize(C.s));
   }
-  auto t4 = clk::now();
-  // coarse dense inverse
+  for (int l = 1; l <= C.L; ++l) dev::corrected_prolongation(C.lv[l]->A, C.lv[l]->tdev, C.lv[l]->Pm, C.lv[l]->PT, C.s);
+  CK(cudaStreamSynchronize(C.s));
+  const auto t3 = clk::now();
+  // coarse dense inverse: Gauss-Jordan with partial pivoting on the device (kernels.cu dense_invert)
   {
     Level& V0 = *C.lv[0];
     C.n0 = int(V0.n);
     std::vector<double> A0 = download_bsr(C, V0), D(size_t(C.n0) * C.n0, 0.0);
     for (int r = 0; r < V0.nb; ++r)
-      for (int s = 0; s < host::kSlots; ++s) {
-        const int c = V0.plan.cols[size_t(r) * host::kSlots + s];
+      for (int sl = 0; sl < host::kSlots; ++sl) {
+        const int c = V0.plan.cols[size_t(r) * host::kSlots + sl];
         if (c < 0) continue;
         for (int i = 0; i < 2; ++i)
-          for (int j = 0; j < 2; ++j) D[size_t(2 * r + i) * C.n0 + 2 * c + j] = A0[((size_t(r) * host::kSlots + s) * 2 + i) * 2 + j];
+          for (int j = 0; j < 2; ++j)
+            D[size_t(2 * r + i) * C.n0 + 2 * c + j] = A0[((size_t(r) * host::kSlots + sl) * 2 + i) * 2 + j];
       }
-    // Gauss-Jordan with partial pivoting on the device (kernels.cu dense_invert)
     double* dA = dupload(D, C.s);
-    C.coarse_inv = dalloc<double>(size_t(C.n0) * C.n0);
+    if (!C.coarse_inv) C.coarse_inv = dalloc<double>(size_t(C.n0) * C.n0);
     dev::dense_invert(C.n0, dA, C.coarse_inv, C.s);
     CK(cudaStreamSynchronize(C.s));
     cudaFree(dA);
-    C.gemv_work = dalloc<double>(size_t(C.n0) * ((C.n0 + 63) / 64 + 1));  // kGemvChunk = 64
+    if (!C.gemv_work) C.gemv_work = dalloc<double>(size_t(C.n0) * ((C.n0 + 63) / 64 + 1));  // kGemvChunk = 64
   }
-  auto t5 = clk::now();
-  // solver workspace
-  Level& T = C.top();
-  for (double** p : {&C.kx, &C.kb, &C.kr, &C.kz, &C.kp, &C.kAp, &C.ktmp, &C.io_a, &C.io_b}) *p = dalloc<double>(T.n);
-  C.pres = dalloc<double>(fine.ne());
-  C.div = dalloc<double>(fine.ne());
-  C.urhs = dalloc<double>(T.n);
-  build_apply_graph(C);
-  CK(cudaStreamSynchronize(C.s));
-  auto t6 = clk::now();
-  auto sec = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
-  C.setup_parts[0] = sec(t0, t1);  // mesh + tables
-  C.setup_parts[1] = sec(t1, t2);  // condensation + assembly
-  C.setup_parts[2] = sec(t2, t3);  // patch inverses
-  C.setup_parts[3] = sec(t3, t4);  // transfers
-  C.setup_parts[4] = sec(t4, t5);  // coarse inverse
-  C.setup_parts[5] = sec(t5, t6);  // workspace + graph
-  C.setup_parts[6] = sec(t0, t6);
+  const auto t4 = clk::now();
+  C.lin_parts[0] = sec(t1, t2);
+  C.lin_parts[1] = sec(t2, t3);
+  C.lin_parts[2] = sec(t3, t4);
+  C.lin_parts[3] = sec(t0, t1);
 }
 
 template <typename F>
@@ -991,6 +1047,54 @@ int hpmg_create(hpmg_ctx** out, const hpmg_mesh_desc* mesh, const hpmg_options* 
   return HPMG_OK;
 }
 
+int hpmg_update(hpmg_ctx* ctx, const hpmg_options* opt, const hpmg_problem* prob) {
+  return guarded(ctx, [&] {
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
+    hpmg_ctx& C = *ctx;
+    const bool advected = prob && (prob->wind_compound || prob->wind);
+    if (opt->k != C.opt.k || opt->cycle != C.opt.cycle || opt->smoother != C.opt.smoother ||
+        opt->smooth_steps != C.opt.smooth_steps || opt->schedule != C.opt.schedule || advected != C.advected)
+      throw std::invalid_argument("hpmg_update changes only the linearisation state (wind, Newton, mass terms, nu, "
+                                  "beta, inv_eps); order, cycle, smoother and symmetry need a new context");
+    if (prob && prob->newton && !advected)
+      throw std::invalid_argument("a Newton linearisation needs the advection state (wind)");
+    C.opt.nu = opt->nu;
+    C.opt.beta = opt->beta;
+    C.opt.mass_coef = opt->mass_coef;
+    C.opt.inv_eps = opt->inv_eps;
+    C.opt.jacobi_damping = opt->jacobi_damping;
+    // Dirichlet data of the (possibly new) boundary function, same constraint pattern
+    const int k = C.opt.k;
+    const host::TriMesh& fine = C.mesh[C.L];
+    const std::vector<double> gfac = dirichlet_data(fine, k, prob ? prob->bc : nullptr, prob ? prob->bc_user : nullptr);
+    CK(cudaMemcpyAsync(C.g_fac, gfac.data(), sizeof(double) * gfac.size(), cudaMemcpyHostToDevice, C.s));
+    {
+      const int nfd = k + 1, bs = 2 * nfd;
+      const int64_t nflux = int64_t(fine.nf()) * nfd;
+      for (int f = 0; f < fine.nf(); ++f)
+        for (int i = 0; i < nfd; ++i) {
+          C.g_full[int64_t(f) * nfd + i] = gfac[size_t(f) * bs + 2 * i];
+          C.g_full[nflux + int64_t(f) * nfd + i] = gfac[size_t(f) * bs + 2 * i + 1];
+        }
+    }
+    CK(cudaStreamSynchronize(C.s));
+    std::unique_ptr<host::RefTensors> Tk;
+    if (prob && prob->wind) Tk = host::build_ref_tensors(k);
+    linearise(C, prob, Tk.get());
+    if (C.apply_graph) cudaGraphExecDestroy(C.apply_graph);
+    C.apply_graph = nullptr;
+    build_apply_graph(C);
+    CK(cudaStreamSynchronize(C.s));
+    C.setup_parts[1] = C.lin_parts[3];
+    C.setup_parts[2] = C.lin_parts[0];
+    C.setup_parts[3] = C.lin_parts[1];
+    C.setup_parts[4] = C.lin_parts[2];
+    C.setup_parts[0] = C.setup_parts[5] = 0.0;
+    C.setup_parts[6] = std::chrono::duration<double>(clk::now() - t0).count();
+  });
+}
+
 void hpmg_destroy(hpmg_ctx* ctx) {
   if (!ctx) return;
   cudaStreamSynchronize(ctx->s);
@@ -1004,7 +1108,10 @@ void hpmg_destroy(hpmg_ctx* ctx) {
                     (void*)V->PT.val, (void*)V->x, (void*)V->b, (void*)V->r, (void*)V->y, (void*)V->bw, (void*)V->xw,
                     (void*)V->dbuf, (void*)V->geo, (void*)V->row_elems, (void*)V->elem_facets, (void*)V->facet_block,
                     (void*)V->d_wave_ptr, (void*)V->rec.rec, (void*)V->srec.rec, (void*)V->flow_flags,
-                    (void*)V->flow_ctl, (void*)V->P.ndep, (void*)V->P.dep, (void*)V->d_passes})
+                    (void*)V->flow_ctl, (void*)V->P.ndep, (void*)V->P.dep, (void*)V->d_passes, (void*)V->gath,
+                    (void*)V->block_facet, (void*)V->tdev.nmed, (void*)V->tdev.med, (void*)V->tdev.ncol,
+                    (void*)V->tdev.col, (void*)V->tdev.pos, (void*)V->tdev.avg_ptr, (void*)V->tdev.avg_col,
+                    (void*)V->tdev.avg_val, (void*)V->tdev.base, (void*)V->tdev.tperm})
       fr(p);
   };
   for (auto& V : ctx->lv) free_level(V.get());
@@ -1016,7 +1123,7 @@ void hpmg_destroy(hpmg_ctx* ctx) {
                   (void*)ctx->sc, (void*)ctx->rhs, (void*)ctx->g_fac, (void*)ctx->facet_dir, (void*)ctx->kx,
                   (void*)ctx->kb, (void*)ctx->kr, (void*)ctx->kz, (void*)ctx->kp, (void*)ctx->kAp, (void*)ctx->ktmp,
                   (void*)ctx->io_a, (void*)ctx->io_b, (void*)ctx->pres, (void*)ctx->div, (void*)ctx->urhs,
-                  (void*)ctx->fine_load, (void*)ctx->fine_wind, (void*)ctx->fine_mass})
+                  (void*)ctx->fine_load, (void*)ctx->fine_wind, (void*)ctx->fine_mass, (void*)ctx->acr})
     fr(p);
   if (ctx->sc_host) cudaFreeHost(ctx->sc_host);
   if (ctx->s) cudaStreamDestroy(ctx->s);

@@ -1,21 +1,40 @@
-// Host construction of the CR-GMG prolongation between consecutive
-// lowest-order levels, in 2x2 blocks (fine free facet x coarse free facet):
-//   averaging transfer  (reference inc/transfer.hpp:19-71)
+// Structure of the CR-GMG prolongation between consecutive lowest-order
+// levels, in 2x2 blocks (fine free facet x coarse free facet):
+//   averaging transfer  (reference inc/transfer.hpp:19-71), geometry only
 //   interior patches    (inc/transfer.hpp:75-88)
-//   harmonic correction P_T = I_T - A_TT^{-1} (A I)_T  (inc/transfer.hpp:95-133)
-// The correction reads the assembled fine operator (downloaded once from the
-// device). Setup-only work on small fixed-capacity row buffers (a fine row
-// touches at most 5 coarse facets, a corrected row at most 9); the apply runs
-// on the device (dev::prolong_add / dev::restrict_).
+//   the pattern of the harmonic correction P_T = I_T - A_TT^{-1} (A I)_T
+//   (inc/transfer.hpp:95-133), whose values the device computes from the
+//   current fine operator (kernels.cu corrected_prolongation).
+// Setup-only host work on small fixed-capacity row buffers (a fine row
+// touches at most 5 coarse facets, a corrected row at most 9).
 #pragma once
 
+#include <algorithm>
 #include <array>
+#include <thread>
 #include <vector>
 
 #include "plan.hpp"
 
 namespace hpmg {
 namespace host {
+
+/// Static-chunked parallel loop over [0, n) on up to 16 host threads (setup).
+template <class F>
+inline void parallel_for(int n, F&& f) {
+  const int nt = std::max(1, std::min<int>({16, int(std::thread::hardware_concurrency()), n / 2048 + 1}));
+  if (nt == 1) {
+    for (int i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nt; ++t)
+    pool.emplace_back([&, t] {
+      const int a = int(int64_t(n) * t / nt), b = int(int64_t(n) * (t + 1) / nt);
+      for (int i = a; i < b; ++i) f(i);
+    });
+  for (auto& th : pool) th.join();
+}
 
 struct BlockCsrH {
   int nrows = 0, ncols = 0;
@@ -65,7 +84,7 @@ inline std::vector<BlockRow<kAvgCap>> averaging_blocks(const LevelPlan& C, const
   const TriMesh& cm = *C.mesh;
   const TriMesh& fm = *F.mesh;
   std::vector<BlockRow<kAvgCap>> rows(F.nb);
-  for (int rf = 0; rf < F.nb; ++rf) {
+  parallel_for(F.nb, [&](int rf) {
     const int ff = F.block_facet[rf];
     int se[2] = {-1, -1};
     double sw[2] = {0, 0};
@@ -104,7 +123,7 @@ inline std::vector<BlockRow<kAvgCap>> averaging_blocks(const LevelPlan& C, const
         b[2] += phi * (tfx * ncx + tfy * ncy);  // (tang, flux)
       }
     }
-  }
+  });
   return rows;
 }
 
@@ -135,119 +154,118 @@ inline void lu_solve_multi(std::vector<double> A, int n, std::vector<double>& B,
     }
 }
 
-/// Corrected prolongation in block form. `Aval` is the fine level's ELL-BSR
-/// value array (bs = 2), pattern from F.cols.
-inline BlockCsrH corrected_prolongation(const LevelPlan& C, const LevelPlan& F, const Refinement& R,
-                                        const std::vector<double>& Aval) {
+/// Structure of the corrected prolongation for the device build (built once
+/// per level pair; only A changes between linearisations): the averaging
+/// transfer as block CSR (geometry only), per coarse element its interior
+/// (medial) fine blocks and the coarse columns their correction touches, the
+/// final pattern P = averaging + correction (zero blocks kept, so the pattern
+/// never depends on values) with the averaging values as its base, and the
+/// block positions where each element's correction lands.
+struct TransferPlan {
+  static constexpr int kMedMax = 3, kColMax = kCorrCap;
+  int nrows = 0, ncols = 0, nelem = 0;
+  BlockCsrH avg;                      // fine rows of the averaging transfer
+  BlockCsrH P;                        // final pattern, val = averaging part
+  std::vector<int> nmed, med;         // [nelem], [nelem][3] fine blocks (ascending facet id)
+  std::vector<int> ncol, col;         // [nelem], [nelem][kColMax] coarse blocks (ascending)
+  std::vector<int> pos;               // [nelem][3][kColMax] block index into P (or -1)
+  BlockCsrH PT;                       // transposed pattern
+  std::vector<int> tperm;             // PT block d <- P block tperm[d] (2x2 transposed)
+};
+
+inline TransferPlan transfer_plan(const LevelPlan& C, const LevelPlan& F, const Refinement& R) {
+  TransferPlan T;
+  T.nrows = F.nb;
+  T.ncols = C.nb;
   auto rows = averaging_blocks(C, F, R);
+  T.avg.nrows = F.nb;
+  T.avg.ncols = C.nb;
+  for (int rf = 0; rf < F.nb; ++rf) {
+    for (int q = 0; q < rows[rf].n; ++q) {
+      T.avg.col.push_back(rows[rf].col[q]);
+      for (int t = 0; t < 4; ++t) T.avg.val.push_back(rows[rf].v[q][t]);
+    }
+    T.avg.ptr.push_back(int(T.avg.col.size()));
+  }
   const TriMesh& fm = *F.mesh;
-  // interior patches: medial fine facets per coarse element, ascending facet id
-  std::vector<std::array<int, 3>> med(R.children.size(), {-1, -1, -1});
-  std::vector<int> nmed(R.children.size(), 0);
+  T.nelem = int(R.children.size());
+  T.nmed.assign(T.nelem, 0);
+  T.med.assign(size_t(T.nelem) * 3, -1);
   for (int ff = 0; ff < fm.nf(); ++ff)
     if (R.fclass[ff] == kMedial && F.facet_block[ff] >= 0) {
       const int e = R.parent_elem[ff];
-      med[e][nmed[e]++] = F.facet_block[ff];
+      T.med[size_t(e) * 3 + T.nmed[e]++] = F.facet_block[ff];
     }
-  auto Aent = [&](int rb, int rt, int cb, int ct) -> double {
-    for (int s = 0; s < kSlots; ++s)
-      if (F.cols[size_t(rb) * kSlots + s] == cb) return Aval[((size_t(rb) * kSlots + s) * 2 + rt) * 2 + ct];
-    return 0.0;
-  };
-  std::vector<BlockRow<kCorrCap>> corr(F.nb);
-  std::vector<double> Att, B;
-  for (size_t e = 0; e < med.size(); ++e) {
-    const int nt = 2 * nmed[e];
-    if (nt == 0) continue;
-    // W_T = (A I_avg) restricted to the rows of T: per T-row, coarse block -> (flux, tang)
-    BlockRow<kCorrCap> W[6];
-    for (int r = 0; r < nt; ++r) {
-      const int rb = med[e][r / 2], rt = r % 2;
-      for (int s = 0; s < kSlots; ++s) {
-        const int jb = F.cols[size_t(rb) * kSlots + s];
+  // correction columns from the pattern of A and of the averaging rows
+  T.ncol.assign(T.nelem, 0);
+  T.col.assign(size_t(T.nelem) * TransferPlan::kColMax, -1);
+  std::vector<BlockRow<kCorrCap>> rowcols(F.nb);  // per fine row: correction columns
+  // the medial rows of different coarse elements are disjoint
+  parallel_for(T.nelem, [&](int e) {
+    BlockRow<kCorrCap> cols;
+    for (int i = 0; i < T.nmed[e]; ++i) {
+      const int rb = T.med[size_t(e) * 3 + i];
+      for (int sl = 0; sl < kSlots; ++sl) {
+        const int jb = F.cols[size_t(rb) * kSlots + sl];
         if (jb < 0) continue;
-        for (int jt = 0; jt < 2; ++jt) {
-          const double a = Aval[((size_t(rb) * kSlots + s) * 2 + rt) * 2 + jt];
-          if (a == 0.0) continue;
-          const auto& ar = rows[jb];
-          for (int q = 0; q < ar.n; ++q) {
-            auto& w = W[r].at(ar.col[q]);
-            w[0] += a * ar.v[q][jt * 2 + 0];
-            w[1] += a * ar.v[q][jt * 2 + 1];
-          }
-        }
+        for (int q = 0; q < rows[jb].n; ++q) cols.at(rows[jb].col[q]);
       }
     }
-    BlockRow<kCorrCap> cols;  // union of W columns
-    for (int r = 0; r < nt; ++r)
-      for (int q = 0; q < W[r].n; ++q) cols.at(W[r].col[q]);
-    if (cols.n == 0) continue;
-    const int m = 2 * cols.n;
-    Att.assign(size_t(nt) * nt, 0.0);
-    B.assign(size_t(nt) * m, 0.0);
-    for (int r = 0; r < nt; ++r) {
-      for (int c = 0; c < nt; ++c) Att[size_t(r) * nt + c] = Aent(med[e][r / 2], r % 2, med[e][c / 2], c % 2);
-      for (int q = 0; q < W[r].n; ++q) {
-        int j = 0;
-        while (cols.col[j] != W[r].col[q]) ++j;
-        B[size_t(r) * m + 2 * j] = W[r].v[q][0];
-        B[size_t(r) * m + 2 * j + 1] = W[r].v[q][1];
+    T.ncol[e] = cols.n;
+    for (int j = 0; j < cols.n; ++j) T.col[size_t(e) * TransferPlan::kColMax + j] = cols.col[j];
+    for (int i = 0; i < T.nmed[e]; ++i)
+      for (int j = 0; j < cols.n; ++j) rowcols[T.med[size_t(e) * 3 + i]].at(cols.col[j]);
+  });
+  // final pattern: averaging columns + correction columns per fine row
+  T.P.nrows = F.nb;
+  T.P.ncols = C.nb;
+  std::vector<BlockRow<kCorrCap>> merged(F.nb);
+  parallel_for(F.nb, [&](int rf) {
+    BlockRow<kCorrCap>& m = merged[rf];
+    for (int q = 0; q < rows[rf].n; ++q) m.at(rows[rf].col[q]) = rows[rf].v[q];
+    for (int q = 0; q < rowcols[rf].n; ++q) m.at(rowcols[rf].col[q]);
+  });
+  T.P.ptr.assign(F.nb + 1, 0);
+  for (int rf = 0; rf < F.nb; ++rf) T.P.ptr[rf + 1] = T.P.ptr[rf] + merged[rf].n;
+  T.P.col.resize(T.P.ptr[F.nb]);
+  T.P.val.resize(size_t(T.P.ptr[F.nb]) * 4);
+  parallel_for(F.nb, [&](int rf) {
+    for (int q = 0; q < merged[rf].n; ++q) {
+      T.P.col[T.P.ptr[rf] + q] = merged[rf].col[q];
+      for (int t = 0; t < 4; ++t) T.P.val[size_t(T.P.ptr[rf] + q) * 4 + t] = merged[rf].v[q][t];
+    }
+  });
+  T.pos.assign(size_t(T.nelem) * 3 * TransferPlan::kColMax, -1);
+  parallel_for(T.nelem, [&](int e) {
+    for (int i = 0; i < T.nmed[e]; ++i) {
+      const int rb = T.med[size_t(e) * 3 + i];
+      for (int j = 0; j < T.ncol[e]; ++j) {
+        const int c = T.col[size_t(e) * TransferPlan::kColMax + j];
+        for (int q = T.P.ptr[rb]; q < T.P.ptr[rb + 1]; ++q)
+          if (T.P.col[q] == c) T.pos[(size_t(e) * 3 + i) * TransferPlan::kColMax + j] = q;
       }
     }
-    lu_solve_multi(Att, nt, B, m);
-    for (int r = 0; r < nt; ++r)
-      for (int j = 0; j < cols.n; ++j) {
-        auto& b = corr[med[e][r / 2]].at(cols.col[j]);
-        b[(r % 2) * 2 + 0] -= B[size_t(r) * m + 2 * j];
-        b[(r % 2) * 2 + 1] -= B[size_t(r) * m + 2 * j + 1];
-      }
-  }
-  BlockCsrH P;
-  P.nrows = F.nb;
-  P.ncols = C.nb;
-  P.col.reserve(size_t(F.nb) * 6);
-  P.val.reserve(size_t(F.nb) * 24);
-  for (int rf = 0; rf < F.nb; ++rf) {
-    BlockRow<kCorrCap> merged;
-    for (int q = 0; q < rows[rf].n; ++q) merged.at(rows[rf].col[q]) = rows[rf].v[q];
-    for (int q = 0; q < corr[rf].n; ++q) {
-      auto& b = merged.at(corr[rf].col[q]);
-      for (int t = 0; t < 4; ++t) b[t] += corr[rf].v[q][t];
+  });
+  // transposed pattern and the block permutation
+  T.PT.nrows = C.nb;
+  T.PT.ncols = F.nb;
+  std::vector<int> cnt(C.nb + 1, 0);
+  for (int c : T.P.col) cnt[c + 1]++;
+  for (int i = 0; i < C.nb; ++i) cnt[i + 1] += cnt[i];
+  T.PT.ptr = cnt;
+  T.PT.col.assign(T.P.col.size(), 0);
+  T.tperm.assign(T.P.col.size(), 0);
+  std::vector<int> at(cnt.begin(), cnt.end() - 1);
+  for (int r = 0; r < F.nb; ++r)
+    for (int q = T.P.ptr[r]; q < T.P.ptr[r + 1]; ++q) {
+      const int d = at[T.P.col[q]]++;
+      T.PT.col[d] = r;
+      T.tperm[d] = q;
     }
-    for (int q = 0; q < merged.n; ++q) {
-      const auto& v = merged.v[q];
-      if (v[0] == 0.0 && v[1] == 0.0 && v[2] == 0.0 && v[3] == 0.0) continue;
-      P.col.push_back(merged.col[q]);
-      for (int t = 0; t < 4; ++t) P.val.push_back(v[t]);
-    }
-    P.ptr.push_back(int(P.col.size()));
-  }
-  return P;
-}
-
-inline BlockCsrH transpose_blocks(const BlockCsrH& P) {
-  BlockCsrH T;
-  T.nrows = P.ncols;
-  T.ncols = P.nrows;
-  std::vector<int> cnt(P.ncols + 1, 0);
-  for (int c : P.col) cnt[c + 1]++;
-  for (int i = 0; i < P.ncols; ++i) cnt[i + 1] += cnt[i];
-  T.ptr = cnt;
-  T.col.assign(P.col.size(), 0);
-  T.val.assign(P.val.size(), 0.0);
-  std::vector<int> pos(cnt.begin(), cnt.end() - 1);
-  for (int r = 0; r < P.nrows; ++r)
-    for (int q = P.ptr[r]; q < P.ptr[r + 1]; ++q) {
-      const int c = P.col[q], d = pos[c]++;
-      T.col[d] = r;
-      const double* v = &P.val[size_t(q) * 4];
-      T.val[size_t(d) * 4 + 0] = v[0];
-      T.val[size_t(d) * 4 + 1] = v[2];
-      T.val[size_t(d) * 4 + 2] = v[1];
-      T.val[size_t(d) * 4 + 3] = v[3];
-    }
+  T.PT.val.assign(T.P.val.size(), 0.0);
   return T;
 }
+
 
 }  // namespace host
 }  // namespace hpmg

@@ -587,6 +587,93 @@ __global__ void k_bcsr_group(BlockCsr M, const double* __restrict__ v, double* _
   }
 }
 
+/// One thread per coarse element: gather A_TT and W_T = (A I_avg)_T of its
+/// medial fine blocks, LU with partial pivoting (the host algorithm,
+/// reference transfer.hpp:119-130), subtract the solution into P.
+__global__ void k_corrected_prolongation(Bsr A, TransferDev T, double* __restrict__ Pval) {
+  constexpr int kM = 2 * kTransferColMax;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < T.nelem; e += gridDim.x * blockDim.x) {
+    const int nt = 2 * T.nmed[e];
+    if (nt == 0) continue;
+    const int nc = T.ncol[e], m = 2 * nc;
+    const int* med = T.med + size_t(e) * 3;
+    const int* cl = T.col + size_t(e) * kTransferColMax;
+    double Att[36], Bm[6 * kM];
+    for (int r = 0; r < nt; ++r) {
+      const int rb = med[r / 2], rt = r % 2;
+      for (int c = 0; c < nt; ++c) {
+        const int cb = med[c / 2], ct = c % 2;
+        double v = 0.0;
+        for (int sl = 0; sl < kSlots; ++sl)
+          if (A.cols[rb * kSlots + sl] == cb) v = A.val[((size_t(rb) * kSlots + sl) * 2 + rt) * 2 + ct];
+        Att[r * nt + c] = v;
+      }
+      for (int j = 0; j < m; ++j) Bm[r * m + j] = 0.0;
+      for (int sl = 0; sl < kSlots; ++sl) {
+        const int jb = A.cols[rb * kSlots + sl];
+        if (jb < 0) continue;
+        for (int jt = 0; jt < 2; ++jt) {
+          const double a = A.val[((size_t(rb) * kSlots + sl) * 2 + rt) * 2 + jt];
+          if (a == 0.0) continue;
+          for (int q = T.avg_ptr[jb]; q < T.avg_ptr[jb + 1]; ++q) {
+            int j = 0;
+            while (cl[j] != T.avg_col[q]) ++j;
+            Bm[r * m + 2 * j] += a * T.avg_val[size_t(q) * 4 + jt * 2 + 0];
+            Bm[r * m + 2 * j + 1] += a * T.avg_val[size_t(q) * 4 + jt * 2 + 1];
+          }
+        }
+      }
+    }
+    for (int k = 0; k < nt; ++k) {
+      int p = k;
+      for (int i = k + 1; i < nt; ++i)
+        if (fabs(Att[i * nt + k]) > fabs(Att[p * nt + k])) p = i;
+      if (p != k) {
+        for (int j = 0; j < nt; ++j) {
+          const double t = Att[k * nt + j];
+          Att[k * nt + j] = Att[p * nt + j];
+          Att[p * nt + j] = t;
+        }
+        for (int j = 0; j < m; ++j) {
+          const double t = Bm[k * m + j];
+          Bm[k * m + j] = Bm[p * m + j];
+          Bm[p * m + j] = t;
+        }
+      }
+      const double d = Att[k * nt + k];
+      for (int i = k + 1; i < nt; ++i) {
+        const double l = Att[i * nt + k] / d;
+        if (l == 0.0) continue;
+        for (int j = k + 1; j < nt; ++j) Att[i * nt + j] -= l * Att[k * nt + j];
+        for (int j = 0; j < m; ++j) Bm[i * m + j] -= l * Bm[k * m + j];
+      }
+    }
+    for (int j = 0; j < m; ++j)
+      for (int i = nt - 1; i >= 0; --i) {
+        double sv = Bm[i * m + j];
+        for (int l = i + 1; l < nt; ++l) sv -= Att[i * nt + l] * Bm[l * m + j];
+        Bm[i * m + j] = sv / Att[i * nt + i];
+      }
+    for (int r = 0; r < nt; ++r)
+      for (int j = 0; j < nc; ++j) {
+        const int q = T.pos[(size_t(e) * 3 + r / 2) * kTransferColMax + j];
+        Pval[size_t(q) * 4 + (r % 2) * 2 + 0] -= Bm[r * m + 2 * j];
+        Pval[size_t(q) * 4 + (r % 2) * 2 + 1] -= Bm[r * m + 2 * j + 1];
+      }
+  }
+}
+
+__global__ void k_block_transpose_perm(int nnz, const int* __restrict__ perm, const double* __restrict__ Pval,
+                                       double* __restrict__ PTval) {
+  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < nnz; d += gridDim.x * blockDim.x) {
+    const double* v = Pval + size_t(perm[d]) * 4;
+    PTval[size_t(d) * 4 + 0] = v[0];
+    PTval[size_t(d) * 4 + 1] = v[2];
+    PTval[size_t(d) * 4 + 2] = v[1];
+    PTval[size_t(d) * 4 + 3] = v[3];
+  }
+}
+
 /// x = Inv b for the dense coarse inverse (column-major), 2-stage over
 /// column chunks for parallelism: work[chunk][n] partials then a fixed-order sum.
 constexpr int kGemvChunk = 64;
@@ -1010,6 +1097,15 @@ void jacobi_patch(const Bsr& A, const Patches& P, const double* r, double* d, in
 void jacobi_combine(int nb, int bs, const Patches& P, const double* d, int max_nf, double damping, double* x,
                     cudaStream_t s) {
   k_jacobi_combine<<<grid_for(int64_t(nb) * bs, 256), 256, 0, s>>>(nb, bs, P, max_nf * bs, d, damping, x);
+  HPMG_LAUNCH_CHECK();
+}
+
+void corrected_prolongation(const Bsr& A, const TransferDev& T, BlockCsr& P, BlockCsr& PT, cudaStream_t s) {
+  cudaError_t err = cudaMemcpyAsync(P.val, T.base, sizeof(double) * 4 * size_t(T.nnz), cudaMemcpyDeviceToDevice, s);
+  if (err != cudaSuccess) throw std::runtime_error(std::string("CUDA copy: ") + cudaGetErrorString(err));
+  if (T.nelem > 0) k_corrected_prolongation<<<grid_for(T.nelem, 128), 128, 0, s>>>(A, T, P.val);
+  HPMG_LAUNCH_CHECK();
+  if (T.nnz > 0) k_block_transpose_perm<<<grid_for(T.nnz, 256), 256, 0, s>>>(T.nnz, T.tperm, P.val, PT.val);
   HPMG_LAUNCH_CHECK();
 }
 

@@ -40,7 +40,7 @@ struct Patches {
 
 /// 2x2-block CSR (prolongation P: fine rows; PT: coarse rows).
 struct BlockCsr {
-  int nrows = 0;
+  int nrows = 0, nnz = 0;
   int* ptr = nullptr;
   int* col = nullptr;
   double* val = nullptr;  // [nnzb][2][2] row-major
@@ -129,6 +129,20 @@ void small_pre(const Bsr& A, const PatchRecords& R, const int2* passes, int npas
 void small_post(const Bsr& A, const PatchRecords& R, const int2* passes, int npass, int sweeps, const BlockCsr& Pm,
                 const double* e, const double* b, double* x, cudaStream_t s);
 
+/// Device arrays of host::TransferPlan (corrected prolongation structure).
+struct TransferDev {
+  int nelem = 0, nnz = 0;
+  int *nmed = nullptr, *med = nullptr, *ncol = nullptr, *col = nullptr, *pos = nullptr;
+  int *avg_ptr = nullptr, *avg_col = nullptr;
+  double* avg_val = nullptr;
+  double* base = nullptr;  // averaging part in the final pattern [nnz][4]
+  int* tperm = nullptr;    // PT block d <- P block tperm[d]
+};
+constexpr int kTransferColMax = 16;
+/// P = averaging + harmonic correction -A_TT^{-1} (A I_avg)_T per coarse
+/// element (reference transfer.hpp:95-133) from the fine operator A on the
+/// device, into P's fixed pattern; PT by the block permutation.
+void corrected_prolongation(const Bsr& A, const TransferDev& T, BlockCsr& P, BlockCsr& PT, cudaStream_t s);
 void prolong_add(const BlockCsr& P, const double* e, double* x, cudaStream_t s);
 void restrict_(const BlockCsr& PT, const double* r, double* rc, cudaStream_t s);
 void dense_gemv(int n, const double* inv_colmajor, const double* b, double* x, double* work, cudaStream_t s);

@@ -1,10 +1,10 @@
 // Stationary Navier-Stokes driver (reference inc/ns.hpp:69-149) on top of the
-// C ABI: every linearised step is a fresh hp-MG preconditioner built on the
-// device around the current velocity (condensation, patch inverses, coarse
-// inverse and the solve all on the GPU), an AL-Uzawa solve warm-started from
-// the previous velocity, and the device recovery of the interior RT
-// coefficients that the next linearisation needs. Host work per step is the
-// mesh/plan bookkeeping and the CR transfer construction.
+// C ABI: every linearised step re-linearises one hp-MG preconditioner in place
+// around the current velocity (hpmg_update: condensation, patch inverses,
+// coarse inverse on the GPU, CR transfer correction on host threads; the
+// hierarchy, plans and wave schedules are built once), solves with AL-Uzawa
+// warm-started from the previous velocity, and recovers on the device the
+// interior RT coefficients the next linearisation needs.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -52,12 +52,21 @@ extern "C" int hpmg_ns_solve(const hpmg_mesh_desc* mesh, const hpmg_options* opt
 
     State cur, prev;
     double setup_s = 0.0;
+    // the Stokes context (also used for the norms) and one advected context,
+    // created for the first Picard step and re-linearised in place afterwards
+    // (the reference rebuilds the preconditioner per step, ns.hpp:84)
+    Step stokes, adv;
     // one linearised step (ns.hpp:81-100); false on breakdown / non-convergence
     auto linear_step = [&](const hpmg_options& o, const hpmg_problem& p, const State* warm, int* inner, int* ninner,
                            int cap) -> bool {
-      Step st;
+      const bool advected = p.wind_compound != nullptr;
+      Step& st = advected ? adv : stokes;
       const auto ts = clk::now();
-      if (hpmg_create(&st.ctx, mesh, &o, &p)) fail(nullptr);
+      if (!st.ctx) {
+        if (hpmg_create(&st.ctx, mesh, &o, &p)) fail(nullptr);
+      } else if (hpmg_update(st.ctx, &o, &p)) {
+        fail(st.ctx);
+      }
       setup_s += std::chrono::duration<double>(clk::now() - ts).count();
       const int64_t nfull = hpmg_n_full(st.ctx);
       const int ne = hpmg_ne(st.ctx);
@@ -83,12 +92,10 @@ extern "C" int hpmg_ns_solve(const hpmg_mesh_desc* mesh, const hpmg_options* opt
       rep->final_divergence = ur.final_divergence;
       return true;
     };
-    // ||a - b||_L2 and ||a||_L2 of RT fields (assembly.hpp:487-501), on the
-    // device through a Stokes context of the same mesh and order
-    Step norms;
+    // ||a - b||_L2 and ||a||_L2 of RT fields (assembly.hpp:487-501), on the device
     auto rt_norm = [&](const std::vector<double>& c, const std::vector<double>& i) {
-      const double v = hpmg_rt_l2_norm(norms.ctx, c.data(), i.data());
-      if (v < 0) fail(norms.ctx);
+      const double v = hpmg_rt_l2_norm(stokes.ctx, c.data(), i.data());
+      if (v < 0) fail(stokes.ctx);
       return v;
     };
     auto diff = [&](const State& a, const State& b) {
@@ -111,11 +118,6 @@ extern "C" int hpmg_ns_solve(const hpmg_mesh_desc* mesh, const hpmg_options* opt
     // Stokes initial guess (ns.hpp:102-104)
     int stokes_inner[64], nstokes = 0;
     if (!linear_step(aopt, base, nullptr, stokes_inner, &nstokes, 64)) return finish(0);
-    {
-      const auto ts = clk::now();
-      if (hpmg_create(&norms.ctx, mesh, &aopt, &base)) fail(nullptr);
-      setup_s += std::chrono::duration<double>(clk::now() - ts).count();
-    }
     prev = cur;
     // Picard (ns.hpp:106-123)
     for (int n = 0; n < ns->max_picard; ++n) {

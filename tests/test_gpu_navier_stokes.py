@@ -150,3 +150,27 @@ def test_navier_stokes_newton_quadratic_on_device():
     ro = O.ns_solve(base_n=2, levels=3, k=0, nu=1e-2, inv_eps=1e4, bc=O.BC_LID_TOP, cycle=O.CYCLE_VARV,
                     picard_tol=1e-1)
     assert r.picard_iterations == ro["picard_iterations"] and r.newton_iterations == ro["newton_iterations"]
+
+
+@pytest.mark.parametrize("k", [0, 2])
+def test_update_in_place_equals_fresh_context(k):
+    # hpmg_update re-linearises the hierarchy in place: Picard wind -> Newton
+    # about a second wind with a pseudo-time mass field and a new nu; the result
+    # must be bit-identical to a context created for the final state
+    n_f = 8
+    F = O.seeded_load(n_f, 3, -0.1, 0.1)
+    base = dict(base_n=2, levels=3, k=k, inv_eps=1e3, bc="lid_unit", structured_load=(n_f, F), cycle=H.CYCLE_V)
+    gpu = H.MGPreconditioner(nu=1e-2, wind="rotation", **base)
+    probe = H.MGPreconditioner(nu=1e-2, **base)
+    w2 = probe.interpolate("config5_wind")
+    gpu.update(wind=w2, newton=True, mass_field=w2, nu=5e-3, mass_coef=3.0)
+    fresh = H.MGPreconditioner(nu=5e-3, mass_coef=3.0, wind=w2, newton=True, mass_field=w2, **base)
+    b = O.random_vec(gpu.n, 4)
+    assert np.array_equal(gpu.rhs(), fresh.rhs())
+    assert np.array_equal(gpu.spmv(b), fresh.spmv(b))
+    assert np.array_equal(gpu.apply(b), fresh.apply(b))
+    u = O.random_vec(gpu.n_full, 5)
+    for a, c in zip(gpu.recover(u), fresh.recover(u)):
+        assert np.array_equal(a, c)
+    with pytest.raises(H.HpmgError):
+        gpu.update()  # advected -> Stokes is a structural change
