@@ -210,11 +210,13 @@ typedef struct {
  * current velocity and warm-starts the AL-Uzawa solve from it. `opt` supplies
  * k, nu, inv_eps and the MG options (beta and mass_coef are ignored as in the
  * reference driver); `prob` supplies bc and load (its wind fields are ignored).
- * Outputs: final velocity (full compound n_full), interior (ne*k(k+1)),
- * pressure (ne); host pointers. */
+ * Outputs: final velocity (full compound n_full), interior (ne*k(k+1), this
+ * library's interior basis), pressure (ne) and, if non-NULL, the recovered
+ * locals of the final state (LocalSolution: p_ortho ne*(ns-1), grad ne*4ns,
+ * ns = (k+1)(k+2)/2); host pointers. */
 int hpmg_ns_solve(const hpmg_mesh_desc* mesh, const hpmg_options* opt, const hpmg_problem* prob,
                   const hpmg_ns_opts* ns, double* velocity, double* interior, double* pressure,
-                  hpmg_ns_report* rep);
+                  hpmg_ns_report* rep, double* p_ortho, double* grad);
 /* recover_locals on the finest system: interior (ne*k(k+1)), p_ortho (ne*(ns-1)),
  * grad (ne*4*ns, element-major); interior coefficients refer to this library's
  * interior RT basis (same span as the reference's). */

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "hdivmg/multigrid.hpp"
+#include "hdivmg/ns.hpp"
 #include "hdivmg/uzawa.hpp"
 #include "hpmg/capi.h"
 
@@ -35,6 +36,7 @@ inline void check(int rc, const hpmg_ctx* ctx = nullptr) {
   if (rc == HPMG_ERR_LOGIC) throw std::logic_error(msg);
   throw std::runtime_error(msg);
 }
+inline void to_std(const Vec& v, std::vector<double>& out) { out.assign(v.data(), v.data() + v.size()); }
 inline void field_trampoline(double x, double y, double* out, void* user) {
   const auto& f = *static_cast<const std::function<Vec2(const Vec2&)>*>(user);
   Vec2 v = f(Vec2(x, y));
@@ -79,12 +81,23 @@ class MGPreconditioner {
       p.load = &detail::field_trampoline;
       p.load_user = &load_;
     }
+    // Advection / pseudo-time states: the compound part is canonical; the
+    // interior coefficients are in the generating library's interior basis,
+    // which differs from the reference's in the divergence-free bubbles for
+    // k >= 2 (use states produced by hpmg_ns_solve / hpmg_interpolate_hdg, or
+    // a point field through hpmg_problem.wind, at k >= 2).
     if (fine_opt.advection) {
-      wind_c_ = fine_opt.advection->compound;
-      wind_i_ = fine_opt.advection->interior;
+      detail::to_std(fine_opt.advection->compound, wind_c_);
+      detail::to_std(fine_opt.advection->interior, wind_i_);
       p.wind_compound = wind_c_.data();
       p.wind_interior = wind_i_.data();
       p.newton = fine_opt.newton;
+    }
+    if (fine_opt.mass_field) {
+      detail::to_std(fine_opt.mass_field->compound, mass_c_);
+      detail::to_std(fine_opt.mass_field->interior, mass_i_);
+      p.mass_compound = mass_c_.data();
+      p.mass_interior = mass_i_.data();
     }
     hpmg_ctx* c = nullptr;
     detail::check(hpmg_create(&c, &md, &o, &p));
@@ -120,7 +133,7 @@ class MGPreconditioner {
     t.reserve(nnz);
     for (int64_t i = 0; i < n; ++i)
       for (int64_t q = ptr[i]; q < ptr[i + 1]; ++q) t.emplace_back(int(i), int(idx[q]), val[q]);
-    hdivmg::SpMat A(int(n), int(n));
+    hdivmg::SpMat A(static_cast<int>(n), static_cast<int>(n));  // not A(int(n), int(n)): most vexing parse
     A.setFromTriplets(t.begin(), t.end());
     return A;
   }
@@ -138,7 +151,7 @@ class MGPreconditioner {
     void operator()(hpmg_ctx* c) const { hpmg_destroy(c); }
   };
   std::function<Vec2(const Vec2&)> bc_, load_;
-  std::vector<double> xy_, wind_c_, wind_i_;
+  std::vector<double> xy_, wind_c_, wind_i_, mass_c_, mass_i_;
   std::vector<int> el_, tags_;
   std::unique_ptr<hpmg_ctx, Del> ctx_;
 };
@@ -172,7 +185,8 @@ inline hdivmg::SolveStats gmres(const MGPreconditioner& B, const Vec& b, Vec& x,
 
 /// Augmented-Lagrangian Uzawa on the device (uzawa.hpp:51-91).
 inline hdivmg::StokesSolution uzawa_solve(const MGPreconditioner& B, const hdivmg::UzawaOptions& opt = {}) {
-  hpmg_uzawa_opts o{opt.outer_iterations, {opt.krylov.rel_tol, opt.krylov.abs_tol, opt.krylov.max_iterations, 0}};
+  hpmg_uzawa_opts o{opt.outer_iterations, {opt.krylov.rel_tol, opt.krylov.abs_tol, opt.krylov.max_iterations, 0},
+                    opt.initial_velocity ? opt.initial_velocity->data() : nullptr};
   hdivmg::StokesSolution sol;
   sol.velocity.resize(hpmg_n_full(B.handle()));
   sol.pressure.resize(hpmg_ne(B.handle()));
@@ -186,6 +200,80 @@ inline hdivmg::StokesSolution uzawa_solve(const MGPreconditioner& B, const hdivm
   sol.report.not_applicable = rep.not_applicable != 0;
   sol.report.final_divergence = rep.final_divergence;
   return sol;
+}
+
+/// Stationary Navier-Stokes driver on the device (ns.hpp:69-149): same
+/// arguments and report; velocity.interior / locals are in this library's
+/// interior basis (see the MGPreconditioner note).
+inline hdivmg::NSSolution navier_stokes_solve(const hdivmg::MeshHierarchy& hier, int k, const hdivmg::VelocityBC& bc,
+                                              Real nu, const std::function<Vec2(const Vec2&)>& load, Real inv_eps,
+                                              const hdivmg::NSOptions& opt = {}) {
+  const hdivmg::Mesh& base = hier.levels.front();
+  std::vector<double> xy;
+  std::vector<int> el, tags;
+  for (const auto& v : base.vertices) {
+    xy.push_back(v.x());
+    xy.push_back(v.y());
+  }
+  for (const auto& e : base.elements)
+    for (int i = 0; i < 3; ++i) el.push_back(e.v[i]);
+  for (const auto& f : base.facets)
+    if (f.tag == hdivmg::bc::kOutflow) {
+      tags.push_back(f.a);
+      tags.push_back(f.b);
+      tags.push_back(HPMG_TAG_OUTFLOW);
+    }
+  hpmg_mesh_desc md{base.nv(), xy.data(), base.ne(), el.data(), int(tags.size() / 3), tags.data(),
+                    int(hier.levels.size())};
+  const auto& mg = opt.mg;
+  hpmg_options o{k, nu, 0.0, 0.0, inv_eps,
+                 mg.cycle == hdivmg::CycleKind::V ? HPMG_CYCLE_V
+                 : mg.cycle == hdivmg::CycleKind::W ? HPMG_CYCLE_W
+                                                    : HPMG_CYCLE_VARIABLE_V,
+                 mg.smoother == hdivmg::SmootherKind::Multiplicative ? HPMG_SMOOTH_MULTIPLICATIVE
+                                                                     : HPMG_SMOOTH_ADDITIVE,
+                 mg.smooth_steps, mg.jacobi_damping, HPMG_SCHEDULE_WAVES};
+  std::function<Vec2(const Vec2&)> g = bc.g, f = load;
+  hpmg_problem p{};
+  if (g) {
+    p.bc = &detail::field_trampoline;
+    p.bc_user = &g;
+  }
+  if (f) {
+    p.load = &detail::field_trampoline;
+    p.load_user = &f;
+  }
+  hpmg_ns_opts no{opt.picard_tol, opt.newton_rel_tol, opt.newton_abs_tol, opt.max_picard, opt.max_newton,
+                  opt.pseudo_time_inv,
+                  {opt.uzawa.outer_iterations,
+                   {opt.uzawa.krylov.rel_tol, opt.uzawa.krylov.abs_tol, opt.uzawa.krylov.max_iterations, 0},
+                   nullptr}};
+  const hdivmg::Mesh& mesh = hier.levels.back();
+  hdivmg::NSSolution out;
+  out.velocity.V = hdivmg::CompoundSpace(mesh, k);
+  const int ns = (k + 1) * (k + 2) / 2;
+  out.velocity.compound = Vec::Zero(out.velocity.V.n_compound());
+  out.velocity.interior = Vec::Zero(Index(mesh.ne()) * k * (k + 1));
+  out.pressure = Vec::Zero(mesh.ne());
+  out.locals.p_ortho = Vec::Zero(Index(mesh.ne()) * (ns - 1));
+  std::vector<double> grad(size_t(mesh.ne()) * 4 * ns);
+  hpmg_ns_report r{};
+  detail::check(hpmg_ns_solve(&md, &o, &p, &no, out.velocity.compound.data(), out.velocity.interior.data(),
+                              out.pressure.data(), &r, out.locals.p_ortho.data(), grad.data()));
+  out.locals.interior = out.velocity.interior;
+  out.locals.grad_coeffs = hdivmg::Mat(4 * ns, mesh.ne());
+  for (int e = 0; e < mesh.ne(); ++e)
+    for (int q = 0; q < 4 * ns; ++q) out.locals.grad_coeffs(q, e) = grad[size_t(e) * 4 * ns + q];
+  out.report.picard_iterations = r.picard_iterations;
+  out.report.newton_iterations = r.newton_iterations;
+  out.report.picard_inner.assign(r.picard_inner, r.picard_inner + r.n_picard_inner);
+  out.report.newton_inner.assign(r.newton_inner, r.newton_inner + r.n_newton_inner);
+  out.report.picard_diffs.assign(r.picard_diffs, r.picard_diffs + std::min(r.picard_iterations, 128));
+  out.report.newton_diffs.assign(r.newton_diffs, r.newton_diffs + std::min(r.newton_iterations, 64));
+  out.report.converged = r.converged != 0;
+  out.report.not_applicable = r.not_applicable != 0;
+  out.report.final_divergence = r.final_divergence;
+  return out;
 }
 
 }  // namespace hpmg

@@ -129,7 +129,7 @@ def lib():
     L.hpmg_rt_l2_norm.restype = C.c_double
     L.hpmg_rt_l2_norm.argtypes = [vp, dp, dp]
     L.hpmg_ns_solve.argtypes = [C.POINTER(_Mesh), C.POINTER(_Options), C.POINTER(_Problem), C.POINTER(_NSOpts),
-                                dp, dp, dp, C.POINTER(_NSReport)]
+                                dp, dp, dp, C.POINTER(_NSReport), dp, dp]
     L.hpmg_stream.restype = vp
     L.hpmg_stream.argtypes = [vp]
     L.hpmg_vcycle_bytes.restype = C.c_double
@@ -543,7 +543,7 @@ def navier_stokes_solve(*, mesh="unit_square", base_n=2, levels=2, k=0, nu=1.0, 
     pres = np.zeros(ne)
     rep = _NSReport()
     rc = L.hpmg_ns_solve(C.byref(md), C.byref(opt), C.byref(prob), C.byref(o), _dp(vel), _dp(interior), _dp(pres),
-                         C.byref(rep))
+                         C.byref(rep), None, None)
     if rc:
         raise HpmgError(L.hpmg_last_error().decode())
     r = NSReport(rep.picard_iterations, rep.newton_iterations, list(rep.picard_inner[: rep.n_picard_inner]),

@@ -18,7 +18,7 @@
 namespace {
 
 struct State {
-  std::vector<double> compound, interior, pressure;
+  std::vector<double> compound, interior, pressure, p_ortho, grad;
 };
 
 struct Step {
@@ -34,7 +34,7 @@ struct Step {
 
 extern "C" int hpmg_ns_solve(const hpmg_mesh_desc* mesh, const hpmg_options* opt_in, const hpmg_problem* prob_in,
                              const hpmg_ns_opts* ns, double* velocity, double* interior, double* pressure,
-                             hpmg_ns_report* rep) {
+                             hpmg_ns_report* rep, double* p_ortho, double* grad) {
   using clk = std::chrono::steady_clock;
   const auto t0 = clk::now();
   std::memset(rep, 0, sizeof(*rep));
@@ -86,9 +86,12 @@ extern "C" int hpmg_ns_solve(const hpmg_mesh_desc* mesh, const hpmg_options* opt
           gr(size_t(ne) * 4 * ns_);
       if (hpmg_recover(st.ctx, u.data(), in.data(), po.data(), gr.data())) fail(st.ctx);
       in.resize(size_t(ne) * k * (k + 1));
+      po.resize(size_t(ne) * (ns_ - 1));
       cur.compound = std::move(u);
       cur.interior = std::move(in);
       cur.pressure = std::move(pr);
+      cur.p_ortho = std::move(po);
+      cur.grad = std::move(gr);
       rep->final_divergence = ur.final_divergence;
       return true;
     };
@@ -109,6 +112,8 @@ extern "C" int hpmg_ns_solve(const hpmg_mesh_desc* mesh, const hpmg_options* opt
         std::memcpy(velocity, cur.compound.data(), sizeof(double) * cur.compound.size());
         if (!cur.interior.empty()) std::memcpy(interior, cur.interior.data(), sizeof(double) * cur.interior.size());
         std::memcpy(pressure, cur.pressure.data(), sizeof(double) * cur.pressure.size());
+        if (p_ortho && !cur.p_ortho.empty()) std::memcpy(p_ortho, cur.p_ortho.data(), sizeof(double) * cur.p_ortho.size());
+        if (grad) std::memcpy(grad, cur.grad.data(), sizeof(double) * cur.grad.size());
       }
       rep->setup_seconds = setup_s;
       rep->seconds = std::chrono::duration<double>(clk::now() - t0).count();
