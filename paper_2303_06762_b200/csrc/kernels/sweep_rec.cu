@@ -201,12 +201,17 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
     for (int u = 0; u < kPer; ++u)
       if (t + u * TP < ne) xs[t + u * TP] = v[u];
   }
+  // TR threads per patch row: with TR = 2 each takes one external block of
+  // the residual and half of the GEMV columns, combined by a lane shuffle
+  constexpr int TR = TP >= 2 * kMaxPatchF * BS ? 2 : 1;
+  const int row = t / TR, part = t % TR;
   double bv = 0.0;
-  if (t < np) bv = __ldg(b + size_t(fac[t / BS]) * BS + t % BS);
+  if (row < np && part == 0) bv = __ldg(b + size_t(fac[row / BS]) * BS + row % BS);
   __syncthreads();
   sweep_stamp(R, 2);
-  if (t < np) {
-    const int lf = t / BS, i = t % BS;
+  double rsum = 0.0;
+  if (row < np) {
+    const int lf = row / BS, i = row % BS;
     // external blocks are stored column-major: A(i, j) at j*BS + i, so the
     // rows of a block are consecutive words; the column order is rotated by
     // the facet so the facets of a warp hit distinct banks, while all rows of
@@ -215,27 +220,35 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
     const double* xr = xs + lf * kExt * BS;
     double a0 = bv, a1 = 0.0;
 #pragma unroll
-    for (int sl = 0; sl < kExt; ++sl)
+    for (int sq = 0; sq < kExt / TR; ++sq) {
+      const int sl = sq * TR + part;
 #pragma unroll
       for (int jj = 0; jj < BS; jj += 2) {
         const int j0 = (jj + lf) % BS, j1 = (jj + 1 + lf) % BS;
         a0 = fma(-acol[sl * BS * BS + j0 * BS], xr[sl * BS + j0], a0);
         a1 = fma(-acol[sl * BS * BS + j1 * BS], xr[sl * BS + j1], a1);
       }
-    r[threadIdx.x] = a0 + a1;
+    }
+    rsum = a0 + a1;
   }
+  if (TR == 2) rsum += __shfl_xor_sync(0xffffffffu, rsum, 1);
+  if (row < np && part == 0) r[lp * TP + row] = rsum;
   __syncthreads();
   bar_wait(&bar_s);
   sweep_stamp(R, 3);
-  if (t < np) {
+  double dsum = 0.0;
+  if (row < np) {
     // S(t, j): j < t in column j at cs(j) + t - j, j >= t in column t at ct + j,
-    // cs(j) = j np - j (j - 1) / 2 the uniform column start (packed lower, by columns)
+    // cs(j) = j np - j (j - 1) / 2 the uniform column start (packed lower, by columns);
+    // with TR = 2 the two lanes of a row take the columns [0, np/2) and [np/2, np)
+    const int t = row;
     const double* S = rec;
     const double* rr = r + lp * TP;
     const int ct = t * np - t * (t - 1) / 2 - t;
+    const int jb = TR == 2 ? part * (np / 2) : 0, je = TR == 2 ? (part + 1) * (np / 2) : np;
     double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-    int cs = 0, j = 0;
-    for (; j + 3 < np; j += 4) {
+    int cs = jb * np - jb * (jb - 1) / 2, j = jb;
+    for (; j + 3 < je; j += 4) {
       const int o0 = j < t ? cs + t - j : ct + j;
       cs += np - j;
       const int o1 = j + 1 < t ? cs + t - j - 1 : ct + j + 1;
@@ -251,12 +264,14 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
       d2 = fma(S[o2], r23.x, d2);
       d3 = fma(S[o3], r23.y, d3);
     }
-    for (; j < np; ++j) {
+    for (; j < je; ++j) {
       d0 = fma(S[j < t ? cs + t - j : ct + j], rr[j], d0);
       cs += np - j;
     }
-    x[size_t(fac[t / BS]) * BS + t % BS] = (d0 + d1) + (d2 + d3);
+    dsum = (d0 + d1) + (d2 + d3);
   }
+  if (TR == 2) dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);
+  if (row < np && part == 0) x[size_t(fac[row / BS]) * BS + row % BS] = dsum;
   if (DAG) {
     __syncthreads();  // x_p written by every thread of the CTA
     if (threadIdx.x == 0) {
@@ -340,7 +355,7 @@ struct RecCfg<6> {
 };
 template <>
 struct RecCfg<8> {
-  static constexpr int TP = 64, G = 1;
+  static constexpr int TP = 128, G = 1;  // two threads per patch row
 };
 
 /// dataflow launches carry a fixed per-CTA cost (dependency polls, release
@@ -354,7 +369,8 @@ template <int BS, bool DAG>
 void launch(const PatchRecords& R, int p0, int p1, int nblocks, const SweepOrder& O, const DagState& D, const double* b,
             double* x, cudaStream_t s) {
   constexpr int TP = RecCfg<BS>::TP, G = Grp<BS, DAG>::G;
-  if (R.max_nf * BS > TP) throw std::runtime_error("vertex patch too large for the record sweep");
+  if (R.max_nf * BS * (TP >= 2 * kMaxPatchF * BS ? 2 : 1) > TP)
+    throw std::runtime_error("vertex patch too large for the record sweep");
   if (DAG && D.max_dep > TP) throw std::runtime_error("too many patch dependencies for the dataflow sweep");
   const size_t smem = sizeof(double) * (size_t(G) * R.stride + size_t(G) * R.max_nf * kExt * BS + G * TP);
   static bool attr = false;
