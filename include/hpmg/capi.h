@@ -18,6 +18,9 @@
  *   hpmg_recover                <- recover_locals(mesh, V, opt, u) assembly.hpp:513-549
  *   hpmg_smooth                 <- PatchSmoother::forward/backward/jacobi
  *                                                                  smoother.hpp:53-80
+ *   hpmg_postprocess            <- postprocess_velocity(mesh, V, nu, u, grad) postprocess.hpp:29-80
+ *   hpmg_measure_errors         <- measure_errors(..., exact_velocity, exact_gradient)
+ *                                                                  postprocess.hpp:142-188
  *
  * Conventions (identical to the reference):
  *  - Vectors crossing the boundary are in the reference FREE order
@@ -107,6 +110,26 @@ typedef struct {
 void hpmg_field_config5_wind(double x, double y, double* out, void* user);
 void hpmg_field_rotation(double x, double y, double* out, void* user);
 void hpmg_field_lid_unit(double x, double y, double* out, void* user);
+
+/* Point callback of a 2x2 tensor field, row-major: out = {d u0/dx, d u0/dy,
+ * d u1/dx, d u1/dy} (measure_errors' exact_gradient). */
+typedef void (*hpmg_tensor_fn)(double x, double y, double* out, void* user);
+/* The manufactured flow of the reference convergence tests (manufactured.hpp:
+ * 16-65): u = curl of -G(x)G(y), G(s) = s^2 (s-1)^2; p = x(1-x)(1-y) - 1/12.
+ * Loads: stokes_load user = double[2] {nu, beta} (-nu lap u + beta u + grad p);
+ * ns_load user = double* nu (-nu lap u + (grad u) u + grad p). The linear flow
+ * u = (1 + 2y + 3x, 4 - 3y + 5x) with load 2u + (1, 1) (nu = 1/2, beta = 2,
+ * p = x + y - 1) of the reference exactness test (test_postprocess.cpp:120-157).
+ * Passing the library's own velocity/gradient pair to hpmg_measure_errors
+ * evaluates it on the device. */
+void hpmg_field_mms_velocity(double x, double y, double* out, void* user);
+void hpmg_tensor_mms_gradient(double x, double y, double* out, void* user);
+double hpmg_mms_pressure(double x, double y);
+void hpmg_field_mms_stokes_load(double x, double y, double* out, void* user);
+void hpmg_field_mms_ns_load(double x, double y, double* out, void* user);
+void hpmg_field_linear_flow(double x, double y, double* out, void* user);
+void hpmg_tensor_linear_flow_gradient(double x, double y, double* out, void* user);
+void hpmg_field_linear_flow_load(double x, double y, double* out, void* user);
 
 typedef struct {
   double rel_tol, abs_tol;    /* KrylovOptions (krylov.hpp:12-16): 1e-8, 1e-10 */
@@ -221,6 +244,21 @@ int hpmg_ns_solve(const hpmg_mesh_desc* mesh, const hpmg_options* opt, const hpm
  * grad (ne*4*ns, element-major); interior coefficients refer to this library's
  * interior RT basis (same span as the reference's). */
 int hpmg_recover(hpmg_ctx* ctx, const double* velocity_full, double* interior, double* p_ortho, double* grad);
+
+/* ---- post-processing (postprocess.hpp:16-188) ---- */
+/* postprocess_velocity: u* in [P^{k+1}]^2 per element from a velocity (full
+ * compound + this library's interior coefficients) and its gradient variable
+ * (grad as hpmg_recover writes it); post [ne][2 ns_hi] (x modes then y modes of
+ * the orthonormal order-(k+1) basis, ns_hi = (k+2)(k+3)/2; the reference's
+ * PostprocessedVelocity::coeffs column e). Host pointers. */
+int hpmg_postprocess(hpmg_ctx* ctx, const double* velocity_full, const double* interior, const double* grad,
+                     double* post);
+/* measure_errors: out[4] = (e_u, e_L, e_ustar, div_u), the L2 errors of the
+ * velocity, of the gradient variable against -nu grad u, of u*, and the L2
+ * norm of div u_h, at the degree-16 rule. Host pointers. */
+int hpmg_measure_errors(hpmg_ctx* ctx, const double* velocity_full, const double* interior, const double* grad,
+                        const double* post, hpmg_field_fn u_exact, void* u_user, hpmg_tensor_fn grad_exact,
+                        void* g_user, double* out);
 
 /* ---- measurement hooks (bench.py) ---- */
 void* hpmg_stream(hpmg_ctx* ctx);               /* cudaStream_t the context launches on */

@@ -6,6 +6,7 @@
 
 #include "orc_mg.hpp"
 #include "orc_ns.hpp"
+#include "orc_post.hpp"
 
 using namespace orc;
 
@@ -64,13 +65,20 @@ Field make_bc(int kind) {
     case 4: return [](const V2& x) { return x.y > 1.0 - 1e-12 ? V2(1.0, 0.0) : V2(0, 0); };
     case 5: return [](const V2&) { return V2(0.8, -0.55); };
     case 6: return [](const V2&) { return V2(0.0, 0.0); };
+    case 7: return [](const V2& x) { return linflow::velocity(x); };  // test_postprocess.cpp:138-139
   }
   throw std::invalid_argument("bc kind");
 }
 
-Field make_named_load(int kind) {
+Field make_named_load(int kind, Real nu = 0.0, Real beta = 0.0) {
   switch (kind) {
     case 0: return nullptr;
+    case 6: return [nu, beta](const V2& x) { return mms::stokes_load(nu, beta, x); };
+    case 7: return [nu](const V2& x) { return mms::ns_load(nu, x); };
+    case 8: return [](const V2& x) {  // tests/test_postprocess.cpp:133-135
+      const V2 u = linflow::velocity(x);
+      return V2(2.0 * u.x + 1.0, 2.0 * u.y + 1.0);
+    };
     case 2: return [](const V2& x) { return V2(std::sin(2 * x.x) + x.y, std::cos(x.y) - x.x * x.x); };
     case 3: return [](const V2& x) { return V2(std::sin(2 * x.x), x.y); };
     case 4: return [](const V2& x) { return V2(std::sin(3 * x.x) - x.y, std::cos(2 * x.y) + x.x * x.y); };
@@ -146,7 +154,7 @@ void* orc_mg_create(const orc_problem* p) {
       const double* F = pr->loadcopy.data();
       pr->opt.load = [F, nf](const V2& x) { return structured_load(F, nf, x); };
     } else {
-      pr->opt.load = make_named_load(p->load_kind);
+      pr->opt.load = make_named_load(p->load_kind, p->nu, p->beta);
     }
     if (p->wind_kind) {
       pr->wind = interpolate_hdg(fine, p->k, make_wind(p->wind_kind));
@@ -320,6 +328,60 @@ double orc_mg_rt_l2_norm(void* h, const double* compound_full, const double* int
   return rt_l2_norm(*V.mesh, V, c, i);
 }
 
+/// postprocess_velocity (inc/postprocess.hpp:29-80): post [ne][2 ns_hi];
+/// grad [ne][4 ns] as orc_mg_recover writes it.
+void orc_mg_postprocess(void* h, const double* compound_full, const double* interior, const double* grad, double* post) {
+  auto* p = static_cast<Problem*>(h);
+  const Space& V = p->mg->space();
+  const int ns = (V.k + 1) * (V.k + 2) / 2;
+  Vec c(compound_full, compound_full + V.n_compound()), i(interior, interior + V.n_interior());
+  std::vector<Real> g(grad, grad + std::size_t(V.mesh->ne()) * 4 * ns);
+  std::vector<Real> out = postprocess_velocity(*V.mesh, V, p->opt.nu, c, i, g);
+  std::memcpy(post, out.data(), sizeof(double) * out.size());
+}
+
+/// measure_errors (inc/postprocess.hpp:142-188) against exact flow kind
+/// (1 manufactured, 2 linear): out = (e_u, e_L, e_ustar, div_u).
+void orc_mg_errors(void* h, const double* compound_full, const double* interior, const double* grad,
+                   const double* post, int kind, double* out) {
+  auto* p = static_cast<Problem*>(h);
+  const Space& V = p->mg->space();
+  const int ns = (V.k + 1) * (V.k + 2) / 2, nh = (V.k + 2) * (V.k + 3) / 2;
+  const std::size_t ne = V.mesh->ne();
+  Vec c(compound_full, compound_full + V.n_compound()), i(interior, interior + V.n_interior());
+  std::vector<Real> g(grad, grad + ne * 4 * ns), ps(post, post + ne * 2 * nh);
+  ErrorNorms e = measure_errors(*V.mesh, V, p->opt.nu, c, i, g, ps, kind);
+  out[0] = e.e_u;
+  out[1] = e.e_L;
+  out[2] = e.e_ustar;
+  out[3] = e.div_u;
+}
+
+/// Element centroids of the finest mesh, [ne][2].
+void orc_mg_centroids(void* h, double* out) {
+  const Mesh& m = *static_cast<Problem*>(h)->mg->space().mesh;
+  for (int e = 0; e < m.ne(); ++e) {
+    V2 c(0, 0);
+    for (int i = 0; i < 3; ++i) c = c + m.vtx[m.el[e].v[i]];
+    out[2 * e] = c.x / 3.0;
+    out[2 * e + 1] = c.y / 3.0;
+  }
+}
+
+/// Manufactured-flow pointwise values for the source-term check
+/// (tests/test_postprocess.cpp:44-118): out = u(2), grad u(4), lap u(2),
+/// p, grad p(2), stokes_load(nu, beta)(2), ns_load(nu)(2).
+void orc_mms_point(double x, double y, double nu, double beta, double* out) {
+  const V2 X(x, y);
+  const V2 u = mms::velocity(X), l = mms::laplacian(X), gp = mms::pressure_gradient(X);
+  Real g[2][2];
+  mms::gradient(X, g);
+  const V2 fs = mms::stokes_load(nu, beta, X), fn = mms::ns_load(nu, X);
+  const double v[15] = {u.x, u.y, g[0][0], g[0][1], g[1][0], g[1][1], l.x, l.y, mms::pressure(X), gp.x, gp.y,
+                        fs.x, fs.y, fn.x, fn.y};
+  std::memcpy(out, v, sizeof(v));
+}
+
 /// navier_stokes_solve (inc/ns.hpp:69-149) for the problem description `p`
 /// (mesh, k, nu, inv_eps, bc, load, MG options; wind/beta/mass ignored as in
 /// the reference driver). Outputs the final compound velocity, interior
@@ -337,7 +399,7 @@ int orc_ns_solve(const orc_problem* p, const orc_ns_opts* o, double* velocity, d
       const double* F = loadcopy.data();
       load = [F, nf](const V2& x) { return structured_load(F, nf, x); };
     } else {
-      load = make_named_load(p->load_kind);
+      load = make_named_load(p->load_kind, p->nu, p->beta);
     }
     NSOpt no;
     no.picard_tol = o->picard_tol;

@@ -4,6 +4,7 @@
 #include <random>
 
 #include "orc_mg.hpp"
+#include "orc_post.hpp"
 
 using namespace orc;
 
@@ -291,6 +292,81 @@ double orc_check_picard_newton() {
     for (int i = 0; i < cx.nv; ++i) m = std::max(m, std::abs((rp[i] - bp.rhs[i]) - (rn[i] - bn.rhs[i])));
   }
   return m;
+}
+
+/// test_postprocess.cpp:159-225: post-processing preserves element means and
+/// satisfies its weak gradient equation, for random normal(0,1) data drawn by
+/// std::mt19937(11) in the reference's order (compound, interior, gradient
+/// coefficients column by column). out[0] max |mean(u*) - mean(u_h)|,
+/// out[1] max per-element residual norm, evaluated at the error rule.
+void orc_check_postprocess_weak(double* out) {
+  Mesh mesh = unit_square(2);
+  const int k = 2;
+  Space V(mesh, k);
+  const Real nu = 1.3;
+  std::mt19937 rng(11);
+  std::normal_distribution<Real> coef(0.0, 1.0);
+  Vec compound(V.n_compound()), interior(V.n_interior());
+  for (auto& v : compound) v = coef(rng);
+  for (auto& v : interior) v = coef(rng);
+  const RefData& rd = ref_data(k);
+  const int ns = rd.ns();
+  std::vector<Real> grad(std::size_t(mesh.ne()) * 4 * ns);
+  for (auto& v : grad) v = coef(rng);
+  std::vector<Real> post = postprocess_velocity(mesh, V, nu, compound, interior, grad);
+  const PostTables& pt = post_tables(k);
+  const int nh = pt.ns_hi;
+  Real mean_err = 0, res_max = 0;
+  for (int e = 0; e < mesh.ne(); ++e) {
+    ElemCtx cx(mesh, V, e);
+    const Vec c = local_rt(cx, V, compound, interior, e);
+    const Geo& g = cx.geo;
+    Real ms[2] = {0, 0}, mh[2] = {0, 0};
+    std::vector<Real> res(2 * nh, 0.0);
+    for (std::size_t q = 0; q < pt.err.pts.size(); ++q) {
+      const Real w = pt.err.wts[q] * g.detJ;
+      const V2 xh = pt.err.pts[q];
+      Real hx = 0, hy = 0;
+      for (int r = 0; r < cx.nrt; ++r) {
+        hx += rd.rt.val[r][0].eval(xh.x, xh.y) * c[r];
+        hy += rd.rt.val[r][1].eval(xh.x, xh.y) * c[r];
+      }
+      const V2 uh = g.applyJ(hx, hy) / g.detJ;
+      mh[0] += w * uh.x;
+      mh[1] += w * uh.y;
+      std::vector<Real> gx(nh), gy(nh), hv(nh);
+      for (int s = 0; s < nh; ++s) {
+        hv[s] = pt.hi[s].eval(xh.x, xh.y);
+        const Real a = pt.hi_grad[s][0].eval(xh.x, xh.y), b = pt.hi_grad[s][1].eval(xh.x, xh.y);
+        gx[s] = g.Ji[0][0] * a + g.Ji[1][0] * b;
+        gy[s] = g.Ji[0][1] * a + g.Ji[1][1] * b;
+      }
+      Real L[2][2];
+      for (int comp = 0; comp < 4; ++comp) {
+        Real v = 0;
+        for (int m = 0; m < ns; ++m) v += rd.scalar[m].eval(xh.x, xh.y) * grad[(std::size_t(e) * 4 + comp) * ns + m];
+        L[comp / 2][comp % 2] = v;
+      }
+      for (int i = 0; i < 2; ++i) {
+        const Real* pc = &post[std::size_t(e) * 2 * nh + i * nh];
+        Real us = 0, gsx = 0, gsy = 0;
+        for (int s = 0; s < nh; ++s) {
+          us += hv[s] * pc[s];
+          gsx += gx[s] * pc[s];
+          gsy += gy[s] * pc[s];
+        }
+        ms[i] += w * us;
+        const Real tx = gsx + L[i][0] / nu, ty = gsy + L[i][1] / nu;
+        for (int s = 0; s < nh; ++s) res[i * nh + s] += w * (gx[s] * tx + gy[s] * ty);
+      }
+    }
+    mean_err = std::max(mean_err, std::hypot(ms[0] - mh[0], ms[1] - mh[1]));
+    Real r2 = 0;
+    for (Real v : res) r2 += v * v;
+    res_max = std::max(res_max, std::sqrt(r2));
+  }
+  out[0] = mean_err;
+  out[1] = res_max;
 }
 
 /// test_assembly.cpp:221-240: upwind transport sees boundary data. out: max err

@@ -23,6 +23,7 @@ SMOOTH_MULTIPLICATIVE, SMOOTH_ADDITIVE = 0, 1
 DEVICE_PTRS = 1
 
 FIELD_FN = C.CFUNCTYPE(None, C.c_double, C.c_double, C.POINTER(C.c_double), C.c_void_p)
+TENSOR_FN = FIELD_FN  # same signature, 4 outputs (row-major gradient)
 
 
 class _Mesh(C.Structure):
@@ -124,6 +125,10 @@ def lib():
     L.hpmg_gmres.argtypes = [vp, vp, vp, C.POINTER(_KOpts), C.POINTER(_Stats), C.c_int]
     L.hpmg_uzawa.argtypes = [vp, C.POINTER(_UOpts), dp, dp, C.POINTER(_UReport)]
     L.hpmg_recover.argtypes = [vp, vp, vp, vp, vp]
+    L.hpmg_postprocess.argtypes = [vp, dp, dp, dp, dp]
+    L.hpmg_measure_errors.argtypes = [vp, dp, dp, dp, dp, FIELD_FN, vp, TENSOR_FN, vp, dp]
+    L.hpmg_mms_pressure.restype = C.c_double
+    L.hpmg_mms_pressure.argtypes = [C.c_double, C.c_double]
     L.hpmg_interpolate_hdg.argtypes = [vp, FIELD_FN, vp, dp, dp]
     L.hpmg_update.argtypes = [vp, C.POINTER(_Options), C.POINTER(_Problem)]
     L.hpmg_rt_l2_norm.restype = C.c_double
@@ -153,7 +158,55 @@ def _dp(a):
 
 
 NAMED_FIELDS = {"config5_wind": "hpmg_field_config5_wind", "rotation": "hpmg_field_rotation",
-                "lid_unit": "hpmg_field_lid_unit"}
+                "lid_unit": "hpmg_field_lid_unit",
+                # reference manufactured.hpp / test_postprocess.cpp flows; the two
+                # parametrised loads take ("mms_stokes_load", (nu, beta)) / ("mms_ns_load", (nu,))
+                "mms_velocity": "hpmg_field_mms_velocity", "mms_stokes_load": "hpmg_field_mms_stokes_load",
+                "mms_ns_load": "hpmg_field_mms_ns_load", "linear_flow": "hpmg_field_linear_flow",
+                "linear_flow_load": "hpmg_field_linear_flow_load"}
+NAMED_TENSORS = {"mms_gradient": "hpmg_tensor_mms_gradient", "linear_flow_gradient": "hpmg_tensor_linear_flow_gradient"}
+# exact flows of measure_errors by name: (velocity, gradient)
+EXACT_FLOWS = {"mms": ("mms_velocity", "mms_gradient"), "linear_flow": ("linear_flow", "linear_flow_gradient")}
+
+
+def _field_user(spec):
+    """(callback, user pointer, keep-alive) of a field spec: None, a callable,
+    a NAMED_FIELDS name, or (name, params) for the parametrised named loads."""
+    if isinstance(spec, tuple) and len(spec) == 2 and isinstance(spec[0], str):
+        params = np.ascontiguousarray(spec[1], dtype=np.float64)
+        return _field(spec[0]), C.c_void_p(params.ctypes.data), params
+    return _field(spec), None, None
+
+
+def _tensor(fn):
+    """Wraps a callable (x, y) -> 2x2 (d u_i / d x_j) or a NAMED_TENSORS name."""
+    if isinstance(fn, str):
+        return C.cast(getattr(lib(), NAMED_TENSORS[fn]), TENSOR_FN)
+
+    def cb(x, y, out, _user):
+        g = np.asarray(fn(x, y), dtype=np.float64).reshape(4)
+        for i in range(4):
+            out[i] = float(g[i])
+
+    return TENSOR_FN(cb)
+
+
+@dataclass
+class ErrorNorms:
+    """reference postprocess.hpp:84-89"""
+    e_u: float = 0.0
+    e_L: float = 0.0
+    e_ustar: float = 0.0
+    div_u: float = 0.0
+
+
+def estimated_order(coarse, fine):
+    """EOC between two error levels under uniform refinement (postprocess.hpp:190-194)."""
+    return float(np.log2(coarse / fine))
+
+
+def mms_pressure(x, y):
+    return lib().hpmg_mms_pressure(x, y)
 
 
 def _field(fn):
@@ -246,8 +299,8 @@ class MGPreconditioner:
                              smoother=smoother, smooth_steps=smooth_steps, jacobi_damping=jacobi_damping,
                              schedule=SCHEDULES[schedule])
         opt = _Options(**self._optargs)
-        self._bc = _field(bc)
-        self._load = _field(load)
+        self._bc, self._bc_user, self._bc_keep = _field_user(bc)
+        self._load, self._load_user, self._load_keep = _field_user(load)
         self._static = dict(load_per_element=load_per_element, structured_load=structured_load)
         prob = self._problem(wind, newton, mass_field)
         h = C.c_void_p()
@@ -267,7 +320,8 @@ class MGPreconditioner:
         # name) interpolated by the library, or an HDG velocity (compound, interior)
         hdg_wind = isinstance(wind, tuple)
         self._wind = _field(None if hdg_wind else wind)
-        prob = _Problem(self._bc, None, self._load, None, None, None, None, int(bool(newton)), None, 0, self._wind,
+        prob = _Problem(self._bc, self._bc_user, self._load, self._load_user, None, None, None, int(bool(newton)),
+                        None, 0, self._wind,
                         None, None, None)
         if hdg_wind:
             wc, wi = (np.ascontiguousarray(a, dtype=np.float64) for a in wind)
@@ -416,6 +470,34 @@ class MGPreconditioner:
         self._check(lib().hpmg_recover(self.h, v.ctypes.data, interior.ctypes.data, p.ctypes.data, g.ctypes.data))
         return interior[:, : k * (k + 1)], p[:, : ns - 1], g
 
+    def postprocess(self, velocity_full, interior, grad):
+        """postprocess_velocity (reference postprocess.hpp:24-80): u* in
+        [P^{k+1}]^2 per element, [ne, 2 ns_hi] (x modes then y modes)."""
+        nh = (self.k + 2) * (self.k + 3) // 2
+        out = np.zeros((self.ne, 2 * nh))
+        v = np.ascontiguousarray(velocity_full, dtype=np.float64)
+        i = np.ascontiguousarray(interior, dtype=np.float64).ravel()
+        g = np.ascontiguousarray(grad, dtype=np.float64)
+        self._check(lib().hpmg_postprocess(self.h, _dp(v), _dp(i) if i.size else None, _dp(g), _dp(out)))
+        return out
+
+    def measure_errors(self, velocity_full, interior, grad, post, exact="mms"):
+        """measure_errors (reference postprocess.hpp:140-188) against an exact
+        flow: a name from EXACT_FLOWS (evaluated on the device) or a pair of
+        callables (velocity (x, y) -> 2, gradient (x, y) -> 2x2)."""
+        if isinstance(exact, str):
+            fu, fg = _field(EXACT_FLOWS[exact][0]), _tensor(EXACT_FLOWS[exact][1])
+        else:
+            fu, fg = _field(exact[0]), _tensor(exact[1])
+        out = np.zeros(4)
+        v = np.ascontiguousarray(velocity_full, dtype=np.float64)
+        i = np.ascontiguousarray(interior, dtype=np.float64).ravel()
+        g = np.ascontiguousarray(grad, dtype=np.float64)
+        p = np.ascontiguousarray(post, dtype=np.float64)
+        self._check(lib().hpmg_measure_errors(self.h, _dp(v), _dp(i) if i.size else None, _dp(g), _dp(p), fu, None,
+                                              fg, None, _dp(out)))
+        return ErrorNorms(*out)
+
     # -- measurement hooks
     def stream(self):
         return lib().hpmg_stream(self.h)
@@ -499,6 +581,7 @@ class NSSolution:
     interior: np.ndarray   # [ne, k(k+1)] interior RT coefficients
     pressure: np.ndarray   # element means
     report: NSReport
+    grad: np.ndarray = None  # [ne, 4 ns] gradient variable of the final state (LocalSolution::grad_coeffs)
 
 
 def navier_stokes_solve(*, mesh="unit_square", base_n=2, levels=2, k=0, nu=1.0, inv_eps=1e6, bc=None, load=None,
@@ -515,8 +598,10 @@ def navier_stokes_solve(*, mesh="unit_square", base_n=2, levels=2, k=0, nu=1.0, 
     if rc:
         raise HpmgError(L.hpmg_last_error().decode())
     opt = _Options(k, nu, 0.0, 0.0, inv_eps, cycle, smoother, smooth_steps, jacobi_damping, SCHEDULES[schedule])
-    keep = [_field(bc), _field(load)]
-    prob = _Problem(keep[0], None, keep[1], None, None, None, None, 0, None, 0, FIELD_FN(), None, None, None)
+    bcf, bcu, bck = _field_user(bc)
+    ldf, ldu, ldk = _field_user(load)
+    keep = [bcf, ldf, bck, ldk]
+    prob = _Problem(bcf, bcu, ldf, ldu, None, None, None, 0, None, 0, FIELD_FN(), None, None, None)
     if load_per_element is not None:
         a = np.ascontiguousarray(load_per_element, dtype=np.float64)
         keep.append(a)
@@ -541,13 +626,14 @@ def navier_stokes_solve(*, mesh="unit_square", base_n=2, levels=2, k=0, nu=1.0, 
     vel = np.zeros(2 * (k + 1) * nf)
     interior = np.zeros(max(ne * k * (k + 1), 1))
     pres = np.zeros(ne)
+    grad = np.zeros((ne, 2 * (k + 1) * (k + 2)))
     rep = _NSReport()
     rc = L.hpmg_ns_solve(C.byref(md), C.byref(opt), C.byref(prob), C.byref(o), _dp(vel), _dp(interior), _dp(pres),
-                         C.byref(rep), None, None)
+                         C.byref(rep), None, _dp(grad))
     if rc:
         raise HpmgError(L.hpmg_last_error().decode())
     r = NSReport(rep.picard_iterations, rep.newton_iterations, list(rep.picard_inner[: rep.n_picard_inner]),
                  list(rep.newton_inner[: rep.n_newton_inner]), list(rep.picard_diffs[: rep.picard_iterations]),
                  list(rep.newton_diffs[: rep.newton_iterations]), bool(rep.converged), bool(rep.not_applicable),
                  rep.final_divergence, rep.seconds, rep.setup_seconds)
-    return NSSolution(vel, interior[: ne * k * (k + 1)].reshape(ne, k * (k + 1)), pres, r)
+    return NSSolution(vel, interior[: ne * k * (k + 1)].reshape(ne, k * (k + 1)), pres, r, grad)

@@ -112,6 +112,10 @@ struct hpmg_ctx {
   std::vector<std::unique_ptr<Level>> lv;
   std::unique_ptr<Level> head;  // order-k system (k >= 1)
   DevRef ref0, refk;
+  DevRef post;  // post-processing tables (built on first use); post.T unused
+  dev::PostT post_t{};
+  const double* post_x0 = nullptr;  // finest element origins [ne][2]
+  double* post_red = nullptr;       // error partials [4][kRedBlocks] + result [4]
   double* coarse_inv = nullptr;
   double* gemv_work = nullptr;
   int n0 = 0;
@@ -1118,6 +1122,7 @@ void hpmg_destroy(hpmg_ctx* ctx) {
   free_level(ctx->head.get());
   for (void* p : ctx->ref0.owned) fr(p);
   for (void* p : ctx->refk.owned) fr(p);
+  for (void* p : ctx->post.owned) fr(p);
   for (double* p : ctx->gm_basis) fr(p);
   for (void* p : {(void*)ctx->coarse_inv, (void*)ctx->gemv_work, (void*)ctx->red.partial, (void*)ctx->red.counter,
                   (void*)ctx->sc, (void*)ctx->rhs, (void*)ctx->g_fac, (void*)ctx->facet_dir, (void*)ctx->kx,
@@ -1392,6 +1397,133 @@ int hpmg_recover(hpmg_ctx* ctx, const double* velocity_full, double* interior, d
   });
 }
 
+namespace {
+
+/// Post-processing tables and element origins of the finest mesh, on first use.
+const dev::PostT& post_tables(hpmg_ctx& C) {
+  if (C.post_t.Lv) return C.post_t;
+  const int k = C.opt.k;
+  const DevRef& R = k > 0 ? C.refk : C.ref0;
+  auto T = host::build_ref_tensors(k);
+  const host::PostTables H = host::build_post_tables(*T);
+  auto up = [&](const std::vector<double>& v) {
+    double* p = dupload(v, C.s);
+    C.post.owned.push_back(p);
+    return (const double*)p;
+  };
+  const host::TriMesh& M = C.mesh.back();
+  std::vector<double> x0(size_t(2) * M.ne());
+  for (int e = 0; e < M.ne(); ++e) {
+    x0[2 * e] = M.vx[M.ev[e][0]];
+    x0[2 * e + 1] = M.vy[M.ev[e][0]];
+  }
+  dev::PostT P;
+  P.k = k;
+  P.nfd = R.T.nfd;
+  P.nrt = R.T.nrt;
+  P.no = R.T.no;
+  P.ns = R.T.ns;
+  P.nh = H.nh;
+  P.Lv = R.T.Lv;
+  P.Kh = up(H.Kh);
+  P.Bh = up(H.Bh);
+  P.ref_mean = H.ref_mean;
+  P.nqe = H.nqe;
+  P.ex = up(H.ex);
+  P.ew = up(H.ew);
+  P.eval = up(H.eval);
+  P.ediv = up(H.ediv);
+  P.escal = up(H.escal);
+  P.ehi = up(H.ehi);
+  C.post_x0 = up(x0);
+  C.post_red = const_cast<double*>(up(std::vector<double>(size_t(4) * dev::kRedBlocks + 4, 0.0)));
+  CK(cudaStreamSynchronize(C.s));
+  C.post_t = P;
+  return C.post_t;
+}
+
+}  // namespace
+
+int hpmg_postprocess(hpmg_ctx* ctx, const double* velocity_full, const double* interior, const double* grad,
+                     double* post) {
+  return guarded(ctx, [&] {
+    hpmg_ctx& C = *ctx;
+    Level& T = C.top();
+    const dev::PostT& P = post_tables(C);
+    const int ne = T.ne;
+    const size_t nfull = C.g_full.size(), ni = size_t(ne) * P.no, ng = size_t(ne) * 4 * P.ns, np = size_t(ne) * 2 * P.nh;
+    double* comp = dalloc<double>(nfull);
+    double* di = dalloc<double>(std::max<size_t>(ni, 1));
+    double* dg = dalloc<double>(ng);
+    double* dp = dalloc<double>(np);
+    CK(cudaMemcpyAsync(comp, velocity_full, sizeof(double) * nfull, cudaMemcpyHostToDevice, C.s));
+    if (ni) CK(cudaMemcpyAsync(di, interior, sizeof(double) * ni, cudaMemcpyHostToDevice, C.s));
+    CK(cudaMemcpyAsync(dg, grad, sizeof(double) * ng, cudaMemcpyHostToDevice, C.s));
+    dev::postprocess(P, T.geo, ne, T.elem_facets, C.opt.nu, comp, di, dg, dp, C.s);
+    CK(cudaMemcpyAsync(post, dp, sizeof(double) * np, cudaMemcpyDeviceToHost, C.s));
+    CK(cudaStreamSynchronize(C.s));
+    for (double* p : {comp, di, dg, dp}) cudaFree(p);
+  });
+}
+
+int hpmg_measure_errors(hpmg_ctx* ctx, const double* velocity_full, const double* interior, const double* grad,
+                        const double* post, hpmg_field_fn u_exact, void* u_user, hpmg_tensor_fn grad_exact,
+                        void* g_user, double* out) {
+  return guarded(ctx, [&] {
+    if (!u_exact || !grad_exact) throw std::invalid_argument("measure_errors needs the exact velocity and gradient");
+    hpmg_ctx& C = *ctx;
+    Level& T = C.top();
+    const dev::PostT& P = post_tables(C);
+    const int ne = T.ne;
+    // the library's own analytic flows are evaluated on the device
+    int kind = 0;
+    if (u_exact == hpmg_field_mms_velocity && grad_exact == hpmg_tensor_mms_gradient) kind = 1;
+    if (u_exact == hpmg_field_linear_flow && grad_exact == hpmg_tensor_linear_flow_gradient) kind = 2;
+    const size_t nfull = C.g_full.size(), ni = size_t(ne) * P.no, ng = size_t(ne) * 4 * P.ns, np = size_t(ne) * 2 * P.nh;
+    std::vector<void*> tmp;
+    auto alloc = [&](size_t n) {
+      double* p = dalloc<double>(std::max<size_t>(n, 1));
+      tmp.push_back(p);
+      return p;
+    };
+    double *comp = alloc(nfull), *di = alloc(ni), *dg = alloc(ng), *dp = alloc(np), *ue = nullptr, *ge = nullptr;
+    CK(cudaMemcpyAsync(comp, velocity_full, sizeof(double) * nfull, cudaMemcpyHostToDevice, C.s));
+    if (ni) CK(cudaMemcpyAsync(di, interior, sizeof(double) * ni, cudaMemcpyHostToDevice, C.s));
+    CK(cudaMemcpyAsync(dg, grad, sizeof(double) * ng, cudaMemcpyHostToDevice, C.s));
+    CK(cudaMemcpyAsync(dp, post, sizeof(double) * np, cudaMemcpyHostToDevice, C.s));
+    std::vector<double> hu, hg;
+    if (kind == 0) {  // user callbacks: tabulate at the physical error-rule points
+      const host::TriMesh& M = C.mesh.back();
+      auto T0 = host::build_ref_tensors(C.opt.k);
+      const host::PostTables H = host::build_post_tables(*T0);
+      hu.resize(size_t(ne) * H.nqe * 2);
+      hg.resize(size_t(ne) * H.nqe * 4);
+      for (int e = 0; e < ne; ++e) {
+        const auto& v = M.ev[e];
+        const double x0 = M.vx[v[0]], y0 = M.vy[v[0]];
+        const double j00 = M.vx[v[1]] - x0, j10 = M.vy[v[1]] - y0, j01 = M.vx[v[2]] - x0, j11 = M.vy[v[2]] - y0;
+        for (int q = 0; q < H.nqe; ++q) {
+          const double xh = H.ex[2 * q], yh = H.ex[2 * q + 1];
+          const double x = x0 + j00 * xh + j01 * yh, y = y0 + j10 * xh + j11 * yh;
+          const size_t o = size_t(e) * H.nqe + q;
+          u_exact(x, y, &hu[2 * o], u_user);
+          grad_exact(x, y, &hg[4 * o], g_user);
+        }
+      }
+      ue = alloc(hu.size());
+      ge = alloc(hg.size());
+      CK(cudaMemcpyAsync(ue, hu.data(), sizeof(double) * hu.size(), cudaMemcpyHostToDevice, C.s));
+      CK(cudaMemcpyAsync(ge, hg.data(), sizeof(double) * hg.size(), cudaMemcpyHostToDevice, C.s));
+    }
+    double* partial = C.post_red;
+    dev::measure_errors(P, T.geo, C.post_x0, ne, T.elem_facets, C.opt.nu, comp, di, dg, dp, kind, ue, ge, partial,
+                        partial + 4 * dev::kRedBlocks, C.s);
+    CK(cudaMemcpyAsync(out, partial + 4 * dev::kRedBlocks, sizeof(double) * 4, cudaMemcpyDeviceToHost, C.s));
+    CK(cudaStreamSynchronize(C.s));
+    for (void* p : tmp) cudaFree(p);
+  });
+}
+
 void* hpmg_stream(hpmg_ctx* ctx) { return ctx->s; }
 
 double hpmg_spmv_bytes(const hpmg_ctx* ctx) {
@@ -1595,6 +1727,66 @@ void hpmg_field_config5_wind(double x, double y, double* out, void*) {
 void hpmg_field_rotation(double x, double y, double* out, void*) {
   out[0] = y - 0.5;
   out[1] = 0.5 - x;
+}
+// manufactured flow (reference inc/manufactured.hpp:16-65): bump G(s) = s^2 (s-1)^2
+namespace {
+inline double mb(double s) { return s * s * (s - 1.0) * (s - 1.0); }
+inline double mb1(double s) { return 2.0 * s * (s - 1.0) * (2.0 * s - 1.0); }
+inline double mb2(double s) { return 12.0 * s * s - 12.0 * s + 2.0; }
+inline double mb3(double s) { return 24.0 * s - 12.0; }
+void mms_parts(double x, double y, double* u, double* g, double* lap, double* gp) {
+  u[0] = -mb(x) * mb1(y);
+  u[1] = mb1(x) * mb(y);
+  g[0] = -mb1(x) * mb1(y);
+  g[1] = -mb(x) * mb2(y);
+  g[2] = mb2(x) * mb(y);
+  g[3] = mb1(x) * mb1(y);
+  lap[0] = -mb2(x) * mb1(y) - mb(x) * mb3(y);
+  lap[1] = mb3(x) * mb(y) + mb1(x) * mb2(y);
+  gp[0] = (1.0 - 2.0 * x) * (1.0 - y);
+  gp[1] = x * x - x;
+}
+}  // namespace
+void hpmg_field_mms_velocity(double x, double y, double* out, void*) {
+  out[0] = -mb(x) * mb1(y);
+  out[1] = mb1(x) * mb(y);
+}
+void hpmg_tensor_mms_gradient(double x, double y, double* out, void*) {
+  out[0] = -mb1(x) * mb1(y);
+  out[1] = -mb(x) * mb2(y);
+  out[2] = mb2(x) * mb(y);
+  out[3] = mb1(x) * mb1(y);
+}
+double hpmg_mms_pressure(double x, double y) { return x * (1.0 - x) * (1.0 - y) - 1.0 / 12.0; }
+void hpmg_field_mms_stokes_load(double x, double y, double* out, void* user) {
+  const double* p = static_cast<const double*>(user);
+  const double nu = p[0], beta = p[1];
+  double u[2], g[4], l[2], gp[2];
+  mms_parts(x, y, u, g, l, gp);
+  out[0] = -nu * l[0] + beta * u[0] + gp[0];
+  out[1] = -nu * l[1] + beta * u[1] + gp[1];
+}
+void hpmg_field_mms_ns_load(double x, double y, double* out, void* user) {
+  const double nu = *static_cast<const double*>(user);
+  double u[2], g[4], l[2], gp[2];
+  mms_parts(x, y, u, g, l, gp);
+  out[0] = -nu * l[0] + (g[0] * u[0] + g[1] * u[1]) + gp[0];
+  out[1] = -nu * l[1] + (g[2] * u[0] + g[3] * u[1]) + gp[1];
+}
+void hpmg_field_linear_flow(double x, double y, double* out, void*) {
+  out[0] = 1 + 2 * y + 3 * x;
+  out[1] = 4 - 3 * y + 5 * x;
+}
+void hpmg_tensor_linear_flow_gradient(double, double, double* out, void*) {
+  out[0] = 3;
+  out[1] = 2;
+  out[2] = 5;
+  out[3] = -3;
+}
+void hpmg_field_linear_flow_load(double x, double y, double* out, void*) {
+  hpmg_field_linear_flow(x, y, out, nullptr);
+  out[0] = 2.0 * out[0] + 1.0;
+  out[1] = 2.0 * out[1] + 1.0;
 }
 void hpmg_field_lid_unit(double x, double y, double* out, void*) {
   out[0] = y > 1.0 - 1e-12 ? 1.0 : 0.0;

@@ -510,5 +510,70 @@ inline std::unique_ptr<RefTensors> build_ref_tensors(int k) {
   return T;
 }
 
+/// Host tables of the element post-processing (reference inc/postprocess.hpp:
+/// 24-136), see dev::PostT. The P^{k+1} integrals use the assembly rule (exact
+/// for their degree-2k integrands); the error rule is the degree-16 Duffy rule.
+struct PostTables {
+  int nh = 3, nqe = 0;
+  double ref_mean = 0.0;
+  std::vector<double> Kh, Bh, ex, ew, eval, ediv, escal, ehi;
+};
+
+inline PostTables build_post_tables(const RefTensors& T) {
+  PostTables P;
+  const std::vector<Poly> hi = onb(T.k + 1);
+  const int nh = int(hi.size()), m = nh - 1, ns = T.ns, nrt = T.nrt;
+  P.nh = nh;
+  P.ref_mean = l2(hi[0], Poly::mono(0, 0));
+  std::vector<Poly> a(nh), b(nh);
+  for (int s = 0; s < nh; ++s) {
+    a[s] = hi[s].dx();
+    b[s] = hi[s].dy();
+  }
+  P.Kh.assign(size_t(3) * m * m, 0.0);
+  P.Bh.assign(size_t(2) * m * ns, 0.0);
+  std::vector<double> av(nh), bv(nh), sv(ns);
+  for (int q = 0; q < T.nq; ++q) {
+    const double x = T.qx[q], y = T.qy[q], w = T.qw[q];
+    for (int s = 1; s < nh; ++s) {
+      av[s] = a[s](x, y);
+      bv[s] = b[s](x, y);
+    }
+    for (int j = 0; j < ns; ++j) sv[j] = T.scal[j](x, y);
+    for (int s = 0; s < m; ++s) {
+      for (int t = 0; t < m; ++t) {
+        const size_t i = size_t(s) * m + t;
+        P.Kh[i] += w * av[s + 1] * av[t + 1];
+        P.Kh[size_t(m) * m + i] += w * bv[s + 1] * bv[t + 1];
+        P.Kh[size_t(2) * m * m + i] += w * (av[s + 1] * bv[t + 1] + bv[s + 1] * av[t + 1]);
+      }
+      for (int j = 0; j < ns; ++j) {
+        P.Bh[size_t(s) * ns + j] += w * av[s + 1] * sv[j];
+        P.Bh[size_t(m + s) * ns + j] += w * bv[s + 1] * sv[j];
+      }
+    }
+  }
+  std::vector<double> px, py, pw;
+  duffy(16, px, py, pw);
+  P.nqe = int(pw.size());
+  P.ew = pw;
+  std::vector<Poly> dv(nrt);
+  for (int r = 0; r < nrt; ++r) {
+    dv[r] = T.rt.fn[r][0].dx();
+    dv[r].axpy(1.0, T.rt.fn[r][1].dy());
+  }
+  for (int q = 0; q < P.nqe; ++q) {
+    const double x = px[q], y = py[q];
+    P.ex.push_back(x);
+    P.ex.push_back(y);
+    for (int l = 0; l < 2; ++l)
+      for (int r = 0; r < nrt; ++r) P.eval.push_back(T.rt.fn[r][l](x, y));
+    for (int r = 0; r < nrt; ++r) P.ediv.push_back(dv[r](x, y));
+    for (int j = 0; j < ns; ++j) P.escal.push_back(T.scal[j](x, y));
+    for (int s = 0; s < nh; ++s) P.ehi.push_back(hi[s](x, y));
+  }
+  return P;
+}
+
 }  // namespace host
 }  // namespace hpmg

@@ -160,6 +160,33 @@ void dot(const double* a, const double* b, int64_t n, const Reduce& red, double*
 constexpr int kMaxRt = 24;  // 3(k+1) + k(k+1) at k = 3
 void rt_norm2(const RefT& T, const ElemGeo* geo, int ne, const int* elem_facets, const double* compound,
               const double* interior, const Reduce& red, double* out, cudaStream_t s);
+/// Post-processing tables of one order (post.cu; reference inc/postprocess.hpp).
+/// a, b: reference x / y derivatives of the orthonormal P^{k+1} modes 1..nh-1.
+struct PostT {
+  int k = 0, nfd = 1, nrt = 3, no = 0, ns = 1, nh = 3;
+  const double* Lv = nullptr;  // [2][nrt] sum_q w v^_{r,i} (assembly rule)
+  const double* Kh = nullptr;  // [3][nh-1][nh-1] sum_q w a_s a_t, b_s b_t, a_s b_t + b_s a_t
+  const double* Bh = nullptr;  // [2][nh-1][ns]   sum_q w a_s s_m, b_s s_m
+  double ref_mean = 0.0;       // int_ref P^{k+1} mode 0
+  int nqe = 0;                 // error rule (degree 16)
+  const double* ex = nullptr;  // [nqe][2] reference points
+  const double* ew = nullptr;  // [nqe]
+  const double* eval = nullptr;   // [nqe][2][nrt]
+  const double* ediv = nullptr;   // [nqe][nrt]
+  const double* escal = nullptr;  // [nqe][ns]
+  const double* ehi = nullptr;    // [nqe][nh]
+};
+/// u* in [P^{k+1}]^2 per element (reference postprocess.hpp:24-80): post [ne][2 nh]
+/// (x modes then y modes); grad [ne][4 ns] as recover() writes it.
+void postprocess(const PostT& P, const ElemGeo* geo, int ne, const int* elem_facets, double nu, const double* compound,
+                 const double* interior, const double* grad, double* post, cudaStream_t s);
+/// out4 = (e_u, e_L, e_ustar, div_u) (reference postprocess.hpp:140-188) against
+/// exact flow `kind` (1 manufactured, 2 linear) or, kind 0, host-tabulated
+/// values ue [ne][nqe][2], ge [ne][nqe][4] at the error rule; x0 [ne][2] the
+/// element origins; partial [4][kRedBlocks] scratch.
+void measure_errors(const PostT& P, const ElemGeo* geo, const double* x0, int ne, const int* elem_facets, double nu,
+                    const double* compound, const double* interior, const double* grad, const double* post, int kind,
+                    const double* ue, const double* ge, double* partial, double* out4, cudaStream_t s);
 /// PCG update: alpha = sc[i_num]/sc[i_den]; x += alpha p; r -= alpha Ap; sc[i_rr] = |r|^2
 void pcg_update(double* x, double* r, const double* p, const double* Ap, int64_t n, double* sc, int i_num, int i_den,
                 const Reduce& red, int i_rr, cudaStream_t s);

@@ -16,8 +16,12 @@ ORACLE_DIR = os.path.join(ROOT, "oracle")
 LIB_PATH = os.path.join(ORACLE_DIR, "_build", "liborc.so")
 
 # enums shared with oracle/orc_capi.cpp
-BC_NONE, BC_LID_TOP, BC_LID_ALL, BC_INLET, BC_LID_UNIT, BC_CONST, BC_ZERO = range(7)
+BC_NONE, BC_LID_TOP, BC_LID_ALL, BC_INLET, BC_LID_UNIT, BC_CONST, BC_ZERO, BC_LINEAR_FLOW = range(8)
 LOAD_NONE, LOAD_ARRAY, LOAD_SMOOTH_UZAWA, LOAD_SIN_ADV, LOAD_EQUIV, LOAD_ASSEMBLY = range(6)
+# manufactured Stokes load (nu, beta of the problem), manufactured NS load (nu),
+# the linear flow's load 2u + (1, 1) (reference tests/test_postprocess.cpp)
+LOAD_MMS_STOKES, LOAD_MMS_NS, LOAD_LINEAR_FLOW = 6, 7, 8
+EXACT_MMS, EXACT_LINEAR = 1, 2
 WIND_NONE, WIND_ROT, WIND_CURL = range(3)
 CYCLE_V, CYCLE_W, CYCLE_VARV = range(3)
 SM_MULT, SM_ADD = range(2)
@@ -108,6 +112,10 @@ def lib():
         L.orc_mg_patches.argtypes = [P, C.c_int, lp, lp]
         L.orc_mg_recover.argtypes = [P, dp, dp, dp, dp]
         L.orc_mg_wind.argtypes = [P, dp, dp]
+        L.orc_mg_postprocess.argtypes = [P, dp, dp, dp, dp]
+        L.orc_mg_errors.argtypes = [P, dp, dp, dp, dp, C.c_int, dp]
+        L.orc_mms_point.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, dp]
+        L.orc_mg_centroids.argtypes = [P, dp]
         _lib = L
     return _lib
 
@@ -275,6 +283,39 @@ class OracleMG:
         if i.size == 0:
             i = np.zeros(1)
         return lib().orc_mg_rt_l2_norm(self.h, _dp(c), _dp(i))
+
+
+    def postprocess(self, compound_full, interior, grad):
+        """postprocess_velocity: [ne][2 ns_hi] (x modes, then y modes)."""
+        nh = (self.k + 2) * (self.k + 3) // 2
+        out = np.zeros((self.ne, 2 * nh))
+        i = np.ascontiguousarray(interior, dtype=np.float64).ravel()
+        lib().orc_mg_postprocess(self.h, _dp(np.ascontiguousarray(compound_full, dtype=np.float64)),
+                                 _dp(i if i.size else np.zeros(1)), _dp(np.ascontiguousarray(grad, dtype=np.float64)),
+                                 _dp(out))
+        return out
+
+    def centroids(self):
+        out = np.zeros((self.ne, 2))
+        lib().orc_mg_centroids(self.h, _dp(out))
+        return out
+
+    def errors(self, compound_full, interior, grad, post, kind):
+        """measure_errors against exact flow `kind`: dict e_u, e_L, e_ustar, div_u."""
+        out = np.zeros(4)
+        i = np.ascontiguousarray(interior, dtype=np.float64).ravel()
+        lib().orc_mg_errors(self.h, _dp(np.ascontiguousarray(compound_full, dtype=np.float64)),
+                            _dp(i if i.size else np.zeros(1)), _dp(np.ascontiguousarray(grad, dtype=np.float64)),
+                            _dp(np.ascontiguousarray(post, dtype=np.float64)), kind, _dp(out))
+        return dict(zip(("e_u", "e_L", "e_ustar", "div_u"), out))
+
+
+def mms_point(x, y, nu, beta):
+    """Manufactured flow at (x, y): u(2), grad u(4, row-major), lap u(2), p,
+    grad p(2), stokes_load(nu, beta)(2), ns_load(nu)(2)."""
+    out = np.zeros(15)
+    lib().orc_mms_point(x, y, nu, beta, _dp(out))
+    return out
 
 
 def ns_solve(*, mesh_kind=0, base_n=2, levels=2, k=0, nu=1.0, inv_eps=1e3, bc=BC_LID_UNIT, load_kind=LOAD_NONE,
