@@ -13,6 +13,7 @@
  *                                                                  uzawa.hpp:42, krylov.hpp:10
  *   hpmg_matrix_csr, hpmg_rhs,  <- matrix(), rhs(), constraints(), symmetric(), penalty()
  *   hpmg_free_to_full, ...                                          multigrid.hpp:133-146
+ *   hpmg_write_matrix_market    <- write_matrix_market(os, B.matrix()) io.hpp:74-81
  *   hpmg_pcg / hpmg_gmres       <- pcg(A, M, b, x, opt) / gmres(...)  krylov.hpp:30-144
  *   hpmg_uzawa                  <- uzawa_solve(B, opt)             uzawa.hpp:51-91
  *   hpmg_recover                <- recover_locals(mesh, V, opt, u) assembly.hpp:513-549
@@ -185,6 +186,9 @@ int hpmg_rhs(hpmg_ctx* ctx, double* out, int flags);
 /* CSR of the finest operator (level -1) or of lowest-order level l, reference
  * order: call with NULL arrays to get nnz through *nnz. */
 int hpmg_matrix_csr(hpmg_ctx* ctx, int level, int64_t* nnz, int64_t* ptr, int64_t* idx, double* val);
+/* write_matrix_market (io.hpp:72-81) of the same operator: MatrixMarket
+ * coordinate real general, 1-based, %.17g, column by column. */
+int hpmg_write_matrix_market(hpmg_ctx* ctx, int level, const char* path);
 
 /* ---- operators ---- */
 int hpmg_spmv(hpmg_ctx* ctx, const double* x, double* y, int flags);

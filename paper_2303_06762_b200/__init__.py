@@ -126,6 +126,7 @@ def lib():
     L.hpmg_uzawa.argtypes = [vp, C.POINTER(_UOpts), dp, dp, C.POINTER(_UReport)]
     L.hpmg_recover.argtypes = [vp, vp, vp, vp, vp]
     L.hpmg_postprocess.argtypes = [vp, dp, dp, dp, dp]
+    L.hpmg_write_matrix_market.argtypes = [vp, C.c_int, C.c_char_p]
     L.hpmg_measure_errors.argtypes = [vp, dp, dp, dp, dp, FIELD_FN, vp, TENSOR_FN, vp, dp]
     L.hpmg_mms_pressure.restype = C.c_double
     L.hpmg_mms_pressure.argtypes = [C.c_double, C.c_double]
@@ -435,6 +436,10 @@ class MGPreconditioner:
         self._check(L.hpmg_matrix_csr(self.h, level, C.byref(nnz), ptr.ctypes.data_as(C.POINTER(C.c_int64)),
                                       idx.ctypes.data_as(C.POINTER(C.c_int64)), _dp(val)))
         return sp.csr_matrix((val, idx, ptr), shape=(rows, rows))
+
+    def write_matrix_market(self, path, level=-1):
+        """MatrixMarket dump of matrix(level) by the native writer (io.hpp:74-81)."""
+        self._check(lib().hpmg_write_matrix_market(self.h, level, os.fsencode(path)))
 
     # -- operators (host numpy in, host numpy out)
     def apply(self, b):

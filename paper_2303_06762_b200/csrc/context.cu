@@ -8,6 +8,7 @@
 
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -1201,6 +1202,37 @@ int hpmg_matrix_csr(hpmg_ctx* ctx, int level, int64_t* nnz, int64_t* ptr, int64_
       }
     }
     ptr[V.n] = q;
+  });
+}
+
+int hpmg_write_matrix_market(hpmg_ctx* ctx, int level, const char* path) {
+  int64_t nnz = 0;
+  if (int rc = hpmg_matrix_csr(ctx, level, &nnz, nullptr, nullptr, nullptr)) return rc;
+  const int64_t n = level < 0 ? ctx->top().n : ctx->lv.at(level)->n;
+  std::vector<int64_t> ptr(n + 1), idx(nnz);
+  std::vector<double> val(nnz);
+  if (int rc = hpmg_matrix_csr(ctx, level, &nnz, ptr.data(), idx.data(), val.data())) return rc;
+  return guarded(ctx, [&] {
+    // column by column, rows ascending: the order of a column-major Eigen
+    // SparseMatrix walked by write_matrix_market (io.hpp:74-81)
+    std::vector<int64_t> cptr(n + 1, 0), order(nnz);
+    for (int64_t q = 0; q < nnz; ++q) ++cptr[idx[q] + 1];
+    for (int64_t c = 0; c < n; ++c) cptr[c + 1] += cptr[c];
+    std::vector<int64_t> fill(cptr.begin(), cptr.end() - 1), rowof(nnz);
+    for (int64_t r = 0; r < n; ++r)
+      for (int64_t q = ptr[r]; q < ptr[r + 1]; ++q) {
+        const int64_t d = fill[idx[q]]++;
+        order[d] = q;
+        rowof[d] = r;
+      }
+    FILE* f = std::fopen(path, "w");
+    if (!f) throw std::runtime_error(std::string("cannot open ") + path);
+    std::fprintf(f, "%%%%MatrixMarket matrix coordinate real general\n%lld %lld %lld\n", (long long)n, (long long)n,
+                 (long long)nnz);
+    for (int64_t c = 0; c < n; ++c)
+      for (int64_t d = cptr[c]; d < cptr[c + 1]; ++d)
+        std::fprintf(f, "%lld %lld %.17g\n", (long long)(rowof[d] + 1), (long long)(c + 1), val[order[d]]);
+    if (std::fclose(f) != 0) throw std::runtime_error(std::string("write failed: ") + path);
   });
 }
 
