@@ -7,7 +7,7 @@
 //     hpmg::MGPreconditioner B(hier, k, bc, opt, inv_eps, mg);
 //     auto sol = hpmg::uzawa_solve(B);
 // Signatures and semantics follow proj/include/hdivmg/multigrid.hpp:43-146,
-// krylov.hpp:30-144 and uzawa.hpp:23-91. Setup errors are rethrown as the
+// krylov.hpp:30-144, uzawa.hpp:23-91, ns.hpp:69-149 and postprocess.hpp:24-188. Setup errors are rethrown as the
 // reference's exception types; Krylov breakdown stays in-band.
 #pragma once
 
@@ -18,6 +18,7 @@
 
 #include "hdivmg/multigrid.hpp"
 #include "hdivmg/ns.hpp"
+#include "hdivmg/postprocess.hpp"
 #include "hdivmg/uzawa.hpp"
 #include "hpmg/capi.h"
 
@@ -42,6 +43,14 @@ inline void field_trampoline(double x, double y, double* out, void* user) {
   Vec2 v = f(Vec2(x, y));
   out[0] = v.x();
   out[1] = v.y();
+}
+inline void tensor_trampoline(double x, double y, double* out, void* user) {
+  const auto& f = *static_cast<const std::function<hdivmg::Mat2(const Vec2&)>*>(user);
+  const hdivmg::Mat2 g = f(Vec2(x, y));
+  out[0] = g(0, 0);
+  out[1] = g(0, 1);
+  out[2] = g(1, 0);
+  out[3] = g(1, 1);
 }
 }  // namespace detail
 
@@ -273,6 +282,44 @@ inline hdivmg::NSSolution navier_stokes_solve(const hdivmg::MeshHierarchy& hier,
   out.report.converged = r.converged != 0;
   out.report.not_applicable = r.not_applicable != 0;
   out.report.final_divergence = r.final_divergence;
+  return out;
+}
+
+/// postprocess_velocity (postprocess.hpp:29-80) on the device, on B's finest
+/// mesh with B's nu; u.interior in this library's interior basis (the
+/// MGPreconditioner note), grad_coeffs as recover_locals / navier_stokes_solve
+/// return them. Result: coefficients of the orthonormal P^{k+1} basis, column
+/// e = x modes then y modes, exactly as the reference's.
+inline hdivmg::PostprocessedVelocity postprocess_velocity(const MGPreconditioner& B, const hdivmg::HDGVelocity& u,
+                                                         const hdivmg::Mat& grad_coeffs) {
+  const int ne = hpmg_ne(B.handle()), k = u.V.k, nh = (k + 2) * (k + 3) / 2;
+  hdivmg::PostprocessedVelocity out;
+  out.k_hi = k + 1;
+  out.coeffs = hdivmg::Mat::Zero(2 * nh, ne);
+  detail::check(hpmg_postprocess(B.handle(), u.compound.data(), u.interior.data(), grad_coeffs.data(),
+                                 out.coeffs.data()),
+                B.handle());
+  return out;
+}
+
+/// measure_errors (postprocess.hpp:142-188) on the device; the exact fields are
+/// tabulated through the callbacks at the degree-16 rule.
+inline hdivmg::ErrorNorms measure_errors(const MGPreconditioner& B, const hdivmg::HDGVelocity& u,
+                                         const hdivmg::Mat& grad_coeffs, const hdivmg::PostprocessedVelocity& post,
+                                         const std::function<Vec2(const Vec2&)>& exact_velocity,
+                                         const std::function<hdivmg::Mat2(const Vec2&)>& exact_gradient) {
+  double e[4];
+  detail::check(hpmg_measure_errors(B.handle(), u.compound.data(), u.interior.data(), grad_coeffs.data(),
+                                    post.coeffs.data(), &detail::field_trampoline,
+                                    const_cast<std::function<Vec2(const Vec2&)>*>(&exact_velocity),
+                                    &detail::tensor_trampoline,
+                                    const_cast<std::function<hdivmg::Mat2(const Vec2&)>*>(&exact_gradient), e),
+                B.handle());
+  hdivmg::ErrorNorms out;
+  out.e_u = e[0];
+  out.e_L = e[1];
+  out.e_ustar = e[2];
+  out.div_u = e[3];
   return out;
 }
 

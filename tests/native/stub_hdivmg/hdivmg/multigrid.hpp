@@ -29,8 +29,15 @@ struct Mat {
   Mat() = default;
   Mat(Index r, Index c) : rows(r), d(size_t(r * c)) {}
   double& operator()(Index i, Index j) { return d[size_t(j * rows + i)]; }
+  double* data() { return d.data(); }
+  const double* data() const { return d.data(); }
+  static Mat Zero(Index r, Index c) { return Mat(r, c); }
   Index rows = 0;
   std::vector<double> d;
+};
+struct Mat2 {
+  double m[4] = {0, 0, 0, 0};
+  double operator()(int i, int j) const { return m[2 * i + j]; }
 };
 struct Triplet {
   Triplet(int r, int c, double v) : r(r), c(c), v(v) {}
@@ -64,8 +71,9 @@ struct MeshHierarchy {
 };
 struct CompoundSpace {
   CompoundSpace() = default;
-  CompoundSpace(const Mesh&, int) {}
+  CompoundSpace(const Mesh&, int order) : k(order) {}
   Index n_compound() const { return 0; }
+  int k = 0;
 };
 struct HDGVelocity {
   CompoundSpace V;

@@ -16,7 +16,12 @@ def test_hdivmg_adapter_compiles(tmp_path):
                    "  hdivmg::Vec x(B.rhs().size());\n"
                    "  hpmg::pcg(B, B.rhs(), x);\n"
                    "  hpmg::uzawa_solve(B);\n"
-                   "  return hpmg::navier_stokes_solve(h, 2, hdivmg::VelocityBC{}, 1e-2, {}, 1e3);\n"
+                   "  auto sol = hpmg::navier_stokes_solve(h, 2, hdivmg::VelocityBC{}, 1e-2, {}, 1e3);\n"
+                   "  auto post = hpmg::postprocess_velocity(B, sol.velocity, sol.locals.grad_coeffs);\n"
+                   "  hpmg::measure_errors(B, sol.velocity, sol.locals.grad_coeffs, post,\n"
+                   "                       [](const hdivmg::Vec2& x) { return x; },\n"
+                   "                       [](const hdivmg::Vec2&) { return hdivmg::Mat2{}; });\n"
+                   "  return sol;\n"
                    "}\n")
     r = subprocess.run(["g++", "-std=c++17", "-fsyntax-only", "-I", os.path.join(ROOT, "include"),
                         "-I", os.path.join(ROOT, "tests", "native", "stub_hdivmg"), str(src)],
