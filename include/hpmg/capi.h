@@ -9,6 +9,7 @@
  *                                  fine_opt, inv_eps, mg)          multigrid.hpp:45-114
  *   hpmg_apply                  <- MGPreconditioner::apply / as_operator
  *                                                                  multigrid.hpp:117-131
+ *   hpmg_apply_batch            <- apply() over independent right-hand sides, copies overlapped
  *   hpmg_spmv                   <- the LinearOperator [&B](v){ return B.matrix()*v; }
  *                                                                  uzawa.hpp:42, krylov.hpp:10
  *   hpmg_matrix_csr, hpmg_rhs,  <- matrix(), rhs(), constraints(), symmetric(), penalty()
@@ -193,6 +194,11 @@ int hpmg_write_matrix_market(hpmg_ctx* ctx, int level, const char* path);
 /* ---- operators ---- */
 int hpmg_spmv(hpmg_ctx* ctx, const double* x, double* y, int flags);
 int hpmg_apply(hpmg_ctx* ctx, const double* r, double* z, int flags);
+/* z[i] = apply(r[i]) for m independent host vectors (reference order; pinned
+ * memory for overlap): copy-in of vector i+1 and copy-out of result i-1 run on
+ * two copy streams while V-cycle i runs, so PCIe transfers hide behind the
+ * device work. Results are identical to m hpmg_apply calls. */
+int hpmg_apply_batch(hpmg_ctx* ctx, int m, const double* const* r, double* const* z);
 /* which: 0 forward, 1 backward, 2 additive (jacobi) on level l (-1 = order-k head) */
 int hpmg_smooth(hpmg_ctx* ctx, int level, int which, double* x, const double* b, int sweeps, int flags);
 

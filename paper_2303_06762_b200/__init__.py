@@ -126,6 +126,7 @@ def lib():
     L.hpmg_uzawa.argtypes = [vp, C.POINTER(_UOpts), dp, dp, C.POINTER(_UReport)]
     L.hpmg_recover.argtypes = [vp, vp, vp, vp, vp]
     L.hpmg_postprocess.argtypes = [vp, dp, dp, dp, dp]
+    L.hpmg_apply_batch.argtypes = [vp, C.c_int, C.POINTER(vp), C.POINTER(vp)]
     L.hpmg_write_matrix_market.argtypes = [vp, C.c_int, C.c_char_p]
     L.hpmg_measure_errors.argtypes = [vp, dp, dp, dp, dp, FIELD_FN, vp, TENSOR_FN, vp, dp]
     L.hpmg_mms_pressure.restype = C.c_double
@@ -447,6 +448,18 @@ class MGPreconditioner:
         z = np.empty(self.n)
         self._check(lib().hpmg_apply(self.h, b.ctypes.data, z.ctypes.data, 0))
         return z
+
+    def apply_batch(self, rs, zs=None):
+        """apply() over independent host vectors with the PCIe copies of
+        neighbouring vectors overlapped with the V-cycles (hpmg_apply_batch).
+        rs / zs: sequences of float64 host arrays (pinned for overlap)."""
+        rs = [np.ascontiguousarray(r, dtype=np.float64) for r in rs]
+        if zs is None:
+            zs = [np.empty(self.n) for _ in rs]
+        rp = (C.c_void_p * len(rs))(*[r.ctypes.data for r in rs])
+        zp = (C.c_void_p * len(zs))(*[z.ctypes.data for z in zs])
+        self._check(lib().hpmg_apply_batch(self.h, len(rs), rp, zp))
+        return zs
 
     def spmv(self, x):
         x = np.ascontiguousarray(x, dtype=np.float64)

@@ -131,6 +131,11 @@ struct hpmg_ctx {
   // krylov workspace (block layout, finest system)
   double *kx = nullptr, *kb = nullptr, *kr = nullptr, *kz = nullptr, *kp = nullptr, *kAp = nullptr, *ktmp = nullptr;
   double *io_a = nullptr, *io_b = nullptr;  // reference-order staging
+  // pipelined batch apply (hpmg_apply_batch): copy streams, double-buffered staging
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  double *bin[2] = {nullptr, nullptr}, *bout[2] = {nullptr, nullptr};
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr},
+              ev_out[2] = {nullptr, nullptr}, ev_start = nullptr;
   std::vector<double*> gm_basis;
   // uzawa
   double *pres = nullptr, *div = nullptr, *urhs = nullptr;
@@ -1124,6 +1129,15 @@ void hpmg_destroy(hpmg_ctx* ctx) {
   for (void* p : ctx->ref0.owned) fr(p);
   for (void* p : ctx->refk.owned) fr(p);
   for (void* p : ctx->post.owned) fr(p);
+  for (int i = 0; i < 2; ++i) {
+    fr(ctx->bin[i]);
+    fr(ctx->bout[i]);
+    for (cudaEvent_t e : {ctx->ev_in[i], ctx->ev_used[i], ctx->ev_done[i], ctx->ev_out[i]})
+      if (e) cudaEventDestroy(e);
+  }
+  if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
+  if (ctx->s_h2d) cudaStreamDestroy(ctx->s_h2d);
+  if (ctx->s_d2h) cudaStreamDestroy(ctx->s_d2h);
   for (double* p : ctx->gm_basis) fr(p);
   for (void* p : {(void*)ctx->coarse_inv, (void*)ctx->gemv_work, (void*)ctx->red.partial, (void*)ctx->red.counter,
                   (void*)ctx->sc, (void*)ctx->rhs, (void*)ctx->g_fac, (void*)ctx->facet_dir, (void*)ctx->kx,
@@ -1249,6 +1263,53 @@ int hpmg_apply(hpmg_ctx* ctx, const double* r, double* z, int flags) {
     in_vec(*ctx, r, ctx->kr, flags);
     apply_graph(*ctx);
     out_vec(*ctx, ctx->kz, z, flags);
+  });
+}
+
+int hpmg_apply_batch(hpmg_ctx* ctx, int m, const double* const* r, double* const* z) {
+  return guarded(ctx, [&] {
+    if (m < 0 || (m > 0 && (!r || !z))) throw std::invalid_argument("apply_batch: bad vector list");
+    if (m == 0) return;
+    hpmg_ctx& C = *ctx;
+    Level& T = C.top();
+    const size_t bytes = sizeof(double) * T.n;
+    if (!C.s_h2d) {
+      CK(cudaStreamCreateWithFlags(&C.s_h2d, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&C.s_d2h, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i) {
+        C.bin[i] = dalloc<double>(T.n);
+        C.bout[i] = dalloc<double>(T.n);
+        for (cudaEvent_t* e : {&C.ev_in[i], &C.ev_used[i], &C.ev_done[i], &C.ev_out[i]})
+          CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+      }
+      CK(cudaEventCreateWithFlags(&C.ev_start, cudaEventDisableTiming));
+    }
+    // everything below is ordered after the work already queued on the context stream
+    CK(cudaEventRecord(C.ev_start, C.s));
+    CK(cudaStreamWaitEvent(C.s_h2d, C.ev_start, 0));
+    CK(cudaStreamWaitEvent(C.s_d2h, C.ev_start, 0));
+    for (int i = 0; i < m; ++i) {
+      const int j = i & 1;
+      // H2D of vector i into staging j once apply i-2 has consumed it
+      if (i >= 2) CK(cudaStreamWaitEvent(C.s_h2d, C.ev_used[j], 0));
+      CK(cudaMemcpyAsync(C.bin[j], r[i], bytes, cudaMemcpyHostToDevice, C.s_h2d));
+      CK(cudaEventRecord(C.ev_in[j], C.s_h2d));
+      // V-cycle i on the context stream
+      CK(cudaStreamWaitEvent(C.s, C.ev_in[j], 0));
+      dev::to_blocks(T.nb, T.k + 1, C.bin[j], C.kr, C.s);
+      CK(cudaEventRecord(C.ev_used[j], C.s));
+      apply_graph(C);
+      if (i >= 2) CK(cudaStreamWaitEvent(C.s, C.ev_out[j], 0));  // D2H of result i-2 left bout[j]
+      dev::to_reference(T.nb, T.k + 1, C.kz, C.bout[j], C.s);
+      CK(cudaEventRecord(C.ev_done[j], C.s));
+      // D2H of result i
+      CK(cudaStreamWaitEvent(C.s_d2h, C.ev_done[j], 0));
+      CK(cudaMemcpyAsync(z[i], C.bout[j], bytes, cudaMemcpyDeviceToHost, C.s_d2h));
+      CK(cudaEventRecord(C.ev_out[j], C.s_d2h));
+    }
+    // the context stream ends after the last copy-out (callers time on it)
+    CK(cudaStreamWaitEvent(C.s, C.ev_out[(m - 1) & 1], 0));
+    CK(cudaStreamSynchronize(C.s));
   });
 }
 

@@ -129,6 +129,16 @@ def test_apply_bit_identical_repeat():
     assert np.array_equal(gpu.apply(b), gpu.apply(b))
 
 
+@pytest.mark.parametrize("m", [1, 2, 5])
+def test_apply_batch_equals_apply(m):
+    # pipelined batch (copies overlapped on two streams) == m plain applies, bitwise
+    _, gpu = pair(2)
+    rs = [O.random_vec(gpu.n, 40 + i) for i in range(m)]
+    zs = gpu.apply_batch(rs)
+    for r, z in zip(rs, zs):
+        assert np.array_equal(z, gpu.apply(r))
+
+
 @pytest.mark.parametrize("k", [0, 1, 2, 3])
 def test_pcg_counts_and_solution(k):
     orc, gpu = pair(k, levels=4, bc=lid_top)
