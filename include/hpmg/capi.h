@@ -284,6 +284,11 @@ double hpmg_spmv_bytes(const hpmg_ctx* ctx);
  * 8 doubles) receives per-phase averages from an event-instrumented pass. */
 double hpmg_time_apply(hpmg_ctx* ctx, int reps, double* phase_ms);
 int hpmg_kernel_launches_per_apply(const hpmg_ctx* ctx);
+/* Device-resident timing of `reps` finest-operator applies (k_spmv, stream-ordered,
+ * no graph); returns ms per spmv. bytes (optional, 2 doubles): [0] bytes one
+ * spmv streams as stored (ELL-BSR values + columns, x, y), [1] the SURVEY 8(d)
+ * reference CSR accounting. */
+double hpmg_time_spmv(hpmg_ctx* ctx, int reps, double* bytes);
 /* Per-level split of one V-cycle (event-instrumented, no graph): out[0] coarse
  * solve, out[2l] / out[2l+1] pre / post part of level l, out[2L+2..2L+4] head
  * pre-sweep, head residual, head post-sweep (ms). Returns the entry count. */

@@ -127,6 +127,8 @@ def lib():
     L.hpmg_recover.argtypes = [vp, vp, vp, vp, vp]
     L.hpmg_postprocess.argtypes = [vp, dp, dp, dp, dp]
     L.hpmg_apply_batch.argtypes = [vp, C.c_int, C.POINTER(vp), C.POINTER(vp)]
+    L.hpmg_time_spmv.restype = C.c_double
+    L.hpmg_time_spmv.argtypes = [vp, C.c_int, dp]
     L.hpmg_write_matrix_market.argtypes = [vp, C.c_int, C.c_char_p]
     L.hpmg_measure_errors.argtypes = [vp, dp, dp, dp, dp, FIELD_FN, vp, TENSOR_FN, vp, dp]
     L.hpmg_mms_pressure.restype = C.c_double
@@ -532,6 +534,12 @@ class MGPreconditioner:
         ph = np.zeros(8)
         ms = lib().hpmg_time_apply(self.h, reps, _dp(ph) if phases else None)
         return ms, ph
+
+    def time_spmv(self, reps):
+        """(ms per finest-operator spmv, bytes as stored, reference-accounting bytes)."""
+        b = np.zeros(2)
+        ms = lib().hpmg_time_spmv(self.h, reps, _dp(b))
+        return ms, b[0], b[1]
 
     def launches_per_apply(self):
         return lib().hpmg_kernel_launches_per_apply(self.h)

@@ -1656,6 +1656,32 @@ double hpmg_vcycle_bytes(const hpmg_ctx* ctx, double* parts) {
   return tot;
 }
 
+double hpmg_time_spmv(hpmg_ctx* ctx, int reps, double* bytes) {
+  double ms_per = -1;
+  guarded(ctx, [&] {
+    hpmg_ctx& C = *ctx;
+    Level& T = C.top();
+    if (bytes) {  // as stored: ELL-BSR values + slot columns, x read once, y written
+      bytes[0] = double(T.nb) * host::kSlots * T.bs * T.bs * 8.0 + double(T.nb) * host::kSlots * 4.0 + 16.0 * T.n;
+      bytes[1] = T.bytes_spmv;  // SURVEY 8(d) reference CSR accounting
+    }
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    for (int i = 0; i < 3; ++i) dev::spmv(T.A, C.kp, nullptr, C.kAp, 0, nullptr, nullptr, C.s);
+    CK(cudaEventRecord(e0, C.s));
+    for (int i = 0; i < reps; ++i) dev::spmv(T.A, C.kp, nullptr, C.kAp, 0, nullptr, nullptr, C.s);
+    CK(cudaEventRecord(e1, C.s));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms_per = ms / reps;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
+  return ms_per;
+}
+
 double hpmg_time_apply(hpmg_ctx* ctx, int reps, double* phase_ms) {
   double ms_per = -1;
   guarded(ctx, [&] {

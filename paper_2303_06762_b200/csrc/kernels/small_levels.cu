@@ -127,9 +127,14 @@ __device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, i
     if (trace && k < 1000) d_trace[4 * k + 1] = clock64();
     const double* rec = v.ring + (size_t(k % kStages) * kPass + lp) * R.stride;
     int np = 0, g = 0;
+    // row t of S_p into registers now: these loads do not depend on the
+    // residual, so they overlap it instead of following the barrier
+    double srow[2 * kMaxPatchF];
     if (lp < ps.y) {
       const int* meta = reinterpret_cast<const int*>(rec + R.meta_off);
       np = 2 * meta[0];
+#pragma unroll
+      for (int j = 0; j < 2 * kMaxPatchF; ++j) srow[j] = (t < np && j < np) ? rec[j * np + t] : 0.0;
       if (t < np) {
         const int lf = t >> 1, i = t & 1;
         g = 2 * meta[1 + lf] + i;
@@ -154,7 +159,7 @@ __device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, i
       double d[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int j = 0; j < 2 * kMaxPatchF; ++j)
-        if (j < np) d[j & 3] = fma(rec[j * np + t], rr[j], d[j & 3]);
+        if (j < np) d[j & 3] = fma(srow[j], rr[j], d[j & 3]);
       v.sx[g] = (d[0] + d[1]) + (d[2] + d[3]);  // x_p = S_p (b_p - A_pe x_e), sweep_rec.cu
     }
     __syncthreads();

@@ -185,6 +185,13 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
   const int* fac = meta + 1;
   const int* ecol = meta + 1 + R.max_nf;
   double* xs = sx + lp * R.max_nf * kExt * BS;
+  // TR threads per patch row: with TR = 2 each takes one external block of
+  // the residual and half of the GEMV columns, combined by a lane shuffle
+  constexpr int TR = TP >= 2 * kMaxPatchF * BS ? 2 : 1;
+  const int row = t / TR, part = t % TR;
+  // b_p is issued together with the x_e gather (both L2 round trips)
+  double bv = 0.0;
+  if (row < np && part == 0) bv = __ldg(b + size_t(fac[row / BS]) * BS + row % BS);
   {
     // all loads of this thread in flight at once, then the shared stores;
     // L2 (.cg) loads in the dataflow kernel: x changes under a running grid
@@ -201,12 +208,6 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
     for (int u = 0; u < kPer; ++u)
       if (t + u * TP < ne) xs[t + u * TP] = v[u];
   }
-  // TR threads per patch row: with TR = 2 each takes one external block of
-  // the residual and half of the GEMV columns, combined by a lane shuffle
-  constexpr int TR = TP >= 2 * kMaxPatchF * BS ? 2 : 1;
-  const int row = t / TR, part = t % TR;
-  double bv = 0.0;
-  if (row < np && part == 0) bv = __ldg(b + size_t(fac[row / BS]) * BS + row % BS);
   __syncthreads();
   sweep_stamp(R, 2);
   double rsum = 0.0;
