@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
   double* srec = reinterpret_cast<double*>(smraw);  // G * stride
   double* sx = srec + size_t(G) * R.stride;          // G * max_nf * kExt * BS
   double* r = sx + G * R.max_nf * kExt * BS;         // G * TP
-  __shared__ unsigned long long bar, bar_s;
+  __shared__ unsigned long long bar, bar_s, bar_m;
   __shared__ unsigned s_base;
   const int lp = threadIdx.x / TP, t = threadIdx.x % TP;
   int q0, ng, sweep = 0;
@@ -136,17 +136,24 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
   }
   sweep_stamp(R, 0);
   if (threadIdx.x == 0) {
-    // two copies per patch: [A_pe | meta] first (gather + residual start on
-    // it), then the inverse S_p, which lands while x_e is being gathered
+    // three copies per patch: the meta words first (the x_e gather needs only
+    // them), then A_pe (residual), then the inverse S_p, which lands while
+    // x_e is being gathered
     bar_init(&bar);
     bar_init(&bar_s);
+    bar_init(&bar_m);
     unsigned long long pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    const unsigned tail = unsigned(R.stride - R.a_off) * 8u, head = unsigned(R.a_off) * 8u;
-    bar_expect(&bar, unsigned(ng) * tail);
+    const unsigned mbytes = unsigned(R.stride - R.meta_off) * 8u, abytes = unsigned(R.meta_off - R.a_off) * 8u,
+                   head = unsigned(R.a_off) * 8u;
+    bar_expect(&bar_m, unsigned(ng) * mbytes);
+    bar_expect(&bar, unsigned(ng) * abytes);
     bar_expect(&bar_s, unsigned(ng) * head);
     for (int q = 0; q < ng; ++q)
-      tma_part(srec + size_t(q) * R.stride + R.a_off, R.rec + size_t(q0 + q) * R.stride + R.a_off, tail, &bar, pol);
+      tma_part(srec + size_t(q) * R.stride + R.meta_off, R.rec + size_t(q0 + q) * R.stride + R.meta_off, mbytes,
+               &bar_m, pol);
+    for (int q = 0; q < ng; ++q)
+      tma_part(srec + size_t(q) * R.stride + R.a_off, R.rec + size_t(q0 + q) * R.stride + R.a_off, abytes, &bar, pol);
     for (int q = 0; q < ng; ++q)
       tma_part(srec + size_t(q) * R.stride, R.rec + size_t(q0 + q) * R.stride, head, &bar_s, pol);
   }
@@ -177,7 +184,7 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
     }
   }
   __syncthreads();
-  bar_wait(&bar);
+  bar_wait(&bar_m);
   sweep_stamp(R, 1);
   const double* rec = srec + size_t(lp) * R.stride;
   const int* meta = reinterpret_cast<const int*>(rec + R.meta_off);
@@ -208,6 +215,7 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
     for (int u = 0; u < kPer; ++u)
       if (t + u * TP < ne) xs[t + u * TP] = v[u];
   }
+  bar_wait(&bar);
   __syncthreads();
   sweep_stamp(R, 2);
   double rsum = 0.0;
