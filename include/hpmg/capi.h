@@ -83,9 +83,11 @@ typedef struct {
   int schedule;            /* multiplicative sweep schedule (symmetric operators):
                               HPMG_SCHEDULE_WAVES (0, one launch per independent wave) or
                               HPMG_SCHEDULE_DATAFLOW (1, one launch per sweep ordered by
-                              per-patch completion flags); identical results */
+                              per-patch completion flags) or HPMG_SCHEDULE_PERSISTENT (2,
+                              one cooperative launch per smoothing phase, grid barrier
+                              per wave); identical results */
 } hpmg_options;
-enum { HPMG_SCHEDULE_WAVES = 0, HPMG_SCHEDULE_DATAFLOW = 1 };
+enum { HPMG_SCHEDULE_WAVES = 0, HPMG_SCHEDULE_DATAFLOW = 1, HPMG_SCHEDULE_PERSISTENT = 2 };
 
 /* Problem data: boundary values, load and (Oseen) advection state. */
 typedef struct {

@@ -34,7 +34,7 @@ class _Mesh(C.Structure):
 
 # multiplicative sweep schedules (identical results): one launch per wave, or
 # one dataflow launch per sweep ordered by per-patch completion flags
-SCHEDULES = {"waves": 0, "dataflow": 1}
+SCHEDULES = {"waves": 0, "dataflow": 1, "persistent": 2}
 
 
 class _Options(C.Structure):

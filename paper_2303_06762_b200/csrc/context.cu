@@ -79,6 +79,7 @@ struct Level {
   dev::PatchRecords srec;  // full-inverse records of the one-CTA path
   unsigned* flow_flags = nullptr;  // [npatch] completion epochs of the dataflow sweep
   unsigned* flow_ctl = nullptr;    // [2] epoch base, arrival counter
+  unsigned* coop_ctl = nullptr;    // [2] grid-barrier state of the persistent sweep
   bool small = false;      // whole pre/post phase in one CTA (small_levels.cu)
   int2* d_passes = nullptr;
   int npass = 0;
@@ -419,6 +420,8 @@ void build_patch_inverses(hpmg_ctx& C, Level& V) {
     if (const char* d = std::getenv("HPMG_DBG")) V.rec.dbg = std::atoi(d);
     V.flow_flags = dalloc<unsigned>(V.P.n);
     V.flow_ctl = dalloc<unsigned>(2);
+    V.coop_ctl = dalloc<unsigned>(2);
+    CK(cudaMemsetAsync(V.coop_ctl, 0, 2 * sizeof(unsigned), C.s));
     CK(cudaMemsetAsync(V.flow_flags, 0, sizeof(unsigned) * V.P.n, C.s));
     CK(cudaMemsetAsync(V.flow_ctl, 0, sizeof(unsigned) * 2, C.s));
     dev::build_records(V.A, V.P, V.rec, C.s);
@@ -501,6 +504,12 @@ void smooth(hpmg_ctx& C, Level& V, double* x, const double* b, bool post) {
   };
   const void* pf;
   size_t pl;
+  if (V.P.packed && C.opt.schedule == HPMG_SCHEDULE_PERSISTENT && nw <= dev::kMaxSweepWaves) {
+    // all waves of all steps in one cooperative launch, grid barrier per wave
+    dev::sweep_persistent(V.rec, V.wave_ptr.data(), nw, V.steps, post, b, x, V.coop_ctl, C.s);
+    count(C);
+    return;
+  }
   if (V.P.packed && C.opt.schedule == HPMG_SCHEDULE_DATAFLOW && nw <= dev::kMaxSweepWaves) {
     // all waves of all steps in one dataflow launch (sweep_rec.cu)
     dev::sweep_dag(V.rec, V.wave_ptr.data(), nw, V.P, V.steps, post, b, x, V.flow_flags, V.flow_ctl, C.s);
@@ -1118,7 +1127,7 @@ void hpmg_destroy(hpmg_ctx* ctx) {
                     (void*)V->PT.val, (void*)V->x, (void*)V->b, (void*)V->r, (void*)V->y, (void*)V->bw, (void*)V->xw,
                     (void*)V->dbuf, (void*)V->geo, (void*)V->row_elems, (void*)V->elem_facets, (void*)V->facet_block,
                     (void*)V->d_wave_ptr, (void*)V->rec.rec, (void*)V->srec.rec, (void*)V->flow_flags,
-                    (void*)V->flow_ctl, (void*)V->P.ndep, (void*)V->P.dep, (void*)V->d_passes, (void*)V->gath,
+                    (void*)V->flow_ctl, (void*)V->coop_ctl, (void*)V->P.ndep, (void*)V->P.dep, (void*)V->d_passes, (void*)V->gath,
                     (void*)V->block_facet, (void*)V->tdev.nmed, (void*)V->tdev.med, (void*)V->tdev.ncol,
                     (void*)V->tdev.col, (void*)V->tdev.pos, (void*)V->tdev.avg_ptr, (void*)V->tdev.avg_col,
                     (void*)V->tdev.avg_val, (void*)V->tdev.base, (void*)V->tdev.tperm})

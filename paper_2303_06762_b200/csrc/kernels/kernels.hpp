@@ -109,6 +109,12 @@ constexpr int kMaxSweepWaves = 64;
 void sweep_dag(const PatchRecords& R, const int* wave_ptr_host, int nwaves, const Patches& P, int nsweeps,
                bool reverse, const double* b, double* x, unsigned* flags, unsigned* ctl, cudaStream_t s);
 
+/// `nsweeps` whole sweeps in ONE cooperative launch with a grid barrier per
+/// wave boundary and double-buffered record copies (sweep_rec.cu); ctl [2]
+/// zero-initialised barrier state, self-resetting.
+void sweep_persistent(const PatchRecords& R, const int* wave_ptr_host, int nwaves, int nsweeps, bool reverse,
+                      const double* b, double* x, unsigned* ctl, cudaStream_t s);
+
 /// Additive sweep pieces: d_p = Inv_p r_p for all patches; x += damping * sum_p d_p.
 void jacobi_patch(const Bsr& A, const Patches& P, const double* r, double* d, int max_nf, cudaStream_t s);
 void jacobi_combine(int nb, int bs, const Patches& P, const double* d, int max_nf, double damping, double* x,

@@ -295,6 +295,200 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
   }
 }
 
+/// Grid barrier number `i` (0-based) of a cooperative (co-resident) launch:
+/// ctl[0] counts arrivals monotonically within the launch (one release
+/// atomic per CTA, then acquire polls until (i + 1) * grid have arrived);
+/// ctl[1] counts exiting CTAs and the last one resets both, so every launch
+/// (stream-ordered) starts from zero. The x rows written before the barrier
+/// are visible at L2 after it.
+__device__ __forceinline__ void grid_sync(unsigned* ctl, unsigned i) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned old;
+    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctl) : "memory");
+    const unsigned target = (i + 1u) * gridDim.x;
+    if (old + 1u != target)
+      while (ld_acquire(ctl) < target) {
+      }
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void grid_exit(unsigned* ctl) {
+  if (threadIdx.x == 0) {
+    unsigned old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctl + 1) : "memory");
+    if (old + 1u == gridDim.x) {
+      ctl[0] = 0u;
+      ctl[1] = 0u;
+    }
+  }
+}
+
+__device__ __forceinline__ void bar_wait_parity(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(su32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+/// Persistent sweep (HPMG_SCHEDULE_PERSISTENT): one cooperative launch runs
+/// all waves of `nsweeps` sweeps; a grid barrier replaces each wave boundary
+/// (kernel drain + launch) and the records of a CTA's next item are copied
+/// (double buffer) while it works on the current one, so after a barrier only
+/// the x_e gather and the arithmetic remain on the critical path. Per item the
+/// arithmetic is k_sweep's.
+template <int BS, int TP, int G>
+__global__ void __launch_bounds__(G* TP) k_sweep_coop(PatchRecords R, SweepOrder O, int nsweeps,
+                                                      const double* __restrict__ b, double* __restrict__ x,
+                                                      unsigned* ctl) {
+  constexpr int kRow = kExt * BS * BS;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double* srec = reinterpret_cast<double*>(smraw);    // 2 slots x G * stride
+  double* sx = srec + size_t(2) * G * R.stride;          // G * max_nf * kExt * BS
+  double* r = sx + G * R.max_nf * kExt * BS;           // G * TP
+  __shared__ unsigned long long bars[2][3];            // per slot: meta, A_pe, S_p
+  const int lp = threadIdx.x / TP, t = threadIdx.x % TP;
+  if (threadIdx.x == 0) {
+    for (int sl = 0; sl < 2; ++sl)
+      for (int i = 0; i < 3; ++i) bar_init(&bars[sl][i]);
+  }
+  __syncthreads();
+  // this CTA's items in processing order: (sweep, wave, item), item strided by the grid
+  struct Cur {
+    int sw, w, it;
+  };
+  auto norm = [&](Cur c) {
+    while (c.sw < nsweeps && c.it >= O.item0[c.w + 1]) {
+      if (++c.w == O.nw) {
+        c.w = 0;
+        ++c.sw;
+      }
+      c.it = O.item0[c.w] + int(blockIdx.x);
+    }
+    return c;
+  };
+  auto issue = [&](const Cur& c, int sl) {
+    const int q0 = O.wbeg[c.w] + (c.it - O.item0[c.w]) * G, ng = min(G, O.wend[c.w] - q0);
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    const unsigned mbytes = unsigned(R.stride - R.meta_off) * 8u, abytes = unsigned(R.meta_off - R.a_off) * 8u,
+                   head = unsigned(R.a_off) * 8u;
+    double* dst = srec + size_t(sl) * G * R.stride;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    bar_expect(&bars[sl][0], unsigned(ng) * mbytes);
+    bar_expect(&bars[sl][1], unsigned(ng) * abytes);
+    bar_expect(&bars[sl][2], unsigned(ng) * head);
+    for (int q = 0; q < ng; ++q)
+      tma_part(dst + size_t(q) * R.stride + R.meta_off, R.rec + size_t(q0 + q) * R.stride + R.meta_off, mbytes,
+               &bars[sl][0], pol);
+    for (int q = 0; q < ng; ++q)
+      tma_part(dst + size_t(q) * R.stride + R.a_off, R.rec + size_t(q0 + q) * R.stride + R.a_off, abytes,
+               &bars[sl][1], pol);
+    for (int q = 0; q < ng; ++q)
+      tma_part(dst + size_t(q) * R.stride, R.rec + size_t(q0 + q) * R.stride, head, &bars[sl][2], pol);
+  };
+  Cur cur = norm(Cur{0, 0, O.item0[0] + int(blockIdx.x)});
+  if (threadIdx.x == 0 && cur.sw < nsweeps) issue(cur, 0);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  int k = 0;
+  for (int sw = 0; sw < nsweeps; ++sw)
+    for (int w = 0; w < O.nw; ++w) {
+      while (cur.sw == sw && cur.w == w) {
+        const int sl = k & 1;
+        const unsigned par = unsigned(k >> 1) & 1u;
+        const Cur nxt = norm(Cur{cur.sw, cur.w, cur.it + int(gridDim.x)});
+        if (threadIdx.x == 0 && nxt.sw < nsweeps) issue(nxt, sl ^ 1);  // slot sl^1 was released by item k-1
+        const int q0 = O.wbeg[cur.w] + (cur.it - O.item0[cur.w]) * G, ng = min(G, O.wend[cur.w] - q0);
+        bar_wait_parity(&bars[sl][0], par);
+        const double* rec = srec + (size_t(sl) * G + lp) * R.stride;
+        const int* meta = reinterpret_cast<const int*>(rec + R.meta_off);
+        const int nf = lp < ng ? meta[0] : 0, np = nf * BS;
+        const int* fac = meta + 1;
+        const int* ecol = meta + 1 + R.max_nf;
+        double* xs = sx + lp * R.max_nf * kExt * BS;
+        constexpr int TR = TP >= 2 * kMaxPatchF * BS ? 2 : 1;
+        const int row = t / TR, part = t % TR;
+        double bv = 0.0;
+        if (row < np && part == 0) bv = __ldg(b + size_t(fac[row / BS]) * BS + row % BS);
+        {
+          constexpr int kPer = (kMaxPatchF * kExt * BS + TP - 1) / TP;
+          const int ne = nf * kExt * BS;
+          double v[kPer];
+#pragma unroll
+          for (int u = 0; u < kPer; ++u) {
+            const int e = t + u * TP;
+            const int c = e < ne ? ecol[e / BS] : -1;
+            v[u] = c < 0 ? 0.0 : __ldcg(x + size_t(c) * BS + e % BS);  // L2: written by other CTAs
+          }
+#pragma unroll
+          for (int u = 0; u < kPer; ++u)
+            if (t + u * TP < ne) xs[t + u * TP] = v[u];
+        }
+        bar_wait_parity(&bars[sl][1], par);
+        __syncthreads();
+        double rsum = 0.0;
+        if (row < np) {
+          const int lf = row / BS, i = row % BS;
+          const double* acol = rec + R.a_off + lf * kRow + i;
+          const double* xr = xs + lf * kExt * BS;
+          double a0 = bv, a1 = 0.0;
+#pragma unroll
+          for (int sq = 0; sq < kExt / TR; ++sq) {
+            const int sli = sq * TR + part;
+#pragma unroll
+            for (int jj = 0; jj < BS; jj += 2) {
+              const int j0 = (jj + lf) % BS, j1 = (jj + 1 + lf) % BS;
+              a0 = fma(-acol[sli * BS * BS + j0 * BS], xr[sli * BS + j0], a0);
+              a1 = fma(-acol[sli * BS * BS + j1 * BS], xr[sli * BS + j1], a1);
+            }
+          }
+          rsum = a0 + a1;
+        }
+        if (TR == 2) rsum += __shfl_xor_sync(0xffffffffu, rsum, 1);
+        if (row < np && part == 0) r[lp * TP + row] = rsum;
+        __syncthreads();
+        bar_wait_parity(&bars[sl][2], par);
+        double dsum = 0.0;
+        if (row < np) {
+          const int tt = row;
+          const double* S = rec;
+          const double* rr = r + lp * TP;
+          const int ct = tt * np - tt * (tt - 1) / 2 - tt;
+          const int jb = TR == 2 ? part * (np / 2) : 0, je = TR == 2 ? (part + 1) * (np / 2) : np;
+          double d0 = 0.0, d1 = 0.0;
+          int cs = jb * np - jb * (jb - 1) / 2, j = jb;
+          for (; j + 1 < je; j += 2) {
+            const int o0 = j < tt ? cs + tt - j : ct + j;
+            cs += np - j;
+            const int o1 = j + 1 < tt ? cs + tt - j - 1 : ct + j + 1;
+            cs += np - j - 1;
+            d0 = fma(S[o0], rr[j], d0);
+            d1 = fma(S[o1], rr[j + 1], d1);
+          }
+          for (; j < je; ++j) {
+            d0 = fma(S[j < tt ? cs + tt - j : ct + j], rr[j], d0);
+            cs += np - j;
+          }
+          dsum = d0 + d1;
+        }
+        if (TR == 2) dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);
+        if (row < np && part == 0) __stcg(x + size_t(fac[row / BS]) * BS + row % BS, dsum);
+        __syncthreads();  // slot sl and xs/r free for item k+1
+        cur = nxt;
+        ++k;
+      }
+      if (sw + 1 < nsweeps || w + 1 < O.nw) grid_sync(ctl, unsigned(sw * O.nw + w));
+    }
+  grid_exit(ctl);
+}
+
 /// Advances the sweep epoch after a dataflow launch (stream-ordered after it,
 /// so every CTA of that launch has read the old base).
 __global__ void k_epoch(unsigned* ctl, int nsweeps) {
@@ -452,6 +646,70 @@ void gs_wave_rec(const PatchRecords& R, int w0, int w1, const double* b, double*
   if (w1 <= w0) return;
   const int G = group_of(R.bs, false);
   launch_bs<false>(R, w0, w1, (w1 - w0 + G - 1) / G, SweepOrder{}, DagState{}, b, x, s);
+}
+
+namespace {
+template <int BS>
+void launch_coop(const PatchRecords& R, const SweepOrder& O, int nsweeps, const double* b, double* x, unsigned* ctl,
+                 cudaStream_t s) {
+  constexpr int TP = RecCfg<BS>::TP, G = RecCfg<BS>::G;
+  if (R.max_nf * BS * (TP >= 2 * kMaxPatchF * BS ? 2 : 1) > TP)
+    throw std::runtime_error("vertex patch too large for the record sweep");
+  const size_t smem = sizeof(double) * (size_t(2) * G * R.stride + size_t(G) * R.max_nf * kExt * BS + G * TP);
+  static int capacity = 0;
+  static size_t cap_smem = 0;
+  if (capacity == 0 || cap_smem != smem) {
+    cudaFuncSetAttribute(k_sweep_coop<BS, TP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_coop<BS, TP, G>, G * TP, smem);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    capacity = per_sm * sms;
+    cap_smem = smem;
+    if (capacity <= 0) throw std::runtime_error("persistent sweep does not fit on an SM");
+  }
+  int widest = 0;
+  for (int i = 0; i < O.nw; ++i) widest = std::max(widest, O.item0[i + 1] - O.item0[i]);
+  const int grid = std::max(1, std::min(widest, capacity));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(G * TP);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t err = cudaLaunchKernelEx(&cfg, k_sweep_coop<BS, TP, G>, R, O, nsweeps, b, x, ctl);
+  if (err == cudaSuccess) err = cudaGetLastError();
+  if (err != cudaSuccess) throw std::runtime_error(std::string("CUDA launch (persistent sweep): ") + cudaGetErrorString(err));
+}
+}  // namespace
+
+void sweep_persistent(const PatchRecords& R, const int* wave_ptr_host, int nwaves, int nsweeps, bool reverse,
+                      const double* b, double* x, unsigned* ctl, cudaStream_t s) {
+  if (nwaves > kMaxSweepWaves) throw std::runtime_error("too many waves for the persistent sweep");
+  if (nsweeps < 1 || nwaves < 1) return;
+  const int G = group_of(R.bs, false);
+  SweepOrder O;
+  O.nw = nwaves;
+  O.reverse = reverse ? 1 : 0;
+  O.item0[0] = 0;
+  for (int i = 0; i < nwaves; ++i) {
+    const int w = reverse ? nwaves - 1 - i : i;
+    O.wbeg[i] = wave_ptr_host[w];
+    O.wend[i] = wave_ptr_host[w + 1];
+    O.item0[i + 1] = O.item0[i] + (O.wend[i] - O.wbeg[i] + G - 1) / G;
+  }
+  O.nitems = O.item0[nwaves];
+  switch (R.bs) {
+    case 2: launch_coop<2>(R, O, nsweeps, b, x, ctl, s); break;
+    case 4: launch_coop<4>(R, O, nsweeps, b, x, ctl, s); break;
+    case 6: launch_coop<6>(R, O, nsweeps, b, x, ctl, s); break;
+    case 8: launch_coop<8>(R, O, nsweeps, b, x, ctl, s); break;
+    default: throw std::runtime_error("unsupported block size");
+  }
 }
 
 void sweep_dag(const PatchRecords& R, const int* wave_ptr_host, int nwaves, const Patches& P, int nsweeps,

@@ -80,12 +80,14 @@ def test_smoother_sweeps(k):
         assert rel(xg, xo) < apply_tol()
 
 
+@pytest.mark.parametrize("schedule", ["dataflow", "persistent"])
 @pytest.mark.parametrize("k,sweeps", [(0, 1), (1, 3), (3, 2)])
-def test_dataflow_schedule_sweeps(k, sweeps):
-    # one launch per sweep ordered by neighbour completion flags: same result
-    # as the wave schedule, forward and reverse, several sweeps per launch,
-    # repeated calls (the flag epochs advance, never reset)
-    orc, gpu = pair(k, levels=4, schedule="dataflow")
+def test_dataflow_schedule_sweeps(k, sweeps, schedule):
+    # one launch per sweep ordered by neighbour completion flags (dataflow) or
+    # by a grid barrier per wave (persistent): same result as the wave
+    # schedule, forward and reverse, several sweeps per launch, repeated calls
+    # (the flag epochs advance, never reset; the barrier resets itself)
+    orc, gpu = pair(k, levels=4, schedule=schedule)
     level = -1 if k > 0 else 3
     n = gpu.level_n(level) if k == 0 else orc.n
     for rep in range(2):
@@ -94,9 +96,10 @@ def test_dataflow_schedule_sweeps(k, sweeps):
             assert rel(gpu.smooth(level, which, x0, b, sweeps), orc.smooth(level, which, x0, b, sweeps)) < apply_tol()
 
 
+@pytest.mark.parametrize("schedule", ["dataflow", "persistent"])
 @pytest.mark.parametrize("k,cycle", [(0, O.CYCLE_V), (2, O.CYCLE_VARV), (3, O.CYCLE_V)])
-def test_dataflow_schedule_apply(k, cycle):
-    orc, gpu = pair(k, levels=4, cycle=cycle, schedule="dataflow")
+def test_dataflow_schedule_apply(k, cycle, schedule):
+    orc, gpu = pair(k, levels=4, cycle=cycle, schedule=schedule)
     for seed in (11, 12):
         b = O.random_vec(orc.n, seed)
         assert rel(gpu.apply(b), orc.apply(b)) < apply_tol()
