@@ -38,6 +38,9 @@ CONFIGS = {
     "config2": dict(base_n=16, levels=5, k=3, nu=1.0, beta=1e-2, inv_eps=1e3),
     "config1": dict(base_n=8, levels=5, k=1, nu=1.0, beta=1.0, inv_eps=1e3),
     "config3": dict(base_n=8, levels=5, k=2, nu=1.0, beta=0.0, inv_eps=1e4),
+    # the robustness sweep's orders beyond the reference's k <= 3 (parity unpinned)
+    "config3_k4": dict(base_n=8, levels=5, k=4, nu=1.0, beta=0.0, inv_eps=1e4),
+    "config3_k6": dict(base_n=8, levels=5, k=6, nu=1.0, beta=0.0, inv_eps=1e4),
 }
 METRIC = "hp-MG V-cycles/sec (k=3, 256^2x2 tri, 1.57M DOFs)"
 

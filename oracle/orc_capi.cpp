@@ -130,6 +130,14 @@ extern "C" {
 
 const char* orc_last_error() { return g_err.c_str(); }
 
+/// Raise the highest accepted order beyond the reference's 3 (device tests of
+/// k = 4..6 only; returns the previous value).
+int orc_set_max_order(int k) {
+  const int old = max_order();
+  max_order() = k;
+  return old;
+}
+
 /// Seeded per-triangle force: std::mt19937(seed) and
 /// std::uniform_real_distribution<double>(lo, hi), drawn in structured
 /// (j, i, lower/upper, (fx, fy)) order.

@@ -46,8 +46,17 @@ struct RTRef {
 /// Builds the hierarchical RT_k basis: RT0 facet functions, facet functions
 /// i>=1 from a square constrained solve, divergence-free bubbles and
 /// divergence-reproducing interior functions (inc/fespace.hpp:114-228).
+/// Highest order accepted: 3 as in the reference (inc/fespace.hpp:115); tests
+/// of the device path beyond the reference raise it (orc_set_max_order), the
+/// construction itself being order-generic.
+inline int& max_order() {
+  static int m = 3;
+  return m;
+}
+
 inline RTRef build_rt(int k) {
-  if (k < 0 || k > 3) throw std::invalid_argument("order k must be in 0..3");
+  if (k < 0 || k > max_order())
+    throw std::invalid_argument(max_order() == 3 ? "order k must be in 0..3" : "order k out of range");
   RTRef rt;
   rt.k = k;
   rt.n_facet = k + 1;

@@ -802,7 +802,7 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     throw std::runtime_error("no CUDA device: hpmg has no CPU fallback");
-  if (opt->k < 0 || opt->k > 3) throw std::invalid_argument("order k must be in 0..3");
+  if (opt->k < 0 || opt->k > 6) throw std::invalid_argument("order k must be in 0..6");
   if (md->levels < 1) throw std::invalid_argument("levels must be >= 1");
   C.opt = *opt;
   C.advected = prob && (prob->wind_compound || prob->wind);

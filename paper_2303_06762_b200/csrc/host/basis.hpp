@@ -241,7 +241,7 @@ struct RTBasis {
 };
 
 inline RTBasis build_rt_basis(int k) {
-  if (k < 0 || k > 3) throw std::invalid_argument("order k must be in 0..3");
+  if (k < 0 || k > 6) throw std::invalid_argument("order k must be in 0..6");
   RTBasis B;
   B.k = k;
   B.nfd = k + 1;

@@ -21,7 +21,7 @@ namespace dev {
 #define HPMG_LAUNCH_CHECK()                                                                        \
   do {                                                                                             \
     cudaError_t err__ = cudaGetLastError();                                                        \
-    if (err__ != cudaSuccess) throw std::runtime_error(std::string("CUDA launch: ") + cudaGetErrorString(err__)); \
+    if (err__ != cudaSuccess) throw std::runtime_error(std::string("CUDA launch (") + __func__ + "): " + cudaGetErrorString(err__)); \
   } while (0)
 
 namespace {
@@ -806,6 +806,7 @@ __global__ void k_dot(const double* __restrict__ a, const double* __restrict__ b
 /// Squared L2 norm of an RT velocity field (reference inc/assembly.hpp:487-501):
 /// one thread per element, local coefficients from the compound flux part and
 /// the interior part, sum over the volume nodes of w detJ |J v_hat c / detJ|^2.
+template <int MaxRt>
 __global__ void k_rt_norm2(RefT T, const ElemGeo* __restrict__ geo, int ne, const int* __restrict__ elem_facets,
                            const double* __restrict__ compound, const double* __restrict__ interior, Reduce red,
                            double* out) {
@@ -813,7 +814,7 @@ __global__ void k_rt_norm2(RefT T, const ElemGeo* __restrict__ geo, int ne, cons
   const int nfd = T.nfd, nrt = T.nrt;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x) {
     const ElemGeo& g = geo[e];
-    double c[kMaxRt];
+    double c[MaxRt];
     for (int r = 0; r < nrt; ++r) {
       if (r < 3 * nfd) {
         const int le = r / nfd, i = r % nfd;
@@ -959,6 +960,9 @@ void by_bs(int bs, F&& f) {
     case 4: f(std::integral_constant<int, 4>()); break;
     case 6: f(std::integral_constant<int, 6>()); break;
     case 8: f(std::integral_constant<int, 8>()); break;
+    case 10: f(std::integral_constant<int, 10>()); break;  // k = 4..6: beyond the reference's k <= 3
+    case 12: f(std::integral_constant<int, 12>()); break;
+    case 14: f(std::integral_constant<int, 14>()); break;
     default: throw std::runtime_error("unsupported block size");
   }
 }
@@ -973,7 +977,9 @@ void condense(const RefT& T, const ElemGeo* geo, int ne, CondenseParams prm, con
   const size_t smem = sizeof(double) * condense_scratch(T.ns, T.nv, T.nc, nz, T.nrt, T.nq, T.nqe);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_condense, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, k_condense);  // opt-in maximum minus the kernel's static shared memory
+    cudaFuncSetAttribute(k_condense, cudaFuncAttributeMaxDynamicSharedMemorySize, int(227 * 1024 - fa.sharedSizeBytes));
     attr = true;
   }
   k_condense<<<ne, 128, smem, s>>>(T, geo, prm, load, load_stride, out, T.nc * T.nc + T.nc, wind, mass_field);
@@ -989,7 +995,9 @@ void recover(const RefT& T, const ElemGeo* geo, int ne, CondenseParams prm, cons
       sizeof(double) * (condense_scratch(T.ns, T.nv, T.nc, nz, T.nrt, T.nq, T.nqe) + T.nc + nz + 1 + 4 * T.ns);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_recover, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, k_recover);  // opt-in maximum minus the kernel's static shared memory
+    cudaFuncSetAttribute(k_recover, cudaFuncAttributeMaxDynamicSharedMemorySize, int(227 * 1024 - fa.sharedSizeBytes));
     attr = true;
   }
   k_recover<<<ne, 128, smem, s>>>(T, geo, prm, load, load_stride, elem_facets, nflux, compound, interior, pres, grad,
@@ -1174,7 +1182,10 @@ void sub(double* y, const double* a, const double* b, int64_t n, cudaStream_t s)
 void rt_norm2(const RefT& T, const ElemGeo* geo, int ne, const int* elem_facets, const double* compound,
               const double* interior, const Reduce& red, double* out, cudaStream_t s) {
   if (T.nrt > kMaxRt) throw std::runtime_error("RT space too large for rt_norm2");
-  k_rt_norm2<<<kRedBlocks, 256, 0, s>>>(T, geo, ne, elem_facets, compound, interior, red, out);
+  if (T.nrt <= 24)
+    k_rt_norm2<24><<<kRedBlocks, 256, 0, s>>>(T, geo, ne, elem_facets, compound, interior, red, out);
+  else
+    k_rt_norm2<kMaxRt><<<kRedBlocks, 256, 0, s>>>(T, geo, ne, elem_facets, compound, interior, red, out);
   HPMG_LAUNCH_CHECK();
 }
 void dot(const double* a, const double* b, int64_t n, const Reduce& red, double* out, cudaStream_t s) {

@@ -163,7 +163,7 @@ void sub(double* y, const double* a, const double* b, int64_t n, cudaStream_t s)
 void dot(const double* a, const double* b, int64_t n, const Reduce& red, double* out, cudaStream_t s);
 /// *out = ||u||^2_{L2} of the RT field with compound (flux part, reference
 /// layout) and interior [ne][no] coefficients (reference assembly.hpp:487-501)
-constexpr int kMaxRt = 24;  // 3(k+1) + k(k+1) at k = 3
+constexpr int kMaxRt = 64;  // 3(k+1) + k(k+1) = 63 at k = 6 (kernels specialise k <= 3 at 24)
 void rt_norm2(const RefT& T, const ElemGeo* geo, int ne, const int* elem_facets, const double* compound,
               const double* interior, const Reduce& red, double* out, cudaStream_t s);
 /// Post-processing tables of one order (post.cu; reference inc/postprocess.hpp).

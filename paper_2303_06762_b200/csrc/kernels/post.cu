@@ -8,7 +8,8 @@
 // to three reference matrices (sum_q w a_s a_t, b_s b_t, a_s b_t + b_s a_t)
 // weighted by detJ Ji Ji^T, and two (sum_q w a_s s_m, b_s s_m) contracted with
 // Ji and the gradient coefficients. The (ns_hi-1)^2 SPD system is then
-// Cholesky-solved in registers/local memory (<= 14 unknowns at k = 3).
+// Cholesky-solved in registers/local memory (<= 14 unknowns at k = 3, 35 at
+// k = 6; two size classes).
 //
 // measure_errors: one thread per element over the degree-16 error rule, the
 // exact flow evaluated on the device (manufactured / linear) or read from a
@@ -27,13 +28,14 @@ namespace dev {
 #define HPMG_LAUNCH_CHECK()                                                                        \
   do {                                                                                             \
     cudaError_t err__ = cudaGetLastError();                                                        \
-    if (err__ != cudaSuccess) throw std::runtime_error(std::string("CUDA launch: ") + cudaGetErrorString(err__)); \
+    if (err__ != cudaSuccess) throw std::runtime_error(std::string("CUDA launch (") + __func__ + "): " + cudaGetErrorString(err__)); \
   } while (0)
 
 namespace {
 
-constexpr int kMaxH = 14;  // ns_hi - 1 at k = 3
-constexpr int kMaxS = 10;  // ns at k = 3
+// size classes: k <= 3 (the reference's orders) and k <= 6
+constexpr int kMaxH = 35;  // ns_hi - 1 at k = 6
+constexpr int kMaxS = 28;  // ns at k = 6
 
 __device__ __forceinline__ void local_coeffs(const PostT& P, const ElemGeo& g, int e, const int* elem_facets,
                                              const double* compound, const double* interior, double* c) {
@@ -49,6 +51,7 @@ __device__ __forceinline__ void local_coeffs(const PostT& P, const ElemGeo& g, i
   }
 }
 
+template <int MaxRt, int MaxH>
 __global__ void k_postprocess(PostT P, const ElemGeo* __restrict__ geo, int ne, const int* __restrict__ elem_facets,
                               double nu, const double* __restrict__ compound, const double* __restrict__ interior,
                               const double* __restrict__ grad, double* __restrict__ post) {
@@ -56,7 +59,7 @@ __global__ void k_postprocess(PostT P, const ElemGeo* __restrict__ geo, int ne, 
   if (e >= ne) return;
   const ElemGeo& g = geo[e];
   const int nrt = P.nrt, ns = P.ns, nh = P.nh, m = nh - 1;
-  double c[kMaxRt];
+  double c[MaxRt];
   local_coeffs(P, g, e, elem_facets, compound, interior, c);
   // mean: sum_q w (J v^ c) / detJ = J (Lv c) / detJ
   double l0 = 0.0, l1 = 0.0;
@@ -69,7 +72,7 @@ __global__ void k_postprocess(PostT P, const ElemGeo* __restrict__ geo, int ne, 
   const double mxx = g.detJ * (g.Ji[0] * g.Ji[0] + g.Ji[1] * g.Ji[1]);
   const double myy = g.detJ * (g.Ji[2] * g.Ji[2] + g.Ji[3] * g.Ji[3]);
   const double mxy = g.detJ * (g.Ji[0] * g.Ji[2] + g.Ji[1] * g.Ji[3]);
-  double Lc[kMaxH * (kMaxH + 1) / 2];  // packed lower Cholesky factor, row-major
+  double Lc[MaxH * (MaxH + 1) / 2];  // packed lower Cholesky factor, row-major
   for (int s = 0; s < m; ++s)
     for (int t = 0; t <= s; ++t) {
       const int i = s * m + t;
@@ -93,7 +96,7 @@ __global__ void k_postprocess(PostT P, const ElemGeo* __restrict__ geo, int ne, 
     // rhs_s = -(detJ/nu) sum_m [(Ji00 Ba + Ji10 Bb) G_{comp,x} + (Ji01 Ba + Ji11 Bb) G_{comp,y}]_{s m}
     const double* Gx = G + (2 * comp) * ns;
     const double* Gy = G + (2 * comp + 1) * ns;
-    double y[kMaxH];
+    double y[MaxH];
     for (int s = 0; s < m; ++s) {
       double ax = 0.0, ay = 0.0, bx = 0.0, by = 0.0;
       for (int q = 0; q < ns; ++q) {
@@ -143,6 +146,7 @@ __device__ __forceinline__ void exact_flow(int kind, double x, double y, double*
 
 constexpr int kErrThreads = 128;
 
+template <int MaxRt>
 __global__ void __launch_bounds__(kErrThreads) k_errors(PostT P, const ElemGeo* __restrict__ geo,
                                                         const double* __restrict__ x0, int ne,
                                                         const int* __restrict__ elem_facets, double nu,
@@ -156,7 +160,7 @@ __global__ void __launch_bounds__(kErrThreads) k_errors(PostT P, const ElemGeo* 
   const int nrt = P.nrt, ns = P.ns, nh = P.nh, nq = P.nqe;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x) {
     const ElemGeo& g = geo[e];
-    double c[kMaxRt];
+    double c[MaxRt];
     local_coeffs(P, g, e, elem_facets, compound, interior, c);
     const double* G = grad + size_t(e) * 4 * ns;
     const double* ps = post + size_t(e) * 2 * nh;
@@ -237,7 +241,11 @@ void postprocess(const PostT& P, const ElemGeo* geo, int ne, const int* elem_fac
                  const double* interior, const double* grad, double* post, cudaStream_t s) {
   if (P.nrt > kMaxRt || P.nh - 1 > kMaxH || P.ns > kMaxS) throw std::runtime_error("order too high for postprocess");
   if (ne == 0) return;
-  k_postprocess<<<(ne + 127) / 128, 128, 0, s>>>(P, geo, ne, elem_facets, nu, compound, interior, grad, post);
+  if (P.nrt <= 24 && P.nh - 1 <= 14)
+    k_postprocess<24, 14><<<(ne + 127) / 128, 128, 0, s>>>(P, geo, ne, elem_facets, nu, compound, interior, grad, post);
+  else
+    k_postprocess<kMaxRt, kMaxH><<<(ne + 127) / 128, 128, 0, s>>>(P, geo, ne, elem_facets, nu, compound, interior,
+                                                                   grad, post);
   HPMG_LAUNCH_CHECK();
 }
 
@@ -245,8 +253,12 @@ void measure_errors(const PostT& P, const ElemGeo* geo, const double* x0, int ne
                     const double* compound, const double* interior, const double* grad, const double* post, int kind,
                     const double* ue, const double* ge, double* partial, double* out4, cudaStream_t s) {
   if (P.nrt > kMaxRt || P.ns > kMaxS) throw std::runtime_error("order too high for measure_errors");
-  k_errors<<<kRedBlocks, kErrThreads, 0, s>>>(P, geo, x0, ne, elem_facets, nu, compound, interior, grad, post, kind,
-                                              ue, ge, partial);
+  if (P.nrt <= 24)
+    k_errors<24><<<kRedBlocks, kErrThreads, 0, s>>>(P, geo, x0, ne, elem_facets, nu, compound, interior, grad, post,
+                                                    kind, ue, ge, partial);
+  else
+    k_errors<kMaxRt><<<kRedBlocks, kErrThreads, 0, s>>>(P, geo, x0, ne, elem_facets, nu, compound, interior, grad,
+                                                        post, kind, ue, ge, partial);
   HPMG_LAUNCH_CHECK();
   k_errors_final<<<1, 128, 0, s>>>(partial, kRedBlocks, out4);
   HPMG_LAUNCH_CHECK();

@@ -560,6 +560,18 @@ template <>
 struct RecCfg<8> {
   static constexpr int TP = 128, G = 1;  // two threads per patch row
 };
+template <>
+struct RecCfg<10> {  // k = 4..6 (beyond the reference): one thread per row, np <= 8 * 14
+  static constexpr int TP = 128, G = 1;
+};
+template <>
+struct RecCfg<12> {
+  static constexpr int TP = 128, G = 1;
+};
+template <>
+struct RecCfg<14> {
+  static constexpr int TP = 128, G = 1;
+};
 
 /// dataflow launches carry a fixed per-CTA cost (dependency polls, release
 /// fence), so they group more patches per CTA
@@ -604,6 +616,9 @@ void launch_bs(const PatchRecords& R, int p0, int p1, int nblocks, const SweepOr
     case 4: launch<4, DAG>(R, p0, p1, nblocks, O, D, b, x, s); break;
     case 6: launch<6, DAG>(R, p0, p1, nblocks, O, D, b, x, s); break;
     case 8: launch<8, DAG>(R, p0, p1, nblocks, O, D, b, x, s); break;
+    case 10: launch<10, DAG>(R, p0, p1, nblocks, O, D, b, x, s); break;
+    case 12: launch<12, DAG>(R, p0, p1, nblocks, O, D, b, x, s); break;
+    case 14: launch<14, DAG>(R, p0, p1, nblocks, O, D, b, x, s); break;
     default: throw std::runtime_error("unsupported block size");
   }
 }
@@ -614,6 +629,9 @@ int group_of(int bs, bool dag) {
     case 4: return dag ? Grp<4, true>::G : Grp<4, false>::G;
     case 6: return dag ? Grp<6, true>::G : Grp<6, false>::G;
     case 8: return dag ? Grp<8, true>::G : Grp<8, false>::G;
+    case 10: return dag ? Grp<10, true>::G : Grp<10, false>::G;
+    case 12: return dag ? Grp<12, true>::G : Grp<12, false>::G;
+    case 14: return dag ? Grp<14, true>::G : Grp<14, false>::G;
     default: throw std::runtime_error("unsupported block size");
   }
 }
@@ -708,6 +726,9 @@ void sweep_persistent(const PatchRecords& R, const int* wave_ptr_host, int nwave
     case 4: launch_coop<4>(R, O, nsweeps, b, x, ctl, s); break;
     case 6: launch_coop<6>(R, O, nsweeps, b, x, ctl, s); break;
     case 8: launch_coop<8>(R, O, nsweeps, b, x, ctl, s); break;
+    case 10: launch_coop<10>(R, O, nsweeps, b, x, ctl, s); break;
+    case 12: launch_coop<12>(R, O, nsweeps, b, x, ctl, s); break;
+    case 14: launch_coop<14>(R, O, nsweeps, b, x, ctl, s); break;
     default: throw std::runtime_error("unsupported block size");
   }
 }

@@ -116,6 +116,7 @@ def lib():
         L.orc_mg_errors.argtypes = [P, dp, dp, dp, dp, C.c_int, dp]
         L.orc_mms_point.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, dp]
         L.orc_mg_centroids.argtypes = [P, dp]
+        L.orc_set_max_order.argtypes = [C.c_int]
         _lib = L
     return _lib
 
@@ -308,6 +309,11 @@ class OracleMG:
                             _dp(i if i.size else np.zeros(1)), _dp(np.ascontiguousarray(grad, dtype=np.float64)),
                             _dp(np.ascontiguousarray(post, dtype=np.float64)), kind, _dp(out))
         return dict(zip(("e_u", "e_L", "e_ustar", "div_u"), out))
+
+
+def set_max_order(k):
+    """Highest accepted order (3 = the reference's cap); returns the previous one."""
+    return lib().orc_set_max_order(k)
 
 
 def mms_point(x, y, nu, beta):

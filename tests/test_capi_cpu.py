@@ -44,6 +44,8 @@ def plan(base_n, levels, k, level=-1, mesh="unit_square"):
     (16, 5, 3, 1568768),    # config 2
     (8, 5, 2, 293376),      # config 3, k=2
     (8, 6, 2, 1176576),     # config 5
+    (8, 5, 4, 488960),      # config 3, k=4 (beyond the reference's k <= 3)
+    (8, 5, 6, 684544),      # config 3, k=6
 ])
 def test_config_sizes_and_wave_schedule(base_n, levels, k, n_expect):
     p = plan(base_n, levels, k)

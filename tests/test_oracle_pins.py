@@ -222,3 +222,11 @@ def test_ns_pseudo_time_shares_the_fixed_point():
     plain = O.ns_solve(**kw)
     assert marched["converged"] and plain["converged"]
     assert _field_gap(marched, plain, 0, 2, 2) < 1e-9
+
+
+def test_orders_above_three_rejected_like_the_reference():
+    # inc/fespace.hpp:115: build_rt_reference throws for k > 3; the oracle keeps
+    # that by default (the device tests of k = 4..6 raise the cap explicitly)
+    import pytest as _pytest
+    with _pytest.raises(RuntimeError, match="0..3"):
+        O.OracleMG(base_n=2, levels=2, k=4)
