@@ -233,12 +233,24 @@ std::vector<int> transpose_slots(const host::LevelPlan& P);
 
 /// Structure of one level: plan (patterns, patches, waves), geometry and every
 /// device allocation whose size does not depend on the linearisation state.
-void plan_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, bool finest) {
+/// Development: HPMG_SETUP_TRACE=1 prints setup sub-phase times to stderr.
+struct SetupTrace {
+  bool on = std::getenv("HPMG_SETUP_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[setup] %-28s %8.2f ms\n", what, std::chrono::duration<double>(n - t).count() * 1e3);
+    t = n;
+  }
+};
+
+void plan_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, bool finest, host::LevelPlan&& plan) {
   cudaStream_t s = C.s;
   V.k = k;
   V.bs = 2 * (k + 1);
   V.finest = finest;
-  V.plan = host::make_level(m, k);
+  V.plan = std::move(plan);
   host::set_inverse_layout(V.plan, !C.advected);  // packed symmetric inverses for Stokes
   V.nb = V.plan.nb;
   V.n = V.plan.n();
@@ -837,6 +849,8 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
     C.ref.push_back(std::move(R));
   }
   C.L = md->levels - 1;
+  SetupTrace tr;
+  tr.mark("mesh hierarchy");
   const host::TriMesh& fine = C.mesh[C.L];
   for (int f = 0; f < fine.nf(); ++f)
     if (fine.ftag[f] == host::kTagOutflow) C.enclosed = false;
@@ -848,6 +862,7 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
     tTk = host::build_ref_tensors(k);
     upload_ref(C.refk, *tTk, C.s);
   }
+  tr.mark("reference tensors");
   // reductions and scalars
   C.red.partial = dalloc<double>(dev::kRedBlocks);
   C.red.counter = dalloc<unsigned>(1);
@@ -880,18 +895,38 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
   auto t1 = clk::now();
   // structure of every level
   C.lv.resize(C.L + 1);
-  for (int l = 0; l <= C.L; ++l) {
-    C.lv[l] = std::make_unique<Level>();
-    Level& V = *C.lv[l];
-    const bool finest = (k == 0 && l == C.L);
-    plan_level(C, V, C.mesh[l], 0, finest);
-    V.steps = opt->cycle == HPMG_CYCLE_VARIABLE_V ? (opt->smooth_steps << (C.L - l)) : opt->smooth_steps;
+  {
+    // host plans of all levels (and the order-k head) on concurrent threads
+    std::vector<host::LevelPlan> plans(C.L + 2);
+    std::vector<std::string> errs(C.L + 2);
+    std::vector<std::thread> pool;
+    for (int l = 0; l <= C.L + (k > 0 ? 1 : 0); ++l)
+      pool.emplace_back([&, l] {
+        try {
+          plans[l] = l <= C.L ? host::make_level(C.mesh[l], 0) : host::make_level(fine, k);
+        } catch (const std::exception& e) {
+          errs[l] = e.what();
+        }
+      });
+    for (auto& t : pool) t.join();
+    for (auto& e : errs)
+      if (!e.empty()) throw std::runtime_error(e);
+    tr.mark("dirichlet + level plans");
+    for (int l = 0; l <= C.L; ++l) {
+      C.lv[l] = std::make_unique<Level>();
+      Level& V = *C.lv[l];
+      const bool finest = (k == 0 && l == C.L);
+      plan_level(C, V, C.mesh[l], 0, finest, std::move(plans[l]));
+      V.steps = opt->cycle == HPMG_CYCLE_VARIABLE_V ? (opt->smooth_steps << (C.L - l)) : opt->smooth_steps;
+      tr.mark("level upload");
+    }
+    if (k > 0) {
+      C.head = std::make_unique<Level>();
+      plan_level(C, *C.head, fine, k, true, std::move(plans[C.L + 1]));
+      C.head->steps = opt->smooth_steps;
+    }
   }
-  if (k > 0) {
-    C.head = std::make_unique<Level>();
-    plan_level(C, *C.head, fine, k, true);
-    C.head->steps = opt->smooth_steps;
-  }
+  tr.mark("level uploads");
   C.rhs = dalloc<double>(int64_t(C.free_to_full.size()));
   // everything that depends on the linearisation state
   linearise(C, prob, k > 0 ? tTk.get() : tT0.get());
@@ -908,6 +943,7 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
   C.urhs = dalloc<double>(T.n);
   build_apply_graph(C);
   CK(cudaStreamSynchronize(C.s));
+  tr.mark("workspace + graph");
   auto t6 = clk::now();
   auto sec = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
   C.setup_parts[0] = sec(t0, t1);                      // mesh + tables
@@ -924,6 +960,7 @@ void linearise(hpmg_ctx& C, const hpmg_problem* prob, const host::RefTensors* Tk
   using clk = std::chrono::steady_clock;
   auto sec = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
   const auto t0 = clk::now();
+  SetupTrace tr;
   const int k = C.opt.k;
   const host::TriMesh& fine = C.mesh[C.L];
   std::vector<host::HdgField> adv;
@@ -943,34 +980,74 @@ void linearise(hpmg_ctx& C, const hpmg_problem* prob, const host::RefTensors* Tk
     adv[C.L] = k > 0 ? host::lowest_order(fine, wind_k) : wind_k;
     for (int l = C.L; l > 0; --l) adv[l - 1] = host::restrict_wind(C.mesh[l - 1], C.mesh[l], C.ref[l - 1], adv[l]);
   }
+  // transfer structure (host, first linearisation only) on a helper thread
+  // while the condensation, patch inverses and coarse inverse run on the device
+  static_assert(host::TransferPlan::kColMax == dev::kTransferColMax, "transfer column capacity");
+  const bool need_tp = C.L >= 1 && !C.lv[1]->tdev.base;
+  std::vector<host::TransferPlan> tp(C.L + 1);
+  std::vector<std::string> tp_errs(C.L + 1);
+  std::thread tp_thread;
+  if (need_tp)
+    tp_thread = std::thread([&] {
+      std::vector<std::thread> pool;
+      for (int l = 1; l <= C.L; ++l)
+        pool.emplace_back([&, l] {
+          try {
+            tp[l] = host::transfer_plan(C.lv[l - 1]->plan, C.lv[l]->plan, C.ref[l - 1]);
+          } catch (const std::exception& e) {
+            tp_errs[l] = e.what();
+          }
+        });
+      for (auto& t : pool) t.join();
+    });
+  struct Joiner {
+    std::thread& t;
+    ~Joiner() {
+      if (t.joinable()) t.join();
+    }
+  } joiner{tp_thread};
   for (int l = 0; l <= C.L; ++l)
     linearise_level(C, *C.lv[l], C.mesh[l], C.ref0, prob, C.lv[l]->finest ? C.rhs : nullptr,
                     C.advected ? &adv[l] : nullptr);
   if (k > 0) linearise_level(C, *C.head, fine, C.refk, prob, C.rhs, C.advected ? &wind_k : nullptr);
   CK(cudaStreamSynchronize(C.s));
+  tr.mark("condense + assemble");
   const auto t1 = clk::now();
   for (int l = 1; l <= C.L; ++l) build_patch_inverses(C, *C.lv[l]);
   if (k > 0) build_patch_inverses(C, *C.head);
   CK(cudaStreamSynchronize(C.s));
+  tr.mark("patch inverses + records");
   const auto t2 = clk::now();
-  // transfers: structure once on host threads (one per level), the harmonic
+  // coarse dense inverse: Gauss-Jordan with partial pivoting on the device
+  // (kernels.cu dense_invert), still overlapping the host transfer plans
+  {
+    Level& V0 = *C.lv[0];
+    C.n0 = int(V0.n);
+    std::vector<double> A0 = download_bsr(C, V0), D(size_t(C.n0) * C.n0, 0.0);
+    for (int r = 0; r < V0.nb; ++r)
+      for (int sl = 0; sl < host::kSlots; ++sl) {
+        const int c = V0.plan.cols[size_t(r) * host::kSlots + sl];
+        if (c < 0) continue;
+        for (int i = 0; i < 2; ++i)
+          for (int j = 0; j < 2; ++j)
+            D[size_t(2 * r + i) * C.n0 + 2 * c + j] = A0[((size_t(r) * host::kSlots + sl) * 2 + i) * 2 + j];
+      }
+    double* dA = dupload(D, C.s);
+    if (!C.coarse_inv) C.coarse_inv = dalloc<double>(size_t(C.n0) * C.n0);
+    dev::dense_invert(C.n0, dA, C.coarse_inv, C.s);
+    CK(cudaStreamSynchronize(C.s));
+    cudaFree(dA);
+    if (!C.gemv_work) C.gemv_work = dalloc<double>(size_t(C.n0) * ((C.n0 + 63) / 64 + 1));  // kGemvChunk = 64
+  }
+  tr.mark("coarse inverse");
+  const auto t_coarse = clk::now();
+  // transfers: structure once (the helper thread above), the harmonic
   // correction from the current fine operators on the device
-  static_assert(host::TransferPlan::kColMax == dev::kTransferColMax, "transfer column capacity");
-  if (C.L >= 1 && !C.lv[1]->tdev.base) {
-    std::vector<host::TransferPlan> tp(C.L + 1);
-    std::vector<std::thread> pool;
-    std::vector<std::string> errs(C.L + 1);
-    for (int l = 1; l <= C.L; ++l)
-      pool.emplace_back([&, l] {
-        try {
-          tp[l] = host::transfer_plan(C.lv[l - 1]->plan, C.lv[l]->plan, C.ref[l - 1]);
-        } catch (const std::exception& e) {
-          errs[l] = e.what();
-        }
-      });
-    for (auto& t : pool) t.join();
+  if (need_tp) {
+    tp_thread.join();
+    tr.mark("transfer plans (host wait)");
     for (int l = 1; l <= C.L; ++l) {
-      if (!errs[l].empty()) throw std::runtime_error(errs[l]);
+      if (!tp_errs[l].empty()) throw std::runtime_error(tp_errs[l]);
       Level& V = *C.lv[l];
       const host::TransferPlan& T = tp[l];
       V.Pm = upload_blockcsr(T.P, C.s);
@@ -995,31 +1072,11 @@ void linearise(hpmg_ctx& C, const hpmg_problem* prob, const host::RefTensors* Tk
   }
   for (int l = 1; l <= C.L; ++l) dev::corrected_prolongation(C.lv[l]->A, C.lv[l]->tdev, C.lv[l]->Pm, C.lv[l]->PT, C.s);
   CK(cudaStreamSynchronize(C.s));
-  const auto t3 = clk::now();
-  // coarse dense inverse: Gauss-Jordan with partial pivoting on the device (kernels.cu dense_invert)
-  {
-    Level& V0 = *C.lv[0];
-    C.n0 = int(V0.n);
-    std::vector<double> A0 = download_bsr(C, V0), D(size_t(C.n0) * C.n0, 0.0);
-    for (int r = 0; r < V0.nb; ++r)
-      for (int sl = 0; sl < host::kSlots; ++sl) {
-        const int c = V0.plan.cols[size_t(r) * host::kSlots + sl];
-        if (c < 0) continue;
-        for (int i = 0; i < 2; ++i)
-          for (int j = 0; j < 2; ++j)
-            D[size_t(2 * r + i) * C.n0 + 2 * c + j] = A0[((size_t(r) * host::kSlots + sl) * 2 + i) * 2 + j];
-      }
-    double* dA = dupload(D, C.s);
-    if (!C.coarse_inv) C.coarse_inv = dalloc<double>(size_t(C.n0) * C.n0);
-    dev::dense_invert(C.n0, dA, C.coarse_inv, C.s);
-    CK(cudaStreamSynchronize(C.s));
-    cudaFree(dA);
-    if (!C.gemv_work) C.gemv_work = dalloc<double>(size_t(C.n0) * ((C.n0 + 63) / 64 + 1));  // kGemvChunk = 64
-  }
+  tr.mark("transfer upload + correction");
   const auto t4 = clk::now();
   C.lin_parts[0] = sec(t1, t2);
-  C.lin_parts[1] = sec(t2, t3);
-  C.lin_parts[2] = sec(t3, t4);
+  C.lin_parts[1] = sec(t_coarse, t4);  // transfers: what is left after the overlap
+  C.lin_parts[2] = sec(t2, t_coarse);
   C.lin_parts[3] = sec(t0, t1);
 }
 

@@ -10,6 +10,8 @@
 #pragma once
 
 #include <algorithm>
+#include <climits>
+#include <new>
 #include <array>
 #include <thread>
 #include <vector>
@@ -76,14 +78,48 @@ struct BlockRow {
   }
 };
 
+/// Array of n default-constructed T whose pages are first touched by
+/// parallel_for threads (a serial std::vector<T>(n) of ~100 MB of row
+/// buffers spends most of its time in page faults). T trivially destructible.
+template <class T>
+struct ParArray {
+  T* p = nullptr;
+  int n = 0;
+  explicit ParArray(int count) : p(static_cast<T*>(::operator new(sizeof(T) * size_t(std::max(count, 1))))), n(count) {
+    parallel_for(n, [&](int i) { new (p + i) T(); });
+  }
+  ParArray(const ParArray&) = delete;
+  ParArray& operator=(const ParArray&) = delete;
+  ParArray(ParArray&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  ~ParArray() { ::operator delete(p); }
+  T& operator[](int i) { return p[i]; }
+  const T& operator[](int i) const { return p[i]; }
+};
+
+/// Sorted set of at most N block columns (no values).
+template <int N>
+struct ColRow {
+  int n = 0;
+  int col[N];
+  void add(int c) {
+    int i = 0;
+    while (i < n && col[i] < c) ++i;
+    if (i < n && col[i] == c) return;
+    if (n == N) throw std::runtime_error("transfer row capacity exceeded");
+    for (int j = n; j > i; --j) col[j] = col[j - 1];
+    col[i] = c;
+    ++n;
+  }
+};
+
 constexpr int kAvgCap = 8;   // fine row of the averaging transfer: <= 5 coarse facets
 constexpr int kCorrCap = 16; // corrected row: facets of a coarse element and its neighbours (<= 9)
 
 /// Rows of the averaging transfer (reference inc/transfer.hpp:19-71).
-inline std::vector<BlockRow<kAvgCap>> averaging_blocks(const LevelPlan& C, const LevelPlan& F, const Refinement& R) {
+inline ParArray<BlockRow<kAvgCap>> averaging_blocks(const LevelPlan& C, const LevelPlan& F, const Refinement& R) {
   const TriMesh& cm = *C.mesh;
   const TriMesh& fm = *F.mesh;
-  std::vector<BlockRow<kAvgCap>> rows(F.nb);
+  ParArray<BlockRow<kAvgCap>> rows(F.nb);
   parallel_for(F.nb, [&](int rf) {
     const int ff = F.block_facet[rf];
     int se[2] = {-1, -1};
@@ -199,42 +235,51 @@ inline TransferPlan transfer_plan(const LevelPlan& C, const LevelPlan& F, const 
   // correction columns from the pattern of A and of the averaging rows
   T.ncol.assign(T.nelem, 0);
   T.col.assign(size_t(T.nelem) * TransferPlan::kColMax, -1);
-  std::vector<BlockRow<kCorrCap>> rowcols(F.nb);  // per fine row: correction columns
+  ParArray<ColRow<kCorrCap>> rowcols(F.nb);  // per fine row: correction columns
   // the medial rows of different coarse elements are disjoint
   parallel_for(T.nelem, [&](int e) {
-    BlockRow<kCorrCap> cols;
+    ColRow<kCorrCap> cols;
     for (int i = 0; i < T.nmed[e]; ++i) {
       const int rb = T.med[size_t(e) * 3 + i];
       for (int sl = 0; sl < kSlots; ++sl) {
         const int jb = F.cols[size_t(rb) * kSlots + sl];
         if (jb < 0) continue;
-        for (int q = 0; q < rows[jb].n; ++q) cols.at(rows[jb].col[q]);
+        for (int q = 0; q < rows[jb].n; ++q) cols.add(rows[jb].col[q]);
       }
     }
     T.ncol[e] = cols.n;
     for (int j = 0; j < cols.n; ++j) T.col[size_t(e) * TransferPlan::kColMax + j] = cols.col[j];
     for (int i = 0; i < T.nmed[e]; ++i)
-      for (int j = 0; j < cols.n; ++j) rowcols[T.med[size_t(e) * 3 + i]].at(cols.col[j]);
+      for (int j = 0; j < cols.n; ++j) rowcols[T.med[size_t(e) * 3 + i]].add(cols.col[j]);
   });
-  // final pattern: averaging columns + correction columns per fine row
+  // final pattern: averaging columns + correction columns per fine row (sorted
+  // merge of two small sorted lists; correction-only blocks start at zero)
   T.P.nrows = F.nb;
   T.P.ncols = C.nb;
-  std::vector<BlockRow<kCorrCap>> merged(F.nb);
-  parallel_for(F.nb, [&](int rf) {
-    BlockRow<kCorrCap>& m = merged[rf];
-    for (int q = 0; q < rows[rf].n; ++q) m.at(rows[rf].col[q]) = rows[rf].v[q];
-    for (int q = 0; q < rowcols[rf].n; ++q) m.at(rowcols[rf].col[q]);
-  });
+  std::vector<int> cnt_row(F.nb);
+  auto merge = [&](int rf, int* col, double* val) {
+    const BlockRow<kAvgCap>& a = rows[rf];
+    const ColRow<kCorrCap>& c = rowcols[rf];
+    int i = 0, j = 0, n = 0;
+    while (i < a.n || j < c.n) {
+      const int ca = i < a.n ? a.col[i] : INT_MAX, cc = j < c.n ? c.col[j] : INT_MAX;
+      const int cm = std::min(ca, cc);
+      if (col) {
+        col[n] = cm;
+        for (int t = 0; t < 4; ++t) val[size_t(n) * 4 + t] = ca == cm ? a.v[i][t] : 0.0;
+      }
+      if (ca == cm) ++i;
+      if (cc == cm) ++j;
+      ++n;
+    }
+    return n;
+  };
+  parallel_for(F.nb, [&](int rf) { cnt_row[rf] = merge(rf, nullptr, nullptr); });
   T.P.ptr.assign(F.nb + 1, 0);
-  for (int rf = 0; rf < F.nb; ++rf) T.P.ptr[rf + 1] = T.P.ptr[rf] + merged[rf].n;
+  for (int rf = 0; rf < F.nb; ++rf) T.P.ptr[rf + 1] = T.P.ptr[rf] + cnt_row[rf];
   T.P.col.resize(T.P.ptr[F.nb]);
   T.P.val.resize(size_t(T.P.ptr[F.nb]) * 4);
-  parallel_for(F.nb, [&](int rf) {
-    for (int q = 0; q < merged[rf].n; ++q) {
-      T.P.col[T.P.ptr[rf] + q] = merged[rf].col[q];
-      for (int t = 0; t < 4; ++t) T.P.val[size_t(T.P.ptr[rf] + q) * 4 + t] = merged[rf].v[q][t];
-    }
-  });
+  parallel_for(F.nb, [&](int rf) { merge(rf, &T.P.col[T.P.ptr[rf]], &T.P.val[size_t(T.P.ptr[rf]) * 4]); });
   T.pos.assign(size_t(T.nelem) * 3 * TransferPlan::kColMax, -1);
   parallel_for(T.nelem, [&](int e) {
     for (int i = 0; i < T.nmed[e]; ++i) {

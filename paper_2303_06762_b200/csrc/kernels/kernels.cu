@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -766,6 +767,99 @@ __global__ void k_gj_eliminate(int n, int k, double* __restrict__ aug, const dou
   }
 }
 
+/// Grid barrier of a cooperative launch: ctl[0] counts arrivals within the
+/// launch (release atomic, acquire polls), ctl[1] exits; the last CTA out
+/// resets both for the next launch.
+__device__ __forceinline__ void gj_grid_sync(unsigned* ctl, unsigned i) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned old;
+    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctl) : "memory");
+    const unsigned target = (i + 1u) * gridDim.x;
+    if (old + 1u != target) {
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctl) : "memory");
+      } while (v < target);
+    }
+  }
+  __syncthreads();
+}
+
+/// All n Gauss-Jordan steps in one cooperative launch: per step, block 0
+/// pivots (the k_gj_pivot arithmetic), a grid barrier, every block
+/// eliminates (k_gj_eliminate's), a grid barrier. Same operations in the same
+/// order as the two-kernel loop, without its 2n launches.
+__global__ void __launch_bounds__(256) k_gj_coop(int n, double* __restrict__ aug, double* __restrict__ rowk,
+                                                 double* __restrict__ colk, int* __restrict__ status, unsigned* ctl) {
+  __shared__ double bv[32];
+  __shared__ int bi[32];
+  const int w = 2 * n;
+  unsigned bar = 0;
+  for (int k = 0; k < n; ++k) {
+    if (blockIdx.x == 0) {
+      double best = -1.0;
+      int besti = k;
+      for (int i = k + threadIdx.x; i < n; i += blockDim.x) {
+        const double v = fabs(__ldcg(aug + size_t(i) * w + k));
+        if (v > best) { best = v; besti = i; }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, besti, o);
+        if (ob > best || (ob == best && oi < besti)) { best = ob; besti = oi; }
+      }
+      if ((threadIdx.x & 31) == 0) { bv[threadIdx.x >> 5] = best; bi[threadIdx.x >> 5] = besti; }
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        const int nw = blockDim.x >> 5;
+        best = threadIdx.x < nw ? bv[threadIdx.x] : -1.0;
+        besti = threadIdx.x < nw ? bi[threadIdx.x] : n;
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, besti, o);
+          if (ob > best || (ob == best && oi < besti)) { best = ob; besti = oi; }
+        }
+        if (threadIdx.x == 0) { bi[0] = besti; bv[0] = best; }
+      }
+      __syncthreads();
+      const int p = bi[0];
+      if (threadIdx.x == 0 && !(bv[0] > 0.0)) *status = 1;  // singular
+      for (int j = threadIdx.x; j < w; j += blockDim.x) {
+        const double a = __ldcg(aug + size_t(k) * w + j), b = __ldcg(aug + size_t(p) * w + j);
+        __stcg(aug + size_t(k) * w + j, b);
+        __stcg(aug + size_t(p) * w + j, a);
+        __stcg(rowk + j, b);
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += blockDim.x)
+        __stcg(colk + i, i == k ? 0.0 : __ldcg(aug + size_t(i) * w + k));
+    }
+    gj_grid_sync(ctl, bar++);
+    const double inv = 1.0 / __ldcg(rowk + k);
+    // left-part columns j < k are already eliminated (rowk[j] = 0 there, so
+    // the update would leave them unchanged): only j in [k, 2n) is touched
+    const int span = w - k;
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+      const double ci = __ldcg(colk + i);
+      double* row = aug + size_t(i) * w + k;
+      for (int jj = threadIdx.x; jj < span; jj += blockDim.x) {
+        const double r = __ldcg(rowk + k + jj) * inv;
+        __stcg(row + jj, i == k ? r : __ldcg(row + jj) - ci * r);
+      }
+    }
+    gj_grid_sync(ctl, bar++);
+  }
+  if (threadIdx.x == 0) {
+    unsigned old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctl + 1) : "memory");
+    if (old + 1u == gridDim.x) {
+      ctl[0] = 0u;
+      ctl[1] = 0u;
+    }
+  }
+}
+
 __global__ void k_gj_extract(int n, const double* __restrict__ aug, double* __restrict__ inv) {
   const int64_t tot = int64_t(n) * n;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
@@ -1147,10 +1241,36 @@ void dense_invert(int n, const double* A_rowmajor, double* inv_colmajor, cudaStr
   cudaMemsetAsync(status, 0, sizeof(int), s);
   const int64_t tot = int64_t(n) * 2 * n;
   k_gj_init<<<grid_for(tot, 256), 256, 0, s>>>(n, A_rowmajor, aug);
-  for (int k = 0; k < n; ++k) {
-    k_gj_pivot<<<1, 1024, 0, s>>>(n, k, aug, rowk, colk, status);
-    k_gj_eliminate<<<grid_for(tot, 256), 256, 0, s>>>(n, k, aug, rowk, colk);
+  // one cooperative launch for all steps when the grid can be co-resident
+  int per_sm = 0, dev = 0, sms = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gj_coop, 256, 0);
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  unsigned* ctl = nullptr;
+  bool coop = per_sm > 0 && cudaMalloc(&ctl, 2 * sizeof(unsigned)) == cudaSuccess;
+  if (coop) {
+    cudaMemsetAsync(ctl, 0, 2 * sizeof(unsigned), s);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(std::min<int64_t>(int64_t(per_sm) * sms, n)));  // a block per row at most
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t le = cudaLaunchKernelEx(&cfg, k_gj_coop, n, aug, rowk, colk, status, ctl);
+    coop = le == cudaSuccess;
+    if (!coop) cudaGetLastError();
+    if (std::getenv("HPMG_SETUP_TRACE"))
+      std::fprintf(stderr, "[setup] coarse GJ: n %d, cooperative %d (%s), grid %u\n", n, int(coop),
+                   cudaGetErrorString(le), cfg.gridDim.x);
   }
+  if (!coop)
+    for (int k = 0; k < n; ++k) {
+      k_gj_pivot<<<1, 1024, 0, s>>>(n, k, aug, rowk, colk, status);
+      k_gj_eliminate<<<grid_for(tot, 256), 256, 0, s>>>(n, k, aug, rowk, colk);
+    }
   k_gj_extract<<<grid_for(int64_t(n) * n, 256), 256, 0, s>>>(n, aug, inv_colmajor);
   HPMG_LAUNCH_CHECK();
   int hs = 0;
@@ -1160,6 +1280,7 @@ void dense_invert(int n, const double* A_rowmajor, double* inv_colmajor, cudaStr
   cudaFree(rowk);
   cudaFree(colk);
   cudaFree(status);
+  if (ctl) cudaFree(ctl);
   if (hs) throw std::runtime_error("singular coarse operator");
 }
 
