@@ -236,7 +236,18 @@ def run_hpmg(args, rank, world, local, dist):
         pass
     # operator apply (finest condensed operator, k_spmv) against the same peak
     ms_spmv, spmv_bytes, spmv_ref_bytes = B.time_spmv(max(10, args.steps))
-    # time-to-solution: device Uzawa (2 outer PCG solves to 1e-8)
+    # time-to-solution: device Uzawa (2 outer PCG solves to 1e-8); the setup is
+    # timed again on a second context (the first one in a process also pays
+    # the one-time CUDA module loading)
+    t0 = time.perf_counter()
+    B2 = H.MGPreconditioner(mesh="unit_square", base_n=cfg["base_n"], levels=cfg["levels"], k=cfg["k"],
+                            nu=cfg["nu"], beta=cfg["beta"], inv_eps=cfg["inv_eps"], cycle=H.CYCLE_V,
+                            smoother=H.SMOOTH_MULTIPLICATIVE, smooth_steps=1, structured_load=(n_f, F))
+    setup_warm = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    sol2 = H.uzawa_solve(B2)
+    solve_wall = time.perf_counter() - t0
+    B2.close()
     sol = H.uzawa_solve(B)
     launches = B.launches_per_apply()
     out = None
@@ -290,6 +301,10 @@ def run_hpmg(args, rank, world, local, dist):
                                "frac": spmv_bytes / (ms_spmv * 1e-3) / 1e9 / hbm if ms_spmv > 0 else None,
                                "reference_storage_bytes": spmv_ref_bytes},
             "tts": {"uzawa_device_s": sol.report.seconds, "setup_wall_s": setup_wall,
+                    "setup_wall_warm_s": setup_warm, "uzawa_wall_s": solve_wall,
+                    "tts_warm_s": setup_warm + solve_wall,
+                    "tts_note": "tts_warm_s = setup (second context in the process) + AL-Uzawa wall time "
+                                "(2 outer PCG solves to 1e-8, velocity and pressure back on the host)",
                     "setup_parts_s": [float(x) for x in setup_parts[:7]],
                     "inner_iterations": sol.report.inner_iterations,
                     "final_divergence": sol.report.final_divergence, "converged": sol.report.converged},
