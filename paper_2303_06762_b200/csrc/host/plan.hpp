@@ -14,7 +14,10 @@
 #include <algorithm>
 #include <array>
 #include <cstdint>
+#include <exception>
 #include <functional>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include "../kernels/condense.cuh"
@@ -27,6 +30,39 @@ constexpr int kSlots = 5;      // self + 4 neighbours: a facet touches <= 2 tria
 constexpr int kMaxPatchF = 8;  // facets per vertex patch supported by the kernels
 
 using Field = std::function<void(double x, double y, double* out2)>;
+
+/// Static-chunked parallel loop over [0, n) on up to 16 host threads (setup);
+/// the first exception thrown by any iteration is rethrown after the join.
+template <class F>
+inline void parallel_for(int n, F&& f) {
+  const int nt = std::max(1, std::min<int>({16, int(std::thread::hardware_concurrency()), n / 2048 + 1}));
+  if (nt == 1) {
+    for (int i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::exception_ptr err;
+  std::mutex mu;
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nt; ++t)
+    pool.emplace_back([&, t] {
+      try {
+        const int a = int(int64_t(n) * t / nt), b = int(int64_t(n) * (t + 1) / nt);
+        for (int i = a; i < b; ++i) f(i);
+      } catch (...) {
+        std::lock_guard<std::mutex> lock(mu);
+        if (!err) err = std::current_exception();
+      }
+    });
+  for (auto& th : pool) th.join();
+  if (err) std::rethrow_exception(err);
+}
+
+/// Compressed adjacency built from (key, value) pairs in input order.
+struct Csr32 {
+  std::vector<int> ptr, val;
+  const int* begin(int i) const { return val.data() + ptr[i]; }
+  const int* end(int i) const { return val.data() + ptr[i + 1]; }
+};
 
 /// Reference edge lengths: edge 0 = (1,0)-(0,1), edges 1, 2 unit.
 inline double ref_edge_len(int le) { return le == 0 ? std::sqrt(2.0) : 1.0; }
@@ -109,9 +145,9 @@ inline LevelPlan make_level(const TriMesh& m, int k) {
   L.cols.assign(size_t(L.nb) * kSlots, -1);
   L.gath.assign(size_t(L.nb) * kSlots * 6, -1);
   L.row_elems.assign(size_t(L.nb) * 4, -1);
-  for (int r = 0; r < L.nb; ++r) {
+  parallel_for(L.nb, [&](int r) {
     const int f = L.block_facet[r];
-    std::vector<int> nb;
+    int nbv[6], nnb = 0;  // facets of the <= 2 elements of f, then sorted unique
     int slot_e = 0;
     for (int s = 0; s < 2; ++s) {
       const int e = m.fe[f][s];
@@ -120,12 +156,12 @@ inline LevelPlan make_level(const TriMesh& m, int k) {
       slot_e++;
       for (int lf = 0; lf < 3; ++lf) {
         int g = L.facet_block[m.ef[e][lf]];
-        if (g >= 0) nb.push_back(g);
+        if (g >= 0) nbv[nnb++] = g;
       }
     }
-    std::sort(nb.begin(), nb.end());
-    nb.erase(std::unique(nb.begin(), nb.end()), nb.end());
-    if (int(nb.size()) > kSlots) throw std::runtime_error("facet couples to more than 5 facets");
+    std::sort(nbv, nbv + nnb);
+    nnb = int(std::unique(nbv, nbv + nnb) - nbv);
+    if (nnb > kSlots) throw std::runtime_error("facet couples to more than 5 facets");
     std::array<int, 2> es = {m.fe[f][0], m.fe[f][1]};
     if (es[1] >= 0 && es[1] < es[0]) std::swap(es[0], es[1]);
     int re = 0;
@@ -138,8 +174,8 @@ inline LevelPlan make_level(const TriMesh& m, int k) {
       L.row_elems[size_t(r) * 4 + 2 * re + 1] = lf;
       ++re;
     }
-    for (size_t s = 0; s < nb.size(); ++s) {
-      const int c = nb[s];
+    for (int s = 0; s < nnb; ++s) {
+      const int c = nbv[s];
       L.cols[size_t(r) * kSlots + s] = c;
       const int gf = L.block_facet[c];
       int cnt = 0;
@@ -159,27 +195,46 @@ inline LevelPlan make_level(const TriMesh& m, int k) {
       }
     }
     (void)slot_e;
-  }
+  });
   // vertex patches: facets incident to each vertex in facet order (inc/mesh.hpp:301-308)
-  std::vector<std::vector<int>> vp(m.nv());
+  Csr32 vp;  // vertex -> incident facets (ascending facet id)
+  Csr32 nbr;  // vertex -> mesh neighbours (the other end of those facets)
+  vp.ptr.assign(m.nv() + 1, 0);
   for (int f = 0; f < m.nf(); ++f) {
-    vp[m.fa[f]].push_back(f);
-    vp[m.fb[f]].push_back(f);
+    ++vp.ptr[m.fa[f] + 1];
+    ++vp.ptr[m.fb[f] + 1];
+  }
+  for (int v = 0; v < m.nv(); ++v) vp.ptr[v + 1] += vp.ptr[v];
+  vp.val.resize(vp.ptr[m.nv()]);
+  nbr.ptr = vp.ptr;
+  nbr.val.resize(vp.val.size());
+  {
+    std::vector<int> at(vp.ptr.begin(), vp.ptr.end() - 1);
+    for (int f = 0; f < m.nf(); ++f) {
+      const int a = at[m.fa[f]]++, b = at[m.fb[f]]++;
+      vp.val[a] = f;
+      nbr.val[a] = m.fb[f];
+      vp.val[b] = f;
+      nbr.val[b] = m.fa[f];
+    }
   }
   std::vector<int> vertex_patch(m.nv(), -1);
   L.facet_patches.assign(size_t(L.nb) * 2, -1);
   for (int v = 0; v < m.nv(); ++v) {
-    std::vector<int> blocks;
-    for (int f : vp[v])
-      if (L.facet_block[f] >= 0) blocks.push_back(L.facet_block[f]);
-    if (blocks.empty()) continue;
-    if (int(blocks.size()) > kMaxPatchF) throw std::runtime_error("vertex patch larger than supported");
+    int blocks[kMaxPatchF], nblk = 0;
+    for (const int* fp = vp.begin(v); fp != vp.end(v); ++fp)
+      if (L.facet_block[*fp] >= 0) {
+        if (nblk == kMaxPatchF) throw std::runtime_error("vertex patch larger than supported");
+        blocks[nblk++] = L.facet_block[*fp];
+      }
+    if (nblk == 0) continue;
     const int p = L.npatch++;
     vertex_patch[v] = p;
-    L.patch_nf.push_back(int(blocks.size()));
-    L.max_patch_f = std::max(L.max_patch_f, int(blocks.size()));
-    for (int q = 0; q < kMaxPatchF; ++q) L.patch_fac.push_back(q < int(blocks.size()) ? blocks[q] : -1);
-    for (int b : blocks) {
+    L.patch_nf.push_back(nblk);
+    L.max_patch_f = std::max(L.max_patch_f, nblk);
+    for (int q = 0; q < kMaxPatchF; ++q) L.patch_fac.push_back(q < nblk ? blocks[q] : -1);
+    for (int bi = 0; bi < nblk; ++bi) {
+      const int b = blocks[bi];
       int* fp = &L.facet_patches[size_t(b) * 2];
       if (fp[0] < 0) fp[0] = p;
       else fp[1] = p;
@@ -188,18 +243,13 @@ inline LevelPlan make_level(const TriMesh& m, int k) {
   // exact wave schedule of the ascending-vertex sweep: depth(v) = 1 + max depth
   // of mesh neighbours u < v owning a patch. Same-depth
   // patches share no DOF and no operator coupling.
-  std::vector<std::vector<int>> nbr(m.nv());
-  for (int f = 0; f < m.nf(); ++f) {
-    nbr[m.fa[f]].push_back(m.fb[f]);
-    nbr[m.fb[f]].push_back(m.fa[f]);
-  }
   std::vector<int> depth(m.nv(), -1);
   int maxd = -1;
   for (int v = 0; v < m.nv(); ++v) {
     if (vertex_patch[v] < 0) continue;
     int d = 0;
-    for (int u : nbr[v])
-      if (u < v && vertex_patch[u] >= 0) d = std::max(d, depth[u] + 1);
+    for (const int* up = nbr.begin(v); up != nbr.end(v); ++up)
+      if (*up < v && vertex_patch[*up] >= 0) d = std::max(d, depth[*up] + 1);
     depth[v] = d;
     maxd = std::max(maxd, d);
   }
@@ -227,22 +277,28 @@ inline LevelPlan make_level(const TriMesh& m, int k) {
   for (auto& fp : L.facet_patches)
     if (fp >= 0) fp = newid[fp];
   {
-    std::vector<std::vector<int>> dep(L.npatch);
-    for (int v = 0; v < m.nv(); ++v) {
-      if (vertex_patch[v] < 0) continue;
-      auto& d = dep[newid[vertex_patch[v]]];
-      for (int u : nbr[v])
-        if (vertex_patch[u] >= 0) d.push_back(newid[vertex_patch[u]]);
-      std::sort(d.begin(), d.end());
-      d.erase(std::unique(d.begin(), d.end()), d.end());
-      L.max_dep = std::max(L.max_dep, int(d.size()));
-    }
+    // neighbour patches of every patch, sorted unique (<= 16: vertex degree)
+    constexpr int kDepCap = 16;
+    std::vector<int> tmp(size_t(L.npatch) * kDepCap, -1);
     L.patch_ndep.assign(L.npatch, 0);
+    parallel_for(m.nv(), [&](int v) {
+      if (vertex_patch[v] < 0) return;
+      const int p = newid[vertex_patch[v]];
+      int* d = &tmp[size_t(p) * kDepCap];
+      int nd = 0;
+      for (const int* up = nbr.begin(v); up != nbr.end(v); ++up)
+        if (vertex_patch[*up] >= 0) {
+          if (nd == kDepCap) throw std::runtime_error("vertex degree too large for the dependency lists");
+          d[nd++] = newid[vertex_patch[*up]];
+        }
+      std::sort(d, d + nd);
+      L.patch_ndep[p] = int(std::unique(d, d + nd) - d);
+    });
+    for (int p = 0; p < L.npatch; ++p) L.max_dep = std::max(L.max_dep, L.patch_ndep[p]);
     L.patch_dep.assign(size_t(L.npatch) * std::max(L.max_dep, 1), -1);
-    for (int p = 0; p < L.npatch; ++p) {
-      L.patch_ndep[p] = int(dep[p].size());
-      for (size_t i = 0; i < dep[p].size(); ++i) L.patch_dep[size_t(p) * L.max_dep + i] = dep[p][i];
-    }
+    parallel_for(L.npatch, [&](int p) {
+      for (int i = 0; i < L.patch_ndep[p]; ++i) L.patch_dep[size_t(p) * L.max_dep + i] = tmp[size_t(p) * kDepCap + i];
+    });
   }
   for (int q = 0; q < L.npatch; ++q) L.wave_patch[q] = q;
   set_inverse_layout(L, true);

@@ -21,23 +21,6 @@
 namespace hpmg {
 namespace host {
 
-/// Static-chunked parallel loop over [0, n) on up to 16 host threads (setup).
-template <class F>
-inline void parallel_for(int n, F&& f) {
-  const int nt = std::max(1, std::min<int>({16, int(std::thread::hardware_concurrency()), n / 2048 + 1}));
-  if (nt == 1) {
-    for (int i = 0; i < n; ++i) f(i);
-    return;
-  }
-  std::vector<std::thread> pool;
-  for (int t = 0; t < nt; ++t)
-    pool.emplace_back([&, t] {
-      const int a = int(int64_t(n) * t / nt), b = int(int64_t(n) * (t + 1) / nt);
-      for (int i = a; i < b; ++i) f(i);
-    });
-  for (auto& th : pool) th.join();
-}
-
 struct BlockCsrH {
   int nrows = 0, ncols = 0;
   std::vector<int> ptr{0}, col;
