@@ -37,6 +37,23 @@ namespace {
 
 thread_local std::string g_last_error;
 
+/// Owning device buffer for the temporaries of one C-ABI call (freed on every
+/// exit path, including a CUDA error thrown half-way).
+struct DevTemps {
+  std::vector<void*> ptrs;
+  DevTemps() = default;
+  DevTemps(const DevTemps&) = delete;
+  DevTemps& operator=(const DevTemps&) = delete;
+  ~DevTemps() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+  template <typename T>
+  T* add(T* p) {
+    ptrs.push_back(p);
+    return p;
+  }
+};
+
 template <typename T>
 T* dalloc(size_t n) {
   void* p = nullptr;
@@ -1032,11 +1049,11 @@ void linearise(hpmg_ctx& C, const hpmg_problem* prob, const host::RefTensors* Tk
           for (int j = 0; j < 2; ++j)
             D[size_t(2 * r + i) * C.n0 + 2 * c + j] = A0[((size_t(r) * host::kSlots + sl) * 2 + i) * 2 + j];
       }
-    double* dA = dupload(D, C.s);
+    DevTemps tmp;
+    double* dA = tmp.add(dupload(D, C.s));
     if (!C.coarse_inv) C.coarse_inv = dalloc<double>(size_t(C.n0) * C.n0);
     dev::dense_invert(C.n0, dA, C.coarse_inv, C.s);
     CK(cudaStreamSynchronize(C.s));
-    cudaFree(dA);
     if (!C.gemv_work) C.gemv_work = dalloc<double>(size_t(C.n0) * ((C.n0 + 63) / 64 + 1));  // kGemvChunk = 64
   }
   tr.mark("coarse inverse");
@@ -1521,15 +1538,14 @@ double hpmg_rt_l2_norm(hpmg_ctx* ctx, const double* compound_full, const double*
     Level& T = C.top();
     const DevRef& R = C.opt.k > 0 ? C.refk : C.ref0;
     const size_t nfull = C.g_full.size(), ni = size_t(T.ne) * R.T.no;
-    double* comp = dalloc<double>(nfull);
-    double* di = dalloc<double>(std::max<size_t>(ni, 1));
+    DevTemps tmp;
+    double* comp = tmp.add(dalloc<double>(nfull));
+    double* di = tmp.add(dalloc<double>(std::max<size_t>(ni, 1)));
     CK(cudaMemcpyAsync(comp, compound_full, sizeof(double) * nfull, cudaMemcpyHostToDevice, C.s));
     if (ni) CK(cudaMemcpyAsync(di, interior, sizeof(double) * ni, cudaMemcpyHostToDevice, C.s));
     dev::rt_norm2(R.T, T.geo, T.ne, T.elem_facets, comp, di, C.red, C.sc + S_TMP, C.s);
     read_scalars(C);
     out = std::sqrt(C.sc_host[S_TMP]);
-    cudaFree(comp);
-    cudaFree(di);
   });
   return rc == 0 ? out : -1.0;
 }
@@ -1541,10 +1557,11 @@ int hpmg_recover(hpmg_ctx* ctx, const double* velocity_full, double* interior, d
     const DevRef& R = C.opt.k > 0 ? C.refk : C.ref0;
     const int ne = T.ne, no = R.T.no, np = R.T.ns - 1, ng = 4 * R.T.ns;
     const size_t nfull = C.g_full.size();
-    double* comp = dalloc<double>(nfull);
-    double* di = dalloc<double>(size_t(ne) * std::max(no, 1));
-    double* dp = dalloc<double>(size_t(ne) * std::max(np, 1));
-    double* dg = dalloc<double>(size_t(ne) * ng);
+    DevTemps tmp;
+    double* comp = tmp.add(dalloc<double>(nfull));
+    double* di = tmp.add(dalloc<double>(size_t(ne) * std::max(no, 1)));
+    double* dp = tmp.add(dalloc<double>(size_t(ne) * std::max(np, 1)));
+    double* dg = tmp.add(dalloc<double>(size_t(ne) * ng));
     CK(cudaMemcpyAsync(comp, velocity_full, sizeof(double) * nfull, cudaMemcpyHostToDevice, C.s));
     dev::recover(R.T, T.geo, ne, C.fine_prm, C.fine_load, C.fine_lstride, T.elem_facets, (long long)(nfull / 2), comp,
                  di, dp, dg, C.s, C.fine_wind, C.fine_mass);
@@ -1552,7 +1569,6 @@ int hpmg_recover(hpmg_ctx* ctx, const double* velocity_full, double* interior, d
     if (np) CK(cudaMemcpyAsync(p_ortho, dp, sizeof(double) * ne * np, cudaMemcpyDeviceToHost, C.s));
     CK(cudaMemcpyAsync(grad, dg, sizeof(double) * ne * ng, cudaMemcpyDeviceToHost, C.s));
     CK(cudaStreamSynchronize(C.s));
-    for (double* p : {comp, di, dp, dg}) cudaFree(p);
   });
 }
 
@@ -1611,17 +1627,17 @@ int hpmg_postprocess(hpmg_ctx* ctx, const double* velocity_full, const double* i
     const dev::PostT& P = post_tables(C);
     const int ne = T.ne;
     const size_t nfull = C.g_full.size(), ni = size_t(ne) * P.no, ng = size_t(ne) * 4 * P.ns, np = size_t(ne) * 2 * P.nh;
-    double* comp = dalloc<double>(nfull);
-    double* di = dalloc<double>(std::max<size_t>(ni, 1));
-    double* dg = dalloc<double>(ng);
-    double* dp = dalloc<double>(np);
+    DevTemps tmp;
+    double* comp = tmp.add(dalloc<double>(nfull));
+    double* di = tmp.add(dalloc<double>(std::max<size_t>(ni, 1)));
+    double* dg = tmp.add(dalloc<double>(ng));
+    double* dp = tmp.add(dalloc<double>(np));
     CK(cudaMemcpyAsync(comp, velocity_full, sizeof(double) * nfull, cudaMemcpyHostToDevice, C.s));
     if (ni) CK(cudaMemcpyAsync(di, interior, sizeof(double) * ni, cudaMemcpyHostToDevice, C.s));
     CK(cudaMemcpyAsync(dg, grad, sizeof(double) * ng, cudaMemcpyHostToDevice, C.s));
     dev::postprocess(P, T.geo, ne, T.elem_facets, C.opt.nu, comp, di, dg, dp, C.s);
     CK(cudaMemcpyAsync(post, dp, sizeof(double) * np, cudaMemcpyDeviceToHost, C.s));
     CK(cudaStreamSynchronize(C.s));
-    for (double* p : {comp, di, dg, dp}) cudaFree(p);
   });
 }
 
@@ -1639,12 +1655,8 @@ int hpmg_measure_errors(hpmg_ctx* ctx, const double* velocity_full, const double
     if (u_exact == hpmg_field_mms_velocity && grad_exact == hpmg_tensor_mms_gradient) kind = 1;
     if (u_exact == hpmg_field_linear_flow && grad_exact == hpmg_tensor_linear_flow_gradient) kind = 2;
     const size_t nfull = C.g_full.size(), ni = size_t(ne) * P.no, ng = size_t(ne) * 4 * P.ns, np = size_t(ne) * 2 * P.nh;
-    std::vector<void*> tmp;
-    auto alloc = [&](size_t n) {
-      double* p = dalloc<double>(std::max<size_t>(n, 1));
-      tmp.push_back(p);
-      return p;
-    };
+    DevTemps tmp;
+    auto alloc = [&](size_t n) { return tmp.add(dalloc<double>(std::max<size_t>(n, 1))); };
     double *comp = alloc(nfull), *di = alloc(ni), *dg = alloc(ng), *dp = alloc(np), *ue = nullptr, *ge = nullptr;
     CK(cudaMemcpyAsync(comp, velocity_full, sizeof(double) * nfull, cudaMemcpyHostToDevice, C.s));
     if (ni) CK(cudaMemcpyAsync(di, interior, sizeof(double) * ni, cudaMemcpyHostToDevice, C.s));
@@ -1679,7 +1691,6 @@ int hpmg_measure_errors(hpmg_ctx* ctx, const double* velocity_full, const double
                         partial + 4 * dev::kRedBlocks, C.s);
     CK(cudaMemcpyAsync(out, partial + 4 * dev::kRedBlocks, sizeof(double) * 4, cudaMemcpyDeviceToHost, C.s));
     CK(cudaStreamSynchronize(C.s));
-    for (void* p : tmp) cudaFree(p);
   });
 }
 

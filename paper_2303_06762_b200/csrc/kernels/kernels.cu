@@ -1234,6 +1234,15 @@ void dense_gemv(int n, const double* inv, const double* b, double* x, double* wo
 void dense_invert(int n, const double* A_rowmajor, double* inv_colmajor, cudaStream_t s) {
   double *aug = nullptr, *rowk = nullptr, *colk = nullptr;
   int* status = nullptr;
+  unsigned* ctl = nullptr;
+  struct Free {  // scratch released on every exit path (launch errors throw)
+    void** p[5];
+    ~Free() {
+      for (void** q : p)
+        if (*q) cudaFree(*q);
+    }
+  } release{{reinterpret_cast<void**>(&aug), reinterpret_cast<void**>(&rowk), reinterpret_cast<void**>(&colk),
+             reinterpret_cast<void**>(&status), reinterpret_cast<void**>(&ctl)}};
   if (cudaMalloc(&aug, sizeof(double) * size_t(n) * 2 * n) != cudaSuccess ||
       cudaMalloc(&rowk, sizeof(double) * 2 * n) != cudaSuccess || cudaMalloc(&colk, sizeof(double) * n) != cudaSuccess ||
       cudaMalloc(&status, sizeof(int)) != cudaSuccess)
@@ -1246,7 +1255,6 @@ void dense_invert(int n, const double* A_rowmajor, double* inv_colmajor, cudaStr
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gj_coop, 256, 0);
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  unsigned* ctl = nullptr;
   bool coop = per_sm > 0 && cudaMalloc(&ctl, 2 * sizeof(unsigned)) == cudaSuccess;
   if (coop) {
     cudaMemsetAsync(ctl, 0, 2 * sizeof(unsigned), s);
@@ -1276,11 +1284,7 @@ void dense_invert(int n, const double* A_rowmajor, double* inv_colmajor, cudaStr
   int hs = 0;
   cudaMemcpyAsync(&hs, status, sizeof(int), cudaMemcpyDeviceToHost, s);
   cudaStreamSynchronize(s);
-  cudaFree(aug);
-  cudaFree(rowk);
-  cudaFree(colk);
-  cudaFree(status);
-  if (ctl) cudaFree(ctl);
+
   if (hs) throw std::runtime_error("singular coarse operator");
 }
 
