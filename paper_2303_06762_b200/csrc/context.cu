@@ -604,16 +604,19 @@ void h_cycle(hpmg_ctx& C, int l, const double* b, double* x) {
     count(C, 2);
     return;
   }
-  dev::fill(x, 0.0, V.n, C.s);
-  count(C);
+  // x = 0 was written by the kernel that produced b (restriction / E^T injection)
   smooth(C, V, x, b, false);
   dev::spmv(V.A, x, b, V.r, 1, nullptr, nullptr, C.s);
-  dev::restrict_(V.PT, V.r, W.b, C.s);
+  dev::restrict_(V.PT, V.r, W.b, C.s, l - 1 > 0 ? W.x : nullptr);
   count(C, 2);
   h_cycle(C, l - 1, W.b, W.x);
   for (int i = 1; i < q; ++i) {
     dev::spmv(W.A, W.x, W.b, W.bw, 1, nullptr, nullptr, C.s);
     count(C);
+    if (l - 1 > 0) {  // h_cycle expects x = 0 on entry
+      dev::fill(W.xw, 0.0, W.n, C.s);
+      count(C);
+    }
     h_cycle(C, l - 1, W.bw, W.xw);
     dev::axpy(W.x, 1.0, W.xw, W.n, C.s);
     count(C);
@@ -626,6 +629,11 @@ void h_cycle(hpmg_ctx& C, int l, const double* b, double* x) {
 /// apply(b) -> x on the finest system, block layout (inc/multigrid.hpp:117-128)
 void apply_blocks(hpmg_ctx& C, const double* b, double* x) {
   if (C.opt.k == 0) {
+    if (C.L > 0 && !(C.lv[C.L]->small && C.opt.smoother == HPMG_SMOOTH_MULTIPLICATIVE &&
+                     C.opt.cycle != HPMG_CYCLE_W)) {
+      dev::fill(x, 0.0, C.lv[C.L]->n, C.s);  // h_cycle expects x = 0 on entry (restriction zeroes it below)
+      count(C);
+    }
     h_cycle(C, C.L, b, x);
     return;
   }
@@ -634,7 +642,7 @@ void apply_blocks(hpmg_ctx& C, const double* b, double* x) {
   dev::fill(x, 0.0, H.n, C.s);
   count(C);
   smooth(C, H, x, b, false);
-  dev::inject_residual(H.A, x, b, F.b, C.s);
+  dev::inject_residual(H.A, x, b, F.b, C.s, F.x);
   count(C);
   h_cycle(C, C.L, F.b, F.x);
   dev::embed_add(H.nb, H.bs, F.x, x, C.s);
@@ -1787,7 +1795,7 @@ double hpmg_time_apply(hpmg_ctx* ctx, int reps, double* phase_ms) {
           dev::fill(C.kz, 0.0, H.n, C.s);
           smooth(C, H, C.kz, C.kr, false);
           CK(cudaEventRecord(ev[1], C.s));
-          dev::inject_residual(H.A, C.kz, C.kr, F.b, C.s);
+          dev::inject_residual(H.A, C.kz, C.kr, F.b, C.s, F.x);
           CK(cudaEventRecord(ev[2], C.s));
           h_cycle(C, C.L, F.b, F.x);
           dev::embed_add(H.nb, H.bs, F.x, C.kz, C.s);

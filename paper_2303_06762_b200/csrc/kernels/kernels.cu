@@ -266,7 +266,7 @@ __global__ void k_spmv(Bsr A, const double* __restrict__ x, const double* __rest
 
 template <int BS>
 __global__ void k_inject_residual(Bsr A, const double* __restrict__ x, const double* __restrict__ b,
-                                  double* __restrict__ r0) {
+                                  double* __restrict__ r0, double* __restrict__ x0_zero) {
   const int64_t n = int64_t(A.nb) * 2;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
     const int f = int(t >> 1), i = int(t & 1);
@@ -285,6 +285,7 @@ __global__ void k_inject_residual(Bsr A, const double* __restrict__ x, const dou
       }
     }
     r0[t] = b[size_t(f) * BS + i] - s;
+    if (x0_zero) x0_zero[t] = 0.0;  // the lowest-order pre-smoothing starts from x = 0
   }
 }
 
@@ -552,7 +553,8 @@ __global__ void k_jacobi_combine(int nb, int bs, Patches P, int max_np, const do
 /// fixed-order butterfly): PT rows hold ~25 blocks, P rows ~6, so one thread
 /// per row would serialise that many dependent L2 round trips.
 template <int G, bool ACC>
-__global__ void k_bcsr_group(BlockCsr M, const double* __restrict__ v, double* __restrict__ y) {
+__global__ void k_bcsr_group(BlockCsr M, const double* __restrict__ v, double* __restrict__ y,
+                             double* __restrict__ zero_out = nullptr) {
   // warp-uniform grid stride: every lane of a warp runs the same trip count (shuffles)
   const int64_t total = int64_t(M.nrows) * G, stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t base = blockIdx.x * int64_t(blockDim.x) + (threadIdx.x & ~31); base < total; base += stride) {
@@ -577,6 +579,9 @@ __global__ void k_bcsr_group(BlockCsr M, const double* __restrict__ v, double* _
     s1 += __shfl_xor_sync(0xffffffffu, s1, o, G);
   }
   if (live && lane == 0) {
+    // restriction: the coarse level's pre-smoothing starts from x = 0, zeroed
+    // here instead of by a separate fill launch
+    if (zero_out) reinterpret_cast<double2*>(zero_out)[row] = make_double2(0.0, 0.0);
     double2* yr = reinterpret_cast<double2*>(y) + row;
     if (ACC) {
       const double2 o = *yr;
@@ -1134,8 +1139,10 @@ void spmv(const Bsr& A, const double* x, const double* b, double* y, int minus, 
   HPMG_LAUNCH_CHECK();
 }
 
-void inject_residual(const Bsr& A, const double* x, const double* b, double* r0, cudaStream_t s) {
-  by_bs(A.bs, [&](auto BS) { k_inject_residual<BS><<<grid_for(int64_t(A.nb) * 2, 256), 256, 0, s>>>(A, x, b, r0); });
+void inject_residual(const Bsr& A, const double* x, const double* b, double* r0, cudaStream_t s, double* x0_zero) {
+  by_bs(A.bs, [&](auto BS) {
+    k_inject_residual<BS><<<grid_for(int64_t(A.nb) * 2, 256), 256, 0, s>>>(A, x, b, r0, x0_zero);
+  });
   HPMG_LAUNCH_CHECK();
 }
 
@@ -1217,9 +1224,9 @@ void prolong_add(const BlockCsr& P, const double* e, double* x, cudaStream_t s) 
   HPMG_LAUNCH_CHECK();
 }
 
-void restrict_(const BlockCsr& PT, const double* r, double* rc, cudaStream_t s) {
+void restrict_(const BlockCsr& PT, const double* r, double* rc, cudaStream_t s, double* xc_zero) {
   constexpr int G = 8;
-  k_bcsr_group<G, false><<<grid_for(int64_t(PT.nrows) * G, 256), 256, 0, s>>>(PT, r, rc);
+  k_bcsr_group<G, false><<<grid_for(int64_t(PT.nrows) * G, 256), 256, 0, s>>>(PT, r, rc, xc_zero);
   HPMG_LAUNCH_CHECK();
 }
 

@@ -73,7 +73,8 @@ void spmv(const Bsr& A, const double* x, const double* b, double* y, int minus, 
           cudaStream_t s);
 /// Residual restricted to mode-0 rows, written in lowest-order layout
 /// (fused E^T (b - A x), reference multigrid.hpp:123-124).
-void inject_residual(const Bsr& A, const double* x, const double* b, double* r0, cudaStream_t s);
+void inject_residual(const Bsr& A, const double* x, const double* b, double* r0, cudaStream_t s,
+                     double* x0_zero = nullptr);  // optionally zeroes x0 (same length as r0)
 /// x[f][0..1] += e[f][0..1] (the embedding E, transfer.hpp:140-158).
 void embed_add(int nb, int bs, const double* e, double* x, cudaStream_t s);
 
@@ -150,7 +151,8 @@ constexpr int kTransferColMax = 16;
 /// device, into P's fixed pattern; PT by the block permutation.
 void corrected_prolongation(const Bsr& A, const TransferDev& T, BlockCsr& P, BlockCsr& PT, cudaStream_t s);
 void prolong_add(const BlockCsr& P, const double* e, double* x, cudaStream_t s);
-void restrict_(const BlockCsr& PT, const double* r, double* rc, cudaStream_t s);
+void restrict_(const BlockCsr& PT, const double* r, double* rc, cudaStream_t s,
+               double* xc_zero = nullptr);  // optionally zeroes xc (same length as rc)
 void dense_gemv(int n, const double* inv_colmajor, const double* b, double* x, double* work, cudaStream_t s);
 /// Gauss-Jordan inverse with partial pivoting of a dense row-major matrix (setup).
 void dense_invert(int n, const double* A_rowmajor, double* inv_colmajor, cudaStream_t s);
