@@ -31,7 +31,9 @@
  *    Internally the device uses a facet-major block layout; the permutation
  *    is applied inside the call.
  *  - Pointers are host memory unless HPMG_DEVICE_PTRS is passed in `flags`,
- *    in which case they are device pointers (still reference order).
+ *    in which case they are device pointers (still reference order) and the
+ *    call is stream-ordered on hpmg_stream(ctx): inputs must be ready on that
+ *    stream, outputs are complete once it is synchronised (or waited on).
  *  - Errors: setup errors return a nonzero status and hpmg_last_error()
  *    describes them (the C++ adapter rethrows them as the reference's
  *    exception types); solver breakdown / indefiniteness is reported in-band

@@ -681,9 +681,8 @@ void in_vec(hpmg_ctx& C, const double* src, double* dst_blk, int flags) {
 }
 void out_vec(hpmg_ctx& C, const double* src_blk, double* dst, int flags) {
   Level& T = C.top();
-  if (flags & HPMG_DEVICE_PTRS) {
+  if (flags & HPMG_DEVICE_PTRS) {  // stream-ordered: the caller synchronises hpmg_stream(ctx) as needed
     dev::to_reference(T.nb, T.k + 1, src_blk, dst, C.s);
-    CK(cudaStreamSynchronize(C.s));
     return;
   }
   dev::to_reference(T.nb, T.k + 1, src_blk, C.io_b, C.s);

@@ -132,6 +132,23 @@ def test_apply_bit_identical_repeat():
     assert np.array_equal(gpu.apply(b), gpu.apply(b))
 
 
+def test_device_pointer_apply_is_stream_ordered():
+    # HPMG_DEVICE_PTRS: no host sync inside the call; after synchronising the
+    # context stream the result equals the host-pointer apply, bitwise
+    import ctypes
+    import torch
+    _, gpu = pair(2)
+    b = O.random_vec(gpu.n, 21)
+    r = torch.from_numpy(b).cuda()
+    z = torch.empty_like(r)
+    torch.cuda.synchronize()
+    for _ in range(3):  # back-to-back calls queue on the stream
+        assert H.lib().hpmg_apply(gpu.h, ctypes.c_void_p(r.data_ptr()), ctypes.c_void_p(z.data_ptr()),
+                                  H.DEVICE_PTRS) == 0
+    torch.cuda.synchronize()
+    assert np.array_equal(z.cpu().numpy(), gpu.apply(b))
+
+
 @pytest.mark.parametrize("m", [1, 2, 5])
 def test_apply_batch_equals_apply(m):
     # pipelined batch (copies overlapped on two streams) == m plain applies, bitwise
