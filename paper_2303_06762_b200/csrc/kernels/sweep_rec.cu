@@ -115,6 +115,7 @@ template <int BS, int TP, int G, bool DAG>
 __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1, SweepOrder O, DagState D,
                                                  const double* __restrict__ b, double* __restrict__ x) {
   constexpr int kRow = kExt * BS * BS;
+  constexpr bool kOneCopy = G > 1 && !DAG;  // grouped small records: one copy per CTA
   extern __shared__ __align__(128) unsigned char smraw[];
   double* srec = reinterpret_cast<double*>(smraw);  // G * stride
   double* sx = srec + size_t(G) * R.stride;          // G * max_nf * kExt * BS
@@ -144,18 +145,26 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
     bar_init(&bar_m);
     unsigned long long pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    const unsigned mbytes = unsigned(R.stride - R.meta_off) * 8u, abytes = unsigned(R.meta_off - R.a_off) * 8u,
-                   head = unsigned(R.a_off) * 8u;
-    bar_expect(&bar_m, unsigned(ng) * mbytes);
-    bar_expect(&bar, unsigned(ng) * abytes);
-    bar_expect(&bar_s, unsigned(ng) * head);
-    for (int q = 0; q < ng; ++q)
-      tma_part(srec + size_t(q) * R.stride + R.meta_off, R.rec + size_t(q0 + q) * R.stride + R.meta_off, mbytes,
-               &bar_m, pol);
-    for (int q = 0; q < ng; ++q)
-      tma_part(srec + size_t(q) * R.stride + R.a_off, R.rec + size_t(q0 + q) * R.stride + R.a_off, abytes, &bar, pol);
-    for (int q = 0; q < ng; ++q)
-      tma_part(srec + size_t(q) * R.stride, R.rec + size_t(q0 + q) * R.stride, head, &bar_s, pol);
+    if (kOneCopy) {
+      // small records of consecutive patches: one bulk copy for the group
+      const unsigned all = unsigned(ng) * unsigned(R.stride) * 8u;
+      bar_expect(&bar_m, all);
+      tma_part(srec, R.rec + size_t(q0) * R.stride, all, &bar_m, pol);
+    } else {
+      const unsigned mbytes = unsigned(R.stride - R.meta_off) * 8u, abytes = unsigned(R.meta_off - R.a_off) * 8u,
+                     head = unsigned(R.a_off) * 8u;
+      bar_expect(&bar_m, unsigned(ng) * mbytes);
+      bar_expect(&bar, unsigned(ng) * abytes);
+      bar_expect(&bar_s, unsigned(ng) * head);
+      for (int q = 0; q < ng; ++q)
+        tma_part(srec + size_t(q) * R.stride + R.meta_off, R.rec + size_t(q0 + q) * R.stride + R.meta_off, mbytes,
+                 &bar_m, pol);
+      for (int q = 0; q < ng; ++q)
+        tma_part(srec + size_t(q) * R.stride + R.a_off, R.rec + size_t(q0 + q) * R.stride + R.a_off, abytes, &bar,
+                 pol);
+      for (int q = 0; q < ng; ++q)
+        tma_part(srec + size_t(q) * R.stride, R.rec + size_t(q0 + q) * R.stride, head, &bar_s, pol);
+    }
   }
   // dependency lists do not depend on the previous kernel: load them now
   int dq = -1;
@@ -215,7 +224,7 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
     for (int u = 0; u < kPer; ++u)
       if (t + u * TP < ne) xs[t + u * TP] = v[u];
   }
-  bar_wait(&bar);
+  if (!kOneCopy) bar_wait(&bar);
   __syncthreads();
   sweep_stamp(R, 2);
   double rsum = 0.0;
@@ -243,7 +252,7 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
   if (TR == 2) rsum += __shfl_xor_sync(0xffffffffu, rsum, 1);
   if (row < np && part == 0) r[lp * TP + row] = rsum;
   __syncthreads();
-  bar_wait(&bar_s);
+  if (!kOneCopy) bar_wait(&bar_s);
   sweep_stamp(R, 3);
   double dsum = 0.0;
   if (row < np) {
