@@ -555,7 +555,7 @@ template <int BS>
 struct RecCfg;
 template <>
 struct RecCfg<2> {
-  static constexpr int TP = 16, G = 8;
+  static constexpr int TP = 16, G = 4;
 };
 template <>
 struct RecCfg<4> {
