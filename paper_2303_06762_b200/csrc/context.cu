@@ -1061,7 +1061,7 @@ void linearise(hpmg_ctx& C, const hpmg_problem* prob, const host::RefTensors* Tk
     if (!C.coarse_inv) C.coarse_inv = dalloc<double>(size_t(C.n0) * C.n0);
     dev::dense_invert(C.n0, dA, C.coarse_inv, C.s);
     CK(cudaStreamSynchronize(C.s));
-    if (!C.gemv_work) C.gemv_work = dalloc<double>(size_t(C.n0) * ((C.n0 + 63) / 64 + 1));  // kGemvChunk = 64
+    if (!C.gemv_work) C.gemv_work = dalloc<double>(dev::dense_gemv_work(C.n0));
   }
   tr.mark("coarse inverse");
   const auto t_coarse = clk::now();

@@ -682,7 +682,7 @@ __global__ void k_block_transpose_perm(int nnz, const int* __restrict__ perm, co
 
 /// x = Inv b for the dense coarse inverse (column-major), 2-stage over
 /// column chunks for parallelism: work[chunk][n] partials then a fixed-order sum.
-constexpr int kGemvChunk = 64;
+constexpr int kGemvChunk = 32;  // columns per partial: 2 rounds of 16 loads in flight per thread
 __global__ void k_gemv_partial(int n, const double* __restrict__ inv, const double* __restrict__ b,
                                double* __restrict__ work) {
   __shared__ double sb[kGemvChunk];
@@ -692,10 +692,17 @@ __global__ void k_gemv_partial(int n, const double* __restrict__ inv, const doub
   __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  // eight independent accumulators keep 8 column loads in flight per thread
+  // eight independent accumulators; 16 column loads in flight per thread
   double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const double* col = inv + size_t(j0) * n + i;
   int j = j0;
+  for (; j + 16 <= j1; j += 16) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = __ldg(col + size_t(j - j0 + u) * n);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) s[u & 7] = fma(v[u], sb[j - j0 + u], s[u & 7]);
+  }
   for (; j + 8 <= j1; j += 8) {
     double v[8];
 #pragma unroll
@@ -1229,6 +1236,8 @@ void restrict_(const BlockCsr& PT, const double* r, double* rc, cudaStream_t s, 
   k_bcsr_group<G, false><<<grid_for(int64_t(PT.nrows) * G, 256), 256, 0, s>>>(PT, r, rc, xc_zero);
   HPMG_LAUNCH_CHECK();
 }
+
+size_t dense_gemv_work(int n) { return size_t(n) * ((n + kGemvChunk - 1) / kGemvChunk + 1); }
 
 void dense_gemv(int n, const double* inv, const double* b, double* x, double* work, cudaStream_t s) {
   const int chunks = (n + kGemvChunk - 1) / kGemvChunk;

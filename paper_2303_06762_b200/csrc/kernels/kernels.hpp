@@ -154,6 +154,7 @@ void prolong_add(const BlockCsr& P, const double* e, double* x, cudaStream_t s);
 void restrict_(const BlockCsr& PT, const double* r, double* rc, cudaStream_t s,
                double* xc_zero = nullptr);  // optionally zeroes xc (same length as rc)
 void dense_gemv(int n, const double* inv_colmajor, const double* b, double* x, double* work, cudaStream_t s);
+size_t dense_gemv_work(int n);  // doubles of dense_gemv's partial-sum scratch
 /// Gauss-Jordan inverse with partial pivoting of a dense row-major matrix (setup).
 void dense_invert(int n, const double* A_rowmajor, double* inv_colmajor, cudaStream_t s);
 
