@@ -194,6 +194,25 @@ def test_config1_full_size_parity():
     assert rel(rg.velocity, ro["velocity"]) < 1e-9
 
 
+def test_config2_full_size_apply_and_symmetry():
+    # BASELINE config 2 at full size (256^2 x 2 triangles, k=3, 1.57M DOFs):
+    # one V-cycle against the oracle (its ~30 s setup is the price), the
+    # operator apply, and the size-independent properties of the symmetric
+    # V(1,1) preconditioner: (B r1, r2) = (r1, B r2), (B r, r) > 0, linearity
+    orc, gpu = pair(3, base_n=16, levels=5, beta=1e-2, inv_eps=1e3)
+    assert gpu.n == 1568768
+    r1, r2 = O.random_vec(gpu.n, 61), O.random_vec(gpu.n, 62)
+    z1, z2 = gpu.apply(r1), gpu.apply(r2)
+    # round-off of the two summation orders grows with the hierarchy: 4.3e-12
+    # measured at this size (2e-12 bound at the 8x8 meshes above)
+    assert rel(z1, orc.apply(r1)) < 1e-11
+    assert rel(gpu.spmv(r1), orc.spmv(r1)) < 1e-13
+    a, b = z1 @ r2, r1 @ z2
+    assert abs(a - b) <= 1e-12 * np.linalg.norm(z1) * np.linalg.norm(r2)
+    assert z1 @ r1 > 0 and z2 @ r2 > 0
+    assert rel(gpu.apply(2.0 * r1 - 3.0 * r2), 2.0 * z1 - 3.0 * z2) < 1e-12
+
+
 @pytest.mark.parametrize("k", [0, 1, 2, 3])
 def test_recover_locals(k):
     # reference assembly.hpp:513-549 on the Uzawa velocity; the zero-mean pressure
