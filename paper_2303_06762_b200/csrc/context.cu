@@ -589,7 +589,7 @@ void smooth(hpmg_ctx& C, Level& V, double* x, const double* b, bool post) {
 void h_cycle(hpmg_ctx& C, int l, const double* b, double* x) {
   if (l == 0) {
     dev::dense_gemv(C.n0, C.coarse_inv, b, x, C.gemv_work, C.s);
-    count(C, 2);
+    count(C);
     return;
   }
   Level& V = *C.lv[l];
@@ -1061,7 +1061,10 @@ void linearise(hpmg_ctx& C, const hpmg_problem* prob, const host::RefTensors* Tk
     if (!C.coarse_inv) C.coarse_inv = dalloc<double>(size_t(C.n0) * C.n0);
     dev::dense_invert(C.n0, dA, C.coarse_inv, C.s);
     CK(cudaStreamSynchronize(C.s));
-    if (!C.gemv_work) C.gemv_work = dalloc<double>(dev::dense_gemv_work(C.n0));
+    if (!C.gemv_work) {
+      C.gemv_work = dalloc<double>(dev::dense_gemv_work(C.n0));
+      CK(cudaMemsetAsync(C.gemv_work, 0, sizeof(double) * dev::dense_gemv_work(C.n0), C.s));  // arrival counters
+    }
   }
   tr.mark("coarse inverse");
   const auto t_coarse = clk::now();

@@ -680,45 +680,57 @@ __global__ void k_block_transpose_perm(int nnz, const int* __restrict__ perm, co
   }
 }
 
-/// x = Inv b for the dense coarse inverse (column-major), 2-stage over
-/// column chunks for parallelism: work[chunk][n] partials then a fixed-order sum.
-constexpr int kGemvChunk = 32;  // columns per partial: 2 rounds of 16 loads in flight per thread
-__global__ void k_gemv_partial(int n, const double* __restrict__ inv, const double* __restrict__ b,
-                               double* __restrict__ work) {
+/// x = Inv b for the dense coarse inverse (column-major) in ONE launch: CTA
+/// (rb, chunk) forms the partial sums of rows [128 rb, 128 rb + 128) over the
+/// columns of its chunk (all 32 column loads of a thread in flight at once,
+/// L2 evict-last so the 17 MB inverse of a 1472-DOF coarse level stays
+/// L2-resident across V-cycles), writes them to work[chunk][n], and the last
+/// CTA of the row block to arrive (threadfence + counter, as CUDA's
+/// threadFenceReduction sample) sums the partials in chunk order: the result
+/// is independent of CTA scheduling. The counter resets itself, so captured
+/// graphs replay it.
+constexpr int kGemvChunk = 32;
+__global__ void __launch_bounds__(128) k_gemv(int n, int chunks, const double* __restrict__ inv,
+                                              const double* __restrict__ b, double* __restrict__ work,
+                                              unsigned* __restrict__ counter, double* __restrict__ x) {
   __shared__ double sb[kGemvChunk];
+  __shared__ bool last;
   const int chunk = blockIdx.y;
-  const int j0 = chunk * kGemvChunk, j1 = min(n, j0 + kGemvChunk);
-  for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) sb[j - j0] = b[j];
+  const int j0 = chunk * kGemvChunk, nj = min(kGemvChunk, n - j0);
+  if (threadIdx.x < nj) sb[threadIdx.x] = b[j0 + threadIdx.x];
   __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  // eight independent accumulators; 16 column loads in flight per thread
-  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const double* col = inv + size_t(j0) * n + i;
-  int j = j0;
-  for (; j + 16 <= j1; j += 16) {
-    double v[16];
+  if (i < n) {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    const double* col = inv + size_t(j0) * n + i;
+    double v[kGemvChunk];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) v[u] = __ldg(col + size_t(j - j0 + u) * n);
+    for (int u = 0; u < kGemvChunk; ++u) {
+      v[u] = 0.0;
+      if (u < nj)
+        asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;"
+                     : "=d"(v[u])
+                     : "l"(col + size_t(u) * n), "l"(pol));
+    }
+    double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-    for (int u = 0; u < 16; ++u) s[u & 7] = fma(v[u], sb[j - j0 + u], s[u & 7]);
+    for (int u = 0; u < kGemvChunk; ++u)
+      if (u < nj) s[u & 7] = fma(v[u], sb[u], s[u & 7]);
+    work[size_t(chunk) * n + i] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
   }
-  for (; j + 8 <= j1; j += 8) {
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __ldg(col + size_t(j - j0 + u) * n);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) s[u] = fma(v[u], sb[j - j0 + u], s[u]);
-  }
-  for (; j < j1; ++j) s[0] = fma(__ldg(col + size_t(j - j0) * n), sb[j - j0], s[0]);
-  work[size_t(chunk) * n + i] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
-}
-__global__ void k_gemv_sum(int n, int chunks, const double* __restrict__ work, double* __restrict__ x) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter + blockIdx.x, 1u) == unsigned(chunks - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (i < n) {
     double s = 0.0;
-    for (int c = 0; c < chunks; ++c) s += work[size_t(c) * n + i];
+    for (int c = 0; c < chunks; ++c) s += __ldcg(work + size_t(c) * n + i);
     x[i] = s;
   }
+  if (threadIdx.x == 0) counter[blockIdx.x] = 0u;
 }
 
 // ---------------------------------------------- dense coarse inverse (setup)
@@ -1237,13 +1249,13 @@ void restrict_(const BlockCsr& PT, const double* r, double* rc, cudaStream_t s, 
   HPMG_LAUNCH_CHECK();
 }
 
-size_t dense_gemv_work(int n) { return size_t(n) * ((n + kGemvChunk - 1) / kGemvChunk + 1); }
+// partials [chunks][n] then the per-row-block arrival counters (zero-initialised by the caller)
+size_t dense_gemv_work(int n) { return size_t(n) * ((n + kGemvChunk - 1) / kGemvChunk) + (n + 127) / 128 + 1; }
 
 void dense_gemv(int n, const double* inv, const double* b, double* x, double* work, cudaStream_t s) {
   const int chunks = (n + kGemvChunk - 1) / kGemvChunk;
-  dim3 grid((n + 127) / 128, chunks);
-  k_gemv_partial<<<grid, 128, 0, s>>>(n, inv, b, work);
-  k_gemv_sum<<<(n + 127) / 128, 128, 0, s>>>(n, chunks, work, x);
+  unsigned* counter = reinterpret_cast<unsigned*>(work + size_t(n) * chunks);
+  k_gemv<<<dim3((n + 127) / 128, chunks), 128, 0, s>>>(n, chunks, inv, b, work, counter, x);
   HPMG_LAUNCH_CHECK();
 }
 

@@ -127,34 +127,40 @@ __device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, i
     if (trace && k < 1000) d_trace[4 * k + 1] = clock64();
     const double* rec = v.ring + (size_t(k % kStages) * kPass + lp) * R.stride;
     int np = 0, g = 0;
-    // row t of S_p into registers now: these loads do not depend on the
-    // residual, so they overlap it instead of following the barrier
+    // every shared load of the residual and of row t of S_p is addressed
+    // without the patch's own size (S_p zero-padded to the level's largest
+    // patch, meta padded with -1), so all of them issue right after the
+    // ring wait instead of behind the meta[0] load
     double srow[2 * kMaxPatchF];
     if (lp < ps.y) {
       const int* meta = reinterpret_cast<const int*>(rec + R.meta_off);
+      const int npm = 2 * R.max_nf;
+#pragma unroll
+      for (int j = 0; j < 2 * kMaxPatchF; ++j) srow[j] = j < npm ? rec[j * npm + t] : 0.0;
+      const int lf = t >> 1, i = t & 1;
+      const bool rowok = lf < R.max_nf;
+      const int f = rowok ? meta[1 + lf] : -1;
+      int c[kExt];
+      const int* cols = meta + 1 + R.max_nf + lf * kExt;
+#pragma unroll
+      for (int sl = 0; sl < kExt; ++sl) c[sl] = rowok ? cols[sl] : -1;
       np = 2 * meta[0];
+      const double* acol = rec + R.a_off + lf * kExt * 4 + i;  // column-major 2x2 blocks
+      g = 2 * (f >= 0 ? f : 0) + i;
+      double a0 = v.sb[g], a1 = 0.0;
 #pragma unroll
-      for (int j = 0; j < 2 * kMaxPatchF; ++j) srow[j] = (t < np && j < np) ? rec[j * np + t] : 0.0;
-      if (t < np) {
-        const int lf = t >> 1, i = t & 1;
-        g = 2 * meta[1 + lf] + i;
-        const int* cols = meta + 1 + R.max_nf + lf * kExt;
-        const double* acol = rec + R.a_off + lf * kExt * 4 + i;  // column-major 2x2 blocks
-        double a0 = v.sb[g], a1 = 0.0;
-#pragma unroll
-        for (int sl = 0; sl < kExt; ++sl) {
-          const int c = cols[sl];
-          const int cc = c >= 0 ? c : 0;  // empty slots hold zero blocks
-          a0 = fma(-acol[sl * 4], v.sx[2 * cc], a0);
-          a1 = fma(-acol[sl * 4 + 2], v.sx[2 * cc + 1], a1);
-        }
-        v.r[threadIdx.x] = a0 + a1;
+      for (int sl = 0; sl < kExt; ++sl) {
+        const int cc = c[sl] >= 0 ? c[sl] : 0;  // empty slots hold zero blocks
+        const double w0 = rowok ? acol[sl * 4] : 0.0, w1 = rowok ? acol[sl * 4 + 2] : 0.0;
+        a0 = fma(-w0, v.sx[2 * cc], a0);
+        a1 = fma(-w1, v.sx[2 * cc + 1], a1);
       }
+      if (t < np) v.r[threadIdx.x] = a0 + a1;
     }
     __syncthreads();
     if (trace && k < 1000) d_trace[4 * k + 2] = clock64();
     if (t < np) {
-      // full column-major inverse: S(t, j) at j*np + t
+      // full column-major inverse: S(t, j) at j*npmax + t
       const double* rr = v.r + lp * kTP;
       double d[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll

@@ -512,11 +512,15 @@ __global__ void k_build_records(Bsr A, Patches P, PatchRecords R, int bs) {
   const int nf = P.nf[p], np = nf * bs;
   const int pk = np * (np + 1) / 2;
   const double* inv = P.inv + P.off[p];
-  if (R.full) {  // unpack the symmetric triangle: (r, c) at c*np + r
+  if (R.full) {
+    // unpack the symmetric triangle: (r, c) at c*npmax + r, zero-padded to the
+    // level's largest patch, so readers address S without the patch's own size
+    const int npmax = R.max_nf * bs;
     for (int k = threadIdx.x; k < R.a_off; k += blockDim.x) {
       double v = 0.0;
-      if (k < np * np) {
-        const int c = k / np, r = k % np, lo = r > c ? c : r, hi = r > c ? r : c;
+      const int c = k / npmax, r = k % npmax;
+      if (c < np && r < np) {
+        const int lo = r > c ? c : r, hi = r > c ? r : c;
         v = inv[lo * np - lo * (lo - 1) / 2 + (hi - lo)];
       }
       rec[k] = v;
