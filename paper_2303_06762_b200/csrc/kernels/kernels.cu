@@ -810,69 +810,136 @@ __device__ __forceinline__ void gj_grid_sync(unsigned* ctl, unsigned i) {
   __syncthreads();
 }
 
-/// All n Gauss-Jordan steps in one cooperative launch: per step, block 0
-/// pivots (the k_gj_pivot arithmetic), a grid barrier, every block
-/// eliminates (k_gj_eliminate's), a grid barrier. Same operations in the same
-/// order as the two-kernel loop, without its 2n launches.
-__global__ void __launch_bounds__(256) k_gj_coop(int n, double* __restrict__ aug, double* __restrict__ rowk,
-                                                 double* __restrict__ colk, int* __restrict__ status, unsigned* ctl) {
-  __shared__ double bv[32];
-  __shared__ int bi[32];
-  const int w = 2 * n;
+/// (value, row) candidate of a pivot search; ties go to the lowest row.
+struct GjCand {
+  double v;
+  int i, pad;
+};
+__device__ __forceinline__ void gj_better(double& bv, int& bi, double ov, int oi) {
+  if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+}
+/// block-wide argmax (256 threads); the result is valid in every thread
+__device__ __forceinline__ void gj_block_argmax(double& bv, int& bi, double* sv, int* si) {
+  for (int o = 16; o > 0; o >>= 1) gj_better(bv, bi, __shfl_xor_sync(0xffffffffu, bv, o), __shfl_xor_sync(0xffffffffu, bi, o));
+  if ((threadIdx.x & 31) == 0) { sv[threadIdx.x >> 5] = bv; si[threadIdx.x >> 5] = bi; }
+  __syncthreads();
+  bv = sv[0];
+  bi = si[0];
+  for (int q = 1; q < int(blockDim.x >> 5); ++q) gj_better(bv, bi, sv[q], si[q]);
+  __syncthreads();
+}
+
+constexpr int kGjMaxRows = 64;  // rows owned per CTA
+constexpr int kGjBatch = 12;    // loads in flight per thread and row (2n <= 3072 in one batch)
+/// All n Gauss-Jordan steps (partial pivoting) in one cooperative launch with
+/// ONE grid barrier per step and no row swaps. CTA b owns the rows b, b + G,
+/// ...; pivot rows are tracked, not swapped (inverse row k = right part of
+/// pivot row p_k). Step k: every CTA reduces the per-CTA candidates of column
+/// k (ties: lowest row) to the pivot p, reads the multipliers a_ik of its own
+/// rows, and updates them over columns [k, 2n) as a_ij - a_ik (a_pj / a_pk)
+/// (the left columns < k are already eliminated); then it publishes the
+/// candidate of column k+1 among its unused rows. Row p is read by every CTA
+/// during step k, so its owner normalises it (a_pj / a_pk) only at the start
+/// of step k+1, where no other CTA reads it. Operations per entry are those of
+/// the swapping formulation (k_gj_pivot + k_gj_eliminate); the only
+/// difference is the tie-break order among exactly equal pivot candidates.
+__global__ void __launch_bounds__(256) k_gj_implicit(int n, double* __restrict__ aug, GjCand* __restrict__ cand,
+                                                     int* __restrict__ piv, int* __restrict__ status, unsigned* ctl) {
+  extern __shared__ double srow[];  // [2n] scaled pivot row
+  __shared__ double m[kGjMaxRows];
+  __shared__ unsigned char used[kGjMaxRows];
+  __shared__ double sv[32];
+  __shared__ int si[32];
+  const int w = 2 * n, G = int(gridDim.x), b = int(blockIdx.x);
+  const int nown = (n - b + G - 1) / G;
+  for (int r = threadIdx.x; r < kGjMaxRows; r += blockDim.x) used[r] = 0;
+  __syncthreads();
+  auto publish = [&](int col, int slot) {  // candidate of column col among the unused own rows
+    double bv = -1.0;
+    int bi = n;
+    for (int r = threadIdx.x; r < nown; r += blockDim.x)
+      if (!used[r]) {
+        const int i = b + r * G;
+        gj_better(bv, bi, fabs(__ldcg(aug + size_t(i) * w + col)), i);
+      }
+    gj_block_argmax(bv, bi, sv, si);
+    if (threadIdx.x == 0) {
+      __stcg(&cand[size_t(slot) * G + b].v, bv);
+      __stcg(&cand[size_t(slot) * G + b].i, bi);
+    }
+  };
+  publish(0, 0);
   unsigned bar = 0;
+  gj_grid_sync(ctl, bar++);
+  int prev = -1;
+  double prev_inv = 0.0;
   for (int k = 0; k < n; ++k) {
-    if (blockIdx.x == 0) {
-      double best = -1.0;
-      int besti = k;
-      for (int i = k + threadIdx.x; i < n; i += blockDim.x) {
-        const double v = fabs(__ldcg(aug + size_t(i) * w + k));
-        if (v > best) { best = v; besti = i; }
-      }
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, besti, o);
-        if (ob > best || (ob == best && oi < besti)) { best = ob; besti = oi; }
-      }
-      if ((threadIdx.x & 31) == 0) { bv[threadIdx.x >> 5] = best; bi[threadIdx.x >> 5] = besti; }
-      __syncthreads();
-      if (threadIdx.x < 32) {
-        const int nw = blockDim.x >> 5;
-        best = threadIdx.x < nw ? bv[threadIdx.x] : -1.0;
-        besti = threadIdx.x < nw ? bi[threadIdx.x] : n;
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, besti, o);
-          if (ob > best || (ob == best && oi < besti)) { best = ob; besti = oi; }
-        }
-        if (threadIdx.x == 0) { bi[0] = besti; bv[0] = best; }
-      }
-      __syncthreads();
-      const int p = bi[0];
-      if (threadIdx.x == 0 && !(bv[0] > 0.0)) *status = 1;  // singular
-      for (int j = threadIdx.x; j < w; j += blockDim.x) {
-        const double a = __ldcg(aug + size_t(k) * w + j), b = __ldcg(aug + size_t(p) * w + j);
-        __stcg(aug + size_t(k) * w + j, b);
-        __stcg(aug + size_t(p) * w + j, a);
-        __stcg(rowk + j, b);
-      }
-      __syncthreads();
-      for (int i = threadIdx.x; i < n; i += blockDim.x)
-        __stcg(colk + i, i == k ? 0.0 : __ldcg(aug + size_t(i) * w + k));
+    double bv = -1.0;
+    int p = n;
+    for (int q = threadIdx.x; q < G; q += blockDim.x) {
+      const GjCand* c = cand + size_t(k & 1) * G + q;  // L2: written by other CTAs
+      gj_better(bv, p, __ldcg(&c->v), __ldcg(&c->i));
     }
-    gj_grid_sync(ctl, bar++);
-    const double inv = 1.0 / __ldcg(rowk + k);
-    // left-part columns j < k are already eliminated (rowk[j] = 0 there, so
-    // the update would leave them unchanged): only j in [k, 2n) is touched
-    const int span = w - k;
-    for (int i = blockIdx.x; i < n; i += gridDim.x) {
-      const double ci = __ldcg(colk + i);
-      double* row = aug + size_t(i) * w + k;
-      for (int jj = threadIdx.x; jj < span; jj += blockDim.x) {
-        const double r = __ldcg(rowk + k + jj) * inv;
-        __stcg(row + jj, i == k ? r : __ldcg(row + jj) - ci * r);
+    gj_block_argmax(bv, p, sv, si);
+    if (b == 0 && threadIdx.x == 0) {
+      piv[k] = p;
+      if (!(bv > 0.0)) *status = 1;  // singular
+    }
+    if (p >= n) p = 0;  // singular (flagged above): keep the addressing in bounds
+    // deferred normalisation of the previous pivot row (k_gj_eliminate: rowk[j] * inv)
+    if (prev >= 0 && prev % G == b) {
+      double* row = aug + size_t(prev) * w;
+      for (int j0 = k + threadIdx.x; j0 < w; j0 += kGjBatch * 256) {
+        double v[kGjBatch];
+#pragma unroll
+        for (int u = 0; u < kGjBatch; ++u) v[u] = j0 + u * 256 < w ? __ldcg(row + j0 + u * 256) : 0.0;
+#pragma unroll
+        for (int u = 0; u < kGjBatch; ++u)
+          if (j0 + u * 256 < w) __stcg(row + j0 + u * 256, v[u] * prev_inv);
+      }
+      __syncthreads();
+    }
+    for (int r = threadIdx.x; r < nown; r += blockDim.x) m[r] = __ldcg(aug + size_t(b + r * G) * w + k);
+    if (p % G == b && threadIdx.x == 0) used[p / G] = 1;
+    __syncthreads();
+    const double* R = aug + size_t(p) * w;
+    const double inv = 1.0 / __ldcg(R + k);
+    // the scaled pivot row a_pj / a_pk once into shared memory, then per own
+    // row all of a thread's loads in flight before its stores (loads and
+    // stores of aug may alias as far as the compiler knows: without the
+    // batching every element would cost its own L2 round trip)
+    for (int j0 = k + threadIdx.x; j0 < w; j0 += kGjBatch * 256) {
+      double v[kGjBatch];
+#pragma unroll
+      for (int u = 0; u < kGjBatch; ++u) v[u] = j0 + u * 256 < w ? __ldcg(R + j0 + u * 256) : 0.0;
+#pragma unroll
+      for (int u = 0; u < kGjBatch; ++u)
+        if (j0 + u * 256 < w) srow[j0 + u * 256 - k] = v[u] * inv;
+    }
+    __syncthreads();
+    for (int r = 0; r < nown; ++r) {
+      const int i = b + r * G;
+      if (i == p) continue;
+      const double mi = m[r];
+      double* row = aug + size_t(i) * w;
+      for (int j0 = k + threadIdx.x; j0 < w; j0 += kGjBatch * 256) {
+        double v[kGjBatch];
+#pragma unroll
+        for (int u = 0; u < kGjBatch; ++u) v[u] = j0 + u * 256 < w ? __ldcg(row + j0 + u * 256) : 0.0;
+#pragma unroll
+        for (int u = 0; u < kGjBatch; ++u)
+          if (j0 + u * 256 < w) __stcg(row + j0 + u * 256, v[u] - mi * srow[j0 + u * 256 - k]);
       }
     }
+    __syncthreads();
+    if (k + 1 < n) publish(k + 1, (k + 1) & 1);
+    prev = p;
+    prev_inv = inv;
     gj_grid_sync(ctl, bar++);
+  }
+  if (prev >= 0 && prev % G == b) {
+    double* row = aug + size_t(prev) * w;
+    for (int j = n + threadIdx.x; j < w; j += blockDim.x) __stcg(row + j, __ldcg(row + j) * prev_inv);
   }
   if (threadIdx.x == 0) {
     unsigned old;
@@ -881,6 +948,16 @@ __global__ void __launch_bounds__(256) k_gj_coop(int n, double* __restrict__ aug
       ctl[0] = 0u;
       ctl[1] = 0u;
     }
+  }
+}
+
+/// inverse row k = right part of pivot row piv[k] (column-major output)
+__global__ void k_gj_extract_piv(int n, const double* __restrict__ aug, const int* __restrict__ piv,
+                                 double* __restrict__ inv) {
+  const int64_t tot = int64_t(n) * n;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
+    const int j = int(e / n), k = int(e % n);
+    inv[e] = aug[size_t(piv[k]) * 2 * n + n + j];
   }
 }
 
@@ -1263,14 +1340,17 @@ void dense_invert(int n, const double* A_rowmajor, double* inv_colmajor, cudaStr
   double *aug = nullptr, *rowk = nullptr, *colk = nullptr;
   int* status = nullptr;
   unsigned* ctl = nullptr;
+  GjCand* cand = nullptr;
+  int* piv = nullptr;
   struct Free {  // scratch released on every exit path (launch errors throw)
-    void** p[5];
+    void** p[7];
     ~Free() {
       for (void** q : p)
         if (*q) cudaFree(*q);
     }
   } release{{reinterpret_cast<void**>(&aug), reinterpret_cast<void**>(&rowk), reinterpret_cast<void**>(&colk),
-             reinterpret_cast<void**>(&status), reinterpret_cast<void**>(&ctl)}};
+             reinterpret_cast<void**>(&status), reinterpret_cast<void**>(&ctl), reinterpret_cast<void**>(&cand),
+             reinterpret_cast<void**>(&piv)}};
   if (cudaMalloc(&aug, sizeof(double) * size_t(n) * 2 * n) != cudaSuccess ||
       cudaMalloc(&rowk, sizeof(double) * 2 * n) != cudaSuccess || cudaMalloc(&colk, sizeof(double) * n) != cudaSuccess ||
       cudaMalloc(&status, sizeof(int)) != cudaSuccess)
@@ -1280,34 +1360,43 @@ void dense_invert(int n, const double* A_rowmajor, double* inv_colmajor, cudaStr
   k_gj_init<<<grid_for(tot, 256), 256, 0, s>>>(n, A_rowmajor, aug);
   // one cooperative launch for all steps when the grid can be co-resident
   int per_sm = 0, dev = 0, sms = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gj_coop, 256, 0);
+  cudaFuncSetAttribute(k_gj_implicit, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gj_implicit, 256, sizeof(double) * 2 * size_t(n));
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  bool coop = per_sm > 0 && cudaMalloc(&ctl, 2 * sizeof(unsigned)) == cudaSuccess;
+  // two CTAs per SM: enough for the row updates, few candidates to reduce per step
+  const int grid = int(std::min<int64_t>(std::min(per_sm, 2) * int64_t(sms), n));
+  bool coop = per_sm > 0 && int64_t(grid) * kGjMaxRows >= n && 2 * size_t(n) * sizeof(double) <= 200 * 1024 && cudaMalloc(&ctl, 2 * sizeof(unsigned)) == cudaSuccess &&
+              cudaMalloc(&cand, sizeof(GjCand) * 2 * size_t(grid)) == cudaSuccess &&
+              cudaMalloc(&piv, sizeof(int) * size_t(n)) == cudaSuccess;
   if (coop) {
     cudaMemsetAsync(ctl, 0, 2 * sizeof(unsigned), s);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned(std::min<int64_t>(int64_t(per_sm) * sms, n)));  // a block per row at most
+    cfg.gridDim = dim3(unsigned(grid));
     cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = sizeof(double) * 2 * size_t(n);
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeCooperative;
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    const cudaError_t le = cudaLaunchKernelEx(&cfg, k_gj_coop, n, aug, rowk, colk, status, ctl);
+    const cudaError_t le = cudaLaunchKernelEx(&cfg, k_gj_implicit, n, aug, cand, piv, status, ctl);
     coop = le == cudaSuccess;
     if (!coop) cudaGetLastError();
     if (std::getenv("HPMG_SETUP_TRACE"))
       std::fprintf(stderr, "[setup] coarse GJ: n %d, cooperative %d (%s), grid %u\n", n, int(coop),
                    cudaGetErrorString(le), cfg.gridDim.x);
   }
-  if (!coop)
+  if (coop) {
+    k_gj_extract_piv<<<grid_for(int64_t(n) * n, 256), 256, 0, s>>>(n, aug, piv, inv_colmajor);
+  } else {
     for (int k = 0; k < n; ++k) {
       k_gj_pivot<<<1, 1024, 0, s>>>(n, k, aug, rowk, colk, status);
       k_gj_eliminate<<<grid_for(tot, 256), 256, 0, s>>>(n, k, aug, rowk, colk);
     }
-  k_gj_extract<<<grid_for(int64_t(n) * n, 256), 256, 0, s>>>(n, aug, inv_colmajor);
+    k_gj_extract<<<grid_for(int64_t(n) * n, 256), 256, 0, s>>>(n, aug, inv_colmajor);
+  }
   HPMG_LAUNCH_CHECK();
   int hs = 0;
   cudaMemcpyAsync(&hs, status, sizeof(int), cudaMemcpyDeviceToHost, s);

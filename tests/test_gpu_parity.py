@@ -105,6 +105,20 @@ def test_dataflow_schedule_apply(k, cycle, schedule):
         assert rel(gpu.apply(b), orc.apply(b)) < apply_tol()
 
 
+@pytest.mark.parametrize("base_n", [4, 8, 16])
+def test_coarse_solve(base_n):
+    # one level, k = 0: the preconditioner is the coarse solve itself
+    # (reference multigrid.hpp:87,170, PartialPivLU), here the swap-free
+    # Gauss-Jordan inverse (one grid barrier per step) applied as a GEMV;
+    # base 16 is config 2's 1472-DOF coarse level. An explicit inverse and an
+    # LU solve differ by ~cond(A) eps (measured 7.8e-12 at base 16, AL 1e3):
+    # a bare coarse solve is not damped by smoothing as in the V-cycle tests
+    orc, gpu = pair(0, base_n=base_n, levels=1)
+    for seed in (21, 22):
+        b = O.random_vec(orc.n, seed)
+        assert rel(gpu.apply(b), orc.apply(b)) < 5e-11
+
+
 @pytest.mark.parametrize("k,cycle", [(0, O.CYCLE_V), (1, O.CYCLE_V), (2, O.CYCLE_W), (3, O.CYCLE_V),
                                      (1, O.CYCLE_VARV)])
 def test_preconditioner_apply(k, cycle):
