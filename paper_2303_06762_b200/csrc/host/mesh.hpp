@@ -71,28 +71,50 @@ struct TriMesh {
   /// Builds facets from elements; `keep_tags` carries over the tags of
   /// facets that existed before (matched by vertex pair).
   void build_facets(const std::unordered_map<uint64_t, int>* keep_tags = nullptr) {
-    std::unordered_map<uint64_t, int> seen;
-    seen.reserve(size_t(ne()) * 2);
+    // facets numbered by first appearance (element order, local edge order):
+    // the numbering fixes the DOF layout and the Gauss-Seidel order. Edges are
+    // found in per-vertex buckets (CSR over the lower vertex, sized by the
+    // number of element edges it starts) instead of a hash map.
     fa.clear(); fb.clear(); fe.clear(); ftag.clear();
     ef.assign(ne(), {0, 0, 0});
+    const int nvv = nv();
+    std::vector<int> start(size_t(nvv) + 1, 0);
+    for (int e = 0; e < ne(); ++e)
+      for (int i = 0; i < 3; ++i) {
+        const int a = ev[e][(i + 1) % 3], b = ev[e][(i + 2) % 3];
+        ++start[size_t(a < b ? a : b) + 1];
+      }
+    for (int v = 0; v < nvv; ++v) start[v + 1] += start[v];
+    const size_t nslots = size_t(start[nvv]);
+    std::vector<int> bhi(nslots), bid(nslots), used(size_t(nvv), 0);
+    fa.reserve(size_t(ne()) * 2);
+    fb.reserve(size_t(ne()) * 2);
+    fe.reserve(size_t(ne()) * 2);
+    ftag.reserve(size_t(ne()) * 2);
     for (int e = 0; e < ne(); ++e)
       for (int i = 0; i < 3; ++i) {
         int a = ev[e][(i + 1) % 3], b = ev[e][(i + 2) % 3];
         int lo = a < b ? a : b, hi = a < b ? b : a;
-        uint64_t key = (uint64_t(uint32_t(lo)) << 32) | uint32_t(hi);
-        auto it = seen.find(key);
-        if (it == seen.end()) {
-          int id = nf();
-          seen.emplace(key, id);
+        const int s0 = start[lo], cnt = used[lo];
+        int id = -1;
+        for (int j = s0; j < s0 + cnt; ++j)
+          if (bhi[j] == hi) {
+            id = bid[j];
+            break;
+          }
+        if (id < 0) {
+          id = nf();
+          bhi[size_t(s0 + cnt)] = hi;
+          bid[size_t(s0 + cnt)] = id;
+          ++used[lo];
           fa.push_back(lo);
           fb.push_back(hi);
           fe.push_back({e, -1});
           ftag.push_back(kTagInterior);
-          ef[e][i] = id;
         } else {
-          fe[it->second][1] = e;
-          ef[e][i] = it->second;
+          fe[id][1] = e;
         }
+        ef[e][i] = id;
       }
     for (int f = 0; f < nf(); ++f) {
       if (fe[f][1] < 0) ftag[f] = kTagDirichlet;

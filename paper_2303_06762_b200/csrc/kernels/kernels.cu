@@ -297,31 +297,41 @@ __global__ void k_embed_add(int nb, int bs, const double* __restrict__ e, double
 
 // ------------------------------------------------------------ smoothers
 /// Patch matrix gather + Gauss-Jordan inversion with partial pivoting,
-/// one CTA per patch; the inverse is stored column-major.
+/// one CTA per patch; the inverse is stored column-major (or packed).
+/// Thread t owns column c = t % W of the augmented [A_pp | I] (W = 2 np_max,
+/// blockDim = RG W) and the rows r = t / W + RG i: no index division per
+/// element, the pivot-row entry a_kc stays in a register for the step.
+/// Per step and entry the arithmetic is the textbook one (pivot: largest
+/// |a_ik|, lowest row on ties; a_kc <- a_kc / a_kk; a_rc <- a_rc - a_rk a_kc).
 template <int BS>
-__global__ void k_patch_inverse(Bsr A, Patches P) {
+__global__ void k_patch_inverse(Bsr A, Patches P, int rg) {
   extern __shared__ double aug[];
   const bool packed = P.packed != 0;
   __shared__ int fac[kMaxPatchF];
   __shared__ int piv_row;
   const int p = blockIdx.x;
   const int nf = P.nf[p], np = nf * BS, w = 2 * np;
+  const int W = blockDim.x / rg;  // 2 np_max >= w
+  const int c = threadIdx.x % W, g = threadIdx.x / W;
+  const bool col = c < w;
   if (threadIdx.x < kMaxPatchF) fac[threadIdx.x] = P.fac[p * kMaxPatchF + threadIdx.x];
   __syncthreads();
-  for (int e = threadIdx.x; e < np * w; e += blockDim.x) {
-    const int r = e / w, c = e % w;
-    double v = 0.0;
-    if (c < np) {
-      const int fr = fac[r / BS], fcn = fac[c / BS];
-      for (int sl = 0; sl < kSlots; ++sl)
-        if (A.cols[fr * kSlots + sl] == fcn) {
-          v = A.val[(size_t(fr * kSlots + sl) * BS + r % BS) * BS + c % BS];
-          break;
-        }
-    } else {
-      v = (c - np == r) ? 1.0 : 0.0;
+  if (col) {
+    const int fcn = c < np ? fac[c / BS] : -1;
+    for (int r = g; r < np; r += rg) {
+      double v = 0.0;
+      if (c < np) {
+        const int fr = fac[r / BS];
+        for (int sl = 0; sl < kSlots; ++sl)
+          if (A.cols[fr * kSlots + sl] == fcn) {
+            v = A.val[(size_t(fr * kSlots + sl) * BS + r % BS) * BS + c % BS];
+            break;
+          }
+      } else {
+        v = (c - np == r) ? 1.0 : 0.0;
+      }
+      aug[r * w + c] = v;
     }
-    aug[e] = v;
   }
   __syncthreads();
   for (int k = 0; k < np; ++k) {
@@ -341,40 +351,41 @@ __global__ void k_patch_inverse(Bsr A, Patches P) {
     }
     __syncthreads();
     const int pr = piv_row;
-    if (pr != k)
-      for (int c = threadIdx.x; c < w; c += blockDim.x) {
-        double t = aug[k * w + c];
-        aug[k * w + c] = aug[pr * w + c];
-        aug[pr * w + c] = t;
-      }
-    __syncthreads();
-    const double inv = 1.0 / aug[k * w + k];
-    __syncthreads();
-    for (int c = threadIdx.x; c < w; c += blockDim.x) aug[k * w + c] *= inv;
-    __syncthreads();
-    for (int e = threadIdx.x; e < np * w; e += blockDim.x) {
-      const int r = e / w, c = e % w;
-      if (r == k || c == k) continue;
-      aug[e] -= aug[r * w + k] * aug[k * w + c];
+    if (pr != k && g == 0 && col) {
+      const double t = aug[k * w + c];
+      aug[k * w + c] = aug[pr * w + c];
+      aug[pr * w + c] = t;
     }
     __syncthreads();
-    for (int r = threadIdx.x; r < np; r += blockDim.x)
-      if (r != k) aug[r * w + k] = 0.0;
+    const double inv = 1.0 / aug[k * w + k];
+    const double akc = col ? aug[k * w + c] * inv : 0.0;
+    __syncthreads();  // every thread has read a_kk and its a_kc
+    if (col) {
+      if (g == 0) aug[k * w + c] = akc;
+      if (c != k)
+        for (int r = g; r < np; r += rg)
+          if (r != k) aug[r * w + c] -= aug[r * w + k] * akc;
+    }
     __syncthreads();
+    if (c == k)
+      for (int r = g; r < np; r += rg)
+        if (r != k) aug[r * w + k] = 0.0;
+    // (column k is read again only after the next step's pivot barrier)
   }
+  __syncthreads();
   double* out = P.inv + P.off[p];
   if (packed) {
     // symmetric operator: symmetrised inverse, lower triangle packed by columns
     // (column c holds rows c..np-1 at c*np - c(c-1)/2)
     for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
-      const int c = e / np, r = e % np;
-      if (r < c) continue;
-      out[c * np - c * (c - 1) / 2 + (r - c)] = 0.5 * (aug[r * w + np + c] + aug[c * w + np + r]);
+      const int cc = e / np, r = e % np;
+      if (r < cc) continue;
+      out[cc * np - cc * (cc - 1) / 2 + (r - cc)] = 0.5 * (aug[r * w + np + cc] + aug[cc * w + np + r]);
     }
   } else {
     for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
-      const int c = e / np, r = e % np;  // column-major: (r, c) at c*np + r
-      out[e] = aug[r * w + np + c];
+      const int cc = e / np, r = e % np;  // column-major: (r, c) at c*np + r
+      out[e] = aug[r * w + np + cc];
     }
   }
 }
@@ -1253,7 +1264,9 @@ void patch_inverse(const Bsr& A, const Patches& P, int max_nf, cudaStream_t s) {
     const int np = max_nf * BS;
     const size_t smem = sizeof(double) * size_t(np) * 2 * np;
     cudaFuncSetAttribute(k_patch_inverse<BS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    k_patch_inverse<BS><<<P.n, 128, smem, s>>>(A, P);
+    // one thread per augmented column, row groups up to ~256 threads
+    const int W = 2 * np, rg = std::max(1, std::min(np, 256 / W));
+    k_patch_inverse<BS><<<P.n, rg * W, smem, s>>>(A, P, rg);
   });
   HPMG_LAUNCH_CHECK();
 }
