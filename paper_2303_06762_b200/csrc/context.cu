@@ -94,6 +94,7 @@ struct Level {
   int* d_wave_ptr = nullptr;
   dev::PatchRecords rec;
   dev::PatchRecords srec;  // full-inverse records of the one-CTA path
+  dev::PatchRecords rect;  // A^T / S_p^T records of the transposed sweep (advected operators)
   unsigned* flow_flags = nullptr;  // [npatch] completion epochs of the dataflow sweep
   unsigned* flow_ctl = nullptr;    // [2] epoch base, arrival counter
   unsigned* coop_ctl = nullptr;    // [2] grid-barrier state of the persistent sweep
@@ -419,7 +420,11 @@ void linearise_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, const DevRef
 void build_patch_inverses(hpmg_ctx& C, Level& V) {
   if (V.P.n == 0) return;
   dev::patch_inverse(V.A, V.P, V.max_nf, C.s);
-  if (V.P.packed) {  // fixed-stride patch records for the TMA sweep (sweep_rec.cu)
+  // fixed-stride patch records for the TMA sweep (sweep_rec.cu); nonsymmetric
+  // operators: full inverses, plus A^T / S_p^T records for the transposed sweep
+  // (HPMG_NONSYM_RECORDS=0: the direct-gather sweeps of kernels.cu instead)
+  static const bool nonsym_records = !std::getenv("HPMG_NONSYM_RECORDS") || std::atoi(std::getenv("HPMG_NONSYM_RECORDS"));
+  if (V.P.packed || nonsym_records) {
     // every patch facet couples to at most kExt facets outside the patch (triangle meshes)
     double vec_bytes = 0;
     for (int p = 0; p < V.P.n; ++p)
@@ -437,14 +442,20 @@ void build_patch_inverses(hpmg_ctx& C, Level& V) {
       }
     if (V.rec.rec) {  // re-linearisation: same layout, rebuild the record contents in place
       dev::build_records(V.A, V.P, V.rec, C.s);
+      if (V.rect.rec) dev::build_records(V.AT, V.P, V.rect, C.s, true);
       if (V.small) dev::build_records(V.A, V.P, V.srec, C.s);
       return;
     }
     V.P.max_dep = V.plan.max_dep;
     V.P.ndep = dupload(V.plan.patch_ndep, C.s);
     V.P.dep = dupload(V.plan.patch_dep, C.s);
-    V.rec = dev::record_layout(V.bs, V.max_nf);
+    V.rec = dev::record_layout(V.bs, V.max_nf, !V.P.packed);
     V.rec.rec = dalloc<double>(size_t(V.P.n) * V.rec.stride);
+    if (C.advected) {
+      V.rect = V.rec;
+      V.rect.rec = dalloc<double>(size_t(V.P.n) * V.rect.stride);
+      dev::build_records(V.AT, V.P, V.rect, C.s, true);
+    }
     V.rec.n = V.P.n;
     if (const char* d = std::getenv("HPMG_DBG")) V.rec.dbg = std::atoi(d);
     V.flow_flags = dalloc<unsigned>(V.P.n);
@@ -463,7 +474,7 @@ void build_patch_inverses(hpmg_ctx& C, Level& V) {
     // of a coarse base mesh (26 / 50 waves); refined levels have 9 wide waves
     const int nwaves = int(V.wave_ptr.size()) - 1;
     const dev::PatchRecords full = dev::record_layout(V.bs, V.max_nf, true);
-    if (V.k == 0 && nwaves > 12 && dev::small_level_fits(V.nb, full.stride, int(passes.size()))) {
+    if (V.P.packed && V.k == 0 && nwaves > 12 && dev::small_level_fits(V.nb, full.stride, int(passes.size()))) {
       V.srec = full;
       V.srec.rec = dalloc<double>(size_t(V.P.n) * V.srec.stride);
       dev::build_records(V.A, V.P, V.srec, C.s);
@@ -548,7 +559,7 @@ void smooth(hpmg_ctx& C, Level& V, double* x, const double* b, bool post) {
   if (!post) {
     for (int s = 0; s < V.steps; ++s)
       for (int w = 0; w < nw; ++w) {
-        if (V.P.packed) {
+        if (V.rec.rec) {
           dev::gs_wave_rec(V.rec, V.wave_ptr[w], V.wave_ptr[w + 1], b, x, C.s);
         } else {
           next_inv(w + 1 < nw ? w + 1 : (s + 1 < V.steps ? 0 : -1), &pf, &pl);
@@ -578,7 +589,10 @@ void smooth(hpmg_ctx& C, Level& V, double* x, const double* b, bool post) {
   count(C, 2);
   for (int s = 0; s < V.steps; ++s)
     for (int w = nw - 1; w >= 0; --w) {
-      dev::gs_wave(V.AT, V.P, V.wave_ptr[w], V.wave_ptr[w + 1], V.r, V.y, 1, V.max_nf, C.s);
+      if (V.rect.rec)
+        dev::gs_wave_rec(V.rect, V.wave_ptr[w], V.wave_ptr[w + 1], V.r, V.y, C.s);
+      else
+        dev::gs_wave(V.AT, V.P, V.wave_ptr[w], V.wave_ptr[w + 1], V.r, V.y, 1, V.max_nf, C.s);
       count(C);
     }
   dev::axpy(x, 1.0, V.y, V.n, C.s);
@@ -1210,7 +1224,7 @@ void hpmg_destroy(hpmg_ctx* ctx) {
                     (void*)V->Pm.ptr, (void*)V->Pm.col, (void*)V->Pm.val, (void*)V->PT.ptr, (void*)V->PT.col,
                     (void*)V->PT.val, (void*)V->x, (void*)V->b, (void*)V->r, (void*)V->y, (void*)V->bw, (void*)V->xw,
                     (void*)V->dbuf, (void*)V->geo, (void*)V->row_elems, (void*)V->elem_facets, (void*)V->facet_block,
-                    (void*)V->d_wave_ptr, (void*)V->rec.rec, (void*)V->srec.rec, (void*)V->flow_flags,
+                    (void*)V->d_wave_ptr, (void*)V->rec.rec, (void*)V->srec.rec, (void*)V->rect.rec, (void*)V->flow_flags,
                     (void*)V->flow_ctl, (void*)V->coop_ctl, (void*)V->P.ndep, (void*)V->P.dep, (void*)V->d_passes, (void*)V->gath,
                     (void*)V->block_facet, (void*)V->tdev.nmed, (void*)V->tdev.med, (void*)V->tdev.ncol,
                     (void*)V->tdev.col, (void*)V->tdev.pos, (void*)V->tdev.avg_ptr, (void*)V->tdev.avg_col,

@@ -98,7 +98,8 @@ struct PatchRecords {
   int dbg = 0;       // development: 4 = per-CTA globaltimer trace (sweep_trace)
 };
 PatchRecords record_layout(int bs, int max_nf, bool full = false);
-void build_records(const Bsr& A, const Patches& P, PatchRecords& R, cudaStream_t s);
+/// transpose: records of the transposed sweep (A = A^T rows, S_p^T; full layout only)
+void build_records(const Bsr& A, const Patches& P, PatchRecords& R, cudaStream_t s, bool transpose = false);
 /// One symmetric wave over the patch records [w0, w1) (one TMA per CTA).
 void gs_wave_rec(const PatchRecords& R, int w0, int w1, const double* b, double* x, cudaStream_t s);
 void sweep_trace(long long* out);  // development timeline, 5 x 32768 stamps

@@ -255,7 +255,24 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
   if (!kOneCopy) bar_wait(&bar_s);
   sweep_stamp(R, 3);
   double dsum = 0.0;
-  if (row < np) {
+  if (row < np && R.full) {
+    // full inverse (nonsymmetric operators), column-major with the level's
+    // largest patch as column stride: S(t, j) at j*npm + t
+    const int npm = R.max_nf * BS;
+    const double* S = rec + row;
+    const double* rr = r + lp * TP;
+    const int jb = TR == 2 ? part * (np / 2) : 0, je = TR == 2 ? (part + 1) * (np / 2) : np;
+    double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+    int j = jb;
+    for (; j + 3 < je; j += 4) {
+      d0 = fma(S[j * npm], rr[j], d0);
+      d1 = fma(S[(j + 1) * npm], rr[j + 1], d1);
+      d2 = fma(S[(j + 2) * npm], rr[j + 2], d2);
+      d3 = fma(S[(j + 3) * npm], rr[j + 3], d3);
+    }
+    for (; j < je; ++j) d0 = fma(S[j * npm], rr[j], d0);
+    dsum = (d0 + d1) + (d2 + d3);
+  } else if (row < np) {
     // S(t, j): j < t in column j at cs(j) + t - j, j >= t in column t at ct + j,
     // cs(j) = j np - j (j - 1) / 2 the uniform column start (packed lower, by columns);
     // with TR = 2 the two lanes of a row take the columns [0, np/2) and [np/2, np)
@@ -506,7 +523,7 @@ __global__ void k_epoch(unsigned* ctl, int nsweeps) {
 }
 
 /// Builds the records from the packed inverses and the ELL operator.
-__global__ void k_build_records(Bsr A, Patches P, PatchRecords R, int bs) {
+__global__ void k_build_records(Bsr A, Patches P, PatchRecords R, int bs, int transpose) {
   const int p = blockIdx.x;
   double* rec = R.rec + size_t(p) * R.stride;
   const int nf = P.nf[p], np = nf * bs;
@@ -520,8 +537,12 @@ __global__ void k_build_records(Bsr A, Patches P, PatchRecords R, int bs) {
       double v = 0.0;
       const int c = k / npmax, r = k % npmax;
       if (c < np && r < np) {
-        const int lo = r > c ? c : r, hi = r > c ? r : c;
-        v = inv[lo * np - lo * (lo - 1) / 2 + (hi - lo)];
+        if (P.packed) {
+          const int lo = r > c ? c : r, hi = r > c ? r : c;
+          v = inv[lo * np - lo * (lo - 1) / 2 + (hi - lo)];
+        } else {  // full column-major inverse (nonsymmetric); S^T for the transposed sweep
+          v = transpose ? inv[r * np + c] : inv[c * np + r];
+        }
       }
       rec[k] = v;
     }
@@ -664,9 +685,10 @@ PatchRecords record_layout(int bs, int max_nf, bool full) {
   return R;
 }
 
-void build_records(const Bsr& A, const Patches& P, PatchRecords& R, cudaStream_t s) {
+void build_records(const Bsr& A, const Patches& P, PatchRecords& R, cudaStream_t s, bool transpose) {
   if (P.n == 0) return;
-  k_build_records<<<P.n, 128, 0, s>>>(A, P, R, R.bs);
+  if (!P.packed && !R.full) throw std::runtime_error("nonsymmetric patch inverses need full records");
+  k_build_records<<<P.n, 128, 0, s>>>(A, P, R, R.bs, transpose ? 1 : 0);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) throw std::runtime_error(std::string("CUDA launch (build_records): ") + cudaGetErrorString(err));
 }
@@ -683,6 +705,7 @@ namespace {
 template <int BS>
 void launch_coop(const PatchRecords& R, const SweepOrder& O, int nsweeps, const double* b, double* x, unsigned* ctl,
                  cudaStream_t s) {
+  if (R.full) throw std::runtime_error("persistent sweep needs packed patch records");
   constexpr int TP = RecCfg<BS>::TP, G = RecCfg<BS>::G;
   if (R.max_nf * BS * (TP >= 2 * kMaxPatchF * BS ? 2 : 1) > TP)
     throw std::runtime_error("vertex patch too large for the record sweep");
