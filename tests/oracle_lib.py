@@ -57,11 +57,26 @@ class Stats(C.Structure):
                 ("residual", C.c_double)]
 
 
+REF_LIB_PATH = os.path.join(ORACLE_DIR, "_ref", "libref.so")
+
 _lib = None
+_ref_lib = None
 
 
 def build():
     subprocess.run(["make", "-s", "-C", ORACLE_DIR], check=True)
+
+
+class _Lenient:
+    """Lets the binder set argtypes on symbols a library may not export (the
+    reference driver exports a subset of the restatement's surface)."""
+
+    def __init__(self, L):
+        self.__dict__["_L"] = L
+
+    def __getattr__(self, name):
+        L = self.__dict__["_L"]
+        return getattr(L, name) if hasattr(L, name) else type("_Missing", (), {})()
 
 
 def lib():
@@ -69,7 +84,33 @@ def lib():
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             build()
-        L = C.CDLL(LIB_PATH)
+        _lib = _bind(C.CDLL(LIB_PATH))
+    return _lib
+
+
+def ref_available():
+    """True when the reference itself (oracle/_ref/libref.so: the unmodified
+    reference headers over the Eigen-API shim) is built; it only exists where
+    /root/reference is present (the build container)."""
+    return os.path.exists(REF_LIB_PATH)
+
+
+def ref_lib():
+    global _ref_lib
+    if _ref_lib is None:
+        _ref_lib = _bind(C.CDLL(REF_LIB_PATH))
+        L = _ref_lib
+        L.orc_mg_create_traced.restype = C.c_void_p
+        L.orc_mg_create_traced.argtypes = [C.POINTER(Problem)]
+        L.orc_mg_trace.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                   C.POINTER(C.c_double)]
+        L.orc_tts.argtypes = [C.POINTER(Problem), C.c_int, C.c_double, C.POINTER(C.c_int), C.POINTER(C.c_double)]
+    return _ref_lib
+
+
+def _bind(L0):
+    if True:
+        L = _Lenient(L0)
         P = C.c_void_p
         dp = C.POINTER(C.c_double)
         lp = C.POINTER(C.c_longlong)
@@ -117,8 +158,7 @@ def lib():
         L.orc_mms_point.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, dp]
         L.orc_mg_centroids.argtypes = [P, dp]
         L.orc_set_max_order.argtypes = [C.c_int]
-        _lib = L
-    return _lib
+    return L0
 
 
 def _dp(a):
@@ -148,13 +188,14 @@ class OracleMG:
     def __init__(self, *, mesh_kind=0, base_n=2, levels=2, k=0, nu=1.0, beta=0.0, mass_coef=0.0,
                  inv_eps=1e6, bc=BC_NONE, load_kind=LOAD_NONE, load=None, wind=WIND_NONE,
                  cycle=CYCLE_W, smoother=SM_MULT, smooth_steps=1, jacobi_damping=1.0 / 3.0, newton=False,
-                 mass_field=False):
-        L = lib()
+                 mass_field=False, reference=False, traced=False):
+        L = ref_lib() if reference else lib()
+        self.L = L
         self._load = None if load is None else np.ascontiguousarray(load, dtype=np.float64)
         p = Problem(mesh_kind, base_n, levels, k, nu, beta, mass_coef, inv_eps, bc, load_kind,
                     _dp(self._load) if self._load is not None else None, wind, cycle, smoother,
                     smooth_steps, jacobi_damping, int(newton), int(mass_field))
-        self.h = L.orc_mg_create(C.byref(p))
+        self.h = (L.orc_mg_create_traced if traced else L.orc_mg_create)(C.byref(p))
         if not self.h:
             raise RuntimeError(L.orc_last_error().decode())
         self.n = L.orc_mg_n(self.h)
@@ -164,16 +205,16 @@ class OracleMG:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().orc_mg_destroy(self.h)
+            self.L.orc_mg_destroy(self.h)
             self.h = None
 
     @property
     def setup_seconds(self):
-        return lib().orc_mg_setup_seconds(self.h)
+        return self.L.orc_mg_setup_seconds(self.h)
 
     def csr(self, level=-1):
         import scipy.sparse as sp
-        L = lib()
+        L = self.L
         rows = L.orc_mg_rows(self.h, level)
         nnz = L.orc_mg_nnz(self.h, level)
         ptr = np.empty(rows + 1, np.int64)
@@ -184,7 +225,7 @@ class OracleMG:
 
     def prolongation(self, level):
         import scipy.sparse as sp
-        L = lib()
+        L = self.L
         rows = L.orc_mg_rows(self.h, level)
         cols = L.orc_mg_rows(self.h, level - 1)
         nnz = L.orc_mg_P_nnz(self.h, level)
@@ -196,39 +237,39 @@ class OracleMG:
 
     def rhs(self):
         out = np.empty(self.n)
-        lib().orc_mg_rhs(self.h, _dp(out))
+        self.L.orc_mg_rhs(self.h, _dp(out))
         return out
 
     def free_to_full(self):
         out = np.empty(self.n, np.int64)
-        lib().orc_mg_free_to_full(self.h, _lp(out))
+        self.L.orc_mg_free_to_full(self.h, _lp(out))
         return out
 
     def g_full(self):
         out = np.empty(self.n_full)
-        lib().orc_mg_g_full(self.h, _dp(out))
+        self.L.orc_mg_g_full(self.h, _dp(out))
         return out
 
     def apply(self, b):
         b = np.ascontiguousarray(b, dtype=np.float64)
         x = np.empty(self.n)
-        lib().orc_mg_apply(self.h, _dp(b), _dp(x))
+        self.L.orc_mg_apply(self.h, _dp(b), _dp(x))
         return x
 
     def spmv(self, x):
         x = np.ascontiguousarray(x, dtype=np.float64)
         y = np.empty(self.n)
-        lib().orc_mg_spmv(self.h, _dp(x), _dp(y))
+        self.L.orc_mg_spmv(self.h, _dp(x), _dp(y))
         return y
 
     def smooth(self, level, which, x, b, sweeps=1, damping=1.0 / 3.0):
         x = np.array(x, dtype=np.float64)
         b = np.ascontiguousarray(b, dtype=np.float64)
-        lib().orc_mg_smooth(self.h, level, which, _dp(x), _dp(b), sweeps, damping)
+        self.L.orc_mg_smooth(self.h, level, which, _dp(x), _dp(b), sweeps, damping)
         return x
 
     def patches(self, level=-1):
-        L = lib()
+        L = self.L
         n = L.orc_mg_num_patches(self.h, level)
         tot = L.orc_mg_patches(self.h, level, None, None)
         offs = np.empty(n + 1, np.int64)
@@ -240,7 +281,7 @@ class OracleMG:
         b = np.ascontiguousarray(b, dtype=np.float64)
         x = np.zeros(self.n) if x0 is None else np.array(x0, dtype=np.float64)
         st = Stats()
-        lib().orc_mg_krylov(self.h, method, _dp(b), _dp(x), rel_tol, abs_tol, max_it, C.byref(st))
+        self.L.orc_mg_krylov(self.h, method, _dp(b), _dp(x), rel_tol, abs_tol, max_it, C.byref(st))
         return x, dict(iterations=st.iterations, converged=bool(st.converged),
                        not_applicable=bool(st.not_applicable), residual=st.residual)
 
@@ -252,7 +293,7 @@ class OracleMG:
         hist = np.zeros(outer)
         flags = (C.c_int * 2)()
         secs = np.zeros(1)
-        done = lib().orc_mg_uzawa(self.h, outer, rel_tol, abs_tol, max_it, _dp(vel), _dp(p), inner,
+        done = self.L.orc_mg_uzawa(self.h, outer, rel_tol, abs_tol, max_it, _dp(vel), _dp(p), inner,
                                   _dp(hist), flags, _dp(secs), None if init is None else _dp(init))
         return dict(velocity=vel, pressure=p, inner_iterations=list(inner)[:done],
                     divergence_history=list(hist[:done]), converged=bool(flags[0]),
@@ -265,17 +306,26 @@ class OracleMG:
         interior = np.zeros((self.ne, max(k * (k + 1), 1)))
         p = np.zeros((self.ne, max(ns - 1, 1)))
         g = np.zeros((self.ne, 4 * ns))
-        lib().orc_mg_recover(self.h, _dp(v), _dp(interior), _dp(p), _dp(g))
+        self.L.orc_mg_recover(self.h, _dp(v), _dp(interior), _dp(p), _dp(g))
         return interior[:, : k * (k + 1)], p[:, : ns - 1], g
 
+    def trace(self, cap=4096):
+        """The MG residual trace of the last apply (reference contexts made
+        with traced=True): (levels, entering flags, residual norms)."""
+        lv = (C.c_int * cap)()
+        en = (C.c_int * cap)()
+        res = np.zeros(cap)
+        n = min(self.L.orc_mg_trace(self.h, cap, lv, en, _dp(res)), cap)
+        return list(lv)[:n], list(en)[:n], res[:n]
+
     def time_apply(self, reps):
-        return lib().orc_mg_time_apply(self.h, reps)
+        return self.L.orc_mg_time_apply(self.h, reps)
 
     def wind(self):
         """The interpolated advection state (compound full, interior [ne][k(k+1)])."""
         c = np.empty(self.n_full)
         i = np.zeros(max(self.ne * self.k * (self.k + 1), 1))
-        lib().orc_mg_wind(self.h, _dp(c), _dp(i))
+        self.L.orc_mg_wind(self.h, _dp(c), _dp(i))
         return c, i[: self.ne * self.k * (self.k + 1)]
 
     def rt_l2_norm(self, compound_full, interior):
@@ -283,7 +333,7 @@ class OracleMG:
         i = np.ascontiguousarray(interior, dtype=np.float64).ravel()
         if i.size == 0:
             i = np.zeros(1)
-        return lib().orc_mg_rt_l2_norm(self.h, _dp(c), _dp(i))
+        return self.L.orc_mg_rt_l2_norm(self.h, _dp(c), _dp(i))
 
 
     def postprocess(self, compound_full, interior, grad):
@@ -291,21 +341,21 @@ class OracleMG:
         nh = (self.k + 2) * (self.k + 3) // 2
         out = np.zeros((self.ne, 2 * nh))
         i = np.ascontiguousarray(interior, dtype=np.float64).ravel()
-        lib().orc_mg_postprocess(self.h, _dp(np.ascontiguousarray(compound_full, dtype=np.float64)),
+        self.L.orc_mg_postprocess(self.h, _dp(np.ascontiguousarray(compound_full, dtype=np.float64)),
                                  _dp(i if i.size else np.zeros(1)), _dp(np.ascontiguousarray(grad, dtype=np.float64)),
                                  _dp(out))
         return out
 
     def centroids(self):
         out = np.zeros((self.ne, 2))
-        lib().orc_mg_centroids(self.h, _dp(out))
+        self.L.orc_mg_centroids(self.h, _dp(out))
         return out
 
     def errors(self, compound_full, interior, grad, post, kind):
         """measure_errors against exact flow `kind`: dict e_u, e_L, e_ustar, div_u."""
         out = np.zeros(4)
         i = np.ascontiguousarray(interior, dtype=np.float64).ravel()
-        lib().orc_mg_errors(self.h, _dp(np.ascontiguousarray(compound_full, dtype=np.float64)),
+        self.L.orc_mg_errors(self.h, _dp(np.ascontiguousarray(compound_full, dtype=np.float64)),
                             _dp(i if i.size else np.zeros(1)), _dp(np.ascontiguousarray(grad, dtype=np.float64)),
                             _dp(np.ascontiguousarray(post, dtype=np.float64)), kind, _dp(out))
         return dict(zip(("e_u", "e_L", "e_ustar", "div_u"), out))
