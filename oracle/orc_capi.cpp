@@ -116,6 +116,7 @@ struct Problem {
   AsmOpt opt;
   std::unique_ptr<MG> mg;
   Real setup_seconds = 0;
+  int restart = 0;  // GMRES(m) cycle length for krylov / uzawa calls (0: unrestarted)
 };
 
 Mesh base_mesh(const orc_problem* p) {
@@ -185,6 +186,8 @@ void* orc_mg_create(const orc_problem* p) {
 }
 
 void orc_mg_destroy(void* h) { delete static_cast<Problem*>(h); }
+/// GMRES(m) cycle length used by the next orc_mg_krylov / orc_mg_uzawa calls.
+void orc_mg_set_restart(void* h, int m) { static_cast<Problem*>(h)->restart = m; }
 double orc_mg_setup_seconds(void* h) { return static_cast<Problem*>(h)->setup_seconds; }
 long long orc_mg_n(void* h) { return static_cast<Problem*>(h)->mg->constraints().n_free; }
 long long orc_mg_n_full(void* h) { return static_cast<Problem*>(h)->mg->constraints().n_full; }
@@ -271,7 +274,7 @@ void orc_mg_krylov(void* h, int method, const double* b, double* x, double rel_t
   auto* p = static_cast<Problem*>(h);
   Index n = p->mg->constraints().n_free;
   Vec bv(b, b + n), xv(x, x + n);
-  KrylovOpt o{rel_tol, abs_tol, max_it};
+  KrylovOpt o{rel_tol, abs_tol, max_it, p->restart};
   Op A = [p](const Vec& v) { return p->mg->matrix().mul(v); };
   Op M = [p](const Vec& v) { return p->mg->apply(v); };
   SolveStats st = method == 0 ? pcg(A, M, bv, xv, o) : gmres(A, M, bv, xv, o);
@@ -289,7 +292,7 @@ int orc_mg_uzawa(void* h, int outer, double rel_tol, double abs_tol, int max_it,
   auto* p = static_cast<Problem*>(h);
   UzawaOpt o;
   o.outer_iterations = outer;
-  o.krylov = {rel_tol, abs_tol, max_it};
+  o.krylov = {rel_tol, abs_tol, max_it, p->restart};
   Vec init;
   if (initial_full) {  // warm start (UzawaOptions::initial_velocity)
     init.assign(initial_full, initial_full + p->mg->constraints().n_full);

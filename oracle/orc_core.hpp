@@ -96,6 +96,22 @@ struct LU {
   std::vector<int> piv;  // row permutation: row i of PA = row piv[i] of A
   LU() = default;
   explicit LU(const Mat& A) { factor(A); }
+  /// Diagnostic variant (ORC_VARIANT, orc_mg.hpp): solves by an explicit
+  /// inverse (columns solve(e_j)) applied as a mat-vec, the device's
+  /// formulation, to measure how much that arithmetic alone moves results.
+  Mat inv;
+  bool use_inv = false;
+  void make_inverse() {
+    Mat X(n, n);
+    for (int j = 0; j < n; ++j) {
+      Vec e(n, 0.0);
+      e[j] = 1.0;
+      Vec c = solve(e);
+      for (int i = 0; i < n; ++i) X(i, j) = c[i];
+    }
+    inv = X;
+    use_inv = true;
+  }
   void factor(const Mat& A) {
     assert(A.r == A.c);
     n = A.r;
@@ -122,6 +138,15 @@ struct LU {
     }
   }
   Vec solve(const Vec& b) const {
+    if (use_inv) {
+      Vec x(n, 0.0);
+      for (int i = 0; i < n; ++i) {
+        Real s = 0;
+        for (int j = 0; j < n; ++j) s += inv(i, j) * b[j];
+        x[i] = s;
+      }
+      return x;
+    }
     Vec y(n);
     for (int i = 0; i < n; ++i) y[i] = b[piv[i]];
     for (int i = 0; i < n; ++i) {
@@ -138,6 +163,15 @@ struct LU {
   }
   /// Solves A^T x = b (reference inc/smoother.hpp:88, lu.transpose().solve).
   Vec solve_t(const Vec& b) const {
+    if (use_inv) {
+      Vec x(n, 0.0);
+      for (int i = 0; i < n; ++i) {
+        Real s = 0;
+        for (int j = 0; j < n; ++j) s += inv(j, i) * b[j];
+        x[i] = s;
+      }
+      return x;
+    }
     // A^T = U^T L^T P  =>  U^T z = b, L^T w = z, x = P^T w
     Vec z(b);
     for (int i = 0; i < n; ++i) {

@@ -288,6 +288,20 @@ inline std::vector<std::vector<Index>> velocity_patches(const Space& V, const Co
 /// Overlapping vertex-patch smoother with exact dense patch solves
 /// (inc/smoother.hpp:35-100). A^T is held as a CSR of the transpose so that
 /// "column i of A" reads as row i of AT.
+/// Diagnostic arithmetic variants (env ORC_VARIANT, a bit mask; default 0 =
+/// the reference's arithmetic): 1 patch solves by explicit inverses, 2 the
+/// coarse solve by an explicit inverse, 4 "pull" sweeps (each patch recomputes
+/// its residual rows b_p - A_p x from the current iterate instead of updating
+/// a running residual). All are exact-arithmetic identities; they exist to
+/// attribute device-vs-reference differences (tools/variant_floor.py).
+inline int variant() {
+  static const int v = [] {
+    const char* e = std::getenv("ORC_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 class PatchSmoother {
  public:
   PatchSmoother(const Csr& A, const Csr& AT, std::vector<std::vector<Index>> patches)
@@ -299,10 +313,16 @@ class PatchSmoother {
       for (int r = 0; r < np; ++r)
         for (int c = 0; c < np; ++c) App(r, c) = a_->coeff(p[r], p[c]);
       lu_.emplace_back(App);
+      if (variant() & 1) lu_.back().make_inverse();
     }
   }
   const std::vector<std::vector<Index>>& patches() const { return patches_; }
   void forward(Vec& x, const Vec& b, int sweeps) const {
+    if (variant() & 4) {  // pull: r_p = b_p - A_p x at patch time
+      for (int s = 0; s < sweeps; ++s)
+        for (std::size_t j = 0; j < patches_.size(); ++j) pull_patch(j, x, b, *a_, false);
+      return;
+    }
     Vec r = residual(x, b);
     for (int s = 0; s < sweeps; ++s)
       for (std::size_t j = 0; j < patches_.size(); ++j) apply_patch(j, x, r, *at_, false);
@@ -310,8 +330,13 @@ class PatchSmoother {
   void backward(Vec& x, const Vec& b, int sweeps) const {
     Vec y(x.size(), 0.0);
     Vec r = residual(x, b);
-    for (int s = 0; s < sweeps; ++s)
-      for (std::size_t j = patches_.size(); j-- > 0;) apply_patch(j, y, r, *a_, true);
+    if (variant() & 4) {  // pull: r_p = r0_p - (A^T)_p y at patch time
+      for (int s = 0; s < sweeps; ++s)
+        for (std::size_t j = patches_.size(); j-- > 0;) pull_patch(j, y, r, *at_, true);
+    } else {
+      for (int s = 0; s < sweeps; ++s)
+        for (std::size_t j = patches_.size(); j-- > 0;) apply_patch(j, y, r, *a_, true);
+    }
     for (std::size_t i = 0; i < x.size(); ++i) x[i] += y[i];
   }
   void jacobi(Vec& x, const Vec& b, int sweeps, Real damping) const {
@@ -344,6 +369,18 @@ class PatchSmoother {
       x[p[i]] += d[i];
       for (Index q = cols_of.ptr[p[i]]; q < cols_of.ptr[p[i] + 1]; ++q) r[cols_of.idx[q]] -= cols_of.val[q] * d[i];
     }
+  }
+  // rows_of: ROW i gives residual row i as a function of the iterate
+  void pull_patch(std::size_t j, Vec& x, const Vec& b, const Csr& rows_of, bool transposed) const {
+    const auto& p = patches_[j];
+    Vec rp(p.size());
+    for (std::size_t i = 0; i < p.size(); ++i) {
+      Real s = b[p[i]];
+      for (Index q = rows_of.ptr[p[i]]; q < rows_of.ptr[p[i] + 1]; ++q) s -= rows_of.val[q] * x[rows_of.idx[q]];
+      rp[i] = s;
+    }
+    Vec d = transposed ? lu_[j].solve_t(rp) : lu_[j].solve(rp);
+    for (std::size_t i = 0; i < p.size(); ++i) x[p[i]] += d[i];
   }
   const Csr* a_;
   const Csr* at_;
@@ -403,6 +440,7 @@ class MG {
       }
     }
     coarse_ = LU(h_[0].A.dense());
+    if (variant() & 2) coarse_.make_inverse();
     for (int l = 1; l <= L; ++l) {
       Csr avg = averaging_transfer(h_[l - 1].V, h_[l - 1].con, h_[l].V, h_[l].con, hier.maps[l - 1]);
       h_[l].P = corrected_prolongation(avg, h_[l].A, interior_patch_dofs(h_[l].V, h_[l].con, hier.maps[l - 1]));
@@ -502,6 +540,12 @@ using Op = std::function<Vec(const Vec&)>;
 struct KrylovOpt {
   Real rel_tol = 1e-8, abs_tol = 1e-10;
   int max_iterations = 500;
+  /// GMRES(m) cycle length (BASELINE config 5's restarted GMRes(50)); 0 =
+  /// the reference's unrestarted method (krylov.hpp:79-84). An extension of
+  /// the reference: a cycle that reaches m Arnoldi steps forms its update
+  /// and restarts from the true residual exactly like a recurrence-converged
+  /// cycle that failed the true-residual check (krylov.hpp:127-143).
+  int restart = 0;
 };
 struct SolveStats {
   int iterations = 0;
@@ -558,7 +602,8 @@ inline SolveStats gmres(const Op& A, const Op& M, const Vec& b, Vec& x, const Kr
     std::vector<Vec> hc;
     Vec cs, sn, g{beta};
     bool stalled = false;
-    for (int j = 0; st.iterations < o.max_iterations; ++j) {
+    const int cap = o.restart > 0 ? o.restart : (1 << 30);
+    for (int j = 0; st.iterations < o.max_iterations && j < cap; ++j) {
       Vec w = A(M(V[j]));
       Vec h(j + 2, 0.0);
       for (int i = 0; i <= j; ++i) {

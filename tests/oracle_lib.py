@@ -60,7 +60,7 @@ class Stats(C.Structure):
 REF_LIB_PATH = os.path.join(ORACLE_DIR, "_ref", "libref.so")
 
 _lib = None
-_ref_lib = None
+_ref_libs = {}
 
 
 def build():
@@ -95,17 +95,20 @@ def ref_available():
     return os.path.exists(REF_LIB_PATH)
 
 
-def ref_lib():
-    global _ref_lib
-    if _ref_lib is None:
-        _ref_lib = _bind(C.CDLL(REF_LIB_PATH))
-        L = _ref_lib
+def ref_lib(variant=""):
+    """The reference build (variant "": oracle/_ref/libref.so; "fma": the same
+    sources compiled with FMA contraction, oracle/_ref/libref_fma.so, used to
+    measure the reference's own round-off floor)."""
+    if variant not in _ref_libs:
+        path = REF_LIB_PATH if not variant else os.path.join(ORACLE_DIR, "_ref", f"libref_{variant}.so")
+        _ref_libs[variant] = _bind(C.CDLL(path))
+        L = _ref_libs[variant]
         L.orc_mg_create_traced.restype = C.c_void_p
         L.orc_mg_create_traced.argtypes = [C.POINTER(Problem)]
         L.orc_mg_trace.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                    C.POINTER(C.c_double)]
         L.orc_tts.argtypes = [C.POINTER(Problem), C.c_int, C.c_double, C.POINTER(C.c_int), C.POINTER(C.c_double)]
-    return _ref_lib
+    return _ref_libs[variant]
 
 
 def _bind(L0):
@@ -137,6 +140,7 @@ def _bind(L0):
                      "orc_mg_setup_seconds"]:
             getattr(L, name).argtypes = [P]
         L.orc_mg_time_apply.argtypes = [P, C.c_int]
+        L.orc_mg_set_restart.argtypes = [P, C.c_int]
         # every handle-taking entry point gets an explicit void* first argument
         # (an untyped Python int would be truncated to 32 bits)
         L.orc_mg_rows.argtypes = [P, C.c_int]
@@ -189,7 +193,7 @@ class OracleMG:
                  inv_eps=1e6, bc=BC_NONE, load_kind=LOAD_NONE, load=None, wind=WIND_NONE,
                  cycle=CYCLE_W, smoother=SM_MULT, smooth_steps=1, jacobi_damping=1.0 / 3.0, newton=False,
                  mass_field=False, reference=False, traced=False):
-        L = ref_lib() if reference else lib()
+        L = (ref_lib("" if reference is True else reference)) if reference else lib()
         self.L = L
         self._load = None if load is None else np.ascontiguousarray(load, dtype=np.float64)
         p = Problem(mesh_kind, base_n, levels, k, nu, beta, mass_coef, inv_eps, bc, load_kind,
@@ -308,6 +312,11 @@ class OracleMG:
         g = np.zeros((self.ne, 4 * ns))
         self.L.orc_mg_recover(self.h, _dp(v), _dp(interior), _dp(p), _dp(g))
         return interior[:, : k * (k + 1)], p[:, : ns - 1], g
+
+    def set_restart(self, m):
+        """GMRES(m) for the following krylov/uzawa calls (restatement only:
+        the reference's GMRES is unrestarted)."""
+        self.L.orc_mg_set_restart(self.h, int(m))
 
     def trace(self, cap=4096):
         """The MG residual trace of the last apply (reference contexts made
