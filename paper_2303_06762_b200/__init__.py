@@ -445,8 +445,16 @@ class MGPreconditioner:
         self._check(lib().hpmg_write_matrix_market(self.h, level, os.fsencode(path)))
 
     # -- operators (host numpy in, host numpy out)
+    def _vec(self, v, name="vector"):
+        """A C-contiguous float64 host copy/view of length n (the native side
+        reads exactly n doubles through the raw pointer)."""
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        if v.ndim != 1 or v.shape[0] != self.n:
+            raise ValueError(f"{name} must have shape ({self.n},), got {v.shape}")
+        return v
+
     def apply(self, b):
-        b = np.ascontiguousarray(b, dtype=np.float64)
+        b = self._vec(b, "b")
         z = np.empty(self.n)
         self._check(lib().hpmg_apply(self.h, b.ctypes.data, z.ctypes.data, 0))
         return z
@@ -455,16 +463,23 @@ class MGPreconditioner:
         """apply() over independent host vectors with the PCIe copies of
         neighbouring vectors overlapped with the V-cycles (hpmg_apply_batch).
         rs / zs: sequences of float64 host arrays (pinned for overlap)."""
-        rs = [np.ascontiguousarray(r, dtype=np.float64) for r in rs]
+        rs = [self._vec(r, "rs[i]") for r in rs]
         if zs is None:
             zs = [np.empty(self.n) for _ in rs]
+        if len(zs) != len(rs):
+            raise ValueError(f"apply_batch: {len(rs)} inputs but {len(zs)} outputs")
+        for z in zs:  # written in place by the native side: no silent copies
+            if not (isinstance(z, np.ndarray) and z.dtype == np.float64 and z.ndim == 1 and z.shape[0] == self.n
+                    and z.flags.c_contiguous and z.flags.writeable):
+                raise ValueError(f"apply_batch: every output must be a writable C-contiguous float64 array of "
+                                 f"length {self.n}")
         rp = (C.c_void_p * len(rs))(*[r.ctypes.data for r in rs])
         zp = (C.c_void_p * len(zs))(*[z.ctypes.data for z in zs])
         self._check(lib().hpmg_apply_batch(self.h, len(rs), rp, zp))
         return zs
 
     def spmv(self, x):
-        x = np.ascontiguousarray(x, dtype=np.float64)
+        x = self._vec(x, "x")
         y = np.empty(self.n)
         self._check(lib().hpmg_spmv(self.h, x.ctypes.data, y.ctypes.data, 0))
         return y
@@ -472,6 +487,9 @@ class MGPreconditioner:
     def smooth(self, level, which, x, b, sweeps=1):
         x = np.array(x, dtype=np.float64)
         b = np.ascontiguousarray(b, dtype=np.float64)
+        nl = self.level_n(level)
+        if x.shape != (nl,) or b.shape != (nl,):
+            raise ValueError(f"smooth: x and b must have shape ({nl},)")
         self._check(lib().hpmg_smooth(self.h, level, which, x.ctypes.data, b.ctypes.data, sweeps, 0))
         return x
 
@@ -553,8 +571,8 @@ class MGPreconditioner:
 def pcg(B: MGPreconditioner, b, x=None, opt: KrylovOptions | None = None):
     """Device PCG with B.matrix() and B.apply (reference krylov.hpp:30-73)."""
     opt = opt or KrylovOptions()
-    b = np.ascontiguousarray(b, dtype=np.float64)
-    x = np.zeros(B.n) if x is None else np.array(x, dtype=np.float64)
+    b = B._vec(b, "b")
+    x = np.zeros(B.n) if x is None else B._vec(np.array(x, dtype=np.float64), "x")
     st = _Stats()
     B._check(lib().hpmg_pcg(B.h, b.ctypes.data, x.ctypes.data, C.byref(opt.c()), C.byref(st), 0))
     return x, SolveStats(st.iterations, bool(st.converged), bool(st.not_applicable), st.residual)
@@ -563,8 +581,8 @@ def pcg(B: MGPreconditioner, b, x=None, opt: KrylovOptions | None = None):
 def gmres(B: MGPreconditioner, b, x=None, opt: KrylovOptions | None = None):
     """Device right-preconditioned MGS GMRES (reference krylov.hpp:79-144)."""
     opt = opt or KrylovOptions()
-    b = np.ascontiguousarray(b, dtype=np.float64)
-    x = np.zeros(B.n) if x is None else np.array(x, dtype=np.float64)
+    b = B._vec(b, "b")
+    x = np.zeros(B.n) if x is None else B._vec(np.array(x, dtype=np.float64), "x")
     st = _Stats()
     B._check(lib().hpmg_gmres(B.h, b.ctypes.data, x.ctypes.data, C.byref(opt.c()), C.byref(st), 0))
     return x, SolveStats(st.iterations, bool(st.converged), bool(st.not_applicable), st.residual)
@@ -579,6 +597,8 @@ def uzawa_solve(B: MGPreconditioner, outer_iterations=2, krylov: KrylovOptions |
     p = np.empty(B.ne)
     rep = _UReport()
     init = None if initial_velocity is None else np.ascontiguousarray(initial_velocity, dtype=np.float64)
+    if init is not None and init.shape != (B.n_full,):
+        raise ValueError(f"initial_velocity must have shape ({B.n_full},)")
     o = _UOpts(outer_iterations, krylov.c(), None if init is None else _dp(init))
     B._check(lib().hpmg_uzawa(B.h, C.byref(o), _dp(vel), _dp(p), C.byref(rep)))
     r = UzawaReport(list(rep.inner_iterations[: rep.n_outer]), list(rep.divergence_history[: rep.n_outer]),

@@ -424,7 +424,18 @@ void build_patch_inverses(hpmg_ctx& C, Level& V) {
   // operators: full inverses, plus A^T / S_p^T records for the transposed sweep
   // (HPMG_NONSYM_RECORDS=0: the direct-gather sweeps of kernels.cu instead)
   static const bool nonsym_records = !std::getenv("HPMG_NONSYM_RECORDS") || std::atoi(std::getenv("HPMG_NONSYM_RECORDS"));
-  if (V.P.packed || nonsym_records) {
+  bool use_records = V.P.packed || nonsym_records;
+  if (use_records && !V.P.packed && !V.rec.rec) {
+    // nonsymmetric records hold full inverses twice (S_p and S_p^T sets, ~5x the
+    // packed footprint at k = 3): where they do not fit next to a safety margin,
+    // stay on the direct-gather sweeps (same results) instead of failing setup
+    const dev::PatchRecords lay = dev::record_layout(V.bs, V.max_nf, true);
+    const double need = 8.0 * double(V.P.n) * double(lay.stride) * (C.advected ? 2.0 : 1.0);
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    if (need + 0.05 * double(total_b) > double(free_b)) use_records = false;
+  }
+  if (use_records) {
     // every patch facet couples to at most kExt facets outside the patch (triangle meshes)
     double vec_bytes = 0;
     for (int p = 0; p < V.P.n; ++p)

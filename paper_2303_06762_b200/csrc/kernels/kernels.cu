@@ -893,7 +893,7 @@ __global__ void __launch_bounds__(256) k_gj_implicit(int n, double* __restrict__
     }
     gj_block_argmax(bv, p, sv, si);
     if (b == 0 && threadIdx.x == 0) {
-      piv[k] = p;
+      piv[k] = p < n ? p : 0;  // an all-NaN column leaves p = n: keep k_gj_extract_piv in bounds
       if (!(bv > 0.0)) *status = 1;  // singular
     }
     if (p >= n) p = 0;  // singular (flagged above): keep the addressing in bounds

@@ -125,6 +125,7 @@ extern "C" int hpmg_ns_solve(const hpmg_mesh_desc* mesh, const hpmg_options* opt
     if (!linear_step(aopt, base, nullptr, stokes_inner, &nstokes, 64)) return finish(0);
     prev = cur;
     // Picard (ns.hpp:106-123)
+    double last_picard_diff = 0.0;
     for (int n = 0; n < ns->max_picard; ++n) {
       hpmg_options o = aopt;
       hpmg_problem p = base;
@@ -139,12 +140,13 @@ extern "C" int hpmg_ns_solve(const hpmg_mesh_desc* mesh, const hpmg_options* opt
       ++rep->picard_iterations;
       const double d = diff(cur, prev);
       if (n < 128) rep->picard_diffs[n] = d;
+      last_picard_diff = d;
       prev = cur;
       if (d < ns->picard_tol) break;
     }
     if (ns->max_newton == 0) {
-      const int np = rep->picard_iterations;
-      rep->converged = np > 0 && rep->picard_diffs[std::min(np, 128) - 1] < ns->picard_tol;
+      // the last step's difference (picard_diffs keeps only the first 128)
+      rep->converged = rep->picard_iterations > 0 && last_picard_diff < ns->picard_tol;
       return finish(0);
     }
     // Newton (ns.hpp:130-147)
