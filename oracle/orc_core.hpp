@@ -24,7 +24,11 @@
 
 namespace orc {
 
+#ifdef ORC_REAL
+using Real = ORC_REAL;  // extended-precision diagnostic build (oracle/hp_solve.cpp)
+#else
 using Real = double;
+#endif
 using Index = std::int64_t;
 using Vec = std::vector<Real>;
 
@@ -273,7 +277,7 @@ struct SVD {
             gamma += B(i, p) * B(i, q);
           }
           if (gamma == 0.0) continue;
-          Real rel = std::abs(gamma) / std::sqrt(std::max(alpha * beta, 1e-300));
+          Real rel = std::abs(gamma) / std::sqrt(std::max(alpha * beta, Real(1e-300)));
           off = std::max(off, rel);
           if (rel < 1e-16) continue;
           Real zeta = (beta - alpha) / (2 * gamma);

@@ -66,6 +66,28 @@ def _run(name, use_reference, restart, seed):
                 setup_s=t1 - t0, solve_s=time.time() - t1)
 
 
+HP_SOLVE = os.path.join(O.ORACLE_DIR, "_build", "hp_solve")
+
+
+def _run_hp(name, seed):
+    """The restatement in extended precision (oracle/hp_solve.cpp, Real =
+    long double) on a homogeneous-Dirichlet Stokes config: the yardstick for
+    how far a double-precision run of the algorithm lands from its
+    exact-arithmetic result."""
+    import subprocess
+    import tempfile
+
+    kw, n, _, wind = config_problem(name)
+    assert wind is None
+    t0 = time.time()
+    with tempfile.NamedTemporaryFile(suffix=".bin") as f:
+        out = subprocess.run([HP_SOLVE, str(kw["base_n"]), str(kw["levels"]), str(kw["k"]), repr(kw["beta"]),
+                              repr(kw["inv_eps"]), str(seed), f.name], capture_output=True, text=True, check=True)
+        vel = np.fromfile(f.name)
+    return dict(name=name, reference=False, restart="hp", inner=[int(v) for v in out.stdout.split()],
+                velocity=vel, converged=True, setup_s=0.0, solve_s=time.time() - t0)
+
+
 class RefPool:
     """Submits named runs at construction; result(name, ...) blocks on one."""
 
@@ -73,7 +95,10 @@ class RefPool:
         workers = workers or max(1, min(len(runs), (os.cpu_count() or 2) - 1))
         self.ex = cf.ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("spawn"))
         self.fut = {}
-        for name, restart in runs:
+        for name, restart in runs:  # restart: 0 unrestarted, m > 0 GMRES(m), "hp" extended precision
+            if restart == "hp":
+                self.fut[(name, restart)] = self.ex.submit(_run_hp, name, 1)
+                continue
             use_ref = O.ref_available() and not restart
             self.fut[(name, restart)] = self.ex.submit(_run, name, use_ref, restart, 1)
 

