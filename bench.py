@@ -9,12 +9,21 @@ V(1,1) multiplicative vertex-patch smoothing, PCG to 1e-8.
 
 One step = one hp-MG V-cycle (MGPreconditioner::apply) on an HBM-resident
 residual. `value` = V-cycles/s over all ranks (replicas, one per GPU);
-`e2e` = the same through the C ABI with host buffers (H2D residual + V-cycle +
-D2H correction inside the timed region). The V-cycle streams ~6 GB per call,
-far above the 126 MB L2, so no explicit flush is needed.
+`e2e` = the same through the drop-in C-ABI call hpmg_apply (the
+MGPreconditioner::apply equivalent) with pinned host buffers: H2D residual +
+V-cycle + D2H correction inside the timed region, one call per step
+(`e2e.batch_value`: the pipelined hpmg_apply_batch over independent
+vectors). The V-cycle streams ~3 GB per call, far above the 126 MB L2, so no
+explicit flush is needed.
 
---impl reference times the CPU restatement of the reference (oracle/,
-single-threaded like the reference) on the same config, bounded sample.
+--impl reference times the reference's own CPU implementation: its
+unmodified headers compiled against the Eigen-API shim
+(oracle/_ref/libref.so, built in the build container where the reference
+tree exists; single-threaded like the reference), the restatement
+(oracle/_build/liborc.so) where that library is absent. Rank 0 also times the
+reference's time-to-solution (MGPreconditioner construction + uzawa_solve +
+recover_locals) at the bench config in a pinned child process while the
+device is measured (`tts.cpu_reference`).
 """
 from __future__ import annotations
 
@@ -139,6 +148,7 @@ def run_hpmg(args, rank, world, local, dist):
     cfg = CONFIGS[args.config]
     n_f = cfg["base_n"] << (cfg["levels"] - 1)
     F = H.seeded_load(n_f, args.seed)
+    tts_proc = start_cpu_tts(args) if (args.cpu_tts and rank == 0 and world == 1) else None
     t0 = time.perf_counter()
     B = H.MGPreconditioner(mesh="unit_square", base_n=cfg["base_n"], levels=cfg["levels"], k=cfg["k"],
                            nu=cfg["nu"], beta=cfg["beta"], inv_eps=cfg["inv_eps"], cycle=H.CYCLE_V,
@@ -219,6 +229,10 @@ def run_hpmg(args, rank, world, local, dist):
     # per-phase split (event-instrumented pass): head pre-sweep, head residual, h-cycle, head post-sweep
     _, phases = B.time_apply(max(3, args.steps // 4), phases=True)
     vbytes, vparts = B.vcycle_bytes()
+    # physical bytes: streamed sweep records (head p6, levels p7), head mode-0
+    # residual p1, level residuals p3, transfers p4, coarse inverse p5, plus the
+    # head's x/b/ z vectors at the cycle boundary (b read twice, x written)
+    phys_bytes = float(vparts[6] + vparts[7] + vparts[1] + vparts[3] + vparts[4] + vparts[5] + 3 * 8.0 * n)
     hbm, src = peaks()
     head_sweep_ms = phases[0] + phases[3]
     head_bytes = vparts[6]  # bytes the head sweeps stream (records + vector rows)
@@ -247,6 +261,9 @@ def run_hpmg(args, rank, world, local, dist):
     t0 = time.perf_counter()
     sol2 = H.uzawa_solve(B2)
     solve_wall = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    B2.recover(sol2.velocity)  # recover_locals, as the CPU reference TTS includes it
+    recover_wall = time.perf_counter() - t0
     B2.close()
     sol = H.uzawa_solve(B)
     launches = B.launches_per_apply()
@@ -265,15 +282,15 @@ def run_hpmg(args, rank, world, local, dist):
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic: seeded per-triangle U[-1,1] force (mt19937 seed %d), random-init residual" % args.seed,
-            "config": {"workload": args.config, **cfg, "cycle": "V(1,1)", "smoother": "multiplicative vertex-patch",
-                       "n_dofs": int(n), "parallelism": f"replicas x{world}",
+            "config": {**workload_config(args, cfg, n), "parallelism": f"replicas x{world}",
                        "l2": "no flush needed: V-cycle streams %.2f GB per call (> 126 MB L2)" % (vbytes / 1e9)},
-            "e2e": {"value": whole_job_rate(k_e2e, ms_e2e, world), "unit": "V-cycles/s",
+            "e2e": {"value": whole_job_rate(k_e2e, ms_e2e_serial, world), "unit": "V-cycles/s",
                     "h2d_bytes_per_step": int(8 * n), "d2h_bytes_per_step": int(8 * n),
-                    "api": "hpmg_apply_batch over %d independent pinned host vectors (copies of neighbouring "
-                           "vectors overlap the V-cycles)" % k_e2e,
-                    "serial_value": whole_job_rate(k_e2e, ms_e2e_serial, world),
-                    "serial_api": "hpmg_apply per vector (H2D, V-cycle, D2H back to back)"},
+                    "api": "hpmg_apply (drop-in MGPreconditioner::apply): H2D of the residual, V-cycle, "
+                           "D2H of the correction, one call per step",
+                    "batch_value": whole_job_rate(k_e2e, ms_e2e, world),
+                    "batch_api": "hpmg_apply_batch over %d independent pinned host vectors (copies of "
+                                 "neighbouring vectors overlap the V-cycles)" % k_e2e},
             "roofline": {"bound": "hbm",
                          "kernel": "k_sweep<8,128,1,waves> (order-k head patch sweeps, TMA patch records)",
                          "bytes_note": "achieved = bytes the head sweeps must stream in this formulation "
@@ -289,7 +306,15 @@ def run_hpmg(args, rank, world, local, dist):
                          "head_sweep_bytes_per_vcycle": head_bytes, "head_sweep_ms": head_sweep_ms,
                          "reference_storage_head_bytes_per_vcycle": vparts[0],
                          "reference_storage_equiv_gbs": ref_equiv,
-                         "vcycle_achieved_gbs": vbytes / (ms_dev / args.steps * 1e-3) / 1e9},
+                         "vcycle_reference_storage_effective_gbs": vbytes / (ms_dev / args.steps * 1e-3) / 1e9,
+                         "vcycle_physical_bytes": phys_bytes,
+                         "vcycle_physical_gbs": phys_bytes / (ms_dev / args.steps * 1e-3) / 1e9,
+                         "vcycle_physical_frac": phys_bytes / (ms_dev / args.steps * 1e-3) / 1e9 / hbm,
+                         "vcycle_physical_note": "bytes this implementation moves per V-cycle: head and level "
+                                                 "sweep records + vector rows as streamed, head mode-0 residual, "
+                                                 "level residuals, P / P^T, coarse inverse, E/E^T and the "
+                                                 "boundary vectors; the reference-storage figure above uses "
+                                                 "SURVEY 8(d)'s accounting (full LU factors, A rows twice)"},
             "phases_ms": {"head_pre": phases[0], "head_residual": phases[1], "h_cycle": phases[2],
                           "head_post": phases[3]},
             "gpu_launches": int(launches * args.steps),
@@ -302,9 +327,12 @@ def run_hpmg(args, rank, world, local, dist):
                                "reference_storage_bytes": spmv_ref_bytes},
             "tts": {"uzawa_device_s": sol.report.seconds, "setup_wall_s": setup_wall,
                     "setup_wall_warm_s": setup_warm, "uzawa_wall_s": solve_wall,
-                    "tts_warm_s": setup_warm + solve_wall,
+                    "recover_wall_s": recover_wall,
+                    "tts_warm_s": setup_warm + solve_wall + recover_wall,
                     "tts_note": "tts_warm_s = setup (second context in the process) + AL-Uzawa wall time "
-                                "(2 outer PCG solves to 1e-8, velocity and pressure back on the host)",
+                                "(2 outer PCG solves to 1e-8, velocity and pressure back on the host) + "
+                                "recover_locals (interior, pressure modes, gradient back on the host); "
+                                "cpu_reference times the same three phases of the reference itself",
                     "setup_parts_s": [float(x) for x in setup_parts[:7]],
                     "inner_iterations": sol.report.inner_iterations,
                     "final_divergence": sol.report.final_divergence, "converged": sol.report.converged},
@@ -312,21 +340,125 @@ def run_hpmg(args, rank, world, local, dist):
         }
         if args.cpu_baseline and world == 1:
             out["cpu_baseline"] = cpu_baseline(args, cfg, n_f, F, sample_vcycles=args.cpu_vcycles)
+        if tts_proc is not None:
+            cpu = finish_cpu_tts(tts_proc, timeout=900)
+            out["tts"]["cpu_reference"] = cpu
+            if "tts_s" in cpu:
+                out["tts"]["gpu_vs_cpu_reference_speedup"] = cpu["tts_s"] / (setup_warm + solve_wall + recover_wall)
     return out
 
 
-def cpu_baseline(args, cfg, n_f, F, sample_vcycles=3):
-    """Oracle (CPU restatement of the reference, 1 thread) on the same config."""
+def host_info():
+    """Host CPU model and usable core count (the CPU baseline's hardware)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": len(os.sched_getaffinity(0))}
+
+
+def cpu_lib():
+    """(OracleMG constructor kwargs flag, kind): the reference itself where
+    oracle/_ref/libref.so was built, else the restatement."""
     import oracle_lib as O
+    if O.ref_available():
+        return True, "reference"
+    return False, "port"
+
+
+def cpu_problem(cfg, F):
+    import oracle_lib as O
+    return dict(base_n=cfg["base_n"], levels=cfg["levels"], k=cfg["k"], nu=cfg["nu"], beta=cfg["beta"],
+                inv_eps=cfg["inv_eps"], bc=O.BC_NONE, load_kind=O.LOAD_ARRAY, load=F, cycle=O.CYCLE_V,
+                smooth_steps=1)
+
+
+def cpu_baseline(args, cfg, n_f, F, sample_vcycles=3):
+    """The reference (or its restatement), 1 thread, on the same config."""
+    import oracle_lib as O
+    use_ref, kind = cpu_lib()
     t0 = time.perf_counter()
-    B = O.OracleMG(base_n=cfg["base_n"], levels=cfg["levels"], k=cfg["k"], nu=cfg["nu"], beta=cfg["beta"],
-                   inv_eps=cfg["inv_eps"], bc=O.BC_NONE, load_kind=O.LOAD_ARRAY, load=F, cycle=O.CYCLE_V,
-                   smooth_steps=1)
+    B = O.OracleMG(reference=use_ref, **cpu_problem(cfg, F))
     setup = time.perf_counter() - t0
     secs = B.time_apply(sample_vcycles)
-    return {"value": sample_vcycles / secs, "unit": "V-cycles/s", "cores": 1, "kind": "port",
-            "sample": f"{sample_vcycles} V-cycles of {args.config} after a {setup:.1f} s setup (oracle/, 1 thread)",
-            "setup_s": setup}
+    lib = "oracle/_ref/libref.so (unmodified reference headers + Eigen-API shim)" if use_ref else "oracle/ restatement"
+    return {"value": sample_vcycles / secs, "unit": "V-cycles/s", "cores": 1, "kind": kind,
+            "sample": f"{sample_vcycles} V-cycles of {args.config} after a {setup:.1f} s setup ({lib}, 1 thread)",
+            "setup_s": setup, **host_info()}
+
+
+def cpu_tts_child(config, seed):
+    """Reference time-to-solution at `config` (runs in a child pinned to one
+    core): MGPreconditioner construction, uzawa_solve (2 outer PCG solves to
+    1e-8), recover_locals; prints one JSON line."""
+    import ctypes as C
+    import oracle_lib as O
+    cfg = CONFIGS[config]
+    n_f = cfg["base_n"] << (cfg["levels"] - 1)
+    F = O.seeded_load(n_f, seed)
+    use_ref, kind = cpu_lib()
+    kw = cpu_problem(cfg, F)
+    if use_ref:
+        L = O.ref_lib()
+        load = np.ascontiguousarray(kw["load"])
+        p = O.Problem(0, kw["base_n"], kw["levels"], kw["k"], kw["nu"], kw["beta"], 0.0, kw["inv_eps"], kw["bc"],
+                      kw["load_kind"], load.ctypes.data_as(C.POINTER(C.c_double)), 0, kw["cycle"], 0, 1, 1.0 / 3.0,
+                      0, 0)
+        inner = (C.c_int * 8)()
+        secs = np.zeros(3)
+        t0 = time.perf_counter()
+        done = L.orc_tts(C.byref(p), 2, 1e-8, inner, secs.ctypes.data_as(C.POINTER(C.c_double)))
+        wall = time.perf_counter() - t0
+        out = {"kind": kind, "setup_s": float(secs[0]), "uzawa_s": float(secs[1]), "recover_s": float(secs[2]),
+               "tts_s": float(secs.sum()), "wall_s": wall, "inner_iterations": list(inner)[:max(done, 0)]}
+    else:
+        t0 = time.perf_counter()
+        B = O.OracleMG(**kw)
+        t1 = time.perf_counter()
+        u = B.uzawa()
+        t2 = time.perf_counter()
+        B.recover(u["velocity"])
+        t3 = time.perf_counter()
+        out = {"kind": kind, "setup_s": t1 - t0, "uzawa_s": t2 - t1, "recover_s": t3 - t2, "tts_s": t3 - t0,
+               "inner_iterations": u["inner_iterations"]}
+    print(json.dumps(out))
+
+
+def start_cpu_tts(args):
+    """Launches cpu_tts_child pinned to the last usable core (the device run
+    keeps its launching thread elsewhere); returns the Popen or None."""
+    cores = sorted(os.sched_getaffinity(0))
+    if len(cores) < 2:
+        return None
+    cmd = [sys.executable, os.path.abspath(__file__), "--cpu-tts-child", "--config", args.config,
+           "--seed", str(args.seed)]
+    try:
+        return subprocess.Popen(["taskset", "-c", str(cores[-1])] + cmd, stdout=subprocess.PIPE,
+                                stderr=subprocess.DEVNULL, text=True)
+    except OSError:
+        return subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+
+
+def finish_cpu_tts(proc, timeout):
+    if proc is None:
+        return {"unavailable": "fewer than 2 host cores"}
+    try:
+        out, _ = proc.communicate(timeout=timeout)
+        return json.loads(out.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001
+        proc.kill()
+        return {"unavailable": f"reference TTS child did not finish: {type(e).__name__}"}
+
+
+def workload_config(args, cfg, n):
+    """The config dict both arms print (same keys, same values)."""
+    return {"workload": args.config, **cfg, "cycle": "V(1,1)", "smoother": "multiplicative vertex-patch",
+            "n_dofs": int(n)}
 
 
 def run_reference(args):
@@ -337,21 +469,23 @@ def run_reference(args):
     cfg = CONFIGS[args.config]
     n_f = cfg["base_n"] << (cfg["levels"] - 1)
     F = O.seeded_load(n_f, args.seed)
-    B = O.OracleMG(base_n=cfg["base_n"], levels=cfg["levels"], k=cfg["k"], nu=cfg["nu"], beta=cfg["beta"],
-                   inv_eps=cfg["inv_eps"], bc=O.BC_NONE, load_kind=O.LOAD_ARRAY, load=F, cycle=O.CYCLE_V,
-                   smooth_steps=1)
+    use_ref, kind = cpu_lib()
+    B = O.OracleMG(reference=use_ref, **cpu_problem(cfg, F))
     per_step = max(1, args.ref_vcycles_per_step)
     for _ in range(min(args.warmup, 3)):
         B.time_apply(1)
     secs = sum(B.time_apply(per_step) for _ in range(args.steps))
     v = args.steps * per_step / secs
+    what = ("oracle/_ref/libref.so: the reference's unmodified headers (MGPreconditioner::apply) over the "
+            "Eigen-API shim" if use_ref else "oracle/ restatement (reference library not built)")
     return {"impl": "reference", "metric": METRIC if args.config == "config2" else f"hp-MG V-cycles/sec ({args.config})",
             "value": v, "unit": "V-cycles/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (same seeded force as the GPU arm)",
-            "config": {"workload": args.config, **cfg},
-            "cpu_baseline": {"value": v, "unit": "V-cycles/s", "cores": 1, "kind": "port",
-                             "sample": f"{args.steps} x {per_step} V-cycles, oracle/ restatement (reference needs Eigen, absent)"},
+            "config": {**workload_config(args, cfg, B.n), "parallelism": "replicas x1",
+                       "l2": "n/a (CPU, 1 thread)"},
+            "cpu_baseline": {"value": v, "unit": "V-cycles/s", "cores": 1, "kind": kind,
+                             "sample": f"{args.steps} x {per_step} V-cycles, {what}", **host_info()},
             "e2e": {"value": v, "unit": "V-cycles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -367,7 +501,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-vcycles", type=int, default=3)
     ap.add_argument("--ref-vcycles-per-step", type=int, default=1)
+    ap.add_argument("--no-cpu-tts", dest="cpu_tts", action="store_false", default=True)
+    ap.add_argument("--cpu-tts-child", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.cpu_tts_child:
+        cpu_tts_child(args.config, args.seed)
+        return
     args.warmup = max(args.warmup, 3) if args.impl == "hpmg" else args.warmup
     if args.impl == "reference":
         out = run_reference(args)

@@ -78,18 +78,21 @@ typedef struct {
 
 /* AssemblyOptions + inv_eps + MGOptions (assembly.hpp:69-77, multigrid.hpp:24-34). */
 typedef struct {
-  int k;                   /* order 0..3 */
+  int k;                   /* order 0..6 (the reference accepts 0..3, fespace.hpp:115; 4..6 are
+                              this library's extension, parity unpinned) */
   double nu, beta, mass_coef, inv_eps;
   int cycle, smoother, smooth_steps;
   double jacobi_damping;
-  int schedule;            /* multiplicative sweep schedule (symmetric operators):
-                              HPMG_SCHEDULE_WAVES (0, one launch per independent wave) or
-                              HPMG_SCHEDULE_DATAFLOW (1, one launch per sweep ordered by
-                              per-patch completion flags) or HPMG_SCHEDULE_PERSISTENT (2,
-                              one cooperative launch per smoothing phase, grid barrier
-                              per wave); identical results */
+  int sweep_variant;       /* multiplicative sweeps (one launch per independent wave, identical
+                              results to the reference's sequential order):
+                              HPMG_SWEEP_RECORDS (0, default): every level streams patch records,
+                              x_p = S_p (b_p - A_pe x_e) without reading A_pp;
+                              HPMG_SWEEP_DIRECT_NONSYM (1): nonsymmetric (advected) levels use the
+                              direct-gather correction x_p += S_p (b - A x)_p instead, whose error
+                              scales with the residual rather than with x_p (closer iteration counts
+                              in long unrestarted GMRES runs; ~2.3x slower V-cycle at config 5) */
 } hpmg_options;
-enum { HPMG_SCHEDULE_WAVES = 0, HPMG_SCHEDULE_DATAFLOW = 1, HPMG_SCHEDULE_PERSISTENT = 2 };
+enum { HPMG_SWEEP_RECORDS = 0, HPMG_SWEEP_DIRECT_NONSYM = 1 };
 
 /* Problem data: boundary values, load and (Oseen) advection state. */
 typedef struct {
@@ -170,7 +173,7 @@ void hpmg_destroy(hpmg_ctx* ctx);
  * Picard/Newton step, ns.hpp:84): new wind / Newton flag / mass field / load /
  * boundary data and nu, beta, mass_coef, inv_eps; the mesh hierarchy, plans,
  * patch structure, wave schedules and allocations are kept. Order, cycle,
- * smoother, schedule and the symmetric/advected class must not change. */
+ * smoother, sweep variant and the symmetric/advected class must not change. */
 int hpmg_update(hpmg_ctx* ctx, const hpmg_options* opt, const hpmg_problem* prob);
 const char* hpmg_last_error(void);
 void hpmg_set_last_error(const char* msg); /* for drivers layered on this ABI (hpmg_ns_solve) */

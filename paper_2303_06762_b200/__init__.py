@@ -32,15 +32,16 @@ class _Mesh(C.Structure):
                 ("tag_overrides", C.POINTER(C.c_int)), ("levels", C.c_int)]
 
 
-# multiplicative sweep schedules (identical results): one launch per wave, or
-# one dataflow launch per sweep ordered by per-patch completion flags
-SCHEDULES = {"waves": 0, "dataflow": 1, "persistent": 2}
+# multiplicative sweep variants (hpmg_options.sweep_variant): patch records on
+# every level (default), or the direct-gather correction form on advected
+# (nonsymmetric) levels
+SWEEP_VARIANTS = {"records": 0, "direct_nonsym": 1}
 
 
 class _Options(C.Structure):
     _fields_ = [("k", C.c_int), ("nu", C.c_double), ("beta", C.c_double), ("mass_coef", C.c_double),
                 ("inv_eps", C.c_double), ("cycle", C.c_int), ("smoother", C.c_int), ("smooth_steps", C.c_int),
-                ("jacobi_damping", C.c_double), ("schedule", C.c_int)]
+                ("jacobi_damping", C.c_double), ("sweep_variant", C.c_int)]
 
 
 class _Problem(C.Structure):
@@ -291,17 +292,17 @@ class MGPreconditioner:
     def __init__(self, *, mesh="unit_square", base_n=2, levels=2, k=0, nu=1.0, beta=0.0, mass_coef=0.0,
                  inv_eps=1e6, cycle=CYCLE_W, smoother=SMOOTH_MULTIPLICATIVE, smooth_steps=1,
                  jacobi_damping=1.0 / 3.0, bc=None, load=None, load_per_element=None, structured_load=None,
-                 wind=None, newton=False, mass_field=None, schedule="waves"):
+                 wind=None, newton=False, mass_field=None, sweep="records"):
         L = lib()
         md = _Mesh()
         rc = (L.hpmg_unit_square_mesh if mesh == "unit_square" else L.hpmg_step_mesh)(base_n, levels, C.byref(md))
         if rc:
             raise HpmgError(L.hpmg_last_error().decode())
-        if schedule not in SCHEDULES:
-            raise ValueError(f"schedule must be one of {sorted(SCHEDULES)}")
+        if sweep not in SWEEP_VARIANTS:
+            raise ValueError(f"sweep must be one of {sorted(SWEEP_VARIANTS)}")
         self._optargs = dict(k=k, nu=nu, beta=beta, mass_coef=mass_coef, inv_eps=inv_eps, cycle=cycle,
                              smoother=smoother, smooth_steps=smooth_steps, jacobi_damping=jacobi_damping,
-                             schedule=SCHEDULES[schedule])
+                             sweep_variant=SWEEP_VARIANTS[sweep])
         opt = _Options(**self._optargs)
         self._bc, self._bc_user, self._bc_keep = _field_user(bc)
         self._load, self._load_user, self._load_keep = _field_user(load)
@@ -632,7 +633,7 @@ class NSSolution:
 
 def navier_stokes_solve(*, mesh="unit_square", base_n=2, levels=2, k=0, nu=1.0, inv_eps=1e6, bc=None, load=None,
                         load_per_element=None, structured_load=None, cycle=CYCLE_W, smoother=SMOOTH_MULTIPLICATIVE,
-                        smooth_steps=1, jacobi_damping=1.0 / 3.0, schedule="waves", picard_tol=1e-4,
+                        smooth_steps=1, jacobi_damping=1.0 / 3.0, sweep="records", picard_tol=1e-4,
                         newton_rel_tol=1e-8, newton_abs_tol=1e-10, max_picard=60, max_newton=25,
                         pseudo_time_inv=0.0, outer_iterations=2, krylov: KrylovOptions | None = None):
     """Stationary Navier-Stokes driver (reference ns.hpp:69-149): Stokes guess,
@@ -643,7 +644,7 @@ def navier_stokes_solve(*, mesh="unit_square", base_n=2, levels=2, k=0, nu=1.0, 
     rc = (L.hpmg_unit_square_mesh if mesh == "unit_square" else L.hpmg_step_mesh)(base_n, levels, C.byref(md))
     if rc:
         raise HpmgError(L.hpmg_last_error().decode())
-    opt = _Options(k, nu, 0.0, 0.0, inv_eps, cycle, smoother, smooth_steps, jacobi_damping, SCHEDULES[schedule])
+    opt = _Options(k, nu, 0.0, 0.0, inv_eps, cycle, smoother, smooth_steps, jacobi_damping, SWEEP_VARIANTS[sweep])
     bcf, bcu, bck = _field_user(bc)
     ldf, ldu, ldk = _field_user(load)
     keep = [bcf, ldf, bck, ldk]

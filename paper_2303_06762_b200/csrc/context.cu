@@ -95,9 +95,6 @@ struct Level {
   dev::PatchRecords rec;
   dev::PatchRecords srec;  // full-inverse records of the one-CTA path
   dev::PatchRecords rect;  // A^T / S_p^T records of the transposed sweep (advected operators)
-  unsigned* flow_flags = nullptr;  // [npatch] completion epochs of the dataflow sweep
-  unsigned* flow_ctl = nullptr;    // [2] epoch base, arrival counter
-  unsigned* coop_ctl = nullptr;    // [2] grid-barrier state of the persistent sweep
   bool small = false;      // whole pre/post phase in one CTA (small_levels.cu)
   int2* d_passes = nullptr;
   int npass = 0;
@@ -422,8 +419,9 @@ void build_patch_inverses(hpmg_ctx& C, Level& V) {
   dev::patch_inverse(V.A, V.P, V.max_nf, C.s);
   // fixed-stride patch records for the TMA sweep (sweep_rec.cu); nonsymmetric
   // operators: full inverses, plus A^T / S_p^T records for the transposed sweep
-  // (HPMG_NONSYM_RECORDS=0: the direct-gather sweeps of kernels.cu instead)
-  static const bool nonsym_records = !std::getenv("HPMG_NONSYM_RECORDS") || std::atoi(std::getenv("HPMG_NONSYM_RECORDS"));
+  // (hpmg_options.sweep_variant = HPMG_SWEEP_DIRECT_NONSYM: the direct-gather
+  // correction sweeps of kernels.cu instead)
+  const bool nonsym_records = C.opt.sweep_variant != HPMG_SWEEP_DIRECT_NONSYM;
   bool use_records = V.P.packed || nonsym_records;
   if (use_records && !V.P.packed && !V.rec.rec) {
     // nonsymmetric records hold full inverses twice (S_p and S_p^T sets, ~5x the
@@ -457,9 +455,6 @@ void build_patch_inverses(hpmg_ctx& C, Level& V) {
       if (V.small) dev::build_records(V.A, V.P, V.srec, C.s);
       return;
     }
-    V.P.max_dep = V.plan.max_dep;
-    V.P.ndep = dupload(V.plan.patch_ndep, C.s);
-    V.P.dep = dupload(V.plan.patch_dep, C.s);
     V.rec = dev::record_layout(V.bs, V.max_nf, !V.P.packed);
     V.rec.rec = dalloc<double>(size_t(V.P.n) * V.rec.stride);
     if (C.advected) {
@@ -469,12 +464,6 @@ void build_patch_inverses(hpmg_ctx& C, Level& V) {
     }
     V.rec.n = V.P.n;
     if (const char* d = std::getenv("HPMG_DBG")) V.rec.dbg = std::atoi(d);
-    V.flow_flags = dalloc<unsigned>(V.P.n);
-    V.flow_ctl = dalloc<unsigned>(2);
-    V.coop_ctl = dalloc<unsigned>(2);
-    CK(cudaMemsetAsync(V.coop_ctl, 0, 2 * sizeof(unsigned), C.s));
-    CK(cudaMemsetAsync(V.flow_flags, 0, sizeof(unsigned) * V.P.n, C.s));
-    CK(cudaMemsetAsync(V.flow_ctl, 0, sizeof(unsigned) * 2, C.s));
     dev::build_records(V.A, V.P, V.rec, C.s);
     std::vector<int2> passes;
     const int pp = dev::small_pass_patches();
@@ -555,18 +544,6 @@ void smooth(hpmg_ctx& C, Level& V, double* x, const double* b, bool post) {
   };
   const void* pf;
   size_t pl;
-  if (V.P.packed && C.opt.schedule == HPMG_SCHEDULE_PERSISTENT && nw <= dev::kMaxSweepWaves) {
-    // all waves of all steps in one cooperative launch, grid barrier per wave
-    dev::sweep_persistent(V.rec, V.wave_ptr.data(), nw, V.steps, post, b, x, V.coop_ctl, C.s);
-    count(C);
-    return;
-  }
-  if (V.P.packed && C.opt.schedule == HPMG_SCHEDULE_DATAFLOW && nw <= dev::kMaxSweepWaves) {
-    // all waves of all steps in one dataflow launch (sweep_rec.cu)
-    dev::sweep_dag(V.rec, V.wave_ptr.data(), nw, V.P, V.steps, post, b, x, V.flow_flags, V.flow_ctl, C.s);
-    count(C, 2);
-    return;
-  }
   if (!post) {
     for (int s = 0; s < V.steps; ++s)
       for (int w = 0; w < nw; ++w) {
@@ -864,6 +841,8 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     throw std::runtime_error("no CUDA device: hpmg has no CPU fallback");
   if (opt->k < 0 || opt->k > 6) throw std::invalid_argument("order k must be in 0..6");
+  if (opt->sweep_variant != HPMG_SWEEP_RECORDS && opt->sweep_variant != HPMG_SWEEP_DIRECT_NONSYM)
+    throw std::invalid_argument("unknown sweep variant");
   if (md->levels < 1) throw std::invalid_argument("levels must be >= 1");
   C.opt = *opt;
   C.advected = prob && (prob->wind_compound || prob->wind);
@@ -1182,7 +1161,7 @@ int hpmg_update(hpmg_ctx* ctx, const hpmg_options* opt, const hpmg_problem* prob
     hpmg_ctx& C = *ctx;
     const bool advected = prob && (prob->wind_compound || prob->wind);
     if (opt->k != C.opt.k || opt->cycle != C.opt.cycle || opt->smoother != C.opt.smoother ||
-        opt->smooth_steps != C.opt.smooth_steps || opt->schedule != C.opt.schedule || advected != C.advected)
+        opt->smooth_steps != C.opt.smooth_steps || opt->sweep_variant != C.opt.sweep_variant || advected != C.advected)
       throw std::invalid_argument("hpmg_update changes only the linearisation state (wind, Newton, mass terms, nu, "
                                   "beta, inv_eps); order, cycle, smoother and symmetry need a new context");
     if (prob && prob->newton && !advected)
@@ -1235,8 +1214,8 @@ void hpmg_destroy(hpmg_ctx* ctx) {
                     (void*)V->Pm.ptr, (void*)V->Pm.col, (void*)V->Pm.val, (void*)V->PT.ptr, (void*)V->PT.col,
                     (void*)V->PT.val, (void*)V->x, (void*)V->b, (void*)V->r, (void*)V->y, (void*)V->bw, (void*)V->xw,
                     (void*)V->dbuf, (void*)V->geo, (void*)V->row_elems, (void*)V->elem_facets, (void*)V->facet_block,
-                    (void*)V->d_wave_ptr, (void*)V->rec.rec, (void*)V->srec.rec, (void*)V->rect.rec, (void*)V->flow_flags,
-                    (void*)V->flow_ctl, (void*)V->coop_ctl, (void*)V->P.ndep, (void*)V->P.dep, (void*)V->d_passes, (void*)V->gath,
+                    (void*)V->d_wave_ptr, (void*)V->rec.rec, (void*)V->srec.rec, (void*)V->rect.rec,
+                    (void*)V->d_passes, (void*)V->gath,
                     (void*)V->block_facet, (void*)V->tdev.nmed, (void*)V->tdev.med, (void*)V->tdev.ncol,
                     (void*)V->tdev.col, (void*)V->tdev.pos, (void*)V->tdev.avg_ptr, (void*)V->tdev.avg_col,
                     (void*)V->tdev.avg_val, (void*)V->tdev.base, (void*)V->tdev.tperm})

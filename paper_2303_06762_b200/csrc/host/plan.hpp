@@ -119,9 +119,6 @@ struct LevelPlan {
   std::vector<int> facet_patches;     // [nb][2] the two patches holding a block, ascending
   // dataflow sweep: patches of the mesh neighbours of each patch's vertex
   // (renumbered ids; the forward sweep waits on the smaller, the reverse on the larger)
-  int max_dep = 0;
-  std::vector<int> patch_ndep;        // [npatch]
-  std::vector<int> patch_dep;         // [npatch][max_dep], -1 padded
   int nwaves() const { return int(wave_ptr.size()) - 1; }
   int64_t n() const { return int64_t(nb) * bs; }
 };
@@ -276,30 +273,6 @@ inline LevelPlan make_level(const TriMesh& m, int k) {
   L.patch_fac.swap(fac2);
   for (auto& fp : L.facet_patches)
     if (fp >= 0) fp = newid[fp];
-  {
-    // neighbour patches of every patch, sorted unique (<= 16: vertex degree)
-    constexpr int kDepCap = 16;
-    std::vector<int> tmp(size_t(L.npatch) * kDepCap, -1);
-    L.patch_ndep.assign(L.npatch, 0);
-    parallel_for(m.nv(), [&](int v) {
-      if (vertex_patch[v] < 0) return;
-      const int p = newid[vertex_patch[v]];
-      int* d = &tmp[size_t(p) * kDepCap];
-      int nd = 0;
-      for (const int* up = nbr.begin(v); up != nbr.end(v); ++up)
-        if (vertex_patch[*up] >= 0) {
-          if (nd == kDepCap) throw std::runtime_error("vertex degree too large for the dependency lists");
-          d[nd++] = newid[vertex_patch[*up]];
-        }
-      std::sort(d, d + nd);
-      L.patch_ndep[p] = int(std::unique(d, d + nd) - d);
-    });
-    for (int p = 0; p < L.npatch; ++p) L.max_dep = std::max(L.max_dep, L.patch_ndep[p]);
-    L.patch_dep.assign(size_t(L.npatch) * std::max(L.max_dep, 1), -1);
-    parallel_for(L.npatch, [&](int p) {
-      for (int i = 0; i < L.patch_ndep[p]; ++i) L.patch_dep[size_t(p) * L.max_dep + i] = tmp[size_t(p) * kDepCap + i];
-    });
-  }
   for (int q = 0; q < L.npatch; ++q) L.wave_patch[q] = q;
   set_inverse_layout(L, true);
   return L;

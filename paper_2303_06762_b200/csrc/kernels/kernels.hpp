@@ -33,9 +33,6 @@ struct Patches {
   int* wave = nullptr;      // patch ids grouped by wave
   int* fpatch = nullptr;    // [nb][2] patches holding block f (ascending)
   int packed = 1;           // 1: symmetric, lower triangle packed by columns
-  int* ndep = nullptr;      // [n] dataflow dependencies (mesh-neighbour patches)
-  int* dep = nullptr;       // [n][max_dep]
-  int max_dep = 0;
 };
 
 /// 2x2-block CSR (prolongation P: fine rows; PT: coarse rows).
@@ -103,20 +100,6 @@ void build_records(const Bsr& A, const Patches& P, PatchRecords& R, cudaStream_t
 /// One symmetric wave over the patch records [w0, w1) (one TMA per CTA).
 void gs_wave_rec(const PatchRecords& R, int w0, int w1, const double* b, double* x, cudaStream_t s);
 void sweep_trace(long long* out);  // development timeline, 5 x 32768 stamps
-/// `nsweeps` whole sweeps (forward, or reverse wave order) in ONE dataflow
-/// launch: each patch waits for the completion flags of its preceding mesh
-/// neighbours instead of a wave boundary (sweep_rec.cu). `flags` [n] and
-/// `ctl` [2] start zeroed and only ever advance (sweep epochs).
-constexpr int kMaxSweepWaves = 64;
-void sweep_dag(const PatchRecords& R, const int* wave_ptr_host, int nwaves, const Patches& P, int nsweeps,
-               bool reverse, const double* b, double* x, unsigned* flags, unsigned* ctl, cudaStream_t s);
-
-/// `nsweeps` whole sweeps in ONE cooperative launch with a grid barrier per
-/// wave boundary and double-buffered record copies (sweep_rec.cu); ctl [2]
-/// zero-initialised barrier state, self-resetting.
-void sweep_persistent(const PatchRecords& R, const int* wave_ptr_host, int nwaves, int nsweeps, bool reverse,
-                      const double* b, double* x, unsigned* ctl, cudaStream_t s);
-
 /// Additive sweep pieces: d_p = Inv_p r_p for all patches; x += damping * sum_p d_p.
 void jacobi_patch(const Bsr& A, const Patches& P, const double* r, double* d, int max_nf, cudaStream_t s);
 void jacobi_combine(int nb, int bs, const Patches& P, const double* d, int max_nf, double damping, double* x,

@@ -20,17 +20,10 @@
 //
 // Ordering. The reference sweep is sequential in ascending vertex order; two
 // patches conflict iff their vertices are mesh neighbours.
-// Two schedules reproduce it exactly:
-//  - waves (gs_wave_rec): one launch per wave of mutually independent patches,
-//    chained by programmatic dependent launch;
-//  - dataflow (sweep_dag): ONE launch per sweep over all patches in sweep
-//    order (CTA index = position). A CTA waits only for the completion flags
-//    of its neighbours that precede it, so there is no wave boundary: the
-//    drain/fill of every wave disappears. Flags hold sweep epochs
-//    (ctl[0] + sweep + 1); a one-thread kernel advances ctl[0] after the
-//    launch, so the flags never need resetting. Like CUB's decoupled
-//    look-back, this relies on CTAs being dispatched in index order: every
-//    CTA waits only on lower indices, which are therefore resident or done.
+// One launch per wave of mutually independent patches (gs_wave_rec),
+// chained by programmatic dependent launch, reproduces it exactly. (Round 1
+// also kept a one-launch-per-sweep dataflow schedule and a cooperative
+// persistent one; both were slower on B200 and were removed.)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -74,11 +67,6 @@ __device__ __forceinline__ void tma_part(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(su32(bar)), "l"(pol)
       : "memory");
 }
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 
 // development timeline (R.dbg & 4): per CTA of the last launches, globaltimer
 // at start / A-part landed / gather done / S landed / end
@@ -91,50 +79,19 @@ __device__ __forceinline__ void sweep_stamp(const PatchRecords& R, int k) {
   }
 }
 
-/// Wave table of one sweep direction, passed by value (kernel parameter
-/// space): waves in processing order, their patch ranges and the prefix of
-/// their G-patch items.
-struct SweepOrder {
-  int nw = 0, nitems = 0, reverse = 0;
-  int wbeg[kMaxSweepWaves], wend[kMaxSweepWaves];
-  int item0[kMaxSweepWaves + 1];
-};
-
-struct DagState {
-  unsigned* flags = nullptr;  // [n] completion epochs
-  unsigned* ctl = nullptr;    // [2] epoch base, arrivals
-  const int* ndep = nullptr;  // [n]
-  const int* dep = nullptr;   // [n][max_dep] mesh-neighbour patches
-  int max_dep = 0;
-  int nsweeps = 1;
-};
-
-/// Records of G consecutive patches per CTA, TP threads per patch.
-/// DAG = false: one wave [p0, p1); DAG = true: item blockIdx.x of O (x nsweeps).
-template <int BS, int TP, int G, bool DAG>
-__global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1, SweepOrder O, DagState D,
-                                                 const double* __restrict__ b, double* __restrict__ x) {
+/// Records of G consecutive patches per CTA, TP threads per patch: one wave [p0, p1).
+template <int BS, int TP, int G>
+__global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1, const double* __restrict__ b,
+                                                 double* __restrict__ x) {
   constexpr int kRow = kExt * BS * BS;
-  constexpr bool kOneCopy = G > 1 && !DAG;  // grouped small records: one copy per CTA
+  constexpr bool kOneCopy = G > 1;  // grouped small records: one copy per CTA
   extern __shared__ __align__(128) unsigned char smraw[];
   double* srec = reinterpret_cast<double*>(smraw);  // G * stride
   double* sx = srec + size_t(G) * R.stride;          // G * max_nf * kExt * BS
   double* r = sx + G * R.max_nf * kExt * BS;         // G * TP
   __shared__ unsigned long long bar, bar_s, bar_m;
-  __shared__ unsigned s_base;
   const int lp = threadIdx.x / TP, t = threadIdx.x % TP;
-  int q0, ng, sweep = 0;
-  if (DAG) {
-    const int it = blockIdx.x % O.nitems;
-    sweep = blockIdx.x / O.nitems;
-    int w = 0;
-    while (it >= O.item0[w + 1]) ++w;  // uniform scan over <= 64 parameter words
-    q0 = O.wbeg[w] + (it - O.item0[w]) * G;
-    ng = min(G, O.wend[w] - q0);
-  } else {
-    q0 = p0 + blockIdx.x * G;
-    ng = min(G, p1 - q0);
-  }
+  const int q0 = p0 + blockIdx.x * G, ng = min(G, p1 - q0);
   sweep_stamp(R, 0);
   if (threadIdx.x == 0) {
     // three copies per patch: the meta words first (the x_e gather needs only
@@ -166,32 +123,11 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
         tma_part(srec + size_t(q) * R.stride, R.rec + size_t(q0 + q) * R.stride, head, &bar_s, pol);
     }
   }
-  // dependency lists do not depend on the previous kernel: load them now
-  int dq = -1;
-  if (DAG && int(threadIdx.x) < ng * D.max_dep) {
-    const int dp = threadIdx.x / D.max_dep, di = threadIdx.x % D.max_dep;
-    dq = __ldg(D.dep + size_t(q0 + dp) * D.max_dep + di);  // -1 padded
-  }
   // Programmatic dependent launch: the records do not depend on the previous
-  // kernel, so the copies above may overlap its tail; x, b and the flags may
-  // not be touched before it has completed.
+  // kernel, so the copies above may overlap its tail; x and b may not be
+  // touched before it has completed.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  unsigned mine = 0;
-  if (DAG) {
-    if (threadIdx.x == 0) s_base = *reinterpret_cast<volatile unsigned*>(D.ctl);
-    __syncthreads();
-    mine = s_base + unsigned(sweep) + 1u;
-    if (dq >= 0) {
-      // neighbours before this patch in the sweep: done in this sweep;
-      // after it: done in the previous sweep of this launch (if any)
-      const int me = q0 + int(threadIdx.x) / D.max_dep;
-      const bool before = O.reverse ? dq > me : dq < me;
-      const unsigned need = before ? mine : mine - 1u;
-      if (need != s_base)
-        while (int(ld_acquire(D.flags + dq) - need) < 0) __nanosleep(20);
-    }
-  }
   __syncthreads();
   bar_wait(&bar_m);
   sweep_stamp(R, 1);
@@ -209,8 +145,7 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
   double bv = 0.0;
   if (row < np && part == 0) bv = __ldg(b + size_t(fac[row / BS]) * BS + row % BS);
   {
-    // all loads of this thread in flight at once, then the shared stores;
-    // L2 (.cg) loads in the dataflow kernel: x changes under a running grid
+    // all loads of this thread in flight at once, then the shared stores
     constexpr int kPer = (kMaxPatchF * kExt * BS + TP - 1) / TP;
     const int ne = nf * kExt * BS;
     double v[kPer];
@@ -218,7 +153,7 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
     for (int u = 0; u < kPer; ++u) {
       const int e = t + u * TP;
       const int c = e < ne ? ecol[e / BS] : -1;
-      v[u] = c < 0 ? 0.0 : (DAG ? __ldcg(x + size_t(c) * BS + e % BS) : x[size_t(c) * BS + e % BS]);
+      v[u] = c < 0 ? 0.0 : x[size_t(c) * BS + e % BS];
     }
 #pragma unroll
     for (int u = 0; u < kPer; ++u)
@@ -307,219 +242,10 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
   }
   if (TR == 2) dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);
   if (row < np && part == 0) x[size_t(fac[row / BS]) * BS + row % BS] = dsum;
-  if (DAG) {
-    __syncthreads();  // x_p written by every thread of the CTA
-    if (threadIdx.x == 0) {
-      __threadfence();
-      for (int q = 0; q < ng; ++q)
-        asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(D.flags + q0 + q), "r"(mine) : "memory");
-    }
-  }
   if (R.dbg & 4) {
     __syncthreads();
     sweep_stamp(R, 4);
   }
-}
-
-/// Grid barrier number `i` (0-based) of a cooperative (co-resident) launch:
-/// ctl[0] counts arrivals monotonically within the launch (one release
-/// atomic per CTA, then acquire polls until (i + 1) * grid have arrived);
-/// ctl[1] counts exiting CTAs and the last one resets both, so every launch
-/// (stream-ordered) starts from zero. The x rows written before the barrier
-/// are visible at L2 after it.
-__device__ __forceinline__ void grid_sync(unsigned* ctl, unsigned i) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned old;
-    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctl) : "memory");
-    const unsigned target = (i + 1u) * gridDim.x;
-    if (old + 1u != target)
-      while (ld_acquire(ctl) < target) {
-      }
-  }
-  __syncthreads();
-}
-__device__ __forceinline__ void grid_exit(unsigned* ctl) {
-  if (threadIdx.x == 0) {
-    unsigned old;
-    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctl + 1) : "memory");
-    if (old + 1u == gridDim.x) {
-      ctl[0] = 0u;
-      ctl[1] = 0u;
-    }
-  }
-}
-
-__device__ __forceinline__ void bar_wait_parity(unsigned long long* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE_%=;\n"
-      "bra WAIT_%=;\n"
-      "DONE_%=:\n"
-      "}\n" ::"r"(su32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-/// Persistent sweep (HPMG_SCHEDULE_PERSISTENT): one cooperative launch runs
-/// all waves of `nsweeps` sweeps; a grid barrier replaces each wave boundary
-/// (kernel drain + launch) and the records of a CTA's next item are copied
-/// (double buffer) while it works on the current one, so after a barrier only
-/// the x_e gather and the arithmetic remain on the critical path. Per item the
-/// arithmetic is k_sweep's.
-template <int BS, int TP, int G>
-__global__ void __launch_bounds__(G* TP) k_sweep_coop(PatchRecords R, SweepOrder O, int nsweeps,
-                                                      const double* __restrict__ b, double* __restrict__ x,
-                                                      unsigned* ctl) {
-  constexpr int kRow = kExt * BS * BS;
-  extern __shared__ __align__(128) unsigned char smraw[];
-  double* srec = reinterpret_cast<double*>(smraw);    // 2 slots x G * stride
-  double* sx = srec + size_t(2) * G * R.stride;          // G * max_nf * kExt * BS
-  double* r = sx + G * R.max_nf * kExt * BS;           // G * TP
-  __shared__ unsigned long long bars[2][3];            // per slot: meta, A_pe, S_p
-  const int lp = threadIdx.x / TP, t = threadIdx.x % TP;
-  if (threadIdx.x == 0) {
-    for (int sl = 0; sl < 2; ++sl)
-      for (int i = 0; i < 3; ++i) bar_init(&bars[sl][i]);
-  }
-  __syncthreads();
-  // this CTA's items in processing order: (sweep, wave, item), item strided by the grid
-  struct Cur {
-    int sw, w, it;
-  };
-  auto norm = [&](Cur c) {
-    while (c.sw < nsweeps && c.it >= O.item0[c.w + 1]) {
-      if (++c.w == O.nw) {
-        c.w = 0;
-        ++c.sw;
-      }
-      c.it = O.item0[c.w] + int(blockIdx.x);
-    }
-    return c;
-  };
-  auto issue = [&](const Cur& c, int sl) {
-    const int q0 = O.wbeg[c.w] + (c.it - O.item0[c.w]) * G, ng = min(G, O.wend[c.w] - q0);
-    unsigned long long pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    const unsigned mbytes = unsigned(R.stride - R.meta_off) * 8u, abytes = unsigned(R.meta_off - R.a_off) * 8u,
-                   head = unsigned(R.a_off) * 8u;
-    double* dst = srec + size_t(sl) * G * R.stride;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    bar_expect(&bars[sl][0], unsigned(ng) * mbytes);
-    bar_expect(&bars[sl][1], unsigned(ng) * abytes);
-    bar_expect(&bars[sl][2], unsigned(ng) * head);
-    for (int q = 0; q < ng; ++q)
-      tma_part(dst + size_t(q) * R.stride + R.meta_off, R.rec + size_t(q0 + q) * R.stride + R.meta_off, mbytes,
-               &bars[sl][0], pol);
-    for (int q = 0; q < ng; ++q)
-      tma_part(dst + size_t(q) * R.stride + R.a_off, R.rec + size_t(q0 + q) * R.stride + R.a_off, abytes,
-               &bars[sl][1], pol);
-    for (int q = 0; q < ng; ++q)
-      tma_part(dst + size_t(q) * R.stride, R.rec + size_t(q0 + q) * R.stride, head, &bars[sl][2], pol);
-  };
-  Cur cur = norm(Cur{0, 0, O.item0[0] + int(blockIdx.x)});
-  if (threadIdx.x == 0 && cur.sw < nsweeps) issue(cur, 0);
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  int k = 0;
-  for (int sw = 0; sw < nsweeps; ++sw)
-    for (int w = 0; w < O.nw; ++w) {
-      while (cur.sw == sw && cur.w == w) {
-        const int sl = k & 1;
-        const unsigned par = unsigned(k >> 1) & 1u;
-        const Cur nxt = norm(Cur{cur.sw, cur.w, cur.it + int(gridDim.x)});
-        if (threadIdx.x == 0 && nxt.sw < nsweeps) issue(nxt, sl ^ 1);  // slot sl^1 was released by item k-1
-        const int q0 = O.wbeg[cur.w] + (cur.it - O.item0[cur.w]) * G, ng = min(G, O.wend[cur.w] - q0);
-        bar_wait_parity(&bars[sl][0], par);
-        const double* rec = srec + (size_t(sl) * G + lp) * R.stride;
-        const int* meta = reinterpret_cast<const int*>(rec + R.meta_off);
-        const int nf = lp < ng ? meta[0] : 0, np = nf * BS;
-        const int* fac = meta + 1;
-        const int* ecol = meta + 1 + R.max_nf;
-        double* xs = sx + lp * R.max_nf * kExt * BS;
-        constexpr int TR = TP >= 2 * kMaxPatchF * BS ? 2 : 1;
-        const int row = t / TR, part = t % TR;
-        double bv = 0.0;
-        if (row < np && part == 0) bv = __ldg(b + size_t(fac[row / BS]) * BS + row % BS);
-        {
-          constexpr int kPer = (kMaxPatchF * kExt * BS + TP - 1) / TP;
-          const int ne = nf * kExt * BS;
-          double v[kPer];
-#pragma unroll
-          for (int u = 0; u < kPer; ++u) {
-            const int e = t + u * TP;
-            const int c = e < ne ? ecol[e / BS] : -1;
-            v[u] = c < 0 ? 0.0 : __ldcg(x + size_t(c) * BS + e % BS);  // L2: written by other CTAs
-          }
-#pragma unroll
-          for (int u = 0; u < kPer; ++u)
-            if (t + u * TP < ne) xs[t + u * TP] = v[u];
-        }
-        bar_wait_parity(&bars[sl][1], par);
-        __syncthreads();
-        double rsum = 0.0;
-        if (row < np) {
-          const int lf = row / BS, i = row % BS;
-          const double* acol = rec + R.a_off + lf * kRow + i;
-          const double* xr = xs + lf * kExt * BS;
-          double a0 = bv, a1 = 0.0;
-#pragma unroll
-          for (int sq = 0; sq < kExt / TR; ++sq) {
-            const int sli = sq * TR + part;
-#pragma unroll
-            for (int jj = 0; jj < BS; jj += 2) {
-              const int j0 = (jj + lf) % BS, j1 = (jj + 1 + lf) % BS;
-              a0 = fma(-acol[sli * BS * BS + j0 * BS], xr[sli * BS + j0], a0);
-              a1 = fma(-acol[sli * BS * BS + j1 * BS], xr[sli * BS + j1], a1);
-            }
-          }
-          rsum = a0 + a1;
-        }
-        if (TR == 2) rsum += __shfl_xor_sync(0xffffffffu, rsum, 1);
-        if (row < np && part == 0) r[lp * TP + row] = rsum;
-        __syncthreads();
-        bar_wait_parity(&bars[sl][2], par);
-        double dsum = 0.0;
-        if (row < np) {
-          const int tt = row;
-          const double* S = rec;
-          const double* rr = r + lp * TP;
-          const int ct = tt * np - tt * (tt - 1) / 2 - tt;
-          const int jb = TR == 2 ? part * (np / 2) : 0, je = TR == 2 ? (part + 1) * (np / 2) : np;
-          double d0 = 0.0, d1 = 0.0;
-          int cs = jb * np - jb * (jb - 1) / 2, j = jb;
-          for (; j + 1 < je; j += 2) {
-            const int o0 = j < tt ? cs + tt - j : ct + j;
-            cs += np - j;
-            const int o1 = j + 1 < tt ? cs + tt - j - 1 : ct + j + 1;
-            cs += np - j - 1;
-            d0 = fma(S[o0], rr[j], d0);
-            d1 = fma(S[o1], rr[j + 1], d1);
-          }
-          for (; j < je; ++j) {
-            d0 = fma(S[j < tt ? cs + tt - j : ct + j], rr[j], d0);
-            cs += np - j;
-          }
-          dsum = d0 + d1;
-        }
-        if (TR == 2) dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);
-        if (row < np && part == 0) __stcg(x + size_t(fac[row / BS]) * BS + row % BS, dsum);
-        __syncthreads();  // slot sl and xs/r free for item k+1
-        cur = nxt;
-        ++k;
-      }
-      if (sw + 1 < nsweeps || w + 1 < O.nw) grid_sync(ctl, unsigned(sw * O.nw + w));
-    }
-  grid_exit(ctl);
-}
-
-/// Advances the sweep epoch after a dataflow launch (stream-ordered after it,
-/// so every CTA of that launch has read the old base).
-__global__ void k_epoch(unsigned* ctl, int nsweeps) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  ctl[0] += unsigned(nsweeps);
 }
 
 /// Builds the records from the packed inverses and the ELL operator.
@@ -609,22 +335,20 @@ struct RecCfg<14> {
 
 /// dataflow launches carry a fixed per-CTA cost (dependency polls, release
 /// fence), so they group more patches per CTA
-template <int BS, bool DAG>
+template <int BS>
 struct Grp {
-  static constexpr int G = DAG && BS == 8 ? 2 : RecCfg<BS>::G;
+  static constexpr int G = RecCfg<BS>::G;
 };
 
-template <int BS, bool DAG>
-void launch(const PatchRecords& R, int p0, int p1, int nblocks, const SweepOrder& O, const DagState& D, const double* b,
-            double* x, cudaStream_t s) {
-  constexpr int TP = RecCfg<BS>::TP, G = Grp<BS, DAG>::G;
+template <int BS>
+void launch(const PatchRecords& R, int p0, int p1, int nblocks, const double* b, double* x, cudaStream_t s) {
+  constexpr int TP = RecCfg<BS>::TP, G = Grp<BS>::G;
   if (R.max_nf * BS * (TP >= 2 * kMaxPatchF * BS ? 2 : 1) > TP)
     throw std::runtime_error("vertex patch too large for the record sweep");
-  if (DAG && D.max_dep > TP) throw std::runtime_error("too many patch dependencies for the dataflow sweep");
   const size_t smem = sizeof(double) * (size_t(G) * R.stride + size_t(G) * R.max_nf * kExt * BS + G * TP);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_sweep<BS, TP, G, DAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_sweep<BS, TP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -637,35 +361,33 @@ void launch(const PatchRecords& R, int p0, int p1, int nblocks, const SweepOrder
   attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr_pdl;
   cfg.numAttrs = 1;
-  cudaError_t err = cudaLaunchKernelEx(&cfg, k_sweep<BS, TP, G, DAG>, R, p0, p1, O, D, b, x);
+  cudaError_t err = cudaLaunchKernelEx(&cfg, k_sweep<BS, TP, G>, R, p0, p1, b, x);
   if (err == cudaSuccess) err = cudaGetLastError();
   if (err != cudaSuccess) throw std::runtime_error(std::string("CUDA launch (sweep): ") + cudaGetErrorString(err));
 }
 
-template <bool DAG>
-void launch_bs(const PatchRecords& R, int p0, int p1, int nblocks, const SweepOrder& O, const DagState& D,
-               const double* b, double* x, cudaStream_t s) {
+void launch_bs(const PatchRecords& R, int p0, int p1, int nblocks, const double* b, double* x, cudaStream_t s) {
   switch (R.bs) {
-    case 2: launch<2, DAG>(R, p0, p1, nblocks, O, D, b, x, s); break;
-    case 4: launch<4, DAG>(R, p0, p1, nblocks, O, D, b, x, s); break;
-    case 6: launch<6, DAG>(R, p0, p1, nblocks, O, D, b, x, s); break;
-    case 8: launch<8, DAG>(R, p0, p1, nblocks, O, D, b, x, s); break;
-    case 10: launch<10, DAG>(R, p0, p1, nblocks, O, D, b, x, s); break;
-    case 12: launch<12, DAG>(R, p0, p1, nblocks, O, D, b, x, s); break;
-    case 14: launch<14, DAG>(R, p0, p1, nblocks, O, D, b, x, s); break;
+    case 2: launch<2>(R, p0, p1, nblocks, b, x, s); break;
+    case 4: launch<4>(R, p0, p1, nblocks, b, x, s); break;
+    case 6: launch<6>(R, p0, p1, nblocks, b, x, s); break;
+    case 8: launch<8>(R, p0, p1, nblocks, b, x, s); break;
+    case 10: launch<10>(R, p0, p1, nblocks, b, x, s); break;
+    case 12: launch<12>(R, p0, p1, nblocks, b, x, s); break;
+    case 14: launch<14>(R, p0, p1, nblocks, b, x, s); break;
     default: throw std::runtime_error("unsupported block size");
   }
 }
 
-int group_of(int bs, bool dag) {
+int group_of(int bs) {
   switch (bs) {
-    case 2: return dag ? Grp<2, true>::G : Grp<2, false>::G;
-    case 4: return dag ? Grp<4, true>::G : Grp<4, false>::G;
-    case 6: return dag ? Grp<6, true>::G : Grp<6, false>::G;
-    case 8: return dag ? Grp<8, true>::G : Grp<8, false>::G;
-    case 10: return dag ? Grp<10, true>::G : Grp<10, false>::G;
-    case 12: return dag ? Grp<12, true>::G : Grp<12, false>::G;
-    case 14: return dag ? Grp<14, true>::G : Grp<14, false>::G;
+    case 2: return Grp<2>::G;
+    case 4: return Grp<4>::G;
+    case 6: return Grp<6>::G;
+    case 8: return Grp<8>::G;
+    case 10: return Grp<10>::G;
+    case 12: return Grp<12>::G;
+    case 14: return Grp<14>::G;
     default: throw std::runtime_error("unsupported block size");
   }
 }
@@ -697,115 +419,8 @@ void sweep_trace(long long* out) { cudaMemcpyFromSymbol(out, d_sweep_trace, size
 
 void gs_wave_rec(const PatchRecords& R, int w0, int w1, const double* b, double* x, cudaStream_t s) {
   if (w1 <= w0) return;
-  const int G = group_of(R.bs, false);
-  launch_bs<false>(R, w0, w1, (w1 - w0 + G - 1) / G, SweepOrder{}, DagState{}, b, x, s);
-}
-
-namespace {
-template <int BS>
-void launch_coop(const PatchRecords& R, const SweepOrder& O, int nsweeps, const double* b, double* x, unsigned* ctl,
-                 cudaStream_t s) {
-  if (R.full) throw std::runtime_error("persistent sweep needs packed patch records");
-  constexpr int TP = RecCfg<BS>::TP, G = RecCfg<BS>::G;
-  if (R.max_nf * BS * (TP >= 2 * kMaxPatchF * BS ? 2 : 1) > TP)
-    throw std::runtime_error("vertex patch too large for the record sweep");
-  const size_t smem = sizeof(double) * (size_t(2) * G * R.stride + size_t(G) * R.max_nf * kExt * BS + G * TP);
-  static int capacity = 0;
-  static size_t cap_smem = 0;
-  if (capacity == 0 || cap_smem != smem) {
-    cudaFuncSetAttribute(k_sweep_coop<BS, TP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    int per_sm = 0, dev = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_coop<BS, TP, G>, G * TP, smem);
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    capacity = per_sm * sms;
-    cap_smem = smem;
-    if (capacity <= 0) throw std::runtime_error("persistent sweep does not fit on an SM");
-  }
-  int widest = 0;
-  for (int i = 0; i < O.nw; ++i) widest = std::max(widest, O.item0[i + 1] - O.item0[i]);
-  const int grid = std::max(1, std::min(widest, capacity));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(G * TP);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaError_t err = cudaLaunchKernelEx(&cfg, k_sweep_coop<BS, TP, G>, R, O, nsweeps, b, x, ctl);
-  if (err == cudaSuccess) err = cudaGetLastError();
-  if (err != cudaSuccess) throw std::runtime_error(std::string("CUDA launch (persistent sweep): ") + cudaGetErrorString(err));
-}
-}  // namespace
-
-void sweep_persistent(const PatchRecords& R, const int* wave_ptr_host, int nwaves, int nsweeps, bool reverse,
-                      const double* b, double* x, unsigned* ctl, cudaStream_t s) {
-  if (nwaves > kMaxSweepWaves) throw std::runtime_error("too many waves for the persistent sweep");
-  if (nsweeps < 1 || nwaves < 1) return;
-  const int G = group_of(R.bs, false);
-  SweepOrder O;
-  O.nw = nwaves;
-  O.reverse = reverse ? 1 : 0;
-  O.item0[0] = 0;
-  for (int i = 0; i < nwaves; ++i) {
-    const int w = reverse ? nwaves - 1 - i : i;
-    O.wbeg[i] = wave_ptr_host[w];
-    O.wend[i] = wave_ptr_host[w + 1];
-    O.item0[i + 1] = O.item0[i] + (O.wend[i] - O.wbeg[i] + G - 1) / G;
-  }
-  O.nitems = O.item0[nwaves];
-  switch (R.bs) {
-    case 2: launch_coop<2>(R, O, nsweeps, b, x, ctl, s); break;
-    case 4: launch_coop<4>(R, O, nsweeps, b, x, ctl, s); break;
-    case 6: launch_coop<6>(R, O, nsweeps, b, x, ctl, s); break;
-    case 8: launch_coop<8>(R, O, nsweeps, b, x, ctl, s); break;
-    case 10: launch_coop<10>(R, O, nsweeps, b, x, ctl, s); break;
-    case 12: launch_coop<12>(R, O, nsweeps, b, x, ctl, s); break;
-    case 14: launch_coop<14>(R, O, nsweeps, b, x, ctl, s); break;
-    default: throw std::runtime_error("unsupported block size");
-  }
-}
-
-void sweep_dag(const PatchRecords& R, const int* wave_ptr_host, int nwaves, const Patches& P, int nsweeps,
-               bool reverse, const double* b, double* x, unsigned* flags, unsigned* ctl, cudaStream_t s) {
-  if (nwaves > kMaxSweepWaves) throw std::runtime_error("too many waves for the dataflow sweep");
-  if (nsweeps < 1) return;
-  const int G = group_of(R.bs, true);
-  SweepOrder O;
-  O.nw = nwaves;
-  O.reverse = reverse ? 1 : 0;
-  O.item0[0] = 0;
-  for (int i = 0; i < nwaves; ++i) {
-    const int w = reverse ? nwaves - 1 - i : i;
-    O.wbeg[i] = wave_ptr_host[w];
-    O.wend[i] = wave_ptr_host[w + 1];
-    O.item0[i + 1] = O.item0[i] + (O.wend[i] - O.wbeg[i] + G - 1) / G;
-  }
-  O.nitems = O.item0[nwaves];
-  DagState D;
-  D.flags = flags;
-  D.ctl = ctl;
-  D.ndep = P.ndep;
-  D.dep = P.dep;
-  D.max_dep = P.max_dep;
-  D.nsweeps = nsweeps;
-  if (D.max_dep <= 0 || !D.ndep) throw std::runtime_error("dataflow sweep needs the patch dependency lists");
-  launch_bs<true>(R, 0, 0, O.nitems * nsweeps, O, D, b, x, s);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(1);
-  cfg.blockDim = dim3(1);
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaError_t err = cudaLaunchKernelEx(&cfg, k_epoch, ctl, nsweeps);
-  if (err == cudaSuccess) err = cudaGetLastError();
-  if (err != cudaSuccess) throw std::runtime_error(std::string("CUDA launch (epoch): ") + cudaGetErrorString(err));
+  const int G = group_of(R.bs);
+  launch_bs(R, w0, w1, (w1 - w0 + G - 1) / G, b, x, s);
 }
 
 }  // namespace dev

@@ -1,7 +1,19 @@
 """GPU-vs-oracle parity of the advected (Oseen/Picard) path: upwinded
 condensation, A^T backward sweeps, nonsymmetric V-cycle, device GMRES and the
 Uzawa loop (BASELINE config 5 shape at small sizes). Tolerances as in
-test_gpu_parity.py; GMRES counts +-1."""
+test_gpu_parity.py; GMRES counts +-1 up to 100 iterations.
+
+Beyond ~100 unrestarted MGS-GMRES iterations the count follows round-off
+chaotically; the reference itself moves there: at nu = 1e-3 (180 its) its
+FMA-contracted build takes 182 iterations, its plain build 180, the
+restatement 180 and the same algorithm in extended precision 179
+(tests/test_reference_pins.py, oracle/hp_solve.cpp). The device's
+direct-gather correction sweeps (sweep="direct_nonsym": x_p += S_p (b-Ax)_p,
+error proportional to the residual) stay within that spread (+-4). The
+default patch-record sweeps (x_p = S_p (b_p - A_pe x_e), which never read
+A_pp and make the config-5 V-cycle 2.3x faster) carry the explicit inverse's
+rounding on x_p itself and trade count parity in such long runs for that
+speed: 194 iterations there, checked against a 10% band and the solution."""
 import numpy as np
 import pytest
 
@@ -15,15 +27,15 @@ WIND = {"rotation": O.WIND_ROT, "config5_wind": O.WIND_CURL}
 
 
 def pair(k, wind="config5_wind", base_n=2, levels=3, nu=1e-2, beta=0.0, inv_eps=1e3, lid=True, seed=3, m=1,
-         cycle=O.CYCLE_V):
+         cycle=O.CYCLE_V, sweep="records", reference=False):
     n_f = base_n << (levels - 1)
     F = O.seeded_load(n_f, seed, -0.1, 0.1)
-    orc = O.OracleMG(base_n=base_n, levels=levels, k=k, nu=nu, beta=beta, inv_eps=inv_eps,
+    orc = O.OracleMG(reference=reference, base_n=base_n, levels=levels, k=k, nu=nu, beta=beta, inv_eps=inv_eps,
                      bc=O.BC_LID_UNIT if lid else O.BC_NONE, load_kind=O.LOAD_ARRAY, load=F, wind=WIND[wind],
                      cycle=cycle, smooth_steps=m)
     gpu = H.MGPreconditioner(base_n=base_n, levels=levels, k=k, nu=nu, beta=beta, inv_eps=inv_eps,
                              bc="lid_unit" if lid else None, structured_load=(n_f, F), wind=wind, cycle=cycle,
-                             smooth_steps=m)
+                             smooth_steps=m, sweep=sweep)
     return orc, gpu
 
 
@@ -60,22 +72,30 @@ def test_advected_vcycle(k):
     assert rel(gpu.apply(b), orc.apply(b)) < 1e-10
 
 
-@pytest.mark.parametrize("k,nu", [(0, 1.0), (1, 1e-2), (2, 1e-2), (2, 1e-3)])
-def test_gmres_counts_and_solution(k, nu):
-    orc, gpu = pair(k, nu=nu, levels=4)
+@pytest.mark.parametrize("k,nu,sweep", [(0, 1.0, "records"), (1, 1e-2, "records"), (2, 1e-2, "records"),
+                                         (2, 1e-2, "direct_nonsym"), (2, 1e-3, "direct_nonsym")])
+def test_gmres_counts_and_solution(k, nu, sweep):
+    orc, gpu = pair(k, nu=nu, levels=4, sweep=sweep, reference=O.ref_available())
     b = orc.rhs()
     xo, so = orc.krylov(b, method=1)
     xg, sg = H.gmres(gpu, b)
     assert so["converged"] and sg.converged
-    # +-1 (north star) up to ~100 iterations. Unrestarted MGS-GMRES beyond that
-    # (nu = 1e-3: 180 its) loses orthogonality at the round-off level and the
-    # count follows the preconditioner's rounding chaotically: with V-cycles
-    # that agree with the oracle to 1.0e-11 (direct-gather sweeps) and 1.5e-11
-    # (patch-record sweeps, the default) it ends at 183 and 194
-    # (tools/oseen_margin.py); the count moves by 2-3 even between FMA-contracted
-    # and plain transfer builds. Long runs get 10 %; the solution must agree.
-    band = 1 if so["iterations"] <= 100 else int(0.10 * so["iterations"])
-    assert abs(sg.iterations - so["iterations"]) <= max(1, band)
+    # +-1 (north star) up to 100 iterations; beyond, the reference's own spread
+    # (its FMA / plain builds: 182 / 180 at nu = 1e-3, module docstring)
+    band = 1 if so["iterations"] <= 100 else 4
+    assert abs(sg.iterations - so["iterations"]) <= band
+    assert rel(xg, xo) < 1e-8
+
+
+def test_gmres_long_run_record_sweeps():
+    # the default record sweeps in the 180-iteration case: solution parity, and
+    # the count within 10% (documented trade-off, module docstring)
+    orc, gpu = pair(2, nu=1e-3, levels=4, reference=O.ref_available())
+    b = orc.rhs()
+    xo, so = orc.krylov(b, method=1)
+    xg, sg = H.gmres(gpu, b)
+    assert so["converged"] and sg.converged
+    assert abs(sg.iterations - so["iterations"]) <= int(0.10 * so["iterations"])
     assert rel(xg, xo) < 1e-8
 
 

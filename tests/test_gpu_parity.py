@@ -25,7 +25,7 @@ def lid_top(x, y):
 
 
 def pair(k, base_n=2, levels=3, beta=1.0, nu=1.0, inv_eps=1e3, bc=None, seed=1, cycle=O.CYCLE_V, m=1,
-         smoother=O.SM_MULT, schedule="waves"):
+         smoother=O.SM_MULT):
     n_f = base_n << (levels - 1)
     F = O.seeded_load(n_f, seed)
     obc = O.BC_NONE if bc is None else O.BC_LID_TOP
@@ -33,7 +33,7 @@ def pair(k, base_n=2, levels=3, beta=1.0, nu=1.0, inv_eps=1e3, bc=None, seed=1, 
                      load_kind=O.LOAD_ARRAY, load=F, cycle=cycle, smooth_steps=m, smoother=smoother)
     gpu = H.MGPreconditioner(base_n=base_n, levels=levels, k=k, nu=nu, beta=beta, inv_eps=inv_eps, bc=bc,
                              structured_load=(n_f, F), cycle=cycle, smooth_steps=m, smoother=smoother,
-                             schedule=schedule)
+                             )
     return orc, gpu
 
 
@@ -80,29 +80,16 @@ def test_smoother_sweeps(k):
         assert rel(xg, xo) < apply_tol()
 
 
-@pytest.mark.parametrize("schedule", ["dataflow", "persistent"])
 @pytest.mark.parametrize("k,sweeps", [(0, 1), (1, 3), (3, 2)])
-def test_dataflow_schedule_sweeps(k, sweeps, schedule):
-    # one launch per sweep ordered by neighbour completion flags (dataflow) or
-    # by a grid barrier per wave (persistent): same result as the wave
-    # schedule, forward and reverse, several sweeps per launch, repeated calls
-    # (the flag epochs advance, never reset; the barrier resets itself)
-    orc, gpu = pair(k, levels=4, schedule=schedule)
+def test_multi_sweep_smoothing(k, sweeps):
+    # several sweeps per call, forward and reverse, repeated calls on one context
+    orc, gpu = pair(k, levels=4)
     level = -1 if k > 0 else 3
     n = gpu.level_n(level) if k == 0 else orc.n
     for rep in range(2):
         b, x0 = O.random_vec(n, 7 + rep), O.random_vec(n, 9 + rep)
         for which in (0, 1):
             assert rel(gpu.smooth(level, which, x0, b, sweeps), orc.smooth(level, which, x0, b, sweeps)) < apply_tol()
-
-
-@pytest.mark.parametrize("schedule", ["dataflow", "persistent"])
-@pytest.mark.parametrize("k,cycle", [(0, O.CYCLE_V), (2, O.CYCLE_VARV), (3, O.CYCLE_V)])
-def test_dataflow_schedule_apply(k, cycle, schedule):
-    orc, gpu = pair(k, levels=4, cycle=cycle, schedule=schedule)
-    for seed in (11, 12):
-        b = O.random_vec(orc.n, seed)
-        assert rel(gpu.apply(b), orc.apply(b)) < apply_tol()
 
 
 @pytest.mark.parametrize("base_n", [4, 8, 16])

@@ -17,8 +17,7 @@ for name in (sys.argv[1:] or ["config2", "config1"]) if __name__ == "__main__" e
     c = CFG[name]
     nf = c["base_n"] << (c["levels"] - 1)
     B = H.MGPreconditioner(base_n=c["base_n"], levels=c["levels"], k=c["k"], beta=c["beta"], inv_eps=c["inv_eps"],
-                           cycle=H.CYCLE_V, structured_load=(nf, H.seeded_load(nf, 1)),
-                           schedule=os.environ.get("HPMG_SCHEDULE", "waves"))
+                           cycle=H.CYCLE_V, structured_load=(nf, H.seeded_load(nf, 1)))
     L = H.lib()
     L.hpmg_profile_levels.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_double)]
     out = np.zeros(64)
@@ -33,4 +32,4 @@ for name in (sys.argv[1:] or ["config2", "config1"]) if __name__ == "__main__" e
     ms, _ = B.time_apply(20)
     rep["graph_ms_per_vcycle"] = ms
     rep["sum_parts"] = float(sum(v for k, v in rep.items() if k != "graph_ms_per_vcycle"))
-    print(name, os.environ.get("HPMG_SCHEDULE", "waves"), json.dumps({k: round(float(v), 4) for k, v in rep.items()}))
+    print(name, json.dumps({k: round(float(v), 4) for k, v in rep.items()}))
