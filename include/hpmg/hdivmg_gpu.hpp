@@ -80,7 +80,7 @@ class MGPreconditioner {
                                                       : HPMG_CYCLE_VARIABLE_V,
                    mg.smoother == hdivmg::SmootherKind::Multiplicative ? HPMG_SMOOTH_MULTIPLICATIVE
                                                                        : HPMG_SMOOTH_ADDITIVE,
-                   mg.smooth_steps, mg.jacobi_damping};
+                   mg.smooth_steps, mg.jacobi_damping, HPMG_SWEEP_RECORDS};
     hpmg_problem p{};
     if (bc_) {
       p.bc = &detail::field_trampoline;
@@ -111,6 +111,10 @@ class MGPreconditioner {
     hpmg_ctx* c = nullptr;
     detail::check(hpmg_create(&c, &md, &o, &p));
     ctx_.reset(c);
+    // host-side space and constraints of the finest system (multigrid.hpp:138-141):
+    // bookkeeping only, built exactly as the reference builds them
+    space_ = hdivmg::CompoundSpace(hier.levels.back(), k);
+    con_ = hdivmg::Constraints::build(space_, bc);
   }
   MGPreconditioner(const MGPreconditioner&) = delete;
   MGPreconditioner& operator=(const MGPreconditioner&) = delete;
@@ -146,6 +150,14 @@ class MGPreconditioner {
     A.setFromTriplets(t.begin(), t.end());
     return A;
   }
+  /// transpose of matrix() for advected operators, matrix() otherwise (multigrid.hpp:136-138)
+  hdivmg::SpMat matrix_transpose() const {
+    hdivmg::SpMat A = matrix();
+    if (symmetric()) return A;
+    return hdivmg::SpMat(A.transpose());
+  }
+  const hdivmg::CompoundSpace& space() const { return space_; }
+  const hdivmg::Constraints& constraints() const { return con_; }
   Vec rhs() const {
     Vec r(hpmg_n(ctx_.get()));
     detail::check(hpmg_rhs(ctx_.get(), r.data(), 0), ctx_.get());
@@ -160,10 +172,31 @@ class MGPreconditioner {
     void operator()(hpmg_ctx* c) const { hpmg_destroy(c); }
   };
   std::function<Vec2(const Vec2&)> bc_, load_;
+  hdivmg::CompoundSpace space_;
+  hdivmg::Constraints con_;
   std::vector<double> xy_, wind_c_, wind_i_, mass_c_, mass_i_;
   std::vector<int> el_, tags_;
   std::unique_ptr<hpmg_ctx, Del> ctx_;
 };
+
+/// The reference's operator-generic solvers (krylov.hpp:30,79), so call sites
+/// written against hdivmg::pcg / hdivmg::gmres with LinearOperator arguments
+/// recompile unchanged with `using namespace hpmg` or hpmg:: qualification;
+/// with B.as_operator() as M every preconditioner application runs on the
+/// device (host vectors in and out). The device-resident loops below
+/// (pcg(B, b, x), gmres(B, b, x)) keep the whole iteration on the GPU.
+inline hdivmg::SolveStats pcg(const hdivmg::LinearOperator& A, const hdivmg::LinearOperator& M, const Vec& b, Vec& x,
+                              const hdivmg::KrylovOptions& opt = {}) {
+  return hdivmg::pcg(A, M, b, x, opt);
+}
+inline hdivmg::SolveStats gmres(const hdivmg::LinearOperator& A, const hdivmg::LinearOperator& M, const Vec& b,
+                                Vec& x, const hdivmg::KrylovOptions& opt = {}) {
+  return hdivmg::gmres(A, M, b, x, opt);
+}
+/// A LinearOperator of B.matrix() evaluated on the device (uzawa.hpp:42).
+inline hdivmg::LinearOperator matrix_operator(const MGPreconditioner& B) {
+  return [&B](const Vec& v) { return B.spmv(v); };
+}
 
 /// Device PCG with B.matrix() and B.apply (krylov.hpp:30-73).
 inline hdivmg::SolveStats pcg(const MGPreconditioner& B, const Vec& b, Vec& x, const hdivmg::KrylovOptions& opt = {}) {
@@ -241,7 +274,7 @@ inline hdivmg::NSSolution navier_stokes_solve(const hdivmg::MeshHierarchy& hier,
                                                     : HPMG_CYCLE_VARIABLE_V,
                  mg.smoother == hdivmg::SmootherKind::Multiplicative ? HPMG_SMOOTH_MULTIPLICATIVE
                                                                      : HPMG_SMOOTH_ADDITIVE,
-                 mg.smooth_steps, mg.jacobi_damping, HPMG_SCHEDULE_WAVES};
+                 mg.smooth_steps, mg.jacobi_damping, HPMG_SWEEP_RECORDS};
   std::function<Vec2(const Vec2&)> g = bc.g, f = load;
   hpmg_problem p{};
   if (g) {
