@@ -170,6 +170,19 @@ struct hpmg_ctx {
   double setup_parts[8] = {0};
   // CUDA graph of apply(kr -> kz)
   cudaGraphExec_t apply_graph = nullptr;
+  // device-resident PCG iteration: one graph with a while node (built lazily)
+  cudaGraphExec_t pcg_loop = nullptr;
+  bool pcg_loop_failed = false;
+  cudaStream_t s_cap = nullptr;  // second capture stream (conditional bodies)
+  cudaStream_t s_nest[4] = {nullptr, nullptr, nullptr, nullptr};  // nested conditional-body captures
+  // device-resident GMRES: workspace for `gm_cap` Arnoldi steps per cycle and its loop graph
+  dev::GmDev gm;
+  int gm_cap = 0, gm_graph_cap = 0;
+  cudaGraphExec_t gm_loop = nullptr;
+  bool gm_loop_failed = false;
+  bool gm_coop = true;             // fused cooperative MGS (else one launch per MGS step)
+  double* gm_part = nullptr;       // [2 * grid] partials of the cooperative MGS
+  unsigned* gm_bar = nullptr;      // its grid barrier
 
   Level& top() { return opt.k > 0 ? *head : *lv[L]; }
   int64_t nfree() { return top().n; }
@@ -693,7 +706,106 @@ void out_vec(hpmg_ctx& C, const double* src_blk, double* dst, int flags) {
 }
 
 // ---------------------------------------------------------------- solvers
-/// PCG on the device (reference inc/krylov.hpp:30-73); x/b in kx/kb.
+/// One PCG iteration as a CUDA graph: a while node whose body is
+///   Ap = A p, p.Ap | x += a p, r -= a Ap, r.r | count, stop test
+///   | if (more): z = M r (the V-cycle launch sequence), r.z, beta, p = z + beta p
+///   | continue while running
+/// (reference krylov.hpp:44-70). The branch and loop predicates are set on
+/// the device (cudaGraphSetConditional), so a whole solve is one graph launch
+/// with no host round trip per iteration. Returns false (and the host loop is
+/// used) where the driver cannot build it.
+bool build_pcg_loop(hpmg_ctx& C) {
+  Level& T = C.top();
+  const int64_t n = T.n;
+  cudaGraph_t g = nullptr;
+  cudaStream_t s_main = C.s;
+  bool capturing = false, capturing2 = false;
+  auto fail = [&](cudaError_t e) {
+    if (capturing2) {
+      cudaGraph_t tmp;
+      cudaStreamEndCapture(C.s_cap, &tmp);
+    }
+    C.s = s_main;
+    if (capturing) {
+      cudaGraph_t tmp;
+      cudaStreamEndCapture(s_main, &tmp);
+    }
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    if (std::getenv("HPMG_DEBUG_GRAPH")) std::fprintf(stderr, "pcg loop graph: %s\n", cudaGetErrorString(e));
+    return false;
+  };
+  cudaError_t e;
+  if (!C.s_cap && (e = cudaStreamCreateWithFlags(&C.s_cap, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);
+  if ((e = cudaGraphCreate(&g, 0)) != cudaSuccess) return fail(e);
+  cudaGraphConditionalHandle h_loop, h_more;
+  if ((e = cudaGraphConditionalHandleCreate(&h_loop, g, 1, cudaGraphCondAssignDefault)) != cudaSuccess) return fail(e);
+  if ((e = cudaGraphConditionalHandleCreate(&h_more, g, 0, cudaGraphCondAssignDefault)) != cudaSuccess) return fail(e);
+  cudaGraphNodeParams wp = {};
+  wp.type = cudaGraphNodeTypeConditional;
+  wp.conditional.handle = h_loop;
+  wp.conditional.type = cudaGraphCondTypeWhile;
+  wp.conditional.size = 1;
+  cudaGraphNode_t wnode;
+  if ((e = cudaGraphAddNode(&wnode, g, nullptr, 0, &wp)) != cudaSuccess) return fail(e);
+  cudaGraph_t body = wp.conditional.phGraph_out[0];
+  try {
+    if ((e = cudaStreamBeginCaptureToGraph(s_main, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal)) !=
+        cudaSuccess)
+      return fail(e);
+    capturing = true;
+    dev::spmv(T.A, C.kp, nullptr, C.kAp, 0, &C.red, C.sc + S_PAP, s_main);
+    dev::pcg_update(C.kx, C.kr, C.kp, C.kAp, n, C.sc, S_RZ0, S_PAP, C.red, S_RR, s_main);
+    dev::pcg_loop_check(C.sc, h_more, s_main);
+    // the if node, appended to the capture
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    cudaGraph_t capg;
+    if ((e = cudaStreamGetCaptureInfo(s_main, &cs, nullptr, &capg, &deps, &ndeps)) != cudaSuccess) return fail(e);
+    cudaGraphNodeParams ip = {};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = h_more;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    cudaGraphNode_t inode;
+    if ((e = cudaGraphAddNode(&inode, capg, deps, ndeps, &ip)) != cudaSuccess) return fail(e);
+    // the branch body, captured on the second stream (the V-cycle launches on C.s)
+    if ((e = cudaStreamBeginCaptureToGraph(C.s_cap, ip.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
+      return fail(e);
+    capturing2 = true;
+    C.s = C.s_cap;
+    apply_blocks(C, C.kr, C.kz);  // z = M r
+    dev::dot(C.kr, C.kz, n, C.red, C.sc + S_RZ1, C.s);
+    dev::pcg_loop_beta(C.sc, C.s);
+    dev::pcg_loop_direction(C.kp, C.kz, n, C.sc, C.s);
+    C.s = s_main;
+    cudaGraph_t ibody;
+    capturing2 = false;
+    if ((e = cudaStreamEndCapture(C.s_cap, &ibody)) != cudaSuccess) return fail(e);
+    if ((e = cudaStreamUpdateCaptureDependencies(s_main, &inode, 1, cudaStreamSetCaptureDependencies)) != cudaSuccess)
+      return fail(e);
+    dev::loop_continue(C.sc, h_loop, s_main);
+    cudaGraph_t b2;
+    capturing = false;
+    if ((e = cudaStreamEndCapture(s_main, &b2)) != cudaSuccess) return fail(e);
+  } catch (const std::exception&) {
+    return fail(cudaErrorUnknown);
+  }
+  if ((e = cudaGraphInstantiate(&C.pcg_loop, g, 0)) != cudaSuccess) {
+    C.pcg_loop = nullptr;
+    return fail(e);
+  }
+  cudaGraphDestroy(g);
+  return true;
+}
+
+/// PCG on the device (reference inc/krylov.hpp:30-73); x/b in kx/kb. The
+/// setup (r0, z0, r0.z0) syncs twice per solve; the iterations run as one
+/// graph launch (build_pcg_loop) unless HPMG_KRYLOV_HOST=1 or the graph is
+/// unavailable, where a host loop with two syncs per iteration does the same
+/// arithmetic in the same order.
 hpmg_solve_stats pcg_device(hpmg_ctx& C, const hpmg_krylov_opts& o) {
   hpmg_solve_stats st{0, 0, 0, 0.0};
   Level& T = C.top();
@@ -717,6 +829,20 @@ hpmg_solve_stats pcg_device(hpmg_ctx& C, const hpmg_krylov_opts& o) {
     return st;
   }
   dev::copy(C.kp, C.kz, n, C.s);
+  if (o.max_iterations <= 0) return st;
+  static const bool host_loop = std::getenv("HPMG_KRYLOV_HOST") && std::atoi(std::getenv("HPMG_KRYLOV_HOST"));
+  if (!host_loop && !C.pcg_loop && !C.pcg_loop_failed) C.pcg_loop_failed = !build_pcg_loop(C);
+  if (!host_loop && C.pcg_loop) {
+    dev::pcg_loop_init(C.sc, target, double(o.max_iterations), C.s);
+    CK(cudaGraphLaunch(C.pcg_loop, C.s));
+    read_scalars(C);
+    const double status = C.sc_host[dev::kScStatus];
+    st.iterations = int(C.sc_host[dev::kScIt]);
+    st.residual = std::sqrt(C.sc_host[S_RR]);
+    st.converged = status == dev::kLoopConverged;
+    st.not_applicable = status == dev::kLoopNaPAp || status == dev::kLoopNaRZ;
+    return st;
+  }
   for (int it = 0; it < o.max_iterations; ++it) {
     dev::spmv(T.A, C.kp, nullptr, C.kAp, 0, &C.red, C.sc + S_PAP, C.s);
     dev::pcg_update(C.kx, C.kr, C.kp, C.kAp, n, C.sc, cur, S_PAP, C.red, S_RR, C.s);
@@ -744,6 +870,160 @@ hpmg_solve_stats pcg_device(hpmg_ctx& C, const hpmg_krylov_opts& o) {
   return st;
 }
 
+
+// ------------------------------------------------ conditional-graph capture
+struct GraphError {
+  cudaError_t e;
+};
+inline void GK(cudaError_t e) {
+  if (e != cudaSuccess) throw GraphError{e};
+}
+/// Appends a conditional node after the work captured so far on `s`; later
+/// captured work depends on it. Returns the node's body graph.
+cudaGraph_t add_conditional(cudaStream_t s, cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type) {
+  cudaStreamCaptureStatus cs;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  cudaGraph_t capg;
+  GK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &capg, &deps, &ndeps));
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = type;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  GK(cudaGraphAddNode(&node, capg, deps, ndeps, &p));
+  GK(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+  return p.conditional.phGraph_out[0];
+}
+/// Captures fn() into `body` on nesting stream `depth`, with C.s pointing at
+/// that stream meanwhile (the V-cycle helpers launch on C.s).
+template <class F>
+void capture_body(hpmg_ctx& C, cudaGraph_t body, int depth, F fn) {
+  if (!C.s_nest[depth]) GK(cudaStreamCreateWithFlags(&C.s_nest[depth], cudaStreamNonBlocking));
+  cudaStream_t q = C.s_nest[depth], saved = C.s;
+  GK(cudaStreamBeginCaptureToGraph(q, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  C.s = q;
+  try {
+    fn();
+  } catch (...) {
+    C.s = saved;
+    cudaGraph_t tmp;
+    cudaStreamEndCapture(q, &tmp);
+    throw;
+  }
+  C.s = saved;
+  cudaGraph_t tmp;
+  GK(cudaStreamEndCapture(q, &tmp));
+}
+
+/// GMRES workspace for `cap` Arnoldi steps per cycle (grows only).
+void gm_workspace(hpmg_ctx& C, int cap) {
+  if (cap <= C.gm_cap) return;
+  for (void* p : {(void*)C.gm.V, (void*)C.gm.H, (void*)C.gm.cs, (void*)C.gm.sn, (void*)C.gm.g, (void*)C.gm.y})
+    if (p) cudaFree(p);
+  const int64_t n = C.top().n;
+  C.gm.ldv = (n + 31) & ~int64_t(31);
+  C.gm.ldh = cap + 1;
+  C.gm.V = dalloc<double>(size_t(cap + 1) * size_t(C.gm.ldv));
+  C.gm.H = dalloc<double>(size_t(cap) * size_t(cap + 1));
+  C.gm.cs = dalloc<double>(cap);
+  C.gm.sn = dalloc<double>(cap);
+  C.gm.g = dalloc<double>(cap + 1);
+  C.gm.y = dalloc<double>(cap);
+  if (!C.gm.st) C.gm.st = dalloc<double>(8);
+  if (!C.gm_part) {
+    C.gm_part = dalloc<double>(size_t(2) * std::max(dev::mgs_coop_grid(), 1));
+    C.gm_bar = dalloc<unsigned>(1);
+    CK(cudaMemsetAsync(C.gm_bar, 0, sizeof(unsigned), C.s));
+  }
+  C.gm_cap = cap;
+  if (C.gm_loop) cudaGraphExecDestroy(C.gm_loop);
+  C.gm_loop = nullptr;
+}
+
+/// The whole restarted GMRES (reference krylov.hpp:79-144) as one graph:
+///   while (running):                                  -- restart cycles
+///     r = b - A x, r.r, true-residual test
+///     if (not converged):
+///       V0 = r / beta
+///       while (Arnoldi continues):                    -- steps j
+///         kr = V[j]; kz = M kr (V-cycle); w = A kz
+///         while (i <= j): w -= h(i-1) V[i-1]; h(i) = w.V[i]   (fused MGS)
+///         w -= h(j) V[j], |w|; V[j+1] = w / h(j+1); Givens, g, stop test
+///       y = H \ g; kr = sum y_i V[i]; kz = M kr; x += kz
+///       r = b - A x, r.r; converged / stalled / out of iterations
+/// Every predicate is set on the device.
+bool build_gm_loop(hpmg_ctx& C) {
+  Level& T = C.top();
+  const int64_t n = T.n;
+  const dev::GmDev G = C.gm;
+  cudaGraph_t g = nullptr;
+  try {
+    GK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h_outer, h_cyc, h_inner, h_mgs;
+    GK(cudaGraphConditionalHandleCreate(&h_outer, g, 1, cudaGraphCondAssignDefault));
+    GK(cudaGraphConditionalHandleCreate(&h_cyc, g, 0, cudaGraphCondAssignDefault));
+    GK(cudaGraphConditionalHandleCreate(&h_inner, g, 0, cudaGraphCondAssignDefault));
+    GK(cudaGraphConditionalHandleCreate(&h_mgs, g, 0, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams wp = {};
+    wp.type = cudaGraphNodeTypeConditional;
+    wp.conditional.handle = h_outer;
+    wp.conditional.type = cudaGraphCondTypeWhile;
+    wp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    GK(cudaGraphAddNode(&wnode, g, nullptr, 0, &wp));
+    capture_body(C, wp.conditional.phGraph_out[0], 0, [&] {
+      dev::spmv(T.A, C.kx, C.kb, C.kr, 1, nullptr, nullptr, C.s);
+      dev::dot(C.kr, C.kr, n, C.red, C.sc + S_RR, C.s);
+      dev::gm_start(C.sc, G, h_cyc, h_inner, C.s);
+      cudaGraph_t cyc = add_conditional(C.s, h_cyc, cudaGraphCondTypeIf);
+      capture_body(C, cyc, 1, [&] {
+        dev::gm_v0(G, C.kr, n, C.s);
+        cudaGraph_t inner = add_conditional(C.s, h_inner, cudaGraphCondTypeWhile);
+        capture_body(C, inner, 2, [&] {
+          dev::gm_copy(G, C.kr, n, h_mgs, C.s);
+          apply_blocks(C, C.kr, C.kz);                                  // z = M v_j
+          dev::spmv(T.A, C.kz, nullptr, C.ktmp, 0, nullptr, nullptr, C.s);  // w = A z
+          if (C.gm_coop) {
+            // all of the column's Gram-Schmidt, h(j+1) and V[j+1] in one cooperative launch
+            if (!dev::mgs_coop(G, C.ktmp, n, C.gm_part, C.gm_bar, C.s)) throw GraphError{cudaErrorNotSupported};
+            dev::gm_givens(C.sc, G, h_inner, C.s);
+          } else {
+            cudaGraph_t mgs = add_conditional(C.s, h_mgs, cudaGraphCondTypeWhile);
+            capture_body(C, mgs, 3, [&] { dev::mgs_step(G, C.ktmp, n, C.red, h_mgs, C.s); });
+            dev::mgs_tail(G, C.ktmp, n, C.red, C.s);
+            dev::gm_arnoldi_close(C.sc, G, C.ktmp, n, h_inner, C.s);
+          }
+        });
+        dev::gm_update(G, C.kr, n, C.s);  // u = V y into the preconditioner's input
+        apply_blocks(C, C.kr, C.kz);
+        dev::axpy(C.kx, 1.0, C.kz, n, C.s);
+        dev::spmv(T.A, C.kx, C.kb, C.kr, 1, nullptr, nullptr, C.s);
+        dev::dot(C.kr, C.kr, n, C.red, C.sc + S_RR, C.s);
+        dev::gm_end(C.sc, G, C.s);
+      });
+      dev::loop_continue(C.sc, h_outer, C.s);
+    });
+    GK(cudaGraphInstantiate(&C.gm_loop, g, 0));
+  } catch (const GraphError& e) {
+    if (g) cudaGraphDestroy(g);
+    C.gm_loop = nullptr;
+    cudaGetLastError();
+    if (std::getenv("HPMG_DEBUG_GRAPH")) std::fprintf(stderr, "gmres loop graph: %s\n", cudaGetErrorString(e.e));
+    return false;
+  } catch (const std::exception& e) {
+    if (g) cudaGraphDestroy(g);
+    C.gm_loop = nullptr;
+    cudaGetLastError();
+    if (std::getenv("HPMG_DEBUG_GRAPH")) std::fprintf(stderr, "gmres loop graph: %s\n", e.what());
+    return false;
+  }
+  cudaGraphDestroy(g);
+  C.gm_graph_cap = C.gm_cap;
+  return true;
+}
+
 double* gm_vec(hpmg_ctx& C, int i) {
   while (int(C.gm_basis.size()) <= i) C.gm_basis.push_back(dalloc<double>(C.top().n));
   return C.gm_basis[i];
@@ -758,6 +1038,31 @@ hpmg_solve_stats gmres_device(hpmg_ctx& C, const hpmg_krylov_opts& o) {
   dev::dot(C.kb, C.kb, n, C.red, C.sc + S_BB, C.s);
   read_scalars(C);
   const double target = std::max(o.rel_tol * std::sqrt(C.sc_host[S_BB]), o.abs_tol);
+  static const bool host_loop = std::getenv("HPMG_KRYLOV_HOST") && std::atoi(std::getenv("HPMG_KRYLOV_HOST"));
+  if (!host_loop && o.max_iterations > 0 && !C.gm_loop_failed) {
+    // one graph launch for the whole solve (build_gm_loop)
+    const int want = o.restart > 0 ? std::min(o.restart, o.max_iterations) : o.max_iterations;
+    gm_workspace(C, want);
+    if (!C.gm_loop || C.gm_graph_cap != C.gm_cap) {
+      static const bool no_coop = std::getenv("HPMG_GMRES_COOP") && !std::atoi(std::getenv("HPMG_GMRES_COOP"));
+      C.gm_coop = !no_coop;
+      bool ok = build_gm_loop(C);
+      if (!ok && C.gm_coop) {  // the fused MGS could not be captured: one launch per MGS step
+        C.gm_coop = false;
+        ok = build_gm_loop(C);
+      }
+      C.gm_loop_failed = !ok;
+    }
+    if (C.gm_loop) {
+      dev::gm_init(C.sc, C.gm, target, double(o.max_iterations), want, C.s);
+      CK(cudaGraphLaunch(C.gm_loop, C.s));
+      read_scalars(C);
+      st.iterations = int(C.sc_host[dev::kScIt]);
+      st.residual = std::sqrt(C.sc_host[S_RR]);
+      st.converged = C.sc_host[dev::kScStatus] == dev::kLoopConverged;
+      return st;
+    }
+  }
   const double breakdown = 1e-14;
   const int cap = o.restart > 0 ? o.restart : (1 << 30);
   while (st.iterations < o.max_iterations) {
@@ -1191,6 +1496,10 @@ int hpmg_update(hpmg_ctx* ctx, const hpmg_options* opt, const hpmg_problem* prob
     linearise(C, prob, Tk.get());
     if (C.apply_graph) cudaGraphExecDestroy(C.apply_graph);
     C.apply_graph = nullptr;
+    if (C.pcg_loop) cudaGraphExecDestroy(C.pcg_loop);
+    C.pcg_loop = nullptr;
+    if (C.gm_loop) cudaGraphExecDestroy(C.gm_loop);
+    C.gm_loop = nullptr;
     build_apply_graph(C);
     CK(cudaStreamSynchronize(C.s));
     C.setup_parts[1] = C.lin_parts[3];
@@ -1206,6 +1515,14 @@ void hpmg_destroy(hpmg_ctx* ctx) {
   if (!ctx) return;
   cudaStreamSynchronize(ctx->s);
   if (ctx->apply_graph) cudaGraphExecDestroy(ctx->apply_graph);
+  if (ctx->pcg_loop) cudaGraphExecDestroy(ctx->pcg_loop);
+  if (ctx->s_cap) cudaStreamDestroy(ctx->s_cap);
+  if (ctx->gm_loop) cudaGraphExecDestroy(ctx->gm_loop);
+  for (cudaStream_t q : ctx->s_nest)
+    if (q) cudaStreamDestroy(q);
+  for (void* p : {(void*)ctx->gm.V, (void*)ctx->gm.H, (void*)ctx->gm.cs, (void*)ctx->gm.sn, (void*)ctx->gm.g,
+                  (void*)ctx->gm.y, (void*)ctx->gm.st, (void*)ctx->gm_part, (void*)ctx->gm_bar})
+    if (p) cudaFree(p);
   auto fr = [](void* p) { if (p) cudaFree(p); };
   auto free_level = [&](Level* V) {
     if (!V) return;

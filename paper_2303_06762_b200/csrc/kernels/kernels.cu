@@ -1062,6 +1062,312 @@ __global__ void k_pcg_update(double* __restrict__ x, double* __restrict__ r, con
   }
   finalize<false>(s, red, sc + i_rr);
 }
+// ---- device-resident PCG iteration (one CUDA-graph while loop per solve;
+// reference krylov.hpp:30-73). Scalars live in sc[]: the loop slots below,
+// the reduction results written by the vector kernels.
+/// after the x/r update: iteration count, stop decision, the if-branch handle
+__global__ void k_pcg_loop_check(double* sc, cudaGraphConditionalHandle h_more) {
+  double st = kLoopRunning;
+  if (!(sc[kScPAp] > 0.0)) {
+    st = kLoopNaPAp;  // krylov.hpp:49-53; k_pcg_update left x and r untouched
+  } else {
+    sc[kScIt] += 1.0;  // st.iterations = it + 1
+    if (sqrt(sc[kScRR]) <= sc[kScTarget]) st = kLoopConverged;
+    else if (sc[kScIt] >= sc[kScMaxIt]) st = kLoopLast;  // the reference still forms z, r.z once more
+  }
+  sc[kScStatus] = st;
+  cudaGraphSetConditional(h_more, (st == kLoopRunning || st == kLoopLast) ? 1u : 0u);
+}
+/// after r.z: positivity (krylov.hpp:63-68), beta = rz_next / rz, rz = rz_next
+__global__ void k_pcg_loop_beta(double* sc) {
+  const double rzn = sc[kScRZn];
+  if (!(rzn > 0.0)) {
+    sc[kScStatus] = kLoopNaRZ;
+    return;
+  }
+  if (sc[kScStatus] == kLoopLast) {
+    sc[kScStatus] = kLoopMaxIt;
+    return;
+  }
+  sc[kScBeta] = rzn / sc[kScRZ];
+  sc[kScRZ] = rzn;
+}
+/// p = z + beta p while running (krylov.hpp:69)
+__global__ void k_pcg_loop_direction(double* __restrict__ p, const double* __restrict__ z, int64_t n,
+                                     const double* sc) {
+  if (sc[kScStatus] != kLoopRunning) return;
+  const double beta = sc[kScBeta];
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x)
+    p[t] = z[t] + beta * p[t];
+}
+/// last node of the loop body: iterate again while running
+__global__ void k_loop_continue(const double* sc, cudaGraphConditionalHandle h_loop) {
+  cudaGraphSetConditional(h_loop, sc[kScStatus] == kLoopRunning ? 1u : 0u);
+}
+__global__ void k_gm_init(double* sc, GmDev G, double target, double max_it, double cap) {
+  sc[kScIt] = 0.0;
+  sc[kScStatus] = kLoopRunning;
+  sc[kScTarget] = target;
+  sc[kScMaxIt] = max_it;
+  G.st[kGmCap] = cap;
+}
+__global__ void k_pcg_loop_init(double* sc, double target, double max_it) {
+  sc[kScIt] = 0.0;
+  sc[kScStatus] = kLoopRunning;
+  sc[kScTarget] = target;
+  sc[kScMaxIt] = max_it;
+}
+
+// ---- device-resident GMRES (reference krylov.hpp:79-144): restart cycles
+// and Arnoldi steps as nested graph loops; modified Gram-Schmidt one fused
+// pass per basis vector; Givens rotations and the triangular solve in
+// single-thread kernels on the device-side Hessenberg columns.
+/// top of a cycle, after r = b - A x and r.r: true-residual test, g = (beta)
+__global__ void k_gm_start(double* sc, GmDev G, cudaGraphConditionalHandle h_cyc,
+                           cudaGraphConditionalHandle h_inner) {
+  const double beta = sqrt(sc[kScRR]);
+  if (beta <= sc[kScTarget]) {
+    sc[kScStatus] = kLoopConverged;
+    cudaGraphSetConditional(h_cyc, 0u);
+    cudaGraphSetConditional(h_inner, 0u);
+    return;
+  }
+  G.st[kGmBeta] = beta;
+  G.st[kGmJ] = 0.0;
+  G.st[kGmM] = 0.0;
+  G.st[kGmStalled] = 0.0;
+  G.g[0] = beta;
+  cudaGraphSetConditional(h_cyc, 1u);
+  cudaGraphSetConditional(h_inner, sc[kScIt] < sc[kScMaxIt] ? 1u : 0u);
+}
+/// V[0] = r / beta
+__global__ void k_gm_v0(GmDev G, const double* __restrict__ r, int64_t n) {
+  const double beta = G.st[kGmBeta];
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x)
+    G.V[t] = r[t] / beta;
+}
+/// dst = V[j] (the preconditioner's input); arms the Gram-Schmidt loop
+__global__ void k_gm_copy(GmDev G, double* __restrict__ dst, int64_t n, cudaGraphConditionalHandle h_mgs) {
+  const double* v = G.V + int64_t(G.st[kGmJ]) * G.ldv;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x)
+    dst[t] = v[t];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    G.st[kGmI] = 0.0;
+    cudaGraphSetConditional(h_mgs, 1u);
+  }
+}
+/// MGS step i of column j (krylov.hpp:100-103), the axpy of step i-1 fused
+/// with the dot of step i: w -= h(i-1) v(i-1); h(i) = w . v(i)
+__global__ void k_mgs(GmDev G, double* __restrict__ w, int64_t n, Reduce red, cudaGraphConditionalHandle h_mgs) {
+  const int i = int(G.st[kGmI]), j = int(G.st[kGmJ]);
+  double* hcol = G.H + int64_t(j) * G.ldh;
+  const double* vi = G.V + int64_t(i) * G.ldv;
+  double s = 0.0;
+  if (i > 0) {
+    const double hp = hcol[i - 1];
+    const double* vp = G.V + int64_t(i - 1) * G.ldv;
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+      const double wt = w[t] - hp * vp[t];
+      w[t] = wt;
+      s = fma(wt, vi[t], s);
+    }
+  } else {
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x)
+      s = fma(w[t], vi[t], s);
+  }
+  __shared__ bool last;
+  s = block_reduce<false>(s);
+  if (threadIdx.x == 0) {
+    red.partial[blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(red.counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    double a = 0.0;
+    for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x) a += __ldcg(&red.partial[b]);
+    a = block_reduce<false>(a);
+    if (threadIdx.x == 0) {
+      hcol[i] = a;
+      *red.counter = 0u;
+      G.st[kGmI] = double(i + 1);
+      cudaGraphSetConditional(h_mgs, i + 1 <= j ? 1u : 0u);
+    }
+  }
+}
+/// Grid barrier number `epoch` (1-based) of a cooperative launch: one
+/// release arrival per CTA on a monotonic counter, acquire polls.
+__device__ __forceinline__ void coop_barrier(unsigned* bar, unsigned epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    const unsigned target = epoch * gridDim.x;
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+/// The whole modified Gram-Schmidt of Arnoldi column j in ONE cooperative
+/// launch (krylov.hpp:100-106): each CTA keeps its contiguous slice of w and
+/// of the previous basis vector in registers, so per step i only V[i] is
+/// read (once); the dot of step i is reduced grid-wide through a barrier and
+/// summed by every CTA in the same fixed order. Step i performs the axpy of
+/// step i-1 then the dot of step i, i.e. per entry exactly the reference's
+/// sequence; after step j the norm of w gives h(j+1), the happy-breakdown
+/// flag, and V[j+1] = w / h(j+1).
+template <int E>
+__global__ void __launch_bounds__(256) k_mgs_coop(GmDev G, const double* __restrict__ w_in, int64_t n,
+                                                  double* __restrict__ part, unsigned* bar) {
+  __shared__ double bcast;
+  const int j = int(G.st[kGmJ]);
+  const int64_t per = ((n + gridDim.x - 1) / gridDim.x + 255) / 256 * 256;
+  const int64_t c0 = int64_t(blockIdx.x) * per;
+  double w[E], vp[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int64_t t = c0 + threadIdx.x + int64_t(e) * 256;
+    w[e] = (t < n && t < c0 + per) ? w_in[t] : 0.0;
+    vp[e] = 0.0;
+  }
+  double* hcol = G.H + int64_t(j) * G.ldh;
+  double hprev = 0.0;
+  unsigned epoch = 0;
+  for (int i = 0; i <= j + 1; ++i) {
+    double s = 0.0;
+    if (i <= j) {
+      const double* vi = G.V + int64_t(i) * G.ldv;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int64_t t = c0 + threadIdx.x + int64_t(e) * 256;
+        if (i > 0) w[e] = w[e] - hprev * vp[e];
+        const double v = (t < n && t < c0 + per) ? vi[t] : 0.0;
+        vp[e] = v;
+        s = fma(w[e], v, s);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        w[e] = w[e] - hprev * vp[e];
+        s = fma(w[e], w[e], s);
+      }
+    }
+    s = block_reduce<false>(s);
+    double* pb = part + size_t(i & 1) * gridDim.x;
+    if (threadIdx.x == 0) pb[blockIdx.x] = s;
+    coop_barrier(bar, ++epoch);
+    double a = 0.0;
+    for (int b = threadIdx.x; b < int(gridDim.x); b += blockDim.x) a += __ldcg(pb + b);
+    a = block_reduce<false>(a);
+    if (threadIdx.x == 0) bcast = a;
+    __syncthreads();
+    hprev = bcast;
+    if (i <= j && blockIdx.x == 0 && threadIdx.x == 0) hcol[i] = hprev;
+  }
+  const double h = sqrt(hprev);
+  const bool happy = h <= 1e-14 * G.st[kGmBeta];
+  if (!happy) {
+    double* vn = G.V + int64_t(j + 1) * G.ldv;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int64_t t = c0 + threadIdx.x + int64_t(e) * 256;
+      if (t < n && t < c0 + per) vn[t] = w[e] / h;
+    }
+  }
+  // every CTA has read the partials of the last step: reset for the next launch
+  coop_barrier(bar, ++epoch);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    hcol[j + 1] = h;
+    G.st[kGmHn] = hprev;
+    G.st[kGmHappy] = happy ? 1.0 : 0.0;
+    bar[0] = 0u;
+  }
+}
+
+/// last axpy of column j and |w|^2
+__global__ void k_mgs_tail(GmDev G, double* __restrict__ w, int64_t n, Reduce red) {
+  const int j = int(G.st[kGmJ]);
+  const double hp = G.H[int64_t(j) * G.ldh + j];
+  const double* vp = G.V + int64_t(j) * G.ldv;
+  double s = 0.0;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const double wt = w[t] - hp * vp[t];
+    w[t] = wt;
+    s = fma(wt, wt, s);
+  }
+  finalize<false>(s, red, G.st + kGmHn);
+}
+/// h(j+1) = |w|, the happy-breakdown flag (krylov.hpp:104-105)
+__global__ void k_gm_hnorm(GmDev G) {
+  const int j = int(G.st[kGmJ]);
+  const double h = sqrt(G.st[kGmHn]);
+  G.H[int64_t(j) * G.ldh + j + 1] = h;
+  G.st[kGmHappy] = h <= 1e-14 * G.st[kGmBeta] ? 1.0 : 0.0;
+}
+/// V[j+1] = w / h(j+1) unless happy (krylov.hpp:106)
+__global__ void k_gm_newv(GmDev G, const double* __restrict__ w, int64_t n) {
+  if (G.st[kGmHappy] != 0.0) return;
+  const int j = int(G.st[kGmJ]);
+  const double h = G.H[int64_t(j) * G.ldh + j + 1];
+  double* v = G.V + int64_t(j + 1) * G.ldv;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x)
+    v[t] = w[t] / h;
+}
+/// previous rotations on column j, the new rotation, g, the stop test
+/// (krylov.hpp:107-124)
+__global__ void k_gm_givens(double* sc, GmDev G, cudaGraphConditionalHandle h_inner) {
+  const int j = int(G.st[kGmJ]);
+  double* h = G.H + int64_t(j) * G.ldh;
+  for (int i = 0; i < j; ++i) {
+    const double t = G.cs[i] * h[i] + G.sn[i] * h[i + 1];
+    h[i + 1] = -G.sn[i] * h[i] + G.cs[i] * h[i + 1];
+    h[i] = t;
+  }
+  const double rho = hypot(h[j], h[j + 1]);
+  G.cs[j] = h[j] / rho;
+  G.sn[j] = h[j + 1] / rho;
+  h[j] = rho;
+  h[j + 1] = 0.0;
+  G.g[j + 1] = -G.sn[j] * G.g[j];
+  G.g[j] *= G.cs[j];
+  sc[kScIt] += 1.0;
+  G.st[kGmM] = double(j + 1);
+  const bool happy = G.st[kGmHappy] != 0.0;
+  const double gn = fabs(G.g[j + 1]);
+  const bool exit = gn <= sc[kScTarget] || happy;
+  if (exit) G.st[kGmStalled] = (happy && gn > sc[kScTarget]) ? 1.0 : 0.0;
+  const bool more = !exit && sc[kScIt] < sc[kScMaxIt] && double(j + 1) < G.st[kGmCap];
+  if (more) G.st[kGmJ] = double(j + 1);
+  cudaGraphSetConditional(h_inner, more ? 1u : 0u);
+}
+/// back substitution H y = g over the m columns (krylov.hpp:126-131)
+__global__ void k_gm_solve(GmDev G) {
+  const int m = int(G.st[kGmM]);
+  for (int i = m - 1; i >= 0; --i) {
+    double s = G.g[i];
+    for (int l = i + 1; l < m; ++l) s -= G.H[int64_t(l) * G.ldh + i] * G.y[l];
+    G.y[i] = s / G.H[int64_t(i) * G.ldh + i];
+  }
+}
+/// u = sum_i y(i) V[i] (krylov.hpp:132-133), in ascending i per entry
+__global__ void k_gm_combine(GmDev G, double* __restrict__ u, int64_t n) {
+  const int m = int(G.st[kGmM]);
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    double a = 0.0;
+    for (int i = 0; i < m; ++i) a += G.y[i] * G.V[int64_t(i) * G.ldv + t];
+    u[t] = a;
+  }
+}
+/// after x += M u and r.r: the cycle's exit (krylov.hpp:134-143)
+__global__ void k_gm_end(double* sc, GmDev G) {
+  if (sqrt(sc[kScRR]) <= sc[kScTarget]) sc[kScStatus] = kLoopConverged;
+  else if (G.st[kGmStalled] != 0.0 || sc[kScIt] >= sc[kScMaxIt]) sc[kScStatus] = kLoopMaxIt;
+}
+
 __global__ void k_pcg_direction(double* __restrict__ p, const double* __restrict__ z, int64_t n, const double* sc,
                                 int i_new, int i_old) {
   const double beta = sc[i_new] / sc[i_old];
@@ -1450,6 +1756,112 @@ void dot(const double* a, const double* b, int64_t n, const Reduce& red, double*
 void pcg_update(double* x, double* r, const double* p, const double* Ap, int64_t n, double* sc, int i_num, int i_den,
                 const Reduce& red, int i_rr, cudaStream_t s) {
   k_pcg_update<<<kRedBlocks, 256, 0, s>>>(x, r, p, Ap, n, sc, i_num, i_den, red, i_rr);
+  HPMG_LAUNCH_CHECK();
+}
+void gm_init(double* sc, const GmDev& G, double target, double max_it, int cap, cudaStream_t s) {
+  k_gm_init<<<1, 1, 0, s>>>(sc, G, target, max_it, double(cap));
+  HPMG_LAUNCH_CHECK();
+}
+void gm_start(double* sc, const GmDev& G, cudaGraphConditionalHandle h_cyc, cudaGraphConditionalHandle h_inner,
+              cudaStream_t s) {
+  k_gm_start<<<1, 1, 0, s>>>(sc, G, h_cyc, h_inner);
+  HPMG_LAUNCH_CHECK();
+}
+void gm_v0(const GmDev& G, const double* r, int64_t n, cudaStream_t s) {
+  k_gm_v0<<<grid_for(n, 256), 256, 0, s>>>(G, r, n);
+  HPMG_LAUNCH_CHECK();
+}
+void gm_copy(const GmDev& G, double* dst, int64_t n, cudaGraphConditionalHandle h_mgs, cudaStream_t s) {
+  k_gm_copy<<<grid_for(n, 256), 256, 0, s>>>(G, dst, n, h_mgs);
+  HPMG_LAUNCH_CHECK();
+}
+void mgs_step(const GmDev& G, double* w, int64_t n, const Reduce& red, cudaGraphConditionalHandle h_mgs,
+              cudaStream_t s) {
+  k_mgs<<<kRedBlocks, 256, 0, s>>>(G, w, n, red, h_mgs);
+  HPMG_LAUNCH_CHECK();
+}
+namespace {
+template <int E>
+bool launch_mgs_coop(const GmDev& G, const double* w, int64_t n, double* part, unsigned* bar, int grid,
+                     cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_mgs_coop<E>, G, w, n, part, bar) == cudaSuccess;
+}
+}  // namespace
+
+int mgs_coop_grid() {
+  static int grid = -1;
+  if (grid < 0) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_mgs_coop<32>, 256, 0);
+    grid = per >= 2 ? 2 * sms : (per >= 1 ? sms : 0);
+  }
+  return grid;
+}
+bool mgs_coop(const GmDev& G, const double* w, int64_t n, double* part, unsigned* bar, cudaStream_t s) {
+  const int grid = mgs_coop_grid();
+  if (grid == 0) return false;
+  const int64_t per_thread = ((n + grid - 1) / grid + 255) / 256;
+  if (per_thread <= 8) return launch_mgs_coop<8>(G, w, n, part, bar, grid, s);
+  if (per_thread <= 16) return launch_mgs_coop<16>(G, w, n, part, bar, grid, s);
+  if (per_thread <= 32) return launch_mgs_coop<32>(G, w, n, part, bar, grid, s);
+  return false;
+}
+void mgs_tail(const GmDev& G, double* w, int64_t n, const Reduce& red, cudaStream_t s) {
+  k_mgs_tail<<<kRedBlocks, 256, 0, s>>>(G, w, n, red);
+  HPMG_LAUNCH_CHECK();
+}
+void gm_arnoldi_close(double* sc, const GmDev& G, const double* w, int64_t n, cudaGraphConditionalHandle h_inner,
+                      cudaStream_t s) {
+  k_gm_hnorm<<<1, 1, 0, s>>>(G);
+  HPMG_LAUNCH_CHECK();
+  k_gm_newv<<<grid_for(n, 256), 256, 0, s>>>(G, w, n);
+  HPMG_LAUNCH_CHECK();
+  k_gm_givens<<<1, 1, 0, s>>>(sc, G, h_inner);
+  HPMG_LAUNCH_CHECK();
+}
+void gm_givens(double* sc, const GmDev& G, cudaGraphConditionalHandle h_inner, cudaStream_t s) {
+  k_gm_givens<<<1, 1, 0, s>>>(sc, G, h_inner);
+  HPMG_LAUNCH_CHECK();
+}
+void gm_update(const GmDev& G, double* u, int64_t n, cudaStream_t s) {
+  k_gm_solve<<<1, 1, 0, s>>>(G);
+  HPMG_LAUNCH_CHECK();
+  k_gm_combine<<<grid_for(n, 256), 256, 0, s>>>(G, u, n);
+  HPMG_LAUNCH_CHECK();
+}
+void gm_end(double* sc, const GmDev& G, cudaStream_t s) {
+  k_gm_end<<<1, 1, 0, s>>>(sc, G);
+  HPMG_LAUNCH_CHECK();
+}
+void pcg_loop_check(double* sc, cudaGraphConditionalHandle h_more, cudaStream_t s) {
+  k_pcg_loop_check<<<1, 1, 0, s>>>(sc, h_more);
+  HPMG_LAUNCH_CHECK();
+}
+void pcg_loop_beta(double* sc, cudaStream_t s) {
+  k_pcg_loop_beta<<<1, 1, 0, s>>>(sc);
+  HPMG_LAUNCH_CHECK();
+}
+void pcg_loop_direction(double* p, const double* z, int64_t n, const double* sc, cudaStream_t s) {
+  k_pcg_loop_direction<<<grid_for(n, 256), 256, 0, s>>>(p, z, n, sc);
+  HPMG_LAUNCH_CHECK();
+}
+void loop_continue(const double* sc, cudaGraphConditionalHandle h_loop, cudaStream_t s) {
+  k_loop_continue<<<1, 1, 0, s>>>(sc, h_loop);
+  HPMG_LAUNCH_CHECK();
+}
+void pcg_loop_init(double* sc, double target, double max_it, cudaStream_t s) {
+  k_pcg_loop_init<<<1, 1, 0, s>>>(sc, target, max_it);
   HPMG_LAUNCH_CHECK();
 }
 void pcg_direction(double* p, const double* z, int64_t n, double* sc, int i_new, int i_old, cudaStream_t s) {

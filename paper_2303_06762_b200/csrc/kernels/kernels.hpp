@@ -185,6 +185,49 @@ void pcg_update(double* x, double* r, const double* p, const double* Ap, int64_t
                 const Reduce& red, int i_rr, cudaStream_t s);
 /// p = z + (sc[i_new]/sc[i_old]) p ; then sc[i_old] = sc[i_new]
 void pcg_direction(double* p, const double* z, int64_t n, double* sc, int i_new, int i_old, cudaStream_t s);
+
+/// Device-resident Krylov loops: scalar slots of the context's sc[] array
+/// (shared with context.cu) and loop states.
+enum : int {
+  kScRZ = 0, kScRZn = 1, kScPAp = 2, kScRR = 3, kScBB = 4,
+  kScIt = 9, kScStatus = 10, kScTarget = 11, kScMaxIt = 12, kScBeta = 13
+};
+constexpr double kLoopRunning = 0.0, kLoopConverged = 1.0, kLoopNaPAp = 2.0, kLoopNaRZ = 3.0, kLoopMaxIt = 4.0,
+                 kLoopLast = 5.0;
+void pcg_loop_init(double* sc, double target, double max_it, cudaStream_t s);
+void pcg_loop_check(double* sc, cudaGraphConditionalHandle h_more, cudaStream_t s);
+void pcg_loop_beta(double* sc, cudaStream_t s);
+void pcg_loop_direction(double* p, const double* z, int64_t n, const double* sc, cudaStream_t s);
+void loop_continue(const double* sc, cudaGraphConditionalHandle h_loop, cudaStream_t s);
+
+/// Device GMRES state: basis slab V[(cap+1)][ldv], Hessenberg columns
+/// H[cap][ldh = cap+1], rotations, g, y, and scalar state st[].
+struct GmDev {
+  double* V = nullptr;
+  int64_t ldv = 0;
+  double* H = nullptr;
+  int ldh = 0;
+  double *cs = nullptr, *sn = nullptr, *g = nullptr, *y = nullptr, *st = nullptr;
+};
+enum : int { kGmBeta = 0, kGmJ = 1, kGmI = 2, kGmHappy = 3, kGmStalled = 4, kGmHn = 5, kGmCap = 6, kGmM = 7 };
+void gm_init(double* sc, const GmDev& G, double target, double max_it, int cap, cudaStream_t s);
+void gm_start(double* sc, const GmDev& G, cudaGraphConditionalHandle h_cyc, cudaGraphConditionalHandle h_inner,
+              cudaStream_t s);
+void gm_v0(const GmDev& G, const double* r, int64_t n, cudaStream_t s);
+void gm_copy(const GmDev& G, double* dst, int64_t n, cudaGraphConditionalHandle h_mgs, cudaStream_t s);
+void mgs_step(const GmDev& G, double* w, int64_t n, const Reduce& red, cudaGraphConditionalHandle h_mgs,
+              cudaStream_t s);
+void mgs_tail(const GmDev& G, double* w, int64_t n, const Reduce& red, cudaStream_t s);
+/// All of Arnoldi column j's MGS, h(j+1), the happy flag and V[j+1] in one
+/// cooperative launch; part [2 * grid] doubles, bar [1] zeroed. False when
+/// the vector is too long for the register slices or co-residency fails.
+int mgs_coop_grid();
+bool mgs_coop(const GmDev& G, const double* w, int64_t n, double* part, unsigned* bar, cudaStream_t s);
+void gm_arnoldi_close(double* sc, const GmDev& G, const double* w, int64_t n, cudaGraphConditionalHandle h_inner,
+                      cudaStream_t s);
+void gm_givens(double* sc, const GmDev& G, cudaGraphConditionalHandle h_inner, cudaStream_t s);
+void gm_update(const GmDev& G, double* u, int64_t n, cudaStream_t s);
+void gm_end(double* sc, const GmDev& G, cudaStream_t s);
 /// y = a * x + b * y with device scalars sc[ia] (or 1 if ia < 0), factor fa
 void scal_axpby(double* y, const double* x, int64_t n, const double* sc, int ia, double fa, double fb, cudaStream_t s);
 
