@@ -201,6 +201,14 @@ int hpmg_write_matrix_market(hpmg_ctx* ctx, int level, const char* path);
 /* ---- operators ---- */
 int hpmg_spmv(hpmg_ctx* ctx, const double* x, double* y, int flags);
 int hpmg_apply(hpmg_ctx* ctx, const double* r, double* z, int flags);
+/* apply() with the reference's optional residual trace (MGOptions::trace /
+ * MGTraceEntry, multigrid.hpp:18-33,120,126,168-183): for every level visit,
+ * (level, entering = 1, |b|) on entry and (level, 0, |b - A x|) on exit, in
+ * the reference's order; the order-k head is level L+1. Writes up to `cap`
+ * entries and the total count. A debugging path: the cycle runs outside the
+ * CUDA graph with a host read per norm. Same z as hpmg_apply. */
+int hpmg_apply_trace(hpmg_ctx* ctx, const double* r, double* z, int flags, int cap, int* level, int* entering,
+                     double* residual, int* count);
 /* z[i] = apply(r[i]) for m independent host vectors (reference order; pinned
  * memory for overlap): copy-in of vector i+1 and copy-out of result i-1 run on
  * two copy streams while V-cycle i runs, so PCIe transfers hide behind the

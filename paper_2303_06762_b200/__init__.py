@@ -128,6 +128,8 @@ def lib():
     L.hpmg_recover.argtypes = [vp, vp, vp, vp, vp]
     L.hpmg_postprocess.argtypes = [vp, dp, dp, dp, dp]
     L.hpmg_apply_batch.argtypes = [vp, C.c_int, C.POINTER(vp), C.POINTER(vp)]
+    L.hpmg_apply_trace.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                   C.POINTER(C.c_double), C.POINTER(C.c_int)]
     L.hpmg_time_spmv.restype = C.c_double
     L.hpmg_time_spmv.argtypes = [vp, C.c_int, dp]
     L.hpmg_write_matrix_market.argtypes = [vp, C.c_int, C.c_char_p]
@@ -459,6 +461,20 @@ class MGPreconditioner:
         z = np.empty(self.n)
         self._check(lib().hpmg_apply(self.h, b.ctypes.data, z.ctypes.data, 0))
         return z
+
+    def apply_trace(self, b, cap=4096):
+        """apply(b) with the MG residual trace (reference MGOptions::trace):
+        returns (z, levels, entering flags, residual norms)."""
+        b = self._vec(b, "b")
+        z = np.empty(self.n)
+        lv = (C.c_int * cap)()
+        en = (C.c_int * cap)()
+        res = np.zeros(cap)
+        cnt = C.c_int(0)
+        self._check(lib().hpmg_apply_trace(self.h, b.ctypes.data, z.ctypes.data, 0, cap, lv, en, _dp(res),
+                                            C.byref(cnt)))
+        n = min(cnt.value, cap)
+        return z, list(lv)[:n], list(en)[:n], res[:n]
 
     def apply_batch(self, rs, zs=None):
         """apply() over independent host vectors with the PCIe copies of

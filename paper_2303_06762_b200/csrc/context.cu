@@ -170,6 +170,13 @@ struct hpmg_ctx {
   double setup_parts[8] = {0};
   // CUDA graph of apply(kr -> kz)
   cudaGraphExec_t apply_graph = nullptr;
+  // MG residual trace (MGOptions::trace, reference multigrid.hpp:18-33): set
+  // only during hpmg_apply_trace, which runs the cycle outside the graph
+  struct TraceEntry {
+    int level, entering;
+    double residual;
+  };
+  std::vector<TraceEntry>* trace = nullptr;
   // device-resident PCG iteration: one graph with a while node (built lazily)
   cudaGraphExec_t pcg_loop = nullptr;
   bool pcg_loop_failed = false;
@@ -600,11 +607,28 @@ void smooth(hpmg_ctx& C, Level& V, double* x, const double* b, bool post) {
   count(C);
 }
 
+void read_scalars(hpmg_ctx& C, int n = 16);
+
+/// Trace entries: |b| on entering a level, |b - A x| on leaving it (the
+/// reference's MGTraceEntry, multigrid.hpp:120,126,168-183). Synchronous;
+/// only hpmg_apply_trace sets C.trace.
+void trace_norm(hpmg_ctx& C, int level, bool entering, const double* v, int64_t n) {
+  dev::dot(v, v, n, C.red, C.sc + S_TMP, C.s);
+  read_scalars(C, 16);
+  C.trace->push_back({level, entering ? 1 : 0, std::sqrt(C.sc_host[S_TMP])});
+}
+void trace_residual(hpmg_ctx& C, int level, const Level& V, const double* b, const double* x, double* scratch) {
+  dev::spmv(V.A, x, b, scratch, 1, nullptr, nullptr, C.s);
+  trace_norm(C, level, false, scratch, V.n);
+}
+
 /// h_cycle(l, b) -> x (reference inc/multigrid.hpp:166-185)
 void h_cycle(hpmg_ctx& C, int l, const double* b, double* x) {
+  if (C.trace) trace_norm(C, l, true, b, C.lv[l]->n);
   if (l == 0) {
     dev::dense_gemv(C.n0, C.coarse_inv, b, x, C.gemv_work, C.s);
     count(C);
+    if (C.trace) trace_residual(C, 0, *C.lv[0], b, x, C.lv[0]->y);  // y: no smoother on level 0; bw may be b (W-cycle)
     return;
   }
   Level& V = *C.lv[l];
@@ -617,6 +641,7 @@ void h_cycle(hpmg_ctx& C, int l, const double* b, double* x) {
     h_cycle(C, l - 1, W.b, W.x);
     dev::small_post(V.A, V.srec, V.d_passes, V.npass, V.steps, V.Pm, W.x, b, x, C.s);
     count(C, 2);
+    if (C.trace) trace_residual(C, l, V, b, x, V.r);
     return;
   }
   // x = 0 was written by the kernel that produced b (restriction / E^T injection)
@@ -639,6 +664,7 @@ void h_cycle(hpmg_ctx& C, int l, const double* b, double* x) {
   dev::prolong_add(V.Pm, W.x, x, C.s);
   count(C);
   smooth(C, V, x, b, true);
+  if (C.trace) trace_residual(C, l, V, b, x, V.r);
 }
 
 /// apply(b) -> x on the finest system, block layout (inc/multigrid.hpp:117-128)
@@ -654,6 +680,7 @@ void apply_blocks(hpmg_ctx& C, const double* b, double* x) {
   }
   Level& H = *C.head;
   Level& F = *C.lv[C.L];
+  if (C.trace) trace_norm(C, C.L + 1, true, b, H.n);  // the head is reported one index above the finest mesh level
   dev::fill(x, 0.0, H.n, C.s);
   count(C);
   smooth(C, H, x, b, false);
@@ -663,6 +690,7 @@ void apply_blocks(hpmg_ctx& C, const double* b, double* x) {
   dev::embed_add(H.nb, H.bs, F.x, x, C.s);
   count(C);
   smooth(C, H, x, b, true);
+  if (C.trace) trace_residual(C, C.L + 1, H, b, x, C.ktmp);
 }
 
 void build_apply_graph(hpmg_ctx& C) {
@@ -679,7 +707,7 @@ void build_apply_graph(hpmg_ctx& C) {
 
 void apply_graph(hpmg_ctx& C) { CK(cudaGraphLaunch(C.apply_graph, C.s)); }
 
-void read_scalars(hpmg_ctx& C, int n = 16) {
+void read_scalars(hpmg_ctx& C, int n) {
   CK(cudaMemcpyAsync(C.sc_host, C.sc, sizeof(double) * n, cudaMemcpyDeviceToHost, C.s));
   CK(cudaStreamSynchronize(C.s));
 }
@@ -1677,6 +1705,32 @@ int hpmg_apply(hpmg_ctx* ctx, const double* r, double* z, int flags) {
     in_vec(*ctx, r, ctx->kr, flags);
     apply_graph(*ctx);
     out_vec(*ctx, ctx->kz, z, flags);
+  });
+}
+
+int hpmg_apply_trace(hpmg_ctx* ctx, const double* r, double* z, int flags, int cap, int* level, int* entering,
+                     double* residual, int* count_out) {
+  return guarded(ctx, [&] {
+    if (cap < 0 || (cap > 0 && (!level || !entering || !residual))) throw std::invalid_argument("apply_trace: bad buffers");
+    hpmg_ctx& C = *ctx;
+    std::vector<hpmg_ctx::TraceEntry> tr;
+    in_vec(C, r, C.kr, flags);
+    C.trace = &tr;
+    try {
+      apply_blocks(C, C.kr, C.kz);  // the cycle outside the graph, with the norms of every level
+    } catch (...) {
+      C.trace = nullptr;
+      throw;
+    }
+    C.trace = nullptr;
+    out_vec(C, C.kz, z, flags);
+    CK(cudaStreamSynchronize(C.s));
+    for (int i = 0; i < int(tr.size()) && i < cap; ++i) {
+      level[i] = tr[i].level;
+      entering[i] = tr[i].entering;
+      residual[i] = tr[i].residual;
+    }
+    if (count_out) *count_out = int(tr.size());
   });
 }
 

@@ -253,3 +253,24 @@ def test_recover_locals_random_skeleton(k):
     if nb == 1:
         assert np.abs(io[:, 0]).max() > 1e-3 * scale
         assert rel(np.abs(ig[:, 0]), np.abs(io[:, 0])) < 1e-10
+
+
+@pytest.mark.parametrize("k,cycle", [(0, O.CYCLE_V), (2, O.CYCLE_V), (1, O.CYCLE_W), (3, O.CYCLE_VARV)])
+def test_mg_residual_trace(k, cycle):
+    # MGOptions::trace (reference multigrid.hpp:18-33,120,126,168-183) through
+    # hpmg_apply_trace, against the reference's own trace on the same input
+    if not O.ref_available():
+        pytest.skip("reference library not built")
+    n_f = 2 << 2
+    F = O.seeded_load(n_f, 1)
+    ref = O.OracleMG(reference=True, traced=True, base_n=2, levels=3, k=k, beta=1.0, inv_eps=1e3,
+                     load_kind=O.LOAD_ARRAY, load=F, cycle=cycle)
+    gpu = H.MGPreconditioner(base_n=2, levels=3, k=k, beta=1.0, inv_eps=1e3, structured_load=(n_f, F), cycle=cycle)
+    b = O.random_vec(ref.n, 3)
+    zr = ref.apply(b)
+    lr, er, rr = ref.trace()
+    zg, lg, eg, rg = gpu.apply_trace(b)
+    assert lg == lr and eg == er
+    assert np.allclose(rg, rr, rtol=1e-10, atol=1e-12 * np.linalg.norm(b))
+    assert rel(zg, zr) < apply_tol()
+    assert np.array_equal(zg, gpu.apply(b))  # the traced cycle is the graph's cycle
