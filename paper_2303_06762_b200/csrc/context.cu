@@ -540,7 +540,10 @@ void count(hpmg_ctx& C, int n = 1) {
   if (C.counting) C.launches_per_apply += n;
 }
 
-void smooth(hpmg_ctx& C, Level& V, double* x, const double* b, bool post) {
+/// x_zero: x = 0 on entry (pre-smoothing inside the cycle): the first wave
+/// of the first sweep sees x_e = 0 (and the transposed post sweep's first
+/// wave y_e = 0), which gs_wave_rec exploits bitwise-exactly.
+void smooth(hpmg_ctx& C, Level& V, double* x, const double* b, bool post, bool x_zero = false) {
   const int nw = int(V.wave_ptr.size()) - 1;
   if (C.opt.smoother == HPMG_SMOOTH_ADDITIVE) {
     for (int s = 0; s < V.steps; ++s) {
@@ -568,7 +571,7 @@ void smooth(hpmg_ctx& C, Level& V, double* x, const double* b, bool post) {
     for (int s = 0; s < V.steps; ++s)
       for (int w = 0; w < nw; ++w) {
         if (V.rec.rec) {
-          dev::gs_wave_rec(V.rec, V.wave_ptr[w], V.wave_ptr[w + 1], b, x, C.s);
+          dev::gs_wave_rec(V.rec, V.wave_ptr[w], V.wave_ptr[w + 1], b, x, C.s, x_zero && s == 0 && w == 0);
         } else {
           next_inv(w + 1 < nw ? w + 1 : (s + 1 < V.steps ? 0 : -1), &pf, &pl);
           dev::gs_wave(V.A, V.P, V.wave_ptr[w], V.wave_ptr[w + 1], b, x, 0, V.max_nf, C.s, pf, pl);
@@ -598,7 +601,7 @@ void smooth(hpmg_ctx& C, Level& V, double* x, const double* b, bool post) {
   for (int s = 0; s < V.steps; ++s)
     for (int w = nw - 1; w >= 0; --w) {
       if (V.rect.rec)
-        dev::gs_wave_rec(V.rect, V.wave_ptr[w], V.wave_ptr[w + 1], V.r, V.y, C.s);
+        dev::gs_wave_rec(V.rect, V.wave_ptr[w], V.wave_ptr[w + 1], V.r, V.y, C.s, s == 0 && w == nw - 1);
       else
         dev::gs_wave(V.AT, V.P, V.wave_ptr[w], V.wave_ptr[w + 1], V.r, V.y, 1, V.max_nf, C.s);
       count(C);
@@ -645,7 +648,7 @@ void h_cycle(hpmg_ctx& C, int l, const double* b, double* x) {
     return;
   }
   // x = 0 was written by the kernel that produced b (restriction / E^T injection)
-  smooth(C, V, x, b, false);
+  smooth(C, V, x, b, false, true);
   dev::spmv(V.A, x, b, V.r, 1, nullptr, nullptr, C.s);
   dev::restrict_(V.PT, V.r, W.b, C.s, l - 1 > 0 ? W.x : nullptr);
   count(C, 2);
@@ -683,7 +686,7 @@ void apply_blocks(hpmg_ctx& C, const double* b, double* x) {
   if (C.trace) trace_norm(C, C.L + 1, true, b, H.n);  // the head is reported one index above the finest mesh level
   dev::fill(x, 0.0, H.n, C.s);
   count(C);
-  smooth(C, H, x, b, false);
+  smooth(C, H, x, b, false, true);
   dev::inject_residual(H.A, x, b, F.b, C.s, F.x);
   count(C);
   h_cycle(C, C.L, F.b, F.x);

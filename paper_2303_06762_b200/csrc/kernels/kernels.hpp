@@ -98,7 +98,9 @@ PatchRecords record_layout(int bs, int max_nf, bool full = false);
 /// transpose: records of the transposed sweep (A = A^T rows, S_p^T; full layout only)
 void build_records(const Bsr& A, const Patches& P, PatchRecords& R, cudaStream_t s, bool transpose = false);
 /// One symmetric wave over the patch records [w0, w1) (one TMA per CTA).
-void gs_wave_rec(const PatchRecords& R, int w0, int w1, const double* b, double* x, cudaStream_t s);
+/// x_zero: every x_e of the wave is zero (first wave of a sweep from x = 0).
+void gs_wave_rec(const PatchRecords& R, int w0, int w1, const double* b, double* x, cudaStream_t s,
+                 bool x_zero = false);
 void sweep_trace(long long* out);  // development timeline, 5 x 32768 stamps
 /// Additive sweep pieces: d_p = Inv_p r_p for all patches; x += damping * sum_p d_p.
 void jacobi_patch(const Bsr& A, const Patches& P, const double* r, double* d, int max_nf, cudaStream_t s);

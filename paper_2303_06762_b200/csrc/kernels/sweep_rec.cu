@@ -80,9 +80,12 @@ __device__ __forceinline__ void sweep_stamp(const PatchRecords& R, int k) {
 }
 
 /// Records of G consecutive patches per CTA, TP threads per patch: one wave [p0, p1).
+/// xz: the wave's x_e is known to be zero (first wave of a sweep started from
+/// x = 0): r_p = b_p exactly, so A_pe is neither copied nor applied and x_e is
+/// not gathered (bitwise the same result).
 template <int BS, int TP, int G>
 __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1, const double* __restrict__ b,
-                                                 double* __restrict__ x) {
+                                                 double* __restrict__ x, int xz) {
   constexpr int kRow = kExt * BS * BS;
   constexpr bool kOneCopy = G > 1;  // grouped small records: one copy per CTA
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -111,14 +114,15 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
       const unsigned mbytes = unsigned(R.stride - R.meta_off) * 8u, abytes = unsigned(R.meta_off - R.a_off) * 8u,
                      head = unsigned(R.a_off) * 8u;
       bar_expect(&bar_m, unsigned(ng) * mbytes);
-      bar_expect(&bar, unsigned(ng) * abytes);
+      if (!xz) bar_expect(&bar, unsigned(ng) * abytes);
       bar_expect(&bar_s, unsigned(ng) * head);
       for (int q = 0; q < ng; ++q)
         tma_part(srec + size_t(q) * R.stride + R.meta_off, R.rec + size_t(q0 + q) * R.stride + R.meta_off, mbytes,
                  &bar_m, pol);
-      for (int q = 0; q < ng; ++q)
-        tma_part(srec + size_t(q) * R.stride + R.a_off, R.rec + size_t(q0 + q) * R.stride + R.a_off, abytes, &bar,
-                 pol);
+      if (!xz)
+        for (int q = 0; q < ng; ++q)
+          tma_part(srec + size_t(q) * R.stride + R.a_off, R.rec + size_t(q0 + q) * R.stride + R.a_off, abytes, &bar,
+                   pol);
       for (int q = 0; q < ng; ++q)
         tma_part(srec + size_t(q) * R.stride, R.rec + size_t(q0 + q) * R.stride, head, &bar_s, pol);
     }
@@ -144,7 +148,7 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
   // b_p is issued together with the x_e gather (both L2 round trips)
   double bv = 0.0;
   if (row < np && part == 0) bv = __ldg(b + size_t(fac[row / BS]) * BS + row % BS);
-  {
+  if (!xz) {
     // all loads of this thread in flight at once, then the shared stores
     constexpr int kPer = (kMaxPatchF * kExt * BS + TP - 1) / TP;
     const int ne = nf * kExt * BS;
@@ -159,11 +163,13 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
     for (int u = 0; u < kPer; ++u)
       if (t + u * TP < ne) xs[t + u * TP] = v[u];
   }
-  if (!kOneCopy) bar_wait(&bar);
+  if (!kOneCopy && !xz) bar_wait(&bar);
   __syncthreads();
   sweep_stamp(R, 2);
   double rsum = 0.0;
-  if (row < np) {
+  if (row < np && xz) {
+    rsum = bv;  // x_e = 0: the residual rows are b_p
+  } else if (row < np) {
     const int lf = row / BS, i = row % BS;
     // external blocks are stored column-major: A(i, j) at j*BS + i, so the
     // rows of a block are consecutive words; the column order is rotated by
@@ -341,7 +347,7 @@ struct Grp {
 };
 
 template <int BS>
-void launch(const PatchRecords& R, int p0, int p1, int nblocks, const double* b, double* x, cudaStream_t s) {
+void launch(const PatchRecords& R, int p0, int p1, int nblocks, const double* b, double* x, int xz, cudaStream_t s) {
   constexpr int TP = RecCfg<BS>::TP, G = Grp<BS>::G;
   if (R.max_nf * BS * (TP >= 2 * kMaxPatchF * BS ? 2 : 1) > TP)
     throw std::runtime_error("vertex patch too large for the record sweep");
@@ -361,20 +367,21 @@ void launch(const PatchRecords& R, int p0, int p1, int nblocks, const double* b,
   attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr_pdl;
   cfg.numAttrs = 1;
-  cudaError_t err = cudaLaunchKernelEx(&cfg, k_sweep<BS, TP, G>, R, p0, p1, b, x);
+  cudaError_t err = cudaLaunchKernelEx(&cfg, k_sweep<BS, TP, G>, R, p0, p1, b, x, xz);
   if (err == cudaSuccess) err = cudaGetLastError();
   if (err != cudaSuccess) throw std::runtime_error(std::string("CUDA launch (sweep): ") + cudaGetErrorString(err));
 }
 
-void launch_bs(const PatchRecords& R, int p0, int p1, int nblocks, const double* b, double* x, cudaStream_t s) {
+void launch_bs(const PatchRecords& R, int p0, int p1, int nblocks, const double* b, double* x, int xz,
+               cudaStream_t s) {
   switch (R.bs) {
-    case 2: launch<2>(R, p0, p1, nblocks, b, x, s); break;
-    case 4: launch<4>(R, p0, p1, nblocks, b, x, s); break;
-    case 6: launch<6>(R, p0, p1, nblocks, b, x, s); break;
-    case 8: launch<8>(R, p0, p1, nblocks, b, x, s); break;
-    case 10: launch<10>(R, p0, p1, nblocks, b, x, s); break;
-    case 12: launch<12>(R, p0, p1, nblocks, b, x, s); break;
-    case 14: launch<14>(R, p0, p1, nblocks, b, x, s); break;
+    case 2: launch<2>(R, p0, p1, nblocks, b, x, xz, s); break;
+    case 4: launch<4>(R, p0, p1, nblocks, b, x, xz, s); break;
+    case 6: launch<6>(R, p0, p1, nblocks, b, x, xz, s); break;
+    case 8: launch<8>(R, p0, p1, nblocks, b, x, xz, s); break;
+    case 10: launch<10>(R, p0, p1, nblocks, b, x, xz, s); break;
+    case 12: launch<12>(R, p0, p1, nblocks, b, x, xz, s); break;
+    case 14: launch<14>(R, p0, p1, nblocks, b, x, xz, s); break;
     default: throw std::runtime_error("unsupported block size");
   }
 }
@@ -417,10 +424,10 @@ void build_records(const Bsr& A, const Patches& P, PatchRecords& R, cudaStream_t
 
 void sweep_trace(long long* out) { cudaMemcpyFromSymbol(out, d_sweep_trace, sizeof(long long) * 5 * 32768); }
 
-void gs_wave_rec(const PatchRecords& R, int w0, int w1, const double* b, double* x, cudaStream_t s) {
+void gs_wave_rec(const PatchRecords& R, int w0, int w1, const double* b, double* x, cudaStream_t s, bool x_zero) {
   if (w1 <= w0) return;
   const int G = group_of(R.bs);
-  launch_bs(R, w0, w1, (w1 - w0 + G - 1) / G, b, x, s);
+  launch_bs(R, w0, w1, (w1 - w0 + G - 1) / G, b, x, x_zero ? 1 : 0, s);
 }
 
 }  // namespace dev
