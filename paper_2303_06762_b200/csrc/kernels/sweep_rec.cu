@@ -79,63 +79,15 @@ __device__ __forceinline__ void sweep_stamp(const PatchRecords& R, int k) {
   }
 }
 
-/// Records of G consecutive patches per CTA, TP threads per patch: one wave [p0, p1).
-/// xz: the wave's x_e is known to be zero (first wave of a sweep started from
-/// x = 0): r_p = b_p exactly, so A_pe is neither copied nor applied and x_e is
-/// not gathered (bitwise the same result).
-template <int BS, int TP, int G>
-__global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1, const double* __restrict__ b,
-                                                 double* __restrict__ x, int xz) {
+/// One patch update x_p = S_p (b_p - A_pe x_e) from its record in shared
+/// memory (meta words landed): the x_e gather with b_p, the residual rows
+/// (waiting for A_pe through wait_a), the packed / full GEMV (waiting for
+/// S_p through wait_s), the store of x_p.
+template <int BS, int TP, bool kOneCopy, class WaitA, class WaitS>
+__device__ __forceinline__ void patch_update(const PatchRecords& R, const double* rec, int lp, int ng, int t,
+                                             double* sx, double* r, const double* __restrict__ b,
+                                             double* __restrict__ x, int xz, WaitA wait_a, WaitS wait_s) {
   constexpr int kRow = kExt * BS * BS;
-  constexpr bool kOneCopy = G > 1;  // grouped small records: one copy per CTA
-  extern __shared__ __align__(128) unsigned char smraw[];
-  double* srec = reinterpret_cast<double*>(smraw);  // G * stride
-  double* sx = srec + size_t(G) * R.stride;          // G * max_nf * kExt * BS
-  double* r = sx + G * R.max_nf * kExt * BS;         // G * TP
-  __shared__ unsigned long long bar, bar_s, bar_m;
-  const int lp = threadIdx.x / TP, t = threadIdx.x % TP;
-  const int q0 = p0 + blockIdx.x * G, ng = min(G, p1 - q0);
-  sweep_stamp(R, 0);
-  if (threadIdx.x == 0) {
-    // three copies per patch: the meta words first (the x_e gather needs only
-    // them), then A_pe (residual), then the inverse S_p, which lands while
-    // x_e is being gathered
-    bar_init(&bar);
-    bar_init(&bar_s);
-    bar_init(&bar_m);
-    unsigned long long pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    if (kOneCopy) {
-      // small records of consecutive patches: one bulk copy for the group
-      const unsigned all = unsigned(ng) * unsigned(R.stride) * 8u;
-      bar_expect(&bar_m, all);
-      tma_part(srec, R.rec + size_t(q0) * R.stride, all, &bar_m, pol);
-    } else {
-      const unsigned mbytes = unsigned(R.stride - R.meta_off) * 8u, abytes = unsigned(R.meta_off - R.a_off) * 8u,
-                     head = unsigned(R.a_off) * 8u;
-      bar_expect(&bar_m, unsigned(ng) * mbytes);
-      if (!xz) bar_expect(&bar, unsigned(ng) * abytes);
-      bar_expect(&bar_s, unsigned(ng) * head);
-      for (int q = 0; q < ng; ++q)
-        tma_part(srec + size_t(q) * R.stride + R.meta_off, R.rec + size_t(q0 + q) * R.stride + R.meta_off, mbytes,
-                 &bar_m, pol);
-      if (!xz)
-        for (int q = 0; q < ng; ++q)
-          tma_part(srec + size_t(q) * R.stride + R.a_off, R.rec + size_t(q0 + q) * R.stride + R.a_off, abytes, &bar,
-                   pol);
-      for (int q = 0; q < ng; ++q)
-        tma_part(srec + size_t(q) * R.stride, R.rec + size_t(q0 + q) * R.stride, head, &bar_s, pol);
-    }
-  }
-  // Programmatic dependent launch: the records do not depend on the previous
-  // kernel, so the copies above may overlap its tail; x and b may not be
-  // touched before it has completed.
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  __syncthreads();
-  bar_wait(&bar_m);
-  sweep_stamp(R, 1);
-  const double* rec = srec + size_t(lp) * R.stride;
   const int* meta = reinterpret_cast<const int*>(rec + R.meta_off);
   const int nf = lp < ng ? meta[0] : 0, np = nf * BS;
   const int* fac = meta + 1;
@@ -163,7 +115,7 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
     for (int u = 0; u < kPer; ++u)
       if (t + u * TP < ne) xs[t + u * TP] = v[u];
   }
-  if (!kOneCopy && !xz) bar_wait(&bar);
+  if (!kOneCopy && !xz) wait_a();
   __syncthreads();
   sweep_stamp(R, 2);
   double rsum = 0.0;
@@ -193,7 +145,7 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
   if (TR == 2) rsum += __shfl_xor_sync(0xffffffffu, rsum, 1);
   if (row < np && part == 0) r[lp * TP + row] = rsum;
   __syncthreads();
-  if (!kOneCopy) bar_wait(&bar_s);
+  if (!kOneCopy) wait_s();
   sweep_stamp(R, 3);
   double dsum = 0.0;
   if (row < np && R.full) {
@@ -248,6 +200,65 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
   }
   if (TR == 2) dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);
   if (row < np && part == 0) x[size_t(fac[row / BS]) * BS + row % BS] = dsum;
+}
+
+/// Records of G consecutive patches per CTA, TP threads per patch: one wave [p0, p1).
+/// xz: the wave's x_e is known to be zero (first wave of a sweep started from
+/// x = 0): r_p = b_p exactly, so A_pe is neither copied nor applied and x_e is
+/// not gathered (bitwise the same result).
+template <int BS, int TP, int G>
+__global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1, const double* __restrict__ b,
+                                                 double* __restrict__ x, int xz) {
+  constexpr bool kOneCopy = G > 1;  // grouped small records: one copy per CTA
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double* srec = reinterpret_cast<double*>(smraw);  // G * stride
+  double* sx = srec + size_t(G) * R.stride;          // G * max_nf * kExt * BS
+  double* r = sx + G * R.max_nf * kExt * BS;         // G * TP
+  __shared__ unsigned long long bar, bar_s, bar_m;
+  const int lp = threadIdx.x / TP, t = threadIdx.x % TP;
+  const int q0 = p0 + blockIdx.x * G, ng = min(G, p1 - q0);
+  sweep_stamp(R, 0);
+  if (threadIdx.x == 0) {
+    // three copies per patch: the meta words first (the x_e gather needs only
+    // them), then A_pe (residual), then the inverse S_p, which lands while
+    // x_e is being gathered
+    bar_init(&bar);
+    bar_init(&bar_s);
+    bar_init(&bar_m);
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    if (kOneCopy) {
+      // small records of consecutive patches: one bulk copy for the group
+      const unsigned all = unsigned(ng) * unsigned(R.stride) * 8u;
+      bar_expect(&bar_m, all);
+      tma_part(srec, R.rec + size_t(q0) * R.stride, all, &bar_m, pol);
+    } else {
+      const unsigned mbytes = unsigned(R.stride - R.meta_off) * 8u, abytes = unsigned(R.meta_off - R.a_off) * 8u,
+                     head = unsigned(R.a_off) * 8u;
+      bar_expect(&bar_m, unsigned(ng) * mbytes);
+      if (!xz) bar_expect(&bar, unsigned(ng) * abytes);
+      bar_expect(&bar_s, unsigned(ng) * head);
+      for (int q = 0; q < ng; ++q)
+        tma_part(srec + size_t(q) * R.stride + R.meta_off, R.rec + size_t(q0 + q) * R.stride + R.meta_off, mbytes,
+                 &bar_m, pol);
+      if (!xz)
+        for (int q = 0; q < ng; ++q)
+          tma_part(srec + size_t(q) * R.stride + R.a_off, R.rec + size_t(q0 + q) * R.stride + R.a_off, abytes, &bar,
+                   pol);
+      for (int q = 0; q < ng; ++q)
+        tma_part(srec + size_t(q) * R.stride, R.rec + size_t(q0 + q) * R.stride, head, &bar_s, pol);
+    }
+  }
+  // Programmatic dependent launch: the records do not depend on the previous
+  // kernel, so the copies above may overlap its tail; x and b may not be
+  // touched before it has completed.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  __syncthreads();
+  bar_wait(&bar_m);
+  sweep_stamp(R, 1);
+  patch_update<BS, TP, kOneCopy>(R, srec + size_t(lp) * R.stride, lp, ng, t, sx, r, b, x, xz,
+                                 [&] { bar_wait(&bar); }, [&] { bar_wait(&bar_s); });
   if (R.dbg & 4) {
     __syncthreads();
     sweep_stamp(R, 4);
