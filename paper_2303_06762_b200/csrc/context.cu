@@ -37,6 +37,8 @@ namespace {
 
 thread_local std::string g_last_error;
 
+inline void dfree(void* p);
+
 /// Owning device buffer for the temporaries of one C-ABI call (freed on every
 /// exit path, including a CUDA error thrown half-way).
 struct DevTemps {
@@ -45,7 +47,7 @@ struct DevTemps {
   DevTemps(const DevTemps&) = delete;
   DevTemps& operator=(const DevTemps&) = delete;
   ~DevTemps() {
-    for (void* p : ptrs) cudaFree(p);
+    for (void* p : ptrs) dfree(p);
   }
   template <typename T>
   T* add(T* p) {
@@ -54,11 +56,57 @@ struct DevTemps {
   }
 };
 
+/// development: time spent in device allocations / uploads (HPMG_SETUP_TRACE)
+inline double& g_alloc_s() {
+  static double t = 0;
+  return t;
+}
+inline double& g_upload_s() {
+  static double t = 0;
+  return t;
+}
+/// Device allocations come from a process-wide stream-ordered memory pool
+/// that keeps freed memory (release threshold = max): a context built after
+/// another one was destroyed (NS re-linearisation drivers, repeated setups)
+/// reuses the pages instead of paying cudaMalloc's page mapping again.
+cudaStream_t alloc_stream() {
+  static cudaStream_t q = [] {
+    cudaStream_t t;
+    CK(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
+    return t;
+  }();
+  return q;
+}
+cudaMemPool_t alloc_pool() {
+  static cudaMemPool_t mp = [] {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t m;
+    CK(cudaMemPoolCreate(&m, &props));
+    uint64_t thr = ~uint64_t(0);
+    CK(cudaMemPoolSetAttribute(m, cudaMemPoolAttrReleaseThreshold, &thr));
+    return m;
+  }();
+  return mp;
+}
+/// Frees a dalloc'ed buffer back to the pool once all device work is done.
+inline void dfree(void* p) {
+  if (!p) return;
+  cudaDeviceSynchronize();  // what cudaFree implied: no kernel may still use p
+  cudaFreeAsync(p, alloc_stream());
+}
 template <typename T>
 T* dalloc(size_t n) {
   void* p = nullptr;
   if (n == 0) n = 1;
-  CK(cudaMalloc(&p, n * sizeof(T)));
+  const auto t0 = std::chrono::steady_clock::now();
+  CK(cudaMallocFromPoolAsync(&p, n * sizeof(T), alloc_pool(), alloc_stream()));
+  CK(cudaStreamSynchronize(alloc_stream()));  // usable from any stream
+  g_alloc_s() += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   // HPMG_POISON=1: every allocation starts as NaN / -1 bytes (uninitialised-read check)
   static const bool poison = std::getenv("HPMG_POISON") != nullptr;
   if (poison) {
@@ -70,7 +118,9 @@ T* dalloc(size_t n) {
 template <typename T>
 T* dupload(const std::vector<T>& v, cudaStream_t s) {
   T* p = dalloc<T>(v.size());
+  const auto t0 = std::chrono::steady_clock::now();
   if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  g_upload_s() += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return p;
 }
 
@@ -275,7 +325,8 @@ struct SetupTrace {
   void mark(const char* what) {
     if (!on) return;
     const auto n = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[setup] %-28s %8.2f ms\n", what, std::chrono::duration<double>(n - t).count() * 1e3);
+    std::fprintf(stderr, "[setup] %-28s %8.2f ms   (allocs so far %.1f ms, uploads %.1f ms)\n", what,
+                 std::chrono::duration<double>(n - t).count() * 1e3, g_alloc_s() * 1e3, g_upload_s() * 1e3);
     t = n;
   }
 };
@@ -347,7 +398,7 @@ void linearise_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, const DevRef
   // condensed element blocks: one persistent scratch sized for the largest level
   const size_t need = size_t(m.ne()) * stride;
   if (C.acr_cap < need) {
-    if (C.acr) cudaFree(C.acr);
+    if (C.acr) dfree(C.acr);
     C.acr = dalloc<double>(need);
     C.acr_cap = need;
   }
@@ -422,15 +473,15 @@ void linearise_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, const DevRef
   CK(cudaStreamSynchronize(s));
   if (finest) {  // kept for recover_locals (same linearisation state)
     for (void* p : {(void*)C.fine_load, (void*)C.fine_wind, (void*)C.fine_mass})
-      if (p) cudaFree(p);
+      if (p) dfree(p);
     C.fine_wind = dwind;
     C.fine_mass = dmass;
     C.fine_load = dload;
     C.fine_lstride = lstride;
     C.fine_prm = prm;
   } else {
-    if (dwind) cudaFree(dwind);
-    if (dload) cudaFree(dload);
+    if (dwind) dfree(dwind);
+    if (dload) dfree(dload);
   }
 }
 
@@ -952,7 +1003,7 @@ void capture_body(hpmg_ctx& C, cudaGraph_t body, int depth, F fn) {
 void gm_workspace(hpmg_ctx& C, int cap) {
   if (cap <= C.gm_cap) return;
   for (void* p : {(void*)C.gm.V, (void*)C.gm.H, (void*)C.gm.cs, (void*)C.gm.sn, (void*)C.gm.g, (void*)C.gm.y})
-    if (p) cudaFree(p);
+    if (p) dfree(p);
   const int64_t n = C.top().n;
   C.gm.ldv = (n + 31) & ~int64_t(31);
   C.gm.ldh = cap + 1;
@@ -1553,8 +1604,8 @@ void hpmg_destroy(hpmg_ctx* ctx) {
     if (q) cudaStreamDestroy(q);
   for (void* p : {(void*)ctx->gm.V, (void*)ctx->gm.H, (void*)ctx->gm.cs, (void*)ctx->gm.sn, (void*)ctx->gm.g,
                   (void*)ctx->gm.y, (void*)ctx->gm.st, (void*)ctx->gm_part, (void*)ctx->gm_bar})
-    if (p) cudaFree(p);
-  auto fr = [](void* p) { if (p) cudaFree(p); };
+    if (p) dfree(p);
+  auto fr = [](void* p) { if (p) dfree(p); };
   auto free_level = [&](Level* V) {
     if (!V) return;
     for (void* p : {(void*)V->A.val, (void*)V->A.cols, (void*)V->AT.val, (void*)V->tslot, (void*)V->P.nf,
