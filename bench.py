@@ -148,13 +148,31 @@ def run_hpmg(args, rank, world, local, dist):
     cfg = CONFIGS[args.config]
     n_f = cfg["base_n"] << (cfg["levels"] - 1)
     F = H.seeded_load(n_f, args.seed)
-    tts_proc = start_cpu_tts(args) if (args.cpu_tts and rank == 0 and world == 1) else None
     t0 = time.perf_counter()
     B = H.MGPreconditioner(mesh="unit_square", base_n=cfg["base_n"], levels=cfg["levels"], k=cfg["k"],
                            nu=cfg["nu"], beta=cfg["beta"], inv_eps=cfg["inv_eps"], cycle=H.CYCLE_V,
                            smoother=H.SMOOTH_MULTIPLICATIVE, smooth_steps=1, structured_load=(n_f, F))
     setup_wall = time.perf_counter() - t0
     setup_dev, setup_parts = B.setup_seconds()
+    # time-to-solution first, on a second context (the first one in a process
+    # also pays the one-time CUDA module loading), before the CPU reference's
+    # TTS child starts loading the host
+    t0 = time.perf_counter()
+    B2 = H.MGPreconditioner(mesh="unit_square", base_n=cfg["base_n"], levels=cfg["levels"], k=cfg["k"],
+                            nu=cfg["nu"], beta=cfg["beta"], inv_eps=cfg["inv_eps"], cycle=H.CYCLE_V,
+                            smoother=H.SMOOTH_MULTIPLICATIVE, smooth_steps=1, structured_load=(n_f, F))
+    setup_warm = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    sol2 = H.uzawa_solve(B2)
+    solve_wall = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    B2.recover(sol2.velocity)  # recover_locals, as the CPU reference TTS includes it
+    recover_wall = time.perf_counter() - t0
+    B2_parts = B2.setup_seconds()
+    B2.close()
+    _, setup_parts_warm = B2_parts
+    tts_proc = start_cpu_tts(args) if (args.cpu_tts and rank == 0 and world == 1) else None
+
     n = B.n
     lib = H.lib()
     stream = torch.cuda.ExternalStream(B.stream())
@@ -253,18 +271,6 @@ def run_hpmg(args, rank, world, local, dist):
     # time-to-solution: device Uzawa (2 outer PCG solves to 1e-8); the setup is
     # timed again on a second context (the first one in a process also pays
     # the one-time CUDA module loading)
-    t0 = time.perf_counter()
-    B2 = H.MGPreconditioner(mesh="unit_square", base_n=cfg["base_n"], levels=cfg["levels"], k=cfg["k"],
-                            nu=cfg["nu"], beta=cfg["beta"], inv_eps=cfg["inv_eps"], cycle=H.CYCLE_V,
-                            smoother=H.SMOOTH_MULTIPLICATIVE, smooth_steps=1, structured_load=(n_f, F))
-    setup_warm = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    sol2 = H.uzawa_solve(B2)
-    solve_wall = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    B2.recover(sol2.velocity)  # recover_locals, as the CPU reference TTS includes it
-    recover_wall = time.perf_counter() - t0
-    B2.close()
     sol = H.uzawa_solve(B)
     launches = B.launches_per_apply()
     out = None
@@ -334,6 +340,9 @@ def run_hpmg(args, rank, world, local, dist):
                                 "recover_locals (interior, pressure modes, gradient back on the host); "
                                 "cpu_reference times the same three phases of the reference itself",
                     "setup_parts_s": [float(x) for x in setup_parts[:7]],
+                    "setup_parts_warm_s": [float(x) for x in setup_parts_warm[:7]],
+                    "setup_parts_note": "mesh+tables, plans+condensation, patch inverses, transfers, coarse "
+                                        "inverse, workspace+graph, total (first context / second context)",
                     "inner_iterations": sol.report.inner_iterations,
                     "final_divergence": sol.report.final_divergence, "converged": sol.report.converged},
             "clocks": clk.summary(),
