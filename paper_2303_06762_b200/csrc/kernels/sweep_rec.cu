@@ -143,6 +143,7 @@ __device__ __forceinline__ void patch_update(const PatchRecords& R, const double
     rsum = a0 + a1;
   }
   if (TR == 2) rsum += __shfl_xor_sync(0xffffffffu, rsum, 1);
+  if (r == sx) __syncthreads();  // r aliases the x_e staging (one patch per CTA)
   if (row < np && part == 0) r[lp * TP + row] = rsum;
   __syncthreads();
   if (!kOneCopy) wait_s();
@@ -213,7 +214,9 @@ __global__ void __launch_bounds__(G* TP) k_sweep(PatchRecords R, int p0, int p1,
   extern __shared__ __align__(128) unsigned char smraw[];
   double* srec = reinterpret_cast<double*>(smraw);  // G * stride
   double* sx = srec + size_t(G) * R.stride;          // G * max_nf * kExt * BS
-  double* r = sx + G * R.max_nf * kExt * BS;         // G * TP
+  // one patch per CTA: the residual rows live in the x_e staging area, dead
+  // once the residual is formed (patch_update orders the two with a barrier)
+  double* r = G == 1 ? sx : sx + G * R.max_nf * kExt * BS;  // G * TP
   __shared__ unsigned long long bar, bar_s, bar_m;
   const int lp = threadIdx.x / TP, t = threadIdx.x % TP;
   const int q0 = p0 + blockIdx.x * G, ng = min(G, p1 - q0);
@@ -362,7 +365,7 @@ void launch(const PatchRecords& R, int p0, int p1, int nblocks, const double* b,
   constexpr int TP = RecCfg<BS>::TP, G = Grp<BS>::G;
   if (R.max_nf * BS * (TP >= 2 * kMaxPatchF * BS ? 2 : 1) > TP)
     throw std::runtime_error("vertex patch too large for the record sweep");
-  const size_t smem = sizeof(double) * (size_t(G) * R.stride + size_t(G) * R.max_nf * kExt * BS + G * TP);
+  const size_t smem = sizeof(double) * (size_t(G) * R.stride + size_t(G) * R.max_nf * kExt * BS + (G == 1 ? 0 : G * TP));
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_sweep<BS, TP, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
