@@ -326,7 +326,7 @@ template <int BS>
 struct RecCfg;
 template <>
 struct RecCfg<2> {
-  static constexpr int TP = 16, G = 4;
+  static constexpr int TP = 16, G = 8;
 };
 template <>
 struct RecCfg<4> {
