@@ -6,8 +6,8 @@
 // whole pre- (resp. post-) smoothing phase of the V-cycle with x and b
 // resident in shared memory. The sweep is cut into passes (<= kPass patches
 // of one wave, host-built list). Warp-specialised: a producer warp streams the
-// patch records of pass k+1 by a TMA bulk copy (L2 evict-last, so they stay
-// L2-resident across V-cycles) into a 2-slot mbarrier ring while the kPass x 16
+// patch records of pass k+2 by a TMA bulk copy (L2 evict-last, so they stay
+// L2-resident across V-cycles) into a 3-slot mbarrier ring while the kPass x 16
 // consumer threads compute pass k: r = b_p - A_pe x_e from the staged external
 // blocks (sweep_rec.cu), then x_p = S r with the FULL patch inverse
 // (column-major in the record, so the GEMV reads are bank-conflict free). A wave costs two __syncthreads().
@@ -28,7 +28,7 @@ constexpr int kTP = 16;                      // threads (rows) per patch
 constexpr int kPass = 24;                    // patches per pass (level-1 waves are 16-17 wide)
 constexpr int kConsumers = kPass * kTP;      // 384
 constexpr int kThreads = kConsumers + 32;    // + one producer warp
-constexpr int kStages = 2;
+constexpr int kStages = 3;
 
 __device__ __forceinline__ unsigned su32(const void* p) { return unsigned(__cvta_generic_to_shared(p)); }
 
