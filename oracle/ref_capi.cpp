@@ -38,6 +38,23 @@ typedef struct {
   int iterations, converged, not_applicable;
   double residual;
 } orc_stats;
+
+typedef struct {
+  double picard_tol, newton_rel_tol, newton_abs_tol;
+  int max_picard, max_newton;
+  double pseudo_time_inv;
+  int outer_iterations;
+  double rel_tol, abs_tol;
+  int max_iterations;
+} orc_ns_opts;
+
+typedef struct {
+  int picard_iterations, newton_iterations, n_picard_inner, n_newton_inner;
+  int picard_inner[512], newton_inner[256];
+  double picard_diffs[128], newton_diffs[64];
+  int converged, not_applicable;
+  double final_divergence, seconds;
+} orc_ns_report;
 }
 
 namespace {
@@ -364,6 +381,59 @@ int orc_tts(const orc_problem* p, int outer, double rel_tol, int* inner, double*
     seconds[2] = std::chrono::duration<double>(t3 - t2).count();
     (void)loc;
     return int(s.report.inner_iterations.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+/// navier_stokes_solve (ns.hpp:69-149) of the reference itself, same surface
+/// as the restatement's orc_ns_solve (orc_capi.cpp).
+int orc_ns_solve(const orc_problem* p, const orc_ns_opts* o, double* velocity, double* interior, double* pressure,
+                 orc_ns_report* rep) {
+  try {
+    auto t0 = std::chrono::steady_clock::now();
+    MeshHierarchy hier =
+        MeshHierarchy::build(p->mesh_kind == 0 ? unit_square_mesh(p->base_n) : step_mesh(p->base_n), p->levels);
+    std::vector<double> loadcopy;
+    Field load = problem_load(p, loadcopy);
+    NSOptions no;
+    no.picard_tol = o->picard_tol;
+    no.newton_rel_tol = o->newton_rel_tol;
+    no.newton_abs_tol = o->newton_abs_tol;
+    no.max_picard = o->max_picard;
+    no.max_newton = o->max_newton;
+    no.pseudo_time_inv = o->pseudo_time_inv;
+    no.mg = mg_options(p);
+    no.uzawa.outer_iterations = o->outer_iterations;
+    no.uzawa.krylov.rel_tol = o->rel_tol;
+    no.uzawa.krylov.abs_tol = o->abs_tol;
+    no.uzawa.krylov.max_iterations = o->max_iterations;
+    VelocityBC bc;
+    bc.g = make_bc(p->bc_kind);
+    NSSolution sol = navier_stokes_solve(hier, p->k, bc, p->nu, load, p->inv_eps, no);
+    std::memset(rep, 0, sizeof(*rep));
+    rep->picard_iterations = sol.report.picard_iterations;
+    rep->newton_iterations = sol.report.newton_iterations;
+    rep->n_picard_inner = int(std::min<std::size_t>(sol.report.picard_inner.size(), 512));
+    rep->n_newton_inner = int(std::min<std::size_t>(sol.report.newton_inner.size(), 256));
+    for (int i = 0; i < rep->n_picard_inner; ++i) rep->picard_inner[i] = sol.report.picard_inner[std::size_t(i)];
+    for (int i = 0; i < rep->n_newton_inner; ++i) rep->newton_inner[i] = sol.report.newton_inner[std::size_t(i)];
+    for (std::size_t i = 0; i < sol.report.picard_diffs.size() && i < 128; ++i)
+      rep->picard_diffs[i] = sol.report.picard_diffs[i];
+    for (std::size_t i = 0; i < sol.report.newton_diffs.size() && i < 64; ++i)
+      rep->newton_diffs[i] = sol.report.newton_diffs[i];
+    rep->converged = sol.report.converged;
+    rep->not_applicable = sol.report.not_applicable;
+    rep->final_divergence = sol.report.final_divergence;
+    if (sol.velocity.compound.size()) {
+      std::memcpy(velocity, sol.velocity.compound.data(), sizeof(double) * std::size_t(sol.velocity.compound.size()));
+      if (sol.velocity.interior.size())
+        std::memcpy(interior, sol.velocity.interior.data(), sizeof(double) * std::size_t(sol.velocity.interior.size()));
+      std::memcpy(pressure, sol.pressure.data(), sizeof(double) * std::size_t(sol.pressure.size()));
+    }
+    rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return 0;
   } catch (const std::exception& e) {
     g_err = e.what();
     return -1;

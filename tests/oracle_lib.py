@@ -386,16 +386,18 @@ def mms_point(x, y, nu, beta):
 def ns_solve(*, mesh_kind=0, base_n=2, levels=2, k=0, nu=1.0, inv_eps=1e3, bc=BC_LID_UNIT, load_kind=LOAD_NONE,
              load=None, cycle=CYCLE_V, smoother=SM_MULT, smooth_steps=1, picard_tol=1e-4, newton_rel_tol=1e-8,
              newton_abs_tol=1e-10, max_picard=60, max_newton=25, pseudo_time_inv=0.0, outer=2, rel_tol=1e-8,
-             abs_tol=1e-10, max_it=500):
-    """Oracle navier_stokes_solve (reference inc/ns.hpp:69-149)."""
-    L = lib()
+             abs_tol=1e-10, max_it=500, reference=False):
+    """Oracle navier_stokes_solve (reference inc/ns.hpp:69-149); reference=True
+    runs the reference's own driver (oracle/_ref/libref.so)."""
+    L = ref_lib() if reference else lib()
     ld = None if load is None else np.ascontiguousarray(load, dtype=np.float64)
     p = Problem(mesh_kind, base_n, levels, k, nu, 0.0, 0.0, inv_eps, bc, load_kind,
                 _dp(ld) if ld is not None else None, WIND_NONE, cycle, smoother, smooth_steps, 1.0 / 3.0, 0, 0)
     o = NSOpts(picard_tol, newton_rel_tol, newton_abs_tol, max_picard, max_newton, pseudo_time_inv, outer, rel_tol,
                abs_tol, max_it)
     # sizes from a throwaway problem of the same mesh and order
-    probe = OracleMG(mesh_kind=mesh_kind, base_n=base_n, levels=levels, k=k, nu=nu, inv_eps=inv_eps, bc=bc)
+    probe = OracleMG(mesh_kind=mesh_kind, base_n=base_n, levels=levels, k=k, nu=nu, inv_eps=inv_eps, bc=bc,
+                     reference=reference)
     vel = np.zeros(probe.n_full)
     interior = np.zeros(max(probe.ne * k * (k + 1), 1))
     pres = np.zeros(probe.ne)
