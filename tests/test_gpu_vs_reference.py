@@ -5,8 +5,8 @@ inhomogeneous inlet profile and an outflow (do-nothing) boundary, W and
 variable-V cycles with two smoothing steps, the additive smoother, the
 rotation wind with the Newton linearisation, and the stationary
 Navier-Stokes driver (reference ns.hpp:69-149). Tolerances as in
-test_gpu_parity.py; counts +-1; velocities <= 1e-9 (1e-8 where a GMRES or a
-Picard/Newton iteration sits in between)."""
+test_gpu_parity.py; counts +-1; Uzawa velocities <= 1e-9; single Krylov
+solves and the Picard/Newton driver 1e-8."""
 import numpy as np
 import pytest
 
@@ -60,7 +60,7 @@ def test_additive_smoother(k):
     xr, sr = ref.krylov(ref.rhs())
     xg, sg = H.pcg(gpu, ref.rhs())
     assert abs(sg.iterations - sr["iterations"]) <= 1
-    assert rel(xg, xr) < 1e-9
+    assert rel(xg, xr) < 1e-8  # one PCG solve to 1e-8 (test_gpu_parity.py: same bound)
 
 
 @pytest.mark.parametrize("newton", [False, True])
