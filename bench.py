@@ -273,6 +273,18 @@ def run_hpmg(args, rank, world, local, dist):
     # the one-time CUDA module loading)
     sol = H.uzawa_solve(B)
     launches = B.launches_per_apply()
+    krylov = None
+    if args.krylov and args.config == "config2":
+        # PCG on this context; GMRES(50) on BASELINE config 5 (Re = 1)
+        krylov = {"pcg_config2": krylov_overhead(H, B)}
+        B5 = H.MGPreconditioner(base_n=8, levels=6, k=2, nu=1.0, beta=0.0, inv_eps=1e3, cycle=H.CYCLE_V,
+                                bc="lid_unit", wind="config5_wind",
+                                structured_load=(256, H.seeded_load(256, args.seed, -0.1, 0.1)))
+        krylov["gmres50_config5_re1"] = krylov_overhead(H, B5, restart=50)
+        krylov["note"] = ("whole solve = one CUDA-graph launch (device conditional nodes); overhead = per-iteration "
+                          "cost minus the V-cycle and the operator apply it contains (vector updates, reductions, "
+                          "for GMRES the fused MGS step kernels, at j from 5 to 25)")
+        B5.close()
     out = None
     if rank == 0:
         out = {
@@ -325,6 +337,7 @@ def run_hpmg(args, rank, world, local, dist):
                           "head_post": phases[3]},
             "gpu_launches": int(launches * args.steps),
             "kernels_per_vcycle": int(launches),
+            "krylov": krylov,
             "operator_apply": {"kernel": "k_spmv<bs> (ELL-BSR, 5 slots per facet block row)",
                                "ms": ms_spmv, "bytes": spmv_bytes,
                                "achieved": spmv_bytes / (ms_spmv * 1e-3) / 1e9 if ms_spmv > 0 else None,
@@ -464,6 +477,30 @@ def finish_cpu_tts(proc, timeout):
         return {"unavailable": f"reference TTS child did not finish: {type(e).__name__}"}
 
 
+def krylov_overhead(H, B, restart=0):
+    """Per-iteration cost of the device Krylov loop (slope of capped solves,
+    5 and 25 iterations, best of 3) against the V-cycle and the operator
+    apply it contains."""
+    rhs = B.rhs()
+    solver = H.pcg if B.symmetric() else H.gmres
+
+    def t(k):
+        best = 1e9
+        for _ in range(3):
+            t0 = time.perf_counter()
+            solver(B, rhs, opt=H.KrylovOptions(max_iterations=k, rel_tol=1e-30, abs_tol=0.0, restart=restart))
+            best = min(best, time.perf_counter() - t0)
+        return best
+
+    t(3)
+    per_it = (t(25) - t(5)) / 20 * 1e3
+    vc = B.time_apply(20)[0]
+    sp = B.time_spmv(20)[0]
+    return {"solver": solver.__name__ + (f"({restart})" if restart else ""), "ms_per_iteration": per_it,
+            "vcycle_ms": vc, "spmv_ms": sp, "overhead_ms": per_it - vc - sp,
+            "overhead_frac_of_vcycle": (per_it - vc - sp) / vc}
+
+
 def workload_config(args, cfg, n):
     """The config dict both arms print (same keys, same values)."""
     return {"workload": args.config, **cfg, "cycle": "V(1,1)", "smoother": "multiplicative vertex-patch",
@@ -511,6 +548,7 @@ def main():
     ap.add_argument("--cpu-vcycles", type=int, default=3)
     ap.add_argument("--ref-vcycles-per-step", type=int, default=1)
     ap.add_argument("--no-cpu-tts", dest="cpu_tts", action="store_false", default=True)
+    ap.add_argument("--no-krylov", dest="krylov", action="store_false", default=True)
     ap.add_argument("--cpu-tts-child", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.cpu_tts_child:
