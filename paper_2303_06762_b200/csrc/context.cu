@@ -1073,7 +1073,10 @@ bool build_gm_loop(hpmg_ctx& C) {
             dev::gm_givens(C.sc, G, h_inner, C.s);
           } else {
             cudaGraph_t mgs = add_conditional(C.s, h_mgs, cudaGraphCondTypeWhile);
-            capture_body(C, mgs, 3, [&] { dev::mgs_step(G, C.ktmp, n, C.red, h_mgs, C.s); });
+            // four MGS steps per loop-body iteration (steps past j return at once)
+            capture_body(C, mgs, 3, [&] {
+              for (int u = 0; u < 4; ++u) dev::mgs_step(G, C.ktmp, n, C.red, h_mgs, C.s);
+            });
             dev::mgs_tail(G, C.ktmp, n, C.red, C.s);
             dev::gm_arnoldi_close(C.sc, G, C.ktmp, n, h_inner, C.s);
           }

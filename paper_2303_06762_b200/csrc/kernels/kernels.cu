@@ -1160,6 +1160,7 @@ __global__ void k_gm_copy(GmDev G, double* __restrict__ dst, int64_t n, cudaGrap
 /// with the dot of step i: w -= h(i-1) v(i-1); h(i) = w . v(i)
 __global__ void k_mgs(GmDev G, double* __restrict__ w, int64_t n, Reduce red, cudaGraphConditionalHandle h_mgs) {
   const int i = int(G.st[kGmI]), j = int(G.st[kGmJ]);
+  if (i > j) return;  // several steps per loop-body iteration: the surplus ones are no-ops
   double* hcol = G.H + int64_t(j) * G.ldh;
   const double* vi = G.V + int64_t(i) * G.ldv;
   double s = 0.0;

@@ -14,7 +14,7 @@ namespace dev {
 
 constexpr int kSlots = 5;
 constexpr int kMaxPatchF = 8;
-constexpr int kRedBlocks = 296;  // 2 x 148 SMs: fixed partial count => deterministic sums
+constexpr int kRedBlocks = 1184;  // 8 x 148 SMs (full occupancy at 256 threads): fixed partial count => deterministic sums
 
 /// Block-sparse operator of one level: nb rows x kSlots fixed-width slots.
 struct Bsr {
