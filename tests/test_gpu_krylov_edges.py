@@ -1,0 +1,109 @@
+"""Edge cases of the device-resident Krylov loops (one CUDA-graph launch per
+solve, decisions on the device) against the reference semantics
+(krylov.hpp:30-144): not-applicable detection, the iteration cap (where the
+reference still forms z = M r and checks r.z after the last iteration), an
+initial guess that already satisfies the tolerance, short GMRES(m) cycles
+against the restatement's GMRES(m), and repeated solves on one context
+(the graphs are built once and relaunched)."""
+import numpy as np
+import pytest
+
+import oracle_lib as O
+
+pytestmark = pytest.mark.gpu
+
+H = pytest.importorskip("paper_2303_06762_b200")
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def inlet(x, y):
+    return (16.0 * (1.0 - y) * (y - 0.5), 0.0) if x < 1e-12 else (0.0, 0.0)
+
+
+def reference():
+    return True if O.ref_available() else False
+
+
+def stokes_pair(k=1, **extra):
+    n_f = 8
+    F = O.seeded_load(n_f, 1)
+    kw = dict(base_n=2, levels=3, k=k, beta=1.0, inv_eps=1e3, cycle=O.CYCLE_V)
+    kw.update(extra)
+    ref = O.OracleMG(reference=reference(), load_kind=O.LOAD_ARRAY, load=F, **kw)
+    gpu = H.MGPreconditioner(structured_load=(n_f, F), **kw)
+    return ref, gpu
+
+
+def test_pcg_not_applicable_matches_reference():
+    # reference tests/acceptance (oracle pin test_w1_loses_definiteness_on_step):
+    # one W(1) smoothing step on the step domain is not positive definite
+    kw = dict(base_n=2, levels=3, k=0, beta=1e3, inv_eps=1e6, cycle=O.CYCLE_W, smooth_steps=1)
+    ref = O.OracleMG(reference=reference(), mesh_kind=1, bc=O.BC_INLET, **kw)
+    gpu = H.MGPreconditioner(mesh="step", bc=inlet, **kw)
+    ur, ug = ref.uzawa(), H.uzawa_solve(gpu)
+    assert ur["not_applicable"] and ug.report.not_applicable
+    assert not ug.report.converged
+    assert ug.report.inner_iterations == ur["inner_iterations"]
+    xr, sr = ref.krylov(ref.rhs())
+    xg, sg = H.pcg(gpu, ref.rhs())
+    assert sr["not_applicable"] and sg.not_applicable
+    assert sg.iterations == sr["iterations"]
+
+
+@pytest.mark.parametrize("cap", [1, 3, 7])
+def test_pcg_iteration_cap(cap):
+    ref, gpu = stokes_pair(k=2)
+    b = ref.rhs()
+    xr, sr = ref.krylov(b, max_it=cap)
+    xg, sg = H.pcg(gpu, b, opt=H.KrylovOptions(max_iterations=cap))
+    assert sg.iterations == sr["iterations"] == cap
+    assert not sg.converged and not sr["converged"]
+    assert rel(xg, xr) < 1e-10
+    assert abs(sg.residual - sr["residual"]) <= 1e-8 * sr["residual"]
+
+
+def test_converged_initial_guess_takes_no_iteration():
+    ref, gpu = stokes_pair(k=1)
+    b = ref.rhs()
+    x, st = H.pcg(gpu, b)
+    x2, st2 = H.pcg(gpu, b, x=x)
+    assert st.converged and st2.converged and st2.iterations == 0
+    assert np.array_equal(x2, x)
+
+
+@pytest.mark.parametrize("m", [3, 8])
+def test_short_gmres_cycles_match_restatement(m):
+    # GMRES(m) has no reference counterpart (krylov.hpp:79-84 is unrestarted):
+    # the restatement's GMRES(m) extension is the checker
+    n_f = 8
+    F = O.seeded_load(n_f, 3, -0.1, 0.1)
+    kw = dict(base_n=2, levels=3, k=1, nu=1e-2, inv_eps=1e3, cycle=O.CYCLE_V)
+    orc = O.OracleMG(bc=O.BC_LID_UNIT, wind=O.WIND_CURL, load_kind=O.LOAD_ARRAY, load=F, **kw)
+    gpu = H.MGPreconditioner(bc="lid_unit", wind="config5_wind", structured_load=(n_f, F), **kw)
+    orc.set_restart(m)
+    b = orc.rhs()
+    xo, so = orc.krylov(b, method=1)
+    xg, sg = H.gmres(gpu, b, opt=H.KrylovOptions(restart=m))
+    assert so["converged"] and sg.converged
+    assert abs(sg.iterations - so["iterations"]) <= 1
+    assert rel(xg, xo) < 1e-8
+    # capped mid-cycle
+    xo2, so2 = orc.krylov(b, method=1, max_it=m + 2)
+    xg2, sg2 = H.gmres(gpu, b, opt=H.KrylovOptions(restart=m, max_iterations=m + 2))
+    assert sg2.iterations == so2["iterations"] == m + 2 and not sg2.converged
+    assert rel(xg2, xo2) < 1e-9
+
+
+def test_repeated_solves_reuse_the_loop_graphs():
+    ref, gpu = stokes_pair(k=1)
+    b = ref.rhs()
+    runs = [H.pcg(gpu, b) for _ in range(3)]
+    for x, st in runs[1:]:
+        assert st.iterations == runs[0][1].iterations
+        assert np.array_equal(x, runs[0][0])
+    # a different cap after a full solve (the graph takes the cap at launch)
+    x3, st3 = H.pcg(gpu, b, opt=H.KrylovOptions(max_iterations=2))
+    assert st3.iterations == 2
