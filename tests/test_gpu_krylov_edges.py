@@ -76,11 +76,12 @@ def test_converged_initial_guess_takes_no_iteration():
 
 @pytest.mark.parametrize("m", [3, 8])
 def test_short_gmres_cycles_match_restatement(m):
+    # nu = 0.1: GMRES(3) converges in ~23 iterations (at nu = 1e-2 it stagnates)
     # GMRES(m) has no reference counterpart (krylov.hpp:79-84 is unrestarted):
     # the restatement's GMRES(m) extension is the checker
     n_f = 8
     F = O.seeded_load(n_f, 3, -0.1, 0.1)
-    kw = dict(base_n=2, levels=3, k=1, nu=1e-2, inv_eps=1e3, cycle=O.CYCLE_V)
+    kw = dict(base_n=2, levels=3, k=1, nu=1e-1, inv_eps=1e3, cycle=O.CYCLE_V)
     orc = O.OracleMG(bc=O.BC_LID_UNIT, wind=O.WIND_CURL, load_kind=O.LOAD_ARRAY, load=F, **kw)
     gpu = H.MGPreconditioner(bc="lid_unit", wind="config5_wind", structured_load=(n_f, F), **kw)
     orc.set_restart(m)
