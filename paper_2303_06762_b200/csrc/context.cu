@@ -789,9 +789,9 @@ void out_vec(hpmg_ctx& C, const double* src_blk, double* dst, int flags) {
 
 // ---------------------------------------------------------------- solvers
 /// One PCG iteration as a CUDA graph: a while node whose body is
-///   Ap = A p, p.Ap | x += a p, r -= a Ap, r.r | count, stop test
-///   | if (more): z = M r (the V-cycle launch sequence), r.z, beta, p = z + beta p
-///   | continue while running
+///   Ap = A p, p.Ap | x += a p, r -= a Ap, r.r, count, stop test
+///   | if (more): z = M r (the V-cycle launch sequence), r.z + beta, p = z + beta p
+/// (the loop handle is cleared by the kernel that decides to stop)
 /// (reference krylov.hpp:44-70). The branch and loop predicates are set on
 /// the device (cudaGraphSetConditional), so a whole solve is one graph launch
 /// with no host round trip per iteration. Returns false (and the host loop is
@@ -837,8 +837,7 @@ bool build_pcg_loop(hpmg_ctx& C) {
       return fail(e);
     capturing = true;
     dev::spmv(T.A, C.kp, nullptr, C.kAp, 0, &C.red, C.sc + S_PAP, s_main);
-    dev::pcg_update(C.kx, C.kr, C.kp, C.kAp, n, C.sc, S_RZ0, S_PAP, C.red, S_RR, s_main);
-    dev::pcg_loop_check(C.sc, h_more, s_main);
+    dev::pcg_loop_update(C.kx, C.kr, C.kp, C.kAp, n, C.sc, C.red, h_more, h_loop, s_main);
     // the if node, appended to the capture
     cudaStreamCaptureStatus cs;
     const cudaGraphNode_t* deps = nullptr;
@@ -859,8 +858,7 @@ bool build_pcg_loop(hpmg_ctx& C) {
     capturing2 = true;
     C.s = C.s_cap;
     apply_blocks(C, C.kr, C.kz);  // z = M r
-    dev::dot(C.kr, C.kz, n, C.red, C.sc + S_RZ1, C.s);
-    dev::pcg_loop_beta(C.sc, C.s);
+    dev::pcg_loop_rz(C.kr, C.kz, n, C.sc, C.red, h_loop, C.s);
     dev::pcg_loop_direction(C.kp, C.kz, n, C.sc, C.s);
     C.s = s_main;
     cudaGraph_t ibody;
@@ -868,7 +866,6 @@ bool build_pcg_loop(hpmg_ctx& C) {
     if ((e = cudaStreamEndCapture(C.s_cap, &ibody)) != cudaSuccess) return fail(e);
     if ((e = cudaStreamUpdateCaptureDependencies(s_main, &inode, 1, cudaStreamSetCaptureDependencies)) != cudaSuccess)
       return fail(e);
-    dev::loop_continue(C.sc, h_loop, s_main);
     cudaGraph_t b2;
     capturing = false;
     if ((e = cudaStreamEndCapture(s_main, &b2)) != cudaSuccess) return fail(e);

@@ -81,6 +81,33 @@ __device__ void finalize(double v, Reduce red, double* out) {
   }
 }
 
+/// finalize() followed by `epi(sum)` on thread 0 of the last block (after the
+/// sum is stored): the single-thread bookkeeping of a Krylov loop rides on
+/// the reduction kernel instead of a launch of its own.
+template <class Epi>
+__device__ void finalize_then(double v, Reduce red, double* out, Epi epi) {
+  __shared__ bool last;
+  v = block_reduce<false>(v);
+  if (threadIdx.x == 0) {
+    red.partial[blockIdx.x] = v;
+    __threadfence();
+    unsigned t = atomicAdd(red.counter, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    double s = 0.0;
+    for (int i = threadIdx.x; i < gridDim.x; i += blockDim.x) s += __ldcg(&red.partial[i]);
+    s = block_reduce<false>(s);
+    if (threadIdx.x == 0) {
+      *out = s;
+      *red.counter = 0u;
+      epi(s);
+    }
+  }
+}
+
 inline int grid_for(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;
   if (g < 1) g = 1;
@@ -1065,33 +1092,59 @@ __global__ void k_pcg_update(double* __restrict__ x, double* __restrict__ r, con
 // ---- device-resident PCG iteration (one CUDA-graph while loop per solve;
 // reference krylov.hpp:30-73). Scalars live in sc[]: the loop slots below,
 // the reduction results written by the vector kernels.
-/// after the x/r update: iteration count, stop decision, the if-branch handle
-__global__ void k_pcg_loop_check(double* sc, cudaGraphConditionalHandle h_more) {
-  double st = kLoopRunning;
-  if (!(sc[kScPAp] > 0.0)) {
-    st = kLoopNaPAp;  // krylov.hpp:49-53; k_pcg_update left x and r untouched
-  } else {
-    sc[kScIt] += 1.0;  // st.iterations = it + 1
-    if (sqrt(sc[kScRR]) <= sc[kScTarget]) st = kLoopConverged;
-    else if (sc[kScIt] >= sc[kScMaxIt]) st = kLoopLast;  // the reference still forms z, r.z once more
-  }
-  sc[kScStatus] = st;
-  cudaGraphSetConditional(h_more, (st == kLoopRunning || st == kLoopLast) ? 1u : 0u);
-}
-/// after r.z: positivity (krylov.hpp:63-68), beta = rz_next / rz, rz = rz_next
-__global__ void k_pcg_loop_beta(double* sc) {
-  const double rzn = sc[kScRZn];
-  if (!(rzn > 0.0)) {
-    sc[kScStatus] = kLoopNaRZ;
+/// x += a p, r -= a Ap, r.r, then (last block) the iteration count and stop
+/// test of k_pcg_loop_check, setting the branch and (when stopping) the loop
+/// handles: one launch instead of two.
+__global__ void k_pcg_loop_update(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                                  const double* __restrict__ Ap, int64_t n, double* sc, Reduce red,
+                                  cudaGraphConditionalHandle h_more, cudaGraphConditionalHandle h_loop) {
+  if (!(sc[kScPAp] > 0.0)) {  // krylov.hpp:49-53: x and r untouched, not applicable
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      sc[kScStatus] = kLoopNaPAp;
+      cudaGraphSetConditional(h_more, 0u);
+      cudaGraphSetConditional(h_loop, 0u);
+    }
     return;
   }
-  if (sc[kScStatus] == kLoopLast) {
-    sc[kScStatus] = kLoopMaxIt;
-    return;
+  const double alpha = sc[kScRZ] / sc[kScPAp];
+  double s = 0.0;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    x[t] += alpha * p[t];
+    const double rv = r[t] - alpha * Ap[t];
+    r[t] = rv;
+    s = fma(rv, rv, s);
   }
-  sc[kScBeta] = rzn / sc[kScRZ];
-  sc[kScRZ] = rzn;
+  finalize_then(s, red, sc + kScRR, [&](double rr) {
+    sc[kScIt] += 1.0;
+    double st = kLoopRunning;
+    if (sqrt(rr) <= sc[kScTarget]) st = kLoopConverged;
+    else if (sc[kScIt] >= sc[kScMaxIt]) st = kLoopLast;
+    sc[kScStatus] = st;
+    cudaGraphSetConditional(h_more, (st == kLoopRunning || st == kLoopLast) ? 1u : 0u);
+    if (st == kLoopConverged) cudaGraphSetConditional(h_loop, 0u);
+  });
 }
+/// r.z, then (last block) k_pcg_loop_beta's positivity test and beta, with the
+/// loop handle cleared when the iteration stops here
+__global__ void k_pcg_loop_rz(const double* __restrict__ r, const double* __restrict__ z, int64_t n, double* sc,
+                              Reduce red, cudaGraphConditionalHandle h_loop) {
+  double s = 0.0;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x)
+    s = fma(r[t], z[t], s);
+  finalize_then(s, red, sc + kScRZn, [&](double rzn) {
+    if (!(rzn > 0.0)) {
+      sc[kScStatus] = kLoopNaRZ;
+      cudaGraphSetConditional(h_loop, 0u);
+    } else if (sc[kScStatus] == kLoopLast) {
+      sc[kScStatus] = kLoopMaxIt;
+      cudaGraphSetConditional(h_loop, 0u);
+    } else {
+      sc[kScBeta] = rzn / sc[kScRZ];
+      sc[kScRZ] = rzn;
+    }
+  });
+}
+
 /// p = z + beta p while running (krylov.hpp:69)
 __global__ void k_pcg_loop_direction(double* __restrict__ p, const double* __restrict__ z, int64_t n,
                                      const double* sc) {
@@ -1845,12 +1898,14 @@ void gm_end(double* sc, const GmDev& G, cudaStream_t s) {
   k_gm_end<<<1, 1, 0, s>>>(sc, G);
   HPMG_LAUNCH_CHECK();
 }
-void pcg_loop_check(double* sc, cudaGraphConditionalHandle h_more, cudaStream_t s) {
-  k_pcg_loop_check<<<1, 1, 0, s>>>(sc, h_more);
+void pcg_loop_update(double* x, double* r, const double* p, const double* Ap, int64_t n, double* sc, const Reduce& red,
+                     cudaGraphConditionalHandle h_more, cudaGraphConditionalHandle h_loop, cudaStream_t s) {
+  k_pcg_loop_update<<<kRedBlocks, 256, 0, s>>>(x, r, p, Ap, n, sc, red, h_more, h_loop);
   HPMG_LAUNCH_CHECK();
 }
-void pcg_loop_beta(double* sc, cudaStream_t s) {
-  k_pcg_loop_beta<<<1, 1, 0, s>>>(sc);
+void pcg_loop_rz(const double* r, const double* z, int64_t n, double* sc, const Reduce& red,
+                 cudaGraphConditionalHandle h_loop, cudaStream_t s) {
+  k_pcg_loop_rz<<<kRedBlocks, 256, 0, s>>>(r, z, n, sc, red, h_loop);
   HPMG_LAUNCH_CHECK();
 }
 void pcg_loop_direction(double* p, const double* z, int64_t n, const double* sc, cudaStream_t s) {

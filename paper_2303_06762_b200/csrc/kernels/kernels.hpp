@@ -197,8 +197,11 @@ enum : int {
 constexpr double kLoopRunning = 0.0, kLoopConverged = 1.0, kLoopNaPAp = 2.0, kLoopNaRZ = 3.0, kLoopMaxIt = 4.0,
                  kLoopLast = 5.0;
 void pcg_loop_init(double* sc, double target, double max_it, cudaStream_t s);
-void pcg_loop_check(double* sc, cudaGraphConditionalHandle h_more, cudaStream_t s);
-void pcg_loop_beta(double* sc, cudaStream_t s);
+/// the update with the count / stop test, r.z with the positivity test and beta
+void pcg_loop_update(double* x, double* r, const double* p, const double* Ap, int64_t n, double* sc, const Reduce& red,
+                     cudaGraphConditionalHandle h_more, cudaGraphConditionalHandle h_loop, cudaStream_t s);
+void pcg_loop_rz(const double* r, const double* z, int64_t n, double* sc, const Reduce& red,
+                 cudaGraphConditionalHandle h_loop, cudaStream_t s);
 void pcg_loop_direction(double* p, const double* z, int64_t n, const double* sc, cudaStream_t s);
 void loop_continue(const double* sc, cudaGraphConditionalHandle h_loop, cudaStream_t s);
 
