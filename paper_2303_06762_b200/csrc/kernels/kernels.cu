@@ -1092,9 +1092,10 @@ __global__ void k_pcg_update(double* __restrict__ x, double* __restrict__ r, con
 // ---- device-resident PCG iteration (one CUDA-graph while loop per solve;
 // reference krylov.hpp:30-73). Scalars live in sc[]: the loop slots below,
 // the reduction results written by the vector kernels.
-/// x += a p, r -= a Ap, r.r, then (last block) the iteration count and stop
-/// test of k_pcg_loop_check, setting the branch and (when stopping) the loop
-/// handles: one launch instead of two.
+/// x += a p, r -= a Ap, r.r, then (last block) the iteration count and the
+/// stop test (krylov.hpp:54-62; at the cap the reference still forms z = M r
+/// and checks r.z once more), setting the branch and, when stopping, the
+/// loop handle.
 __global__ void k_pcg_loop_update(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
                                   const double* __restrict__ Ap, int64_t n, double* sc, Reduce red,
                                   cudaGraphConditionalHandle h_more, cudaGraphConditionalHandle h_loop) {
@@ -1124,8 +1125,9 @@ __global__ void k_pcg_loop_update(double* __restrict__ x, double* __restrict__ r
     if (st == kLoopConverged) cudaGraphSetConditional(h_loop, 0u);
   });
 }
-/// r.z, then (last block) k_pcg_loop_beta's positivity test and beta, with the
-/// loop handle cleared when the iteration stops here
+/// r.z, then (last block) its positivity test (krylov.hpp:63-68) and
+/// beta = rz_next / rz, rz = rz_next; the loop handle is cleared when the
+/// iteration stops here
 __global__ void k_pcg_loop_rz(const double* __restrict__ r, const double* __restrict__ z, int64_t n, double* sc,
                               Reduce red, cudaGraphConditionalHandle h_loop) {
   double s = 0.0;
