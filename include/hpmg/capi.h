@@ -308,6 +308,11 @@ double hpmg_time_spmv(hpmg_ctx* ctx, int reps, double* bytes);
  * solve, out[2l] / out[2l+1] pre / post part of level l, out[2L+2..2L+4] head
  * pre-sweep, head residual, head post-sweep (ms). Returns the entry count. */
 int hpmg_profile_levels(hpmg_ctx* ctx, int reps, double* out);
+/* Development probe of the device-loop cost: ms per iteration of a graph while
+ * loop whose body is (mode 0) a countdown kernel only, (1) the V-cycle +
+ * countdown, (2) an if-node holding the V-cycle, then the countdown (PCG's
+ * nesting), (3) the V-cycle launched as a child-graph node + countdown. */
+double hpmg_debug_loop_probe(hpmg_ctx* ctx, int mode, int iters);
 /* Development hook: clock64 timeline of the one-CTA small-level sweep. */
 void hpmg_debug_small_trace(int arm, long long* out);
 /* development: per-CTA globaltimer stamps of the last wave-sweep launches (HPMG_DBG=4) */

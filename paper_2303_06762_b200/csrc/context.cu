@@ -237,9 +237,6 @@ struct hpmg_ctx {
   int gm_cap = 0, gm_graph_cap = 0;
   cudaGraphExec_t gm_loop = nullptr;
   bool gm_loop_failed = false;
-  bool gm_coop = true;             // fused cooperative MGS (else one launch per MGS step)
-  double* gm_part = nullptr;       // [2 * grid] partials of the cooperative MGS
-  unsigned* gm_bar = nullptr;      // its grid barrier
 
   Level& top() { return opt.k > 0 ? *head : *lv[L]; }
   int64_t nfree() { return top().n; }
@@ -1011,11 +1008,6 @@ void gm_workspace(hpmg_ctx& C, int cap) {
   C.gm.g = dalloc<double>(cap + 1);
   C.gm.y = dalloc<double>(cap);
   if (!C.gm.st) C.gm.st = dalloc<double>(8);
-  if (!C.gm_part) {
-    C.gm_part = dalloc<double>(size_t(2) * std::max(dev::mgs_coop_grid(), 1));
-    C.gm_bar = dalloc<unsigned>(1);
-    CK(cudaMemsetAsync(C.gm_bar, 0, sizeof(unsigned), C.s));
-  }
   C.gm_cap = cap;
   if (C.gm_loop) cudaGraphExecDestroy(C.gm_loop);
   C.gm_loop = nullptr;
@@ -1058,25 +1050,18 @@ bool build_gm_loop(hpmg_ctx& C) {
       dev::gm_start(C.sc, G, h_cyc, h_inner, C.s);
       cudaGraph_t cyc = add_conditional(C.s, h_cyc, cudaGraphCondTypeIf);
       capture_body(C, cyc, 1, [&] {
-        dev::gm_v0(G, C.kr, n, C.s);
+        dev::gm_v0(G, C.kr, C.kr, n, h_mgs, C.s);  // V[0] = r / beta, in place as z's input
         cudaGraph_t inner = add_conditional(C.s, h_inner, cudaGraphCondTypeWhile);
         capture_body(C, inner, 2, [&] {
-          dev::gm_copy(G, C.kr, n, h_mgs, C.s);
           apply_blocks(C, C.kr, C.kz);                                  // z = M v_j
           dev::spmv(T.A, C.kz, nullptr, C.ktmp, 0, nullptr, nullptr, C.s);  // w = A z
-          if (C.gm_coop) {
-            // all of the column's Gram-Schmidt, h(j+1) and V[j+1] in one cooperative launch
-            if (!dev::mgs_coop(G, C.ktmp, n, C.gm_part, C.gm_bar, C.s)) throw GraphError{cudaErrorNotSupported};
-            dev::gm_givens(C.sc, G, h_inner, C.s);
-          } else {
-            cudaGraph_t mgs = add_conditional(C.s, h_mgs, cudaGraphCondTypeWhile);
-            // four MGS steps per loop-body iteration (steps past j return at once)
-            capture_body(C, mgs, 3, [&] {
-              for (int u = 0; u < 4; ++u) dev::mgs_step(G, C.ktmp, n, C.red, h_mgs, C.s);
-            });
-            dev::mgs_tail(G, C.ktmp, n, C.red, C.s);
-            dev::gm_arnoldi_close(C.sc, G, C.ktmp, n, h_inner, C.s);
-          }
+          cudaGraph_t mgs = add_conditional(C.s, h_mgs, cudaGraphCondTypeWhile);
+          // four MGS steps per loop-body iteration (steps past j return at once)
+          capture_body(C, mgs, 3, [&] {
+            for (int u = 0; u < 4; ++u) dev::mgs_step(G, C.ktmp, n, C.red, h_mgs, C.s);
+          });
+          dev::mgs_tail(G, C.ktmp, n, C.red, C.s);
+          dev::gm_arnoldi_close(C.sc, G, C.ktmp, C.kr, n, C.red, h_inner, h_mgs, C.s);
         });
         dev::gm_update(G, C.kr, n, C.s);  // u = V y into the preconditioner's input
         apply_blocks(C, C.kr, C.kz);
@@ -1126,14 +1111,7 @@ hpmg_solve_stats gmres_device(hpmg_ctx& C, const hpmg_krylov_opts& o) {
     const int want = o.restart > 0 ? std::min(o.restart, o.max_iterations) : o.max_iterations;
     gm_workspace(C, want);
     if (!C.gm_loop || C.gm_graph_cap != C.gm_cap) {
-      static const bool no_coop = std::getenv("HPMG_GMRES_COOP") && !std::atoi(std::getenv("HPMG_GMRES_COOP"));
-      C.gm_coop = !no_coop;
-      bool ok = build_gm_loop(C);
-      if (!ok && C.gm_coop) {  // the fused MGS could not be captured: one launch per MGS step
-        C.gm_coop = false;
-        ok = build_gm_loop(C);
-      }
-      C.gm_loop_failed = !ok;
+      C.gm_loop_failed = !build_gm_loop(C);
     }
     if (C.gm_loop) {
       dev::gm_init(C.sc, C.gm, target, double(o.max_iterations), want, C.s);
@@ -1603,7 +1581,7 @@ void hpmg_destroy(hpmg_ctx* ctx) {
   for (cudaStream_t q : ctx->s_nest)
     if (q) cudaStreamDestroy(q);
   for (void* p : {(void*)ctx->gm.V, (void*)ctx->gm.H, (void*)ctx->gm.cs, (void*)ctx->gm.sn, (void*)ctx->gm.g,
-                  (void*)ctx->gm.y, (void*)ctx->gm.st, (void*)ctx->gm_part, (void*)ctx->gm_bar})
+                  (void*)ctx->gm.y, (void*)ctx->gm.st})
     if (p) dfree(p);
   auto fr = [](void* p) { if (p) dfree(p); };
   auto free_level = [&](Level* V) {
@@ -2263,6 +2241,74 @@ void hpmg_debug_sweep_trace(long long* out) { dev::sweep_trace(out); }
 /// Event-instrumented V-cycle (no graph): out[2l], out[2l+1] = pre/post part
 /// of level l (l = 1..L) in ms, out[0] = coarse solve, out[2(L+1)..+2] = head
 /// pre-sweep, residual+embed, post-sweep. Returns the number of entries.
+double hpmg_debug_loop_probe(hpmg_ctx* ctx, int mode, int iters) {
+  double ms_per = -1;
+  guarded(ctx, [&] {
+    hpmg_ctx& C = *ctx;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    double* c = C.sc + 15;
+    try {
+      GK(cudaGraphCreate(&g, 0));
+      cudaGraphConditionalHandle h, hi = 0;
+      GK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+      if (mode == 2) GK(cudaGraphConditionalHandleCreate(&hi, g, 1, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams wp = {};
+      wp.type = cudaGraphNodeTypeConditional;
+      wp.conditional.handle = h;
+      wp.conditional.type = cudaGraphCondTypeWhile;
+      wp.conditional.size = 1;
+      cudaGraphNode_t wnode;
+      GK(cudaGraphAddNode(&wnode, g, nullptr, 0, &wp));
+      capture_body(C, wp.conditional.phGraph_out[0], 0, [&] {
+        if (mode == 1) apply_blocks(C, C.kr, C.kz);
+        if (mode == 2) {
+          cudaGraph_t br = add_conditional(C.s, hi, cudaGraphCondTypeIf);
+          capture_body(C, br, 1, [&] { apply_blocks(C, C.kr, C.kz); });
+        }
+        if (mode == 3) {
+          cudaGraph_t child;
+          GK(cudaGraphCreate(&child, 0));
+          capture_body(C, child, 1, [&] { apply_blocks(C, C.kr, C.kz); });
+          cudaStreamCaptureStatus cs;
+          const cudaGraphNode_t* deps = nullptr;
+          size_t ndeps = 0;
+          cudaGraph_t capg;
+          GK(cudaStreamGetCaptureInfo(C.s, &cs, nullptr, &capg, &deps, &ndeps));
+          cudaGraphNode_t cn;
+          GK(cudaGraphAddChildGraphNode(&cn, capg, deps, ndeps, child));
+          GK(cudaStreamUpdateCaptureDependencies(C.s, &cn, 1, cudaStreamSetCaptureDependencies));
+          cudaGraphDestroy(child);
+        }
+        dev::loop_countdown(c, h, C.s);
+      });
+      GK(cudaGraphInstantiate(&ge, g, 0));
+    } catch (const GraphError& e) {
+      if (g) cudaGraphDestroy(g);
+      throw std::runtime_error(std::string("loop probe: ") + cudaGetErrorString(e.e));
+    }
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    const double warm = 3.0, n = double(iters);
+    CK(cudaMemcpyAsync(c, &warm, sizeof(double), cudaMemcpyHostToDevice, C.s));
+    CK(cudaGraphLaunch(ge, C.s));
+    CK(cudaMemcpyAsync(c, &n, sizeof(double), cudaMemcpyHostToDevice, C.s));
+    CK(cudaEventRecord(e0, C.s));
+    CK(cudaGraphLaunch(ge, C.s));
+    CK(cudaEventRecord(e1, C.s));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms_per = ms / iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+  });
+  return ms_per;
+}
+
 int hpmg_profile_levels(hpmg_ctx* ctx, int reps, double* out) {
   int nout = 0;
   guarded(ctx, [&] {

@@ -1156,6 +1156,11 @@ __global__ void k_pcg_loop_direction(double* __restrict__ p, const double* __res
     p[t] = z[t] + beta * p[t];
 }
 /// last node of the loop body: iterate again while running
+/// development probe: c -= 1; loop while c > 0
+__global__ void k_loop_countdown(double* c, cudaGraphConditionalHandle h_loop) {
+  c[0] -= 1.0;
+  cudaGraphSetConditional(h_loop, c[0] > 0.0 ? 1u : 0u);
+}
 __global__ void k_loop_continue(const double* sc, cudaGraphConditionalHandle h_loop) {
   cudaGraphSetConditional(h_loop, sc[kScStatus] == kLoopRunning ? 1u : 0u);
 }
@@ -1195,17 +1200,16 @@ __global__ void k_gm_start(double* sc, GmDev G, cudaGraphConditionalHandle h_cyc
   cudaGraphSetConditional(h_cyc, 1u);
   cudaGraphSetConditional(h_inner, sc[kScIt] < sc[kScMaxIt] ? 1u : 0u);
 }
-/// V[0] = r / beta
-__global__ void k_gm_v0(GmDev G, const double* __restrict__ r, int64_t n) {
+/// V[0] = r / beta, also into the preconditioner's input u; arms the
+/// Gram-Schmidt loop of column 0
+__global__ void k_gm_v0(GmDev G, const double* r, double* u, int64_t n,  // r may alias u
+                        cudaGraphConditionalHandle h_mgs) {
   const double beta = G.st[kGmBeta];
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x)
-    G.V[t] = r[t] / beta;
-}
-/// dst = V[j] (the preconditioner's input); arms the Gram-Schmidt loop
-__global__ void k_gm_copy(GmDev G, double* __restrict__ dst, int64_t n, cudaGraphConditionalHandle h_mgs) {
-  const double* v = G.V + int64_t(G.st[kGmJ]) * G.ldv;
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x)
-    dst[t] = v[t];
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const double v = r[t] / beta;
+    G.V[t] = v;
+    u[t] = v;
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     G.st[kGmI] = 0.0;
     cudaGraphSetConditional(h_mgs, 1u);
@@ -1252,99 +1256,8 @@ __global__ void k_mgs(GmDev G, double* __restrict__ w, int64_t n, Reduce red, cu
     }
   }
 }
-/// Grid barrier number `epoch` (1-based) of a cooperative launch: one
-/// release arrival per CTA on a monotonic counter, acquire polls.
-__device__ __forceinline__ void coop_barrier(unsigned* bar, unsigned epoch) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1u);
-    const unsigned target = epoch * gridDim.x;
-    unsigned v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-    } while (v < target);
-  }
-  __syncthreads();
-}
-
-/// The whole modified Gram-Schmidt of Arnoldi column j in ONE cooperative
-/// launch (krylov.hpp:100-106): each CTA keeps its contiguous slice of w and
-/// of the previous basis vector in registers, so per step i only V[i] is
-/// read (once); the dot of step i is reduced grid-wide through a barrier and
-/// summed by every CTA in the same fixed order. Step i performs the axpy of
-/// step i-1 then the dot of step i, i.e. per entry exactly the reference's
-/// sequence; after step j the norm of w gives h(j+1), the happy-breakdown
-/// flag, and V[j+1] = w / h(j+1).
-template <int E>
-__global__ void __launch_bounds__(256) k_mgs_coop(GmDev G, const double* __restrict__ w_in, int64_t n,
-                                                  double* __restrict__ part, unsigned* bar) {
-  __shared__ double bcast;
-  const int j = int(G.st[kGmJ]);
-  const int64_t per = ((n + gridDim.x - 1) / gridDim.x + 255) / 256 * 256;
-  const int64_t c0 = int64_t(blockIdx.x) * per;
-  double w[E], vp[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int64_t t = c0 + threadIdx.x + int64_t(e) * 256;
-    w[e] = (t < n && t < c0 + per) ? w_in[t] : 0.0;
-    vp[e] = 0.0;
-  }
-  double* hcol = G.H + int64_t(j) * G.ldh;
-  double hprev = 0.0;
-  unsigned epoch = 0;
-  for (int i = 0; i <= j + 1; ++i) {
-    double s = 0.0;
-    if (i <= j) {
-      const double* vi = G.V + int64_t(i) * G.ldv;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int64_t t = c0 + threadIdx.x + int64_t(e) * 256;
-        if (i > 0) w[e] = w[e] - hprev * vp[e];
-        const double v = (t < n && t < c0 + per) ? vi[t] : 0.0;
-        vp[e] = v;
-        s = fma(w[e], v, s);
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        w[e] = w[e] - hprev * vp[e];
-        s = fma(w[e], w[e], s);
-      }
-    }
-    s = block_reduce<false>(s);
-    double* pb = part + size_t(i & 1) * gridDim.x;
-    if (threadIdx.x == 0) pb[blockIdx.x] = s;
-    coop_barrier(bar, ++epoch);
-    double a = 0.0;
-    for (int b = threadIdx.x; b < int(gridDim.x); b += blockDim.x) a += __ldcg(pb + b);
-    a = block_reduce<false>(a);
-    if (threadIdx.x == 0) bcast = a;
-    __syncthreads();
-    hprev = bcast;
-    if (i <= j && blockIdx.x == 0 && threadIdx.x == 0) hcol[i] = hprev;
-  }
-  const double h = sqrt(hprev);
-  const bool happy = h <= 1e-14 * G.st[kGmBeta];
-  if (!happy) {
-    double* vn = G.V + int64_t(j + 1) * G.ldv;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int64_t t = c0 + threadIdx.x + int64_t(e) * 256;
-      if (t < n && t < c0 + per) vn[t] = w[e] / h;
-    }
-  }
-  // every CTA has read the partials of the last step: reset for the next launch
-  coop_barrier(bar, ++epoch);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    hcol[j + 1] = h;
-    G.st[kGmHn] = hprev;
-    G.st[kGmHappy] = happy ? 1.0 : 0.0;
-    bar[0] = 0u;
-  }
-}
-
-/// last axpy of column j and |w|^2
+/// last axpy of column j and |w|^2; the last block then stores
+/// h(j+1) = |w| into H and the breakdown flag (krylov.hpp:104-106)
 __global__ void k_mgs_tail(GmDev G, double* __restrict__ w, int64_t n, Reduce red) {
   const int j = int(G.st[kGmJ]);
   const double hp = G.H[int64_t(j) * G.ldh + j];
@@ -1355,27 +1268,16 @@ __global__ void k_mgs_tail(GmDev G, double* __restrict__ w, int64_t n, Reduce re
     w[t] = wt;
     s = fma(wt, wt, s);
   }
-  finalize<false>(s, red, G.st + kGmHn);
+  finalize_then(s, red, G.st + kGmHn, [&](double hn) {
+    const double h = sqrt(hn);
+    G.H[int64_t(j) * G.ldh + j + 1] = h;
+    G.st[kGmHappy] = h <= 1e-14 * G.st[kGmBeta] ? 1.0 : 0.0;
+  });
 }
-/// h(j+1) = |w|, the happy-breakdown flag (krylov.hpp:104-105)
-__global__ void k_gm_hnorm(GmDev G) {
-  const int j = int(G.st[kGmJ]);
-  const double h = sqrt(G.st[kGmHn]);
-  G.H[int64_t(j) * G.ldh + j + 1] = h;
-  G.st[kGmHappy] = h <= 1e-14 * G.st[kGmBeta] ? 1.0 : 0.0;
-}
-/// V[j+1] = w / h(j+1) unless happy (krylov.hpp:106)
-__global__ void k_gm_newv(GmDev G, const double* __restrict__ w, int64_t n) {
-  if (G.st[kGmHappy] != 0.0) return;
-  const int j = int(G.st[kGmJ]);
-  const double h = G.H[int64_t(j) * G.ldh + j + 1];
-  double* v = G.V + int64_t(j + 1) * G.ldv;
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x)
-    v[t] = w[t] / h;
-}
-/// previous rotations on column j, the new rotation, g, the stop test
-/// (krylov.hpp:107-124)
-__global__ void k_gm_givens(double* sc, GmDev G, cudaGraphConditionalHandle h_inner) {
+/// Givens rotations of column j and the residual estimate (krylov.hpp:107-118);
+/// decides whether the Arnoldi loop continues. One thread.
+__device__ void gm_givens_step(double* sc, GmDev G, cudaGraphConditionalHandle h_inner,
+                               cudaGraphConditionalHandle h_mgs) {
   const int j = int(G.st[kGmJ]);
   double* h = G.H + int64_t(j) * G.ldh;
   for (int i = 0; i < j; ++i) {
@@ -1397,8 +1299,40 @@ __global__ void k_gm_givens(double* sc, GmDev G, cudaGraphConditionalHandle h_in
   const bool exit = gn <= sc[kScTarget] || happy;
   if (exit) G.st[kGmStalled] = (happy && gn > sc[kScTarget]) ? 1.0 : 0.0;
   const bool more = !exit && sc[kScIt] < sc[kScMaxIt] && double(j + 1) < G.st[kGmCap];
-  if (more) G.st[kGmJ] = double(j + 1);
+  if (more) {
+    G.st[kGmJ] = double(j + 1);
+    G.st[kGmI] = 0.0;  // arm the Gram-Schmidt loop of the next column
+    cudaGraphSetConditional(h_mgs, 1u);
+  }
   cudaGraphSetConditional(h_inner, more ? 1u : 0u);
+}
+/// V[j+1] = w / h(j+1), also into the preconditioner's input u (the next
+/// column's z = M v); the last block then runs the Givens step. Without a
+/// breakdown only: after one the loop ends and u is overwritten by gm_update.
+__global__ void k_gm_newv(double* sc, GmDev G, const double* __restrict__ w, double* __restrict__ u, int64_t n,
+                          unsigned* counter, cudaGraphConditionalHandle h_inner, cudaGraphConditionalHandle h_mgs) {
+  const int j = int(G.st[kGmJ]);
+  if (G.st[kGmHappy] == 0.0) {
+    const double h = G.H[int64_t(j) * G.ldh + j + 1];
+    double* v = G.V + int64_t(j + 1) * G.ldv;
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+      const double x = w[t] / h;
+      v[t] = x;
+      u[t] = x;
+    }
+  }
+  __shared__ bool last;
+  __syncthreads();  // every thread has read st[J] and H before the last block's Givens step changes them
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    *counter = 0u;
+    gm_givens_step(sc, G, h_inner, h_mgs);
+  }
 }
 /// back substitution H y = g over the m columns (krylov.hpp:126-131)
 __global__ void k_gm_solve(GmDev G) {
@@ -1823,12 +1757,8 @@ void gm_start(double* sc, const GmDev& G, cudaGraphConditionalHandle h_cyc, cuda
   k_gm_start<<<1, 1, 0, s>>>(sc, G, h_cyc, h_inner);
   HPMG_LAUNCH_CHECK();
 }
-void gm_v0(const GmDev& G, const double* r, int64_t n, cudaStream_t s) {
-  k_gm_v0<<<grid_for(n, 256), 256, 0, s>>>(G, r, n);
-  HPMG_LAUNCH_CHECK();
-}
-void gm_copy(const GmDev& G, double* dst, int64_t n, cudaGraphConditionalHandle h_mgs, cudaStream_t s) {
-  k_gm_copy<<<grid_for(n, 256), 256, 0, s>>>(G, dst, n, h_mgs);
+void gm_v0(const GmDev& G, const double* r, double* u, int64_t n, cudaGraphConditionalHandle h_mgs, cudaStream_t s) {
+  k_gm_v0<<<grid_for(n, 256), 256, 0, s>>>(G, r, u, n, h_mgs);
   HPMG_LAUNCH_CHECK();
 }
 void mgs_step(const GmDev& G, double* w, int64_t n, const Reduce& red, cudaGraphConditionalHandle h_mgs,
@@ -1836,58 +1766,13 @@ void mgs_step(const GmDev& G, double* w, int64_t n, const Reduce& red, cudaGraph
   k_mgs<<<kRedBlocks, 256, 0, s>>>(G, w, n, red, h_mgs);
   HPMG_LAUNCH_CHECK();
 }
-namespace {
-template <int E>
-bool launch_mgs_coop(const GmDev& G, const double* w, int64_t n, double* part, unsigned* bar, int grid,
-                     cudaStream_t s) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(256);
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_mgs_coop<E>, G, w, n, part, bar) == cudaSuccess;
-}
-}  // namespace
-
-int mgs_coop_grid() {
-  static int grid = -1;
-  if (grid < 0) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_mgs_coop<32>, 256, 0);
-    grid = per >= 2 ? 2 * sms : (per >= 1 ? sms : 0);
-  }
-  return grid;
-}
-bool mgs_coop(const GmDev& G, const double* w, int64_t n, double* part, unsigned* bar, cudaStream_t s) {
-  const int grid = mgs_coop_grid();
-  if (grid == 0) return false;
-  const int64_t per_thread = ((n + grid - 1) / grid + 255) / 256;
-  if (per_thread <= 8) return launch_mgs_coop<8>(G, w, n, part, bar, grid, s);
-  if (per_thread <= 16) return launch_mgs_coop<16>(G, w, n, part, bar, grid, s);
-  if (per_thread <= 32) return launch_mgs_coop<32>(G, w, n, part, bar, grid, s);
-  return false;
-}
 void mgs_tail(const GmDev& G, double* w, int64_t n, const Reduce& red, cudaStream_t s) {
   k_mgs_tail<<<kRedBlocks, 256, 0, s>>>(G, w, n, red);
   HPMG_LAUNCH_CHECK();
 }
-void gm_arnoldi_close(double* sc, const GmDev& G, const double* w, int64_t n, cudaGraphConditionalHandle h_inner,
-                      cudaStream_t s) {
-  k_gm_hnorm<<<1, 1, 0, s>>>(G);
-  HPMG_LAUNCH_CHECK();
-  k_gm_newv<<<grid_for(n, 256), 256, 0, s>>>(G, w, n);
-  HPMG_LAUNCH_CHECK();
-  k_gm_givens<<<1, 1, 0, s>>>(sc, G, h_inner);
-  HPMG_LAUNCH_CHECK();
-}
-void gm_givens(double* sc, const GmDev& G, cudaGraphConditionalHandle h_inner, cudaStream_t s) {
-  k_gm_givens<<<1, 1, 0, s>>>(sc, G, h_inner);
+void gm_arnoldi_close(double* sc, const GmDev& G, const double* w, double* u, int64_t n, const Reduce& red,
+                      cudaGraphConditionalHandle h_inner, cudaGraphConditionalHandle h_mgs, cudaStream_t s) {
+  k_gm_newv<<<kRedBlocks, 256, 0, s>>>(sc, G, w, u, n, red.counter, h_inner, h_mgs);
   HPMG_LAUNCH_CHECK();
 }
 void gm_update(const GmDev& G, double* u, int64_t n, cudaStream_t s) {
@@ -1912,6 +1797,10 @@ void pcg_loop_rz(const double* r, const double* z, int64_t n, double* sc, const 
 }
 void pcg_loop_direction(double* p, const double* z, int64_t n, const double* sc, cudaStream_t s) {
   k_pcg_loop_direction<<<grid_for(n, 256), 256, 0, s>>>(p, z, n, sc);
+  HPMG_LAUNCH_CHECK();
+}
+void loop_countdown(double* c, cudaGraphConditionalHandle h_loop, cudaStream_t s) {
+  k_loop_countdown<<<1, 1, 0, s>>>(c, h_loop);
   HPMG_LAUNCH_CHECK();
 }
 void loop_continue(const double* sc, cudaGraphConditionalHandle h_loop, cudaStream_t s) {

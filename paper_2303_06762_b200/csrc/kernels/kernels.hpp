@@ -204,6 +204,7 @@ void pcg_loop_rz(const double* r, const double* z, int64_t n, double* sc, const 
                  cudaGraphConditionalHandle h_loop, cudaStream_t s);
 void pcg_loop_direction(double* p, const double* z, int64_t n, const double* sc, cudaStream_t s);
 void loop_continue(const double* sc, cudaGraphConditionalHandle h_loop, cudaStream_t s);
+void loop_countdown(double* c, cudaGraphConditionalHandle h_loop, cudaStream_t s);
 
 /// Device GMRES state: basis slab V[(cap+1)][ldv], Hessenberg columns
 /// H[cap][ldh = cap+1], rotations, g, y, and scalar state st[].
@@ -218,19 +219,16 @@ enum : int { kGmBeta = 0, kGmJ = 1, kGmI = 2, kGmHappy = 3, kGmStalled = 4, kGmH
 void gm_init(double* sc, const GmDev& G, double target, double max_it, int cap, cudaStream_t s);
 void gm_start(double* sc, const GmDev& G, cudaGraphConditionalHandle h_cyc, cudaGraphConditionalHandle h_inner,
               cudaStream_t s);
-void gm_v0(const GmDev& G, const double* r, int64_t n, cudaStream_t s);
-void gm_copy(const GmDev& G, double* dst, int64_t n, cudaGraphConditionalHandle h_mgs, cudaStream_t s);
+/// V[0] = r / beta (and into u, the preconditioner input); arms the MGS loop
+void gm_v0(const GmDev& G, const double* r, double* u, int64_t n, cudaGraphConditionalHandle h_mgs, cudaStream_t s);
 void mgs_step(const GmDev& G, double* w, int64_t n, const Reduce& red, cudaGraphConditionalHandle h_mgs,
               cudaStream_t s);
+/// last MGS axpy, |w|, h(j+1) and the breakdown flag
 void mgs_tail(const GmDev& G, double* w, int64_t n, const Reduce& red, cudaStream_t s);
-/// All of Arnoldi column j's MGS, h(j+1), the happy flag and V[j+1] in one
-/// cooperative launch; part [2 * grid] doubles, bar [1] zeroed. False when
-/// the vector is too long for the register slices or co-residency fails.
-int mgs_coop_grid();
-bool mgs_coop(const GmDev& G, const double* w, int64_t n, double* part, unsigned* bar, cudaStream_t s);
-void gm_arnoldi_close(double* sc, const GmDev& G, const double* w, int64_t n, cudaGraphConditionalHandle h_inner,
-                      cudaStream_t s);
-void gm_givens(double* sc, const GmDev& G, cudaGraphConditionalHandle h_inner, cudaStream_t s);
+/// V[j+1] = w / h(j+1) (and into u), then the Givens step and the loop
+/// decisions (h_inner; re-arms h_mgs for the next column)
+void gm_arnoldi_close(double* sc, const GmDev& G, const double* w, double* u, int64_t n, const Reduce& red,
+                      cudaGraphConditionalHandle h_inner, cudaGraphConditionalHandle h_mgs, cudaStream_t s);
 void gm_update(const GmDev& G, double* u, int64_t n, cudaStream_t s);
 void gm_end(double* sc, const GmDev& G, cudaStream_t s);
 /// y = a * x + b * y with device scalars sc[ia] (or 1 if ia < 0), factor fa
