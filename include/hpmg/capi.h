@@ -315,6 +315,9 @@ int hpmg_profile_levels(hpmg_ctx* ctx, int reps, double* out);
 double hpmg_debug_loop_probe(hpmg_ctx* ctx, int mode, int iters);
 /* Development hook: clock64 timeline of the one-CTA small-level sweep. */
 void hpmg_debug_small_trace(int arm, long long* out);
+/* development: (kernel id, step, globaltimer) at the start of the GMRES loop's
+ * Gram-Schmidt / tail / new-vector kernels; out[0] = count, then triples */
+void hpmg_debug_gm_trace(int arm, long long* out);
 /* development: per-CTA globaltimer stamps of the last wave-sweep launches (HPMG_DBG=4) */
 void hpmg_debug_sweep_trace(long long* out);
 double hpmg_setup_seconds(const hpmg_ctx* ctx, double* parts);

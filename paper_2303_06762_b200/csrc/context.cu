@@ -1007,7 +1007,8 @@ void gm_workspace(hpmg_ctx& C, int cap) {
   C.gm.sn = dalloc<double>(cap);
   C.gm.g = dalloc<double>(cap + 1);
   C.gm.y = dalloc<double>(cap);
-  if (!C.gm.st) C.gm.st = dalloc<double>(8);
+  if (!C.gm.st) C.gm.st = dalloc<double>(dev::kGmSlots);
+  if (!C.gm.part) C.gm.part = dalloc<double>(2 * size_t(dev::kRedBlocks));
   C.gm_cap = cap;
   if (C.gm_loop) cudaGraphExecDestroy(C.gm_loop);
   C.gm_loop = nullptr;
@@ -1056,11 +1057,11 @@ bool build_gm_loop(hpmg_ctx& C) {
           apply_blocks(C, C.kr, C.kz);                                  // z = M v_j
           dev::spmv(T.A, C.kz, nullptr, C.ktmp, 0, nullptr, nullptr, C.s);  // w = A z
           cudaGraph_t mgs = add_conditional(C.s, h_mgs, cudaGraphCondTypeWhile);
-          // four MGS steps per loop-body iteration (steps past j return at once)
+          // eight MGS steps per loop-body iteration (steps past j return at once)
           capture_body(C, mgs, 3, [&] {
-            for (int u = 0; u < 4; ++u) dev::mgs_step(G, C.ktmp, n, C.red, h_mgs, C.s);
+            for (int u = 0; u < 8; ++u) dev::mgs_step(G, C.ktmp, n, u, h_mgs, C.s);
           });
-          dev::mgs_tail(G, C.ktmp, n, C.red, C.s);
+          dev::mgs_tail(G, C.ktmp, n, C.s);
           dev::gm_arnoldi_close(C.sc, G, C.ktmp, C.kr, n, C.red, h_inner, h_mgs, C.s);
         });
         dev::gm_update(G, C.kr, n, C.s);  // u = V y into the preconditioner's input
@@ -1581,7 +1582,7 @@ void hpmg_destroy(hpmg_ctx* ctx) {
   for (cudaStream_t q : ctx->s_nest)
     if (q) cudaStreamDestroy(q);
   for (void* p : {(void*)ctx->gm.V, (void*)ctx->gm.H, (void*)ctx->gm.cs, (void*)ctx->gm.sn, (void*)ctx->gm.g,
-                  (void*)ctx->gm.y, (void*)ctx->gm.st})
+                  (void*)ctx->gm.y, (void*)ctx->gm.st, (void*)ctx->gm.part})
     if (p) dfree(p);
   auto fr = [](void* p) { if (p) dfree(p); };
   auto free_level = [&](Level* V) {
@@ -2236,6 +2237,7 @@ int hpmg_kernel_launches_per_apply(const hpmg_ctx* ctx) { return ctx->launches_p
 /// Development hook: arm (1) / disarm (0) the one-CTA sweep timeline and copy
 /// it out (4096 clock64 stamps: per pass start, data ready, residual done, end).
 void hpmg_debug_small_trace(int arm, long long* out) { dev::small_trace(arm, out); }
+void hpmg_debug_gm_trace(int arm, long long* out) { dev::gm_trace(arm, out); }
 void hpmg_debug_sweep_trace(long long* out) { dev::sweep_trace(out); }
 
 /// Event-instrumented V-cycle (no graph): out[2l], out[2l+1] = pre/post part
@@ -2252,7 +2254,9 @@ double hpmg_debug_loop_probe(hpmg_ctx* ctx, int mode, int iters) {
       GK(cudaGraphCreate(&g, 0));
       cudaGraphConditionalHandle h, hi = 0;
       GK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
-      if (mode == 2) GK(cudaGraphConditionalHandleCreate(&hi, g, 1, cudaGraphCondAssignDefault));
+      const int pm = mode >= 32 ? mode - 32 : -1;  // PCG-shaped body, parts by bit
+      if (mode == 2 || (pm >= 0 && (pm & 4)))
+        GK(cudaGraphConditionalHandleCreate(&hi, g, (pm >= 0 && (pm & 2)) ? 0 : 1, cudaGraphCondAssignDefault));
       cudaGraphNodeParams wp = {};
       wp.type = cudaGraphNodeTypeConditional;
       wp.conditional.handle = h;
@@ -2280,6 +2284,23 @@ double hpmg_debug_loop_probe(hpmg_ctx* ctx, int mode, int iters) {
           GK(cudaStreamUpdateCaptureDependencies(C.s, &cn, 1, cudaStreamSetCaptureDependencies));
           cudaGraphDestroy(child);
         }
+        if (pm >= 0) {
+          const int64_t n = C.top().n;
+          if (pm & 1) dev::spmv(C.top().A, C.kp, nullptr, C.kAp, 0, &C.red, C.sc + S_PAP, C.s);
+          if (pm & 2) dev::pcg_loop_update(C.kx, C.kr, C.kp, C.kAp, n, C.sc, C.red, hi ? hi : h, h, C.s);
+          auto branch = [&] {
+            apply_blocks(C, C.kr, C.kz);
+            if (pm & 8) dev::pcg_loop_rz(C.kr, C.kz, n, C.sc, C.red, h, C.s);
+            if (pm & 16) dev::pcg_loop_direction(C.kp, C.kz, n, C.sc, C.s);
+          };
+          if (pm & 4) {
+            cudaGraph_t br = add_conditional(C.s, hi, cudaGraphCondTypeIf);
+            capture_body(C, br, 1, branch);
+          } else {
+            if (pm & 8) dev::pcg_loop_rz(C.kr, C.kz, n, C.sc, C.red, h, C.s);
+            if (pm & 16) dev::pcg_loop_direction(C.kp, C.kz, n, C.sc, C.s);
+          }
+        }
         dev::loop_countdown(c, h, C.s);
       });
       GK(cudaGraphInstantiate(&ge, g, 0));
@@ -2290,6 +2311,15 @@ double hpmg_debug_loop_probe(hpmg_ctx* ctx, int mode, int iters) {
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
+    if (mode >= 32) {  // a live PCG state: r = b, p = z = M r, target 0
+      const int64_t nn = C.top().n;
+      dev::copy(C.kr, C.kb, nn, C.s);
+      dev::fill(C.kx, 0.0, nn, C.s);
+      apply_blocks(C, C.kr, C.kz);
+      dev::copy(C.kp, C.kz, nn, C.s);
+      dev::dot(C.kr, C.kz, nn, C.red, C.sc + dev::kScRZ, C.s);
+      dev::pcg_loop_init(C.sc, 0.0, 1e9, C.s);
+    }
     const double warm = 3.0, n = double(iters);
     CK(cudaMemcpyAsync(c, &warm, sizeof(double), cudaMemcpyHostToDevice, C.s));
     CK(cudaGraphLaunch(ge, C.s));

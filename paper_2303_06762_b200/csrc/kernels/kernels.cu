@@ -108,6 +108,20 @@ __device__ void finalize_then(double v, Reduce red, double* out, Epi epi) {
   }
 }
 
+/// Grid of a fixed-grid (reduction) kernel: kRedBlocks CTAs of 256 threads,
+/// or fewer when the kernel's registers allow fewer than 8 CTAs per SM, so
+/// that every CTA is resident at once (no tail wave of leftover CTAs).
+/// Fixed per kernel, so reductions stay deterministic.
+template <class K>
+int resident_grid(K kernel) {
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, 256, 0);
+  const int g = sms * (per > 0 ? per : 1);
+  return g < kRedBlocks ? g : kRedBlocks;
+}
+
 inline int grid_for(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;
   if (g < 1) g = 1;
@@ -1215,64 +1229,150 @@ __global__ void k_gm_v0(GmDev G, const double* r, double* u, int64_t n,  // r ma
     cudaGraphSetConditional(h_mgs, 1u);
   }
 }
-/// MGS step i of column j (krylov.hpp:100-103), the axpy of step i-1 fused
-/// with the dot of step i: w -= h(i-1) v(i-1); h(i) = w . v(i)
-__global__ void k_mgs(GmDev G, double* __restrict__ w, int64_t n, Reduce red, cudaGraphConditionalHandle h_mgs) {
-  const int i = int(G.st[kGmI]), j = int(G.st[kGmJ]);
-  if (i > j) return;  // several steps per loop-body iteration: the surplus ones are no-ops
-  double* hcol = G.H + int64_t(j) * G.ldh;
-  const double* vi = G.V + int64_t(i) * G.ldv;
-  double s = 0.0;
-  if (i > 0) {
-    const double hp = hcol[i - 1];
-    const double* vp = G.V + int64_t(i - 1) * G.ldv;
-    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
-      const double wt = w[t] - hp * vp[t];
-      w[t] = wt;
-      s = fma(wt, vi[t], s);
-    }
-  } else {
-    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x)
-      s = fma(w[t], vi[t], s);
-  }
-  __shared__ bool last;
-  s = block_reduce<false>(s);
-  if (threadIdx.x == 0) {
-    red.partial[blockIdx.x] = s;
-    __threadfence();
-    last = atomicAdd(red.counter, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (last) {
-    __threadfence();
-    double a = 0.0;
-    for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x) a += __ldcg(&red.partial[b]);
-    a = block_reduce<false>(a);
-    if (threadIdx.x == 0) {
-      hcol[i] = a;
-      *red.counter = 0u;
-      G.st[kGmI] = double(i + 1);
-      cudaGraphSetConditional(h_mgs, i + 1 <= j ? 1u : 0u);
-    }
-  }
+// development timeline of the GMRES loop kernels (off unless gm_trace arms it):
+// (kernel id, step, globaltimer) at the start of CTA 0
+__device__ int d_gmt_on = 0;
+__device__ unsigned d_gmt_n = 0;
+__device__ long long d_gmt[3 * 8192];
+__device__ long long d_gmt_end[8192];  // CTA 0's end time of that kernel
+__device__ __forceinline__ long long gm_now() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
-/// last axpy of column j and |w|^2; the last block then stores
-/// h(j+1) = |w| into H and the breakdown flag (krylov.hpp:104-106)
-__global__ void k_mgs_tail(GmDev G, double* __restrict__ w, int64_t n, Reduce red) {
-  const int j = int(G.st[kGmJ]);
-  const double hp = G.H[int64_t(j) * G.ldh + j];
-  const double* vp = G.V + int64_t(j) * G.ldv;
-  double s = 0.0;
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
-    const double wt = w[t] - hp * vp[t];
-    w[t] = wt;
-    s = fma(wt, wt, s);
+__device__ __forceinline__ int gm_stamp(int id, int step) {
+  if (d_gmt_on && blockIdx.x == 0 && threadIdx.x == 0) {
+    const long long t = gm_now();
+    const unsigned k = atomicAdd(&d_gmt_n, 1u);
+    if (k < 8192) {
+      d_gmt[3 * k] = id;
+      d_gmt[3 * k + 1] = step;
+      d_gmt[3 * k + 2] = t;
+      return int(k);
+    }
   }
-  finalize_then(s, red, G.st + kGmHn, [&](double hn) {
-    const double h = sqrt(hn);
-    G.H[int64_t(j) * G.ldh + j + 1] = h;
-    G.st[kGmHappy] = h <= 1e-14 * G.st[kGmBeta] ? 1.0 : 0.0;
-  });
+  return -1;
+}
+__device__ __forceinline__ void gm_stamp_end(int k) {
+  if (k >= 0) d_gmt_end[k] = gm_now();
+}
+
+/// Sum of the previous kernel's per-CTA partials part[0..np), in the same
+/// fixed order in every CTA (so every CTA holds the bitwise-same value). This
+/// replaces the atomic-ticket last-CTA reduction on a dependent chain: the
+/// kernel boundary is the only synchronisation, and the L2 reads overlap the
+/// vector loads issued before the call.
+__device__ double sum_partials(const double* __restrict__ part, int np) {
+  __shared__ double total;
+  double a = 0.0;
+  for (int b = threadIdx.x; b < np; b += blockDim.x) a += __ldcg(part + b);
+  a = block_reduce<false>(a);
+  if (threadIdx.x == 0) total = a;
+  __syncthreads();
+  return total;
+}
+
+constexpr int kMgsU = 4;  // vector elements per thread per pass, loads issued together
+
+/// MGS step i of column j (krylov.hpp:100-103), the axpy of step i-1 fused
+/// with the dot of step i: w -= h(i-1) v(i-1); partial of w . v(i).
+/// h(i-1) is the sum of step i-1's partials (G.part, parity i-1), taken by
+/// every CTA; CTA 0 stores it into H. Eight steps per loop body (u = 0..7):
+/// steps 0-3 read their base index from st[kGmI], steps 4-7 from st[kGmI2];
+/// step 1 writes the second base and step 5 the first one for the next body,
+/// so no kernel writes a slot that its own CTAs read.
+__global__ void k_mgs(GmDev G, double* __restrict__ w, int64_t n, int u, cudaGraphConditionalHandle h_mgs) {
+  const int base = int(G.st[u < 4 ? kGmI : kGmI2]);
+  const int i = base + (u & 3), j = int(G.st[kGmJ]);
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  const int slot = gm_stamp(i > j ? 2 : 1, i);
+  if (lead && (u & 3) == 1) G.st[u < 4 ? kGmI2 : kGmI] = double(base + 4);
+  if (i > j) {  // past the column's last step: no-op
+    if (lead) cudaGraphSetConditional(h_mgs, 0u);
+    return;
+  }
+  const double* vi = G.V + int64_t(i) * G.ldv;
+  const double* vp = G.V + int64_t(i > 0 ? i - 1 : 0) * G.ldv;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  double wv[kMgsU], pv[kMgsU], iv[kMgsU];
+  auto load = [&](int64_t t0) {
+#pragma unroll
+    for (int q = 0; q < kMgsU; ++q) {
+      const int64_t t = t0 + q * stride;
+      if (t < n) {
+        wv[q] = w[t];
+        iv[q] = vi[t];
+        pv[q] = i > 0 ? vp[t] : 0.0;
+      }
+    }
+  };
+  int64_t t0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  load(t0);  // in flight while the previous step's partials are summed
+  double hp = 0.0;
+  if (i > 0) {
+    hp = sum_partials(G.part + ((i - 1) & 1) * kRedBlocks, gridDim.x);
+    if (lead) G.H[int64_t(j) * G.ldh + i - 1] = hp;
+  }
+  double s = 0.0;
+  for (;;) {
+#pragma unroll
+    for (int q = 0; q < kMgsU; ++q) {
+      const int64_t t = t0 + q * stride;
+      if (t < n) {
+        if (i > 0) {
+          wv[q] = fma(-hp, pv[q], wv[q]);
+          w[t] = wv[q];
+        }
+        s = fma(wv[q], iv[q], s);
+      }
+    }
+    t0 += kMgsU * stride;
+    if (t0 >= n) break;
+    load(t0);
+  }
+  s = block_reduce<false>(s);
+  if (threadIdx.x == 0) G.part[(i & 1) * kRedBlocks + blockIdx.x] = s;
+  if (lead) cudaGraphSetConditional(h_mgs, i + 1 <= j ? 1u : 0u);
+  gm_stamp_end(slot);
+}
+/// last axpy of column j (h(j) from step j's partials) and the partials of |w|^2
+__global__ void k_mgs_tail(GmDev G, double* __restrict__ w, int64_t n) {
+  const int j = int(G.st[kGmJ]);
+  gm_stamp(3, j);
+  const double* vp = G.V + int64_t(j) * G.ldv;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  double wv[kMgsU], pv[kMgsU];
+  auto load = [&](int64_t t0) {
+#pragma unroll
+    for (int q = 0; q < kMgsU; ++q) {
+      const int64_t t = t0 + q * stride;
+      if (t < n) {
+        wv[q] = w[t];
+        pv[q] = vp[t];
+      }
+    }
+  };
+  int64_t t0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  load(t0);
+  const double hp = sum_partials(G.part + (j & 1) * kRedBlocks, gridDim.x);
+  if (blockIdx.x == 0 && threadIdx.x == 0) G.H[int64_t(j) * G.ldh + j] = hp;
+  double s = 0.0;
+  for (;;) {
+#pragma unroll
+    for (int q = 0; q < kMgsU; ++q) {
+      const int64_t t = t0 + q * stride;
+      if (t < n) {
+        const double wt = fma(-hp, pv[q], wv[q]);
+        w[t] = wt;
+        s = fma(wt, wt, s);
+      }
+    }
+    t0 += kMgsU * stride;
+    if (t0 >= n) break;
+    load(t0);
+  }
+  s = block_reduce<false>(s);
+  if (threadIdx.x == 0) G.part[((j + 1) & 1) * kRedBlocks + blockIdx.x] = s;
 }
 /// Givens rotations of column j and the residual estimate (krylov.hpp:107-118);
 /// decides whether the Arnoldi loop continues. One thread.
@@ -1306,14 +1406,18 @@ __device__ void gm_givens_step(double* sc, GmDev G, cudaGraphConditionalHandle h
   }
   cudaGraphSetConditional(h_inner, more ? 1u : 0u);
 }
-/// V[j+1] = w / h(j+1), also into the preconditioner's input u (the next
-/// column's z = M v); the last block then runs the Givens step. Without a
-/// breakdown only: after one the loop ends and u is overwritten by gm_update.
+/// h(j+1) = |w| (the tail's partials, summed in every CTA), the breakdown
+/// test, V[j+1] = w / h(j+1), also into the preconditioner's input u (the next
+/// column's z = M v); the last CTA then stores h(j+1) and runs the Givens
+/// step. After a breakdown the loop ends and u is overwritten by gm_update.
 __global__ void k_gm_newv(double* sc, GmDev G, const double* __restrict__ w, double* __restrict__ u, int64_t n,
-                          unsigned* counter, cudaGraphConditionalHandle h_inner, cudaGraphConditionalHandle h_mgs) {
+                          int np, unsigned* counter, cudaGraphConditionalHandle h_inner,
+                          cudaGraphConditionalHandle h_mgs) {
   const int j = int(G.st[kGmJ]);
-  if (G.st[kGmHappy] == 0.0) {
-    const double h = G.H[int64_t(j) * G.ldh + j + 1];
+  gm_stamp(4, j);
+  const double h = sqrt(sum_partials(G.part + ((j + 1) & 1) * kRedBlocks, np));
+  const bool happy = h <= 1e-14 * G.st[kGmBeta];  // krylov.hpp:104-106
+  if (!happy) {
     double* v = G.V + int64_t(j + 1) * G.ldv;
     for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
       const double x = w[t] / h;
@@ -1322,7 +1426,7 @@ __global__ void k_gm_newv(double* sc, GmDev G, const double* __restrict__ w, dou
     }
   }
   __shared__ bool last;
-  __syncthreads();  // every thread has read st[J] and H before the last block's Givens step changes them
+  __syncthreads();  // every thread has read st[J] before the last CTA's Givens step changes it
   if (threadIdx.x == 0) {
     __threadfence();
     last = atomicAdd(counter, 1u) == gridDim.x - 1;
@@ -1331,6 +1435,9 @@ __global__ void k_gm_newv(double* sc, GmDev G, const double* __restrict__ w, dou
   if (last && threadIdx.x == 0) {
     __threadfence();
     *counter = 0u;
+    G.st[kGmHn] = h * h;
+    G.H[int64_t(j) * G.ldh + j + 1] = h;
+    G.st[kGmHappy] = happy ? 1.0 : 0.0;
     gm_givens_step(sc, G, h_inner, h_mgs);
   }
 }
@@ -1534,7 +1641,8 @@ void spmv(const Bsr& A, const double* x, const double* b, double* y, int minus, 
   const int64_t n = int64_t(A.nb) * A.bs;
   by_bs(A.bs, [&](auto BS) {
     if (red) {
-      k_spmv<BS><<<kRedBlocks, 256, 0, s>>>(A, x, b, y, minus, 1, *red, dot_out);
+      static const int grid = resident_grid(k_spmv<BS>);
+      k_spmv<BS><<<grid, 256, 0, s>>>(A, x, b, y, minus, 1, *red, dot_out);
     } else {
       k_spmv<BS><<<grid_for(n, 256), 256, 0, s>>>(A, x, b, y, minus, 0, Reduce{}, nullptr);
     }
@@ -1761,18 +1869,32 @@ void gm_v0(const GmDev& G, const double* r, double* u, int64_t n, cudaGraphCondi
   k_gm_v0<<<grid_for(n, 256), 256, 0, s>>>(G, r, u, n, h_mgs);
   HPMG_LAUNCH_CHECK();
 }
-void mgs_step(const GmDev& G, double* w, int64_t n, const Reduce& red, cudaGraphConditionalHandle h_mgs,
-              cudaStream_t s) {
-  k_mgs<<<kRedBlocks, 256, 0, s>>>(G, w, n, red, h_mgs);
+void gm_trace(int arm, long long* out) {
+  const unsigned zero = 0;
+  if (arm) cudaMemcpyToSymbol(d_gmt_n, &zero, sizeof(unsigned));
+  cudaMemcpyToSymbol(d_gmt_on, &arm, sizeof(int));
+  if (out) {
+    unsigned k = 0;
+    cudaMemcpyFromSymbol(&k, d_gmt_n, sizeof(unsigned));
+    k = k < 8192 ? k : 8192;
+    out[0] = k;
+    cudaMemcpyFromSymbol(out + 1, d_gmt, sizeof(long long) * 3 * k);
+    cudaMemcpyFromSymbol(out + 1 + 3 * 8192, d_gmt_end, sizeof(long long) * k);
+  }
+}
+constexpr int kMgsGrid = kRedBlocks;  // the MGS kernels' grid = their partial count
+void mgs_step(const GmDev& G, double* w, int64_t n, int u, cudaGraphConditionalHandle h_mgs, cudaStream_t s) {
+  k_mgs<<<kMgsGrid, 256, 0, s>>>(G, w, n, u, h_mgs);
   HPMG_LAUNCH_CHECK();
 }
-void mgs_tail(const GmDev& G, double* w, int64_t n, const Reduce& red, cudaStream_t s) {
-  k_mgs_tail<<<kRedBlocks, 256, 0, s>>>(G, w, n, red);
+void mgs_tail(const GmDev& G, double* w, int64_t n, cudaStream_t s) {
+  k_mgs_tail<<<kMgsGrid, 256, 0, s>>>(G, w, n);
   HPMG_LAUNCH_CHECK();
 }
 void gm_arnoldi_close(double* sc, const GmDev& G, const double* w, double* u, int64_t n, const Reduce& red,
                       cudaGraphConditionalHandle h_inner, cudaGraphConditionalHandle h_mgs, cudaStream_t s) {
-  k_gm_newv<<<kRedBlocks, 256, 0, s>>>(sc, G, w, u, n, red.counter, h_inner, h_mgs);
+  static const int grid = resident_grid(k_gm_newv);
+  k_gm_newv<<<grid, 256, 0, s>>>(sc, G, w, u, n, kMgsGrid, red.counter, h_inner, h_mgs);
   HPMG_LAUNCH_CHECK();
 }
 void gm_update(const GmDev& G, double* u, int64_t n, cudaStream_t s) {

@@ -115,7 +115,8 @@ void jacobi_combine(int nb, int bs, const Patches& P, const double* d, int max_n
 /// inside one wave, in forward sweep order.
 struct PatchRecords;
 int small_pass_patches();
-void small_trace(int arm, long long* out);  // development timeline (clock64 per pass phase)
+void small_trace(int arm, long long* out);
+void gm_trace(int arm, long long* out);  // development timeline of the GMRES loop kernels  // development timeline (clock64 per pass phase)
 bool small_level_fits(int nb, int record_stride, int npass);
 void small_pre(const Bsr& A, const PatchRecords& R, const int2* passes, int npass, int sweeps, const BlockCsr& PT,
                const double* b, double* x, double* r, double* rc, cudaStream_t s);
@@ -214,19 +215,21 @@ struct GmDev {
   double* H = nullptr;
   int ldh = 0;
   double *cs = nullptr, *sn = nullptr, *g = nullptr, *y = nullptr, *st = nullptr;
+  double* part = nullptr;  // [2][kRedBlocks] per-CTA partials of the Gram-Schmidt steps (parity of the step)
 };
-enum : int { kGmBeta = 0, kGmJ = 1, kGmI = 2, kGmHappy = 3, kGmStalled = 4, kGmHn = 5, kGmCap = 6, kGmM = 7 };
+enum : int { kGmBeta = 0, kGmJ = 1, kGmI = 2, kGmHappy = 3, kGmStalled = 4, kGmHn = 5, kGmCap = 6, kGmM = 7,
+             kGmI2 = 8, kGmSlots = 16 };
 void gm_init(double* sc, const GmDev& G, double target, double max_it, int cap, cudaStream_t s);
 void gm_start(double* sc, const GmDev& G, cudaGraphConditionalHandle h_cyc, cudaGraphConditionalHandle h_inner,
               cudaStream_t s);
 /// V[0] = r / beta (and into u, the preconditioner input); arms the MGS loop
 void gm_v0(const GmDev& G, const double* r, double* u, int64_t n, cudaGraphConditionalHandle h_mgs, cudaStream_t s);
-void mgs_step(const GmDev& G, double* w, int64_t n, const Reduce& red, cudaGraphConditionalHandle h_mgs,
-              cudaStream_t s);
-/// last MGS axpy, |w|, h(j+1) and the breakdown flag
-void mgs_tail(const GmDev& G, double* w, int64_t n, const Reduce& red, cudaStream_t s);
-/// V[j+1] = w / h(j+1) (and into u), then the Givens step and the loop
-/// decisions (h_inner; re-arms h_mgs for the next column)
+/// MGS step u (0..7) of a loop body of eight
+void mgs_step(const GmDev& G, double* w, int64_t n, int u, cudaGraphConditionalHandle h_mgs, cudaStream_t s);
+/// last MGS axpy and the partials of |w|^2
+void mgs_tail(const GmDev& G, double* w, int64_t n, cudaStream_t s);
+/// h(j+1), the breakdown test, V[j+1] = w / h(j+1) (and into u), then the
+/// Givens step and the loop decisions (h_inner; re-arms h_mgs for the next column)
 void gm_arnoldi_close(double* sc, const GmDev& G, const double* w, double* u, int64_t n, const Reduce& red,
                       cudaGraphConditionalHandle h_inner, cudaGraphConditionalHandle h_mgs, cudaStream_t s);
 void gm_update(const GmDev& G, double* u, int64_t n, cudaStream_t s);

@@ -16,10 +16,17 @@ B = H.MGPreconditioner(**R.device_kwargs(name))
 L = H.lib()
 L.hpmg_debug_loop_probe.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
 L.hpmg_debug_loop_probe.restype = ctypes.c_double
+if B.symmetric():
+    H.pcg(B, B.rhs(), opt=H.KrylovOptions(max_iterations=1))  # b into the solver's workspace
 out = {"config": name, "graph_vcycle_ms": B.time_apply(30)[0]}
 for mode, label in [(0, "empty_while_ms"), (1, "while_vcycle_ms"), (2, "while_if_vcycle_ms"),
                     (3, "while_child_vcycle_ms")]:
     out[label] = L.hpmg_debug_loop_probe(B.h, mode, 200 if mode == 0 else 30)
+if B.symmetric():
+    # PCG-shaped bodies (32 + bits: 1 spmv+pAp, 2 update, 4 if{V-cycle}, 8 rz, 16 direction)
+    for mode, label in [(63, "pcg_full"), (62, "pcg_no_spmv"), (61, "pcg_no_update"), (59, "pcg_no_vcycle_if"),
+                        (55, "pcg_no_rz"), (47, "pcg_no_direction"), (36, "pcg_if_vcycle_only")]:
+        out[label] = L.hpmg_debug_loop_probe(B.h, mode, 25)
 out["graph_vcycle_ms_2"] = B.time_apply(30)[0]
 print(json.dumps({k: (round(v, 5) if isinstance(v, float) else v) for k, v in out.items()}))
 if out["empty_while_ms"] < 0:
