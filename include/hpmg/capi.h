@@ -335,7 +335,9 @@ int hpmg_structured_to_elements(const hpmg_ctx* ctx, int n, const double* struct
  * lies in exactly two patches (smoother.hpp:13-28), out[4] 1 if no two
  * patches of a wave share a facet or an operator coupling, out[5] 1 if the
  * waves respect every ascending-order dependency, out[6] max patch facets,
- * out[7..7+waves) wave sizes (up to out_len). Returns entries written. */
+ * out[7..7+waves) wave sizes of the device schedule (balanced levelling),
+ * out[7+waves..7+2*waves) the as-soon-as-possible wave sizes
+ * (up to out_len). Returns entries written. */
 int hpmg_plan_check(const hpmg_mesh_desc* mesh, int k, int level, int64_t* out, int out_len);
 
 /* Base meshes of the reference (mesh.hpp:220-279): fills a descriptor whose

@@ -2616,6 +2616,7 @@ int hpmg_plan_check(const hpmg_mesh_desc* md, int k, int level, int64_t* out, in
     int w = 0;
     for (; w < 7 && w < out_len; ++w) out[w] = vals[w];
     for (int i = 0; i < P.nwaves() && w < out_len; ++i, ++w) out[w] = P.wave_ptr[i + 1] - P.wave_ptr[i];
+    for (int i = 0; i < P.nwaves() && w < out_len; ++i, ++w) out[w] = P.asap_sizes[i];
     return w;
   } catch (const std::exception& e) {
     g_last_error = e.what();

@@ -28,6 +28,7 @@ namespace host {
 
 constexpr int kSlots = 5;      // self + 4 neighbours: a facet touches <= 2 triangles
 constexpr int kMaxPatchF = 8;  // facets per vertex patch supported by the kernels
+constexpr int kSmallPass = 24; // patches per pass of the one-CTA level kernel (small_levels.cu kPass)
 
 using Field = std::function<void(double x, double y, double* out2)>;
 
@@ -115,10 +116,9 @@ struct LevelPlan {
   int64_t inv_total = 0;              // doubles stored
   int64_t inv_full_total = 0;         // sum np^2 (reference storage accounting)
   bool packed = true;
-  std::vector<int> wave_ptr, wave_patch;  // forward wave order
+  std::vector<int> wave_ptr, wave_patch;  // forward wave order (balanced, see make_level)
+  std::vector<int> asap_sizes;        // wave sizes of the as-soon-as-possible levelling
   std::vector<int> facet_patches;     // [nb][2] the two patches holding a block, ascending
-  // dataflow sweep: patches of the mesh neighbours of each patch's vertex
-  // (renumbered ids; the forward sweep waits on the smaller, the reverse on the larger)
   int nwaves() const { return int(wave_ptr.size()) - 1; }
   int64_t n() const { return int64_t(nb) * bs; }
 };
@@ -250,9 +250,49 @@ inline LevelPlan make_level(const TriMesh& m, int k) {
     depth[v] = d;
     maxd = std::max(maxd, d);
   }
-  std::vector<std::vector<int>> waves(maxd + 1);
+  // Levelling. Any assignment with wave(u) < wave(v) for every coupled pair
+  // u < v reproduces the sequential sweep exactly (every patch reads the same
+  // x), so the as-soon-as-possible depths above fix only the wave count. On
+  // wide schedules (9 waves, multi-CTA launches) the depths are used as they
+  // are: re-levelling the 256^2 head towards even waves measured slower on
+  // B200 (head sweeps 0.203 -> 0.208 ms). On narrow ones (> 12 waves: the
+  // one-CTA level) every wave is capped at one pass of that kernel
+  // (kSmallPass patches), placing patches from the last vertex down in the
+  // latest wave of [depth, earliest successor wave - 1] below the cap: level
+  // 1 of a 16x16 base goes from 66 to 50 passes per sweep.
+  const int nw = maxd + 1;
+  L.asap_sizes.assign(nw, 0);
   for (int v = 0; v < m.nv(); ++v)
-    if (vertex_patch[v] >= 0) waves[depth[v]].push_back(vertex_patch[v]);
+    if (vertex_patch[v] >= 0) L.asap_sizes[depth[v]]++;
+  const bool narrow = nw > 12;
+  const int cap = kSmallPass;
+  // narrow: placement in descending vertex order (successors first), latest
+  // wave of [depth, earliest successor wave - 1] below the cap, else the least loaded
+  std::vector<int> wave_of_v(m.nv(), -1), load(nw, 0);
+  for (int v = m.nv() - 1; v >= 0; --v) {
+    if (vertex_patch[v] < 0) continue;
+    int w = depth[v];
+    if (narrow) {
+      int hi = maxd;
+      for (const int* up = nbr.begin(v); up != nbr.end(v); ++up)
+        if (*up > v && vertex_patch[*up] >= 0) hi = std::min(hi, wave_of_v[*up] - 1);
+      const int lo = depth[v];
+      if (lo > hi) throw std::logic_error("wave levelling: empty placement range");
+      w = -1;
+      for (int c = hi; c >= lo && w < 0; --c)
+        if (load[c] < cap) w = c;
+      if (w < 0) {
+        w = hi;
+        for (int c = hi - 1; c >= lo; --c)
+          if (load[c] < load[w]) w = c;
+      }
+    }
+    wave_of_v[v] = w;
+    load[w]++;
+  }
+  std::vector<std::vector<int>> waves(nw);
+  for (int v = 0; v < m.nv(); ++v)
+    if (vertex_patch[v] >= 0) waves[wave_of_v[v]].push_back(vertex_patch[v]);
   L.wave_ptr.push_back(0);
   for (auto& w : waves) {
     for (int p : w) L.wave_patch.push_back(p);

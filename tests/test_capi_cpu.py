@@ -35,8 +35,10 @@ def plan(base_n, levels, k, level=-1, mesh="unit_square"):
     L.hpmg_plan_check.argtypes = [C.POINTER(H._Mesh), C.c_int, C.c_int, C.POINTER(C.c_int64), C.c_int]
     n = L.hpmg_plan_check(C.byref(md), k, level, out.ctypes.data_as(C.POINTER(C.c_int64)), 128)
     assert n > 0, L.hpmg_last_error().decode()
-    return dict(n=int(out[0]), patches=int(out[1]), waves=int(out[2]), cover=bool(out[3]), indep=bool(out[4]),
-                order=bool(out[5]), max_nf=int(out[6]), sizes=[int(v) for v in out[7:n]])
+    nw = int(out[2])
+    return dict(n=int(out[0]), patches=int(out[1]), waves=nw, cover=bool(out[3]), indep=bool(out[4]),
+                order=bool(out[5]), max_nf=int(out[6]), sizes=[int(v) for v in out[7:7 + nw]],
+                asap=[int(v) for v in out[7 + nw:7 + 2 * nw]])
 
 
 @pytest.mark.parametrize("base_n,levels,k,n_expect", [
@@ -52,13 +54,15 @@ def test_config_sizes_and_wave_schedule(base_n, levels, k, n_expect):
     assert p["n"] == n_expect
     assert p["cover"] and p["indep"] and p["order"]
     assert p["waves"] == 9  # exact parallel schedule of the ascending sweep on refined levels
-    assert sum(p["sizes"]) == p["patches"]
+    assert sum(p["sizes"]) == p["patches"] == sum(p["asap"])
+    assert p["sizes"] == p["asap"]  # wide schedules keep the as-soon-as-possible levelling
 
 
 def test_wave_sizes_match_survey_appendix_b():
     # 256^2 mesh from an 8x8 base
     p = plan(8, 6, 0, level=5)
-    assert p["sizes"] == [16639, 8376, 10511, 11415, 7128, 5576, 3936, 1521, 945]
+    assert p["asap"] == [16639, 8376, 10511, 11415, 7128, 5576, 3936, 1521, 945]
+    assert p["sizes"] == p["asap"] and p["indep"] and p["order"]
 
 
 @pytest.mark.parametrize("base_n,levels,level,waves", [(8, 5, 1, 26), (16, 5, 1, 50), (8, 5, 2, 9)])
@@ -66,6 +70,8 @@ def test_coarse_level_wave_counts(base_n, levels, level, waves):
     # 26 waves on level 1 of an 8x8 base, 50 for 16x16, then 9
     p = plan(base_n, levels, 0, level=level)
     assert p["waves"] == waves and p["indep"] and p["order"] and p["cover"]
+    if waves > 12:  # the one-CTA level: every wave fits one 24-patch pass (ASAP: 79 / 287 in wave 0)
+        assert max(p["sizes"]) <= 24 < max(p["asap"])
 
 
 def test_step_domain_plan():
