@@ -298,6 +298,9 @@ double hpmg_spmv_bytes(const hpmg_ctx* ctx);
  * already in the internal layout; returns ms per apply. phase_ms (optional,
  * 8 doubles) receives per-phase averages from an event-instrumented pass. */
 double hpmg_time_apply(hpmg_ctx* ctx, int reps, double* phase_ms);
+/* Kernels one hpmg_apply launches (its graph: reference-order input -> blocks
+ * with x = 0, the cycle, blocks -> reference order) once hpmg_apply has run;
+ * before that, the kernels of the cycle graph alone. */
 int hpmg_kernel_launches_per_apply(const hpmg_ctx* ctx);
 /* Device-resident timing of `reps` finest-operator applies (k_spmv, stream-ordered,
  * no graph); returns ms per spmv. bytes (optional, 2 doubles): [0] bytes one

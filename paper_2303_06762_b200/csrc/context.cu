@@ -215,11 +215,20 @@ struct hpmg_ctx {
   int fine_lstride = 0;
   CondenseParams fine_prm{};
   bool enclosed = true;
-  int launches_per_apply = 0;
+  int launches_per_apply = 0;      // kernels of the apply graph (z = M r on block-order kr / kz)
+  int io_launches = 0;             // kernels of the drop-in hpmg_apply's io graph
   bool counting = false;
   double setup_parts[8] = {0};
   // CUDA graph of apply(kr -> kz)
   cudaGraphExec_t apply_graph = nullptr;
+  // drop-in apply: reference-order input -> blocks (+ x = 0), the cycle,
+  // blocks -> reference order, one graph; the end nodes are re-pointed at the
+  // caller's device buffers (or the io staging buffers) per call
+  cudaGraph_t io_tmpl = nullptr;
+  cudaGraphExec_t io_graph = nullptr;
+  cudaGraphNode_t io_in = nullptr, io_out = nullptr;
+  const double* io_in_cur = nullptr;
+  double* io_out_cur = nullptr;
   // MG residual trace (MGOptions::trace, reference multigrid.hpp:18-33): set
   // only during hpmg_apply_trace, which runs the cycle outside the graph
   struct TraceEntry {
@@ -719,10 +728,10 @@ void h_cycle(hpmg_ctx& C, int l, const double* b, double* x) {
 }
 
 /// apply(b) -> x on the finest system, block layout (inc/multigrid.hpp:117-128)
-void apply_blocks(hpmg_ctx& C, const double* b, double* x) {
+void apply_blocks(hpmg_ctx& C, const double* b, double* x, bool x_zeroed = false) {
   if (C.opt.k == 0) {
-    if (C.L > 0 && !(C.lv[C.L]->small && C.opt.smoother == HPMG_SMOOTH_MULTIPLICATIVE &&
-                     C.opt.cycle != HPMG_CYCLE_W)) {
+    if (!x_zeroed && C.L > 0 && !(C.lv[C.L]->small && C.opt.smoother == HPMG_SMOOTH_MULTIPLICATIVE &&
+                                  C.opt.cycle != HPMG_CYCLE_W)) {
       dev::fill(x, 0.0, C.lv[C.L]->n, C.s);  // h_cycle expects x = 0 on entry (restriction zeroes it below)
       count(C);
     }
@@ -732,8 +741,10 @@ void apply_blocks(hpmg_ctx& C, const double* b, double* x) {
   Level& H = *C.head;
   Level& F = *C.lv[C.L];
   if (C.trace) trace_norm(C, C.L + 1, true, b, H.n);  // the head is reported one index above the finest mesh level
-  dev::fill(x, 0.0, H.n, C.s);
-  count(C);
+  if (!x_zeroed) {
+    dev::fill(x, 0.0, H.n, C.s);
+    count(C);
+  }
   smooth(C, H, x, b, false, true);
   dev::inject_residual(H.A, x, b, F.b, C.s, F.x);
   count(C);
@@ -757,6 +768,70 @@ void build_apply_graph(hpmg_ctx& C) {
 }
 
 void apply_graph(hpmg_ctx& C) { CK(cudaGraphLaunch(C.apply_graph, C.s)); }
+
+/// the node the last captured launch on s created
+cudaGraphNode_t last_captured(cudaStream_t s) {
+  cudaStreamCaptureStatus cs;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, nullptr, &deps, &ndeps));
+  if (ndeps != 1) throw std::runtime_error("io graph: unexpected capture fan-in");
+  return deps[0];
+}
+
+void destroy_io_graph(hpmg_ctx& C) {
+  if (C.io_graph) cudaGraphExecDestroy(C.io_graph);
+  if (C.io_tmpl) cudaGraphDestroy(C.io_tmpl);
+  C.io_graph = nullptr;
+  C.io_tmpl = nullptr;
+  C.io_in = C.io_out = nullptr;
+  C.io_in_cur = nullptr;
+  C.io_out_cur = nullptr;
+}
+
+void build_io_graph(hpmg_ctx& C) {
+  Level& T = C.top();
+  CK(cudaStreamBeginCapture(C.s, cudaStreamCaptureModeThreadLocal));
+  try {
+    dev::to_blocks_zero(T.nb, T.k + 1, C.io_a, C.kr, C.kz, C.s);
+    C.io_in = last_captured(C.s);
+    apply_blocks(C, C.kr, C.kz, true);
+    dev::to_reference(T.nb, T.k + 1, C.kz, C.io_b, C.s);
+    C.io_out = last_captured(C.s);
+  } catch (...) {
+    cudaGraph_t tmp;
+    cudaStreamEndCapture(C.s, &tmp);
+    if (tmp) cudaGraphDestroy(tmp);
+    throw;
+  }
+  CK(cudaStreamEndCapture(C.s, &C.io_tmpl));
+  CK(cudaGraphInstantiate(&C.io_graph, C.io_tmpl, 0));
+  size_t nn = 0;
+  CK(cudaGraphGetNodes(C.io_tmpl, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn);
+  CK(cudaGraphGetNodes(C.io_tmpl, nodes.data(), &nn));
+  C.io_launches = 0;
+  for (cudaGraphNode_t nd : nodes) {
+    cudaGraphNodeType ty;
+    CK(cudaGraphNodeGetType(nd, &ty));
+    C.io_launches += ty == cudaGraphNodeTypeKernel;
+  }
+  C.io_in_cur = C.io_a;
+  C.io_out_cur = C.io_b;
+}
+
+/// z = M r through the io graph; r / z on the device (stream-ordered) or the
+/// io staging buffers after / before the host copies
+void apply_io(hpmg_ctx& C, const double* r_dev, double* z_dev) {
+  if (!C.io_graph) build_io_graph(C);
+  if (r_dev != C.io_in_cur || z_dev != C.io_out_cur) {
+    Level& T = C.top();
+    dev::set_io_nodes(C.io_graph, C.io_in, C.io_out, T.nb, T.k + 1, r_dev, C.kr, C.kz, C.kz, z_dev);
+    C.io_in_cur = r_dev;
+    C.io_out_cur = z_dev;
+  }
+  CK(cudaGraphLaunch(C.io_graph, C.s));
+}
 
 void read_scalars(hpmg_ctx& C, int n) {
   CK(cudaMemcpyAsync(C.sc_host, C.sc, sizeof(double) * n, cudaMemcpyDeviceToHost, C.s));
@@ -1557,6 +1632,7 @@ int hpmg_update(hpmg_ctx* ctx, const hpmg_options* opt, const hpmg_problem* prob
     linearise(C, prob, Tk.get());
     if (C.apply_graph) cudaGraphExecDestroy(C.apply_graph);
     C.apply_graph = nullptr;
+    destroy_io_graph(C);
     if (C.pcg_loop) cudaGraphExecDestroy(C.pcg_loop);
     C.pcg_loop = nullptr;
     if (C.gm_loop) cudaGraphExecDestroy(C.gm_loop);
@@ -1576,6 +1652,7 @@ void hpmg_destroy(hpmg_ctx* ctx) {
   if (!ctx) return;
   cudaStreamSynchronize(ctx->s);
   if (ctx->apply_graph) cudaGraphExecDestroy(ctx->apply_graph);
+  destroy_io_graph(*ctx);
   if (ctx->pcg_loop) cudaGraphExecDestroy(ctx->pcg_loop);
   if (ctx->s_cap) cudaStreamDestroy(ctx->s_cap);
   if (ctx->gm_loop) cudaGraphExecDestroy(ctx->gm_loop);
@@ -1735,9 +1812,16 @@ int hpmg_spmv(hpmg_ctx* ctx, const double* x, double* y, int flags) {
 
 int hpmg_apply(hpmg_ctx* ctx, const double* r, double* z, int flags) {
   return guarded(ctx, [&] {
-    in_vec(*ctx, r, ctx->kr, flags);
-    apply_graph(*ctx);
-    out_vec(*ctx, ctx->kz, z, flags);
+    hpmg_ctx& C = *ctx;
+    const size_t bytes = sizeof(double) * C.top().n;
+    if (flags & HPMG_DEVICE_PTRS) {  // stream-ordered: the caller synchronises hpmg_stream(ctx) as needed
+      apply_io(C, r, z);
+      return;
+    }
+    CK(cudaMemcpyAsync(C.io_a, r, bytes, cudaMemcpyHostToDevice, C.s));
+    apply_io(C, C.io_a, C.io_b);
+    CK(cudaMemcpyAsync(z, C.io_b, bytes, cudaMemcpyDeviceToHost, C.s));
+    CK(cudaStreamSynchronize(C.s));
   });
 }
 
@@ -1795,13 +1879,11 @@ int hpmg_apply_batch(hpmg_ctx* ctx, int m, const double* const* r, double* const
       if (i >= 2) CK(cudaStreamWaitEvent(C.s_h2d, C.ev_used[j], 0));
       CK(cudaMemcpyAsync(C.bin[j], r[i], bytes, cudaMemcpyHostToDevice, C.s_h2d));
       CK(cudaEventRecord(C.ev_in[j], C.s_h2d));
-      // V-cycle i on the context stream
+      // V-cycle i on the context stream (the io graph: permutations + cycle)
       CK(cudaStreamWaitEvent(C.s, C.ev_in[j], 0));
-      dev::to_blocks(T.nb, T.k + 1, C.bin[j], C.kr, C.s);
-      CK(cudaEventRecord(C.ev_used[j], C.s));
-      apply_graph(C);
       if (i >= 2) CK(cudaStreamWaitEvent(C.s, C.ev_out[j], 0));  // D2H of result i-2 left bout[j]
-      dev::to_reference(T.nb, T.k + 1, C.kz, C.bout[j], C.s);
+      apply_io(C, C.bin[j], C.bout[j]);
+      CK(cudaEventRecord(C.ev_used[j], C.s));
       CK(cudaEventRecord(C.ev_done[j], C.s));
       // D2H of result i
       CK(cudaStreamWaitEvent(C.s_d2h, C.ev_done[j], 0));
@@ -2232,7 +2314,9 @@ double hpmg_time_apply(hpmg_ctx* ctx, int reps, double* phase_ms) {
   return ms_per;
 }
 
-int hpmg_kernel_launches_per_apply(const hpmg_ctx* ctx) { return ctx->launches_per_apply; }
+int hpmg_kernel_launches_per_apply(const hpmg_ctx* ctx) {
+  return ctx->io_launches > 0 ? ctx->io_launches : ctx->launches_per_apply;
+}
 
 /// Development hook: arm (1) / disarm (0) the one-CTA sweep timeline and copy
 /// it out (4096 clock64 stamps: per pass start, data ready, residual done, end).

@@ -1488,6 +1488,18 @@ __global__ void k_to_blocks(int nb, int nfd, const double* __restrict__ ref, dou
     blk[t] = ref[(tg ? int64_t(nb) * nfd : 0) + f * nfd + i];
   }
 }
+/// k_to_blocks that also zeroes `zero` (the cycle's x) in the same pass
+__global__ void k_to_blocks_zero(int nb, int nfd, const double* __restrict__ ref, double* __restrict__ blk,
+                                 double* __restrict__ zero) {
+  const int bs = 2 * nfd;
+  const int64_t n = int64_t(nb) * bs;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t f = t / bs;
+    const int ii = int(t % bs), i = ii >> 1, tg = ii & 1;
+    blk[t] = ref[(tg ? int64_t(nb) * nfd : 0) + f * nfd + i];
+    zero[t] = 0.0;
+  }
+}
 __global__ void k_to_reference(int nb, int nfd, const double* __restrict__ blk, double* __restrict__ ref) {
   const int bs = 2 * nfd;
   const int64_t n = int64_t(nb) * bs;
@@ -1944,6 +1956,34 @@ void scal_axpby(double* y, const double* x, int64_t n, const double* sc, int ia,
 void to_blocks(int nb, int nfd, const double* ref, double* blk, cudaStream_t s) {
   k_to_blocks<<<grid_for(int64_t(nb) * 2 * nfd, 256), 256, 0, s>>>(nb, nfd, ref, blk);
   HPMG_LAUNCH_CHECK();
+}
+void to_blocks_zero(int nb, int nfd, const double* ref, double* blk, double* zero, cudaStream_t s) {
+  k_to_blocks_zero<<<grid_for(int64_t(nb) * 2 * nfd, 256), 256, 0, s>>>(nb, nfd, ref, blk, zero);
+  HPMG_LAUNCH_CHECK();
+}
+void set_io_nodes(cudaGraphExec_t ge, cudaGraphNode_t in_node, cudaGraphNode_t out_node, int nb, int nfd,
+                  const double* ref_in, double* blk_in, double* zero, const double* blk_out, double* ref_out) {
+  const int grid = grid_for(int64_t(nb) * 2 * nfd, 256);
+  {
+    void* args[] = {&nb, &nfd, &ref_in, &blk_in, &zero};
+    cudaKernelNodeParams p = {};
+    p.func = reinterpret_cast<void*>(k_to_blocks_zero);
+    p.gridDim = dim3(grid);
+    p.blockDim = dim3(256);
+    p.kernelParams = args;
+    const cudaError_t e = cudaGraphExecKernelNodeSetParams(ge, in_node, &p);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("io graph input node: ") + cudaGetErrorString(e));
+  }
+  {
+    void* args[] = {&nb, &nfd, &blk_out, &ref_out};
+    cudaKernelNodeParams p = {};
+    p.func = reinterpret_cast<void*>(k_to_reference);
+    p.gridDim = dim3(grid);
+    p.blockDim = dim3(256);
+    p.kernelParams = args;
+    const cudaError_t e = cudaGraphExecKernelNodeSetParams(ge, out_node, &p);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("io graph output node: ") + cudaGetErrorString(e));
+  }
 }
 void to_reference(int nb, int nfd, const double* blk, double* ref, cudaStream_t s) {
   k_to_reference<<<grid_for(int64_t(nb) * 2 * nfd, 256), 256, 0, s>>>(nb, nfd, blk, ref);

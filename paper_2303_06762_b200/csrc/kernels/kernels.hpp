@@ -240,6 +240,11 @@ void scal_axpby(double* y, const double* x, int64_t n, const double* sc, int ia,
 // layout permutations between the reference free order and the block layout
 void to_blocks(int nb, int nfd, const double* ref, double* blk, cudaStream_t s);
 void to_reference(int nb, int nfd, const double* blk, double* ref, cudaStream_t s);
+/// to_blocks + zero[0..n) = 0 in one pass (the drop-in apply's first kernel)
+void to_blocks_zero(int nb, int nfd, const double* ref, double* blk, double* zero, cudaStream_t s);
+/// points the io graph's first (to_blocks_zero) and last (to_reference) kernel nodes at new buffers
+void set_io_nodes(cudaGraphExec_t ge, cudaGraphNode_t in_node, cudaGraphNode_t out_node, int nb, int nfd,
+                  const double* ref_in, double* blk_in, double* zero, const double* blk_out, double* ref_out);
 
 // augmented-Lagrangian Uzawa pieces (uzawa.hpp:69-82)
 void uzawa_rhs(int nb, int bs, const double* rhs0, const int* row_elems, const ElemGeo* geo, const double* p,
