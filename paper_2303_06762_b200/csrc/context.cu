@@ -137,6 +137,7 @@ struct Level {
   int k = 0, bs = 2, nb = 0;
   int64_t n = 0;
   dev::Bsr A, AT;
+  dev::Bsr A0;  // order-k head: the mode-0 rows of A's blocks, contiguous (cols shared with A)
   int* tslot = nullptr;
   dev::Patches P;
   int max_nf = 0;
@@ -473,6 +474,13 @@ void linearise_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, const DevRef
   dev::condense(R.T, V.geo, m.ne(), prm, dload, lstride, acr, s, dwind, dmass);
   dev::assemble_bsr(V.A, k + 1, acr, stride, nc, V.gath, V.geo, C.opt.inv_eps, s);
   if (C.advected) dev::transpose_bsr(V.A, V.tslot, V.AT, s);
+  if (k > 0) {  // the head residual's rows, streamed contiguously
+    if (!V.A0.val) V.A0.val = dalloc<double>(size_t(V.nb) * host::kSlots * 2 * V.bs);
+    V.A0.nb = V.A.nb;
+    V.A0.bs = V.A.bs;
+    V.A0.cols = V.A.cols;
+    dev::extract_mode0(V.A, V.A0, s);
+  }
   if (finest)
     dev::assemble_rhs(V.nb, V.bs, k + 1, V.row_elems, V.block_facet, V.elem_facets, C.facet_dir, C.g_fac, acr,
                       stride, nc, V.geo, C.opt.inv_eps, rhs_out, s);
@@ -746,7 +754,7 @@ void apply_blocks(hpmg_ctx& C, const double* b, double* x, bool x_zeroed = false
     count(C);
   }
   smooth(C, H, x, b, false, true);
-  dev::inject_residual(H.A, x, b, F.b, C.s, F.x);
+  dev::inject_residual(H.A0, x, b, F.b, C.s, F.x);
   count(C);
   h_cycle(C, C.L, F.b, F.x);
   dev::embed_add(H.nb, H.bs, F.x, x, C.s);
@@ -1664,7 +1672,7 @@ void hpmg_destroy(hpmg_ctx* ctx) {
   auto fr = [](void* p) { if (p) dfree(p); };
   auto free_level = [&](Level* V) {
     if (!V) return;
-    for (void* p : {(void*)V->A.val, (void*)V->A.cols, (void*)V->AT.val, (void*)V->tslot, (void*)V->P.nf,
+    for (void* p : {(void*)V->A.val, (void*)V->A.cols, (void*)V->A0.val, (void*)V->AT.val, (void*)V->tslot, (void*)V->P.nf,
                     (void*)V->P.fac, (void*)V->P.off, (void*)V->P.inv, (void*)V->P.wave, (void*)V->P.fpatch,
                     (void*)V->Pm.ptr, (void*)V->Pm.col, (void*)V->Pm.val, (void*)V->PT.ptr, (void*)V->PT.col,
                     (void*)V->PT.val, (void*)V->x, (void*)V->b, (void*)V->r, (void*)V->y, (void*)V->bw, (void*)V->xw,
@@ -2287,7 +2295,7 @@ double hpmg_time_apply(hpmg_ctx* ctx, int reps, double* phase_ms) {
           dev::fill(C.kz, 0.0, H.n, C.s);
           smooth(C, H, C.kz, C.kr, false);
           CK(cudaEventRecord(ev[1], C.s));
-          dev::inject_residual(H.A, C.kz, C.kr, F.b, C.s, F.x);
+          dev::inject_residual(H.A0, C.kz, C.kr, F.b, C.s, F.x);
           CK(cudaEventRecord(ev[2], C.s));
           h_cycle(C, C.L, F.b, F.x);
           dev::embed_add(H.nb, H.bs, F.x, C.kz, C.s);
@@ -2448,7 +2456,7 @@ int hpmg_profile_levels(hpmg_ctx* ctx, int reps, double* out) {
         dev::fill(C.kz, 0.0, H.n, C.s);
         smooth(C, H, C.kz, C.kr, false);
         CK(cudaEventRecord(ev[e++], C.s));  // 1
-        dev::inject_residual(H.A, C.kz, C.kr, C.lv[L]->b, C.s);
+        dev::inject_residual(H.A0, C.kz, C.kr, C.lv[L]->b, C.s);
         CK(cudaEventRecord(ev[e++], C.s));  // 2
       }
       const int ebase = e;

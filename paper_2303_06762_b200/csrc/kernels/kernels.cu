@@ -305,18 +305,34 @@ __global__ void k_spmv(Bsr A, const double* __restrict__ x, const double* __rest
   if (with_dot) finalize<false>(dacc, red, dot_out);
 }
 
+/// A0 = the mode-0 rows (block rows 0 and 1) of every block of A, stored
+/// [nb][kSlots][2][BS] so that the head residual streams them contiguously
+/// (a column-major ELL variant, one 512-byte stream per (slot, column pair),
+/// measured slower at BS = 8: 37 -> 49 us per V-cycle at config 2)
 template <int BS>
-__global__ void k_inject_residual(Bsr A, const double* __restrict__ x, const double* __restrict__ b,
+__global__ void k_extract_mode0(Bsr A, Bsr A0) {
+  const int64_t n = int64_t(A.nb) * kSlots * 2 * BS;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t blk = t / (2 * BS);
+    const int r = int(t % (2 * BS));  // row i = r / BS, column r % BS
+    A0.val[t] = A.val[blk * BS * BS + r];
+  }
+}
+/// Mode-0 rows of E^T (b - A x) (reference transfer.hpp:140-158 applied to
+/// the residual of multigrid.hpp:124), from A0 (k_extract_mode0): the two rows
+/// of a facet's blocks are 2 x 8 x BS contiguous bytes per slot.
+template <int BS>
+__global__ void k_inject_residual(Bsr A0, const double* __restrict__ x, const double* __restrict__ b,
                                   double* __restrict__ r0, double* __restrict__ x0_zero) {
-  const int64_t n = int64_t(A.nb) * 2;
+  const int64_t n = int64_t(A0.nb) * 2;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
     const int f = int(t >> 1), i = int(t & 1);
     double s = 0.0;
 #pragma unroll
     for (int sl = 0; sl < kSlots; ++sl) {
-      const int c = __ldg(&A.cols[f * kSlots + sl]);
+      const int c = __ldg(&A0.cols[f * kSlots + sl]);
       if (c < 0) continue;
-      const double2* blk = reinterpret_cast<const double2*>(A.val + (size_t(f * kSlots + sl) * BS + i) * BS);
+      const double2* blk = reinterpret_cast<const double2*>(A0.val + (size_t(f * kSlots + sl) * 2 + i) * BS);
       const double2* xc = reinterpret_cast<const double2*>(x + size_t(c) * BS);
 #pragma unroll
       for (int j = 0; j < BS / 2; ++j) {
@@ -1662,6 +1678,12 @@ void spmv(const Bsr& A, const double* x, const double* b, double* y, int minus, 
   HPMG_LAUNCH_CHECK();
 }
 
+void extract_mode0(const Bsr& A, Bsr& A0, cudaStream_t s) {
+  by_bs(A.bs, [&](auto BS) {
+    k_extract_mode0<BS><<<grid_for(int64_t(A.nb) * kSlots * 2 * BS, 256), 256, 0, s>>>(A, A0);
+  });
+  HPMG_LAUNCH_CHECK();
+}
 void inject_residual(const Bsr& A, const double* x, const double* b, double* r0, cudaStream_t s, double* x0_zero) {
   by_bs(A.bs, [&](auto BS) {
     k_inject_residual<BS><<<grid_for(int64_t(A.nb) * 2, 256), 256, 0, s>>>(A, x, b, r0, x0_zero);

@@ -68,9 +68,11 @@ void assemble_rhs(int nb, int bs, int nfd, const int* row_elems, const int* bloc
 /// reduces dot(x, y) into *dot_out.
 void spmv(const Bsr& A, const double* x, const double* b, double* y, int minus, const Reduce* red, double* dot_out,
           cudaStream_t s);
+/// A0.val[nb][kSlots][2][bs] = rows 0 and 1 (mode 0) of every block of A
+void extract_mode0(const Bsr& A, Bsr& A0, cudaStream_t s);
 /// Residual restricted to mode-0 rows, written in lowest-order layout
-/// (fused E^T (b - A x), reference multigrid.hpp:123-124).
-void inject_residual(const Bsr& A, const double* x, const double* b, double* r0, cudaStream_t s,
+/// (fused E^T (b - A x), reference multigrid.hpp:123-124); A0 from extract_mode0.
+void inject_residual(const Bsr& A0, const double* x, const double* b, double* r0, cudaStream_t s,
                      double* x0_zero = nullptr);  // optionally zeroes x0 (same length as r0)
 /// x[f][0..1] += e[f][0..1] (the embedding E, transfer.hpp:140-158).
 void embed_add(int nb, int bs, const double* e, double* x, cudaStream_t s);
