@@ -157,23 +157,29 @@ def run_hpmg(args, rank, world, local, dist):
                            smoother=H.SMOOTH_MULTIPLICATIVE, smooth_steps=1, structured_load=(n_f, F))
     setup_wall = time.perf_counter() - t0
     setup_dev, setup_parts = B.setup_seconds()
-    # time-to-solution first, on a second context (the first one in a process
+    # time-to-solution first, on further contexts (the first one in a process
     # also pays the one-time CUDA module loading), before the CPU reference's
-    # TTS child starts loading the host
-    t0 = time.perf_counter()
-    B2 = H.MGPreconditioner(mesh="unit_square", base_n=cfg["base_n"], levels=cfg["levels"], k=cfg["k"],
-                            nu=cfg["nu"], beta=cfg["beta"], inv_eps=cfg["inv_eps"], cycle=H.CYCLE_V,
-                            smoother=H.SMOOTH_MULTIPLICATIVE, smooth_steps=1, structured_load=(n_f, F))
-    setup_warm = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    sol2 = H.uzawa_solve(B2)
-    solve_wall = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    B2.recover(sol2.velocity)  # recover_locals, as the CPU reference TTS includes it
-    recover_wall = time.perf_counter() - t0
-    B2_parts = B2.setup_seconds()
-    B2.close()
-    _, setup_parts_warm = B2_parts
+    # TTS child starts loading the host; three runs (build, solve, recover,
+    # close), the median reported: a context built while another lives maps
+    # fresh pool memory, which now and then stalls for 0.1-0.4 s
+    tts_runs = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        B2 = H.MGPreconditioner(mesh="unit_square", base_n=cfg["base_n"], levels=cfg["levels"], k=cfg["k"],
+                                nu=cfg["nu"], beta=cfg["beta"], inv_eps=cfg["inv_eps"], cycle=H.CYCLE_V,
+                                smoother=H.SMOOTH_MULTIPLICATIVE, smooth_steps=1, structured_load=(n_f, F))
+        t_setup = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        sol2 = H.uzawa_solve(B2)
+        t_solve = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        B2.recover(sol2.velocity)  # recover_locals, as the CPU reference TTS includes it
+        t_recover = time.perf_counter() - t0
+        _, parts2 = B2.setup_seconds()
+        B2.close()
+        tts_runs.append((t_setup + t_solve + t_recover, t_setup, t_solve, t_recover, parts2))
+    tts_runs_sorted = sorted(tts_runs, key=lambda r: r[0])
+    _, setup_warm, solve_wall, recover_wall, setup_parts_warm = tts_runs_sorted[1]
     tts_proc = start_cpu_tts(args) if (args.cpu_tts and rank == 0 and world == 1) else None
 
     n = B.n
@@ -351,7 +357,9 @@ def run_hpmg(args, rank, world, local, dist):
                     "setup_wall_warm_s": setup_warm, "uzawa_wall_s": solve_wall,
                     "recover_wall_s": recover_wall,
                     "tts_warm_s": setup_warm + solve_wall + recover_wall,
-                    "tts_note": "tts_warm_s = setup (second context in the process) + AL-Uzawa wall time "
+                    "tts_warm_runs_s": [r[0] for r in tts_runs],
+                    "tts_note": "tts_warm_s = median of three runs (tts_warm_runs_s) of setup (a further "
+                                "context in the process) + AL-Uzawa wall time "
                                 "(2 outer PCG solves to 1e-8, velocity and pressure back on the host) + "
                                 "recover_locals (interior, pressure modes, gradient back on the host); "
                                 "cpu_reference times the same three phases of the reference itself",

@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libhpmg.so")
+LIB_PATH = os.environ.get("HPMG_LIB") or os.path.join(_PKG, "lib", "libhpmg.so")  # HPMG_LIB: A/B builds
 
 CYCLE_V, CYCLE_W, CYCLE_VARIABLE_V = 0, 1, 2
 SMOOTH_MULTIPLICATIVE, SMOOTH_ADDITIVE = 0, 1

@@ -1,5 +1,7 @@
-"""Development: one graph-launched V-cycle inside a profiler range (for
-`ncu --profile-from-start off`). Usage: one_vcycle.py config2"""
+"""Development: graph-launched V-cycles inside a profiler range (for
+`ncu --profile-from-start off`): four drop-in hpmg_apply calls on device
+buffers, i.e. the bench step (permutations + cycle). Usage: one_vcycle.py config2"""
+import ctypes
 import os
 import sys
 
@@ -18,6 +20,19 @@ b = np.ones(B.n)
 B.apply(b)
 B.apply(b)
 torch.cuda.synchronize()
+r = torch.from_numpy(b).cuda()
+z = torch.empty_like(r)
+L = H.lib()
+
+
+def step():
+    L.hpmg_apply(B.h, ctypes.c_void_p(r.data_ptr()), ctypes.c_void_p(z.data_ptr()), H.DEVICE_PTRS)
+
+
+step()
+torch.cuda.synchronize()
 torch.cuda.profiler.start()
-B.time_apply(1)
+for _ in range(4):
+    step()
+torch.cuda.synchronize()
 torch.cuda.profiler.stop()
