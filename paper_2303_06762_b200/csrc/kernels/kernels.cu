@@ -619,8 +619,10 @@ __global__ void k_jacobi_combine(int nb, int bs, Patches P, int max_np, const do
 // ------------------------------------------------------------- transfers
 /// y (+)= M v for a 2x2-block CSR, G lanes per block row (q strided by G,
 /// fixed-order butterfly): PT rows hold ~25 blocks, P rows ~6, so one thread
-/// per row would serialise that many dependent L2 round trips.
-template <int G, bool ACC>
+/// per row would serialise that many dependent L2 round trips. The first kU
+/// blocks of a lane issue all their loads together (restriction: level-4
+/// pre-phase 77 -> 73 us at config 2).
+template <int G, bool ACC, int kU>
 __global__ void k_bcsr_group(BlockCsr M, const double* __restrict__ v, double* __restrict__ y,
                              double* __restrict__ zero_out = nullptr) {
   // warp-uniform grid stride: every lane of a warp runs the same trip count (shuffles)
@@ -631,14 +633,34 @@ __global__ void k_bcsr_group(BlockCsr M, const double* __restrict__ v, double* _
   const bool live = row < M.nrows;
   double s0 = 0.0, s1 = 0.0;
   if (live) {
-    const int q1 = __ldg(&M.ptr[row + 1]);
-    for (int q = __ldg(&M.ptr[row]) + lane; q < q1; q += G) {
-      const int c = __ldg(&M.col[q]);
-      const double2 a0 = __ldg(reinterpret_cast<const double2*>(M.val) + size_t(q) * 2);
-      const double2 a1 = __ldg(reinterpret_cast<const double2*>(M.val) + size_t(q) * 2 + 1);
-      const double2 w = __ldg(reinterpret_cast<const double2*>(v) + c);
-      s0 = fma(a0.x, w.x, fma(a0.y, w.y, s0));
-      s1 = fma(a1.x, w.x, fma(a1.y, w.y, s1));
+    // the first kU blocks of the lane with all loads in flight together
+    // (columns first, then values and the gathered v rows), the rest in a loop
+    const int q0 = __ldg(&M.ptr[row]) + lane, q1 = __ldg(&M.ptr[row + 1]);
+    int c[kU > 0 ? kU : 1];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) c[u] = q0 + u * G < q1 ? __ldg(&M.col[q0 + u * G]) : -1;
+    double2 a0[kU > 0 ? kU : 1], a1[kU > 0 ? kU : 1], w[kU > 0 ? kU : 1];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (c[u] >= 0) {
+        const size_t q = size_t(q0 + u * G);
+        a0[u] = __ldg(reinterpret_cast<const double2*>(M.val) + q * 2);
+        a1[u] = __ldg(reinterpret_cast<const double2*>(M.val) + q * 2 + 1);
+        w[u] = __ldg(reinterpret_cast<const double2*>(v) + c[u]);
+      }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (c[u] >= 0) {
+        s0 = fma(a0[u].x, w[u].x, fma(a0[u].y, w[u].y, s0));
+        s1 = fma(a1[u].x, w[u].x, fma(a1[u].y, w[u].y, s1));
+      }
+    for (int q = q0 + kU * G; q < q1; q += G) {
+      const int cq = __ldg(&M.col[q]);
+      const double2 b0 = __ldg(reinterpret_cast<const double2*>(M.val) + size_t(q) * 2);
+      const double2 b1 = __ldg(reinterpret_cast<const double2*>(M.val) + size_t(q) * 2 + 1);
+      const double2 wq = __ldg(reinterpret_cast<const double2*>(v) + cq);
+      s0 = fma(b0.x, wq.x, fma(b0.y, wq.y, s0));
+      s1 = fma(b1.x, wq.x, fma(b1.y, wq.y, s1));
     }
   }
 #pragma unroll
@@ -1767,13 +1789,15 @@ void corrected_prolongation(const Bsr& A, const TransferDev& T, BlockCsr& P, Blo
 
 void prolong_add(const BlockCsr& P, const double* e, double* x, cudaStream_t s) {
   constexpr int G = 4;
-  k_bcsr_group<G, true><<<grid_for(int64_t(P.nrows) * G, 256), 256, 0, s>>>(P, e, x);
+  // P rows hold ~6 blocks (1-2 per lane): the plain loop; unrolling it measured slower
+  k_bcsr_group<G, true, 0><<<grid_for(int64_t(P.nrows) * G, 256), 256, 0, s>>>(P, e, x);
   HPMG_LAUNCH_CHECK();
 }
 
 void restrict_(const BlockCsr& PT, const double* r, double* rc, cudaStream_t s, double* xc_zero) {
   constexpr int G = 8;
-  k_bcsr_group<G, false><<<grid_for(int64_t(PT.nrows) * G, 256), 256, 0, s>>>(PT, r, rc, xc_zero);
+  // PT rows hold ~25 blocks (3-4 per lane): four in flight at once
+  k_bcsr_group<G, false, 4><<<grid_for(int64_t(PT.nrows) * G, 256), 256, 0, s>>>(PT, r, rc, xc_zero);
   HPMG_LAUNCH_CHECK();
 }
 
