@@ -285,17 +285,21 @@ __global__ void k_spmv(Bsr A, const double* __restrict__ x, const double* __rest
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
     const int f = int(t / BS), i = int(t % BS);
     double s = 0.0;
+    // branch-free over the slots (empty ones: column 0 read, contribution
+    // selected away), so the loads of all slots can be in flight together
+    int c[kSlots];
+#pragma unroll
+    for (int sl = 0; sl < kSlots; ++sl) c[sl] = __ldg(&A.cols[f * kSlots + sl]);
 #pragma unroll
     for (int sl = 0; sl < kSlots; ++sl) {
-      const int c = __ldg(&A.cols[f * kSlots + sl]);
-      if (c < 0) continue;
+      const bool on = c[sl] >= 0;
       const double2* blk = reinterpret_cast<const double2*>(A.val + (size_t(f * kSlots + sl) * BS + i) * BS);
-      const double2* xc = reinterpret_cast<const double2*>(x + size_t(c) * BS);
+      const double2* xc = reinterpret_cast<const double2*>(x + size_t(on ? c[sl] : 0) * BS);
 #pragma unroll
       for (int j = 0; j < BS / 2; ++j) {
         const double2 a = __ldg(blk + j), xv = xc[j];
-        s = fma(a.x, xv.x, s);
-        s = fma(a.y, xv.y, s);
+        s = fma(on ? a.x : 0.0, on ? xv.x : 0.0, s);  // both zeroed: exact even for non-finite values
+        s = fma(on ? a.y : 0.0, on ? xv.y : 0.0, s);
       }
     }
     const double v = minus ? b[t] - s : s;
