@@ -253,7 +253,7 @@ def run_hpmg(args, rank, world, local, dist):
     k_e2e = max(3, args.steps // 2)
     batch = batch_call(k_e2e)
     ms_e2e = timed_once(batch)
-    # per-phase split (event-instrumented pass): head pre-sweep, head residual, h-cycle, head post-sweep
+    # per-phase split, each phase its own graph: head pre-sweep, head residual, h-cycle + embedding, head post-sweep
     _, phases = B.time_apply(max(3, args.steps // 4), phases=True)
     vbytes, vparts = B.vcycle_bytes()
     # physical bytes: streamed sweep records (head p6, levels p7), head mode-0

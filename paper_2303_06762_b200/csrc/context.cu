@@ -240,7 +240,6 @@ struct hpmg_ctx {
   // device-resident PCG iteration: one graph with a while node (built lazily)
   cudaGraphExec_t pcg_loop = nullptr;
   bool pcg_loop_failed = false;
-  cudaStream_t s_cap = nullptr;  // second capture stream (conditional bodies)
   cudaStream_t s_nest[4] = {nullptr, nullptr, nullptr, nullptr};  // nested conditional-body captures
   // device-resident GMRES: workspace for `gm_cap` Arnoldi steps per cycle and its loop graph
   dev::GmDev gm;
@@ -868,93 +867,95 @@ void out_vec(hpmg_ctx& C, const double* src_blk, double* dst, int flags) {
 }
 
 // ---------------------------------------------------------------- solvers
-/// One PCG iteration as a CUDA graph: a while node whose body is
+// ------------------------------------------------ conditional-graph capture
+struct GraphError {
+  cudaError_t e;
+};
+inline void GK(cudaError_t e) {
+  if (e != cudaSuccess) throw GraphError{e};
+}
+/// Appends a conditional node after the work captured so far on `s`; later
+/// captured work depends on it. Returns the node's body graph.
+cudaGraph_t add_conditional(cudaStream_t s, cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type) {
+  cudaStreamCaptureStatus cs;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  cudaGraph_t capg;
+  GK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &capg, &deps, &ndeps));
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = type;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  GK(cudaGraphAddNode(&node, capg, deps, ndeps, &p));
+  GK(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+  return p.conditional.phGraph_out[0];
+}
+/// Captures fn() into `body` on nesting stream `depth`, with C.s pointing at
+/// that stream meanwhile (the V-cycle helpers launch on C.s).
+template <class F>
+void capture_body(hpmg_ctx& C, cudaGraph_t body, int depth, F fn) {
+  if (!C.s_nest[depth]) GK(cudaStreamCreateWithFlags(&C.s_nest[depth], cudaStreamNonBlocking));
+  cudaStream_t q = C.s_nest[depth], saved = C.s;
+  GK(cudaStreamBeginCaptureToGraph(q, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  C.s = q;
+  try {
+    fn();
+  } catch (...) {
+    C.s = saved;
+    cudaGraph_t tmp;
+    cudaStreamEndCapture(q, &tmp);
+    throw;
+  }
+  C.s = saved;
+  cudaGraph_t tmp;
+  GK(cudaStreamEndCapture(q, &tmp));
+}
+
+/// The PCG iterations (reference krylov.hpp:44-70) as one CUDA graph with no
+/// host round trip: the first iteration's
 ///   Ap = A p, p.Ap | x += a p, r -= a Ap, r.r, count, stop test
-///   | if (more): z = M r (the V-cycle launch sequence), r.z + beta, p = z + beta p
-/// (the loop handle is cleared by the kernel that decides to stop)
-/// (reference krylov.hpp:44-70). The branch and loop predicates are set on
-/// the device (cudaGraphSetConditional), so a whole solve is one graph launch
-/// with no host round trip per iteration. Returns false (and the host loop is
-/// used) where the driver cannot build it.
+/// then a while node whose body is
+///   z = M r (the V-cycle launch sequence) | r.z, positivity test, beta
+///   | Ap = A p' with p' = z + beta p formed on the fly, p'.Ap
+///   | p = p', x += a p, r -= a Ap, r.r, count, stop test.
+/// The loop predicate is set on the device (cudaGraphSetConditional) by the
+/// kernel that decides to stop; the kernels after it in the same body are
+/// no-ops then. No if node: the V-cycle sits directly in the loop body.
+/// Returns false (and the host loop is used) where the driver cannot build it.
 bool build_pcg_loop(hpmg_ctx& C) {
   Level& T = C.top();
   const int64_t n = T.n;
   cudaGraph_t g = nullptr;
-  cudaStream_t s_main = C.s;
-  bool capturing = false, capturing2 = false;
-  auto fail = [&](cudaError_t e) {
-    if (capturing2) {
-      cudaGraph_t tmp;
-      cudaStreamEndCapture(C.s_cap, &tmp);
-    }
-    C.s = s_main;
-    if (capturing) {
-      cudaGraph_t tmp;
-      cudaStreamEndCapture(s_main, &tmp);
-    }
-    if (g) cudaGraphDestroy(g);
-    cudaGetLastError();
-    if (std::getenv("HPMG_DEBUG_GRAPH")) std::fprintf(stderr, "pcg loop graph: %s\n", cudaGetErrorString(e));
-    return false;
-  };
-  cudaError_t e;
-  if (!C.s_cap && (e = cudaStreamCreateWithFlags(&C.s_cap, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);
-  if ((e = cudaGraphCreate(&g, 0)) != cudaSuccess) return fail(e);
-  cudaGraphConditionalHandle h_loop, h_more;
-  if ((e = cudaGraphConditionalHandleCreate(&h_loop, g, 1, cudaGraphCondAssignDefault)) != cudaSuccess) return fail(e);
-  if ((e = cudaGraphConditionalHandleCreate(&h_more, g, 0, cudaGraphCondAssignDefault)) != cudaSuccess) return fail(e);
-  cudaGraphNodeParams wp = {};
-  wp.type = cudaGraphNodeTypeConditional;
-  wp.conditional.handle = h_loop;
-  wp.conditional.type = cudaGraphCondTypeWhile;
-  wp.conditional.size = 1;
-  cudaGraphNode_t wnode;
-  if ((e = cudaGraphAddNode(&wnode, g, nullptr, 0, &wp)) != cudaSuccess) return fail(e);
-  cudaGraph_t body = wp.conditional.phGraph_out[0];
   try {
-    if ((e = cudaStreamBeginCaptureToGraph(s_main, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal)) !=
-        cudaSuccess)
-      return fail(e);
-    capturing = true;
-    dev::spmv(T.A, C.kp, nullptr, C.kAp, 0, &C.red, C.sc + S_PAP, s_main);
-    dev::pcg_loop_update(C.kx, C.kr, C.kp, C.kAp, n, C.sc, C.red, h_more, h_loop, s_main);
-    // the if node, appended to the capture
-    cudaStreamCaptureStatus cs;
-    const cudaGraphNode_t* deps = nullptr;
-    size_t ndeps = 0;
-    cudaGraph_t capg;
-    if ((e = cudaStreamGetCaptureInfo(s_main, &cs, nullptr, &capg, &deps, &ndeps)) != cudaSuccess) return fail(e);
-    cudaGraphNodeParams ip = {};
-    ip.type = cudaGraphNodeTypeConditional;
-    ip.conditional.handle = h_more;
-    ip.conditional.type = cudaGraphCondTypeIf;
-    ip.conditional.size = 1;
-    cudaGraphNode_t inode;
-    if ((e = cudaGraphAddNode(&inode, capg, deps, ndeps, &ip)) != cudaSuccess) return fail(e);
-    // the branch body, captured on the second stream (the V-cycle launches on C.s)
-    if ((e = cudaStreamBeginCaptureToGraph(C.s_cap, ip.conditional.phGraph_out[0], nullptr, nullptr, 0,
-                                           cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
-      return fail(e);
-    capturing2 = true;
-    C.s = C.s_cap;
-    apply_blocks(C, C.kr, C.kz);  // z = M r
-    dev::pcg_loop_rz(C.kr, C.kz, n, C.sc, C.red, h_loop, C.s);
-    dev::pcg_loop_direction(C.kp, C.kz, n, C.sc, C.s);
-    C.s = s_main;
-    cudaGraph_t ibody;
-    capturing2 = false;
-    if ((e = cudaStreamEndCapture(C.s_cap, &ibody)) != cudaSuccess) return fail(e);
-    if ((e = cudaStreamUpdateCaptureDependencies(s_main, &inode, 1, cudaStreamSetCaptureDependencies)) != cudaSuccess)
-      return fail(e);
-    cudaGraph_t b2;
-    capturing = false;
-    if ((e = cudaStreamEndCapture(s_main, &b2)) != cudaSuccess) return fail(e);
-  } catch (const std::exception&) {
-    return fail(cudaErrorUnknown);
-  }
-  if ((e = cudaGraphInstantiate(&C.pcg_loop, g, 0)) != cudaSuccess) {
+    GK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h_loop;
+    GK(cudaGraphConditionalHandleCreate(&h_loop, g, 0, cudaGraphCondAssignDefault));
+    capture_body(C, g, 0, [&] {
+      dev::pcg_spmv_dir(T.A, C.kp, C.kz, C.kAp, 0, C.sc, C.red, C.s);  // p = z0 (pcg_device)
+      dev::pcg_loop_update(C.kx, C.kr, C.kp, C.kz, C.kAp, n, 0, C.sc, C.red, h_loop, C.s);
+      cudaGraph_t body = add_conditional(C.s, h_loop, cudaGraphCondTypeWhile);
+      capture_body(C, body, 1, [&] {
+        apply_blocks(C, C.kr, C.kz);  // z = M r
+        dev::pcg_loop_rz(C.kr, C.kz, n, C.sc, C.red, h_loop, C.s);
+        dev::pcg_spmv_dir(T.A, C.kp, C.kz, C.kAp, 1, C.sc, C.red, C.s);
+        dev::pcg_loop_update(C.kx, C.kr, C.kp, C.kz, C.kAp, n, 1, C.sc, C.red, h_loop, C.s);
+      });
+    });
+    GK(cudaGraphInstantiate(&C.pcg_loop, g, 0));
+  } catch (const GraphError& e) {
+    if (g) cudaGraphDestroy(g);
     C.pcg_loop = nullptr;
-    return fail(e);
+    cudaGetLastError();
+    if (std::getenv("HPMG_DEBUG_GRAPH")) std::fprintf(stderr, "pcg loop graph: %s\n", cudaGetErrorString(e.e));
+    return false;
+  } catch (const std::exception& e) {
+    if (g) cudaGraphDestroy(g);
+    C.pcg_loop = nullptr;
+    cudaGetLastError();
+    if (std::getenv("HPMG_DEBUG_GRAPH")) std::fprintf(stderr, "pcg loop graph: %s\n", e.what());
+    return false;
   }
   cudaGraphDestroy(g);
   return true;
@@ -1029,52 +1030,6 @@ hpmg_solve_stats pcg_device(hpmg_ctx& C, const hpmg_krylov_opts& o) {
   return st;
 }
 
-
-// ------------------------------------------------ conditional-graph capture
-struct GraphError {
-  cudaError_t e;
-};
-inline void GK(cudaError_t e) {
-  if (e != cudaSuccess) throw GraphError{e};
-}
-/// Appends a conditional node after the work captured so far on `s`; later
-/// captured work depends on it. Returns the node's body graph.
-cudaGraph_t add_conditional(cudaStream_t s, cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type) {
-  cudaStreamCaptureStatus cs;
-  const cudaGraphNode_t* deps = nullptr;
-  size_t ndeps = 0;
-  cudaGraph_t capg;
-  GK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &capg, &deps, &ndeps));
-  cudaGraphNodeParams p = {};
-  p.type = cudaGraphNodeTypeConditional;
-  p.conditional.handle = h;
-  p.conditional.type = type;
-  p.conditional.size = 1;
-  cudaGraphNode_t node;
-  GK(cudaGraphAddNode(&node, capg, deps, ndeps, &p));
-  GK(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
-  return p.conditional.phGraph_out[0];
-}
-/// Captures fn() into `body` on nesting stream `depth`, with C.s pointing at
-/// that stream meanwhile (the V-cycle helpers launch on C.s).
-template <class F>
-void capture_body(hpmg_ctx& C, cudaGraph_t body, int depth, F fn) {
-  if (!C.s_nest[depth]) GK(cudaStreamCreateWithFlags(&C.s_nest[depth], cudaStreamNonBlocking));
-  cudaStream_t q = C.s_nest[depth], saved = C.s;
-  GK(cudaStreamBeginCaptureToGraph(q, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-  C.s = q;
-  try {
-    fn();
-  } catch (...) {
-    C.s = saved;
-    cudaGraph_t tmp;
-    cudaStreamEndCapture(q, &tmp);
-    throw;
-  }
-  C.s = saved;
-  cudaGraph_t tmp;
-  GK(cudaStreamEndCapture(q, &tmp));
-}
 
 /// GMRES workspace for `cap` Arnoldi steps per cycle (grows only).
 void gm_workspace(hpmg_ctx& C, int cap) {
@@ -1662,7 +1617,6 @@ void hpmg_destroy(hpmg_ctx* ctx) {
   if (ctx->apply_graph) cudaGraphExecDestroy(ctx->apply_graph);
   destroy_io_graph(*ctx);
   if (ctx->pcg_loop) cudaGraphExecDestroy(ctx->pcg_loop);
-  if (ctx->s_cap) cudaStreamDestroy(ctx->s_cap);
   if (ctx->gm_loop) cudaGraphExecDestroy(ctx->gm_loop);
   for (cudaStream_t q : ctx->s_nest)
     if (q) cudaStreamDestroy(q);
@@ -2282,39 +2236,41 @@ double hpmg_time_apply(hpmg_ctx* ctx, int reps, double* phase_ms) {
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     ms_per = ms / reps;
-    if (phase_ms) {
-      // event-instrumented non-graph pass: head pre-sweep, head post-sweep, rest
+    if (phase_ms && C.opt.k > 0) {
+      // each phase captured as a graph of its own and timed over `reps`
+      // launches: head pre-sweep (from x = 0), head residual (E^T injection),
+      // the lowest-order h-cycle with the embedding, head post-sweep
       for (int i = 0; i < 8; ++i) phase_ms[i] = 0;
-      cudaEvent_t ev[6];
-      for (auto& e : ev) CK(cudaEventCreate(&e));
-      for (int r = 0; r < reps; ++r) {
-        if (C.opt.k > 0) {
-          Level& H = *C.head;
-          Level& F = *C.lv[C.L];
-          CK(cudaEventRecord(ev[0], C.s));
-          dev::fill(C.kz, 0.0, H.n, C.s);
-          smooth(C, H, C.kz, C.kr, false);
-          CK(cudaEventRecord(ev[1], C.s));
-          dev::inject_residual(H.A0, C.kz, C.kr, F.b, C.s, F.x);
-          CK(cudaEventRecord(ev[2], C.s));
-          h_cycle(C, C.L, F.b, F.x);
-          dev::embed_add(H.nb, H.bs, F.x, C.kz, C.s);
-          CK(cudaEventRecord(ev[3], C.s));
-          smooth(C, H, C.kz, C.kr, true);
-          CK(cudaEventRecord(ev[4], C.s));
-          CK(cudaEventSynchronize(ev[4]));
-          float a, b, c, d;
-          cudaEventElapsedTime(&a, ev[0], ev[1]);
-          cudaEventElapsedTime(&b, ev[1], ev[2]);
-          cudaEventElapsedTime(&c, ev[2], ev[3]);
-          cudaEventElapsedTime(&d, ev[3], ev[4]);
-          phase_ms[0] += a / reps;
-          phase_ms[1] += b / reps;
-          phase_ms[2] += c / reps;
-          phase_ms[3] += d / reps;
-        }
-      }
-      for (auto& e : ev) cudaEventDestroy(e);
+      Level& H = *C.head;
+      Level& F = *C.lv[C.L];
+      auto phase = [&](auto fn) {
+        cudaGraph_t g;
+        cudaGraphExec_t ge;
+        CK(cudaStreamBeginCapture(C.s, cudaStreamCaptureModeThreadLocal));
+        fn();
+        CK(cudaStreamEndCapture(C.s, &g));
+        CK(cudaGraphInstantiate(&ge, g, 0));
+        cudaGraphDestroy(g);
+        for (int i = 0; i < 3; ++i) CK(cudaGraphLaunch(ge, C.s));
+        CK(cudaEventRecord(e0, C.s));
+        for (int i = 0; i < reps; ++i) CK(cudaGraphLaunch(ge, C.s));
+        CK(cudaEventRecord(e1, C.s));
+        CK(cudaEventSynchronize(e1));
+        float t = 0;
+        cudaEventElapsedTime(&t, e0, e1);
+        cudaGraphExecDestroy(ge);
+        return double(t) / reps;
+      };
+      phase_ms[0] = phase([&] {
+        dev::fill(C.kz, 0.0, H.n, C.s);
+        smooth(C, H, C.kz, C.kr, false, true);
+      });
+      phase_ms[1] = phase([&] { dev::inject_residual(H.A0, C.kz, C.kr, F.b, C.s, F.x); });
+      phase_ms[2] = phase([&] {
+        h_cycle(C, C.L, F.b, F.x);
+        dev::embed_add(H.nb, H.bs, F.x, C.kz, C.s);
+      });
+      phase_ms[3] = phase([&] { smooth(C, H, C.kz, C.kr, true); });
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
@@ -2378,8 +2334,8 @@ double hpmg_debug_loop_probe(hpmg_ctx* ctx, int mode, int iters) {
         }
         if (pm >= 0) {
           const int64_t n = C.top().n;
-          if (pm & 1) dev::spmv(C.top().A, C.kp, nullptr, C.kAp, 0, &C.red, C.sc + S_PAP, C.s);
-          if (pm & 2) dev::pcg_loop_update(C.kx, C.kr, C.kp, C.kAp, n, C.sc, C.red, hi ? hi : h, h, C.s);
+          if (pm & 1) dev::pcg_spmv_dir(C.top().A, C.kp, C.kz, C.kAp, 1, C.sc, C.red, C.s);
+          if (pm & 2) dev::pcg_loop_update(C.kx, C.kr, C.kp, C.kz, C.kAp, n, 1, C.sc, C.red, h, C.s);
           auto branch = [&] {
             apply_blocks(C, C.kr, C.kz);
             if (pm & 8) dev::pcg_loop_rz(C.kr, C.kz, n, C.sc, C.red, h, C.s);

@@ -309,6 +309,51 @@ __global__ void k_spmv(Bsr A, const double* __restrict__ x, const double* __rest
   if (with_dot) finalize<false>(dacc, red, dot_out);
 }
 
+/// PCG loop operator apply with the direction update folded in (reference
+/// krylov.hpp:46-47,69): Ap = A p' and p'.Ap, where p' = z + beta p when
+/// `dir` (every column block is formed on the fly from z and the previous p,
+/// which stays untouched: k_pcg_loop_update stores p' with the same
+/// arithmetic), p' = p otherwise. A no-op once the loop has stopped.
+template <int BS>
+__global__ void k_spmv_dir(Bsr A, const double* __restrict__ p, const double* __restrict__ z, double* __restrict__ y,
+                           int dir, const double* __restrict__ sc, Reduce red, double* dot_out) {
+  if (sc[kScStatus] != kLoopRunning) return;  // grid-uniform
+  const double beta = dir ? sc[kScBeta] : 0.0;
+  const int64_t n = int64_t(A.nb) * BS;
+  double dacc = 0.0;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+    const int f = int(t / BS), i = int(t % BS);
+    double s = 0.0;
+    int c[kSlots];
+#pragma unroll
+    for (int sl = 0; sl < kSlots; ++sl) c[sl] = __ldg(&A.cols[f * kSlots + sl]);
+#pragma unroll
+    for (int sl = 0; sl < kSlots; ++sl) {
+      const bool on = c[sl] >= 0;
+      const double2* blk = reinterpret_cast<const double2*>(A.val + (size_t(f * kSlots + sl) * BS + i) * BS);
+      const size_t co = size_t(on ? c[sl] : 0) * BS;
+      const double2* pc = reinterpret_cast<const double2*>(p + co);
+      const double2* zc = reinterpret_cast<const double2*>(z + co);
+#pragma unroll
+      for (int j = 0; j < BS / 2; ++j) {
+        const double2 a = __ldg(blk + j), pv = pc[j];
+        double2 xv = pv;
+        if (dir) {
+          const double2 zv = zc[j];
+          xv.x = fma(beta, pv.x, zv.x);
+          xv.y = fma(beta, pv.y, zv.y);
+        }
+        s = fma(on ? a.x : 0.0, on ? xv.x : 0.0, s);
+        s = fma(on ? a.y : 0.0, on ? xv.y : 0.0, s);
+      }
+    }
+    y[t] = s;
+    const double pt = dir ? fma(beta, p[t], z[t]) : p[t];
+    dacc = fma(pt, s, dacc);
+  }
+  finalize<false>(dacc, red, dot_out);
+}
+
 /// A0 = the mode-0 rows (block rows 0 and 1) of every block of A, stored
 /// [nb][kSlots][2][BS] so that the head residual streams them contiguously
 /// (a column-major ELL variant, one 512-byte stream per (slot, column pair),
@@ -1152,21 +1197,27 @@ __global__ void k_pcg_update(double* __restrict__ x, double* __restrict__ r, con
 /// stop test (krylov.hpp:54-62; at the cap the reference still forms z = M r
 /// and checks r.z once more), setting the branch and, when stopping, the
 /// loop handle.
-__global__ void k_pcg_loop_update(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
-                                  const double* __restrict__ Ap, int64_t n, double* sc, Reduce red,
-                                  cudaGraphConditionalHandle h_more, cudaGraphConditionalHandle h_loop) {
+__global__ void k_pcg_loop_update(double* __restrict__ x, double* __restrict__ r, double* __restrict__ p,
+                                  const double* __restrict__ z, const double* __restrict__ Ap, int64_t n, int dir,
+                                  double* sc, Reduce red, cudaGraphConditionalHandle h_loop) {
+  if (sc[kScStatus] != kLoopRunning) return;  // stopped by r.z in this iteration
   if (!(sc[kScPAp] > 0.0)) {  // krylov.hpp:49-53: x and r untouched, not applicable
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       sc[kScStatus] = kLoopNaPAp;
-      cudaGraphSetConditional(h_more, 0u);
       cudaGraphSetConditional(h_loop, 0u);
     }
     return;
   }
   const double alpha = sc[kScRZ] / sc[kScPAp];
+  const double beta = dir ? sc[kScBeta] : 0.0;
   double s = 0.0;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
-    x[t] += alpha * p[t];
+    double pt = p[t];
+    if (dir) {  // p = z + beta p (krylov.hpp:69), as k_spmv_dir formed it
+      pt = fma(beta, pt, z[t]);
+      p[t] = pt;
+    }
+    x[t] += alpha * pt;
     const double rv = r[t] - alpha * Ap[t];
     r[t] = rv;
     s = fma(rv, rv, s);
@@ -1177,8 +1228,8 @@ __global__ void k_pcg_loop_update(double* __restrict__ x, double* __restrict__ r
     if (sqrt(rr) <= sc[kScTarget]) st = kLoopConverged;
     else if (sc[kScIt] >= sc[kScMaxIt]) st = kLoopLast;
     sc[kScStatus] = st;
-    cudaGraphSetConditional(h_more, (st == kLoopRunning || st == kLoopLast) ? 1u : 0u);
-    if (st == kLoopConverged) cudaGraphSetConditional(h_loop, 0u);
+    // the cap still forms z = M r and checks r.z once (k_pcg_loop_rz ends the loop there)
+    cudaGraphSetConditional(h_loop, st == kLoopConverged ? 0u : 1u);
   });
 }
 /// r.z, then (last block) its positivity test (krylov.hpp:63-68) and
@@ -1969,9 +2020,17 @@ void gm_end(double* sc, const GmDev& G, cudaStream_t s) {
   k_gm_end<<<1, 1, 0, s>>>(sc, G);
   HPMG_LAUNCH_CHECK();
 }
-void pcg_loop_update(double* x, double* r, const double* p, const double* Ap, int64_t n, double* sc, const Reduce& red,
-                     cudaGraphConditionalHandle h_more, cudaGraphConditionalHandle h_loop, cudaStream_t s) {
-  k_pcg_loop_update<<<kRedBlocks, 256, 0, s>>>(x, r, p, Ap, n, sc, red, h_more, h_loop);
+void pcg_loop_update(double* x, double* r, double* p, const double* z, const double* Ap, int64_t n, int dir,
+                     double* sc, const Reduce& red, cudaGraphConditionalHandle h_loop, cudaStream_t s) {
+  k_pcg_loop_update<<<kRedBlocks, 256, 0, s>>>(x, r, p, z, Ap, n, dir, sc, red, h_loop);
+  HPMG_LAUNCH_CHECK();
+}
+void pcg_spmv_dir(const Bsr& A, const double* p, const double* z, double* Ap, int dir, double* sc, const Reduce& red,
+                  cudaStream_t s) {
+  by_bs(A.bs, [&](auto BS) {
+    static const int grid = resident_grid(k_spmv_dir<BS>);
+    k_spmv_dir<BS><<<grid, 256, 0, s>>>(A, p, z, Ap, dir, sc, red, sc + kScPAp);
+  });
   HPMG_LAUNCH_CHECK();
 }
 void pcg_loop_rz(const double* r, const double* z, int64_t n, double* sc, const Reduce& red,

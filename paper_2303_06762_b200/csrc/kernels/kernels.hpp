@@ -201,8 +201,11 @@ constexpr double kLoopRunning = 0.0, kLoopConverged = 1.0, kLoopNaPAp = 2.0, kLo
                  kLoopLast = 5.0;
 void pcg_loop_init(double* sc, double target, double max_it, cudaStream_t s);
 /// the update with the count / stop test, r.z with the positivity test and beta
-void pcg_loop_update(double* x, double* r, const double* p, const double* Ap, int64_t n, double* sc, const Reduce& red,
-                     cudaGraphConditionalHandle h_more, cudaGraphConditionalHandle h_loop, cudaStream_t s);
+void pcg_loop_update(double* x, double* r, double* p, const double* z, const double* Ap, int64_t n, int dir,
+                     double* sc, const Reduce& red, cudaGraphConditionalHandle h_loop, cudaStream_t s);
+/// Ap = A p', p'.Ap into sc[kScPAp], p' = z + beta p (dir) or p, p untouched
+void pcg_spmv_dir(const Bsr& A, const double* p, const double* z, double* Ap, int dir, double* sc, const Reduce& red,
+                  cudaStream_t s);
 void pcg_loop_rz(const double* r, const double* z, int64_t n, double* sc, const Reduce& red,
                  cudaGraphConditionalHandle h_loop, cudaStream_t s);
 void pcg_loop_direction(double* p, const double* z, int64_t n, const double* sc, cudaStream_t s);
