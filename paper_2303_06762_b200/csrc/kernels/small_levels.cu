@@ -10,7 +10,7 @@
 // L2-resident across V-cycles) into a 3-slot mbarrier ring while the kPass x 16
 // consumer threads compute pass k: r = b_p - A_pe x_e from the staged external
 // blocks (sweep_rec.cu), then x_p = S r with the FULL patch inverse
-// (column-major in the record, so the GEMV reads are bank-conflict free). A wave costs two __syncthreads().
+// (column-major in the record, so the GEMV reads are bank-conflict free). A pass costs one __syncthreads().
 // Symmetric operators only.
 #include <cuda_runtime.h>
 
@@ -85,9 +85,16 @@ __device__ Smem carve(int n, int stride, double* sm) {
   return v;
 }
 
-/// All passes of `nsweeps` sweeps, forward or reversed, over the patch records.
+/// All passes of `nsweeps` sweeps, forward or reversed, over the patch
+/// records; NPM = 2 max_nf rows per patch (the level's largest patch), so
+/// every load is unpredicated (S_p and the meta words are padded: rows past
+/// the patch have facet -1 and zero S_p rows/columns). A patch's 16 threads
+/// sit in one half-warp: the residual rows are exchanged under __syncwarp,
+/// and one CTA barrier per pass publishes x_p to the next pass.
+template <int NPM>
 __device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, int npass, int nsweeps, bool reverse,
                        const Smem& v) {
+  static_assert(NPM <= kTP && NPM % 2 == 0, "patch rows per half-warp");
   const int lp = threadIdx.x / kTP, t = threadIdx.x % kTP;
   const bool producer = threadIdx.x >= kConsumers;
   const int total = npass * nsweeps;
@@ -110,63 +117,55 @@ __device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, i
   };
   if (producer && threadIdx.x == kConsumers)
     for (int k = 0; k < kStages - 1 && k < total; ++k) issue(k);
-  for (int k = 0; k < total; ++k) {
+  const int lf = t >> 1, i = t & 1;
+  const bool rowthread = t < NPM;
+  double* rr = v.r + lp * kTP;
+  int q = 0;  // k % npass, kept incrementally (no division on the consumers' critical path)
+  for (int k = 0; k < total; ++k, q = q + 1 == npass ? 0 : q + 1) {
     if (producer) {
-      // slot (k+1) % 2 was released by the __syncthreads() that closed pass k-1
+      // slot (k+2) % 3 was released by the __syncthreads() that closed pass k-1
       if (threadIdx.x == kConsumers && k + kStages - 1 < total) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         issue(k + kStages - 1);
       }
       __syncthreads();
-      __syncthreads();
       continue;
     }
-    const int2 ps = pass_of(k);
+    const int2 ps = v.pass[reverse ? npass - 1 - q : q];
     if (trace && k < 1000) d_trace[4 * k] = clock64();
     ring_wait(&v.bar[k % kStages], unsigned((k / kStages) & 1));
     if (trace && k < 1000) d_trace[4 * k + 1] = clock64();
     const double* rec = v.ring + (size_t(k % kStages) * kPass + lp) * R.stride;
-    int np = 0, g = 0;
-    // every shared load of the residual and of row t of S_p is addressed
-    // without the patch's own size (S_p zero-padded to the level's largest
-    // patch, meta padded with -1), so all of them issue right after the
-    // ring wait instead of behind the meta[0] load
-    double srow[2 * kMaxPatchF];
-    if (lp < ps.y) {
+    if (lp < ps.y && rowthread) {
+      // row t of the full column-major S_p: S(t, j) at j*NPM + t
+      double srow[NPM];
+#pragma unroll
+      for (int j = 0; j < NPM; ++j) srow[j] = rec[j * NPM + t];
       const int* meta = reinterpret_cast<const int*>(rec + R.meta_off);
-      const int npm = 2 * R.max_nf;
-#pragma unroll
-      for (int j = 0; j < 2 * kMaxPatchF; ++j) srow[j] = j < npm ? rec[j * npm + t] : 0.0;
-      const int lf = t >> 1, i = t & 1;
-      const bool rowok = lf < R.max_nf;
-      const int f = rowok ? meta[1 + lf] : -1;
-      int c[kExt];
-      const int* cols = meta + 1 + R.max_nf + lf * kExt;
-#pragma unroll
-      for (int sl = 0; sl < kExt; ++sl) c[sl] = rowok ? cols[sl] : -1;
-      np = 2 * meta[0];
-      const double* acol = rec + R.a_off + lf * kExt * 4 + i;  // column-major 2x2 blocks
-      g = 2 * (f >= 0 ? f : 0) + i;
+      const int f = meta[1 + lf];  // -1: row past the patch
+      const int* cols = meta + 1 + (NPM / 2) + lf * kExt;
+      const double* acol = rec + R.a_off + lf * kExt * 4 + i;  // column-major 2x2 blocks (zero for empty slots)
+      const int g = 2 * (f >= 0 ? f : 0) + i;
       double a0 = v.sb[g], a1 = 0.0;
 #pragma unroll
       for (int sl = 0; sl < kExt; ++sl) {
-        const int cc = c[sl] >= 0 ? c[sl] : 0;  // empty slots hold zero blocks
-        const double w0 = rowok ? acol[sl * 4] : 0.0, w1 = rowok ? acol[sl * 4 + 2] : 0.0;
-        a0 = fma(-w0, v.sx[2 * cc], a0);
-        a1 = fma(-w1, v.sx[2 * cc + 1], a1);
+        const int c = cols[sl];
+        const double2 xe = *reinterpret_cast<const double2*>(v.sx + 2 * (c >= 0 ? c : 0));
+        a0 = fma(-acol[sl * 4], xe.x, a0);
+        a1 = fma(-acol[sl * 4 + 2], xe.y, a1);
       }
-      if (t < np) v.r[threadIdx.x] = a0 + a1;
-    }
-    __syncthreads();
-    if (trace && k < 1000) d_trace[4 * k + 2] = clock64();
-    if (t < np) {
-      // full column-major inverse: S(t, j) at j*npmax + t
-      const double* rr = v.r + lp * kTP;
+      rr[t] = f >= 0 ? a0 + a1 : 0.0;
+      __syncwarp(((1u << NPM) - 1u) << (threadIdx.x & 16));  // the patch's row threads
+      if (trace && k < 1000) d_trace[4 * k + 2] = clock64();
+      // x_p = S_p (b_p - A_pe x_e) (sweep_rec.cu); padded columns are zero
       double d[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-      for (int j = 0; j < 2 * kMaxPatchF; ++j)
-        if (j < np) d[j & 3] = fma(srow[j], rr[j], d[j & 3]);
-      v.sx[g] = (d[0] + d[1]) + (d[2] + d[3]);  // x_p = S_p (b_p - A_pe x_e), sweep_rec.cu
+      for (int j = 0; j < NPM; j += 2) {
+        const double2 r2 = *reinterpret_cast<const double2*>(rr + j);
+        d[j & 3] = fma(srow[j], r2.x, d[j & 3]);
+        d[(j + 1) & 3] = fma(srow[j + 1], r2.y, d[(j + 1) & 3]);
+      }
+      if (f >= 0) v.sx[g] = (d[0] + d[1]) + (d[2] + d[3]);
     }
     __syncthreads();
     if (trace && k < 1000) d_trace[4 * k + 3] = clock64();
@@ -176,6 +175,7 @@ __device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, i
 /// x = 0; pre-smooth (reference multigrid.hpp:174-175). The residual and the
 /// restriction run grid-wide after it (small_pre): their latency-bound CSR
 /// loops cost ~90 us in one CTA.
+template <int NPM>
 __global__ void __launch_bounds__(kThreads) k_small_pre(int n, PatchRecords R, const int2* __restrict__ passes,
                                                         int npass, int nsweeps, const double* __restrict__ b,
                                                         double* __restrict__ x) {
@@ -188,13 +188,14 @@ __global__ void __launch_bounds__(kThreads) k_small_pre(int n, PatchRecords R, c
   }
   __syncthreads();
   stamp(4089);
-  sweeps(R, passes, npass, nsweeps, false, v);
+  sweeps<NPM>(R, passes, npass, nsweeps, false, v);
   stamp(4090);
   for (int t = threadIdx.x; t < n; t += blockDim.x) x[t] = v.sx[t];
   stamp(4091);
 }
 
 /// post-smooth (reverse sweep) of x, after the grid-wide x += P e (multigrid.hpp:181-182)
+template <int NPM>
 __global__ void __launch_bounds__(kThreads) k_small_post(int n, PatchRecords R, const int2* __restrict__ passes,
                                                          int npass, int nsweeps, const double* __restrict__ b,
                                                          double* __restrict__ x) {
@@ -207,10 +208,34 @@ __global__ void __launch_bounds__(kThreads) k_small_post(int n, PatchRecords R, 
   }
   __syncthreads();
   stamp(4093);
-  sweeps(R, passes, npass, nsweeps, true, v);
+  sweeps<NPM>(R, passes, npass, nsweeps, true, v);
   stamp(4094);
   for (int t = threadIdx.x; t < n; t += blockDim.x) x[t] = v.sx[t];
   stamp(4095);
+}
+
+/// launches k_small_pre / k_small_post for the level's patch row count
+template <bool kPost>
+void launch_small(const PatchRecords& R, int n, const int2* passes, int npass, int nsweeps, const double* b,
+                  double* x, size_t smem, cudaStream_t s) {
+  auto go = [&](auto kernel) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      attr = true;
+    }
+    kernel<<<1, kThreads, smem, s>>>(n, R, passes, npass, nsweeps, b, x);
+  };
+  switch (R.max_nf) {
+    case 4: go(kPost ? k_small_post<8> : k_small_pre<8>); break;
+    case 5: go(kPost ? k_small_post<10> : k_small_pre<10>); break;
+    case 6: go(kPost ? k_small_post<12> : k_small_pre<12>); break;
+    case 7: go(kPost ? k_small_post<14> : k_small_pre<14>); break;
+    case 8: go(kPost ? k_small_post<16> : k_small_pre<16>); break;
+    default: throw std::runtime_error("small-level sweep: unsupported patch size");
+  }
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) throw std::runtime_error(std::string("CUDA launch: ") + cudaGetErrorString(err));
 }
 
 size_t smem_bytes(int nb, int stride, int npass) {
@@ -234,15 +259,7 @@ bool small_level_fits(int nb, int record_stride, int npass) {
 void small_pre(const Bsr& A, const PatchRecords& R, const int2* passes, int npass, int sweeps, const BlockCsr& PT,
                const double* b, double* x, double* r, double* rc, cudaStream_t s) {
   if (!R.full) throw std::runtime_error("small-level sweeps need full-inverse patch records");
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_small_pre, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(k_small_post, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
-  k_small_pre<<<1, kThreads, smem_bytes(A.nb, R.stride, npass), s>>>(A.nb * 2, R, passes, npass, sweeps, b, x);
-  cudaError_t err = cudaGetLastError();
-  if (err != cudaSuccess) throw std::runtime_error(std::string("CUDA launch: ") + cudaGetErrorString(err));
+  launch_small<false>(R, A.nb * 2, passes, npass, sweeps, b, x, smem_bytes(A.nb, R.stride, npass), s);
   spmv(A, x, b, r, 1, nullptr, nullptr, s);
   restrict_(PT, r, rc, s);
 }
@@ -250,9 +267,7 @@ void small_pre(const Bsr& A, const PatchRecords& R, const int2* passes, int npas
 void small_post(const Bsr& A, const PatchRecords& R, const int2* passes, int npass, int sweeps, const BlockCsr& Pm,
                 const double* e, const double* b, double* x, cudaStream_t s) {
   prolong_add(Pm, e, x, s);
-  k_small_post<<<1, kThreads, smem_bytes(A.nb, R.stride, npass), s>>>(A.nb * 2, R, passes, npass, sweeps, b, x);
-  cudaError_t err = cudaGetLastError();
-  if (err != cudaSuccess) throw std::runtime_error(std::string("CUDA launch: ") + cudaGetErrorString(err));
+  launch_small<true>(R, A.nb * 2, passes, npass, sweeps, b, x, smem_bytes(A.nb, R.stride, npass), s);
 }
 
 }  // namespace dev
