@@ -123,9 +123,11 @@ int resident_grid(K kernel) {
 }
 
 /// Grid of an element-wise (grid-stride) kernel: one CTA per `threads`
-/// elements, at most one full wave of resident CTAs (2048 threads per SM):
-/// a 1.3-wave grid leaves its second wave latency-bound at low occupancy
-/// (config 2 V-cycle 0.721 -> 0.715 ms with the cap).
+/// elements; a grid of one to three waves of resident CTAs (2048 threads per
+/// SM) is folded into one wave, since a 1.3-wave grid leaves its second wave
+/// latency-bound at low occupancy (config 2 V-cycle 0.721 -> 0.715 ms). Longer
+/// streaming grids keep one element per thread (more loads in flight: the
+/// 6,128-CTA head operator apply runs 86 us instead of 99 us capped).
 inline int grid_for(int64_t n, int threads) {
   static const int64_t sms = [] {
     int dev = 0, v = 148;
@@ -133,10 +135,11 @@ inline int grid_for(int64_t n, int threads) {
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     return int64_t(v > 0 ? v : 148);
   }();
-  const int64_t cap = sms * std::max(1, 2048 / threads);
+  const int64_t wave = sms * std::max(1, 2048 / threads);
   int64_t g = (n + threads - 1) / threads;
   if (g < 1) g = 1;
-  if (g > cap) g = cap;
+  if (g > wave && g < 3 * wave) g = wave;
+  if (g > 148 * 64) g = 148 * 64;
   return int(g);
 }
 
