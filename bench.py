@@ -270,7 +270,7 @@ def run_hpmg(args, rank, world, local, dist):
     traffic = None
     try:
         prof = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                                           "r01_head_sweep_ncu.json")))
+                                           "r02_final_head_sweep_ncu.json")))
         if args.config == "config2":
             traffic = prof["dram_bytes_per_patch"] * 2 * B.level_patches(-1)
     except (OSError, KeyError, ValueError):
@@ -328,7 +328,7 @@ def run_hpmg(args, rank, world, local, dist):
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
                          "traffic_note": "bytes per V-cycle over the head sweeps: ncu dram read+write per "
-                                         "patch (profiles/r01_head_sweep_ncu.json) x 2 sweeps x patches",
+                                         "patch (profiles/r02_final_head_sweep_ncu.json) x 2 sweeps x patches",
                          "peak_source": src, "algorithmic_bytes_per_vcycle": vbytes,
                          "head_sweep_bytes_per_vcycle": head_bytes, "head_sweep_ms": head_sweep_ms,
                          "reference_storage_head_bytes_per_vcycle": vparts[0],
