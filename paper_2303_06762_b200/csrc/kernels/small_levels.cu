@@ -120,39 +120,58 @@ __device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, i
   const int lf = t >> 1, i = t & 1;
   const bool rowthread = t < NPM;
   double* rr = v.r + lp * kTP;
-  int q = 0;  // k % npass, kept incrementally (no division on the consumers' critical path)
-  for (int k = 0; k < total; ++k, q = q + 1 == npass ? 0 : q + 1) {
-    if (producer) {
-      // slot (k+2) % 3 was released by the __syncthreads() that closed pass k-1
+  if (producer) {
+    for (int k = 0; k < total; ++k) {
+      // slot (k+2) % 3 held pass k-1, whose records the consumers moved to
+      // registers before the barrier that closed pass k-2
       if (threadIdx.x == kConsumers && k + kStages - 1 < total) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         issue(k + kStages - 1);
       }
       __syncthreads();
-      continue;
     }
+    return;
+  }
+  // Software pipeline: everything of pass k that does not depend on x (the
+  // S_p row, the external blocks, the meta words, b_p) is loaded into
+  // registers during pass k-1, before the barrier that publishes pass k-1's
+  // x; after the barrier a pass is only x_e -> residual -> GEMV -> x_p.
+  double srow[NPM], w0[kExt], w1[kExt], bv = 0.0;
+  int f = -1, c[kExt];
+  bool active = false;
+  auto fetch = [&](int k, int q) {
     const int2 ps = v.pass[reverse ? npass - 1 - q : q];
-    if (trace && k < 1000) d_trace[4 * k] = clock64();
+    active = lp < ps.y && rowthread;
     ring_wait(&v.bar[k % kStages], unsigned((k / kStages) & 1));
-    if (trace && k < 1000) d_trace[4 * k + 1] = clock64();
+    if (!active) return;
     const double* rec = v.ring + (size_t(k % kStages) * kPass + lp) * R.stride;
-    if (lp < ps.y && rowthread) {
-      // row t of the full column-major S_p: S(t, j) at j*NPM + t
-      double srow[NPM];
+    // row t of the full column-major S_p: S(t, j) at j*NPM + t
 #pragma unroll
-      for (int j = 0; j < NPM; ++j) srow[j] = rec[j * NPM + t];
-      const int* meta = reinterpret_cast<const int*>(rec + R.meta_off);
-      const int f = meta[1 + lf];  // -1: row past the patch
-      const int* cols = meta + 1 + (NPM / 2) + lf * kExt;
-      const double* acol = rec + R.a_off + lf * kExt * 4 + i;  // column-major 2x2 blocks (zero for empty slots)
+    for (int j = 0; j < NPM; ++j) srow[j] = rec[j * NPM + t];
+    const int* meta = reinterpret_cast<const int*>(rec + R.meta_off);
+    f = meta[1 + lf];  // -1: row past the patch
+    const int* cols = meta + 1 + (NPM / 2) + lf * kExt;
+    const double* acol = rec + R.a_off + lf * kExt * 4 + i;  // column-major 2x2 blocks (zero for empty slots)
+#pragma unroll
+    for (int sl = 0; sl < kExt; ++sl) {
+      c[sl] = cols[sl];
+      w0[sl] = acol[sl * 4];
+      w1[sl] = acol[sl * 4 + 2];
+    }
+    bv = v.sb[2 * (f >= 0 ? f : 0) + i];
+  };
+  if (total > 0) fetch(0, 0);
+  int q = 0;  // k % npass, kept incrementally (no division on the critical path)
+  for (int k = 0; k < total; ++k) {
+    if (trace && k < 1000) d_trace[4 * k] = d_trace[4 * k + 1] = clock64();
+    if (active) {
       const int g = 2 * (f >= 0 ? f : 0) + i;
-      double a0 = v.sb[g], a1 = 0.0;
+      double a0 = bv, a1 = 0.0;
 #pragma unroll
       for (int sl = 0; sl < kExt; ++sl) {
-        const int c = cols[sl];
-        const double2 xe = *reinterpret_cast<const double2*>(v.sx + 2 * (c >= 0 ? c : 0));
-        a0 = fma(-acol[sl * 4], xe.x, a0);
-        a1 = fma(-acol[sl * 4 + 2], xe.y, a1);
+        const double2 xe = *reinterpret_cast<const double2*>(v.sx + 2 * (c[sl] >= 0 ? c[sl] : 0));
+        a0 = fma(-w0[sl], xe.x, a0);
+        a1 = fma(-w1[sl], xe.y, a1);
       }
       rr[t] = f >= 0 ? a0 + a1 : 0.0;
       __syncwarp(((1u << NPM) - 1u) << (threadIdx.x & 16));  // the patch's row threads
@@ -167,6 +186,8 @@ __device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, i
       }
       if (f >= 0) v.sx[g] = (d[0] + d[1]) + (d[2] + d[3]);
     }
+    q = q + 1 == npass ? 0 : q + 1;
+    if (k + 1 < total) fetch(k + 1, q);
     __syncthreads();
     if (trace && k < 1000) d_trace[4 * k + 3] = clock64();
   }
