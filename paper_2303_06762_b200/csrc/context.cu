@@ -560,6 +560,7 @@ void build_patch_inverses(hpmg_ctx& C, Level& V) {
     const dev::PatchRecords full = dev::record_layout(V.bs, V.max_nf, true);
     if (V.P.packed && V.k == 0 && nwaves > 12 && dev::small_level_fits(V.nb, full.stride, int(passes.size()))) {
       V.srec = full;
+      V.srec.rowext = 1;
       V.srec.rec = dalloc<double>(size_t(V.P.n) * V.srec.stride);
       dev::build_records(V.A, V.P, V.srec, C.s);
       V.npass = int(passes.size());

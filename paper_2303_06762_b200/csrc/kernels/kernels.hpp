@@ -93,6 +93,7 @@ struct PatchRecords {
   int bs = 2, max_nf = 0;
   int stride = 0, a_off = 0, meta_off = 0;  // in doubles
   int full = 0;  // 1: full np x np column-major inverse instead of the packed triangle
+  int rowext = 0;  // 1 (bs = 2, one-CTA levels): external blocks by patch row, [lf][i][slot][col]
   int n = 0;         // patches
   int dbg = 0;       // development: 4 = per-CTA globaltimer trace (sweep_trace)
 };

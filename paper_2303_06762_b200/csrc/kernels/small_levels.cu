@@ -151,12 +151,15 @@ __device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, i
     const int* meta = reinterpret_cast<const int*>(rec + R.meta_off);
     f = meta[1 + lf];  // -1: row past the patch
     const int* cols = meta + 1 + (NPM / 2) + lf * kExt;
-    const double* acol = rec + R.a_off + lf * kExt * 4 + i;  // column-major 2x2 blocks (zero for empty slots)
+    // the row's external-block entries [slot][col], contiguous (rowext
+    // records; zero for empty slots): two 16-byte loads, no bank conflicts
+    const double2* arow = reinterpret_cast<const double2*>(rec + R.a_off + t * kExt * 2);
 #pragma unroll
     for (int sl = 0; sl < kExt; ++sl) {
       c[sl] = cols[sl];
-      w0[sl] = acol[sl * 4];
-      w1[sl] = acol[sl * 4 + 2];
+      const double2 w = arow[sl];
+      w0[sl] = w.x;
+      w1[sl] = w.y;
     }
     bv = v.sb[2 * (f >= 0 ? f : 0) + i];
   };
@@ -279,7 +282,7 @@ bool small_level_fits(int nb, int record_stride, int npass) {
 
 void small_pre(const Bsr& A, const PatchRecords& R, const int2* passes, int npass, int sweeps, const BlockCsr& PT,
                const double* b, double* x, double* r, double* rc, cudaStream_t s) {
-  if (!R.full) throw std::runtime_error("small-level sweeps need full-inverse patch records");
+  if (!R.full || !R.rowext || R.bs != 2) throw std::runtime_error("small-level sweeps need full-inverse row-ordered records");
   launch_small<false>(R, A.nb * 2, passes, npass, sweeps, b, x, smem_bytes(A.nb, R.stride, npass), s);
   spmv(A, x, b, r, 1, nullptr, nullptr, s);
   restrict_(PT, r, rc, s);

@@ -315,8 +315,13 @@ __global__ void k_build_records(Bsr A, Patches P, PatchRecords R, int bs, int tr
       if (inside) continue;
       if (ne == kExt) break;  // excluded by the host check (triangle meshes)
       meta[1 + R.max_nf + lf * kExt + ne] = c;
-      for (int e = 0; e < blk; ++e)  // column-major block: (r, c) at c*bs + r
-        rec[R.a_off + (lf * kExt + ne) * blk + (e % bs) * bs + e / bs] = A.val[(size_t(f) * kSlots + sl) * blk + e];
+      for (int e = 0; e < blk; ++e) {  // A.val block row-major: (r, c) = e
+        const int r = e / bs, c = e % bs;
+        // column-major block: (r, c) at c*bs + r; rowext: a patch row's
+        // 2 x kExt values contiguous (one 32-byte read per row, bs = 2)
+        const int at = R.rowext ? ((lf * bs + r) * kExt + ne) * bs + c : (lf * kExt + ne) * blk + c * bs + r;
+        rec[R.a_off + at] = A.val[(size_t(f) * kSlots + sl) * blk + e];
+      }
       ++ne;
     }
   }
