@@ -313,8 +313,10 @@ double hpmg_time_spmv(hpmg_ctx* ctx, int reps, double* bytes);
 int hpmg_profile_levels(hpmg_ctx* ctx, int reps, double* out);
 /* Development probe of the device-loop cost: ms per iteration of a graph while
  * loop whose body is (mode 0) a countdown kernel only, (1) the V-cycle +
- * countdown, (2) an if-node holding the V-cycle, then the countdown (PCG's
- * nesting), (3) the V-cycle launched as a child-graph node + countdown. */
+ * countdown, (2) an if-node holding the V-cycle, then the countdown (the
+ * nesting of round 2's first PCG loop), (3) the V-cycle launched as a
+ * child-graph node + countdown; 32 + bits: PCG-shaped body (1 operator apply
+ * with the folded direction update, 2 update, 4 if-node, 8 r.z, 16 direction). */
 double hpmg_debug_loop_probe(hpmg_ctx* ctx, int mode, int iters);
 /* Development hook: clock64 timeline of the one-CTA small-level sweep. */
 void hpmg_debug_small_trace(int arm, long long* out);
