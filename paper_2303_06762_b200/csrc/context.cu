@@ -115,11 +115,19 @@ T* dalloc(size_t n) {
   }
   return static_cast<T*>(p);
 }
-template <typename T>
-T* dupload(const std::vector<T>& v, cudaStream_t s) {
+template <typename T, typename Alloc>
+T* dupload(const std::vector<T, Alloc>& v, cudaStream_t s) {
+  (void)s;
   T* p = dalloc<T>(v.size());
   const auto t0 = std::chrono::steady_clock::now();
-  if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  // on the (otherwise idle) allocation stream: a pageable copy synchronises
+  // with its stream first, and on the context stream that meant waiting for
+  // every kernel queued before it; the buffer is fresh, so nothing queued
+  // there can read it, and the copy is complete when dupload returns
+  if (!v.empty()) {
+    CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, alloc_stream()));
+    CK(cudaStreamSynchronize(alloc_stream()));
+  }
   g_upload_s() += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return p;
 }
@@ -185,6 +193,7 @@ struct hpmg_ctx {
   const double* post_x0 = nullptr;  // finest element origins [ne][2]
   double* post_red = nullptr;       // error partials [4][kRedBlocks] + result [4]
   double* coarse_inv = nullptr;
+  double* coarse_dense = nullptr;  // level-0 operator, dense row-major (setup scratch of the inverse)
   double* gemv_work = nullptr;
   int n0 = 0;
   dev::Reduce red;
@@ -483,7 +492,8 @@ void linearise_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, const DevRef
   if (finest)
     dev::assemble_rhs(V.nb, V.bs, k + 1, V.row_elems, V.block_facet, V.elem_facets, C.facet_dir, C.g_fac, acr,
                       stride, nc, V.geo, C.opt.inv_eps, rhs_out, s);
-  CK(cudaStreamSynchronize(s));
+  // no stream synchronisation here: the next level's kernels queue behind
+  // these on the same stream; dfree synchronises before releasing a buffer
   if (finest) {  // kept for recover_locals (same linearisation state)
     for (void* p : {(void*)C.fine_load, (void*)C.fine_wind, (void*)C.fine_mass})
       if (p) dfree(p);
@@ -591,12 +601,15 @@ std::vector<double> download_bsr(hpmg_ctx& C, Level& V) {
   return h;
 }
 
-dev::BlockCsr upload_blockcsr(const host::BlockCsrH& H, cudaStream_t s) {
+/// Block CSR to the device; values uploaded only when `values` (the
+/// prolongation's are formed on the device from the averaging base, the
+/// restriction's by the block transpose: their host arrays are not sent).
+dev::BlockCsr upload_blockcsr(const host::BlockCsrH& H, cudaStream_t s, bool values = true) {
   dev::BlockCsr D;
   D.nrows = H.nrows;
   D.ptr = dupload(H.ptr, s);
   D.col = dupload(H.col, s);
-  D.val = dupload(H.val, s);
+  D.val = values ? dupload(H.val, s) : dalloc<double>(H.col.size() * 4);
   return D;
 }
 
@@ -1362,8 +1375,10 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
   tr.mark("level uploads");
   C.rhs = dalloc<double>(int64_t(C.free_to_full.size()));
   // everything that depends on the linearisation state
+  const auto t_lin = clk::now();
   linearise(C, prob, k > 0 ? tTk.get() : tT0.get());
   auto t2 = clk::now();
+  (void)t2;
   C.setup_parts[2] = C.lin_parts[0];
   C.setup_parts[3] = C.lin_parts[1];
   C.setup_parts[4] = C.lin_parts[2];
@@ -1380,7 +1395,10 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
   auto t6 = clk::now();
   auto sec = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
   C.setup_parts[0] = sec(t0, t1);                      // mesh + tables
-  C.setup_parts[1] = sec(t1, t2) - C.lin_parts[0] - C.lin_parts[1] - C.lin_parts[2];  // plans + condensation
+  // plans + level uploads (host) + condensation (device); parts [2..4] are
+  // device times of phases that overlap the host's transfer uploads, so the
+  // parts need not add up to the total
+  C.setup_parts[1] = sec(t1, t_lin) + C.lin_parts[3];
   C.setup_parts[5] = sec(t5, t6);                      // workspace + graph
   C.setup_parts[6] = sec(t0, t6);
 }
@@ -1392,7 +1410,6 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
 void linearise(hpmg_ctx& C, const hpmg_problem* prob, const host::RefTensors* Tk) {
   using clk = std::chrono::steady_clock;
   auto sec = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
-  const auto t0 = clk::now();
   SetupTrace tr;
   const int k = C.opt.k;
   const host::TriMesh& fine = C.mesh[C.L];
@@ -1439,46 +1456,39 @@ void linearise(hpmg_ctx& C, const hpmg_problem* prob, const host::RefTensors* Tk
       if (t.joinable()) t.join();
     }
   } joiner{tp_thread};
+  // the condensation scratch sized once for the largest level (a regrowth
+  // between levels would synchronise the device)
+  {
+    size_t need = 0;
+    for (int l = 0; l <= C.L; ++l) need = std::max(need, size_t(C.mesh[l].ne()) * (C.ref0.T.nc * C.ref0.T.nc + C.ref0.T.nc));
+    if (k > 0) need = std::max(need, size_t(fine.ne()) * (C.refk.T.nc * C.refk.T.nc + C.refk.T.nc));
+    if (C.acr_cap < need) {
+      if (C.acr) dfree(C.acr);
+      C.acr = dalloc<double>(need);
+      C.acr_cap = need;
+    }
+  }
+  // The device work below is queued without host synchronisation (phase
+  // times from events on the stream), so the host joins and uploads the
+  // transfer structure while the condensation and the patch inverses run.
+  cudaEvent_t ev[5];
+  for (auto& x : ev) CK(cudaEventCreate(&x));
+  CK(cudaEventRecord(ev[0], C.s));
   for (int l = 0; l <= C.L; ++l)
     linearise_level(C, *C.lv[l], C.mesh[l], C.ref0, prob, C.lv[l]->finest ? C.rhs : nullptr,
                     C.advected ? &adv[l] : nullptr);
   if (k > 0) linearise_level(C, *C.head, fine, C.refk, prob, C.rhs, C.advected ? &wind_k : nullptr);
-  CK(cudaStreamSynchronize(C.s));
+  CK(cudaEventRecord(ev[1], C.s));
+  if (tr.on) CK(cudaStreamSynchronize(C.s));
   tr.mark("condense + assemble");
-  const auto t1 = clk::now();
   for (int l = 1; l <= C.L; ++l) build_patch_inverses(C, *C.lv[l]);
   if (k > 0) build_patch_inverses(C, *C.head);
-  CK(cudaStreamSynchronize(C.s));
+  CK(cudaEventRecord(ev[2], C.s));
+  if (tr.on) CK(cudaStreamSynchronize(C.s));
   tr.mark("patch inverses + records");
-  const auto t2 = clk::now();
-  // coarse dense inverse: Gauss-Jordan with partial pivoting on the device
-  // (kernels.cu dense_invert), still overlapping the host transfer plans
-  {
-    Level& V0 = *C.lv[0];
-    C.n0 = int(V0.n);
-    std::vector<double> A0 = download_bsr(C, V0), D(size_t(C.n0) * C.n0, 0.0);
-    for (int r = 0; r < V0.nb; ++r)
-      for (int sl = 0; sl < host::kSlots; ++sl) {
-        const int c = V0.plan.cols[size_t(r) * host::kSlots + sl];
-        if (c < 0) continue;
-        for (int i = 0; i < 2; ++i)
-          for (int j = 0; j < 2; ++j)
-            D[size_t(2 * r + i) * C.n0 + 2 * c + j] = A0[((size_t(r) * host::kSlots + sl) * 2 + i) * 2 + j];
-      }
-    DevTemps tmp;
-    double* dA = tmp.add(dupload(D, C.s));
-    if (!C.coarse_inv) C.coarse_inv = dalloc<double>(size_t(C.n0) * C.n0);
-    dev::dense_invert(C.n0, dA, C.coarse_inv, C.s);
-    CK(cudaStreamSynchronize(C.s));
-    if (!C.gemv_work) {
-      C.gemv_work = dalloc<double>(dev::dense_gemv_work(C.n0));
-      CK(cudaMemsetAsync(C.gemv_work, 0, sizeof(double) * dev::dense_gemv_work(C.n0), C.s));  // arrival counters
-    }
-  }
-  tr.mark("coarse inverse");
-  const auto t_coarse = clk::now();
-  // transfers: structure once (the helper thread above), the harmonic
-  // correction from the current fine operators on the device
+  // transfers: structure once (the helper thread above), uploaded while the
+  // device works; the harmonic correction from the current fine operators
+  const auto t_tp = clk::now();
   if (need_tp) {
     tp_thread.join();
     tr.mark("transfer plans (host wait)");
@@ -1486,8 +1496,8 @@ void linearise(hpmg_ctx& C, const hpmg_problem* prob, const host::RefTensors* Tk
       if (!tp_errs[l].empty()) throw std::runtime_error(tp_errs[l]);
       Level& V = *C.lv[l];
       const host::TransferPlan& T = tp[l];
-      V.Pm = upload_blockcsr(T.P, C.s);
-      V.PT = upload_blockcsr(T.PT, C.s);
+      V.Pm = upload_blockcsr(T.P, C.s, false);  // P = base + correction (corrected_prolongation)
+      V.PT = upload_blockcsr(T.PT, C.s, false);
       V.Pm.nnz = V.PT.nnz = int(T.P.col.size());
       dev::TransferDev& D = V.tdev;
       D.nelem = T.nelem;
@@ -1500,20 +1510,44 @@ void linearise(hpmg_ctx& C, const hpmg_problem* prob, const host::RefTensors* Tk
       D.avg_ptr = dupload(T.avg.ptr, C.s);
       D.avg_col = dupload(T.avg.col, C.s);
       D.avg_val = dupload(T.avg.val, C.s);
-      D.base = dupload(T.P.val, C.s);
+      D.base = dalloc<double>(T.P.col.size() * 4);
+      dev::prolong_base(V.Pm, D, C.s);  // the averaging values in P's pattern
       D.tperm = dupload(T.tperm, C.s);
       V.p_nnz = 4.0 * double(T.P.col.size());
     }
-    CK(cudaStreamSynchronize(C.s));
   }
+  const double t_upload = sec(t_tp, clk::now());
   for (int l = 1; l <= C.L; ++l) dev::corrected_prolongation(C.lv[l]->A, C.lv[l]->tdev, C.lv[l]->Pm, C.lv[l]->PT, C.s);
-  CK(cudaStreamSynchronize(C.s));
+  CK(cudaEventRecord(ev[3], C.s));
   tr.mark("transfer upload + correction");
-  const auto t4 = clk::now();
-  C.lin_parts[0] = sec(t1, t2);
-  C.lin_parts[1] = sec(t_coarse, t4);  // transfers: what is left after the overlap
-  C.lin_parts[2] = sec(t2, t_coarse);
-  C.lin_parts[3] = sec(t0, t1);
+  // coarse dense inverse: Gauss-Jordan with partial pivoting on the device
+  // (kernels.cu dense_invert) of the level-0 operator, densified on the device
+  {
+    Level& V0 = *C.lv[0];
+    C.n0 = int(V0.n);
+    if (!C.coarse_inv) C.coarse_inv = dalloc<double>(size_t(C.n0) * C.n0);
+    if (!C.coarse_dense) C.coarse_dense = dalloc<double>(size_t(C.n0) * C.n0);
+    dev::bsr_to_dense(V0.A, C.coarse_dense, C.s);
+    dev::dense_invert(C.n0, C.coarse_dense, C.coarse_inv, C.s);  // synchronises (singularity status)
+    if (!C.gemv_work) {
+      C.gemv_work = dalloc<double>(dev::dense_gemv_work(C.n0));
+      CK(cudaMemsetAsync(C.gemv_work, 0, sizeof(double) * dev::dense_gemv_work(C.n0), C.s));  // arrival counters
+    }
+  }
+  CK(cudaEventRecord(ev[4], C.s));
+  CK(cudaStreamSynchronize(C.s));
+  tr.mark("coarse inverse");
+  auto el = [&](int a, int b) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev[a], ev[b]);
+    return 1e-3 * double(ms);
+  };
+  C.lin_parts[0] = el(1, 2);             // patch inverses + records (device)
+  C.lin_parts[1] = t_upload + el(2, 3);  // transfer join + uploads (host) + correction (device)
+  C.lin_parts[2] = el(3, 4);             // coarse densify + inverse (device)
+  C.lin_parts[3] = el(0, 1);             // condensation + assembly (device)
+  for (auto& x : ev) cudaEventDestroy(x);
+
 }
 
 template <typename F>
@@ -1654,7 +1688,7 @@ void hpmg_destroy(hpmg_ctx* ctx) {
   if (ctx->s_h2d) cudaStreamDestroy(ctx->s_h2d);
   if (ctx->s_d2h) cudaStreamDestroy(ctx->s_d2h);
   for (double* p : ctx->gm_basis) fr(p);
-  for (void* p : {(void*)ctx->coarse_inv, (void*)ctx->gemv_work, (void*)ctx->red.partial, (void*)ctx->red.counter,
+  for (void* p : {(void*)ctx->coarse_inv, (void*)ctx->coarse_dense, (void*)ctx->gemv_work, (void*)ctx->red.partial, (void*)ctx->red.counter,
                   (void*)ctx->sc, (void*)ctx->rhs, (void*)ctx->g_fac, (void*)ctx->facet_dir, (void*)ctx->kx,
                   (void*)ctx->kb, (void*)ctx->kr, (void*)ctx->kz, (void*)ctx->kp, (void*)ctx->kAp, (void*)ctx->ktmp,
                   (void*)ctx->io_a, (void*)ctx->io_b, (void*)ctx->pres, (void*)ctx->div, (void*)ctx->urhs,

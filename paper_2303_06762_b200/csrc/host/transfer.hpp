@@ -13,6 +13,8 @@
 #include <climits>
 #include <new>
 #include <array>
+#include <memory>
+#include <utility>
 #include <thread>
 #include <vector>
 
@@ -21,10 +23,35 @@
 namespace hpmg {
 namespace host {
 
+/// std::allocator whose value-initialisation (resize) leaves elements
+/// uninitialised: the large index/value arrays below are filled in parallel,
+/// which also spreads their first-touch page faults over the threads.
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = NoInitAlloc<U>;
+  };
+  NoInitAlloc() = default;
+  template <class U>
+  NoInitAlloc(const NoInitAlloc<U>&) noexcept {}
+  template <class U>
+  void construct(U* p) noexcept {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <class U, class... Args>
+  void construct(U* p, Args&&... args) {
+    ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+  }
+};
+template <class T>
+using BigVec = std::vector<T, NoInitAlloc<T>>;
+
 struct BlockCsrH {
   int nrows = 0, ncols = 0;
-  std::vector<int> ptr{0}, col;
-  std::vector<double> val;  // 4 per block, row-major [t][t']
+  std::vector<int> ptr{0};
+  BigVec<int> col;
+  BigVec<double> val;  // 4 per block, row-major [t][t']
 };
 
 /// 1 - 2 * (barycentric coordinate of the opposite vertex): the CR basis of
@@ -184,12 +211,12 @@ struct TransferPlan {
   static constexpr int kMedMax = 3, kColMax = kCorrCap;
   int nrows = 0, ncols = 0, nelem = 0;
   BlockCsrH avg;                      // fine rows of the averaging transfer
-  BlockCsrH P;                        // final pattern, val = averaging part
+  BlockCsrH P;                        // final pattern (values built on the device)
   std::vector<int> nmed, med;         // [nelem], [nelem][3] fine blocks (ascending facet id)
   std::vector<int> ncol, col;         // [nelem], [nelem][kColMax] coarse blocks (ascending)
   std::vector<int> pos;               // [nelem][3][kColMax] block index into P (or -1)
-  BlockCsrH PT;                       // transposed pattern
-  std::vector<int> tperm;             // PT block d <- P block tperm[d] (2x2 transposed)
+  BlockCsrH PT;                       // transposed pattern (values built on the device)
+  BigVec<int> tperm;                  // PT block d <- P block tperm[d] (2x2 transposed)
 };
 
 inline TransferPlan transfer_plan(const LevelPlan& C, const LevelPlan& F, const Refinement& R) {
@@ -199,13 +226,17 @@ inline TransferPlan transfer_plan(const LevelPlan& C, const LevelPlan& F, const 
   auto rows = averaging_blocks(C, F, R);
   T.avg.nrows = F.nb;
   T.avg.ncols = C.nb;
-  for (int rf = 0; rf < F.nb; ++rf) {
+  T.avg.ptr.assign(F.nb + 1, 0);
+  for (int rf = 0; rf < F.nb; ++rf) T.avg.ptr[rf + 1] = T.avg.ptr[rf] + rows[rf].n;
+  T.avg.col.resize(T.avg.ptr[F.nb]);
+  T.avg.val.resize(size_t(T.avg.ptr[F.nb]) * 4);
+  parallel_for(F.nb, [&](int rf) {
     for (int q = 0; q < rows[rf].n; ++q) {
-      T.avg.col.push_back(rows[rf].col[q]);
-      for (int t = 0; t < 4; ++t) T.avg.val.push_back(rows[rf].v[q][t]);
+      const int d = T.avg.ptr[rf] + q;
+      T.avg.col[d] = rows[rf].col[q];
+      for (int t = 0; t < 4; ++t) T.avg.val[size_t(d) * 4 + t] = rows[rf].v[q][t];
     }
-    T.avg.ptr.push_back(int(T.avg.col.size()));
-  }
+  });
   const TriMesh& fm = *F.mesh;
   T.nelem = int(R.children.size());
   T.nmed.assign(T.nelem, 0);
@@ -247,10 +278,9 @@ inline TransferPlan transfer_plan(const LevelPlan& C, const LevelPlan& F, const 
     while (i < a.n || j < c.n) {
       const int ca = i < a.n ? a.col[i] : INT_MAX, cc = j < c.n ? c.col[j] : INT_MAX;
       const int cm = std::min(ca, cc);
-      if (col) {
-        col[n] = cm;
+      if (col) col[n] = cm;
+      if (val)
         for (int t = 0; t < 4; ++t) val[size_t(n) * 4 + t] = ca == cm ? a.v[i][t] : 0.0;
-      }
       if (ca == cm) ++i;
       if (cc == cm) ++j;
       ++n;
@@ -261,8 +291,9 @@ inline TransferPlan transfer_plan(const LevelPlan& C, const LevelPlan& F, const 
   T.P.ptr.assign(F.nb + 1, 0);
   for (int rf = 0; rf < F.nb; ++rf) T.P.ptr[rf + 1] = T.P.ptr[rf] + cnt_row[rf];
   T.P.col.resize(T.P.ptr[F.nb]);
-  T.P.val.resize(size_t(T.P.ptr[F.nb]) * 4);
-  parallel_for(F.nb, [&](int rf) { merge(rf, &T.P.col[T.P.ptr[rf]], &T.P.val[size_t(T.P.ptr[rf]) * 4]); });
+  // P.val stays empty: the averaging values in P's pattern (the base the
+  // correction is added to) are merged on the device (dev::prolong_base)
+  parallel_for(F.nb, [&](int rf) { merge(rf, &T.P.col[T.P.ptr[rf]], nullptr); });
   T.pos.assign(size_t(T.nelem) * 3 * TransferPlan::kColMax, -1);
   parallel_for(T.nelem, [&](int e) {
     for (int i = 0; i < T.nmed[e]; ++i) {
@@ -281,8 +312,8 @@ inline TransferPlan transfer_plan(const LevelPlan& C, const LevelPlan& F, const 
   for (int c : T.P.col) cnt[c + 1]++;
   for (int i = 0; i < C.nb; ++i) cnt[i + 1] += cnt[i];
   T.PT.ptr = cnt;
-  T.PT.col.assign(T.P.col.size(), 0);
-  T.tperm.assign(T.P.col.size(), 0);
+  T.PT.col.resize(T.P.col.size());  // every entry written by the scatter below
+  T.tperm.resize(T.P.col.size());
   std::vector<int> at(cnt.begin(), cnt.end() - 1);
   for (int r = 0; r < F.nb; ++r)
     for (int q = T.P.ptr[r]; q < T.P.ptr[r + 1]; ++q) {
@@ -290,7 +321,7 @@ inline TransferPlan transfer_plan(const LevelPlan& C, const LevelPlan& F, const 
       T.PT.col[d] = r;
       T.tperm[d] = q;
     }
-  T.PT.val.assign(T.P.val.size(), 0.0);
+  // PT.val stays empty: the device fills it from P (k_block_transpose_perm)
   return T;
 }
 

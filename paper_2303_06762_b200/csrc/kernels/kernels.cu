@@ -1847,6 +1847,33 @@ void jacobi_combine(int nb, int bs, const Patches& P, const double* d, int max_n
   HPMG_LAUNCH_CHECK();
 }
 
+namespace {
+/// base[q] = the averaging block of P's block q (zero where only the
+/// correction has a block): a sorted merge of the two column lists per row
+__global__ void k_prolong_base(int nrows, const int* __restrict__ pptr, const int* __restrict__ pcol,
+                               const int* __restrict__ aptr, const int* __restrict__ acol,
+                               const double* __restrict__ aval, double* __restrict__ base) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
+    int j = aptr[r];
+    const int je = aptr[r + 1];
+    for (int q = pptr[r]; q < pptr[r + 1]; ++q) {
+      const int c = pcol[q];
+      while (j < je && acol[j] < c) ++j;
+      const bool hit = j < je && acol[j] == c;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) base[size_t(q) * 4 + t] = hit ? aval[size_t(j) * 4 + t] : 0.0;
+    }
+  }
+}
+}  // namespace
+
+void prolong_base(const BlockCsr& P, const TransferDev& T, cudaStream_t s) {
+  if (P.nrows > 0)
+    k_prolong_base<<<grid_for(P.nrows, 256), 256, 0, s>>>(P.nrows, P.ptr, P.col, T.avg_ptr, T.avg_col, T.avg_val,
+                                                             T.base);
+  HPMG_LAUNCH_CHECK();
+}
+
 void corrected_prolongation(const Bsr& A, const TransferDev& T, BlockCsr& P, BlockCsr& PT, cudaStream_t s) {
   cudaError_t err = cudaMemcpyAsync(P.val, T.base, sizeof(double) * 4 * size_t(T.nnz), cudaMemcpyDeviceToDevice, s);
   if (err != cudaSuccess) throw std::runtime_error(std::string("CUDA copy: ") + cudaGetErrorString(err));
@@ -1877,6 +1904,27 @@ void dense_gemv(int n, const double* inv, const double* b, double* x, double* wo
   const int chunks = (n + kGemvChunk - 1) / kGemvChunk;
   unsigned* counter = reinterpret_cast<unsigned*>(work + size_t(n) * chunks);
   k_gemv<<<dim3((n + 127) / 128, chunks), 128, 0, s>>>(n, chunks, inv, b, work, counter, x);
+  HPMG_LAUNCH_CHECK();
+}
+
+namespace {
+__global__ void k_bsr_to_dense(Bsr A, double* __restrict__ D) {
+  const int n = A.nb * 2;
+  const int64_t tot = int64_t(A.nb) * kSlots * 4;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t q = e >> 2;  // block (row, slot)
+    const int r = int(q / kSlots), ij = int(e & 3), i = ij >> 1, j = ij & 1;
+    const int c = A.cols[q];
+    if (c >= 0) D[int64_t(2 * r + i) * n + 2 * c + j] = A.val[e];
+  }
+}
+}  // namespace
+
+void bsr_to_dense(const Bsr& A, double* D, cudaStream_t s) {
+  if (A.bs != 2) throw std::runtime_error("bsr_to_dense: lowest-order (bs = 2) operators only");
+  const int n = A.nb * 2;
+  cudaMemsetAsync(D, 0, sizeof(double) * size_t(n) * n, s);
+  k_bsr_to_dense<<<grid_for(int64_t(A.nb) * kSlots * 4, 256), 256, 0, s>>>(A, D);
   HPMG_LAUNCH_CHECK();
 }
 

@@ -139,11 +139,15 @@ constexpr int kTransferColMax = 16;
 /// P = averaging + harmonic correction -A_TT^{-1} (A I_avg)_T per coarse
 /// element (reference transfer.hpp:95-133) from the fine operator A on the
 /// device, into P's fixed pattern; PT by the block permutation.
+/// T.base = the averaging transfer's blocks in P's final pattern (zero elsewhere); T.avg_* uploaded
+void prolong_base(const BlockCsr& P, const TransferDev& T, cudaStream_t s);
 void corrected_prolongation(const Bsr& A, const TransferDev& T, BlockCsr& P, BlockCsr& PT, cudaStream_t s);
 void prolong_add(const BlockCsr& P, const double* e, double* x, cudaStream_t s);
 void restrict_(const BlockCsr& PT, const double* r, double* rc, cudaStream_t s,
                double* xc_zero = nullptr);  // optionally zeroes xc (same length as rc)
 void dense_gemv(int n, const double* inv_colmajor, const double* b, double* x, double* work, cudaStream_t s);
+/// D (n x n row-major, n = 2 nb) = the lowest-order operator A, zeros elsewhere
+void bsr_to_dense(const Bsr& A, double* D, cudaStream_t s);
 size_t dense_gemv_work(int n);  // doubles of dense_gemv's partial-sum scratch
 /// Gauss-Jordan inverse with partial pivoting of a dense row-major matrix (setup).
 void dense_invert(int n, const double* A_rowmajor, double* inv_colmajor, cudaStream_t s);
