@@ -18,6 +18,8 @@
 #include <functional>
 #include <mutex>
 #include <thread>
+#include <memory>
+#include <utility>
 #include <vector>
 
 #include "../kernels/condense.cuh"
@@ -57,6 +59,30 @@ inline void parallel_for(int n, F&& f) {
   for (auto& th : pool) th.join();
   if (err) std::rethrow_exception(err);
 }
+
+/// std::allocator whose value-initialisation (resize) leaves elements
+/// uninitialised: the large index/value arrays below are filled in parallel,
+/// which also spreads their first-touch page faults over the threads.
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = NoInitAlloc<U>;
+  };
+  NoInitAlloc() = default;
+  template <class U>
+  NoInitAlloc(const NoInitAlloc<U>&) noexcept {}
+  template <class U>
+  void construct(U* p) noexcept {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <class U, class... Args>
+  void construct(U* p, Args&&... args) {
+    ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+  }
+};
+template <class T>
+using BigVec = std::vector<T, NoInitAlloc<T>>;
 
 /// Compressed adjacency built from (key, value) pairs in input order.
 struct Csr32 {
@@ -104,10 +130,10 @@ struct LevelPlan {
   int nb = 0;                         // free facets = block rows
   std::vector<int> block_facet;       // block -> mesh facet
   std::vector<int> facet_block;       // mesh facet -> block or -1 (Dirichlet)
-  std::vector<int> cols;              // [nb][kSlots] block columns, -1 = empty
+  BigVec<int> cols;                   // [nb][kSlots] block columns, -1 = empty
   // assembly gather per (row, slot): up to two (element, local row facet, local col facet)
-  std::vector<int> gath;              // [nb][kSlots][2][3]
-  std::vector<int> row_elems;         // [nb][2][2] (element, local facet) ascending element
+  BigVec<int> gath;                   // [nb][kSlots][2][3]
+  BigVec<int> row_elems;              // [nb][2][2] (element, local facet) ascending element
   // vertex patches (ascending vertex id, empty ones dropped)
   int npatch = 0, max_patch_f = 0;
   std::vector<int> patch_nf;          // facets per patch
@@ -139,10 +165,15 @@ inline LevelPlan make_level(const TriMesh& m, int k) {
       L.block_facet.push_back(f);
     }
   // ELL pattern: facets sharing an element with the row facet, sorted
-  L.cols.assign(size_t(L.nb) * kSlots, -1);
-  L.gath.assign(size_t(L.nb) * kSlots * 6, -1);
-  L.row_elems.assign(size_t(L.nb) * 4, -1);
+  // uninitialised, each row's slots set to -1 by its own thread below (a
+  // serial fill of these ~30 MB cost more than the rest of the plan)
+  L.cols.resize(size_t(L.nb) * kSlots);
+  L.gath.resize(size_t(L.nb) * kSlots * 6);
+  L.row_elems.resize(size_t(L.nb) * 4);
   parallel_for(L.nb, [&](int r) {
+    std::fill_n(&L.cols[size_t(r) * kSlots], kSlots, -1);
+    std::fill_n(&L.gath[size_t(r) * kSlots * 6], kSlots * 6, -1);
+    std::fill_n(&L.row_elems[size_t(r) * 4], 4, -1);
     const int f = L.block_facet[r];
     int nbv[6], nnb = 0;  // facets of the <= 2 elements of f, then sorted unique
     int slot_e = 0;
@@ -217,6 +248,8 @@ inline LevelPlan make_level(const TriMesh& m, int k) {
   }
   std::vector<int> vertex_patch(m.nv(), -1);
   L.facet_patches.assign(size_t(L.nb) * 2, -1);
+  L.patch_nf.reserve(m.nv());
+  L.patch_fac.reserve(size_t(m.nv()) * kMaxPatchF);
   for (int v = 0; v < m.nv(); ++v) {
     int blocks[kMaxPatchF], nblk = 0;
     for (const int* fp = vp.begin(v); fp != vp.end(v); ++fp)

@@ -23,30 +23,6 @@
 namespace hpmg {
 namespace host {
 
-/// std::allocator whose value-initialisation (resize) leaves elements
-/// uninitialised: the large index/value arrays below are filled in parallel,
-/// which also spreads their first-touch page faults over the threads.
-template <class T>
-struct NoInitAlloc : std::allocator<T> {
-  template <class U>
-  struct rebind {
-    using other = NoInitAlloc<U>;
-  };
-  NoInitAlloc() = default;
-  template <class U>
-  NoInitAlloc(const NoInitAlloc<U>&) noexcept {}
-  template <class U>
-  void construct(U* p) noexcept {
-    ::new (static_cast<void*>(p)) U;
-  }
-  template <class U, class... Args>
-  void construct(U* p, Args&&... args) {
-    ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
-  }
-};
-template <class T>
-using BigVec = std::vector<T, NoInitAlloc<T>>;
-
 struct BlockCsrH {
   int nrows = 0, ncols = 0;
   std::vector<int> ptr{0};
