@@ -1598,6 +1598,9 @@ __global__ void k_to_blocks(int nb, int nfd, const double* __restrict__ ref, dou
 /// k_to_blocks that also zeroes `zero` (the cycle's x) in the same pass
 __global__ void k_to_blocks_zero(int nb, int nfd, const double* __restrict__ ref, double* __restrict__ blk,
                                  double* __restrict__ zero) {
+  // the first pre-smoothing wave (programmatic dependent launch) may start
+  // its record copies now; it reads b and x only after this grid completes
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int bs = 2 * nfd;
   const int64_t n = int64_t(nb) * bs;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
@@ -1607,7 +1610,10 @@ __global__ void k_to_blocks_zero(int nb, int nfd, const double* __restrict__ ref
     zero[t] = 0.0;
   }
 }
+/// (in the drop-in graph launched with programmatic dependent launch after the
+/// last post-smoothing wave: its CTAs come up during that wave's tail)
 __global__ void k_to_reference(int nb, int nfd, const double* __restrict__ blk, double* __restrict__ ref) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int bs = 2 * nfd;
   const int64_t n = int64_t(nb) * bs;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
@@ -2157,7 +2163,17 @@ void set_io_nodes(cudaGraphExec_t ge, cudaGraphNode_t in_node, cudaGraphNode_t o
   }
 }
 void to_reference(int nb, int nfd, const double* blk, double* ref, cudaStream_t s) {
-  k_to_reference<<<grid_for(int64_t(nb) * 2 * nfd, 256), 256, 0, s>>>(nb, nfd, blk, ref);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid_for(int64_t(nb) * 2 * nfd, 256)));
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k_to_reference, nb, nfd, blk, ref);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA launch (to_reference): ") + cudaGetErrorString(e));
   HPMG_LAUNCH_CHECK();
 }
 void uzawa_rhs(int nb, int bs, const double* rhs0, const int* row_elems, const ElemGeo* geo, const double* p,
