@@ -1471,8 +1471,15 @@ void linearise(hpmg_ctx& C, const hpmg_problem* prob, const host::RefTensors* Tk
   // The device work below is queued without host synchronisation (phase
   // times from events on the stream), so the host joins and uploads the
   // transfer structure while the condensation and the patch inverses run.
-  cudaEvent_t ev[5];
-  for (auto& x : ev) CK(cudaEventCreate(&x));
+  struct Events {  // released on every exit path (setup errors throw)
+    cudaEvent_t e[5] = {};
+    ~Events() {
+      for (auto x : e)
+        if (x) cudaEventDestroy(x);
+    }
+  } evs;
+  cudaEvent_t* ev = evs.e;
+  for (int i = 0; i < 5; ++i) CK(cudaEventCreate(&ev[i]));
   CK(cudaEventRecord(ev[0], C.s));
   for (int l = 0; l <= C.L; ++l)
     linearise_level(C, *C.lv[l], C.mesh[l], C.ref0, prob, C.lv[l]->finest ? C.rhs : nullptr,
@@ -1546,7 +1553,6 @@ void linearise(hpmg_ctx& C, const hpmg_problem* prob, const host::RefTensors* Tk
   C.lin_parts[1] = t_upload + el(2, 3);  // transfer join + uploads (host) + correction (device)
   C.lin_parts[2] = el(3, 4);             // coarse densify + inverse (device)
   C.lin_parts[3] = el(0, 1);             // condensation + assembly (device)
-  for (auto& x : ev) cudaEventDestroy(x);
 
 }
 
