@@ -292,7 +292,8 @@ def run_hpmg(args, rank, world, local, dist):
         krylov["gmres50_config5_re1"] = krylov_overhead(H, B5, restart=50)
         krylov["note"] = ("whole solve = one CUDA-graph launch (device conditional nodes); overhead = per-iteration "
                           "cost minus the V-cycle and the operator apply it contains (vector updates, reductions, "
-                          "for GMRES the fused MGS step kernels, at j from 5 to 25)")
+                          "for GMRES the fused MGS step kernels, at j from 5 to 25); slope of capped solves, "
+                          "PCG 5..45 and GMRES 5..25 iterations, best of 5 wall-clock runs each")
         B5.close()
     out = None
     if rank == 0:
@@ -490,21 +491,25 @@ def finish_cpu_tts(proc, timeout):
 
 def krylov_overhead(H, B, restart=0):
     """Per-iteration cost of the device Krylov loop (slope of capped solves,
-    5 and 25 iterations, best of 3) against the V-cycle and the operator
-    apply it contains."""
+    best of 5: PCG 5 and 45 iterations, GMRES 5 and 25, i.e. Arnoldi steps
+    j = 5..25) against the V-cycle and the operator apply it contains."""
     rhs = B.rhs()
     solver = H.pcg if B.symmetric() else H.gmres
+    hi = 45 if B.symmetric() else 25
 
     def t(k):
         best = 1e9
-        for _ in range(3):
+        for _ in range(5):
             t0 = time.perf_counter()
             solver(B, rhs, opt=H.KrylovOptions(max_iterations=k, rel_tol=1e-30, abs_tol=0.0, restart=restart))
             best = min(best, time.perf_counter() - t0)
         return best
 
+    _, st = solver(B, rhs, opt=H.KrylovOptions(max_iterations=hi, rel_tol=1e-30, abs_tol=0.0, restart=restart))
+    if st.iterations != hi:  # stopped early (breakdown past machine precision): the shorter window
+        hi = 25
     t(3)
-    per_it = (t(25) - t(5)) / 20 * 1e3
+    per_it = (t(hi) - t(5)) / (hi - 5) * 1e3
     vc = B.time_apply(20)[0]
     sp = B.time_spmv(20)[0]
     return {"solver": solver.__name__ + (f"({restart})" if restart else ""), "ms_per_iteration": per_it,
