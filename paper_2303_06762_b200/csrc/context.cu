@@ -194,6 +194,8 @@ struct hpmg_ctx {
   double* post_red = nullptr;       // error partials [4][kRedBlocks] + result [4]
   double* coarse_inv = nullptr;
   double* coarse_dense = nullptr;  // level-0 operator, dense row-major (setup scratch of the inverse)
+  dev::DenseInvertWork gj;         // Gauss-Jordan scratch of the coarse inverse
+  cudaStream_t s_coarse = nullptr; // setup: the coarse inverse runs beside the finer levels' work
   double* gemv_work = nullptr;
   int n0 = 0;
   dev::Reduce red;
@@ -1472,16 +1474,34 @@ void linearise(hpmg_ctx& C, const hpmg_problem* prob, const host::RefTensors* Tk
   // times from events on the stream), so the host joins and uploads the
   // transfer structure while the condensation and the patch inverses run.
   struct Events {  // released on every exit path (setup errors throw)
-    cudaEvent_t e[5] = {};
+    cudaEvent_t e[8] = {};
     ~Events() {
       for (auto x : e)
         if (x) cudaEventDestroy(x);
     }
   } evs;
   cudaEvent_t* ev = evs.e;
-  for (int i = 0; i < 5; ++i) CK(cudaEventCreate(&ev[i]));
+  for (int i = 0; i < 8; ++i) CK(cudaEventCreate(&ev[i]));
+  // coarse-inverse buffers first: allocations stay out of the queued work
+  Level& V0 = *C.lv[0];
+  C.n0 = int(V0.n);
+  if (!C.coarse_inv) C.coarse_inv = dalloc<double>(size_t(C.n0) * C.n0);
+  if (!C.coarse_dense) C.coarse_dense = dalloc<double>(size_t(C.n0) * C.n0);
+  dev::dense_invert_alloc(C.n0, C.gj);
+  if (!C.s_coarse) CK(cudaStreamCreateWithFlags(&C.s_coarse, cudaStreamNonBlocking));
   CK(cudaEventRecord(ev[0], C.s));
-  for (int l = 0; l <= C.L; ++l)
+  linearise_level(C, V0, C.mesh[0], C.ref0, prob, V0.finest ? C.rhs : nullptr, C.advected ? &adv[0] : nullptr);
+  // the coarse dense inverse (Gauss-Jordan with partial pivoting, kernels.cu
+  // dense_invert_async) of the level-0 operator, densified on the device, on
+  // a side stream: its latency-bound pivot steps run beside the finer levels'
+  // condensation and patch inverses
+  CK(cudaEventRecord(ev[5], C.s));
+  CK(cudaStreamWaitEvent(C.s_coarse, ev[5], 0));
+  CK(cudaEventRecord(ev[6], C.s_coarse));
+  dev::bsr_to_dense(V0.A, C.coarse_dense, C.s_coarse);
+  dev::dense_invert_async(C.n0, C.coarse_dense, C.coarse_inv, C.gj, C.s_coarse);
+  CK(cudaEventRecord(ev[7], C.s_coarse));
+  for (int l = 1; l <= C.L; ++l)
     linearise_level(C, *C.lv[l], C.mesh[l], C.ref0, prob, C.lv[l]->finest ? C.rhs : nullptr,
                     C.advected ? &adv[l] : nullptr);
   if (k > 0) linearise_level(C, *C.head, fine, C.refk, prob, C.rhs, C.advected ? &wind_k : nullptr);
@@ -1527,23 +1547,16 @@ void linearise(hpmg_ctx& C, const hpmg_problem* prob, const host::RefTensors* Tk
   for (int l = 1; l <= C.L; ++l) dev::corrected_prolongation(C.lv[l]->A, C.lv[l]->tdev, C.lv[l]->Pm, C.lv[l]->PT, C.s);
   CK(cudaEventRecord(ev[3], C.s));
   tr.mark("transfer upload + correction");
-  // coarse dense inverse: Gauss-Jordan with partial pivoting on the device
-  // (kernels.cu dense_invert) of the level-0 operator, densified on the device
-  {
-    Level& V0 = *C.lv[0];
-    C.n0 = int(V0.n);
-    if (!C.coarse_inv) C.coarse_inv = dalloc<double>(size_t(C.n0) * C.n0);
-    if (!C.coarse_dense) C.coarse_dense = dalloc<double>(size_t(C.n0) * C.n0);
-    dev::bsr_to_dense(V0.A, C.coarse_dense, C.s);
-    dev::dense_invert(C.n0, C.coarse_dense, C.coarse_inv, C.s);  // synchronises (singularity status)
-    if (!C.gemv_work) {
-      C.gemv_work = dalloc<double>(dev::dense_gemv_work(C.n0));
-      CK(cudaMemsetAsync(C.gemv_work, 0, sizeof(double) * dev::dense_gemv_work(C.n0), C.s));  // arrival counters
-    }
+  // join the coarse inverse
+  CK(cudaStreamWaitEvent(C.s, ev[7], 0));
+  if (!C.gemv_work) {
+    C.gemv_work = dalloc<double>(dev::dense_gemv_work(C.n0));
+    CK(cudaMemsetAsync(C.gemv_work, 0, sizeof(double) * dev::dense_gemv_work(C.n0), C.s));  // arrival counters
   }
   CK(cudaEventRecord(ev[4], C.s));
+  dev::dense_invert_check(C.gj, C.s_coarse);  // synchronises the side stream; throws if singular
   CK(cudaStreamSynchronize(C.s));
-  tr.mark("coarse inverse");
+  tr.mark("coarse inverse (joined)");
   auto el = [&](int a, int b) {
     float ms = 0;
     cudaEventElapsedTime(&ms, ev[a], ev[b]);
@@ -1551,7 +1564,7 @@ void linearise(hpmg_ctx& C, const hpmg_problem* prob, const host::RefTensors* Tk
   };
   C.lin_parts[0] = el(1, 2);             // patch inverses + records (device)
   C.lin_parts[1] = t_upload + el(2, 3);  // transfer join + uploads (host) + correction (device)
-  C.lin_parts[2] = el(3, 4);             // coarse densify + inverse (device)
+  C.lin_parts[2] = el(6, 7);             // coarse densify + inverse (device, side stream, overlapped)
   C.lin_parts[3] = el(0, 1);             // condensation + assembly (device)
 
 }
@@ -1694,6 +1707,8 @@ void hpmg_destroy(hpmg_ctx* ctx) {
   if (ctx->s_h2d) cudaStreamDestroy(ctx->s_h2d);
   if (ctx->s_d2h) cudaStreamDestroy(ctx->s_d2h);
   for (double* p : ctx->gm_basis) fr(p);
+  dev::dense_invert_free(ctx->gj);
+  if (ctx->s_coarse) cudaStreamDestroy(ctx->s_coarse);
   for (void* p : {(void*)ctx->coarse_inv, (void*)ctx->coarse_dense, (void*)ctx->gemv_work, (void*)ctx->red.partial, (void*)ctx->red.counter,
                   (void*)ctx->sc, (void*)ctx->rhs, (void*)ctx->g_fac, (void*)ctx->facet_dir, (void*)ctx->kx,
                   (void*)ctx->kb, (void*)ctx->kr, (void*)ctx->kz, (void*)ctx->kp, (void*)ctx->kAp, (void*)ctx->ktmp,

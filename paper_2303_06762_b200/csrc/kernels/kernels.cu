@@ -1934,28 +1934,17 @@ void bsr_to_dense(const Bsr& A, double* D, cudaStream_t s) {
   HPMG_LAUNCH_CHECK();
 }
 
-void dense_invert(int n, const double* A_rowmajor, double* inv_colmajor, cudaStream_t s) {
-  double *aug = nullptr, *rowk = nullptr, *colk = nullptr;
-  int* status = nullptr;
-  unsigned* ctl = nullptr;
-  GjCand* cand = nullptr;
-  int* piv = nullptr;
-  struct Free {  // scratch released on every exit path (launch errors throw)
-    void** p[7];
-    ~Free() {
-      for (void** q : p)
-        if (*q) cudaFree(*q);
-    }
-  } release{{reinterpret_cast<void**>(&aug), reinterpret_cast<void**>(&rowk), reinterpret_cast<void**>(&colk),
-             reinterpret_cast<void**>(&status), reinterpret_cast<void**>(&ctl), reinterpret_cast<void**>(&cand),
-             reinterpret_cast<void**>(&piv)}};
-  if (cudaMalloc(&aug, sizeof(double) * size_t(n) * 2 * n) != cudaSuccess ||
-      cudaMalloc(&rowk, sizeof(double) * 2 * n) != cudaSuccess || cudaMalloc(&colk, sizeof(double) * n) != cudaSuccess ||
-      cudaMalloc(&status, sizeof(int)) != cudaSuccess)
-    throw std::runtime_error("CUDA allocation failed (dense_invert)");
-  cudaMemsetAsync(status, 0, sizeof(int), s);
-  const int64_t tot = int64_t(n) * 2 * n;
-  k_gj_init<<<grid_for(tot, 256), 256, 0, s>>>(n, A_rowmajor, aug);
+void dense_invert_alloc(int n, DenseInvertWork& W) {
+  if (W.n == n) return;
+  dense_invert_free(W);
+  W.n = n;
+  auto need = [](cudaError_t e) {
+    if (e != cudaSuccess) throw std::runtime_error("CUDA allocation failed (dense_invert)");
+  };
+  need(cudaMalloc(&W.aug, sizeof(double) * size_t(n) * 2 * n));
+  need(cudaMalloc(&W.rowk, sizeof(double) * 2 * n));
+  need(cudaMalloc(&W.colk, sizeof(double) * n));
+  need(cudaMalloc(&W.status, sizeof(int)));
   // one cooperative launch for all steps when the grid can be co-resident
   int per_sm = 0, dev = 0, sms = 0;
   cudaFuncSetAttribute(k_gj_implicit, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -1963,14 +1952,30 @@ void dense_invert(int n, const double* A_rowmajor, double* inv_colmajor, cudaStr
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // two CTAs per SM: enough for the row updates, few candidates to reduce per step
-  const int grid = int(std::min<int64_t>(std::min(per_sm, 2) * int64_t(sms), n));
-  bool coop = per_sm > 0 && int64_t(grid) * kGjMaxRows >= n && 2 * size_t(n) * sizeof(double) <= 200 * 1024 && cudaMalloc(&ctl, 2 * sizeof(unsigned)) == cudaSuccess &&
-              cudaMalloc(&cand, sizeof(GjCand) * 2 * size_t(grid)) == cudaSuccess &&
-              cudaMalloc(&piv, sizeof(int) * size_t(n)) == cudaSuccess;
+  W.grid = int(std::min<int64_t>(std::min(per_sm, 2) * int64_t(sms), n));
+  W.coop = per_sm > 0 && int64_t(W.grid) * kGjMaxRows >= n && 2 * size_t(n) * sizeof(double) <= 200 * 1024 &&
+           cudaMalloc(&W.ctl, 2 * sizeof(unsigned)) == cudaSuccess &&
+           cudaMalloc(&W.cand, sizeof(GjCand) * 2 * size_t(W.grid)) == cudaSuccess &&
+           cudaMalloc(&W.piv, sizeof(int) * size_t(n)) == cudaSuccess;
+  cudaGetLastError();
+}
+
+void dense_invert_free(DenseInvertWork& W) {
+  for (void* p : {(void*)W.aug, (void*)W.rowk, (void*)W.colk, (void*)W.status, (void*)W.ctl, W.cand, (void*)W.piv})
+    if (p) cudaFree(p);
+  W = DenseInvertWork{};
+}
+
+void dense_invert_async(int n, const double* A_rowmajor, double* inv_colmajor, DenseInvertWork& W, cudaStream_t s) {
+  if (W.n != n) throw std::runtime_error("dense_invert: workspace not allocated for this size");
+  cudaMemsetAsync(W.status, 0, sizeof(int), s);
+  const int64_t tot = int64_t(n) * 2 * n;
+  k_gj_init<<<grid_for(tot, 256), 256, 0, s>>>(n, A_rowmajor, W.aug);
+  bool coop = W.coop;
   if (coop) {
-    cudaMemsetAsync(ctl, 0, 2 * sizeof(unsigned), s);
+    cudaMemsetAsync(W.ctl, 0, 2 * sizeof(unsigned), s);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned(grid));
+    cfg.gridDim = dim3(unsigned(W.grid));
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = sizeof(double) * 2 * size_t(n);
     cfg.stream = s;
@@ -1979,7 +1984,8 @@ void dense_invert(int n, const double* A_rowmajor, double* inv_colmajor, cudaStr
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    const cudaError_t le = cudaLaunchKernelEx(&cfg, k_gj_implicit, n, aug, cand, piv, status, ctl);
+    const cudaError_t le = cudaLaunchKernelEx(&cfg, k_gj_implicit, n, W.aug, static_cast<GjCand*>(W.cand), W.piv,
+                                             W.status, W.ctl);
     coop = le == cudaSuccess;
     if (!coop) cudaGetLastError();
     if (std::getenv("HPMG_SETUP_TRACE"))
@@ -1987,20 +1993,33 @@ void dense_invert(int n, const double* A_rowmajor, double* inv_colmajor, cudaStr
                    cudaGetErrorString(le), cfg.gridDim.x);
   }
   if (coop) {
-    k_gj_extract_piv<<<grid_for(int64_t(n) * n, 256), 256, 0, s>>>(n, aug, piv, inv_colmajor);
+    k_gj_extract_piv<<<grid_for(int64_t(n) * n, 256), 256, 0, s>>>(n, W.aug, W.piv, inv_colmajor);
   } else {
     for (int k = 0; k < n; ++k) {
-      k_gj_pivot<<<1, 1024, 0, s>>>(n, k, aug, rowk, colk, status);
-      k_gj_eliminate<<<grid_for(tot, 256), 256, 0, s>>>(n, k, aug, rowk, colk);
+      k_gj_pivot<<<1, 1024, 0, s>>>(n, k, W.aug, W.rowk, W.colk, W.status);
+      k_gj_eliminate<<<grid_for(tot, 256), 256, 0, s>>>(n, k, W.aug, W.rowk, W.colk);
     }
-    k_gj_extract<<<grid_for(int64_t(n) * n, 256), 256, 0, s>>>(n, aug, inv_colmajor);
+    k_gj_extract<<<grid_for(int64_t(n) * n, 256), 256, 0, s>>>(n, W.aug, inv_colmajor);
   }
   HPMG_LAUNCH_CHECK();
-  int hs = 0;
-  cudaMemcpyAsync(&hs, status, sizeof(int), cudaMemcpyDeviceToHost, s);
-  cudaStreamSynchronize(s);
+}
 
+void dense_invert_check(const DenseInvertWork& W, cudaStream_t s) {
+  int hs = 0;
+  cudaMemcpyAsync(&hs, W.status, sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
   if (hs) throw std::runtime_error("singular coarse operator");
+}
+
+void dense_invert(int n, const double* A_rowmajor, double* inv_colmajor, cudaStream_t s) {
+  DenseInvertWork W;
+  struct Free {
+    DenseInvertWork& w;
+    ~Free() { dense_invert_free(w); }
+  } release{W};
+  dense_invert_alloc(n, W);
+  dense_invert_async(n, A_rowmajor, inv_colmajor, W, s);
+  dense_invert_check(W, s);
 }
 
 void fill(double* x, double v, int64_t n, cudaStream_t s) {

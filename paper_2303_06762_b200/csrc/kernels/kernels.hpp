@@ -151,6 +151,22 @@ void bsr_to_dense(const Bsr& A, double* D, cudaStream_t s);
 size_t dense_gemv_work(int n);  // doubles of dense_gemv's partial-sum scratch
 /// Gauss-Jordan inverse with partial pivoting of a dense row-major matrix (setup).
 void dense_invert(int n, const double* A_rowmajor, double* inv_colmajor, cudaStream_t s);
+/// Gauss-Jordan scratch kept by the context (allocated outside any stream work), so the
+/// inversion can be queued asynchronously on a side stream and checked later.
+struct DenseInvertWork {
+  double *aug = nullptr, *rowk = nullptr, *colk = nullptr;
+  int* status = nullptr;
+  unsigned* ctl = nullptr;
+  void* cand = nullptr;
+  int* piv = nullptr;
+  int n = 0, grid = 0;
+  bool coop = false;
+};
+void dense_invert_alloc(int n, DenseInvertWork& W);
+void dense_invert_free(DenseInvertWork& W);
+void dense_invert_async(int n, const double* A_rowmajor, double* inv_colmajor, DenseInvertWork& W, cudaStream_t s);
+/// synchronises s and throws on a singular matrix
+void dense_invert_check(const DenseInvertWork& W, cudaStream_t s);
 
 // vector kernels (n doubles)
 void fill(double* x, double v, int64_t n, cudaStream_t s);
