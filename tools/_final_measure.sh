@@ -1,10 +1,8 @@
 set -x
-mkdir -p gpurun_out/final4
-python bench.py > gpurun_out/final4/bench.json 2> gpurun_out/final4/bench.err
-python bench.py --impl reference > gpurun_out/final4/bench_ref.json 2> gpurun_out/final4/bench_ref.err
-python tools/profile_levels.py config2 config1 > gpurun_out/final4/levels.txt 2>&1
-python tools/trace_small.py > gpurun_out/final4/trace_small.txt 2>&1
-python tools/one_vcycle.py config2 > gpurun_out/final4/ov_plain.log 2>&1 && \
-ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/final4/launches.csv python tools/one_vcycle.py config2 > gpurun_out/final4/ncu1.log 2>&1 && \
-ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:k_small -c 2 -o gpurun_out/final4/small python tools/one_vcycle.py config2 > gpurun_out/final4/ncu3.log 2>&1
+mkdir -p gpurun_out/final5
+python -m pytest tests -m gpu -q > gpurun_out/final5/tests.log 2>&1; tail -2 gpurun_out/final5/tests.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final5/smoke.log 2>&1; cat gpurun_out/final5/smoke.log
+python bench.py > gpurun_out/final5/bench.json 2> gpurun_out/final5/bench.err
+python bench.py --impl reference > gpurun_out/final5/bench_ref.json 2> gpurun_out/final5/bench_ref.err
+python tools/run_configs.py > gpurun_out/final5/configs.jsonl 2> gpurun_out/final5/configs.err
 echo exit=$?
