@@ -15,6 +15,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -2068,6 +2069,47 @@ double hpmg_rt_l2_norm(hpmg_ctx* ctx, const double* compound_full, const double*
   return rc == 0 ? out : -1.0;
 }
 
+/// Process-wide pinned staging buffer for the large host <-> device copies of
+/// the host-pointer API (grow-only, kept across contexts like the device
+/// pool): a pageable copy runs through the driver's small staging buffers at
+/// a fraction of the link rate; here the DMA runs at full rate and host
+/// threads move the data between the staging buffer and the caller's arrays.
+struct PinnedStage {
+  std::mutex m;
+  char* p = nullptr;
+  size_t cap = 0;
+  char* get(size_t bytes) {
+    if (bytes > cap) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      cap = 0;
+      CK(cudaHostAlloc(reinterpret_cast<void**>(&p), bytes, cudaHostAllocDefault));
+      cap = bytes;
+    }
+    return p;
+  }
+};
+PinnedStage& pinned_stage() {
+  static PinnedStage st;
+  return st;
+}
+/// memcpy on up to 8 host threads (large copies are limited per thread by
+/// page faults on the destination and by a single core's bandwidth)
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+  const int nt = int(std::min<size_t>(8, bytes >> 22) + 1);
+  if (nt == 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back([=] {
+      const size_t a = bytes * t / nt, b = bytes * (t + 1) / nt;
+      std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
+    });
+  for (auto& x : th) x.join();
+}
+
 int hpmg_recover(hpmg_ctx* ctx, const double* velocity_full, double* interior, double* p_ortho, double* grad) {
   return guarded(ctx, [&] {
     hpmg_ctx& C = *ctx;
@@ -2080,13 +2122,24 @@ int hpmg_recover(hpmg_ctx* ctx, const double* velocity_full, double* interior, d
     double* di = tmp.add(dalloc<double>(size_t(ne) * std::max(no, 1)));
     double* dp = tmp.add(dalloc<double>(size_t(ne) * std::max(np, 1)));
     double* dg = tmp.add(dalloc<double>(size_t(ne) * ng));
-    CK(cudaMemcpyAsync(comp, velocity_full, sizeof(double) * nfull, cudaMemcpyHostToDevice, C.s));
+    const size_t bi = sizeof(double) * size_t(ne) * no, bp = sizeof(double) * size_t(ne) * np,
+                 bg = sizeof(double) * size_t(ne) * ng, bv = sizeof(double) * nfull;
+    PinnedStage& st = pinned_stage();
+    std::lock_guard<std::mutex> lock(st.m);
+    char* h = st.get(std::max(bv, bi + bp + bg));
+    par_memcpy(h, velocity_full, bv);
+    CK(cudaMemcpyAsync(comp, h, bv, cudaMemcpyHostToDevice, C.s));
     dev::recover(R.T, T.geo, ne, C.fine_prm, C.fine_load, C.fine_lstride, T.elem_facets, (long long)(nfull / 2), comp,
                  di, dp, dg, C.s, C.fine_wind, C.fine_mass);
-    if (no) CK(cudaMemcpyAsync(interior, di, sizeof(double) * ne * no, cudaMemcpyDeviceToHost, C.s));
-    if (np) CK(cudaMemcpyAsync(p_ortho, dp, sizeof(double) * ne * np, cudaMemcpyDeviceToHost, C.s));
-    CK(cudaMemcpyAsync(grad, dg, sizeof(double) * ne * ng, cudaMemcpyDeviceToHost, C.s));
+    // the staging buffer is reused for the results only after the upload has
+    // been consumed: the copies below queue behind the recovery kernel
+    if (no) CK(cudaMemcpyAsync(h, di, bi, cudaMemcpyDeviceToHost, C.s));
+    if (np) CK(cudaMemcpyAsync(h + bi, dp, bp, cudaMemcpyDeviceToHost, C.s));
+    CK(cudaMemcpyAsync(h + bi + bp, dg, bg, cudaMemcpyDeviceToHost, C.s));
     CK(cudaStreamSynchronize(C.s));
+    if (no) par_memcpy(interior, h, bi);
+    if (np) par_memcpy(p_ortho, h + bi, bp);
+    par_memcpy(grad, h + bi + bp, bg);
   });
 }
 
