@@ -193,7 +193,8 @@ def run_hpmg(args, rank, world, local, dist):
         krylov["note"] = ("whole solve = one CUDA-graph launch (device conditional nodes); overhead = per-iteration "
                           "cost minus the V-cycle and the operator apply it contains (vector updates, reductions, "
                           "for GMRES the fused MGS step kernels, at j from 5 to 25); slope of capped solves, "
-                          "PCG 5..45 and GMRES 5..25 iterations, best of 5 wall-clock runs each")
+                          "PCG 5..45 and GMRES 5..25 iterations, best of 5 runs each, CUDA events on the "
+                          "library stream")
         B5.close()
     tts_proc = start_cpu_tts(args) if (args.cpu_tts and rank == 0 and world == 1) else None
 
@@ -499,12 +500,21 @@ def krylov_overhead(H, B, restart=0):
     solver = H.pcg if B.symmetric() else H.gmres
     hi = 45 if B.symmetric() else 25
 
+    # device time on the library's stream: CUDA events around the solve (it
+    # returns after its own synchronisation), so host jitter stays out
+    import torch
+
+    ext = torch.cuda.ExternalStream(B.stream())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
     def t(k):
         best = 1e9
         for _ in range(5):
-            t0 = time.perf_counter()
+            e0.record(ext)
             solver(B, rhs, opt=H.KrylovOptions(max_iterations=k, rel_tol=1e-30, abs_tol=0.0, restart=restart))
-            best = min(best, time.perf_counter() - t0)
+            e1.record(ext)
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1) * 1e-3)
         return best
 
     _, st = solver(B, rhs, opt=H.KrylovOptions(max_iterations=hi, rel_tol=1e-30, abs_tol=0.0, restart=restart))
