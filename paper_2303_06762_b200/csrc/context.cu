@@ -2441,7 +2441,13 @@ double hpmg_debug_loop_probe(hpmg_ctx* ctx, int mode, int iters) {
           GK(cudaStreamUpdateCaptureDependencies(C.s, &cn, 1, cudaStreamSetCaptureDependencies));
           cudaGraphDestroy(child);
         }
-        if (pm >= 0) {
+        if (pm >= 0 && (pm & 64)) {  // the round-2 PCG body: V-cycle | r.z | A p' | update
+          const int64_t n = C.top().n;
+          apply_blocks(C, C.kr, C.kz);
+          if (pm & 8) dev::pcg_loop_rz(C.kr, C.kz, n, C.sc, C.red, h, C.s);
+          if (pm & 1) dev::pcg_spmv_dir(C.top().A, C.kp, C.kz, C.kAp, 1, C.sc, C.red, C.s);
+          if (pm & 2) dev::pcg_loop_update(C.kx, C.kr, C.kp, C.kz, C.kAp, n, 1, C.sc, C.red, h, C.s);
+        } else if (pm >= 0) {
           const int64_t n = C.top().n;
           if (pm & 1) dev::pcg_spmv_dir(C.top().A, C.kp, C.kz, C.kAp, 1, C.sc, C.red, C.s);
           if (pm & 2) dev::pcg_loop_update(C.kx, C.kr, C.kp, C.kz, C.kAp, n, 1, C.sc, C.red, h, C.s);

@@ -27,6 +27,11 @@ if B.symmetric():
     for mode, label in [(63, "pcg_full"), (62, "pcg_no_spmv"), (61, "pcg_no_update"), (59, "pcg_no_vcycle_if"),
                         (55, "pcg_no_rz"), (47, "pcg_no_direction"), (36, "pcg_if_vcycle_only")]:
         out[label] = L.hpmg_debug_loop_probe(B.h, mode, 25)
+    # round-2 loop body (64: V-cycle directly in the body, then 8 r.z, 1 A p', 2 update)
+    for mode, label in [(96 + 11, "pcg2_full"), (96, "pcg2_vcycle_only"), (96 + 8, "pcg2_v_rz"),
+                        (96 + 9, "pcg2_v_rz_spmv"), (32 + 1, "spmv_dir_only"), (32 + 2, "update_only"),
+                        (32 + 8, "rz_only")]:
+        out[label] = L.hpmg_debug_loop_probe(B.h, mode, 25)
 out["graph_vcycle_ms_2"] = B.time_apply(30)[0]
 print(json.dumps({k: (round(v, 5) if isinstance(v, float) else v) for k, v in out.items()}))
 if out["empty_while_ms"] < 0:
