@@ -359,8 +359,8 @@ void plan_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, bool fines
   V.nb = V.plan.nb;
   V.n = V.plan.n();
   V.ne = m.ne();
-  std::vector<ElemGeo> geo(m.ne());
-  for (int e = 0; e < m.ne(); ++e) geo[e] = host::element_geometry(m, e);
+  host::BigVec<ElemGeo> geo(m.ne());  // 240 B per element: filled (and first touched) by the plan threads
+  host::parallel_for(m.ne(), [&](int e) { geo[e] = host::element_geometry(m, e); });
   V.geo = dupload(geo, s);
   V.A.nb = V.nb;
   V.A.bs = V.bs;
