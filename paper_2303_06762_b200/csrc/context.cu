@@ -163,6 +163,7 @@ struct Level {
   double *x = nullptr, *b = nullptr, *r = nullptr, *y = nullptr, *bw = nullptr, *xw = nullptr, *dbuf = nullptr;
   int steps = 1;
   ElemGeo* geo = nullptr;
+  bool geo_shared = false;  // the head's geometry is its mesh level's (same mesh): not freed twice
   int ne = 0;
   std::vector<double> Ahost;  // BSR values mirror (filled on demand)
   // finest-system extras
@@ -349,7 +350,8 @@ struct SetupTrace {
   }
 };
 
-void plan_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, bool finest, host::LevelPlan&& plan) {
+void plan_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, bool finest, host::LevelPlan&& plan,
+                ElemGeo* shared_geo = nullptr) {
   cudaStream_t s = C.s;
   V.k = k;
   V.bs = 2 * (k + 1);
@@ -359,9 +361,14 @@ void plan_level(hpmg_ctx& C, Level& V, const host::TriMesh& m, int k, bool fines
   V.nb = V.plan.nb;
   V.n = V.plan.n();
   V.ne = m.ne();
-  host::BigVec<ElemGeo> geo(m.ne());  // 240 B per element: filled (and first touched) by the plan threads
-  host::parallel_for(m.ne(), [&](int e) { geo[e] = host::element_geometry(m, e); });
-  V.geo = dupload(geo, s);
+  if (shared_geo) {  // the order-k head on the finest mesh: the lowest-order level's geometry
+    V.geo = shared_geo;
+    V.geo_shared = true;
+  } else {
+    host::BigVec<ElemGeo> geo(m.ne());  // 240 B per element: filled (and first touched) by the plan threads
+    host::parallel_for(m.ne(), [&](int e) { geo[e] = host::element_geometry(m, e); });
+    V.geo = dupload(geo, s);
+  }
   V.A.nb = V.nb;
   V.A.bs = V.bs;
   V.A.val = dalloc<double>(size_t(V.nb) * host::kSlots * V.bs * V.bs);
@@ -1371,7 +1378,7 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
     }
     if (k > 0) {
       C.head = std::make_unique<Level>();
-      plan_level(C, *C.head, fine, k, true, std::move(plans[C.L + 1]));
+      plan_level(C, *C.head, fine, k, true, std::move(plans[C.L + 1]), C.lv[C.L]->geo);
       C.head->steps = opt->smooth_steps;
     }
   }
@@ -1685,7 +1692,7 @@ void hpmg_destroy(hpmg_ctx* ctx) {
                     (void*)V->P.fac, (void*)V->P.off, (void*)V->P.inv, (void*)V->P.wave, (void*)V->P.fpatch,
                     (void*)V->Pm.ptr, (void*)V->Pm.col, (void*)V->Pm.val, (void*)V->PT.ptr, (void*)V->PT.col,
                     (void*)V->PT.val, (void*)V->x, (void*)V->b, (void*)V->r, (void*)V->y, (void*)V->bw, (void*)V->xw,
-                    (void*)V->dbuf, (void*)V->geo, (void*)V->row_elems, (void*)V->elem_facets, (void*)V->facet_block,
+                    (void*)V->dbuf, (void*)(V->geo_shared ? nullptr : V->geo), (void*)V->row_elems, (void*)V->elem_facets, (void*)V->facet_block,
                     (void*)V->d_wave_ptr, (void*)V->rec.rec, (void*)V->srec.rec, (void*)V->rect.rec,
                     (void*)V->d_passes, (void*)V->gath,
                     (void*)V->block_facet, (void*)V->tdev.nmed, (void*)V->tdev.med, (void*)V->tdev.ncol,
