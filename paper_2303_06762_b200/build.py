@@ -16,7 +16,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libhpmg.so")
 
-SOURCES = [os.path.join(CSRC, "kernels", "kernels.cu"), os.path.join(CSRC, "kernels", "small_levels.cu"),
+SOURCES = [os.path.join(CSRC, "kernels", "kernels.cu"), os.path.join(CSRC, "kernels", "small_levels.cu"), os.path.join(CSRC, "kernels", "dense_level.cu"),
            os.path.join(CSRC, "kernels", "sweep_rec.cu"), os.path.join(CSRC, "kernels", "post.cu"),
            os.path.join(CSRC, "context.cu"), os.path.join(CSRC, "ns.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, d, f) for d in ("kernels", "host") for f in os.listdir(os.path.join(CSRC, d))] + [

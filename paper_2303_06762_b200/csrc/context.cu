@@ -195,6 +195,8 @@ struct hpmg_ctx {
   const double* post_x0 = nullptr;  // finest element origins [ne][2]
   double* post_red = nullptr;       // error partials [4][kRedBlocks] + result [4]
   double* coarse_inv = nullptr;
+  double* m1 = nullptr;  // level-1 V(1,1) sub-cycle as one dense map (dense_level.cu), or null
+  int m1_n = 0;
   double* coarse_dense = nullptr;  // level-0 operator, dense row-major (setup scratch of the inverse)
   dev::DenseInvertWork gj;         // Gauss-Jordan scratch of the coarse inverse
   cudaStream_t s_coarse = nullptr; // setup: the coarse inverse runs beside the finer levels' work
@@ -725,6 +727,13 @@ void h_cycle(hpmg_ctx& C, int l, const double* b, double* x) {
   Level& V = *C.lv[l];
   Level& W = *C.lv[l - 1];
   const int q = C.opt.cycle == HPMG_CYCLE_W ? 2 : 1;
+  if (l == 1 && C.m1 && !C.trace && V.small && C.opt.smoother == HPMG_SMOOTH_MULTIPLICATIVE && q == 1) {
+    // the whole level-1 sub-cycle (sweeps, transfers, coarse solve) as one
+    // dense map formed at setup (dense_level.cu): one HBM-bound GEMV
+    dev::dense_rowgemv(int(V.n), C.m1, b, x, C.s);
+    count(C);
+    return;
+  }
   if (V.small && C.opt.smoother == HPMG_SMOOTH_MULTIPLICATIVE && q == 1) {
     // whole-level sweeps in one persistent CTA (small_levels.cu)
     dev::small_pre(V.A, V.srec, V.d_passes, V.npass, V.steps, V.PT, b, x, V.r, W.b, C.s);
@@ -1416,6 +1425,34 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
 /// Everything that depends on the linearisation state (the reference rebuilds
 /// the whole MGPreconditioner per Picard / Newton step, ns.hpp:84): the wind
 /// chain (multigrid.hpp:58-66), condensation and assembly of every level, the
+/// The level-1 V(1,1) sub-cycle as one dense map (dense_level.cu) where the
+/// one-CTA level path would run it: V-cycle (or variable V), multiplicative
+/// smoother, level 1 small, n1 <= 8192 (M1 <= 512 MB; past that the GEMV
+/// costs more than the sweeps). HPMG_DENSE_L1=0 keeps the sweeps.
+void build_dense_level1(hpmg_ctx& C) {
+  const char* env = std::getenv("HPMG_DENSE_L1");
+  const bool want = !(env && env[0] == '0') && C.L >= 1 && C.lv[1]->small &&
+                    C.opt.smoother == HPMG_SMOOTH_MULTIPLICATIVE && C.opt.cycle != HPMG_CYCLE_W && C.lv[1]->n <= 8192;
+  if (!want) {
+    if (C.m1) dfree(C.m1);
+    C.m1 = nullptr;
+    C.m1_n = 0;
+    return;
+  }
+  Level& V = *C.lv[1];
+  if (!C.m1 || C.m1_n != int(V.n)) {
+    if (C.m1) dfree(C.m1);
+    C.m1 = dalloc<double>(size_t(V.n) * V.n);
+    C.m1_n = int(V.n);
+  }
+  // scratch from the context pool: stream-ordered, reused by the next context
+  void* w = nullptr;
+  CK(cudaMallocFromPoolAsync(&w, sizeof(double) * dev::dense_level1_work(int(V.n), C.n0), alloc_pool(), C.s));
+  dev::dense_level1(V.A, V.srec, V.d_passes, V.npass, V.steps, V.PT, V.Pm, C.n0, C.coarse_inv, C.m1,
+                    static_cast<double*>(w), C.s);
+  CK(cudaFreeAsync(w, C.s));
+}
+
 /// patch inverses, the corrected prolongations and the coarse inverse.
 void linearise(hpmg_ctx& C, const hpmg_problem* prob, const host::RefTensors* Tk) {
   using clk = std::chrono::steady_clock;
@@ -1574,6 +1611,8 @@ void linearise(hpmg_ctx& C, const hpmg_problem* prob, const host::RefTensors* Tk
   C.lin_parts[1] = t_upload + el(2, 3);  // transfer join + uploads (host) + correction (device)
   C.lin_parts[2] = el(6, 7);             // coarse densify + inverse (device, side stream, overlapped)
   C.lin_parts[3] = el(0, 1);             // condensation + assembly (device)
+  build_dense_level1(C);
+  tr.mark("dense level-1 cycle");
 
 }
 
@@ -1717,7 +1756,7 @@ void hpmg_destroy(hpmg_ctx* ctx) {
   for (double* p : ctx->gm_basis) fr(p);
   dev::dense_invert_free(ctx->gj);
   if (ctx->s_coarse) cudaStreamDestroy(ctx->s_coarse);
-  for (void* p : {(void*)ctx->coarse_inv, (void*)ctx->coarse_dense, (void*)ctx->gemv_work, (void*)ctx->red.partial, (void*)ctx->red.counter,
+  for (void* p : {(void*)ctx->m1, (void*)ctx->coarse_inv, (void*)ctx->coarse_dense, (void*)ctx->gemv_work, (void*)ctx->red.partial, (void*)ctx->red.counter,
                   (void*)ctx->sc, (void*)ctx->rhs, (void*)ctx->g_fac, (void*)ctx->facet_dir, (void*)ctx->kx,
                   (void*)ctx->kb, (void*)ctx->kr, (void*)ctx->kz, (void*)ctx->kp, (void*)ctx->kAp, (void*)ctx->ktmp,
                   (void*)ctx->io_a, (void*)ctx->io_b, (void*)ctx->pres, (void*)ctx->div, (void*)ctx->urhs,

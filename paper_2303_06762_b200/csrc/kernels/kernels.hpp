@@ -125,6 +125,18 @@ void small_pre(const Bsr& A, const PatchRecords& R, const int2* passes, int npas
                const double* b, double* x, double* r, double* rc, cudaStream_t s);
 void small_post(const Bsr& A, const PatchRecords& R, const int2* passes, int npass, int sweeps, const BlockCsr& Pm,
                 const double* e, const double* b, double* x, cudaStream_t s);
+/// batched one-CTA sweeps (setup): CTA j runs the pre (post) phase on column j
+/// of X (leading dimension ld) with b = e_{unit0 + j}
+void small_pre_batch(const PatchRecords& R, int nb, const int2* passes, int npass, int sweeps, int ncols, int unit0,
+                     double* X, int64_t ld, cudaStream_t s);
+void small_post_batch(const PatchRecords& R, int nb, const int2* passes, int npass, int sweeps, int ncols, int unit0,
+                      double* X, int64_t ld, cudaStream_t s);
+/// dense_level.cu: M1 (row-major n x n) = the level-1 V(1,1) sub-cycle
+/// (pre-sweep, residual, P C^-1 P^T, post-sweep) as one linear map; y = M b
+void dense_level1(const Bsr& A, const PatchRecords& R, const int2* passes, int npass, int sweeps, const BlockCsr& PT,
+                  const BlockCsr& Pm, int n0, const double* coarse_inv, double* M1, double* work, cudaStream_t s);
+size_t dense_level1_work(int n, int n0);  // doubles of dense_level1's scratch
+void dense_rowgemv(int n, const double* M, const double* b, double* y, cudaStream_t s);
 
 /// Device arrays of host::TransferPlan (corrected prolongation structure).
 struct TransferDev {

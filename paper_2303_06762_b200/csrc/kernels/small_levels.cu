@@ -202,13 +202,17 @@ __device__ void sweeps(const PatchRecords& R, const int2* __restrict__ passes, i
 template <int NPM>
 __global__ void __launch_bounds__(kThreads) k_small_pre(int n, PatchRecords R, const int2* __restrict__ passes,
                                                         int npass, int nsweeps, const double* __restrict__ b,
-                                                        double* __restrict__ x) {
+                                                        double* __restrict__ x, int64_t ld, int unit0) {
   extern __shared__ __align__(128) double sm[];
   Smem v = carve(n, R.stride, sm);
   stamp(4088);
+  // batched (setup of the dense level-1 cycle, dense_level.cu): CTA j sweeps
+  // column j of x (leading dimension ld) with b = e_{unit0 + j}
+  x += blockIdx.x * ld;
+  const int unit = unit0 >= 0 ? unit0 + int(blockIdx.x) : -1;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     v.sx[i] = 0.0;
-    v.sb[i] = b[i];
+    v.sb[i] = unit >= 0 ? (i == unit ? 1.0 : 0.0) : b[i];
   }
   __syncthreads();
   stamp(4089);
@@ -222,13 +226,15 @@ __global__ void __launch_bounds__(kThreads) k_small_pre(int n, PatchRecords R, c
 template <int NPM>
 __global__ void __launch_bounds__(kThreads) k_small_post(int n, PatchRecords R, const int2* __restrict__ passes,
                                                          int npass, int nsweeps, const double* __restrict__ b,
-                                                         double* __restrict__ x) {
+                                                         double* __restrict__ x, int64_t ld, int unit0) {
   extern __shared__ __align__(128) double sm[];
   Smem v = carve(n, R.stride, sm);
   stamp(4092);
+  x += blockIdx.x * ld;
+  const int unit = unit0 >= 0 ? unit0 + int(blockIdx.x) : -1;
   for (int t = threadIdx.x; t < n; t += blockDim.x) {
     v.sx[t] = x[t];
-    v.sb[t] = b[t];
+    v.sb[t] = unit >= 0 ? (t == unit ? 1.0 : 0.0) : b[t];
   }
   __syncthreads();
   stamp(4093);
@@ -241,14 +247,21 @@ __global__ void __launch_bounds__(kThreads) k_small_post(int n, PatchRecords R, 
 /// launches k_small_pre / k_small_post for the level's patch row count
 template <bool kPost>
 void launch_small(const PatchRecords& R, int n, const int2* passes, int npass, int nsweeps, const double* b,
-                  double* x, size_t smem, cudaStream_t s) {
+                  double* x, size_t smem, cudaStream_t s, int ncols = 1, int64_t ld = 0, int unit0 = -1) {
   auto go = [&](auto kernel) {
-    static bool attr = false;
-    if (!attr) {
+    // once per kernel instantiation (all of them share this lambda's type)
+    static const void* done[16] = {};
+    bool set = false;
+    for (const void* d : done) set = set || d == reinterpret_cast<const void*>(kernel);
+    if (!set) {
       cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      attr = true;
+      for (auto& d : done)
+        if (!d) {
+          d = reinterpret_cast<const void*>(kernel);
+          break;
+        }
     }
-    kernel<<<1, kThreads, smem, s>>>(n, R, passes, npass, nsweeps, b, x);
+    kernel<<<ncols, kThreads, smem, s>>>(n, R, passes, npass, nsweeps, b, x, ld, unit0);
   };
   switch (R.max_nf) {
     case 4: go(kPost ? k_small_post<8> : k_small_pre<8>); break;
@@ -292,6 +305,16 @@ void small_post(const Bsr& A, const PatchRecords& R, const int2* passes, int npa
                 const double* e, const double* b, double* x, cudaStream_t s) {
   prolong_add(Pm, e, x, s);
   launch_small<true>(R, A.nb * 2, passes, npass, sweeps, b, x, smem_bytes(A.nb, R.stride, npass), s);
+}
+
+void small_pre_batch(const PatchRecords& R, int nb, const int2* passes, int npass, int sweeps, int ncols, int unit0,
+                     double* X, int64_t ld, cudaStream_t s) {
+  launch_small<false>(R, nb * 2, passes, npass, sweeps, nullptr, X, smem_bytes(nb, R.stride, npass), s, ncols, ld, unit0);
+}
+
+void small_post_batch(const PatchRecords& R, int nb, const int2* passes, int npass, int sweeps, int ncols, int unit0,
+                      double* X, int64_t ld, cudaStream_t s) {
+  launch_small<true>(R, nb * 2, passes, npass, sweeps, nullptr, X, smem_bytes(nb, R.stride, npass), s, ncols, ld, unit0);
 }
 
 }  // namespace dev
