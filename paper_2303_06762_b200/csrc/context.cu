@@ -328,7 +328,10 @@ std::vector<double> dirichlet_data(const host::TriMesh& m, int k, hpmg_field_fn 
 
 void alloc_level_vectors(Level& V) {
   V.x = dalloc<double>(V.n);
-  V.b = dalloc<double>(V.n);
+  // zero padding past n: the dense level-1 GEMV reads b up to its row stride
+  V.b = dalloc<double>(V.n + dev::kVecPad);
+  CK(cudaMemsetAsync(V.b + V.n, 0, sizeof(double) * dev::kVecPad, alloc_stream()));
+  CK(cudaStreamSynchronize(alloc_stream()));
   V.r = dalloc<double>(V.n);
   V.y = dalloc<double>(V.n);
   V.bw = dalloc<double>(V.n);
@@ -727,7 +730,7 @@ void h_cycle(hpmg_ctx& C, int l, const double* b, double* x) {
   Level& V = *C.lv[l];
   Level& W = *C.lv[l - 1];
   const int q = C.opt.cycle == HPMG_CYCLE_W ? 2 : 1;
-  if (l == 1 && C.m1 && !C.trace && V.small && C.opt.smoother == HPMG_SMOOTH_MULTIPLICATIVE && q == 1) {
+  if (l == 1 && C.m1 && b == V.b && !C.trace && V.small && C.opt.smoother == HPMG_SMOOTH_MULTIPLICATIVE && q == 1) {
     // the whole level-1 sub-cycle (sweeps, transfers, coarse solve) as one
     // dense map formed at setup (dense_level.cu): one HBM-bound GEMV
     dev::dense_rowgemv(int(V.n), C.m1, b, x, C.s);
@@ -1432,7 +1435,8 @@ void setup(hpmg_ctx& C, const hpmg_mesh_desc* md, const hpmg_options* opt, const
 void build_dense_level1(hpmg_ctx& C) {
   const char* env = std::getenv("HPMG_DENSE_L1");
   const bool want = !(env && env[0] == '0') && C.L >= 1 && C.lv[1]->small &&
-                    C.opt.smoother == HPMG_SMOOTH_MULTIPLICATIVE && C.opt.cycle != HPMG_CYCLE_W && C.lv[1]->n <= 8192;
+                    C.opt.smoother == HPMG_SMOOTH_MULTIPLICATIVE && C.opt.cycle != HPMG_CYCLE_W && C.lv[1]->n <= 8192 &&
+                    C.L >= 2;  // level 1's input is then always its own (padded) b
   if (!want) {
     if (C.m1) dfree(C.m1);
     C.m1 = nullptr;
@@ -1442,7 +1446,7 @@ void build_dense_level1(hpmg_ctx& C) {
   Level& V = *C.lv[1];
   if (!C.m1 || C.m1_n != int(V.n)) {
     if (C.m1) dfree(C.m1);
-    C.m1 = dalloc<double>(size_t(V.n) * V.n);
+    C.m1 = dalloc<double>(size_t(V.n) * dev::dense_level1_ld(int(V.n)));
     C.m1_n = int(V.n);
   }
   // scratch from the context pool: stream-ordered, reused by the next context

@@ -115,8 +115,8 @@ __global__ void __launch_bounds__(256) k_dgemm_nn(int n, int m, const double* __
     }
 }
 
-/// M[i][j] = X[j][i] (n x n), 32 x 32 tiles through shared memory
-__global__ void k_transpose_sq(int n, const double* __restrict__ X, double* __restrict__ M) {
+/// M[i][j] = X[j][i] (n x n, M with row stride ld), 32 x 32 tiles through shared memory
+__global__ void k_transpose_sq(int n, int ld, const double* __restrict__ X, double* __restrict__ M) {
   __shared__ double t[32][33];
   const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
@@ -126,47 +126,53 @@ __global__ void k_transpose_sq(int n, const double* __restrict__ X, double* __re
   __syncthreads();
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
     const int i = bx + r, j = by + threadIdx.x;
-    if (i < n && j < n) M[size_t(i) * n + j] = t[threadIdx.x][r];
+    if (i < n && j < n) M[size_t(i) * ld + j] = t[threadIdx.x][r];
   }
 }
 
-/// y = M b, M row-major n x n (n even, rows 16-byte aligned): one warp per
-/// row, double2 loads strided by the warp, eight in flight per lane, M
-/// streamed past L1 (b stays L1-resident), fixed-order shuffle reduction.
-__global__ void __launch_bounds__(256) k_dense_rowgemv(int n, const double* __restrict__ M, const double* __restrict__ b,
-                                                      double* __restrict__ y) {
-  const int row = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (row >= n) return;
-  const double2* m = reinterpret_cast<const double2*>(M + size_t(row) * n);
-  const double2* bb = reinterpret_cast<const double2*>(b);
-  const int n2 = n / 2;
-  double s[4] = {0.0, 0.0, 0.0, 0.0};
-  int q = lane;
-  for (; q + 7 * 32 < n2; q += 8 * 32) {
-    double2 a[8];
+/// y = M b, M row-major n x ld with ld a multiple of 2,048 (zero columns
+/// past n; b readable and zero up to ld). Two rows per 256-thread CTA, four
+/// warps per row; warp w takes the row's 256-double2 batches w, w + 4, ...,
+/// eight loads per lane in flight at constant offsets (no tail: a clamped or
+/// predicated remainder made ptxas serialise each load with its FMAs). M
+/// streams evict-first, b stays cache-resident; the partial sums are combined
+/// in a fixed order (shuffle tree, then the four warps in order). 3,008 CTAs
+/// at n = 6,016 spread evenly over the SMs (one warp per row left a 1.27-wave
+/// tail).
+constexpr int kRowPad = 2048;
+__global__ void __launch_bounds__(256) k_dense_rowgemv(int n, int ld, const double* __restrict__ M,
+                                                      const double* __restrict__ b, double* __restrict__ y) {
+  __shared__ double part[8];
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int row = blockIdx.x * 2 + w / 4, wq = w % 4;
+  double v = 0.0;
+  if (row < n) {
+    const double2* m = reinterpret_cast<const double2*>(M + size_t(row) * ld) + lane;
+    const double2* bb = reinterpret_cast<const double2*>(b) + lane;
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int q = wq * 256; q < ld / 2; q += 4 * 256) {
+      double2 a[8], x[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
-                   : "=d"(a[u].x), "=d"(a[u].y)
-                   : "l"(m + q + 32 * u));
+      for (int u = 0; u < 8; ++u) a[u] = __ldcs(m + q + 32 * u);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const double2 x = __ldg(bb + q + 32 * u);
-      s[u & 3] = fma(a[u].x, x.x, s[u & 3]);
-      s[u & 3] = fma(a[u].y, x.y, s[u & 3]);
+      for (int u = 0; u < 8; ++u) x[u] = __ldg(bb + q + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        s[u & 3] = fma(a[u].x, x[u].x, s[u & 3]);
+        s[u & 3] = fma(a[u].y, x[u].y, s[u & 3]);
+      }
     }
+    v = (s[0] + s[1]) + (s[2] + s[3]);
   }
-  for (; q < n2; q += 32) {
-    double2 a;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(a.x), "=d"(a.y) : "l"(m + q));
-    const double2 x = __ldg(bb + q);
-    s[0] = fma(a.x, x.x, s[0]);
-    s[0] = fma(a.y, x.y, s[0]);
-  }
-  double v = (s[0] + s[1]) + (s[2] + s[3]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if (lane == 0) y[row] = v;
+  if (lane == 0) part[w] = v;
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    const int r = blockIdx.x * 2 + threadIdx.x;
+    const double* p = part + 4 * threadIdx.x;
+    if (r < n) y[r] = (p[0] + p[1]) + (p[2] + p[3]);
+  }
 }
 
 }  // namespace
@@ -175,6 +181,9 @@ void dense_level1(const Bsr& A, const PatchRecords& R, const int2* passes, int n
                   const BlockCsr& Pm, int n0, const double* coarse_inv, double* M1, double* work, cudaStream_t s) {
   const int n = A.nb * 2;
   if (n % 2 || n0 % 2) throw std::runtime_error("dense level 1: odd size");
+  auto chk = [](cudaError_t e) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA dense level 1: ") + cudaGetErrorString(e));
+  };
   const size_t nn = size_t(n) * n, nc = size_t(n0) * n;
   double *X = work, *Rr = X + nn, *Rc = Rr + nn, *E = Rc + nc;
   // X[:, j] = forward sweep(s) of e_j from x = 0
@@ -190,14 +199,18 @@ void dense_level1(const Bsr& A, const PatchRecords& R, const int2* passes, int n
   DL_CHECK();
   // X[:, j] = backward sweep(s) of X[:, j] with b = e_j: column j of M1
   small_post_batch(R, A.nb, passes, npass, sweeps, n, 0, X, n, s);
-  k_transpose_sq<<<dim3((n + 31) / 32, (n + 31) / 32), dim3(32, 8), 0, s>>>(n, X, M1);
+  const int ld = dense_level1_ld(n);
+  chk(cudaMemsetAsync(M1, 0, sizeof(double) * size_t(n) * ld, s));  // zero columns past n
+  k_transpose_sq<<<dim3((n + 31) / 32, (n + 31) / 32), dim3(32, 8), 0, s>>>(n, ld, X, M1);
   DL_CHECK();
 }
 
 size_t dense_level1_work(int n, int n0) { return 2 * (size_t(n) * n + size_t(n0) * n); }
 
+int dense_level1_ld(int n) { return (n + kRowPad - 1) / kRowPad * kRowPad; }
+
 void dense_rowgemv(int n, const double* M, const double* b, double* y, cudaStream_t s) {
-  k_dense_rowgemv<<<(n + 7) / 8, 256, 0, s>>>(n, M, b, y);
+  k_dense_rowgemv<<<(n + 1) / 2, 256, 0, s>>>(n, dense_level1_ld(n), M, b, y);
   DL_CHECK();
 }
 

@@ -136,7 +136,11 @@ void small_post_batch(const PatchRecords& R, int nb, const int2* passes, int npa
 void dense_level1(const Bsr& A, const PatchRecords& R, const int2* passes, int npass, int sweeps, const BlockCsr& PT,
                   const BlockCsr& Pm, int n0, const double* coarse_inv, double* M1, double* work, cudaStream_t s);
 size_t dense_level1_work(int n, int n0);  // doubles of dense_level1's scratch
+/// M row-major with row stride dense_level1_ld(n) (zero columns past n); b
+/// must be readable, and zero, up to that stride (level b buffers are padded)
 void dense_rowgemv(int n, const double* M, const double* b, double* y, cudaStream_t s);
+int dense_level1_ld(int n);
+constexpr int kVecPad = 2048;  // doubles of zero padding after every level's b
 
 /// Device arrays of host::TransferPlan (corrected prolongation structure).
 struct TransferDev {
