@@ -1,0 +1,91 @@
+"""The dense level-1 sub-cycle (csrc/kernels/dense_level.cu).
+
+On V / variable-V cycles with the multiplicative smoother, level 1 of a base
+mesh with many waves (the one-CTA level) and the coarse solve run as one dense
+map M1 formed at setup from the reference steps applied to unit vectors
+(multigrid.hpp:166-185 at l = 1). Checked here: the preconditioner with M1
+against the oracle (same APPLY_TOL as every sweep variant) and against the
+same context type with the map switched off (HPMG_DENSE_L1=0: the one-CTA
+sweeps), PCG counts equal, and the map rebuilt when a context is re-used
+with a W-cycle-free option set.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+
+pytestmark = pytest.mark.gpu
+
+H = pytest.importorskip("paper_2303_06762_b200")
+
+APPLY_TOL = 2e-12  # test_gpu_parity.py, at inv_eps = 1e3
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def build(k, dense, cycle=H.CYCLE_V, m=1, base_n=8, levels=3, beta=1.0):
+    old = os.environ.get("HPMG_DENSE_L1")
+    os.environ["HPMG_DENSE_L1"] = "1" if dense else "0"
+    try:
+        n_f = base_n << (levels - 1)
+        F = O.seeded_load(n_f, 1)
+        return H.MGPreconditioner(base_n=base_n, levels=levels, k=k, beta=beta, inv_eps=1e3,
+                                  structured_load=(n_f, F), cycle=cycle, smooth_steps=m)
+    finally:
+        if old is None:
+            os.environ.pop("HPMG_DENSE_L1")
+        else:
+            os.environ["HPMG_DENSE_L1"] = old
+
+
+@pytest.mark.parametrize("k", [0, 1, 3])
+def test_dense_level1_matches_oracle_and_sweeps(k):
+    base_n, levels = 8, 3
+    n_f = base_n << (levels - 1)
+    F = O.seeded_load(n_f, 1)
+    orc = O.OracleMG(base_n=base_n, levels=levels, k=k, beta=1.0, inv_eps=1e3, load_kind=O.LOAD_ARRAY, load=F,
+                     cycle=O.CYCLE_V)
+    gd, gs = build(k, True), build(k, False)
+    b = O.random_vec(orc.n, 7)
+    zo, zd, zs = orc.apply(b), gd.apply(b), gs.apply(b)
+    assert rel(zd, zo) < APPLY_TOL
+    assert rel(zs, zo) < APPLY_TOL
+    assert rel(zd, zs) < APPLY_TOL
+    # PCG: identical counts with and without the map, solutions to round-off
+    xd, sd = H.pcg(gd, gd.rhs())
+    xs, ss = H.pcg(gs, gs.rhs())
+    xo, so = orc.krylov(orc.rhs())
+    assert sd.iterations == ss.iterations
+    assert abs(sd.iterations - so["iterations"]) <= 1
+    assert rel(xd, xo) < 1e-8
+    gd.close()
+    gs.close()
+
+
+def test_dense_level1_variable_v_and_w_cycle():
+    # variable V (two smoothing steps per level below the finest) keeps the map;
+    # the W-cycle runs the sweeps (the map is only formed for q = 1)
+    base_n, levels, k = 8, 3, 1
+    n_f = base_n << (levels - 1)
+    F = O.seeded_load(n_f, 1)
+    for cyc_h, cyc_o, m in ((H.CYCLE_VARIABLE_V, O.CYCLE_VARV, 1), (H.CYCLE_W, O.CYCLE_W, 1), (H.CYCLE_V, O.CYCLE_V, 2)):
+        orc = O.OracleMG(base_n=base_n, levels=levels, k=k, beta=1.0, inv_eps=1e3, load_kind=O.LOAD_ARRAY, load=F,
+                         cycle=cyc_o, smooth_steps=m)
+        g = build(k, True, cycle=cyc_h, m=m)
+        b = O.random_vec(orc.n, 11)
+        assert rel(g.apply(b), orc.apply(b)) < APPLY_TOL, (cyc_h, m)
+        g.close()
+
+
+def test_dense_level1_repeatable():
+    # the GEMV sums in a fixed order: repeated applies are bitwise identical
+    g = build(2, True)
+    b = O.random_vec(g.n, 5)
+    z1 = g.apply(b)
+    for _ in range(3):
+        assert np.array_equal(g.apply(b), z1)
+    g.close()
