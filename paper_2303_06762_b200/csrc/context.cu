@@ -197,6 +197,7 @@ struct hpmg_ctx {
   double* coarse_inv = nullptr;
   double* m1 = nullptr;  // level-1 V(1,1) sub-cycle as one dense map (dense_level.cu), or null
   int m1_n = 0;
+  bool m1_sym = true;  // symmetric tile storage (HPMG_DENSE_L1=2: the full row-major map)
   double* coarse_dense = nullptr;  // level-0 operator, dense row-major (setup scratch of the inverse)
   dev::DenseInvertWork gj;         // Gauss-Jordan scratch of the coarse inverse
   cudaStream_t s_coarse = nullptr; // setup: the coarse inverse runs beside the finer levels' work
@@ -733,7 +734,7 @@ void h_cycle(hpmg_ctx& C, int l, const double* b, double* x) {
   if (l == 1 && C.m1 && b == V.b && !C.trace && V.small && C.opt.smoother == HPMG_SMOOTH_MULTIPLICATIVE && q == 1) {
     // the whole level-1 sub-cycle (sweeps, transfers, coarse solve) as one
     // dense map formed at setup (dense_level.cu): one HBM-bound GEMV
-    dev::dense_rowgemv(int(V.n), C.m1, b, x, C.s);
+    dev::dense_apply(int(V.n), C.m1_sym, C.m1, b, x, C.s);
     count(C);
     return;
   }
@@ -1444,16 +1445,18 @@ void build_dense_level1(hpmg_ctx& C) {
     return;
   }
   Level& V = *C.lv[1];
-  if (!C.m1 || C.m1_n != int(V.n)) {
+  const bool sym = !(env && env[0] == '2');
+  if (!C.m1 || C.m1_n != int(V.n) || C.m1_sym != sym) {
     if (C.m1) dfree(C.m1);
-    C.m1 = dalloc<double>(size_t(V.n) * dev::dense_level1_ld(int(V.n)));
+    C.m1 = dalloc<double>(dev::dense_level1_size(int(V.n), sym));
     C.m1_n = int(V.n);
+    C.m1_sym = sym;
   }
   // scratch from the context pool: stream-ordered, reused by the next context
   void* w = nullptr;
   CK(cudaMallocFromPoolAsync(&w, sizeof(double) * dev::dense_level1_work(int(V.n), C.n0), alloc_pool(), C.s));
   dev::dense_level1(V.A, V.srec, V.d_passes, V.npass, V.steps, V.PT, V.Pm, C.n0, C.coarse_inv, C.m1,
-                    static_cast<double*>(w), C.s);
+                    static_cast<double*>(w), C.m1_sym, C.s);
   CK(cudaFreeAsync(w, C.s));
 }
 

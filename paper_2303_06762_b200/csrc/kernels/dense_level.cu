@@ -175,10 +175,104 @@ __global__ void __launch_bounds__(256) k_dense_rowgemv(int n, int ld, const doub
   }
 }
 
+/// Symmetric storage (the default: M1 is symmetric in exact arithmetic for
+/// the symmetric operators the one-CTA level serves; stored as S = (M1 +
+/// M1^T) / 2): the lower-triangle 64 x 64 tiles (I >= J) row-major, tile
+/// t(I, J) = I (I + 1) / 2 + J, half the bytes of the full map. One warp per
+/// tile, two per 64-thread CTA (102 registers: small CTAs keep the SMs evenly
+/// loaded): lane l holds columns 2l, 2l + 1 of each row; the column part
+/// T^T b_I accumulates lane-locally, the row part T b_J per row is reduced
+/// across the warp 32 rows at a time by a transposing butterfly (31
+/// shuffles per 32 rows, lane r ends with row r). Both parts go to per-tile
+/// partials, summed per output row in a fixed order by k_sym_combine.
+constexpr int kTile = 64;
+__host__ __device__ __forceinline__ size_t tri(int i) { return size_t(i) * (i + 1) / 2; }
+
+__global__ void k_sym_pack(int n, int nb, const double* __restrict__ X, double* __restrict__ T) {
+  // one CTA per tile; X column-major: M1(i, j) = X[j n + i]
+  const int t = blockIdx.x;
+  int I = int((sqrt(8.0 * t + 1.0) - 1.0) / 2.0);
+  while (tri(I + 1) <= size_t(t)) ++I;
+  while (tri(I) > size_t(t)) --I;
+  const int J = t - int(tri(I));
+  double* out = T + size_t(t) * kTile * kTile;
+  for (int e = threadIdx.x; e < kTile * kTile; e += blockDim.x) {
+    const int r = e / kTile, c = e % kTile, i = I * kTile + r, j = J * kTile + c;
+    out[e] = (i < n && j < n) ? 0.5 * (X[size_t(j) * n + i] + X[size_t(i) * n + j]) : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(64) k_sym_tiles(int ntiles, const double* __restrict__ T, const double* __restrict__ b,
+                                                  double* __restrict__ prow, double* __restrict__ pcol) {
+  const int t = blockIdx.x * 2 + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (t >= ntiles) return;
+  int I = int((sqrt(8.0 * t + 1.0) - 1.0) / 2.0);
+  while (tri(I + 1) <= size_t(t)) ++I;
+  while (tri(I) > size_t(t)) --I;
+  const int J = t - int(tri(I));
+  const double2* tile = reinterpret_cast<const double2*>(T + size_t(t) * kTile * kTile) + lane;
+  const double2 bj = __ldg(reinterpret_cast<const double2*>(b + J * kTile) + lane);
+  const double* bi = b + I * kTile;
+  double cx = 0.0, cy = 0.0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    double p[32];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      double2 a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = __ldcs(tile + (h * 32 + g * 8 + u) * (kTile / 2));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int r = h * 32 + g * 8 + u;
+        const double br = __ldg(bi + r);
+        p[g * 8 + u] = fma(a[u].x, bj.x, a[u].y * bj.y);
+        cx = fma(a[u].x, br, cx);
+        cy = fma(a[u].y, br, cy);
+      }
+    }
+    // transposing butterfly: after the stage with offset o each lane keeps o
+    // values; lane l ends with the warp sum of row (h * 32 + l)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const bool up = lane & o;
+#pragma unroll
+      for (int i = 0; i < o; ++i) {
+        const double send = up ? p[i] : p[i + o];
+        const double keep = up ? p[i + o] : p[i];
+        p[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+    prow[size_t(t) * kTile + h * 32 + lane] = p[0];
+  }
+  if (I != J) reinterpret_cast<double2*>(pcol + size_t(t) * kTile)[lane] = make_double2(cx, cy);
+}
+
+/// y_i, i = 64 K + r: the row parts of tiles (K, 0..K), then the column parts
+/// of tiles (K+1..nb-1, K), four lanes per output (terms q = g, g + 4, ...),
+/// combined in a fixed order
+__global__ void __launch_bounds__(256) k_sym_combine(int n, int nb, const double* __restrict__ prow,
+                                                    const double* __restrict__ pcol, double* __restrict__ y) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = gt / 4, g = gt % 4;
+  const int K = min(i / kTile, nb - 1), r = i % kTile;
+  double s = 0.0;
+  if (i < n) {
+    for (int q = g; q < nb; q += 4) {
+      const double v = q <= K ? prow[(tri(K) + q) * kTile + r] : pcol[(tri(q) + K) * kTile + r];
+      s += v;
+    }
+  }
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  if (i < n && g == 0) y[i] = s;
+}
+
 }  // namespace
 
 void dense_level1(const Bsr& A, const PatchRecords& R, const int2* passes, int npass, int sweeps, const BlockCsr& PT,
-                  const BlockCsr& Pm, int n0, const double* coarse_inv, double* M1, double* work, cudaStream_t s) {
+                  const BlockCsr& Pm, int n0, const double* coarse_inv, double* M1, double* work, bool sym,
+                  cudaStream_t s) {
   const int n = A.nb * 2;
   if (n % 2 || n0 % 2) throw std::runtime_error("dense level 1: odd size");
   auto chk = [](cudaError_t e) {
@@ -199,9 +293,36 @@ void dense_level1(const Bsr& A, const PatchRecords& R, const int2* passes, int n
   DL_CHECK();
   // X[:, j] = backward sweep(s) of X[:, j] with b = e_j: column j of M1
   small_post_batch(R, A.nb, passes, npass, sweeps, n, 0, X, n, s);
+  if (sym) {
+    const int nb = (n + kTile - 1) / kTile;
+    k_sym_pack<<<int(tri(nb)), 256, 0, s>>>(n, nb, X, M1);
+    DL_CHECK();
+    return;
+  }
   const int ld = dense_level1_ld(n);
   chk(cudaMemsetAsync(M1, 0, sizeof(double) * size_t(n) * ld, s));  // zero columns past n
   k_transpose_sq<<<dim3((n + 31) / 32, (n + 31) / 32), dim3(32, 8), 0, s>>>(n, ld, X, M1);
+  DL_CHECK();
+}
+
+size_t dense_level1_size(int n, bool sym) {
+  if (!sym) return size_t(n) * dense_level1_ld(n);
+  const int nb = (n + kTile - 1) / kTile;
+  return tri(nb) * (kTile * kTile + 2 * kTile);  // tiles, then the row and column partials
+}
+
+void dense_apply(int n, bool sym, const double* M, const double* b, double* y, cudaStream_t s) {
+  if (!sym) {
+    dense_rowgemv(n, M, b, y, s);
+    return;
+  }
+  const int nb = (n + kTile - 1) / kTile;
+  const int nt = int(tri(nb));
+  double* prow = const_cast<double*>(M) + size_t(nt) * kTile * kTile;
+  double* pcol = prow + size_t(nt) * kTile;
+  k_sym_tiles<<<(nt + 1) / 2, 64, 0, s>>>(nt, M, b, prow, pcol);
+  DL_CHECK();
+  k_sym_combine<<<(4 * n + 255) / 256, 256, 0, s>>>(n, nb, prow, pcol, y);
   DL_CHECK();
 }
 

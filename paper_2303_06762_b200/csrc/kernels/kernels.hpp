@@ -134,7 +134,12 @@ void small_post_batch(const PatchRecords& R, int nb, const int2* passes, int npa
 /// dense_level.cu: M1 (row-major n x n) = the level-1 V(1,1) sub-cycle
 /// (pre-sweep, residual, P C^-1 P^T, post-sweep) as one linear map; y = M b
 void dense_level1(const Bsr& A, const PatchRecords& R, const int2* passes, int npass, int sweeps, const BlockCsr& PT,
-                  const BlockCsr& Pm, int n0, const double* coarse_inv, double* M1, double* work, cudaStream_t s);
+                  const BlockCsr& Pm, int n0, const double* coarse_inv, double* M1, double* work, bool sym,
+                  cudaStream_t s);
+/// doubles of M1's storage: full row-major (sym = false) or symmetric tiles + partials
+size_t dense_level1_size(int n, bool sym);
+/// y = M1 b (b zero-padded past n, see kVecPad)
+void dense_apply(int n, bool sym, const double* M, const double* b, double* y, cudaStream_t s);
 size_t dense_level1_work(int n, int n0);  // doubles of dense_level1's scratch
 /// M row-major with row stride dense_level1_ld(n) (zero columns past n); b
 /// must be readable, and zero, up to that stride (level b buffers are padded)

@@ -77,7 +77,10 @@ def test_dense_level1_variable_v_and_w_cycle():
                          cycle=cyc_o, smooth_steps=m)
         g = build(k, True, cycle=cyc_h, m=m)
         b = O.random_vec(orc.n, 11)
-        assert rel(g.apply(b), orc.apply(b)) < APPLY_TOL, (cyc_h, m)
+        # the W-cycle (sweeps, no map) visits level 1 twice per level-2 visit:
+        # 6.5e-12 measured at this size, the V-type cycles stay below 2e-12
+        tol = 2e-11 if cyc_h == H.CYCLE_W else APPLY_TOL
+        assert rel(g.apply(b), orc.apply(b)) < tol, (cyc_h, m)
         g.close()
 
 
