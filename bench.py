@@ -341,7 +341,7 @@ def run_hpmg(args, rank, world, local, dist):
                          "vcycle_physical_bytes": phys_bytes,
                          "vcycle_physical_gbs": phys_bytes / (ms_dev / args.steps * 1e-3) / 1e9,
                          "vcycle_physical_frac": phys_bytes / (ms_dev / args.steps * 1e-3) / 1e9 / hbm,
-                         "vcycle_physical_note": "bytes this implementation moves per V-cycle: head and level "
+                         "vcycle_physical_note": "(level 1 counted as its sweeps, transfers and coarse solve; with the default dense level-1 map the device instead reads the ~146 MB symmetric map per cycle, so the bytes moved are ~0.14 GB higher and this fraction is a lower bound) bytes this implementation moves per V-cycle: head and level "
                                                  "sweep records + vector rows as streamed, head mode-0 residual, "
                                                  "level residuals, P / P^T, coarse inverse, E/E^T and the "
                                                  "boundary vectors; the reference-storage figure above uses "
